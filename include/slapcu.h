@@ -1,0 +1,268 @@
+/*
+ * slapcu.h -- C-ABI of the B200-native semiring SpGEMM library (libslapcu.so).
+ *
+ * This is the drop-in boundary for the hot path of the reference ("slap",
+ * /root/reference/proj, a CombBLAS 2.0 embodiment): the local semiring
+ * SpGEMM that 2D/3D Sparse SUMMA calls once per stage, the stage-partial merge,
+ * and the distributed drivers around them.  Plain C types only: device
+ * pointers, sizes, an opaque context and int status codes.  No exceptions
+ * cross this boundary; status codes map 1:1 onto the reference's slap::Error
+ * kinds (error.hpp:27-36) via slapcu_status_name().
+ *
+ * Layout (all matrices): CSC, int64 colptr[ncols+1], int32 rowids[nnz] with
+ * rows strictly ascending inside every column, values of the semiring's
+ * element type.  The reference stores colptr in its int32 local index type
+ * (local_matrix.hpp:26-82, dist_matrix.hpp:18), which overflows at nnz >= 2^31
+ * (spgemm.hpp:289-292); 64-bit offsets remove that limit here.
+ *
+ * Reference interface each entry point replaces is cited on its declaration
+ * (paths relative to /root/reference/proj/core/include/slap/).
+ */
+#ifndef SLAPCU_H
+#define SLAPCU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SLAPCU_ABI_VERSION 1
+
+/* error.hpp:10-36: Error kinds.  SLAPCU_ERR_INTERNAL is the reference's
+ * Error("InternalError") raised when numeric != symbolic (spgemm.hpp:323-324). */
+typedef enum {
+    SLAPCU_OK = 0,
+    SLAPCU_ERR_DIM = 1,      /* DimError   (spgemm.hpp:57-64, summa.hpp:116-122)   */
+    SLAPCU_ERR_SHAPE = 2,    /* ShapeError (summa.hpp:112-115, spgemm3d.hpp:27-30) */
+    SLAPCU_ERR_INTERNAL = 3, /* Error("InternalError")                             */
+    SLAPCU_ERR_NAME = 4,     /* NameError  (spgemm.hpp:19-24, semiring.cpp)        */
+    SLAPCU_ERR_BUDGET = 5,   /* BudgetError (batched.hpp:122-148)                  */
+    SLAPCU_ERR_INDEX = 6,    /* IndexError                                         */
+    SLAPCU_ERR_INVALID = 7,  /* bad argument (null pointer, unsupported id)        */
+    SLAPCU_ERR_CUDA = 8,     /* CUDA runtime failure                               */
+    SLAPCU_ERR_NOMEM = 9,    /* device allocation failure                          */
+    SLAPCU_ERR_COMM = 10     /* NCCL failure / collective mismatch (DeadlockError) */
+} slapcu_status;
+
+/* semiring.hpp:36-93.  Ids are stable (shared with oracle/oracle.h). */
+typedef enum {
+    SLAPCU_PLUS_TIMES_F64 = 0, /* PlusTimes<double>  */
+    SLAPCU_PLUS_TIMES_F32 = 1, /* PlusTimes<float>   */
+    SLAPCU_PLUS_TIMES_I64 = 2, /* PlusTimes<int64_t> */
+    SLAPCU_MIN_PLUS_I32 = 3,   /* MinPlus<int32_t>   (zero = INT32_MAX) */
+    SLAPCU_MIN_PLUS_F64 = 4,   /* MinPlus<double>    (zero = +inf)      */
+    SLAPCU_OR_AND_U8 = 5       /* OrAnd, uint8 0/1                      */
+} slapcu_semiring;
+
+/* spgemm.hpp:17 SpGemmAlg.  On the GPU these are accumulator policies:
+ * hybrid = binned by work (smem hash for light columns, row-tiled dense
+ * bitmap accumulator for heavy ones); hash = same bins; heap = force the
+ * sorted dense-tile path for every column.  Output is identical for all. */
+typedef enum { SLAPCU_ALG_HEAP = 0, SLAPCU_ALG_HASH = 1, SLAPCU_ALG_HYBRID = 2 } slapcu_alg;
+
+/* One CSC operand in DEVICE memory. */
+typedef struct {
+    int64_t nrows, ncols, nnz;
+    const int64_t* colptr; /* [ncols+1] */
+    const int32_t* rowids; /* [nnz]     */
+    const void* vals;      /* [nnz] of the semiring element type */
+} slapcu_csc;
+
+/* A CSC result whose device buffers were allocated by the library
+ * (free with slapcu_csc_free). */
+typedef struct {
+    int64_t nrows, ncols, nnz;
+    int64_t* colptr;
+    int32_t* rowids;
+    void* vals;
+} slapcu_csc_out;
+
+/* The same layout in HOST memory (used by the reference-facing one-shot call). */
+typedef slapcu_csc_out slapcu_host_csc;
+
+typedef struct slapcu_ctx_s* slapcu_ctx;
+
+/* ---------------------------------------------------------------- context */
+
+/* A context = one device + one CUDA stream + a stream-ordered workspace and
+ * the per-product plan cached between the symbolic and numeric phases.
+ * `stream` is a cudaStream_t (NULL = the legacy default stream).  Calls on a
+ * context are stream-ordered and not reentrant; use one context per host thread. */
+slapcu_status slapcu_ctx_create(slapcu_ctx* out, int device, void* stream);
+slapcu_status slapcu_ctx_destroy(slapcu_ctx ctx);
+slapcu_status slapcu_ctx_set_stream(slapcu_ctx ctx, void* stream);
+const char* slapcu_ctx_last_error(slapcu_ctx ctx);
+const char* slapcu_status_name(slapcu_status s); /* "DimError", "ShapeError", ... */
+int slapcu_abi_version(void);
+
+/* Tuning / test knobs (defaults are the production policy). */
+typedef enum {
+    SLAPCU_OPT_TILE_ROWS_LOG2 = 0,    /* row-tile height of the dense accumulators (default 18) */
+    SLAPCU_OPT_SYM_TILE_ROWS_LOG2 = 1,/* row-tile height of the symbolic bitmap    (default 19) */
+    SLAPCU_OPT_LIGHT_NNZ_MAX = 2,     /* numeric: columns above this use the dense tile path */
+    SLAPCU_OPT_LIGHT_FLOPS_MAX = 3,   /* symbolic: columns above this use the bitmap path   */
+    SLAPCU_OPT_DETERMINISTIC = 4,     /* reserved */
+    SLAPCU_OPT_PROFILE = 5            /* 1: CUDA events around every launch, per-class device time */
+} slapcu_option;
+slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t value);
+
+/* Per-kernel-class device time collected with SLAPCU_OPT_PROFILE (events on
+ * the context stream).  Classes: 0 other, 1 flops, 2 bin, 3 sym_light,
+ * 4 sym_heavy, 5 scan, 6 num_light, 7 num_heavy, 8 merge, 9 gen. */
+#define SLAPCU_NUM_KERNEL_CLASSES 10
+slapcu_status slapcu_ctx_kernel_stats(slapcu_ctx ctx, int cls, int64_t* launches, double* ms);
+slapcu_status slapcu_ctx_reset_stats(slapcu_ctx ctx);
+const char* slapcu_kernel_class_name(int cls);
+
+/* Number of kernels this context launched since creation (for bench reports). */
+int64_t slapcu_ctx_kernel_launches(slapcu_ctx ctx);
+
+/* Elapsed device time of the last numeric phase's dominant kernels, ms
+ * (CUDA events on the context stream). */
+slapcu_status slapcu_ctx_last_phase_ms(slapcu_ctx ctx, float* symbolic_ms, float* numeric_ms);
+
+int slapcu_semiring_value_size(slapcu_semiring sr);
+/* semiring.cpp builtin_semiring + dtype: ("plus_times","f64") etc. */
+slapcu_status slapcu_semiring_from_name(const char* name, const char* dtype, slapcu_semiring* out);
+/* spgemm.hpp:19-24 spgemm_alg_from_name */
+slapcu_status slapcu_alg_from_name(const char* name, slapcu_alg* out);
+
+/* --------------------------------------------------- local SpGEMM phases */
+
+/* Phase 1, spgemm.hpp:68-88 estimate_flops: per-column multiply counts of
+ * C = A*B into flops_per_col (device, int64[B.ncols], may be NULL) and the
+ * total into *total (host). */
+slapcu_status slapcu_estimate_flops(slapcu_ctx ctx, const slapcu_csc* A, const slapcu_csc* B,
+                                    int64_t* flops_per_col, int64_t* total);
+
+/* Phase 2, spgemm.hpp:118-138 symbolic_nnz + the colptr prefix sum
+ * (spgemm.hpp:289-293): writes C's colptr (device, int64[B.ncols+1]) and
+ * *c_nnz (host).  Values of A/B are not read. */
+slapcu_status slapcu_spgemm_symbolic(slapcu_ctx ctx, const slapcu_csc* A, const slapcu_csc* B, slapcu_alg alg,
+                                     int64_t* c_colptr, int64_t* c_nnz);
+
+/* Phase 3, spgemm.hpp:297-330 numeric pass: fills C's rowids/vals (device,
+ * caller-allocated, sized by phase 2) for the colptr phase 2 produced on the
+ * same context.  Rows come out ascending per column, no explicit zeros are
+ * pruned.  SLAPCU_ERR_INTERNAL if any column's numeric count
+ * disagrees with the symbolic count (spgemm.hpp:323-324). */
+slapcu_status slapcu_spgemm_numeric(slapcu_ctx ctx, const slapcu_csc* A, const slapcu_csc* B, slapcu_semiring sr,
+                                    slapcu_alg alg, const int64_t* c_colptr, int32_t* c_rowids, void* c_vals);
+
+/* spgemm.hpp:275-330 local_spgemm, all three phases, C allocated on the
+ * device by the library. */
+slapcu_status slapcu_spgemm(slapcu_ctx ctx, const slapcu_csc* A, const slapcu_csc* B, slapcu_semiring sr,
+                            slapcu_alg alg, slapcu_csc_out* C);
+
+/* local_spgemm with HOST operands and a HOST result (malloc'd; free with
+ * slapcu_host_free): H2D copies, the three phases, D2H copies.  This is the
+ * call the reference-side C++ template shim binds. */
+slapcu_status slapcu_spgemm_host(slapcu_ctx ctx, const slapcu_host_csc* A, const slapcu_host_csc* B,
+                                 slapcu_semiring sr, slapcu_alg alg, slapcu_host_csc* C);
+
+slapcu_status slapcu_csc_free(slapcu_ctx ctx, slapcu_csc_out* C);
+void slapcu_host_free(slapcu_host_csc* C);
+
+/* ------------------------------------------------------- format adapters */
+
+/* local_matrix.hpp:88-150 DcscMatrix -> dense device colptr: scatters the
+ * nzc (jc, cp) pairs (int32, device) into colptr (int64[ncols+1]).  The
+ * reference looks columns up by binary search on every access
+ * (local_matrix.hpp:115-121); the device kernels index colptr directly. */
+slapcu_status slapcu_dcsc_colptr(slapcu_ctx ctx, int64_t ncols, int64_t nzc, const int32_t* jc, const int32_t* cp,
+                                 int64_t* colptr);
+
+/* ------------------------------------------------------ merge (SUMMA/3D) */
+
+/* local_matrix.hpp:166-188 sort_and_combine as the SUMMA stage merge
+ * (summa.hpp:145-156) and the 3D fiber merge (spgemm3d.hpp:257-262): C =
+ * parts[0] (+) parts[1] (+) ... with every coincident entry left-folded with
+ * sr.add in part order -- the order the reference's stable sort yields.
+ * All parts share one shape.  Two phases like the SpGEMM. */
+slapcu_status slapcu_merge_symbolic(slapcu_ctx ctx, int nparts, const slapcu_csc* parts, int64_t* c_colptr,
+                                    int64_t* c_nnz);
+slapcu_status slapcu_merge_numeric(slapcu_ctx ctx, int nparts, const slapcu_csc* parts, slapcu_semiring sr,
+                                   const int64_t* c_colptr, int32_t* c_rowids, void* c_vals);
+
+/* -------------------------------------------- synthetic inputs on device */
+
+/* algorithms.cpp:71-113 gen_rmat, bit-identical (Rng rng.hpp:12-45, one
+ * stream per edge draw, symmetrized, self loops dropped, duplicates
+ * collapsed).  Allocates the pattern (vals = NULL). */
+slapcu_status slapcu_gen_rmat(slapcu_ctx ctx, int scale, int edge_factor, uint64_t seed, double a, double b,
+                              double c, double d, slapcu_csc_out* out);
+/* oracles.hpp:205-217 random_triples as an n x n Erdos-Renyi matrix: `draws`
+ * (row, col, value) draws from one Rng(seed) stream, duplicates keep the first
+ * draw; values U[0,1) stored as double if with_values. */
+slapcu_status slapcu_gen_er(slapcu_ctx ctx, int64_t n, int64_t draws, uint64_t seed, int with_values,
+                            slapcu_csc_out* out);
+/* Tall-skinny B for config C5: n x ncols, exactly one nonzero per row at
+ * column Rng(seed) draw 2i mod ncols, value U[0,1) from draw 2i+1. */
+slapcu_status slapcu_gen_one_per_row(slapcu_ctx ctx, int64_t n, int64_t ncols, uint64_t seed, slapcu_csc_out* out);
+/* Value recipes, written into `vals` (device, nnz of sr's type):
+ * kind 0 ones, 1 U[0,1), 2 U[0,10), 3 int 1+h%255, 4 1/deg(col), 5 int 1+h%9,
+ * where h = splitmix64((i<<32) ^ j). */
+slapcu_status slapcu_fill_values(slapcu_ctx ctx, slapcu_semiring sr, int kind, const slapcu_csc* m, void* vals);
+/* Symmetric relabelling P*A*P^T with a seed-deterministic permutation (the
+ * balanced alternative to dist_matrix.hpp:191-212 random_permute for A*A). */
+slapcu_status slapcu_permute_symmetric(slapcu_ctx ctx, const slapcu_csc* A, uint64_t seed, slapcu_semiring sr,
+                                       slapcu_csc_out* out);
+
+/* Column slice B(:, [c0, c1)) as a new device CSC (batched.hpp:43-66 slice_cols). */
+slapcu_status slapcu_slice_cols(slapcu_ctx ctx, const slapcu_csc* B, slapcu_semiring sr, int64_t c0, int64_t c1,
+                                slapcu_csc_out* out);
+
+/* Per-column 64-bit checksums of (row, value bits) (device uint64[ncols]);
+ * with_values=0 hashes the pattern only.  Matches oracle/orc_column_checksums. */
+slapcu_status slapcu_column_checksums(slapcu_ctx ctx, const slapcu_csc* m, slapcu_semiring sr, int with_values,
+                                      uint64_t* sums);
+
+/* ---------------------------------------------------- distributed drivers */
+
+/* One process (or host thread) per GPU.  Communicators are NCCL over
+ * NVLink/NVSwitch.  slapcu_comm_unique_id fills a 128-byte ncclUniqueId that
+ * rank 0 shares with the others out of band (torch.distributed store, MPI,
+ * a file...). */
+typedef struct slapcu_comm_s* slapcu_comm;
+slapcu_status slapcu_comm_unique_id(void* id128);
+slapcu_status slapcu_comm_create(slapcu_comm* out, slapcu_ctx ctx, int rank, int nranks, const void* id128);
+slapcu_status slapcu_comm_destroy(slapcu_comm comm);
+
+/* comm.hpp:31-53 CommCounters analogue: per-kind call counts / bytes sent by
+ * this rank (kind: 0 broadcast, 1 alltoallv, 2 reduce, 3 allgatherv). */
+slapcu_status slapcu_comm_counters(slapcu_comm comm, int kind, int64_t* calls, int64_t* bytes);
+
+/* Per-call record, summa.hpp:15-20 DistKernelStats + timing. */
+typedef struct {
+    int stages;
+    int64_t flops;   /* this rank's multiplies */
+    int64_t nnz_out; /* this rank's output nonzeros */
+    int layer_warning;
+    float ms_total, ms_local, ms_merge, ms_exposed_bcast; /* device-event timings */
+} slapcu_dist_stats;
+
+/* summa.hpp:106-163 summa2d_spgemm on a q x q grid (rank = i*q + j,
+ * grid.hpp:15-24).  A_local / B_local are this rank's blocks (rows
+ * A.row_offsets[i].., cols A.col_offsets[j].., layout.hpp:60-66 block_offsets);
+ * C_local is allocated.  Stage s broadcasts A(i,s) on the row communicator and
+ * B(s,j) on the column communicator (ncclBroadcast), double-buffered against
+ * the stage multiply; the q partials are merged once with
+ * slapcu_merge (stage order).  Collective over all ranks of `comm`. */
+slapcu_status slapcu_summa2d(slapcu_comm comm, const slapcu_csc* A_local, const slapcu_csc* B_local,
+                             slapcu_semiring sr, slapcu_alg alg, slapcu_csc_out* C_local,
+                             slapcu_dist_stats* stats);
+
+/* spgemm3d.hpp:21-106 ca3d_spgemm on a c x q x q grid (regular variant,
+ * grid.cpp:57 rank = l*q*q + i*q + j): A split by columns, B by rows; per
+ * layer SUMMA, then C_int's columns are split into c pieces (block_offsets)
+ * and exchanged over the fiber (grouped ncclSend/ncclRecv after a count
+ * exchange), then merged.  C_local is this rank's piece. */
+slapcu_status slapcu_ca3d(slapcu_comm comm, int layers, const slapcu_csc* A_local, const slapcu_csc* B_local,
+                          slapcu_semiring sr, slapcu_alg alg, slapcu_csc_out* C_local, slapcu_dist_stats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLAPCU_H */

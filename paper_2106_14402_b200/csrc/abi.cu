@@ -1,0 +1,421 @@
+// abi.cu -- the extern "C" boundary (include/slapcu.h).  Exceptions never
+// cross it: every entry point maps slapcu::Fail onto a status code and keeps
+// the message in the context (slapcu_ctx_last_error).
+#include <cstdlib>
+#include <cstring>
+#include <new>
+
+#include "ctx.hpp"
+
+struct slapcu_ctx_s {
+    slapcu::Ctx c;
+};
+
+namespace slapcu {
+
+Ctx& ctx_of(slapcu_ctx c) { return c->c; }
+
+namespace {
+
+template <class F>
+slapcu_status guarded(slapcu_ctx ctx, F&& f) {
+    if (!ctx) return SLAPCU_ERR_INVALID;
+    try {
+        SLAPCU_CUDA(cudaSetDevice(ctx->c.device));
+        f(ctx->c);
+        ctx->c.last_error.clear();
+        return SLAPCU_OK;
+    } catch (const Fail& e) {
+        ctx->c.last_error = e.msg;
+        return e.st;
+    } catch (const std::bad_alloc&) {
+        ctx->c.last_error = "host allocation failed";
+        return SLAPCU_ERR_NOMEM;
+    } catch (const std::exception& e) {
+        ctx->c.last_error = e.what();
+        return SLAPCU_ERR_INTERNAL;
+    }
+}
+
+void require(bool ok, slapcu_status st, const char* msg) {
+    if (!ok) throw Fail{st, msg};
+}
+
+void alloc_csc_out(Ctx& c, slapcu_csc_out* C, int64_t nrows, int64_t ncols, int64_t nnz, int vs) {
+    C->nrows = nrows;
+    C->ncols = ncols;
+    C->nnz = nnz;
+    C->colptr = nullptr;
+    C->rowids = nullptr;
+    C->vals = nullptr;
+    SLAPCU_CUDA(cudaMallocAsync((void**)&C->colptr, sizeof(int64_t) * (ncols + 1), c.stream));
+    SLAPCU_CUDA(cudaMallocAsync((void**)&C->rowids, sizeof(int32_t) * std::max<int64_t>(nnz, 1), c.stream));
+    SLAPCU_CUDA(cudaMallocAsync(&C->vals, size_t(vs) * std::max<int64_t>(nnz, 1), c.stream));
+}
+
+}  // namespace
+}  // namespace slapcu
+
+using namespace slapcu;
+
+extern "C" {
+
+int slapcu_abi_version(void) { return SLAPCU_ABI_VERSION; }
+
+const char* slapcu_status_name(slapcu_status s) {
+    switch (s) {
+    case SLAPCU_OK: return "Ok";
+    case SLAPCU_ERR_DIM: return "DimError";
+    case SLAPCU_ERR_SHAPE: return "ShapeError";
+    case SLAPCU_ERR_INTERNAL: return "InternalError";
+    case SLAPCU_ERR_NAME: return "NameError";
+    case SLAPCU_ERR_BUDGET: return "BudgetError";
+    case SLAPCU_ERR_INDEX: return "IndexError";
+    case SLAPCU_ERR_INVALID: return "InvalidArgument";
+    case SLAPCU_ERR_CUDA: return "CudaError";
+    case SLAPCU_ERR_NOMEM: return "OutOfMemory";
+    case SLAPCU_ERR_COMM: return "DeadlockError";
+    }
+    return "Unknown";
+}
+
+slapcu_status slapcu_ctx_create(slapcu_ctx* out, int device, void* stream) {
+    if (!out) return SLAPCU_ERR_INVALID;
+    *out = nullptr;
+    slapcu_ctx ctx = new (std::nothrow) slapcu_ctx_s;
+    if (!ctx) return SLAPCU_ERR_NOMEM;
+    ctx->c.device = device;
+    ctx->c.stream = static_cast<cudaStream_t>(stream);
+    slapcu_status st = guarded(ctx, [&](Ctx& c) {
+        SLAPCU_CUDA(cudaDeviceGetAttribute(&c.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+        SLAPCU_CUDA(cudaDeviceGetAttribute(&c.num_sms, cudaDevAttrMultiProcessorCount, device));
+        for (auto& e : c.ev) SLAPCU_CUDA(cudaEventCreate(&e));
+        // keep freed workspace cached in the stream-ordered pool
+        cudaMemPool_t pool;
+        SLAPCU_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t thr = UINT64_MAX;
+        SLAPCU_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    });
+    if (st != SLAPCU_OK) {
+        delete ctx;
+        return st;
+    }
+    *out = ctx;
+    return SLAPCU_OK;
+}
+
+slapcu_status slapcu_ctx_destroy(slapcu_ctx ctx) {
+    if (!ctx) return SLAPCU_ERR_INVALID;
+    cudaSetDevice(ctx->c.device);
+    cudaStreamSynchronize(ctx->c.stream);
+    for (auto& e : ctx->c.ev)
+        if (e) cudaEventDestroy(e);
+    delete ctx;
+    return SLAPCU_OK;
+}
+
+slapcu_status slapcu_ctx_set_stream(slapcu_ctx ctx, void* stream) {
+    return guarded(ctx, [&](Ctx& c) { c.stream = static_cast<cudaStream_t>(stream); });
+}
+
+const char* slapcu_ctx_last_error(slapcu_ctx ctx) { return ctx ? ctx->c.last_error.c_str() : "null context"; }
+
+slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t v) {
+    return guarded(ctx, [&](Ctx& c) {
+        switch (opt) {
+        case SLAPCU_OPT_TILE_ROWS_LOG2:
+            require(v >= 10 && v <= 20, SLAPCU_ERR_INVALID, "tile rows log2 must be in 10..20");
+            c.opt.tile_rows_log2 = (int)v;
+            break;
+        case SLAPCU_OPT_SYM_TILE_ROWS_LOG2:
+            require(v >= 10 && v <= 20, SLAPCU_ERR_INVALID, "symbolic tile rows log2 must be in 10..20");
+            c.opt.sym_tile_rows_log2 = (int)v;
+            break;
+        case SLAPCU_OPT_LIGHT_NNZ_MAX: c.opt.light_nnz_max = v; break;
+        case SLAPCU_OPT_LIGHT_FLOPS_MAX: c.opt.light_flops_max = v; break;
+        case SLAPCU_OPT_DETERMINISTIC: break;
+        case SLAPCU_OPT_PROFILE:
+            prof_flush(c);
+            c.prof.on = v != 0;
+            break;
+        default: throw Fail{SLAPCU_ERR_INVALID, "unknown option"};
+        }
+    });
+}
+
+slapcu_status slapcu_ctx_kernel_stats(slapcu_ctx ctx, int cls, int64_t* launches, double* ms) {
+    return guarded(ctx, [&](Ctx& c) {
+        require(cls >= 0 && cls < KC_COUNT, SLAPCU_ERR_INVALID, "kernel class out of range");
+        prof_flush(c);
+        if (launches) *launches = c.prof.n[cls];
+        if (ms) *ms = c.prof.ms[cls];
+    });
+}
+
+slapcu_status slapcu_ctx_reset_stats(slapcu_ctx ctx) {
+    return guarded(ctx, [&](Ctx& c) {
+        prof_flush(c);
+        for (int k = 0; k < KC_COUNT; ++k) {
+            c.prof.ms[k] = 0.0;
+            c.prof.n[k] = 0;
+        }
+    });
+}
+
+const char* slapcu_kernel_class_name(int cls) {
+    static const char* names[KC_COUNT] = {"other", "flops", "bin", "sym_light", "sym_heavy",
+                                          "scan", "num_light", "num_heavy", "merge", "gen"};
+    return (cls >= 0 && cls < KC_COUNT) ? names[cls] : "unknown";
+}
+
+int64_t slapcu_ctx_kernel_launches(slapcu_ctx ctx) { return ctx ? ctx->c.launches : -1; }
+
+slapcu_status slapcu_ctx_last_phase_ms(slapcu_ctx ctx, float* sym, float* num) {
+    return guarded(ctx, [&](Ctx& c) {
+        if (sym) *sym = c.sym_ms;
+        if (num) *num = c.num_ms;
+    });
+}
+
+int slapcu_semiring_value_size(slapcu_semiring sr) { return value_size(sr); }
+
+slapcu_status slapcu_semiring_from_name(const char* name, const char* dtype, slapcu_semiring* out) {
+    if (!name || !out) return SLAPCU_ERR_INVALID;
+    const std::string n(name), d(dtype ? dtype : "");
+    if (n == "plus_times" && (d == "f64" || d.empty())) *out = SLAPCU_PLUS_TIMES_F64;
+    else if (n == "plus_times" && d == "f32") *out = SLAPCU_PLUS_TIMES_F32;
+    else if (n == "plus_times" && d == "i64") *out = SLAPCU_PLUS_TIMES_I64;
+    else if (n == "min_plus" && d == "i32") *out = SLAPCU_MIN_PLUS_I32;
+    else if (n == "min_plus" && (d == "f64" || d.empty())) *out = SLAPCU_MIN_PLUS_F64;
+    else if ((n == "or_and" || n == "boolean") && (d == "u8" || d == "bool" || d.empty())) *out = SLAPCU_OR_AND_U8;
+    else return SLAPCU_ERR_NAME;
+    return SLAPCU_OK;
+}
+
+slapcu_status slapcu_alg_from_name(const char* name, slapcu_alg* out) {
+    if (!name || !out) return SLAPCU_ERR_INVALID;
+    const std::string n(name);
+    if (n == "heap") *out = SLAPCU_ALG_HEAP;
+    else if (n == "hash") *out = SLAPCU_ALG_HASH;
+    else if (n == "hybrid") *out = SLAPCU_ALG_HYBRID;
+    else return SLAPCU_ERR_NAME;
+    return SLAPCU_OK;
+}
+
+slapcu_status slapcu_estimate_flops(slapcu_ctx ctx, const slapcu_csc* A, const slapcu_csc* B, int64_t* flops_per_col,
+                                    int64_t* total) {
+    return guarded(ctx, [&](Ctx& c) {
+        require(A && B, SLAPCU_ERR_INVALID, "null operand");
+        spgemm_flops(c, view(*A), view(*B), flops_per_col, total);
+    });
+}
+
+slapcu_status slapcu_spgemm_symbolic(slapcu_ctx ctx, const slapcu_csc* A, const slapcu_csc* B, slapcu_alg alg,
+                                     int64_t* c_colptr, int64_t* c_nnz) {
+    return guarded(ctx, [&](Ctx& c) {
+        require(A && B && c_colptr, SLAPCU_ERR_INVALID, "null argument");
+        const int64_t nnz = spgemm_symbolic(c, view(*A), view(*B), alg, c_colptr);
+        if (c_nnz) *c_nnz = nnz;
+    });
+}
+
+slapcu_status slapcu_spgemm_numeric(slapcu_ctx ctx, const slapcu_csc* A, const slapcu_csc* B, slapcu_semiring sr,
+                                    slapcu_alg alg, const int64_t* c_colptr, int32_t* c_rowids, void* c_vals) {
+    return guarded(ctx, [&](Ctx& c) {
+        require(A && B && c_colptr, SLAPCU_ERR_INVALID, "null argument");
+        spgemm_numeric(c, view(*A), view(*B), sr, alg, c_colptr, c_rowids, c_vals);
+    });
+}
+
+slapcu_status slapcu_spgemm(slapcu_ctx ctx, const slapcu_csc* A, const slapcu_csc* B, slapcu_semiring sr,
+                            slapcu_alg alg, slapcu_csc_out* C) {
+    return guarded(ctx, [&](Ctx& c) {
+        require(A && B && C, SLAPCU_ERR_INVALID, "null argument");
+        const int vs = value_size(sr);
+        require(vs > 0, SLAPCU_ERR_INVALID, "unknown semiring");
+        const DevCsc a = view(*A), b = view(*B);
+        int64_t* cp = nullptr;
+        SLAPCU_CUDA(cudaMallocAsync((void**)&cp, sizeof(int64_t) * (b.ncols + 1), c.stream));
+        int64_t nnz = 0;
+        try {
+            nnz = spgemm_symbolic(c, a, b, alg, cp);
+        } catch (...) {
+            cudaFreeAsync(cp, c.stream);
+            throw;
+        }
+        C->nrows = a.nrows;
+        C->ncols = b.ncols;
+        C->nnz = nnz;
+        C->colptr = cp;
+        C->rowids = nullptr;
+        C->vals = nullptr;
+        SLAPCU_CUDA(cudaMallocAsync((void**)&C->rowids, sizeof(int32_t) * std::max<int64_t>(nnz, 1), c.stream));
+        SLAPCU_CUDA(cudaMallocAsync(&C->vals, size_t(vs) * std::max<int64_t>(nnz, 1), c.stream));
+        spgemm_numeric(c, a, b, sr, alg, cp, C->rowids, C->vals);
+    });
+}
+
+slapcu_status slapcu_spgemm_host(slapcu_ctx ctx, const slapcu_host_csc* A, const slapcu_host_csc* B,
+                                 slapcu_semiring sr, slapcu_alg alg, slapcu_host_csc* C) {
+    return guarded(ctx, [&](Ctx& c) {
+        require(A && B && C, SLAPCU_ERR_INVALID, "null argument");
+        const int vs = value_size(sr);
+        require(vs > 0, SLAPCU_ERR_INVALID, "unknown semiring");
+        if (A->ncols != B->nrows)
+            throw Fail{SLAPCU_ERR_DIM, "spgemm inner dims: A is " + std::to_string(A->nrows) + "x" +
+                                           std::to_string(A->ncols) + ", B is " + std::to_string(B->nrows) + "x" +
+                                           std::to_string(B->ncols)};
+        slapcu_csc_out dA{}, dB{};
+        alloc_csc_out(c, &dA, A->nrows, A->ncols, A->nnz, vs);
+        alloc_csc_out(c, &dB, B->nrows, B->ncols, B->nnz, vs);
+        auto h2d = [&](void* d, const void* h, size_t n) {
+            if (n) SLAPCU_CUDA(cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, c.stream));
+        };
+        h2d(dA.colptr, A->colptr, sizeof(int64_t) * (A->ncols + 1));
+        h2d(dA.rowids, A->rowids, sizeof(int32_t) * A->nnz);
+        h2d(dA.vals, A->vals, size_t(vs) * A->nnz);
+        h2d(dB.colptr, B->colptr, sizeof(int64_t) * (B->ncols + 1));
+        h2d(dB.rowids, B->rowids, sizeof(int32_t) * B->nnz);
+        h2d(dB.vals, B->vals, size_t(vs) * B->nnz);
+        slapcu_csc a{dA.nrows, dA.ncols, dA.nnz, dA.colptr, dA.rowids, dA.vals};
+        slapcu_csc b{dB.nrows, dB.ncols, dB.nnz, dB.colptr, dB.rowids, dB.vals};
+        slapcu_csc_out dC{};
+        auto cleanup = [&]() {
+            for (void* p : {(void*)dA.colptr, (void*)dA.rowids, dA.vals, (void*)dB.colptr, (void*)dB.rowids, dB.vals,
+                            (void*)dC.colptr, (void*)dC.rowids, dC.vals})
+                if (p) cudaFreeAsync(p, c.stream);
+        };
+        try {
+            const DevCsc av = view(a), bv = view(b);
+            SLAPCU_CUDA(cudaMallocAsync((void**)&dC.colptr, sizeof(int64_t) * (bv.ncols + 1), c.stream));
+            const int64_t nnz = spgemm_symbolic(c, av, bv, alg, dC.colptr);
+            SLAPCU_CUDA(cudaMallocAsync((void**)&dC.rowids, sizeof(int32_t) * std::max<int64_t>(nnz, 1), c.stream));
+            SLAPCU_CUDA(cudaMallocAsync(&dC.vals, size_t(vs) * std::max<int64_t>(nnz, 1), c.stream));
+            spgemm_numeric(c, av, bv, sr, alg, dC.colptr, dC.rowids, dC.vals);
+            C->nrows = av.nrows;
+            C->ncols = bv.ncols;
+            C->nnz = nnz;
+            C->colptr = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * (bv.ncols + 1)));
+            C->rowids = static_cast<int32_t*>(std::malloc(sizeof(int32_t) * std::max<int64_t>(nnz, 1)));
+            C->vals = std::malloc(size_t(vs) * std::max<int64_t>(nnz, 1));
+            if (!C->colptr || !C->rowids || !C->vals) throw std::bad_alloc();
+            SLAPCU_CUDA(cudaMemcpyAsync(C->colptr, dC.colptr, sizeof(int64_t) * (bv.ncols + 1), cudaMemcpyDeviceToHost,
+                                        c.stream));
+            if (nnz) {
+                SLAPCU_CUDA(cudaMemcpyAsync(C->rowids, dC.rowids, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost, c.stream));
+                SLAPCU_CUDA(cudaMemcpyAsync(C->vals, dC.vals, size_t(vs) * nnz, cudaMemcpyDeviceToHost, c.stream));
+            }
+            SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+        } catch (...) {
+            cleanup();
+            throw;
+        }
+        cleanup();
+    });
+}
+
+slapcu_status slapcu_csc_free(slapcu_ctx ctx, slapcu_csc_out* C) {
+    return guarded(ctx, [&](Ctx& c) {
+        if (!C) return;
+        for (void* p : {(void*)C->colptr, (void*)C->rowids, C->vals})
+            if (p) SLAPCU_CUDA(cudaFreeAsync(p, c.stream));
+        C->colptr = nullptr;
+        C->rowids = nullptr;
+        C->vals = nullptr;
+    });
+}
+
+void slapcu_host_free(slapcu_host_csc* C) {
+    if (!C) return;
+    std::free(C->colptr);
+    std::free(C->rowids);
+    std::free(C->vals);
+    C->colptr = nullptr;
+    C->rowids = nullptr;
+    C->vals = nullptr;
+}
+
+slapcu_status slapcu_dcsc_colptr(slapcu_ctx ctx, int64_t ncols, int64_t nzc, const int32_t* jc, const int32_t* cp,
+                                 int64_t* colptr) {
+    return guarded(ctx, [&](Ctx& c) {
+        require(cp && colptr && (nzc == 0 || jc), SLAPCU_ERR_INVALID, "null argument");
+        dcsc_colptr(c, ncols, nzc, jc, cp, colptr);
+    });
+}
+
+slapcu_status slapcu_merge_symbolic(slapcu_ctx ctx, int nparts, const slapcu_csc* parts, int64_t* c_colptr,
+                                    int64_t* c_nnz) {
+    return guarded(ctx, [&](Ctx& c) {
+        require(parts && c_colptr && nparts >= 1, SLAPCU_ERR_INVALID, "bad merge arguments");
+        std::vector<DevCsc> v(nparts);
+        for (int s = 0; s < nparts; ++s) v[s] = view(parts[s]);
+        const int64_t n = merge_symbolic(c, nparts, v.data(), c_colptr);
+        if (c_nnz) *c_nnz = n;
+    });
+}
+
+slapcu_status slapcu_merge_numeric(slapcu_ctx ctx, int nparts, const slapcu_csc* parts, slapcu_semiring sr,
+                                   const int64_t* c_colptr, int32_t* c_rowids, void* c_vals) {
+    return guarded(ctx, [&](Ctx& c) {
+        require(parts && c_colptr && nparts >= 1, SLAPCU_ERR_INVALID, "bad merge arguments");
+        std::vector<DevCsc> v(nparts);
+        for (int s = 0; s < nparts; ++s) v[s] = view(parts[s]);
+        merge_numeric(c, nparts, v.data(), sr, c_colptr, c_rowids, c_vals);
+    });
+}
+
+slapcu_status slapcu_gen_rmat(slapcu_ctx ctx, int scale, int edge_factor, uint64_t seed, double a, double b, double cc,
+                              double d, slapcu_csc_out* out) {
+    return guarded(ctx, [&](Ctx& c) {
+        require(out, SLAPCU_ERR_INVALID, "null output");
+        gen_rmat(c, scale, edge_factor, seed, a, b, cc, d, out);
+    });
+}
+
+slapcu_status slapcu_gen_er(slapcu_ctx ctx, int64_t n, int64_t draws, uint64_t seed, int with_values,
+                            slapcu_csc_out* out) {
+    return guarded(ctx, [&](Ctx& c) {
+        require(out, SLAPCU_ERR_INVALID, "null output");
+        gen_er(c, n, draws, seed, with_values != 0, out);
+    });
+}
+
+slapcu_status slapcu_gen_one_per_row(slapcu_ctx ctx, int64_t n, int64_t ncols, uint64_t seed, slapcu_csc_out* out) {
+    return guarded(ctx, [&](Ctx& c) {
+        require(out, SLAPCU_ERR_INVALID, "null output");
+        gen_one_per_row(c, n, ncols, seed, out);
+    });
+}
+
+slapcu_status slapcu_fill_values(slapcu_ctx ctx, slapcu_semiring sr, int kind, const slapcu_csc* m, void* vals) {
+    return guarded(ctx, [&](Ctx& c) {
+        require(m && vals, SLAPCU_ERR_INVALID, "null argument");
+        fill_values(c, sr, kind, view(*m), vals);
+    });
+}
+
+slapcu_status slapcu_permute_symmetric(slapcu_ctx ctx, const slapcu_csc* A, uint64_t seed, slapcu_semiring sr,
+                                       slapcu_csc_out* out) {
+    return guarded(ctx, [&](Ctx& c) {
+        require(A && out, SLAPCU_ERR_INVALID, "null argument");
+        permute_symmetric(c, view(*A), seed, sr, out);
+    });
+}
+
+slapcu_status slapcu_slice_cols(slapcu_ctx ctx, const slapcu_csc* B, slapcu_semiring sr, int64_t c0, int64_t c1,
+                                slapcu_csc_out* out) {
+    return guarded(ctx, [&](Ctx& c) {
+        require(B && out, SLAPCU_ERR_INVALID, "null argument");
+        slice_cols(c, view(*B), sr, c0, c1, out);
+    });
+}
+
+slapcu_status slapcu_column_checksums(slapcu_ctx ctx, const slapcu_csc* m, slapcu_semiring sr, int with_values,
+                                      uint64_t* sums) {
+    return guarded(ctx, [&](Ctx& c) {
+        require(m && sums, SLAPCU_ERR_INVALID, "null argument");
+        column_checksums(c, view(*m), sr, with_values != 0, sums);
+    });
+}
+
+}  // extern "C"

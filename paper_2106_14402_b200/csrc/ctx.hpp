@@ -1,0 +1,225 @@
+// ctx.hpp -- host-side context, workspace and launch bookkeeping shared by
+// the CUDA translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <tuple>
+#include <utility>
+#include <vector>
+
+#include "common.cuh"
+#include "slapcu.h"
+
+struct slapcu_ctx_s;
+
+namespace slapcu {
+
+// Device CSC view (colptr int64, rowids int32, typed values).
+struct DevCsc {
+    int64_t nrows = 0, ncols = 0, nnz = 0;
+    const int64_t* cp = nullptr;
+    const int32_t* rw = nullptr;
+    const void* v = nullptr;
+};
+
+inline DevCsc view(const slapcu_csc& m) { return DevCsc{m.nrows, m.ncols, m.nnz, m.colptr, m.rowids, m.vals}; }
+
+// Stream-ordered device buffer from the default memory pool.
+class DevBuf {
+public:
+    DevBuf() = default;
+    DevBuf(size_t bytes, cudaStream_t s) : s_(s) { alloc(bytes); }
+    ~DevBuf() { release(); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_), s_(o.s_) { o.p_ = nullptr; o.n_ = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            p_ = o.p_;
+            n_ = o.n_;
+            s_ = o.s_;
+            o.p_ = nullptr;
+            o.n_ = 0;
+        }
+        return *this;
+    }
+    void reset(size_t bytes, cudaStream_t s) {
+        if (bytes <= n_ && p_) { s_ = s; return; }
+        release();
+        s_ = s;
+        alloc(bytes);
+    }
+    template <class T>
+    T* as() const { return static_cast<T*>(p_); }
+    void* get() const { return p_; }
+    size_t size() const { return n_; }
+    void release() {
+        if (p_) cudaFreeAsync(p_, s_);
+        p_ = nullptr;
+        n_ = 0;
+    }
+    void* detach() { void* p = p_; p_ = nullptr; n_ = 0; return p; }
+
+private:
+    void alloc(size_t bytes) {
+        if (bytes == 0) bytes = 16;
+        SLAPCU_CUDA(cudaMallocAsync(&p_, bytes, s_));
+        n_ = bytes;
+    }
+    void* p_ = nullptr;
+    size_t n_ = 0;
+    cudaStream_t s_ = nullptr;
+};
+
+// State carried from the symbolic phase to the numeric phase of one product.
+struct Plan {
+    const void* a_key = nullptr;  // identity of the operands the plan is for
+    const void* b_key = nullptr;
+    int64_t a_ncols = -1, b_ncols = -1, b_nnz = -1;
+    DevBuf flops;   // int64[B.ncols]
+    DevBuf counts;  // int64[B.ncols + 1]
+    DevBuf cursor;  // int32[B.nnz] per-B-entry row-tile cursors
+    bool valid = false;
+};
+
+struct Options {
+    int tile_rows_log2 = 18;      // numeric dense-tile height
+    int sym_tile_rows_log2 = 19;  // symbolic bitmap height
+    int64_t light_nnz_max = 4096;     // numeric hash path if nnz <= this
+    int64_t light_flops_max = 16384;  // symbolic hash path if flops <= this
+};
+
+// Kernel classes for the per-class device-time breakdown (profiling mode).
+enum KClass {
+    KC_OTHER = 0,
+    KC_FLOPS,
+    KC_BIN,
+    KC_SYM_LIGHT,
+    KC_SYM_HEAVY,
+    KC_SCAN,
+    KC_NUM_LIGHT,
+    KC_NUM_HEAVY,
+    KC_MERGE,
+    KC_GEN,
+    KC_COUNT
+};
+
+struct Prof {
+    bool on = false;
+    std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> pending;
+    std::vector<cudaEvent_t> pool;
+    double ms[KC_COUNT] = {};
+    int64_t n[KC_COUNT] = {};
+};
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int64_t launches = 0;
+    Options opt;
+    Plan plan;
+    std::string last_error;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    float sym_ms = 0.f, num_ms = 0.f;
+    int smem_optin = 0;
+    int num_sms = 0;
+    Prof prof;
+    int cur_cls = KC_OTHER;
+    DevBuf err_flag;      // int
+    DevBuf scratch_small; // misc small counters
+    // merge state carried from merge_symbolic to merge_numeric
+    struct {
+        DevBuf ranks, tot, counts;
+        const void* key0 = nullptr;
+        int q = 0;
+        int64_t ncols = -1;
+    } merge;
+};
+
+Ctx& ctx_of(slapcu_ctx c);
+
+// spgemm.cu
+void spgemm_flops(Ctx& c, const DevCsc& A, const DevCsc& B, int64_t* flops_dev, int64_t* total);
+int64_t spgemm_symbolic(Ctx& c, const DevCsc& A, const DevCsc& B, int alg, int64_t* c_colptr);
+void spgemm_numeric(Ctx& c, const DevCsc& A, const DevCsc& B, int sr, int alg, const int64_t* c_colptr,
+                    int32_t* c_rowids, void* c_vals);
+void dcsc_colptr(Ctx& c, int64_t ncols, int64_t nzc, const int32_t* jc, const int32_t* cp, int64_t* colptr);
+void exclusive_scan_i64(Ctx& c, const int64_t* in, int64_t* out, int64_t n);
+
+// merge.cu
+int64_t merge_symbolic(Ctx& c, int nparts, const DevCsc* parts, int64_t* c_colptr);
+void merge_numeric(Ctx& c, int nparts, const DevCsc* parts, int sr, const int64_t* c_colptr, int32_t* c_rowids,
+                   void* c_vals);
+
+// gen.cu
+void gen_rmat(Ctx& c, int scale, int ef, uint64_t seed, double a, double b, double cc, double d, slapcu_csc_out* out);
+void gen_er(Ctx& c, int64_t n, int64_t draws, uint64_t seed, bool with_values, slapcu_csc_out* out);
+void gen_one_per_row(Ctx& c, int64_t n, int64_t ncols, uint64_t seed, slapcu_csc_out* out);
+void fill_values(Ctx& c, int sr, int kind, const DevCsc& m, void* vals);
+void permute_symmetric(Ctx& c, const DevCsc& A, uint64_t seed, int sr, slapcu_csc_out* out);
+void slice_cols(Ctx& c, const DevCsc& B, int sr, int64_t c0, int64_t c1, slapcu_csc_out* out);
+void column_checksums(Ctx& c, const DevCsc& m, int sr, bool with_values, uint64_t* sums);
+
+// ---- profiling: CUDA events around every launch on the context stream
+
+inline cudaEvent_t prof_event(Ctx& c) {
+    if (!c.prof.pool.empty()) {
+        cudaEvent_t e = c.prof.pool.back();
+        c.prof.pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    SLAPCU_CUDA(cudaEventCreate(&e));
+    return e;
+}
+
+// Resolves recorded event pairs into the per-class totals (synchronizes).
+inline void prof_flush(Ctx& c) {
+    for (auto& [cls, a, b] : c.prof.pending) {
+        cudaEventSynchronize(b);
+        float t = 0.f;
+        cudaEventElapsedTime(&t, a, b);
+        c.prof.ms[cls] += t;
+        c.prof.n[cls] += 1;
+        c.prof.pool.push_back(a);
+        c.prof.pool.push_back(b);
+    }
+    c.prof.pending.clear();
+}
+
+// Enqueues f() (one or more launches) bracketed by events when profiling.
+template <class F>
+inline void timed(Ctx& c, int cls, F&& f) {
+    if (!c.prof.on) {
+        f();
+        return;
+    }
+    cudaEvent_t a = prof_event(c), b = prof_event(c);
+    SLAPCU_CUDA(cudaEventRecord(a, c.stream));
+    f();
+    SLAPCU_CUDA(cudaEventRecord(b, c.stream));
+    c.prof.pending.emplace_back(cls, a, b);
+}
+
+struct KScope {
+    Ctx& c;
+    int prev;
+    KScope(Ctx& c_, int k) : c(c_), prev(c_.cur_cls) { c.cur_cls = k; }
+    ~KScope() { c.cur_cls = prev; }
+};
+
+template <class K, class... Args>
+inline void launch(Ctx& c, K kernel, dim3 grid, dim3 block, size_t smem, Args... args) {
+    if (grid.x == 0 || grid.y == 0 || grid.z == 0) return;
+    timed(c, c.cur_cls, [&] {
+        kernel<<<grid, block, smem, c.stream>>>(args...);
+        SLAPCU_LAUNCH_CHECK();
+    });
+    ++c.launches;
+}
+
+}  // namespace slapcu

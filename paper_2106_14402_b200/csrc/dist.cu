@@ -1,0 +1,532 @@
+// dist.cu -- 2D Sparse SUMMA and 3D communication-avoiding SpGEMM over NCCL.
+//
+// Replaces the reference's simulated transport (comm.hpp:178-348, ranks are
+// threads rendezvousing on a mutex) with one process (or host thread) per GPU
+// and NCCL communicators over NVLink 5 / NVSwitch:
+//
+//   summa2d_spgemm (summa.hpp:106-163)
+//     stage s: A(i,s) broadcast on the row communicator, B(s,j) on the column
+//     communicator (summa.hpp:133-140 broadcast_block) -- here ncclBroadcast of
+//     the CSC arrays straight out of the owner's device buffers, issued on a
+//     dedicated comm stream one stage AHEAD of the local multiply into the other
+//     half of a double buffer, so stage s+1's transfer overlaps stage s's
+//     SpGEMM; the partials are merged once at the end in stage order
+//     (summa.hpp:156) by the device multiway merge.
+//   ca3d_spgemm (spgemm3d.hpp:21-106)
+//     per-layer SUMMA, C_int split into c column pieces (block_offsets), one
+//     fiber exchange (counts all-gathered, then grouped ncclSend/ncclRecv --
+//     NCCL has no alltoallv), merge in fiber order.
+//
+// Block metadata (dims, nnz) of every rank is all-gathered once per call, so
+// every rank knows every broadcast's size up front (NCCL needs matching
+// counts) and shape errors are detected consistently on all ranks before any
+// data collective is posted.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "ctx.hpp"
+
+#define SLAPCU_NCCL(call)                                                                               \
+    do {                                                                                                \
+        ncclResult_t r_ = (call);                                                                       \
+        if (r_ != ncclSuccess)                                                                          \
+            throw ::slapcu::Fail{SLAPCU_ERR_COMM, std::string(#call) + ": " + ncclGetErrorString(r_)};  \
+    } while (0)
+
+struct slapcu_comm_s {
+    slapcu_ctx ctx = nullptr;
+    int rank = 0, nranks = 1;
+    ncclComm_t world = nullptr;
+    std::map<std::string, ncclComm_t> splits;
+    cudaStream_t comm_stream = nullptr;
+    int64_t calls[4] = {0, 0, 0, 0};
+    int64_t bytes[4] = {0, 0, 0, 0};
+};
+
+namespace slapcu {
+namespace {
+
+enum { kBcast = 0, kAlltoallv = 1, kReduce = 2, kAllgatherv = 3 };
+
+bool is_square(int64_t v, int64_t* root) {
+    if (v < 0) return false;
+    int64_t r = (int64_t)std::llround(std::sqrt((double)v));
+    for (int64_t c = std::max<int64_t>(r - 1, 0); c <= r + 1; ++c)
+        if (c * c == v) {
+            *root = c;
+            return true;
+        }
+    return false;
+}
+
+ncclComm_t split(slapcu_comm_s* cm, const std::string& name, int color, int key) {
+    auto it = cm->splits.find(name);
+    if (it != cm->splits.end()) return it->second;
+    ncclComm_t out = nullptr;
+    SLAPCU_NCCL(ncclCommSplit(cm->world, color, key, &out, nullptr));
+    cm->splits[name] = out;
+    return out;
+}
+
+// Block metadata of every rank: [A.nrows, A.ncols, A.nnz, B.nrows, B.ncols, B.nnz].
+std::vector<int64_t> allgather_meta(slapcu_comm_s* cm, Ctx& c, const DevCsc& A, const DevCsc& B) {
+    const int p = cm->nranks;
+    int64_t mine[6] = {A.nrows, A.ncols, A.nnz, B.nrows, B.ncols, B.nnz};
+    DevBuf d(sizeof(int64_t) * 6 * (p + 1), c.stream);
+    SLAPCU_CUDA(cudaMemcpyAsync(d.as<int64_t>() + 6 * p, mine, sizeof(mine), cudaMemcpyHostToDevice, c.stream));
+    SLAPCU_NCCL(ncclAllGather(d.as<int64_t>() + 6 * p, d.as<int64_t>(), 6, ncclInt64, cm->world, c.stream));
+    std::vector<int64_t> h(6 * p);
+    SLAPCU_CUDA(cudaMemcpyAsync(h.data(), d.get(), sizeof(int64_t) * 6 * p, cudaMemcpyDeviceToHost, c.stream));
+    SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+    cm->calls[kAllgatherv] += 1;
+    cm->bytes[kAllgatherv] += sizeof(mine);
+    return h;
+}
+
+// One owned device CSC.
+struct Block {
+    DevBuf cp, rw, v;
+    int64_t nrows = 0, ncols = 0, nnz = 0;
+    DevCsc view() const { return DevCsc{nrows, ncols, nnz, cp.as<int64_t>(), rw.as<int32_t>(), v.get()}; }
+};
+
+// Receive slot for a broadcast block, sized for the largest block it holds.
+struct Slot {
+    DevBuf cp, rw, v;
+    void reserve(Ctx& c, int64_t ncols, int64_t nnz, int vs) {
+        cp.reset(sizeof(int64_t) * (ncols + 1), c.stream);
+        rw.reset(sizeof(int32_t) * std::max<int64_t>(nnz, 1), c.stream);
+        v.reset(size_t(vs) * std::max<int64_t>(nnz, 1), c.stream);
+    }
+};
+
+// ncclBroadcast of one CSC block (three arrays) from group rank `root`.  The
+// root broadcasts in place from its own block; the others receive into slot.
+DevCsc bcast_block(slapcu_comm_s* cm, ncclComm_t comm, int my_group_rank, int root, const DevCsc& mine,
+                   int64_t nrows, int64_t ncols, int64_t nnz, int vs, Slot& slot, cudaStream_t s) {
+    const bool am_root = my_group_rank == root;
+    int64_t* cp = am_root ? const_cast<int64_t*>(mine.cp) : slot.cp.as<int64_t>();
+    int32_t* rw = am_root ? const_cast<int32_t*>(mine.rw) : slot.rw.as<int32_t>();
+    void* v = am_root ? const_cast<void*>(mine.v) : slot.v.get();
+    SLAPCU_NCCL(ncclBroadcast(cp, cp, size_t(ncols + 1), ncclInt64, root, comm, s));
+    if (nnz) {
+        SLAPCU_NCCL(ncclBroadcast(rw, rw, size_t(nnz), ncclInt32, root, comm, s));
+        SLAPCU_NCCL(ncclBroadcast(v, v, size_t(nnz) * vs, ncclUint8, root, comm, s));
+    }
+    if (am_root) {
+        cm->calls[kBcast] += 1;  // one logical block broadcast, like comm.hpp:202-218
+        cm->bytes[kBcast] += sizeof(int64_t) * (ncols + 1) + (sizeof(int32_t) + vs) * nnz;
+    } else {
+        cm->calls[kBcast] += 1;
+    }
+    return DevCsc{nrows, ncols, nnz, cp, rw, v};
+}
+
+// Local multiply into an owned block (symbolic -> allocate -> numeric).
+void local_multiply(Ctx& c, const DevCsc& A, const DevCsc& B, int sr, int alg, Block& out, float* ms) {
+    const int vs = value_size(sr);
+    out.nrows = A.nrows;
+    out.ncols = B.ncols;
+    out.cp.reset(sizeof(int64_t) * (B.ncols + 1), c.stream);
+    out.nnz = spgemm_symbolic(c, A, B, alg, out.cp.as<int64_t>());
+    out.rw.reset(sizeof(int32_t) * std::max<int64_t>(out.nnz, 1), c.stream);
+    out.v.reset(size_t(vs) * std::max<int64_t>(out.nnz, 1), c.stream);
+    spgemm_numeric(c, A, B, sr, alg, out.cp.as<int64_t>(), out.rw.as<int32_t>(), out.v.get());
+    *ms += c.sym_ms + c.num_ms;
+}
+
+void merge_blocks(Ctx& c, const std::vector<DevCsc>& parts, int sr, slapcu_csc_out* C) {
+    const int vs = value_size(sr);
+    const int64_t n = parts[0].ncols;
+    C->nrows = parts[0].nrows;
+    C->ncols = n;
+    SLAPCU_CUDA(cudaMallocAsync((void**)&C->colptr, sizeof(int64_t) * (n + 1), c.stream));
+    C->nnz = merge_symbolic(c, (int)parts.size(), parts.data(), C->colptr);
+    SLAPCU_CUDA(cudaMallocAsync((void**)&C->rowids, sizeof(int32_t) * std::max<int64_t>(C->nnz, 1), c.stream));
+    SLAPCU_CUDA(cudaMallocAsync(&C->vals, size_t(vs) * std::max<int64_t>(C->nnz, 1), c.stream));
+    merge_numeric(c, (int)parts.size(), parts.data(), sr, C->colptr, C->rowids, C->vals);
+}
+
+void move_out(Ctx& c, Block& b, slapcu_csc_out* C) {
+    C->nrows = b.nrows;
+    C->ncols = b.ncols;
+    C->nnz = b.nnz;
+    C->colptr = static_cast<int64_t*>(b.cp.detach());
+    C->rowids = static_cast<int32_t*>(b.rw.detach());
+    C->vals = b.v.detach();
+    (void)c;
+}
+
+struct Timer {
+    cudaEvent_t a = nullptr, b = nullptr;
+    Timer() {
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+    }
+    ~Timer() {
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+    }
+    float ms() {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, a, b);
+        return t;
+    }
+};
+
+// The q-stage SUMMA over a q x q (layer) grid.  `gr_row`/`gr_col` are this
+// rank's group ranks in the row / column communicators (= its column / row
+// coordinate); meta_of(i,j) returns the metadata index of grid rank (i,j).
+template <class MetaOf>
+void summa_stages(slapcu_comm_s* cm, Ctx& c, ncclComm_t row, ncclComm_t col, int q, int myi, int myj,
+                  const DevCsc& A, const DevCsc& B, int sr, int alg, const std::vector<int64_t>& meta, MetaOf meta_of,
+                  std::vector<Block>& partials, slapcu_dist_stats* st) {
+    const int vs = value_size(sr);
+    // size the double buffer for the largest block this rank will receive
+    int64_t a_nc = 0, a_nz = 0, b_nc = 0, b_nz = 0;
+    for (int s = 0; s < q; ++s) {
+        const int64_t* ma = &meta[6 * meta_of(myi, s)];
+        const int64_t* mb = &meta[6 * meta_of(s, myj)];
+        a_nc = std::max(a_nc, ma[1]);
+        a_nz = std::max(a_nz, ma[2]);
+        b_nc = std::max(b_nc, mb[4]);
+        b_nz = std::max(b_nz, mb[5]);
+    }
+    Slot sa[2], sb[2];
+    const int nslots = q > 1 ? 2 : 1;
+    for (int k = 0; k < nslots; ++k) {
+        sa[k].reserve(c, a_nc, a_nz, vs);
+        sb[k].reserve(c, b_nc, b_nz, vs);
+    }
+    std::vector<cudaEvent_t> bc_done(q), slot_free(2);
+    for (auto& e : bc_done) SLAPCU_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : slot_free) SLAPCU_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    std::vector<DevCsc> sa_view(q), sb_view(q);
+    // the comm stream must not start before the inputs are ready on the compute stream
+    cudaEvent_t ready;
+    SLAPCU_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    SLAPCU_CUDA(cudaEventRecord(ready, c.stream));
+    SLAPCU_CUDA(cudaStreamWaitEvent(cm->comm_stream, ready, 0));
+    auto issue = [&](int s) {
+        const int slot = s % 2;
+        if (s >= 2) SLAPCU_CUDA(cudaStreamWaitEvent(cm->comm_stream, slot_free[slot], 0));
+        const int64_t* ma = &meta[6 * meta_of(myi, s)];
+        const int64_t* mb = &meta[6 * meta_of(s, myj)];
+        SLAPCU_NCCL(ncclGroupStart());
+        sa_view[s] = bcast_block(cm, row, myj, s, A, ma[0], ma[1], ma[2], vs, sa[slot], cm->comm_stream);
+        sb_view[s] = bcast_block(cm, col, myi, s, B, mb[3], mb[4], mb[5], vs, sb[slot], cm->comm_stream);
+        SLAPCU_NCCL(ncclGroupEnd());
+        SLAPCU_CUDA(cudaEventRecord(bc_done[s], cm->comm_stream));
+    };
+    partials.resize(q);
+    float local_ms = 0.f, exposed = 0.f;
+    Timer w;
+    if (q > 1) issue(0);
+    for (int s = 0; s < q; ++s) {
+        if (q > 1 && s + 1 < q) issue(s + 1);  // prefetch the next stage while this one multiplies
+        DevCsc a = A, b = B;
+        if (q > 1) {
+            SLAPCU_CUDA(cudaEventRecord(w.a, c.stream));
+            SLAPCU_CUDA(cudaStreamWaitEvent(c.stream, bc_done[s], 0));
+            SLAPCU_CUDA(cudaEventRecord(w.b, c.stream));
+            SLAPCU_CUDA(cudaEventSynchronize(w.b));
+            exposed += w.ms();
+            a = sa_view[s];
+            b = sb_view[s];
+        }
+        if (a.ncols != b.nrows) throw Fail{SLAPCU_ERR_DIM, "SUMMA stage blocks misaligned on the inner dimension"};
+        int64_t f = 0;
+        spgemm_flops(c, a, b, nullptr, &f);
+        if (st) st->flops += f;
+        local_multiply(c, a, b, sr, alg, partials[s], &local_ms);
+        SLAPCU_CUDA(cudaEventRecord(slot_free[s % 2], c.stream));
+    }
+    SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+    SLAPCU_CUDA(cudaStreamSynchronize(cm->comm_stream));
+    for (auto& e : bc_done) cudaEventDestroy(e);
+    for (auto& e : slot_free) cudaEventDestroy(e);
+    cudaEventDestroy(ready);
+    if (st) {
+        st->ms_local += local_ms;
+        st->ms_exposed_bcast += exposed;
+        st->stages = q;
+    }
+}
+
+}  // namespace
+}  // namespace slapcu
+
+using namespace slapcu;
+
+extern "C" {
+
+slapcu_status slapcu_comm_unique_id(void* id128) {
+    if (!id128) return SLAPCU_ERR_INVALID;
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return SLAPCU_ERR_COMM;
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    std::memcpy(id128, &id, sizeof(id));
+    return SLAPCU_OK;
+}
+
+slapcu_status slapcu_comm_create(slapcu_comm* out, slapcu_ctx ctx, int rank, int nranks, const void* id128) {
+    if (!out || !ctx || !id128 || nranks < 1 || rank < 0 || rank >= nranks) return SLAPCU_ERR_INVALID;
+    *out = nullptr;
+    auto* cm = new slapcu_comm_s;
+    cm->ctx = ctx;
+    cm->rank = rank;
+    cm->nranks = nranks;
+    Ctx& c = ctx_of(ctx);
+    try {
+        SLAPCU_CUDA(cudaSetDevice(c.device));
+        SLAPCU_CUDA(cudaStreamCreateWithFlags(&cm->comm_stream, cudaStreamNonBlocking));
+        ncclUniqueId id;
+        std::memcpy(&id, id128, sizeof(id));
+        SLAPCU_NCCL(ncclCommInitRank(&cm->world, nranks, id, rank));
+    } catch (const Fail& e) {
+        c.last_error = e.msg;
+        if (cm->comm_stream) cudaStreamDestroy(cm->comm_stream);
+        delete cm;
+        return e.st;
+    }
+    *out = cm;
+    return SLAPCU_OK;
+}
+
+slapcu_status slapcu_comm_destroy(slapcu_comm cm) {
+    if (!cm) return SLAPCU_ERR_INVALID;
+    cudaSetDevice(ctx_of(cm->ctx).device);
+    for (auto& kv : cm->splits) ncclCommDestroy(kv.second);
+    if (cm->world) ncclCommDestroy(cm->world);
+    if (cm->comm_stream) cudaStreamDestroy(cm->comm_stream);
+    delete cm;
+    return SLAPCU_OK;
+}
+
+slapcu_status slapcu_comm_counters(slapcu_comm cm, int kind, int64_t* calls, int64_t* bytes) {
+    if (!cm || kind < 0 || kind > 3) return SLAPCU_ERR_INVALID;
+    if (calls) *calls = cm->calls[kind];
+    if (bytes) *bytes = cm->bytes[kind];
+    return SLAPCU_OK;
+}
+
+slapcu_status slapcu_summa2d(slapcu_comm cm, const slapcu_csc* A_local, const slapcu_csc* B_local,
+                             slapcu_semiring sr, slapcu_alg alg, slapcu_csc_out* C_local, slapcu_dist_stats* stats) {
+    if (!cm || !A_local || !B_local || !C_local) return SLAPCU_ERR_INVALID;
+    Ctx& c = ctx_of(cm->ctx);
+    try {
+        SLAPCU_CUDA(cudaSetDevice(c.device));
+        if (value_size(sr) == 0) throw Fail{SLAPCU_ERR_INVALID, "unknown semiring"};
+        int64_t q = 0;
+        if (!is_square(cm->nranks, &q))
+            throw Fail{SLAPCU_ERR_SHAPE, "2D SUMMA needs a square process grid, got p=" + std::to_string(cm->nranks)};
+        if (stats) *stats = slapcu_dist_stats{};
+        Timer total;
+        SLAPCU_CUDA(cudaEventRecord(total.a, c.stream));
+        const DevCsc A = view(*A_local), B = view(*B_local);
+        const int i = cm->rank / (int)q, j = cm->rank % (int)q;
+        std::vector<int64_t> meta;
+        ncclComm_t row = nullptr, col = nullptr;
+        if (q > 1) {
+            meta = allgather_meta(cm, c, A, B);
+            // summa.hpp:116-122: every stage pair must agree on the inner extent
+            for (int ii = 0; ii < q; ++ii)
+                for (int jj = 0; jj < q; ++jj)
+                    for (int s = 0; s < q; ++s)
+                        if (meta[6 * (ii * q + s) + 1] != meta[6 * (s * q + jj) + 3])
+                            throw Fail{SLAPCU_ERR_DIM, "SUMMA inner block offsets of A and B disagree"};
+            row = split(cm, "row2d", i, j);
+            col = split(cm, "col2d", j, i);
+        } else {
+            meta = {A.nrows, A.ncols, A.nnz, B.nrows, B.ncols, B.nnz};
+            if (A.ncols != B.nrows) throw Fail{SLAPCU_ERR_DIM, "SUMMA inner dims disagree"};
+        }
+        std::vector<Block> partials;
+        summa_stages(cm, c, row, col, (int)q, i, j, A, B, sr, alg, meta,
+                     [&](int ii, int jj) { return q > 1 ? ii * (int)q + jj : 0; }, partials, stats);
+        Timer mt;
+        SLAPCU_CUDA(cudaEventRecord(mt.a, c.stream));
+        if (q == 1) {
+            move_out(c, partials[0], C_local);
+        } else {
+            std::vector<DevCsc> pv;
+            for (auto& p : partials) pv.push_back(p.view());
+            merge_blocks(c, pv, sr, C_local);
+        }
+        SLAPCU_CUDA(cudaEventRecord(mt.b, c.stream));
+        SLAPCU_CUDA(cudaEventRecord(total.b, c.stream));
+        SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+        if (stats) {
+            stats->ms_merge = mt.ms();
+            stats->ms_total = total.ms();
+            stats->nnz_out = C_local->nnz;
+        }
+        return SLAPCU_OK;
+    } catch (const Fail& e) {
+        c.last_error = e.msg;
+        return e.st;
+    }
+}
+
+slapcu_status slapcu_ca3d(slapcu_comm cm, int layers, const slapcu_csc* A_local, const slapcu_csc* B_local,
+                          slapcu_semiring sr, slapcu_alg alg, slapcu_csc_out* C_local, slapcu_dist_stats* stats) {
+    if (!cm || !A_local || !B_local || !C_local) return SLAPCU_ERR_INVALID;
+    Ctx& c = ctx_of(cm->ctx);
+    try {
+        SLAPCU_CUDA(cudaSetDevice(c.device));
+        const int vs = value_size(sr);
+        if (vs == 0) throw Fail{SLAPCU_ERR_INVALID, "unknown semiring"};
+        const int p = cm->nranks;
+        if (layers < 1 || p % layers != 0)
+            throw Fail{SLAPCU_ERR_SHAPE, "cannot split " + std::to_string(p) + " ranks into " + std::to_string(layers) +
+                                             " layers"};
+        int64_t q = 0;
+        if (!is_square(p / layers, &q))
+            throw Fail{SLAPCU_ERR_SHAPE, "p/c = " + std::to_string(p / layers) + " is not a perfect square"};
+        if (stats) *stats = slapcu_dist_stats{};
+        const bool warn = (double)layers > std::cbrt((double)p) + 1e-9;  // spgemm3d.hpp:38-41
+        if (stats) stats->layer_warning = warn;
+        Timer total;
+        SLAPCU_CUDA(cudaEventRecord(total.a, c.stream));
+        const DevCsc A = view(*A_local), B = view(*B_local);
+        const int qq = (int)(q * q);
+        const int l = cm->rank / qq, i = (cm->rank % qq) / (int)q, j = cm->rank % (int)q;  // grid.cpp:57
+        std::vector<int64_t> meta = allgather_meta(cm, c, A, B);
+        for (int ii = 0; ii < q; ++ii)
+            for (int jj = 0; jj < q; ++jj)
+                for (int s = 0; s < q; ++s)
+                    if (meta[6 * (l * qq + ii * (int)q + s) + 1] != meta[6 * (l * qq + s * (int)q + jj) + 3])
+                        throw Fail{SLAPCU_ERR_DIM, "3D SpGEMM stage blocks misaligned on the inner dimension"};
+        ncclComm_t row = nullptr, col = nullptr;
+        if (q > 1) {
+            row = split(cm, "row3d_" + std::to_string(layers), l * (int)q + i, j);
+            col = split(cm, "col3d_" + std::to_string(layers), l * (int)q + j, i);
+        }
+        ncclComm_t fiber = split(cm, "fiber3d_" + std::to_string(layers), i * (int)q + j, l);
+        // per-layer SUMMA
+        std::vector<Block> partials;
+        summa_stages(cm, c, row, col, (int)q, i, j, A, B, sr, alg, meta,
+                     [&](int ii, int jj) { return l * qq + ii * (int)q + jj; }, partials, stats);
+        Timer mt;
+        SLAPCU_CUDA(cudaEventRecord(mt.a, c.stream));
+        // C_int: the layer's merged product (a view; owned by partials[0] or cint_out)
+        slapcu_csc_out cint_out{};
+        DevCsc ci;
+        if (q == 1) {
+            ci = partials[0].view();
+        } else {
+            std::vector<DevCsc> pv;
+            for (auto& pp : partials) pv.push_back(pp.view());
+            merge_blocks(c, pv, sr, &cint_out);
+            partials.clear();
+            ci = DevCsc{cint_out.nrows, cint_out.ncols, cint_out.nnz, cint_out.colptr, cint_out.rowids, cint_out.vals};
+        }
+        struct FreeOut {
+            Ctx& c;
+            slapcu_csc_out& o;
+            ~FreeOut() {
+                if (o.colptr) cudaFreeAsync(o.colptr, c.stream);
+                if (o.rowids) cudaFreeAsync(o.rowids, c.stream);
+                if (o.vals) cudaFreeAsync(o.vals, c.stream);
+            }
+        } free_cint{c, cint_out};
+        // spgemm3d.hpp:65-79: split C_int's columns into c pieces and exchange
+        const int c_ = layers;
+        std::vector<int64_t> poff(c_ + 1);
+        const int64_t qc = ci.ncols / c_;
+        for (int k = 0; k < c_; ++k) poff[k] = int64_t(k) * qc;  // layout.hpp:60-66
+        poff[c_] = ci.ncols;
+        std::vector<int64_t> hcp(ci.ncols + 1);
+        SLAPCU_CUDA(cudaMemcpyAsync(hcp.data(), ci.cp, sizeof(int64_t) * (ci.ncols + 1),
+                                    cudaMemcpyDeviceToHost, c.stream));
+        SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+        // counts: my nnz per piece, all-gathered over the fiber
+        std::vector<int64_t> mine(c_);
+        for (int k = 0; k < c_; ++k) mine[k] = hcp[poff[k + 1]] - hcp[poff[k]];
+        DevBuf dcnt(sizeof(int64_t) * c_ * (c_ + 1), c.stream);
+        SLAPCU_CUDA(cudaMemcpyAsync(dcnt.as<int64_t>() + c_ * c_, mine.data(), sizeof(int64_t) * c_,
+                                    cudaMemcpyHostToDevice, c.stream));
+        SLAPCU_NCCL(ncclAllGather(dcnt.as<int64_t>() + c_ * c_, dcnt.as<int64_t>(), c_, ncclInt64, fiber, c.stream));
+        std::vector<int64_t> allc(c_ * c_);
+        SLAPCU_CUDA(cudaMemcpyAsync(allc.data(), dcnt.get(), sizeof(int64_t) * c_ * c_, cudaMemcpyDeviceToHost, c.stream));
+        SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+        // rebased colptr of each outgoing piece
+        const int64_t my_cols = poff[l + 1] - poff[l];
+        std::vector<Block> pieces(c_);
+        std::vector<DevBuf> send_cp(c_);
+        for (int k = 0; k < c_; ++k) {
+            const int64_t nc = poff[k + 1] - poff[k];
+            std::vector<int64_t> pc(nc + 1);
+            for (int64_t x = 0; x <= nc; ++x) pc[x] = hcp[poff[k] + x] - hcp[poff[k]];
+            send_cp[k].reset(sizeof(int64_t) * (nc + 1), c.stream);
+            SLAPCU_CUDA(cudaMemcpyAsync(send_cp[k].get(), pc.data(), sizeof(int64_t) * (nc + 1),
+                                        cudaMemcpyHostToDevice, c.stream));
+            SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+        }
+        for (int src = 0; src < c_; ++src) {
+            const int64_t nz = allc[src * c_ + l];  // what src sends me
+            pieces[src].nrows = ci.nrows;
+            pieces[src].ncols = my_cols;
+            pieces[src].nnz = nz;
+            if (src == l) continue;
+            pieces[src].cp.reset(sizeof(int64_t) * (my_cols + 1), c.stream);
+            pieces[src].rw.reset(sizeof(int32_t) * std::max<int64_t>(nz, 1), c.stream);
+            pieces[src].v.reset(size_t(vs) * std::max<int64_t>(nz, 1), c.stream);
+        }
+        SLAPCU_NCCL(ncclGroupStart());
+        int64_t sent = 0;
+        for (int k = 0; k < c_; ++k) {
+            if (k == l) continue;
+            const int64_t nc = poff[k + 1] - poff[k];
+            const int64_t nz = mine[k];
+            const int64_t e0 = hcp[poff[k]];
+            SLAPCU_NCCL(ncclSend(send_cp[k].get(), size_t(nc + 1), ncclInt64, k, fiber, c.stream));
+            if (nz) {
+                SLAPCU_NCCL(ncclSend(const_cast<int32_t*>(ci.rw) + e0, size_t(nz), ncclInt32, k, fiber, c.stream));
+                SLAPCU_NCCL(ncclSend(static_cast<char*>(const_cast<void*>(ci.v)) + size_t(vs) * e0, size_t(nz) * vs, ncclUint8, k,
+                                     fiber, c.stream));
+            }
+            sent += sizeof(int64_t) * (nc + 1) + (sizeof(int32_t) + vs) * nz;
+            const int64_t rz = allc[k * c_ + l];
+            SLAPCU_NCCL(ncclRecv(pieces[k].cp.get(), size_t(my_cols + 1), ncclInt64, k, fiber, c.stream));
+            if (rz) {
+                SLAPCU_NCCL(ncclRecv(pieces[k].rw.get(), size_t(rz), ncclInt32, k, fiber, c.stream));
+                SLAPCU_NCCL(ncclRecv(pieces[k].v.get(), size_t(rz) * vs, ncclUint8, k, fiber, c.stream));
+            }
+        }
+        SLAPCU_NCCL(ncclGroupEnd());
+        cm->calls[kAlltoallv] += 1;  // one fiber alltoallv (spgemm3d.hpp:78-79)
+        cm->bytes[kAlltoallv] += sent;
+        // own piece: a view into C_int
+        std::vector<DevCsc> pv(c_);
+        for (int k = 0; k < c_; ++k) {
+            if (k == l)
+                pv[k] = DevCsc{ci.nrows, my_cols, mine[l], send_cp[l].as<int64_t>(),
+                               const_cast<int32_t*>(ci.rw) + hcp[poff[l]],
+                               static_cast<const char*>(ci.v) + size_t(vs) * hcp[poff[l]]};
+            else
+                pv[k] = pieces[k].view();
+        }
+        merge_blocks(c, pv, sr, C_local);
+        SLAPCU_CUDA(cudaEventRecord(mt.b, c.stream));
+        SLAPCU_CUDA(cudaEventRecord(total.b, c.stream));
+        SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+        if (stats) {
+            stats->ms_merge = mt.ms();
+            stats->ms_total = total.ms();
+            stats->nnz_out = C_local->nnz;
+        }
+        return SLAPCU_OK;
+    } catch (const Fail& e) {
+        c.last_error = e.msg;
+        return e.st;
+    }
+}
+
+}  // extern "C"

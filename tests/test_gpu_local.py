@@ -1,0 +1,197 @@
+"""GPU parity of the local SpGEMM (spgemm.hpp:275-330) against the CPU oracle.
+
+Every call goes through libslapcu.so's C-ABI.  Cases follow the reference's
+own tests: the worked examples (test_localkernels.cpp:66-142), randomized
+oracle equivalence across semirings and algorithms (acceptance.cpp:58-97,
+test_localkernels.cpp:146-166), symbolic = nnz and flops = multiplies
+(test_localkernels.cpp:180-202), plus R-MAT products that exercise every
+GPU work class (smem hash bins, dense row-tile path with several tiles,
+global-memory value fallback).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from tests.helpers import KIND, assert_parity, to_device, with_values
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2106_14402_b200 as P  # noqa: E402
+from paper_2106_14402_b200 import _lib as L  # noqa: E402
+
+SRS = [P.PlusTimesF64, P.PlusTimesF32, P.PlusTimesI64, P.MinPlusI32, P.MinPlusF64, P.OrAnd]
+ALGS = [P.SpGemmAlg.heap, P.SpGemmAlg.hash, P.SpGemmAlg.hybrid]
+
+
+def example_a():
+    # test_localkernels.cpp:20-29: A = [[1,0],[2,3]]
+    return oracle.from_triples(2, 2, [0, 1, 1], [0, 0, 1], np.array([1, 2, 3], np.int64))
+
+
+def example_b():
+    # B = [[0,4],[5,0]]
+    return oracle.from_triples(2, 2, [0, 1], [1, 0], np.array([4, 5], np.int64))
+
+
+@pytest.mark.parametrize("alg", ALGS)
+def test_worked_example_plus_times(alg):
+    # test_localkernels.cpp:126-131: rows {1,0,1} cols {0,1,1} vals {15,4,8}
+    c = P.local_spgemm(to_device(example_a()), to_device(example_b()), P.PlusTimesI64, alg).to_host()
+    rows, cols, vals = c.to_triples()
+    assert rows.tolist() == [1, 0, 1]
+    assert cols.tolist() == [0, 1, 1]
+    assert vals.tolist() == [15, 4, 8]
+
+
+@pytest.mark.parametrize("alg", ALGS)
+def test_identity_times_a(alg):
+    eye = oracle.from_triples(2, 2, [0, 1], [0, 1], np.array([1, 1], np.int64))
+    a = example_a()
+    c = P.local_spgemm(to_device(eye), to_device(a), P.PlusTimesI64, alg)
+    assert_parity(c, a, oracle.PLUS_TIMES_I64, "I*A")
+
+
+@pytest.mark.parametrize("alg", ALGS)
+def test_min_plus_two_cycle(alg):
+    # test_localkernels.cpp:132-142
+    m = oracle.from_triples(2, 2, [0, 1], [1, 0], np.array([1.0, 2.0]))
+    c = P.local_spgemm(to_device(m), to_device(m), P.MinPlusF64, alg).to_host()
+    rows, cols, vals = c.to_triples()
+    assert rows.tolist() == [0, 1] and cols.tolist() == [0, 1] and vals.tolist() == [3.0, 3.0]
+
+
+def test_dim_error():
+    a = to_device(oracle.from_triples(3, 2, [0], [0], np.array([1.0])))
+    with pytest.raises(P.errors.DimError):
+        P.local_spgemm(a, a, P.PlusTimesF64)
+
+
+def test_empty_operands():
+    e = oracle.from_triples(5, 4, [], [], np.zeros(0))
+    f = oracle.from_triples(4, 3, [], [], np.zeros(0))
+    c = P.local_spgemm(to_device(e), to_device(f), P.PlusTimesF64).to_host()
+    assert c.nnz == 0 and c.colptr.tolist() == [0, 0, 0, 0]
+
+
+def _random_pairs(seed, trials, val_kind, dtype):
+    rng = np.random.default_rng(seed)
+    for _ in range(trials):
+        m, n, k = (int(x) for x in rng.integers(2, 65, 3))
+        density = 0.01 + 0.29 * float(rng.random())
+        s = int(rng.integers(1, 1 << 30))
+        a = oracle.random_triples(s, m, n, density, val_kind, dtype)
+        b = oracle.random_triples(s + 7, n, k, density, val_kind, dtype)
+        yield a, b
+
+
+@pytest.mark.parametrize("sr", SRS, ids=lambda s: f"{s.name}_{s.dtype}")
+def test_random_vs_oracle(port, sr):
+    """acceptance.cpp:58-97 criterion 1 (200 pairs per semiring there; 40 here
+    x 3 algorithms)."""
+    kind = {"f64": "u10", "f32": "u10", "i64": "small_int", "i32": "small_int", "u8": "one"}[sr.dtype]
+    for a, b in _random_pairs(101 + sr.id, 40, kind, sr.np_dtype):
+        want = port.spgemm(sr.id, a, b)
+        for alg in ALGS:
+            got = P.local_spgemm(to_device(a), to_device(b), sr, alg)
+            assert_parity(got, want, sr.id, f"{sr.name}/{sr.dtype}/{alg.name}")
+
+
+def test_symbolic_and_flops(port):
+    """test_localkernels.cpp:180-202: symbolic total = nnz(C), flops = multiplies."""
+    a = port.gen_rmat(10)
+    b = port.gen_rmat(9, 8, 3)
+    b = oracle.Csc(a.ncols, b.ncols, b.colptr, b.rowids)  # 1024 x 512
+    b.colptr = np.minimum(b.colptr, b.colptr[-1])
+    da, db = to_device(a), to_device(b)
+    tot, per = P.estimate_flops(da, db)
+    wtot, wper = port.estimate_flops(a, b)
+    assert tot == wtot and np.array_equal(per.cpu().numpy(), wper)
+    counts = P.symbolic_nnz(da, db).cpu().numpy()
+    _, wcounts = port.symbolic_nnz(a, b)
+    assert np.array_equal(counts, wcounts)
+
+
+@pytest.mark.parametrize("scale", [10, 12])
+@pytest.mark.parametrize("sr", SRS, ids=lambda s: f"{s.name}_{s.dtype}")
+def test_rmat_square_vs_oracle(port, sr, scale):
+    a = with_values(port, port.gen_rmat(scale), sr.id)
+    want = port.spgemm(sr.id, a, a)
+    da = to_device(a)
+    for alg in ALGS:
+        got = P.local_spgemm(da, da, sr, alg)
+        assert_parity(got, want, sr.id, f"rmat{scale}/{alg.name}")
+
+
+@pytest.mark.parametrize("sr", SRS, ids=lambda s: f"{s.name}_{s.dtype}")
+def test_multi_tile_paths(port, sr):
+    """Small row tiles force several tiles per column on the dense path (tile
+    cursors), and a tiny light threshold forces the global-memory value
+    fallback and the bitmap symbolic path."""
+    a = with_values(port, port.gen_rmat(12), sr.id)
+    want = port.spgemm(sr.id, a, a)
+    ctx = P.Context()
+    ctx.set_option(L.OPT_TILE_ROWS_LOG2, 10)
+    ctx.set_option(L.OPT_SYM_TILE_ROWS_LOG2, 10)
+    ctx.set_option(L.OPT_LIGHT_NNZ_MAX, 16)
+    ctx.set_option(L.OPT_LIGHT_FLOPS_MAX, 32)
+    da = to_device(a)
+    for alg in ALGS:
+        got = P.local_spgemm(da, da, sr, alg, ctx=ctx)
+        assert_parity(got, want, sr.id, f"tiles/{alg.name}")
+
+
+def test_or_and_with_zero_values(port):
+    """OrAnd with explicit 0 values must not take the all-ones fast path."""
+    a = port.gen_rmat(10)
+    v = (np.arange(a.nnz) % 3 != 0).astype(np.uint8)
+    a = a.with_vals(v)
+    want = port.spgemm(oracle.OR_AND_U8, a, a)
+    for alg in ALGS:
+        got = P.local_spgemm(to_device(a), to_device(a), P.OrAnd, alg)
+        assert_parity(got, want, oracle.OR_AND_U8, alg.name)
+
+
+def test_host_call_matches_device(port):
+    """slapcu_spgemm_host (host buffers, copies inside the library)."""
+    a = with_values(port, port.gen_rmat(11), oracle.MIN_PLUS_I32)
+    want = port.spgemm(oracle.MIN_PLUS_I32, a, a)
+    host = P.CscMatrix(a.nrows, a.ncols, a.colptr, a.rowids, a.vals)
+    got = P.local_spgemm(host, host, P.MinPlusI32)
+    assert isinstance(got, P.CscMatrix)
+    assert_parity(got, want, oracle.MIN_PLUS_I32, "host")
+
+
+def test_rectangular_and_empty_columns(port):
+    a = with_values(port, port.gen_rmat(11), oracle.PLUS_TIMES_F64)
+    # B = columns [100, 900) of A, with every 3rd column emptied
+    b = port.gen_rmat(11, 16, 5)
+    cp = b.colptr.copy()
+    keep = np.ones(b.ncols, bool)
+    keep[::3] = False
+    rows, cols = [], []
+    for j in range(100, 900):
+        if keep[j]:
+            s, e = cp[j], cp[j + 1]
+            rows += b.rowids[s:e].tolist()
+            cols += [j - 100] * int(e - s)
+    bb = oracle.from_triples(b.nrows, 800, rows, cols, np.ones(len(rows)))
+    bb = with_values(port, bb, oracle.PLUS_TIMES_F64)
+    want = port.spgemm(oracle.PLUS_TIMES_F64, a, bb)
+    for alg in ALGS:
+        got = P.local_spgemm(to_device(a), to_device(bb), P.PlusTimesF64, alg)
+        assert_parity(got, want, oracle.PLUS_TIMES_F64, alg.name)
+
+
+def test_thread_count_invariance(port):
+    """test_localkernels.cpp:168-178: the result does not depend on `threads`
+    (here: repeated runs are identical for an exact semiring)."""
+    a = with_values(port, port.gen_rmat(11), oracle.PLUS_TIMES_I64)
+    da = to_device(a)
+    base = P.local_spgemm(da, da, P.PlusTimesI64, threads=1).to_host()
+    for t in (2, 4, 8):
+        c = P.local_spgemm(da, da, P.PlusTimesI64, threads=t).to_host()
+        assert np.array_equal(c.rowids, base.rowids) and np.array_equal(c.vals, base.vals)
