@@ -18,11 +18,15 @@ struct slapcu_ctx_s;
 namespace slapcu {
 
 // Device CSC view (colptr int64, rowids int32, typed values).
+// colptr values may be offset (a column window of a larger matrix): entries
+// of column j live at rw[cp[j] .. cp[j+1]).  `base` = cp[0] and `span` =
+// cp[ncols] - cp[0] are filled on the host by resolve() before launches.
 struct DevCsc {
     int64_t nrows = 0, ncols = 0, nnz = 0;
     const int64_t* cp = nullptr;
     const int32_t* rw = nullptr;
     const void* v = nullptr;
+    int64_t base = 0, span = 0;
 };
 
 inline DevCsc view(const slapcu_csc& m) { return DevCsc{m.nrows, m.ncols, m.nnz, m.colptr, m.rowids, m.vals}; }
@@ -79,7 +83,7 @@ private:
 struct Plan {
     const void* a_key = nullptr;  // identity of the operands the plan is for
     const void* b_key = nullptr;
-    int64_t a_ncols = -1, b_ncols = -1, b_nnz = -1;
+    int64_t a_ncols = -1, b_ncols = -1, b_nnz = -1, b_base = -1;
     DevBuf flops;   // int64[B.ncols]
     DevBuf counts;  // int64[B.ncols + 1]
     DevBuf cursor;  // int32[B.nnz] per-B-entry row-tile cursors
@@ -141,6 +145,9 @@ struct Ctx {
 };
 
 Ctx& ctx_of(slapcu_ctx c);
+
+// Reads cp[0] and cp[ncols] (synchronizes the context stream).
+void resolve(Ctx& c, DevCsc& m);
 
 // spgemm.cu
 void spgemm_flops(Ctx& c, const DevCsc& A, const DevCsc& B, int64_t* flops_dev, int64_t* total);

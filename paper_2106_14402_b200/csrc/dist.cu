@@ -74,15 +74,20 @@ ncclComm_t split(slapcu_comm_s* cm, const std::string& name, int color, int key)
     return out;
 }
 
-// Block metadata of every rank: [A.nrows, A.ncols, A.nnz, B.nrows, B.ncols, B.nnz].
+// Block metadata of every rank (kMeta int64 each): A then B as
+// [nrows, ncols, colptr base, entry count] -- operands may be column windows
+// whose colptr does not start at 0 (batched.hpp slices).
+constexpr int kMeta = 8;
+enum { MA_R = 0, MA_C, MA_BASE, MA_NZ, MB_R, MB_C, MB_BASE, MB_NZ };
+
 std::vector<int64_t> allgather_meta(slapcu_comm_s* cm, Ctx& c, const DevCsc& A, const DevCsc& B) {
     const int p = cm->nranks;
-    int64_t mine[6] = {A.nrows, A.ncols, A.nnz, B.nrows, B.ncols, B.nnz};
-    DevBuf d(sizeof(int64_t) * 6 * (p + 1), c.stream);
-    SLAPCU_CUDA(cudaMemcpyAsync(d.as<int64_t>() + 6 * p, mine, sizeof(mine), cudaMemcpyHostToDevice, c.stream));
-    SLAPCU_NCCL(ncclAllGather(d.as<int64_t>() + 6 * p, d.as<int64_t>(), 6, ncclInt64, cm->world, c.stream));
-    std::vector<int64_t> h(6 * p);
-    SLAPCU_CUDA(cudaMemcpyAsync(h.data(), d.get(), sizeof(int64_t) * 6 * p, cudaMemcpyDeviceToHost, c.stream));
+    int64_t mine[kMeta] = {A.nrows, A.ncols, A.base, A.span, B.nrows, B.ncols, B.base, B.span};
+    DevBuf d(sizeof(int64_t) * kMeta * (p + 1), c.stream);
+    SLAPCU_CUDA(cudaMemcpyAsync(d.as<int64_t>() + kMeta * p, mine, sizeof(mine), cudaMemcpyHostToDevice, c.stream));
+    SLAPCU_NCCL(ncclAllGather(d.as<int64_t>() + kMeta * p, d.as<int64_t>(), kMeta, ncclInt64, cm->world, c.stream));
+    std::vector<int64_t> h(kMeta * p);
+    SLAPCU_CUDA(cudaMemcpyAsync(h.data(), d.get(), sizeof(int64_t) * kMeta * p, cudaMemcpyDeviceToHost, c.stream));
     SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
     cm->calls[kAllgatherv] += 1;
     cm->bytes[kAllgatherv] += sizeof(mine);
@@ -107,13 +112,17 @@ struct Slot {
 };
 
 // ncclBroadcast of one CSC block (three arrays) from group rank `root`.  The
-// root broadcasts in place from its own block; the others receive into slot.
+// root broadcasts in place from its own block (only its entry range
+// [base, base+nnz)); the others receive into slot.  colptr travels unchanged,
+// so a receiver addresses the entries through pointers shifted by -base
+// (never dereferenced outside [base, base+nnz)).
 DevCsc bcast_block(slapcu_comm_s* cm, ncclComm_t comm, int my_group_rank, int root, const DevCsc& mine,
-                   int64_t nrows, int64_t ncols, int64_t nnz, int vs, Slot& slot, cudaStream_t s) {
+                   int64_t nrows, int64_t ncols, int64_t base, int64_t nnz, int vs, Slot& slot, cudaStream_t s) {
     const bool am_root = my_group_rank == root;
     int64_t* cp = am_root ? const_cast<int64_t*>(mine.cp) : slot.cp.as<int64_t>();
-    int32_t* rw = am_root ? const_cast<int32_t*>(mine.rw) : slot.rw.as<int32_t>();
-    void* v = am_root ? const_cast<void*>(mine.v) : slot.v.get();
+    int32_t* rw = am_root ? const_cast<int32_t*>(mine.rw) + base : slot.rw.as<int32_t>();
+    char* v = am_root ? static_cast<char*>(const_cast<void*>(mine.v)) + size_t(vs) * base
+                      : static_cast<char*>(slot.v.get());
     SLAPCU_NCCL(ncclBroadcast(cp, cp, size_t(ncols + 1), ncclInt64, root, comm, s));
     if (nnz) {
         SLAPCU_NCCL(ncclBroadcast(rw, rw, size_t(nnz), ncclInt32, root, comm, s));
@@ -125,7 +134,7 @@ DevCsc bcast_block(slapcu_comm_s* cm, ncclComm_t comm, int my_group_rank, int ro
     } else {
         cm->calls[kBcast] += 1;
     }
-    return DevCsc{nrows, ncols, nnz, cp, rw, v};
+    return DevCsc{nrows, ncols, nnz, cp, rw - base, v - size_t(vs) * base, base, nnz};
 }
 
 // Local multiply into an owned block (symbolic -> allocate -> numeric).
@@ -191,12 +200,12 @@ void summa_stages(slapcu_comm_s* cm, Ctx& c, ncclComm_t row, ncclComm_t col, int
     // size the double buffer for the largest block this rank will receive
     int64_t a_nc = 0, a_nz = 0, b_nc = 0, b_nz = 0;
     for (int s = 0; s < q; ++s) {
-        const int64_t* ma = &meta[6 * meta_of(myi, s)];
-        const int64_t* mb = &meta[6 * meta_of(s, myj)];
-        a_nc = std::max(a_nc, ma[1]);
-        a_nz = std::max(a_nz, ma[2]);
-        b_nc = std::max(b_nc, mb[4]);
-        b_nz = std::max(b_nz, mb[5]);
+        const int64_t* ma = &meta[kMeta * meta_of(myi, s)];
+        const int64_t* mb = &meta[kMeta * meta_of(s, myj)];
+        a_nc = std::max(a_nc, ma[MA_C]);
+        a_nz = std::max(a_nz, ma[MA_NZ]);
+        b_nc = std::max(b_nc, mb[MB_C]);
+        b_nz = std::max(b_nz, mb[MB_NZ]);
     }
     Slot sa[2], sb[2];
     const int nslots = q > 1 ? 2 : 1;
@@ -216,11 +225,13 @@ void summa_stages(slapcu_comm_s* cm, Ctx& c, ncclComm_t row, ncclComm_t col, int
     auto issue = [&](int s) {
         const int slot = s % 2;
         if (s >= 2) SLAPCU_CUDA(cudaStreamWaitEvent(cm->comm_stream, slot_free[slot], 0));
-        const int64_t* ma = &meta[6 * meta_of(myi, s)];
-        const int64_t* mb = &meta[6 * meta_of(s, myj)];
+        const int64_t* ma = &meta[kMeta * meta_of(myi, s)];
+        const int64_t* mb = &meta[kMeta * meta_of(s, myj)];
         SLAPCU_NCCL(ncclGroupStart());
-        sa_view[s] = bcast_block(cm, row, myj, s, A, ma[0], ma[1], ma[2], vs, sa[slot], cm->comm_stream);
-        sb_view[s] = bcast_block(cm, col, myi, s, B, mb[3], mb[4], mb[5], vs, sb[slot], cm->comm_stream);
+        sa_view[s] = bcast_block(cm, row, myj, s, A, ma[MA_R], ma[MA_C], ma[MA_BASE], ma[MA_NZ], vs, sa[slot],
+                                 cm->comm_stream);
+        sb_view[s] = bcast_block(cm, col, myi, s, B, mb[MB_R], mb[MB_C], mb[MB_BASE], mb[MB_NZ], vs, sb[slot],
+                                 cm->comm_stream);
         SLAPCU_NCCL(ncclGroupEnd());
         SLAPCU_CUDA(cudaEventRecord(bc_done[s], cm->comm_stream));
     };
@@ -329,7 +340,9 @@ slapcu_status slapcu_summa2d(slapcu_comm cm, const slapcu_csc* A_local, const sl
         if (stats) *stats = slapcu_dist_stats{};
         Timer total;
         SLAPCU_CUDA(cudaEventRecord(total.a, c.stream));
-        const DevCsc A = view(*A_local), B = view(*B_local);
+        DevCsc A = view(*A_local), B = view(*B_local);
+        resolve(c, A);
+        resolve(c, B);
         const int i = cm->rank / (int)q, j = cm->rank % (int)q;
         std::vector<int64_t> meta;
         ncclComm_t row = nullptr, col = nullptr;
@@ -339,12 +352,12 @@ slapcu_status slapcu_summa2d(slapcu_comm cm, const slapcu_csc* A_local, const sl
             for (int ii = 0; ii < q; ++ii)
                 for (int jj = 0; jj < q; ++jj)
                     for (int s = 0; s < q; ++s)
-                        if (meta[6 * (ii * q + s) + 1] != meta[6 * (s * q + jj) + 3])
+                        if (meta[kMeta * (ii * q + s) + MA_C] != meta[kMeta * (s * q + jj) + MB_R])
                             throw Fail{SLAPCU_ERR_DIM, "SUMMA inner block offsets of A and B disagree"};
             row = split(cm, "row2d", i, j);
             col = split(cm, "col2d", j, i);
         } else {
-            meta = {A.nrows, A.ncols, A.nnz, B.nrows, B.ncols, B.nnz};
+            meta = {A.nrows, A.ncols, A.base, A.span, B.nrows, B.ncols, B.base, B.span};
             if (A.ncols != B.nrows) throw Fail{SLAPCU_ERR_DIM, "SUMMA inner dims disagree"};
         }
         std::vector<Block> partials;
@@ -394,14 +407,16 @@ slapcu_status slapcu_ca3d(slapcu_comm cm, int layers, const slapcu_csc* A_local,
         if (stats) stats->layer_warning = warn;
         Timer total;
         SLAPCU_CUDA(cudaEventRecord(total.a, c.stream));
-        const DevCsc A = view(*A_local), B = view(*B_local);
+        DevCsc A = view(*A_local), B = view(*B_local);
+        resolve(c, A);
+        resolve(c, B);
         const int qq = (int)(q * q);
         const int l = cm->rank / qq, i = (cm->rank % qq) / (int)q, j = cm->rank % (int)q;  // grid.cpp:57
         std::vector<int64_t> meta = allgather_meta(cm, c, A, B);
         for (int ii = 0; ii < q; ++ii)
             for (int jj = 0; jj < q; ++jj)
                 for (int s = 0; s < q; ++s)
-                    if (meta[6 * (l * qq + ii * (int)q + s) + 1] != meta[6 * (l * qq + s * (int)q + jj) + 3])
+                    if (meta[kMeta * (l * qq + ii * (int)q + s) + MA_C] != meta[kMeta * (l * qq + s * (int)q + jj) + MB_R])
                         throw Fail{SLAPCU_ERR_DIM, "3D SpGEMM stage blocks misaligned on the inner dimension"};
         ncclComm_t row = nullptr, col = nullptr;
         if (q > 1) {

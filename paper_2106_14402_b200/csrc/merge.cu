@@ -141,23 +141,31 @@ using MergeScratch = decltype(Ctx::merge);
 
 MergeScratch& scratch_for(Ctx& c) { return c.merge; }
 
-PartSet make_parts(Ctx& c, int q, const DevCsc* parts, MergeScratch& ms, bool alloc) {
+// Parts may be column windows (colptr not starting at 0): their entry range
+// [base, base+span) is read from the device and the per-entry rank scratch is
+// addressed with the same absolute indices.
+PartSet make_parts(Ctx& c, int q, const DevCsc* parts_in, MergeScratch& ms, bool alloc) {
     if (q < 1 || q > kMaxParts) throw Fail{SLAPCU_ERR_INVALID, "merge supports 1..16 parts"};
     for (int s = 1; s < q; ++s)
-        if (parts[s].nrows != parts[0].nrows || parts[s].ncols != parts[0].ncols)
+        if (parts_in[s].nrows != parts_in[0].nrows || parts_in[s].ncols != parts_in[0].ncols)
             throw Fail{SLAPCU_ERR_DIM, "merge parts have different shapes"};
+    DevCsc parts[kMaxParts];
+    for (int s = 0; s < q; ++s) {
+        parts[s] = parts_in[s];
+        resolve(c, parts[s]);
+    }
     PartSet P{};
     P.q = q;
     int64_t tot_nnz = 0;
-    for (int s = 0; s < q; ++s) tot_nnz += parts[s].nnz;
+    for (int s = 0; s < q; ++s) tot_nnz += parts[s].span;
     if (alloc) ms.ranks.reset(sizeof(int32_t) * std::max<int64_t>(tot_nnz, 1), c.stream);
     int64_t off = 0;
     for (int s = 0; s < q; ++s) {
         P.cp[s] = parts[s].cp;
         P.rw[s] = parts[s].rw;
         P.v[s] = parts[s].v;
-        P.firstrank[s] = ms.ranks.as<int32_t>() + off;
-        off += parts[s].nnz;
+        P.firstrank[s] = ms.ranks.as<int32_t>() + off - parts[s].base;
+        off += parts[s].span;
     }
     return P;
 }

@@ -25,7 +25,7 @@
 #include <algorithm>
 #include <vector>
 
-#include "ctx.hpp"
+#include "kern.cuh"
 
 namespace slapcu {
 
@@ -57,22 +57,6 @@ __global__ void __launch_bounds__(256) k_flops(const int64_t* __restrict__ Acp, 
 }
 
 // ===================================================================== binning
-
-struct BinSpec {
-    int nlight;            // light bins 0..nlight-1, heavy bin = nlight
-    int64_t thr[12];       // light bin b holds key <= thr[b]
-    int64_t light_max;     // key > light_max -> heavy
-    int all_heavy;         // alg == heap
-    int key_is_nnz;        // 0: key = flops[j]; 1: key = Ccp[j+1]-Ccp[j]
-};
-
-__device__ __forceinline__ int bin_of_key(const BinSpec& s, int64_t key) {
-    if (key <= 0) return -1;
-    if (s.all_heavy || key > s.light_max) return s.nlight;
-    for (int b = 0; b < s.nlight; ++b)
-        if (key <= s.thr[b]) return b;
-    return s.nlight;
-}
 
 __global__ void __launch_bounds__(256) k_bin_count(int64_t n, const int64_t* __restrict__ flops,
                                                    const int64_t* __restrict__ ccp, BinSpec spec,
@@ -115,76 +99,6 @@ __global__ void k_gather_keys(int n, const int* __restrict__ list, const int64_t
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) keys[i] = flops[list[i]];
 }
 
-// ============================================================ product walking
-
-// Sub-group width for walking A(:,k): the power of two closest above the
-// column's mean A-column length, so short A columns do not idle a warp.
-__device__ __forceinline__ int pick_sg(int64_t flops, int64_t nb, int G) {
-    const int64_t avg = nb > 0 ? (flops + nb - 1) / nb : 1;
-    int sg = 1;
-    while (sg < avg && sg < 32 && sg < G) sg <<= 1;
-    return sg;
-}
-
-template <int LOG2S>
-__device__ __forceinline__ unsigned hslot(int r) {
-    return ((unsigned)r * 0x9E3779B1u) >> (32 - LOG2S);
-}
-
-// Insert row id into an open-addressing table of 2^LOG2S int keys (-1 empty),
-// linear probing.  Returns the slot; *is_new tells whether it was inserted.
-template <int LOG2S>
-__device__ __forceinline__ int hash_insert(int* keys, int r, bool* is_new) {
-    constexpr unsigned MASK = (1u << LOG2S) - 1u;
-    unsigned h = hslot<LOG2S>(r);
-    for (;;) {
-        int k = keys[h];
-        if (k == r) {
-            *is_new = false;
-            return (int)h;
-        }
-        if (k == -1) {
-            int old = atomicCAS(&keys[h], -1, r);
-            if (old == -1) {
-                *is_new = true;
-                return (int)h;
-            }
-            if (old == r) {
-                *is_new = false;
-                return (int)h;
-            }
-        }
-        h = (h + 1) & MASK;
-    }
-}
-
-template <int G, int CPB>
-__device__ __forceinline__ void group_sync(int g) {
-    if constexpr (G == 32)
-        __syncwarp();
-    else if constexpr (CPB == 1)
-        __syncthreads();
-    else
-        named_sync(1 + g, G);
-}
-
-template <int G, int CPB>
-__device__ __forceinline__ long long group_sum(long long v, int g, int lane, long long* red) {
-    v = warp_reduce_sum64(v);
-    if constexpr (G == 32) {
-        return v;
-    } else {
-        constexpr int W = G / 32;
-        if ((lane & 31) == 0) red[g * W + (lane >> 5)] = v;
-        group_sync<G, CPB>(g);
-        long long s = 0;
-#pragma unroll
-        for (int w = 0; w < W; ++w) s += red[g * W + w];
-        group_sync<G, CPB>(g);
-        return s;
-    }
-}
-
 // ============================================================ phase 2: light
 
 // One group of G threads per column, CPB columns per block; a 2^LOG2S-slot
@@ -223,53 +137,6 @@ __global__ void __launch_bounds__(G* CPB) k_sym_light(DevCsc A, DevCsc B, const 
 }
 
 // ============================================================ phase 2: heavy
-
-// Walks the entries of A(:,k), k in B(:,j), whose rows fall in [.., t1) of
-// the current row tile, starting from the per-B-entry cursor (A columns are
-// row-sorted, so each tile continues where the previous one stopped).
-// f(p, i, r) is called per product.  If write_cursor, the lane that owns the
-// first out-of-tile position records it for the next tile.  Cursors are
-// double-buffered by tile parity (read cur_in, write cur_out) so no lane can
-// overwrite a start position another lane of its sub-group has yet to read.
-template <class F>
-__device__ __forceinline__ void walk_tile(const DevCsc& A, const DevCsc& B, int64_t bs, int64_t be, int sg, int tid,
-                                          int nt, int t, int ntiles, int t1, const int32_t* __restrict__ cur_in,
-                                          int32_t* __restrict__ cur_out, bool write_cursor, F&& f) {
-    const int sub = tid / sg, nsub = nt / sg, sl = tid % sg;
-    for (int64_t i = bs + sub; i < be; i += nsub) {
-        const int k = B.rw[i];
-        const int64_t as = A.cp[k], ae = A.cp[k + 1];
-        if (ntiles == 1) {
-            for (int64_t p = as + sl; p < ae; p += sg) f(p, i, A.rw[p]);
-            continue;
-        }
-        const int64_t start = (t == 0) ? as : as + cur_in[i];
-        int64_t p = start + sl;
-        for (; p < ae; p += sg) {
-            const int r = A.rw[p];
-            if (r >= t1) break;
-            f(p, i, r);
-        }
-        if (write_cursor) {
-            if (p > ae) p = ae;
-            const bool mine = (p == start) || (A.rw[p - 1] < t1);
-            if (mine) cur_out[i] = (int32_t)(p - as);
-        }
-    }
-}
-
-__device__ __forceinline__ long long block_sum_ll(long long v, long long* red) {
-    v = warp_reduce_sum64(v);
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    __syncthreads();
-    if (l == 0) red[w] = v;
-    __syncthreads();
-    long long s = 0;
-    if (threadIdx.x == 0)
-        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
-    return s;  // valid on thread 0
-}
-
 // One CTA per heavy column; row tiles of 2^tile_log2 rows, each a shared-memory
 // bitmap; count = popcount (PatternSpa::count, spgemm.hpp:107).
 template <int NT>
@@ -290,8 +157,8 @@ __global__ void __launch_bounds__(NT) k_sym_heavy(DevCsc A, DevCsc B, const int*
         const int W = (int)((rows + 31) >> 5);
         for (int w = threadIdx.x; w < W; w += NT) bm[w] = 0u;
         __syncthreads();
-        walk_tile(A, B, bs, be, sg, threadIdx.x, NT, t, ntiles, (int)(t0 + rows), cursor + (t & 1) * B.nnz,
-                  cursor + ((t + 1) & 1) * B.nnz, true,
+        walk_tile(A, B, bs, be, sg, threadIdx.x, NT, t, ntiles, (int)(t0 + rows), cursor + (t & 1) * B.span,
+                  cursor + ((t + 1) & 1) * B.span, true,
                   [&](int64_t, int64_t, int r) {
                       const int rr = r - (int)t0;
                       atomicOr(&bm[rr >> 5], 1u << (rr & 31));
@@ -460,8 +327,8 @@ __global__ void __launch_bounds__(NT)
         for (int w = tid; w < W; w += NT) bm[w] = 0u;
         __syncthreads();
         // (1) pattern
-        int32_t* cin = cursor + (t & 1) * B.nnz;
-        int32_t* cout = cursor + ((t + 1) & 1) * B.nnz;
+        int32_t* cin = cursor + (t & 1) * B.span;
+        int32_t* cout = cursor + ((t + 1) & 1) * B.span;
         walk_tile(A, B, bs, be, sg, tid, NT, t, ntiles, t1, cin, cout, ONES, [&](int64_t, int64_t, int r) {
             const int rr = r - (int)t0;
             atomicOr(&bm[rr >> 5], 1u << (rr & 31));
@@ -554,32 +421,16 @@ __global__ void k_any_zero_u8(int64_t n, const uint8_t* __restrict__ v, int* __r
 
 // ============================================================ host helpers
 
-namespace {
-
 constexpr int kNumLightSym = 10;
 constexpr int kNumLightNum = 8;
 
-// Opt in to more than the default 48 KB of dynamic shared memory.  The
-// kernels also hold a few bytes of static shared memory, which counts
-// against the same 48 KB default, hence the margin.
-template <class K>
-void ensure_smem(K kernel, size_t smem) {
-    if (smem > 40 * 1024) SLAPCU_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-}
-
-int grid_for(Ctx& c, int64_t work, int block, int per_sm = 8) {
+int grid_for(Ctx& c, int64_t work, int block, int per_sm) {
     int64_t g = ceil_div(work, block);
     int64_t cap = int64_t(c.num_sms) * per_sm;
     if (g > cap) g = cap;
     if (g < 1) g = 1;
     return (int)g;
 }
-
-struct Bins {
-    std::vector<int> count;   // per bin
-    std::vector<int> offset;  // per bin
-    DevBuf list;              // int32[n_nonzero]
-};
 
 // Two-pass binning of the columns by key; heavy bin sorted by flops desc (LPT).
 void make_bins(Ctx& c, int64_t n, const int64_t* flops, const int64_t* ccp, const BinSpec& spec, int64_t* zero_counts,
@@ -665,7 +516,7 @@ void prepare_plan(Ctx& c, const DevCsc& A, const DevCsc& B) {
     Plan& p = c.plan;
     p.flops.reset(sizeof(int64_t) * std::max<int64_t>(B.ncols, 1), c.stream);
     p.counts.reset(sizeof(int64_t) * (B.ncols + 1), c.stream);
-    p.cursor.reset(sizeof(int32_t) * 2 * std::max<int64_t>(B.nnz, 1), c.stream);
+    p.cursor.reset(sizeof(int32_t) * 2 * std::max<int64_t>(B.span, 1), c.stream);
     KScope ks(c, KC_FLOPS);
     launch(c, k_flops, dim3(grid_for(c, B.ncols * 32, 256, 16)), dim3(256), 0, A.cp, B.cp, B.rw, B.ncols,
            p.flops.as<int64_t>(), (unsigned long long*)nullptr);
@@ -673,15 +524,18 @@ void prepare_plan(Ctx& c, const DevCsc& A, const DevCsc& B) {
     p.b_key = B.cp;
     p.a_ncols = A.ncols;
     p.b_ncols = B.ncols;
-    p.b_nnz = B.nnz;
+    p.b_nnz = B.span;
+    p.b_base = B.base;
     p.valid = true;
 }
 
 bool plan_matches(const Ctx& c, const DevCsc& A, const DevCsc& B) {
     const Plan& p = c.plan;
     return p.valid && p.a_key == A.cp && p.b_key == B.cp && p.a_ncols == A.ncols && p.b_ncols == B.ncols &&
-           p.b_nnz == B.nnz;
+           p.b_nnz == B.span && p.b_base == B.base;
 }
+
+namespace {
 
 // ---- light launch tables
 
@@ -774,8 +628,11 @@ void exclusive_scan_i64(Ctx& c, const int64_t* in, int64_t* out, int64_t n) {
     ++c.launches;
 }
 
-int64_t spgemm_symbolic(Ctx& c, const DevCsc& A, const DevCsc& B, int alg, int64_t* c_colptr) {
-    check_operands(A, B);
+int64_t spgemm_symbolic(Ctx& c, const DevCsc& A_, const DevCsc& B_, int alg, int64_t* c_colptr) {
+    check_operands(A_, B_);
+    DevCsc A = A_, B = B_;
+    resolve(c, A);
+    resolve(c, B);
     if (!c_colptr) throw Fail{SLAPCU_ERR_INVALID, "null colptr"};
     SLAPCU_CUDA(cudaEventRecord(c.ev[0], c.stream));
     prepare_plan(c, A, B);
@@ -824,9 +681,12 @@ int64_t spgemm_symbolic(Ctx& c, const DevCsc& A, const DevCsc& B, int alg, int64
     return total;
 }
 
-void spgemm_numeric(Ctx& c, const DevCsc& A, const DevCsc& B, int sr, int alg, const int64_t* ccp, int32_t* crw,
+void spgemm_numeric(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int alg, const int64_t* ccp, int32_t* crw,
                     void* cv) {
-    check_operands(A, B);
+    check_operands(A_, B_);
+    DevCsc A = A_, B = B_;
+    resolve(c, A);
+    resolve(c, B);
     if (!ccp) throw Fail{SLAPCU_ERR_INVALID, "null colptr"};
     if (value_size(sr) == 0) throw Fail{SLAPCU_ERR_INVALID, "unknown semiring"};
     if ((A.nnz && !A.v) || (B.nnz && !B.v)) throw Fail{SLAPCU_ERR_INVALID, "operand values are null"};
@@ -839,8 +699,10 @@ void spgemm_numeric(Ctx& c, const DevCsc& A, const DevCsc& B, int sr, int alg, c
     // OrAnd fast path: if no stored value is 0 every product is 1
     bool ones = false;
     if (sr == SLAPCU_OR_AND_U8) {
-        launch(c, k_any_zero_u8, dim3(grid_for(c, A.nnz, 256)), dim3(256), 0, A.nnz, (const uint8_t*)A.v, err + 1);
-        launch(c, k_any_zero_u8, dim3(grid_for(c, B.nnz, 256)), dim3(256), 0, B.nnz, (const uint8_t*)B.v, err + 1);
+        launch(c, k_any_zero_u8, dim3(grid_for(c, A.span, 256)), dim3(256), 0, A.span, (const uint8_t*)A.v + A.base,
+               err + 1);
+        launch(c, k_any_zero_u8, dim3(grid_for(c, B.span, 256)), dim3(256), 0, B.span, (const uint8_t*)B.v + B.base,
+               err + 1);
         int hz = 0;
         SLAPCU_CUDA(cudaMemcpyAsync(&hz, err + 1, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
         SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
@@ -904,6 +766,22 @@ __global__ void k_dcsc_dense(int64_t ncols, int64_t nzc, const int32_t* __restri
         }
         colptr[j] = cp[lo];
     }
+}
+
+void resolve(Ctx& c, DevCsc& m) {
+    int64_t ends[2] = {0, 0};
+    if (m.ncols > 0) {
+        SLAPCU_CUDA(cudaMemcpyAsync(&ends[0], m.cp, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
+        SLAPCU_CUDA(cudaMemcpyAsync(&ends[1], m.cp + m.ncols, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
+        SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+    } else if (m.cp) {
+        SLAPCU_CUDA(cudaMemcpyAsync(&ends[0], m.cp, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
+        SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+        ends[1] = ends[0];
+    }
+    m.base = ends[0];
+    m.span = ends[1] - ends[0];
+    if (m.span < 0) throw Fail{SLAPCU_ERR_INVALID, "colptr is not monotone"};
 }
 
 void dcsc_colptr(Ctx& c, int64_t ncols, int64_t nzc, const int32_t* jc, const int32_t* cp, int64_t* colptr) {

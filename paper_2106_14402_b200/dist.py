@@ -1,0 +1,176 @@
+"""Distributed SpGEMM drivers: host-side mirror of the reference's
+summa2d_spgemm (summa.hpp:106-163), ca3d_spgemm (spgemm3d.hpp:21-106) and
+batched_spgemm (batched.hpp:153-170) over libslapcu's NCCL drivers.
+
+One process per GPU (torchrun).  torch.distributed is used only to share the
+NCCL unique id and for host-side barriers / gathers; every data-path
+collective (stage broadcasts, fiber exchange) runs inside libslapcu on NCCL
+communicators of its own.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from . import errors as E
+from . import grid as G
+from .spgemm import Context, CscMatrix, DeviceCsc, Semiring, SpGemmAlg, _from_out, _sr, default_context
+
+
+class NcclComm:
+    """slapcu_comm spanning the ranks of the default torch.distributed group
+    (the reference's world Comm, comm.hpp:178-348, on NCCL)."""
+
+    def __init__(self, ctx: Context | None = None):
+        import torch.distributed as dist
+
+        self.ctx = ctx or default_context()
+        self.lib = self.ctx.lib
+        self.rank = dist.get_rank()
+        self.size = dist.get_world_size()
+        uid = (C.c_char * 128)()
+        if self.rank == 0:
+            st = self.lib.slapcu_comm_unique_id(uid)
+            if st != L.OK:
+                raise E.DeadlockError("ncclGetUniqueId failed")
+        obj = [bytes(uid)]
+        dist.broadcast_object_list(obj, src=0)
+        buf = (C.c_char * 128).from_buffer_copy(obj[0])
+        h = C.c_void_p()
+        self.ctx.check(self.lib.slapcu_comm_create(C.byref(h), self.ctx.h, self.rank, self.size, buf), "comm_create")
+        self.h = h
+
+    def counters(self, kind: int):
+        """comm.hpp:31-53 CommCounters: (calls, bytes) for kind 0 broadcast,
+        1 alltoallv, 2 reduce, 3 allgatherv."""
+        calls, nbytes = C.c_int64(), C.c_int64()
+        self.lib.slapcu_comm_counters(self.h, kind, C.byref(calls), C.byref(nbytes))
+        return int(calls.value), int(nbytes.value)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.slapcu_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@dataclass
+class DistKernelStats:
+    """summa.hpp:15-20 + device-event timings (ms)."""
+
+    stages: int
+    flops: int
+    nnz_out: int
+    layer_warning: bool
+    ms_total: float
+    ms_local: float
+    ms_merge: float
+    ms_exposed_bcast: float
+
+
+def _stats(s: L.DistStats) -> DistKernelStats:
+    return DistKernelStats(s.stages, s.flops, s.nnz_out, bool(s.layer_warning), s.ms_total, s.ms_local, s.ms_merge,
+                           s.ms_exposed_bcast)
+
+
+def summa2d_spgemm(a_local: DeviceCsc, b_local: DeviceCsc, sr: Semiring, comm: NcclComm,
+                   alg=SpGemmAlg.hybrid, threads: int = 1, raw: bool = False):
+    """Collective 2D Sparse SUMMA on a sqrt(p) x sqrt(p) grid (rank = i*q + j).
+    `a_local` is A's block (i, j), `b_local` is B's block (i, j) with block
+    extents from block_offsets (layout.hpp:60-66).  Returns (C block (i, j),
+    stats); raw=True returns the library-owned L.CscOut instead (free with
+    free_out)."""
+    sr = _sr(sr)
+    ctx = comm.ctx
+    ctx.sync_stream()
+    out = L.CscOut()
+    st = L.DistStats()
+    ctx.check(comm.lib.slapcu_summa2d(comm.h, C.byref(a_local.view()), C.byref(b_local.view()), sr.id, int(alg),
+                                      C.byref(out), C.byref(st)), "summa2d")
+    if raw:
+        return out, _stats(st)
+    return _from_out(ctx, out, sr), _stats(st)
+
+
+def ca3d_spgemm(a3_local: DeviceCsc, b3_local: DeviceCsc, sr: Semiring, comm: NcclComm, layers: int,
+                alg=SpGemmAlg.hybrid, threads: int = 1, raw: bool = False):
+    """Collective 3D SpGEMM on a c x q x q grid (regular variant, rank =
+    l*q*q + i*q + j): A split by columns, B by rows (regular_3d_range).  The
+    result is C3 block (l, i, j) (ca3d_output_range)."""
+    sr = _sr(sr)
+    ctx = comm.ctx
+    ctx.sync_stream()
+    out = L.CscOut()
+    st = L.DistStats()
+    ctx.check(comm.lib.slapcu_ca3d(comm.h, layers, C.byref(a3_local.view()), C.byref(b3_local.view()), sr.id,
+                                   int(alg), C.byref(out), C.byref(st)), "ca3d")
+    if raw:
+        return out, _stats(st)
+    return _from_out(ctx, out, sr), _stats(st)
+
+
+def free_out(ctx: Context, out: L.CscOut):
+    ctx.check(ctx.lib.slapcu_csc_free(ctx.h, C.byref(out)), "csc_free")
+
+
+# ------------------------------------------------------- device block views
+
+
+def column_window(m: DeviceCsc, c0: int, c1: int) -> DeviceCsc:
+    """Columns [c0, c1) of a device CSC without copying (colptr view; entry
+    arrays shared).  The library accepts offset colptrs everywhere."""
+    return DeviceCsc(m.nrows, c1 - c0, m.colptr[c0:c1 + 1], m.rowids, m.vals)
+
+
+def device_block(m: DeviceCsc, r0: int, rl: int, c0: int, cl: int) -> DeviceCsc:
+    """Block rows [r0, r0+rl) x cols [c0, c0+cl) with block-local indices, as a
+    new device CSC (setup-time helper; torch ops on the device)."""
+    cp = m.colptr[c0:c0 + cl + 1]
+    lo, hi = int(cp[0]), int(cp[-1])
+    rw = m.rowids[lo:hi]
+    counts = (cp[1:] - cp[:-1])
+    col = torch.repeat_interleave(torch.arange(cl, device=rw.device), counts)
+    keep = (rw >= r0) & (rw < r0 + rl)
+    col = col[keep]
+    new_rw = (rw[keep] - r0).to(torch.int32)
+    new_v = None if m.vals is None else m.vals[lo:hi][keep]
+    cnt = torch.bincount(col, minlength=cl)
+    colptr = torch.zeros(cl + 1, dtype=torch.int64, device=rw.device)
+    colptr[1:] = torch.cumsum(cnt, 0)
+    return DeviceCsc(rl, cl, colptr, new_rw.contiguous(), None if new_v is None else new_v.contiguous())
+
+
+def block_2d(m: DeviceCsc, q: int, rank: int) -> DeviceCsc:
+    r0, rl, c0, cl = G.block2d_range(m.nrows, m.ncols, q, q, rank // q, rank % q)
+    return device_block(m, r0, rl, c0, cl)
+
+
+def block_3d(m: DeviceCsc, c: int, q: int, rank: int, split: str) -> DeviceCsc:
+    g = G.Grid3D(c, q, rank)
+    l, i, j = g.coords
+    r0, rl, c0, cl = G.regular_3d_range(m.nrows, m.ncols, c, q, split, l, i, j)
+    return device_block(m, r0, rl, c0, cl)
+
+
+def gather_to_host(local: DeviceCsc, row_start: int, col_start: int, nrows: int, ncols: int) -> CscMatrix | None:
+    """gather_matrix (dist_matrix.hpp:121-145): rank 0 receives every block
+    and assembles the global CSC (test / validation helper)."""
+    import torch.distributed as dist
+
+    h = local.to_host()
+    mine = (row_start, col_start, h.colptr, h.rowids, h.vals)
+    parts = [None] * dist.get_world_size() if dist.get_rank() == 0 else None
+    dist.gather_object(mine, parts, dst=0)
+    if dist.get_rank() != 0:
+        return None
+    cp, rw, vv = G.assemble(nrows, ncols, parts)
+    return CscMatrix(nrows, ncols, cp, rw, vv.astype(h.vals.dtype) if h.vals is not None else vv)
