@@ -185,16 +185,23 @@ def run_ours(args):
     A = P.fill_values(P.gen_rmat(args.scale, args.edge_factor, 1, ctx=ctx), sr, kind, ctx=ctx)
     n = A.ncols
     total_flops, flops_per = P.estimate_flops(A, A, ctx=ctx)
+    # exact counts (validation + roofline byte accounting only; not used by the step)
     counts = P.symbolic_nnz(A, A, ctx=ctx).cpu().numpy()
     nnz_c = int(counts.sum())
+    # Column batches sized by the staging bound sum_j min(flops_j, n) -- known
+    # before any product is formed -- so every batch runs the single-pass
+    # begin/finish with no symbolic pre-pass (batched.hpp:122-170 semantics,
+    # with the flops bound in place of the symbolic count).
+    bound = np.minimum(flops_per.cpu().numpy(), A.nrows)
     free, _tot = torch.cuda.mem_get_info()
-    budget = int(args.budget_gb * 2**30) if args.budget_gb > 0 else int(min(0.40 * free, 48 * 2**30))
-    batches = plan_batches(counts, 4 + vs, budget)
-    max_nnz = max(int(counts[s:e].sum()) for s, e in batches)
+    stage_entry = 4 + (0 if sr is P.OrAnd else vs)
+    budget = int(args.budget_gb * 2**30) if args.budget_gb > 0 else int(min(0.30 * free, 40 * 2**30))
+    batches = plan_batches(bound, stage_entry, budget)
+    max_cap = max(int(bound[s:e].sum()) for s, e in batches)
     max_cols = max(e - s for s, e in batches)
     out_cp = torch.empty(max_cols + 1, dtype=torch.int64, device=dev)
-    out_rw = torch.empty(max(max_nnz, 1), dtype=torch.int32, device=dev)
-    out_v = torch.empty(max(max_nnz, 1), dtype=sr.torch_dtype, device=dev)
+    out_rw = torch.empty(max(max_cap, 1), dtype=torch.int32, device=dev)
+    out_v = torch.empty(max(max_cap, 1), dtype=sr.torch_dtype, device=dev)
     av = A.view()
     import ctypes as C
 
@@ -207,10 +214,10 @@ def run_ours(args):
     def step(collect=None):
         for bi, w in enumerate(wins):
             nz = C.c_int64()
-            ctx.check(lib.slapcu_spgemm_symbolic(ctx.h, C.byref(av), C.byref(w), P.SpGemmAlg.hybrid,
-                                                 out_cp.data_ptr(), C.byref(nz)), "symbolic")
-            ctx.check(lib.slapcu_spgemm_numeric(ctx.h, C.byref(av), C.byref(w), sr.id, P.SpGemmAlg.hybrid,
-                                                out_cp.data_ptr(), out_rw.data_ptr(), out_v.data_ptr()), "numeric")
+            ctx.check(lib.slapcu_spgemm_begin(ctx.h, C.byref(av), C.byref(w), sr.id, P.SpGemmAlg.hybrid, 0,
+                                              out_cp.data_ptr(), C.byref(nz)), "begin")
+            ctx.check(lib.slapcu_spgemm_finish(ctx.h, C.byref(av), C.byref(w), sr.id, out_rw.data_ptr(),
+                                               out_v.data_ptr()), "finish")
             if collect is not None:
                 collect(bi, int(nz.value))
 
@@ -247,24 +254,34 @@ def run_ours(args):
     peak, peak_kind = measured_peak_gbs()
     per_step = {k: (nl / args.steps, t / args.steps) for k, (nl, t) in kstats.items() if nl}
     dom = max(per_step, key=lambda k: per_step[k][1])
-    light_max = 4096
+    # heavy columns of the fused path: flops > max(256, min(n/128, 4096))
+    lmax = max(256, min(A.nrows // 128, 4096))
+    fl = flops_per.cpu().numpy()
+    heavy = fl > lmax
     colnnz_b = np.diff(A.colptr.cpu().numpy())
-    if dom == "num_heavy":
-        heavy = counts > light_max
-        dom_bytes = 0
-        for s, e in batches:
-            h = heavy[s:e]
-            dom_bytes += int(counts[s:e][h].sum()) * (4 + vs) + (int(h.sum()) + 1) * 8
-            dom_bytes += int(colnnz_b[s:e][h].sum()) * (4 + vs)
-            dom_bytes += A.nnz * (4 + vs) + (n + 1) * 8
-    else:
-        dom_bytes = bytes_alg(A.nnz, n, A.nnz, n, nnz_c, n, vs)
+    dom_bytes = 0
+    for s, e in batches:
+        h = heavy[s:e] if dom in ("sym_heavy", "num_heavy") else ~heavy[s:e]
+        nh = int(h.sum())
+        if nh == 0:
+            continue
+        c_ent = int(counts[s:e][h].sum())
+        b_ent = int(colnnz_b[s:e][h].sum())
+        if dom == "sym_heavy":  # k_fused_heavy: B cols + A (pattern) in, staged rows out
+            dom_bytes += c_ent * 4 + b_ent * 4 + (nh + 1) * 8 + A.nnz * 4 + (n + 1) * 8
+        elif dom == "num_heavy":  # k_values_heavy: C rows in, values out, B and A with values
+            dom_bytes += c_ent * (4 + vs) + b_ent * (4 + vs) + (nh + 1) * 8 + A.nnz * (4 + vs) + (n + 1) * 8
+        elif dom == "sym_light":  # k_fused_light: staged rows+values out
+            dom_bytes += c_ent * (4 + vs) + b_ent * (4 + vs) + (nh + 1) * 8
+        else:  # copies: read staged, write C
+            dom_bytes += 2 * c_ent * (4 + vs) + (nh + 1) * 8
     dom_ms = per_step[dom][1]
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9
     step_bytes = bytes_alg(A.nnz, n, A.nnz, n, nnz_c, n, vs)
     roofline = {
         "bound": "hbm",
-        "kernel": f"k_{dom}",
+        "kernel": {"sym_heavy": "k_fused_heavy", "sym_light": "k_fused_light", "num_heavy": "k_values_heavy",
+                   "num_light": "k_copy_light+k_copy_heavy"}.get(dom, dom),
         "achieved": round(achieved, 2),
         "peak": peak,
         "unit": "GB/s",
@@ -370,10 +387,10 @@ def run_e2e_single(args, A, sr, batches, counts, total_flops, ctx, stream):
         for s, e in batches:
             w = L.CscView(A.nrows, e - s, A.nnz, d_cp.data_ptr() + 8 * s, d_rw.data_ptr(), d_v.data_ptr())
             nz = C.c_int64()
-            ctx.check(lib.slapcu_spgemm_symbolic(ctx.h, C.byref(av), C.byref(w), P.SpGemmAlg.hybrid,
-                                                 o_cp.data_ptr(), C.byref(nz)), "symbolic")
-            ctx.check(lib.slapcu_spgemm_numeric(ctx.h, C.byref(av), C.byref(w), sr.id, P.SpGemmAlg.hybrid,
-                                                o_cp.data_ptr(), o_rw.data_ptr(), o_v.data_ptr()), "numeric")
+            ctx.check(lib.slapcu_spgemm_begin(ctx.h, C.byref(av), C.byref(w), sr.id, P.SpGemmAlg.hybrid, 0,
+                                              o_cp.data_ptr(), C.byref(nz)), "begin")
+            ctx.check(lib.slapcu_spgemm_finish(ctx.h, C.byref(av), C.byref(w), sr.id, o_rw.data_ptr(),
+                                               o_v.data_ptr()), "finish")
             nzv = int(nz.value)
             h_out_cp[: e - s + 1].copy_(o_cp[: e - s + 1], non_blocking=True)
             d2h += (e - s + 1) * 8

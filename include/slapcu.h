@@ -151,8 +151,22 @@ slapcu_status slapcu_spgemm_symbolic(slapcu_ctx ctx, const slapcu_csc* A, const 
 slapcu_status slapcu_spgemm_numeric(slapcu_ctx ctx, const slapcu_csc* A, const slapcu_csc* B, slapcu_semiring sr,
                                     slapcu_alg alg, const int64_t* c_colptr, int32_t* c_rowids, void* c_vals);
 
+/* Single-product-pass form of the same contract (the production path):
+ * begin() forms every output column once, sorted, into a staging area owned
+ * by the context and writes C's colptr + *c_nnz; the caller allocates rowids
+ * / vals; finish() lays the staged columns out (and, for value semirings,
+ * accumulates heavy columns' values at their popcount rank).  Staging needs
+ * sum_j min(flops_j, A.nrows) entries; if that exceeds staging_budget_bytes
+ * (> 0) begin() fails with SLAPCU_ERR_BUDGET and the caller batches columns
+ * (batched.hpp:153-170).  A and B must be the same objects in both calls. */
+slapcu_status slapcu_spgemm_begin(slapcu_ctx ctx, const slapcu_csc* A, const slapcu_csc* B, slapcu_semiring sr,
+                                  slapcu_alg alg, int64_t staging_budget_bytes, int64_t* c_colptr, int64_t* c_nnz);
+slapcu_status slapcu_spgemm_finish(slapcu_ctx ctx, const slapcu_csc* A, const slapcu_csc* B, slapcu_semiring sr,
+                                   int32_t* c_rowids, void* c_vals);
+
 /* spgemm.hpp:275-330 local_spgemm, all three phases, C allocated on the
- * device by the library. */
+ * device by the library (single-pass begin/finish; falls back to the
+ * symbolic/numeric pair when the staging area does not fit). */
 slapcu_status slapcu_spgemm(slapcu_ctx ctx, const slapcu_csc* A, const slapcu_csc* B, slapcu_semiring sr,
                             slapcu_alg alg, slapcu_csc_out* C);
 

@@ -102,6 +102,8 @@ SIGNATURES = [
     ("slapcu_estimate_flops", _I, [_P, _PV, _PV, _P, C.POINTER(_L)]),
     ("slapcu_spgemm_symbolic", _I, [_P, _PV, _PV, _I, _P, C.POINTER(_L)]),
     ("slapcu_spgemm_numeric", _I, [_P, _PV, _PV, _I, _I, _P, _P, _P]),
+    ("slapcu_spgemm_begin", _I, [_P, _PV, _PV, _I, _I, _L, _P, C.POINTER(_L)]),
+    ("slapcu_spgemm_finish", _I, [_P, _PV, _PV, _I, _P, _P]),
     ("slapcu_spgemm", _I, [_P, _PV, _PV, _I, _I, _PO]),
     ("slapcu_spgemm_host", _I, [_P, _PO, _PO, _I, _I, _PO]),
     ("slapcu_csc_free", _I, [_P, _PO]),

@@ -227,6 +227,30 @@ slapcu_status slapcu_spgemm_numeric(slapcu_ctx ctx, const slapcu_csc* A, const s
     });
 }
 
+slapcu_status slapcu_spgemm_begin(slapcu_ctx ctx, const slapcu_csc* A, const slapcu_csc* B, slapcu_semiring sr,
+                                  slapcu_alg alg, int64_t staging_budget_bytes, int64_t* c_colptr, int64_t* c_nnz) {
+    return guarded(ctx, [&](Ctx& c) {
+        require(A && B && c_colptr, SLAPCU_ERR_INVALID, "null argument");
+        const int64_t nnz = fused_begin(c, view(*A), view(*B), sr, alg, c_colptr, staging_budget_bytes);
+        if (c_nnz) *c_nnz = nnz;
+    });
+}
+
+slapcu_status slapcu_spgemm_finish(slapcu_ctx ctx, const slapcu_csc* A, const slapcu_csc* B, slapcu_semiring sr,
+                                   int32_t* c_rowids, void* c_vals) {
+    return guarded(ctx, [&](Ctx& c) {
+        require(A && B, SLAPCU_ERR_INVALID, "null argument");
+        fused_finish(c, view(*A), view(*B), sr, c_rowids, c_vals);
+    });
+}
+
+// Largest staging area the one-shot call will take: half the free device memory.
+static int64_t default_staging_budget(Ctx& c) {
+    size_t fr = 0, tot = 0;
+    SLAPCU_CUDA(cudaMemGetInfo(&fr, &tot));
+    return int64_t(fr / 2);
+}
+
 slapcu_status slapcu_spgemm(slapcu_ctx ctx, const slapcu_csc* A, const slapcu_csc* B, slapcu_semiring sr,
                             slapcu_alg alg, slapcu_csc_out* C) {
     return guarded(ctx, [&](Ctx& c) {
@@ -237,8 +261,15 @@ slapcu_status slapcu_spgemm(slapcu_ctx ctx, const slapcu_csc* A, const slapcu_cs
         int64_t* cp = nullptr;
         SLAPCU_CUDA(cudaMallocAsync((void**)&cp, sizeof(int64_t) * (b.ncols + 1), c.stream));
         int64_t nnz = 0;
+        bool fused = true;
         try {
-            nnz = spgemm_symbolic(c, a, b, alg, cp);
+            try {
+                nnz = fused_begin(c, a, b, sr, alg, cp, default_staging_budget(c));
+            } catch (const Fail& e) {
+                if (e.st != SLAPCU_ERR_BUDGET) throw;
+                fused = false;  // staging does not fit: two-pass path needs none
+                nnz = spgemm_symbolic(c, a, b, alg, cp);
+            }
         } catch (...) {
             cudaFreeAsync(cp, c.stream);
             throw;
@@ -251,7 +282,10 @@ slapcu_status slapcu_spgemm(slapcu_ctx ctx, const slapcu_csc* A, const slapcu_cs
         C->vals = nullptr;
         SLAPCU_CUDA(cudaMallocAsync((void**)&C->rowids, sizeof(int32_t) * std::max<int64_t>(nnz, 1), c.stream));
         SLAPCU_CUDA(cudaMallocAsync(&C->vals, size_t(vs) * std::max<int64_t>(nnz, 1), c.stream));
-        spgemm_numeric(c, a, b, sr, alg, cp, C->rowids, C->vals);
+        if (fused)
+            fused_finish(c, a, b, sr, C->rowids, C->vals);
+        else
+            spgemm_numeric(c, a, b, sr, alg, cp, C->rowids, C->vals);
     });
 }
 

@@ -90,6 +90,26 @@ struct Plan {
     bool valid = false;
 };
 
+struct Bins {
+    std::vector<int> count;   // per bin
+    std::vector<int> offset;  // per bin
+    DevBuf list;              // int32[n_nonzero]
+};
+
+// State of a fused product carried from spgemm_begin to spgemm_finish.
+struct FusedState {
+    bool valid = false;
+    const void* a_key = nullptr;
+    const void* b_key = nullptr;
+    int sr = -1;
+    int64_t ncols = -1, nnz = 0;
+    const int64_t* colptr = nullptr;
+    bool ones = false;
+    DevBuf srows, svals, cnt, soff, scur, seg_off, seg_cnt;
+    Bins bins;
+    int nlight_bins = 0, tile_log2 = 0, T = 0;
+};
+
 struct Options {
     int tile_rows_log2 = 18;      // numeric dense-tile height
     int sym_tile_rows_log2 = 19;  // symbolic bitmap height
@@ -126,6 +146,7 @@ struct Ctx {
     int64_t launches = 0;
     Options opt;
     Plan plan;
+    FusedState fused;
     std::string last_error;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     float sym_ms = 0.f, num_ms = 0.f;
@@ -154,6 +175,11 @@ void spgemm_flops(Ctx& c, const DevCsc& A, const DevCsc& B, int64_t* flops_dev, 
 int64_t spgemm_symbolic(Ctx& c, const DevCsc& A, const DevCsc& B, int alg, int64_t* c_colptr);
 void spgemm_numeric(Ctx& c, const DevCsc& A, const DevCsc& B, int sr, int alg, const int64_t* c_colptr,
                     int32_t* c_rowids, void* c_vals);
+// fused.cu: single-product-pass begin/finish
+int64_t fused_begin(Ctx& c, const DevCsc& A, const DevCsc& B, int sr, int alg, int64_t* c_colptr,
+                    int64_t staging_budget_bytes);
+void fused_finish(Ctx& c, const DevCsc& A, const DevCsc& B, int sr, int32_t* c_rowids, void* c_vals);
+void any_zero_u8(Ctx& c, const uint8_t* v, int64_t n, int* flag);
 void dcsc_colptr(Ctx& c, int64_t ncols, int64_t nzc, const int32_t* jc, const int32_t* cp, int64_t* colptr);
 void exclusive_scan_i64(Ctx& c, const int64_t* in, int64_t* out, int64_t n);
 

@@ -144,13 +144,222 @@ __device__ __forceinline__ long long block_sum_ll(long long v, long long* red) {
 }
 
 
-// ---------------------------------------------------------------- host side
+// walk_tile with memory-level parallelism: every lane issues U independent
+// row-id loads before applying f to them, so a warp keeps U sectors of A in
+// flight instead of one (the product loop is L2-latency bound otherwise).
+// Same contract (tile range, cursors) as walk_tile.
+template <int U, class F>
+__device__ __forceinline__ void walk_tile_ilp(const DevCsc& A, const DevCsc& B, int64_t bs, int64_t be, int sg,
+                                              int tid, int nt, int t, int ntiles, int t1,
+                                              const int32_t* __restrict__ cur_in, int32_t* __restrict__ cur_out,
+                                              bool write_cursor, F&& f) {
+    const int sub = tid / sg, nsub = nt / sg, sl = tid % sg;
+    for (int64_t i = bs + sub; i < be; i += nsub) {
+        const int k = B.rw[i];
+        const int64_t as = A.cp[k], ae = A.cp[k + 1];
+        const int64_t start = (ntiles == 1 || t == 0) ? as : as + cur_in[i - B.base];
+        int64_t p = start + sl;
+        int64_t stop = -1;
+        while (stop < 0) {
+            int r[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t q = p + int64_t(u) * sg;
+                r[u] = q < ae ? __ldg(&A.rw[q]) : INT_MAX;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (stop < 0) {
+                    if (r[u] < t1)
+                        f(p + int64_t(u) * sg, i, r[u]);
+                    else
+                        stop = p + int64_t(u) * sg;
+                }
+            }
+            p += int64_t(U) * sg;
+        }
+        if (write_cursor && ntiles > 1) {
+            if (stop > ae) stop = ae;
+            const bool mine = (stop == start) || (A.rw[stop - 1] < t1);
+            if (mine) cur_out[i - B.base] = (int32_t)(stop - as);
+        }
+    }
+}
 
-struct Bins {
-    std::vector<int> count;   // per bin
-    std::vector<int> offset;  // per bin
-    DevBuf list;              // int32[n_nonzero]
+// Products of ONE B entry i (A column k, entries [start, ae)) restricted to
+// rows < t1, walked by `width` threads of which this is thread `sl`, U loads
+// in flight per thread.  Returns nothing; writes the tile cursor through
+// cur_out_i (may be null) from the thread that owns the first out-of-tile
+// position.
+template <int U, class F>
+__device__ __forceinline__ void walk_entry(const int32_t* __restrict__ Arw, int64_t i, int64_t as, int64_t start,
+                                           int64_t ae, int sl, int width, int t1, int32_t* cur_out_i, F&& f) {
+    int64_t p = start + sl;
+    int64_t stop = -1;
+    while (stop < 0) {
+        int r[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t q = p + int64_t(u) * width;
+            r[u] = q < ae ? __ldg(&Arw[q]) : INT_MAX;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (stop < 0) {
+                if (r[u] < t1)
+                    f(p + int64_t(u) * width, i, r[u]);
+                else
+                    stop = p + int64_t(u) * width;
+            }
+        }
+        p += int64_t(U) * width;
+    }
+    if (cur_out_i) {
+        if (stop > ae) stop = ae;
+        const bool mine = (stop == start) || (Arw[stop - 1] < t1);
+        if (mine) *cur_out_i = (int32_t)(stop - as);
+    }
+}
+
+// Shared state of walk_balanced (static shared memory of the caller).
+struct WalkShared {
+    int next;      // dynamic hand-out of short entries
+    int nlong;     // long entries collected this round
+    int list[512];  // their B positions (relative to bs)
 };
+
+// Load-balanced walk of all products of column j inside one row tile.  A
+// column's share of the work is its remaining length; R-MAT columns mix hub
+// A columns (10^4 entries) with short ones, and a static entry->sub-group map
+// leaves most warps waiting at the next barrier for the one holding the hub
+// (ncu: `barrier` was the top stall).  Here entries with >= `big` remaining
+// products are walked by the whole CTA cooperatively (collected NT at a time
+// into shared memory), and the others are handed out to sub-groups of sg
+// lanes through a shared atomic counter.  Must be called by all threads of
+// the CTA (contains barriers); NT <= 512.
+template <int U, class F>
+__device__ __forceinline__ void walk_balanced(const DevCsc& A, const DevCsc& B, int64_t bs, int64_t be, int sg,
+                                              int t, int ntiles, int t1, const int32_t* __restrict__ cur_in,
+                                              int32_t* __restrict__ cur_out, int64_t big, WalkShared& ws, F&& f) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const bool tiled = ntiles > 1;
+    const int64_t nb = be - bs;
+    auto start_of = [&](int64_t i, int64_t as) -> int64_t {
+        return (!tiled || t == 0) ? as : as + cur_in[i - B.base];
+    };
+    // phase A: long entries, whole CTA per entry
+    for (int64_t base = 0; base < nb; base += nt) {
+        if (tid == 0) ws.nlong = 0;
+        __syncthreads();
+        const int64_t i = bs + base + tid;
+        if (base + tid < nb) {
+            const int k = B.rw[i];
+            const int64_t as = A.cp[k], ae = A.cp[k + 1];
+            if (ae - start_of(i, as) >= big) ws.list[atomicAdd(&ws.nlong, 1)] = (int)(base + tid);
+        }
+        __syncthreads();
+        const int nl = ws.nlong;
+        for (int li = 0; li < nl; ++li) {
+            const int64_t ii = bs + ws.list[li];
+            const int k = B.rw[ii];
+            const int64_t as = A.cp[k], ae = A.cp[k + 1];
+            walk_entry<U>(A.rw, ii, as, start_of(ii, as), ae, tid, nt, t1, tiled ? cur_out + (ii - B.base) : nullptr,
+                          f);
+        }
+        __syncthreads();
+    }
+    // phase B: short entries, dynamic hand-out to sub-groups
+    if (tid == 0) ws.next = 0;
+    __syncthreads();
+    const int lane = tid & 31, sl = lane % sg, subs = 32 / sg;
+    for (;;) {
+        int got = 0;
+        if (lane == 0) got = atomicAdd(&ws.next, subs);
+        got = __shfl_sync(0xffffffffu, got, 0);
+        if (got >= nb) break;
+        const int64_t e = got + lane / sg;
+        if (e < nb) {
+            const int64_t i = bs + e;
+            const int k = B.rw[i];
+            const int64_t as = A.cp[k], ae = A.cp[k + 1];
+            const int64_t st = start_of(i, as);
+            if (ae - st < big)
+                walk_entry<U>(A.rw, i, as, st, ae, sl, sg, t1, tiled ? cur_out + (i - B.base) : nullptr, f);
+        }
+    }
+    __syncthreads();
+}
+
+// Writes the set bits of a warp's 32 bitmap words (word w0+lane) as row ids
+// rb_lane + bit to out[base ...] in order, 32 consecutive entries per store:
+// output element o is found by a shuffle search for the lane whose exclusive
+// prefix covers o, then __fns for the bit.
+__device__ __forceinline__ void emit_rows_coalesced(unsigned bits, int row_base, int32_t* __restrict__ out,
+                                                    int lane) {
+    int tot;
+    const int ex = warp_excl_scan(__popc(bits), lane, &tot);
+    for (int o0 = 0; o0 < tot; o0 += 32) {
+        const int o = o0 + lane;
+        // largest lane l with ex_l <= o (ex is non-decreasing across lanes)
+        int lo = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+            const int cand = lo + step;
+            const int exc = __shfl_sync(0xffffffffu, ex, cand & 31);
+            if (cand < 32 && exc <= o) lo = cand;
+        }
+        const unsigned w = __shfl_sync(0xffffffffu, bits, lo);
+        const int rb = __shfl_sync(0xffffffffu, row_base, lo);
+        const int exl = __shfl_sync(0xffffffffu, ex, lo);
+        if (o < tot) out[o] = rb + (int)__fns(w, 0, o - exl + 1);
+    }
+}
+
+// Per-word exclusive popcount prefix of a W-word bitmap (the rank of every
+// set bit among the tile's set bits) into pre[], chunk bases in chunk[];
+// returns the tile's popcount (all threads).  Uses warp scans inside 32-word
+// chunks, then one warp scans the chunk totals.
+__device__ __forceinline__ int bitmap_ranks(const unsigned* __restrict__ bm, int* __restrict__ pre,
+                                            int* __restrict__ chunk, int W, int* total_sh) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    const int nch = (W + 31) >> 5;
+    for (int c = warp; c < nch; c += nw) {
+        const int w = c * 32 + lane;
+        const int x = w < W ? __popc(bm[w]) : 0;
+        int tot;
+        const int ex = warp_excl_scan(x, lane, &tot);
+        if (w < W) pre[w] = ex;
+        if (lane == 0) chunk[c] = tot;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        int run = 0;
+        for (int b0 = 0; b0 < nch; b0 += 32) {
+            const int c = b0 + lane;
+            const int x = c < nch ? chunk[c] : 0;
+            int tot;
+            const int ex = warp_excl_scan(x, lane, &tot);
+            if (c < nch) chunk[c] = run + ex;
+            run += tot;
+        }
+        if (lane == 0) *total_sh = run;
+    }
+    __syncthreads();
+    for (int w = tid; w < W; w += blockDim.x) pre[w] += chunk[w >> 5];
+    __syncthreads();
+    return *total_sh;
+}
+
+// Zero n words of shared memory with 16-byte stores (n a multiple of 4 or the
+// tail handled word-wise).
+__device__ __forceinline__ void smem_zero(unsigned* p, int n) {
+    const int n4 = n >> 2;
+    uint4* q = reinterpret_cast<uint4*>(p);
+    for (int i = threadIdx.x; i < n4; i += blockDim.x) q[i] = make_uint4(0u, 0u, 0u, 0u);
+    for (int i = (n4 << 2) + threadIdx.x; i < n; i += blockDim.x) p[i] = 0u;
+}
+
+// ---------------------------------------------------------------- host side
 
 // Opt in to more than the default 48 KB of dynamic shared memory.  The
 // kernels also hold a few bytes of static shared memory, which counts

@@ -591,7 +591,7 @@ void launch_num_heavy(Ctx& c, const DevCsc& A, const DevCsc& B, const int* list,
     while (tl > 10 && (int64_t(1) << (tl - 1)) >= A.nrows) --tl;
     const size_t fixed = heavy_fixed_smem(tl);
     // two CTAs per SM when the bitmap leaves room; otherwise one
-    size_t budget = std::min<size_t>(size_t(c.smem_optin), size_t(113) * 1024);
+    size_t budget = std::min<size_t>(size_t(c.smem_optin), size_t(110) * 1024);
     if (budget < fixed + 1024 * sizeof(Acc)) budget = size_t(c.smem_optin);
     int cap = ONES ? 0 : (int)((budget - fixed) / sizeof(Acc));
     if (cap < 0) cap = 0;
@@ -766,6 +766,10 @@ __global__ void k_dcsc_dense(int64_t ncols, int64_t nzc, const int32_t* __restri
         }
         colptr[j] = cp[lo];
     }
+}
+
+void any_zero_u8(Ctx& c, const uint8_t* v, int64_t n, int* flag) {
+    launch(c, k_any_zero_u8, dim3(grid_for(c, n, 256)), dim3(256), 0, n, v, flag);
 }
 
 void resolve(Ctx& c, DevCsc& m) {

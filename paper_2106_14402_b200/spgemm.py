@@ -366,10 +366,15 @@ def symbolic_nnz(a, b, threads: int = 1, alg=SpGemmAlg.hybrid, ctx: Context | No
     return cp[1:] - cp[:-1]
 
 
-def local_spgemm(a, b, sr: Semiring, alg=SpGemmAlg.hybrid, threads: int = 1, ctx: Context | None = None):
+def local_spgemm(a, b, sr: Semiring, alg=SpGemmAlg.hybrid, threads: int = 1, ctx: Context | None = None,
+                 method: str = "fused"):
     """spgemm.hpp:275-330 local_spgemm.  Returns a DeviceCsc for device
     operands and a host CscMatrix for host operands (the host call runs the
-    H2D copies, the three GPU phases and the D2H copies inside the library)."""
+    H2D copies, the three GPU phases and the D2H copies inside the library).
+
+    method "fused" (default) forms each column once (slapcu_spgemm_begin /
+    _finish) and falls back to "two_pass" (slapcu_spgemm_symbolic / _numeric)
+    when its staging area would not fit in half the free device memory."""
     sr = _sr(sr)
     alg = SpGemmAlg(int(alg))
     ctx = _ctx(ctx)
@@ -385,6 +390,22 @@ def local_spgemm(a, b, sr: Semiring, alg=SpGemmAlg.hybrid, threads: int = 1, ctx
     cp = torch.empty(B.ncols + 1, dtype=torch.int64, device=dev)
     nnz = C.c_int64()
     av, bv = A.view(), B.view()
+    if method == "fused":
+        free, _ = torch.cuda.mem_get_info(dev)
+        st = ctx.lib.slapcu_spgemm_begin(ctx.h, C.byref(av), C.byref(bv), sr.id, int(alg), int(free // 2),
+                                         cp.data_ptr(), C.byref(nnz))
+        if st == L.OK:
+            n = int(nnz.value)
+            rw = torch.empty(n, dtype=torch.int32, device=dev)
+            vals = torch.empty(n, dtype=sr.torch_dtype, device=dev)
+            ctx.check(ctx.lib.slapcu_spgemm_finish(ctx.h, C.byref(av), C.byref(bv), sr.id,
+                                                   rw.data_ptr() if n else None, vals.data_ptr() if n else None),
+                      "finish")
+            return DeviceCsc(A.nrows, B.ncols, cp, rw, vals)
+        if st != 5:  # anything but BudgetError is a real failure
+            ctx.check(st, "begin")
+    elif method != "two_pass":
+        raise ValueError(f"unknown method {method!r}")
     ctx.check(ctx.lib.slapcu_spgemm_symbolic(ctx.h, C.byref(av), C.byref(bv), int(alg), cp.data_ptr(), C.byref(nnz)),
               "symbolic")
     n = int(nnz.value)

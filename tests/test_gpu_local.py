@@ -25,6 +25,7 @@ from paper_2106_14402_b200 import _lib as L  # noqa: E402
 
 SRS = [P.PlusTimesF64, P.PlusTimesF32, P.PlusTimesI64, P.MinPlusI32, P.MinPlusF64, P.OrAnd]
 ALGS = [P.SpGemmAlg.heap, P.SpGemmAlg.hash, P.SpGemmAlg.hybrid]
+METHODS = ["fused", "two_pass"]
 
 
 def example_a():
@@ -96,8 +97,9 @@ def test_random_vs_oracle(port, sr):
     for a, b in _random_pairs(101 + sr.id, 40, kind, sr.np_dtype):
         want = port.spgemm(sr.id, a, b)
         for alg in ALGS:
-            got = P.local_spgemm(to_device(a), to_device(b), sr, alg)
-            assert_parity(got, want, sr.id, f"{sr.name}/{sr.dtype}/{alg.name}")
+            for method in METHODS:
+                got = P.local_spgemm(to_device(a), to_device(b), sr, alg, method=method)
+                assert_parity(got, want, sr.id, f"{sr.name}/{sr.dtype}/{alg.name}/{method}")
 
 
 def test_symbolic_and_flops(port):
@@ -122,8 +124,9 @@ def test_rmat_square_vs_oracle(port, sr, scale):
     want = port.spgemm(sr.id, a, a)
     da = to_device(a)
     for alg in ALGS:
-        got = P.local_spgemm(da, da, sr, alg)
-        assert_parity(got, want, sr.id, f"rmat{scale}/{alg.name}")
+        for method in METHODS:
+            got = P.local_spgemm(da, da, sr, alg, method=method)
+            assert_parity(got, want, sr.id, f"rmat{scale}/{alg.name}/{method}")
 
 
 @pytest.mark.parametrize("sr", SRS, ids=lambda s: f"{s.name}_{s.dtype}")
@@ -140,8 +143,9 @@ def test_multi_tile_paths(port, sr):
     ctx.set_option(L.OPT_LIGHT_FLOPS_MAX, 32)
     da = to_device(a)
     for alg in ALGS:
-        got = P.local_spgemm(da, da, sr, alg, ctx=ctx)
-        assert_parity(got, want, sr.id, f"tiles/{alg.name}")
+        for method in METHODS:
+            got = P.local_spgemm(da, da, sr, alg, ctx=ctx, method=method)
+            assert_parity(got, want, sr.id, f"tiles/{alg.name}/{method}")
 
 
 def test_or_and_with_zero_values(port):
@@ -151,8 +155,9 @@ def test_or_and_with_zero_values(port):
     a = a.with_vals(v)
     want = port.spgemm(oracle.OR_AND_U8, a, a)
     for alg in ALGS:
-        got = P.local_spgemm(to_device(a), to_device(a), P.OrAnd, alg)
-        assert_parity(got, want, oracle.OR_AND_U8, alg.name)
+        for method in METHODS:
+            got = P.local_spgemm(to_device(a), to_device(a), P.OrAnd, alg, method=method)
+            assert_parity(got, want, oracle.OR_AND_U8, f"{alg.name}/{method}")
 
 
 def test_host_call_matches_device(port):
@@ -182,8 +187,9 @@ def test_rectangular_and_empty_columns(port):
     bb = with_values(port, bb, oracle.PLUS_TIMES_F64)
     want = port.spgemm(oracle.PLUS_TIMES_F64, a, bb)
     for alg in ALGS:
-        got = P.local_spgemm(to_device(a), to_device(bb), P.PlusTimesF64, alg)
-        assert_parity(got, want, oracle.PLUS_TIMES_F64, alg.name)
+        for method in METHODS:
+            got = P.local_spgemm(to_device(a), to_device(bb), P.PlusTimesF64, alg, method=method)
+            assert_parity(got, want, oracle.PLUS_TIMES_F64, f"{alg.name}/{method}")
 
 
 def test_thread_count_invariance(port):
@@ -195,3 +201,30 @@ def test_thread_count_invariance(port):
     for t in (2, 4, 8):
         c = P.local_spgemm(da, da, P.PlusTimesI64, threads=t).to_host()
         assert np.array_equal(c.rowids, base.rowids) and np.array_equal(c.vals, base.vals)
+
+
+def test_column_window_operand(port):
+    """B given as a column window (colptr not starting at 0) -- the batched
+    driver's slices (batched.hpp:43-66) -- gives exactly those columns."""
+    from paper_2106_14402_b200 import dist as D
+
+    a = with_values(port, port.gen_rmat(11), oracle.MIN_PLUS_I32)
+    want = port.spgemm(oracle.MIN_PLUS_I32, a, a, 300, 1500)
+    da = to_device(a)
+    for method in METHODS:
+        got = P.local_spgemm(da, D.column_window(da, 300, 1500), P.MinPlusI32, method=method)
+        assert_parity(got, want, oracle.MIN_PLUS_I32, method)
+
+
+def test_staging_budget_error():
+    """begin() refuses a staging area above the budget (BudgetError)."""
+    import ctypes as C
+
+    a = P.gen_rmat(10)
+    a = P.fill_values(a, P.OrAnd, 0)
+    ctx = P.default_context()
+    cp = torch.empty(a.ncols + 1, dtype=torch.int64, device=a.colptr.device)
+    nnz = C.c_int64()
+    st = ctx.lib.slapcu_spgemm_begin(ctx.h, C.byref(a.view()), C.byref(a.view()), P.OrAnd.id, 2, 1024,
+                                     cp.data_ptr(), C.byref(nnz))
+    assert st == 5  # SLAPCU_ERR_BUDGET
