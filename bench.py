@@ -55,7 +55,21 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-cols", type=int, default=256, help="columns per CPU-baseline slice")
     ap.add_argument("--profile", type=int, default=1)
+    ap.add_argument("--sym-tile-log2", type=int, default=0, help="row-tile height of the pattern bitmap (0 = default)")
+    ap.add_argument("--tile-log2", type=int, default=0, help="row-tile height of the value pass (0 = default)")
+    ap.add_argument("--dense-min", type=int, default=None, help="byte-flag pattern path for flops >= this (0 off)")
     return ap.parse_args()
+
+
+def apply_options(ctx, args):
+    from paper_2106_14402_b200 import _lib as L
+
+    if args.sym_tile_log2:
+        ctx.set_option(L.OPT_SYM_TILE_ROWS_LOG2, args.sym_tile_log2)
+    if args.tile_log2:
+        ctx.set_option(L.OPT_TILE_ROWS_LOG2, args.tile_log2)
+    if args.dense_min is not None:
+        ctx.set_option(L.OPT_DENSE_FLOPS_MIN, args.dense_min)
 
 
 # ------------------------------------------------------------------ helpers
@@ -177,6 +191,7 @@ def run_ours(args):
     dev = torch.device("cuda", 0)
     stream = torch.cuda.current_stream()
     ctx = P.Context(0, stream)
+    apply_options(ctx, args)
     lib = ctx.lib
     sr = P.OrAnd if args.semiring == "or_and" else P.MinPlusI32
     kind = 0 if sr is P.OrAnd else 3
@@ -195,13 +210,25 @@ def run_ours(args):
     bound = np.minimum(flops_per.cpu().numpy(), A.nrows)
     free, _tot = torch.cuda.mem_get_info()
     stage_entry = 4 + (0 if sr is P.OrAnd else vs)
-    budget = int(args.budget_gb * 2**30) if args.budget_gb > 0 else int(min(0.30 * free, 40 * 2**30))
+    budget = int(args.budget_gb * 2**30) if args.budget_gb > 0 else int(min(0.15 * free, 24 * 2**30))
     batches = plan_batches(bound, stage_entry, budget)
     max_cap = max(int(bound[s:e].sum()) for s, e in batches)
     max_cols = max(e - s for s, e in batches)
-    out_cp = torch.empty(max_cols + 1, dtype=torch.int64, device=dev)
-    out_rw = torch.empty(max(max_cap, 1), dtype=torch.int32, device=dev)
-    out_v = torch.empty(max(max_cap, 1), dtype=sr.torch_dtype, device=dev)
+    # Two contexts on two streams, batches alternating: batch b+1's pattern
+    # pass (shared-memory bound) runs while batch b's finish (copy / value
+    # pass) is still in flight -- slapcu_spgemm_finish is asynchronous
+    # (SLAPCU_OPT_ASYNC_FINISH) and the next begin() on the same context
+    # settles it.  Each context owns its staging area and output buffers.
+    stream2 = torch.cuda.Stream(device=dev)
+    ctxs = [ctx, P.Context(0, stream2)]
+    apply_options(ctxs[1], args)
+    streams = [stream, stream2]
+    outs = []
+    for cx in ctxs:
+        cx.set_option(L.OPT_ASYNC_FINISH, 1)
+        outs.append((torch.empty(max_cols + 1, dtype=torch.int64, device=dev),
+                     torch.empty(max(max_cap, 1), dtype=torch.int32, device=dev),
+                     torch.empty(max(max_cap, 1), dtype=sr.torch_dtype, device=dev)))
     av = A.view()
     import ctypes as C
 
@@ -213,13 +240,17 @@ def run_ours(args):
 
     def step(collect=None):
         for bi, w in enumerate(wins):
+            cx = ctxs[bi % 2]
+            o_cp, o_rw, o_v = outs[bi % 2]
             nz = C.c_int64()
-            ctx.check(lib.slapcu_spgemm_begin(ctx.h, C.byref(av), C.byref(w), sr.id, P.SpGemmAlg.hybrid, 0,
-                                              out_cp.data_ptr(), C.byref(nz)), "begin")
-            ctx.check(lib.slapcu_spgemm_finish(ctx.h, C.byref(av), C.byref(w), sr.id, out_rw.data_ptr(),
-                                               out_v.data_ptr()), "finish")
+            cx.check(lib.slapcu_spgemm_begin(cx.h, C.byref(av), C.byref(w), sr.id, P.SpGemmAlg.hybrid, 0,
+                                             o_cp.data_ptr(), C.byref(nz)), "begin")
+            cx.check(lib.slapcu_spgemm_finish(cx.h, C.byref(av), C.byref(w), sr.id, o_rw.data_ptr(),
+                                              o_v.data_ptr()), "finish")
             if collect is not None:
                 collect(bi, int(nz.value))
+        for cx in ctxs:
+            cx.check(lib.slapcu_ctx_synchronize(cx.h), "synchronize")
 
     # parity spot check of the benchmarked configuration (column checksums of
     # the first batch vs. the symbolic counts) happens in tests; here we only
@@ -228,26 +259,35 @@ def run_ours(args):
     step(lambda bi, nz: got.append(nz))
     assert sum(got) == nnz_c, (sum(got), nnz_c)
 
-    ctx.set_option(L.OPT_PROFILE, int(args.profile))
+    for cx in ctxs:
+        cx.set_option(L.OPT_PROFILE, int(args.profile))
     for _ in range(args.warmup - 1):
         step()
     torch.cuda.synchronize()
-    ctx.reset_stats()
-    launches0 = ctx.launches
+    for cx in ctxs:
+        cx.reset_stats()
+    launches0 = sum(cx.launches for cx in ctxs)
     clocks = ClockSampler(0)
     clocks.start()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in streams]
     torch.cuda.synchronize()
     ev0.record(stream)
+    stream2.wait_event(ev0)
     for _ in range(args.steps):
         step()
-    ev1.record(stream)
+    for e, s in zip(ev1, streams):
+        e.record(s)
     torch.cuda.synchronize()
     clk = clocks.stop()
-    ms = ev0.elapsed_time(ev1) / args.steps
-    launches = (ctx.launches - launches0) // args.steps
-    kstats = ctx.kernel_stats()
-    ctx.set_option(L.OPT_PROFILE, 0)
+    ms = max(ev0.elapsed_time(e) for e in ev1) / args.steps
+    launches = (sum(cx.launches for cx in ctxs) - launches0) // args.steps
+    kstats = {}
+    for cx in ctxs:
+        for k, (nl, t) in cx.kernel_stats().items():
+            a, b = kstats.get(k, (0, 0.0))
+            kstats[k] = (a + nl, b + t)
+        cx.set_option(L.OPT_PROFILE, 0)
     value = 2.0 * total_flops / (ms / 1e3) / 1e9
 
     # ---- roofline of the dominant kernel class
@@ -358,6 +398,7 @@ def run_e2e_single(args, A, sr, batches, counts, total_flops, ctx, stream):
     from paper_2106_14402_b200 import _lib as L
 
     vs = 1 if sr is P.OrAnd else 4
+    ctx.set_option(L.OPT_ASYNC_FINISH, 0)  # one stream here; errors reported per call
     h_cp = A.colptr.cpu().pin_memory()
     h_rw = A.rowids.cpu().pin_memory()
     h_v = A.vals.cpu().pin_memory()
@@ -416,8 +457,222 @@ def run_e2e_single(args, A, sr, batches, counts, total_flops, ctx, stream):
             "steps": max(args.e2e_steps, 1)}
 
 
+def dist_shape(world: int):
+    """p=4 -> 2D 2x2 SUMMA; p=2 -> 3D c=2 q=1; p=8 -> 3D 2x2x2 (2D needs a square
+    grid, summa.hpp:112-113); other p: 3D with c=p/q^2 for the largest square q^2."""
+    import math
+
+    if int(math.isqrt(world)) ** 2 == world and world > 1 and world != 8:
+        return "summa", 1
+    for q in range(int(math.isqrt(world)), 0, -1):
+        if world % (q * q) == 0:
+            return "ca3d", world // (q * q)
+    return "ca3d", world
+
+
 def run_ours_dist(args, world, rank):
-    raise SystemExit("multi-GPU bench: see bench_dist (not yet enabled)")
+    """N GPUs, one process each: the same C3 product through the NCCL drivers
+    (slapcu_summa2d / slapcu_ca3d), in column batches of every rank's B block
+    (batched.hpp:153-170); time = max over ranks of CUDA-event time."""
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2106_14402_b200 as P
+    from paper_2106_14402_b200 import _lib as L
+    from paper_2106_14402_b200 import dist as D
+    from paper_2106_14402_b200 import grid as G
+
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.current_stream()
+    ctx = P.Context(local, stream)
+    apply_options(ctx, args)
+    comm = D.NcclComm(ctx)
+    sr = P.OrAnd if args.semiring == "or_and" else P.MinPlusI32
+    kind = 0 if sr is P.OrAnd else 3
+    vs = 1 if sr is P.OrAnd else 4
+    A0 = P.fill_values(P.gen_rmat(args.scale, args.edge_factor, 1, ctx=ctx), sr, kind, ctx=ctx)
+    total_flops, flops_per = P.estimate_flops(A0, A0, ctx=ctx)
+    # symmetric relabelling P A P^T: same flops and nnz(C), balanced blocks
+    A = P.permute_symmetric(A0, 7, sr, ctx=ctx)
+    del A0
+    n = A.nrows
+    mode, layers = dist_shape(world)
+    if mode == "summa":
+        q = G.isqrt_exact(world)
+        a_loc = D.block_2d(A, q, rank)
+        b_loc = a_loc
+        out_div = q  # a rank's output is ~ its column block's share over q row blocks
+    else:
+        g = G.Grid3D.make(world, layers, rank)
+        q = g.q
+        a_loc = D.block_3d(A, layers, q, rank, "cols")
+        b_loc = D.block_3d(A, layers, q, rank, "rows")
+        out_div = q * layers
+    fl = flops_per.cpu().numpy()
+    bound_total = int(np.minimum(fl, n).sum())
+    free, _ = torch.cuda.mem_get_info()
+    budget = int(args.budget_gb * 2**30) if args.budget_gb > 0 else int(min(0.18 * free, 24 * 2**30))
+    # per-rank staging bound of one product over the whole local B block
+    est = bound_total * (4 + vs) // max(out_div, 1) * 2
+    nb = max(1, -(-est // budget))
+    t = torch.tensor([nb], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    nb = int(t.item())
+    lc = b_loc.ncols
+    wins = [D.column_window(b_loc, (b * lc) // nb, ((b + 1) * lc) // nb) for b in range(nb)]
+    av = a_loc.view()
+    bvs = [w.view() for w in wins]
+    lib = ctx.lib
+    totals = {"local": 0.0, "merge": 0.0, "bcast": 0.0, "nnz": 0}
+
+    def step(record=False):
+        for bv in bvs:
+            out = L.CscOut()
+            st = L.DistStats()
+            if mode == "summa":
+                rc = lib.slapcu_summa2d(comm.h, C.byref(av), C.byref(bv), sr.id, int(P.SpGemmAlg.hybrid), C.byref(out),
+                                        C.byref(st))
+            else:
+                rc = lib.slapcu_ca3d(comm.h, layers, C.byref(av), C.byref(bv), sr.id, int(P.SpGemmAlg.hybrid),
+                                     C.byref(out), C.byref(st))
+            ctx.check(rc, mode)
+            if record:
+                totals["local"] += st.ms_local
+                totals["merge"] += st.ms_merge
+                totals["bcast"] += st.ms_exposed_bcast
+                totals["nnz"] += int(out.nnz)
+            D.free_out(ctx, out)  # consumer: discard (batched.hpp:168)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches0 = ctx.launches
+    clocks = ClockSampler(local) if rank == 0 else None
+    if clocks:
+        clocks.start()
+    dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for s in range(args.steps):
+        step(record=(s == 0))
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk = clocks.stop() if clocks else None
+    ms_local_rank = ev0.elapsed_time(ev1) / args.steps
+
+    # ---- e2e: this rank's blocks H2D from pinned memory, every output batch D2H
+    e2e_ms, h2d, d2h = 0.0, 0, 0
+    if not args.no_e2e:
+        cud = L.cudart()
+        hbuf = torch.empty(1 << 28, dtype=torch.uint8).pin_memory()
+
+        def pin(m):
+            return [m.colptr.cpu().pin_memory(), m.rowids.cpu().pin_memory(), m.vals.cpu().pin_memory()]
+
+        ha = pin(a_loc)
+        hb = ha if b_loc is a_loc else pin(b_loc)
+        da = [x.to(dev) for x in ha]
+        db = da if hb is ha else [x.to(dev) for x in hb]
+        a2 = P.DeviceCsc(a_loc.nrows, a_loc.ncols, *da)
+        b2 = P.DeviceCsc(b_loc.nrows, b_loc.ncols, *db)
+        av2 = a2.view()
+        bvs2 = [D.column_window(b2, (b * lc) // nb, ((b + 1) * lc) // nb).view() for b in range(nb)]
+        h2d = sum(x.numel() * x.element_size() for x in ha) + (0 if hb is ha else sum(
+            x.numel() * x.element_size() for x in hb))
+
+        def e2e_step():
+            nonlocal d2h
+            d2h = 0
+            for dst, src in zip(da, ha):
+                dst.copy_(src, non_blocking=True)
+            if db is not da:
+                for dst, src in zip(db, hb):
+                    dst.copy_(src, non_blocking=True)
+            for bv in bvs2:
+                out = L.CscOut()
+                st = L.DistStats()
+                if mode == "summa":
+                    rc = lib.slapcu_summa2d(comm.h, C.byref(av2), C.byref(bv), sr.id, int(P.SpGemmAlg.hybrid),
+                                            C.byref(out), C.byref(st))
+                else:
+                    rc = lib.slapcu_ca3d(comm.h, layers, C.byref(av2), C.byref(bv), sr.id, int(P.SpGemmAlg.hybrid),
+                                         C.byref(out), C.byref(st))
+                ctx.check(rc, mode)
+                for ptr, nbytes in ((out.colptr, 8 * (out.ncols + 1)), (out.rowids, 4 * out.nnz),
+                                    (out.vals, vs * out.nnz)):
+                    for o in range(0, nbytes, hbuf.numel()):
+                        m = min(hbuf.numel(), nbytes - o)
+                        cud.cudaMemcpyAsync(C.c_void_p(hbuf.data_ptr()), C.c_void_p(ptr + o), C.c_size_t(m), 2,
+                                            C.c_void_p(stream.cuda_stream))
+                        d2h += m
+                D.free_out(ctx, out)
+            torch.cuda.current_stream().synchronize()
+
+        e2e_step()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(max(args.e2e_steps, 1)):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = e0.elapsed_time(e1) / max(args.e2e_steps, 1)
+        dist.barrier()
+    tm = torch.tensor([ms_local_rank, totals["local"], totals["merge"], totals["bcast"], float(totals["nnz"]), e2e_ms,
+                       float(h2d), float(d2h)], device=dev, dtype=torch.float64)
+    mx = tm.clone()
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    sm = tm.clone()
+    dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+    ms = float(mx[0])
+    launches = (ctx.launches - launches0) // args.steps
+    bc_calls, bc_bytes = comm.counters(0)
+    a2a_calls, a2a_bytes = comm.counters(1)
+    if rank == 0:
+        peak, peak_kind = measured_peak_gbs()
+        nnz_c = int(sm[4])
+        step_bytes = bytes_alg(A.nnz, n, A.nnz, n, nnz_c, n, vs)
+        per_gpu = step_bytes / world / (ms / 1e3) / 1e9
+        value = 2.0 * total_flops / (ms / 1e3) / 1e9
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": sr.dtype, "data": "synthetic",
+            "config": {
+                "workload": f"C3: R-MAT scale {args.scale} ef {args.edge_factor} seed 1, C = A*A, {sr.name} {sr.dtype}",
+                "semiring": f"{sr.name}_{sr.dtype}", "n": n, "nnz_A": A.nnz, "multiplies": total_flops,
+                "nnz_C": nnz_c, "parallelism": ("2D SUMMA %dx%d" % (q, q)) if mode == "summa"
+                else "3D %dx%dx%d" % (layers, q, q),
+                "column_batches": nb, "relabel": "symmetric P*A*P^T (seed 7), flops and nnz(C) unchanged",
+                "l2": "inputs/outputs larger than L2; no flush"},
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "dist": {"ms_local_max": round(float(mx[1]), 3), "ms_merge_max": round(float(mx[2]), 3),
+                     "ms_exposed_bcast_max": round(float(mx[3]), 3),
+                     "ms_exposed_bcast_per_stage_mean": round(float(sm[3]) / world / max(1, nb * q), 4),
+                     "stages": q, "bcast_calls_rank0": bc_calls, "bcast_bytes_rank0": bc_bytes,
+                     "alltoallv_calls_rank0": a2a_calls, "alltoallv_bytes_rank0": a2a_bytes},
+            "roofline": {"bound": "hbm", "kernel": "whole local multiply per GPU",
+                         "achieved": round(per_gpu, 2), "peak": peak, "unit": "GB/s",
+                         "frac": round(per_gpu / peak, 5), "traffic": None, "peak_source": peak_kind,
+                         "algorithmic_bytes_per_step": step_bytes},
+            "e2e": None if args.no_e2e else {
+                "value": round(2.0 * total_flops / (float(mx[5]) / 1e3) / 1e9, 3), "unit": UNIT,
+                "h2d_bytes_per_step": int(sm[6]), "d2h_bytes_per_step": int(sm[7]),
+                "ms_per_step": round(float(mx[5]), 3), "steps": max(args.e2e_steps, 1)},
+            "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+    comm.close()
+    dist.barrier()
+    dist.destroy_process_group()
 
 
 # ----------------------------------------------------------- reference arm

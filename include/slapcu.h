@@ -93,6 +93,8 @@ typedef struct slapcu_ctx_s* slapcu_ctx;
 slapcu_status slapcu_ctx_create(slapcu_ctx* out, int device, void* stream);
 slapcu_status slapcu_ctx_destroy(slapcu_ctx ctx);
 slapcu_status slapcu_ctx_set_stream(slapcu_ctx ctx, void* stream);
+/* Waits for the context's stream and reports any deferred error. */
+slapcu_status slapcu_ctx_synchronize(slapcu_ctx ctx);
 const char* slapcu_ctx_last_error(slapcu_ctx ctx);
 const char* slapcu_status_name(slapcu_status s); /* "DimError", "ShapeError", ... */
 int slapcu_abi_version(void);
@@ -104,7 +106,13 @@ typedef enum {
     SLAPCU_OPT_LIGHT_NNZ_MAX = 2,     /* numeric: columns above this use the dense tile path */
     SLAPCU_OPT_LIGHT_FLOPS_MAX = 3,   /* symbolic: columns above this use the bitmap path   */
     SLAPCU_OPT_DETERMINISTIC = 4,     /* reserved */
-    SLAPCU_OPT_PROFILE = 5            /* 1: CUDA events around every launch, per-class device time */
+    SLAPCU_OPT_PROFILE = 5,           /* 1: CUDA events around every launch, per-class device time */
+    SLAPCU_OPT_DENSE_FLOPS_MIN = 6,   /* fused path: byte-flag tiles for columns with flops >= v
+                                         (-1 auto = nrows/4, 0 = off) */
+    SLAPCU_OPT_DENSE_TILE_ROWS_LOG2 = 7, /* byte-flag tile height (default 17 = 128 KB) */
+    SLAPCU_OPT_ASYNC_FINISH = 8       /* 1: slapcu_spgemm_finish returns without waiting; its
+                                         InternalError surfaces at the next call on the context
+                                         or at slapcu_ctx_synchronize */
 } slapcu_option;
 slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t value);
 

@@ -31,7 +31,8 @@ PLUS_TIMES_F64, PLUS_TIMES_F32, PLUS_TIMES_I64, MIN_PLUS_I32, MIN_PLUS_F64, OR_A
 # slapcu_alg
 ALG_HEAP, ALG_HASH, ALG_HYBRID = 0, 1, 2
 # slapcu_option
-OPT_TILE_ROWS_LOG2, OPT_SYM_TILE_ROWS_LOG2, OPT_LIGHT_NNZ_MAX, OPT_LIGHT_FLOPS_MAX, OPT_DETERMINISTIC, OPT_PROFILE = range(6)
+(OPT_TILE_ROWS_LOG2, OPT_SYM_TILE_ROWS_LOG2, OPT_LIGHT_NNZ_MAX, OPT_LIGHT_FLOPS_MAX, OPT_DETERMINISTIC, OPT_PROFILE,
+ OPT_DENSE_FLOPS_MIN, OPT_DENSE_TILE_ROWS_LOG2, OPT_ASYNC_FINISH) = range(9)
 NUM_KERNEL_CLASSES = 10
 KERNEL_CLASSES = ["other", "flops", "bin", "sym_light", "sym_heavy", "scan", "num_light", "num_heavy", "merge", "gen"]
 
@@ -89,6 +90,7 @@ SIGNATURES = [
     ("slapcu_ctx_create", _I, [C.POINTER(_P), _I, _P]),
     ("slapcu_ctx_destroy", _I, [_P]),
     ("slapcu_ctx_set_stream", _I, [_P, _P]),
+    ("slapcu_ctx_synchronize", _I, [_P]),
     ("slapcu_ctx_last_error", C.c_char_p, [_P]),
     ("slapcu_ctx_set_option", _I, [_P, _I, _L]),
     ("slapcu_ctx_kernel_launches", _L, [_P]),

@@ -22,6 +22,7 @@ slapcu_status guarded(slapcu_ctx ctx, F&& f) {
     if (!ctx) return SLAPCU_ERR_INVALID;
     try {
         SLAPCU_CUDA(cudaSetDevice(ctx->c.device));
+        ctx_settle(ctx->c);  // surface a deferred error of an asynchronous finish()
         f(ctx->c);
         ctx->c.last_error.clear();
         return SLAPCU_OK;
@@ -110,8 +111,13 @@ slapcu_status slapcu_ctx_destroy(slapcu_ctx ctx) {
     cudaStreamSynchronize(ctx->c.stream);
     for (auto& e : ctx->c.ev)
         if (e) cudaEventDestroy(e);
+    if (ctx->c.err_host) cudaFreeHost(ctx->c.err_host);
     delete ctx;
     return SLAPCU_OK;
+}
+
+slapcu_status slapcu_ctx_synchronize(slapcu_ctx ctx) {
+    return guarded(ctx, [&](Ctx& c) { SLAPCU_CUDA(cudaStreamSynchronize(c.stream)); });
 }
 
 slapcu_status slapcu_ctx_set_stream(slapcu_ctx ctx, void* stream) {
@@ -134,6 +140,12 @@ slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t v
         case SLAPCU_OPT_LIGHT_NNZ_MAX: c.opt.light_nnz_max = v; break;
         case SLAPCU_OPT_LIGHT_FLOPS_MAX: c.opt.light_flops_max = v; break;
         case SLAPCU_OPT_DETERMINISTIC: break;
+        case SLAPCU_OPT_DENSE_FLOPS_MIN: c.opt.dense_flops_min = v; break;
+        case SLAPCU_OPT_ASYNC_FINISH: c.opt.async_finish = v != 0; break;
+        case SLAPCU_OPT_DENSE_TILE_ROWS_LOG2:
+            require(v >= 10 && v <= 17, SLAPCU_ERR_INVALID, "dense tile rows log2 must be in 10..17");
+            c.opt.dense_tile_rows_log2 = (int)v;
+            break;
         case SLAPCU_OPT_PROFILE:
             prof_flush(c);
             c.prof.on = v != 0;

@@ -115,6 +115,12 @@ struct Options {
     int sym_tile_rows_log2 = 19;  // symbolic bitmap height
     int64_t light_nnz_max = 4096;     // numeric hash path if nnz <= this
     int64_t light_flops_max = 16384;  // symbolic hash path if flops <= this
+    // fused byte-flag path if flops >= this (-1 auto = nrows/4, 0 off).  Off by
+    // default: measured slower than the bitmap path at R-MAT s20 (8 row tiles
+    // of byte flags re-walk B per tile and the separate launch serialises).
+    int64_t dense_flops_min = 0;
+    int dense_tile_rows_log2 = 17;    // byte-flag tile height (128 KB of flags)
+    bool async_finish = false;        // finish() returns without waiting (errors surface later)
 };
 
 // Kernel classes for the per-class device-time breakdown (profiling mode).
@@ -154,6 +160,8 @@ struct Ctx {
     int num_sms = 0;
     Prof prof;
     int cur_cls = KC_OTHER;
+    int* err_host = nullptr;   // pinned, deferred error flag of an async finish()
+    bool err_pending = false;
     DevBuf err_flag;      // int
     DevBuf scratch_small; // misc small counters
     // merge state carried from merge_symbolic to merge_numeric
@@ -179,6 +187,7 @@ void spgemm_numeric(Ctx& c, const DevCsc& A, const DevCsc& B, int sr, int alg, c
 int64_t fused_begin(Ctx& c, const DevCsc& A, const DevCsc& B, int sr, int alg, int64_t* c_colptr,
                     int64_t staging_budget_bytes);
 void fused_finish(Ctx& c, const DevCsc& A, const DevCsc& B, int sr, int32_t* c_rowids, void* c_vals);
+void ctx_settle(Ctx& c);
 void any_zero_u8(Ctx& c, const uint8_t* v, int64_t n, int* flag);
 void dcsc_colptr(Ctx& c, int64_t ncols, int64_t nzc, const int32_t* jc, const int32_t* cp, int64_t* colptr);
 void exclusive_scan_i64(Ctx& c, const int64_t* in, int64_t* out, int64_t n);

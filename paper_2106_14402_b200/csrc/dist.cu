@@ -143,10 +143,24 @@ void local_multiply(Ctx& c, const DevCsc& A, const DevCsc& B, int sr, int alg, B
     out.nrows = A.nrows;
     out.ncols = B.ncols;
     out.cp.reset(sizeof(int64_t) * (B.ncols + 1), c.stream);
-    out.nnz = spgemm_symbolic(c, A, B, alg, out.cp.as<int64_t>());
+    // single product pass when its staging area fits in half the free memory,
+    // else the two-pass symbolic -> numeric contract
+    size_t fr = 0, tot = 0;
+    SLAPCU_CUDA(cudaMemGetInfo(&fr, &tot));
+    bool fused = true;
+    try {
+        out.nnz = fused_begin(c, A, B, sr, alg, out.cp.as<int64_t>(), int64_t(fr / 2));
+    } catch (const Fail& e) {
+        if (e.st != SLAPCU_ERR_BUDGET) throw;
+        fused = false;
+        out.nnz = spgemm_symbolic(c, A, B, alg, out.cp.as<int64_t>());
+    }
     out.rw.reset(sizeof(int32_t) * std::max<int64_t>(out.nnz, 1), c.stream);
     out.v.reset(size_t(vs) * std::max<int64_t>(out.nnz, 1), c.stream);
-    spgemm_numeric(c, A, B, sr, alg, out.cp.as<int64_t>(), out.rw.as<int32_t>(), out.v.get());
+    if (fused)
+        fused_finish(c, A, B, sr, out.rw.as<int32_t>(), out.v.get());
+    else
+        spgemm_numeric(c, A, B, sr, alg, out.cp.as<int64_t>(), out.rw.as<int32_t>(), out.v.get());
     *ms += c.sym_ms + c.num_ms;
 }
 

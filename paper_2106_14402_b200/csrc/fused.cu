@@ -171,11 +171,14 @@ __global__ void __launch_bounds__(NT)
         const int nch = (W + 31) >> 5;
         smem_zero(bm, W);
         __syncthreads();
+        const int t0i = (int)t0;
+        unsigned* bmp = bm;
         walk_balanced<4>(A, B, bs, be, sg, t, ntiles, (int)(t0 + rows), cursor + (t & 1) * B.span,
-                         cursor + ((t + 1) & 1) * B.span, int64_t(4) * NT, ws, [&](int64_t, int64_t, int r) {
-                             const int rr = r - (int)t0;
-                             atomicOr(&bm[rr >> 5], 1u << (rr & 31));
-                         });
+                         cursor + ((t + 1) & 1) * B.span, int64_t(4) * NT, ws,
+                         per_product([bmp, t0i](int64_t, int64_t, int r) {
+                             const int rr = r - t0i;
+                             atomicOr(&bmp[rr >> 5], 1u << (rr & 31));
+                         }));
         for (int c = warp; c < nch; c += NW) {
             const int w = c * 32 + lane;
             int x = w < W ? __popc(bm[w]) : 0;
@@ -206,6 +209,92 @@ __global__ void __launch_bounds__(NT)
         for (int c = warp; c < nch; c += NW) {
             const int w = c * 32 + lane;
             emit_rows_coalesced(w < W ? bm[w] : 0u, (int)t0 + (w << 5), srows + off + chunk[c], lane);
+        }
+        total += tot_sh;
+        __syncthreads();
+    }
+    if (tid == 0) cnt[j] = total;
+}
+
+// ------------------------------------------------------- K1 heavy, byte flags
+
+// For the heaviest columns (flops >> rows per tile) the per-product shared
+// atomic of k_fused_heavy is the bottleneck (ncu: ~10 L1 wavefronts per warp
+// ATOMS).  Here a product is a plain byte store flags[row] = 1 (benign races:
+// every writer stores the same value), and the pattern is recovered by
+// scanning the tile's flag bytes twice (chunk counts, then coalesced emit +
+// clear).  Tiles of 2^tile_log2 rows of byte flags (128 KB at 2^17), one CTA
+// of NT threads per column.  Output = staging segments exactly like
+// k_fused_heavy (seg index = column slot * T + tile).
+__device__ __forceinline__ unsigned byte_mask16(uint4 v) {
+    // flags are exactly 0 or 1: gather byte k's low bit into bit k
+    auto m4 = [](unsigned x) { return (x & 1u) | ((x >> 7) & 2u) | ((x >> 14) & 4u) | ((x >> 21) & 8u); };
+    return m4(v.x) | (m4(v.y) << 4) | (m4(v.z) << 8) | (m4(v.w) << 12);
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT)
+    k_fused_dense(DevCsc A, DevCsc B, const int* __restrict__ cols, int n, const int64_t* __restrict__ flops,
+                  int tile_log2, int32_t* __restrict__ cursor, int64_t* __restrict__ cnt, int32_t* __restrict__ srows,
+                  unsigned long long* __restrict__ scur, int64_t* __restrict__ seg_off, int* __restrict__ seg_cnt,
+                  int T) {
+    extern __shared__ __align__(16) unsigned char flags[];
+    const int64_t R = int64_t(1) << tile_log2;
+    int* chunk = reinterpret_cast<int*>(flags + R);  // [R/512] chunk bases
+    __shared__ unsigned long long off_sh;
+    __shared__ int tot_sh;
+    __shared__ WalkShared ws;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = NT / 32;
+    const int j = cols[blockIdx.x];
+    const int64_t bs = B.cp[j], be = B.cp[j + 1];
+    const int sg = pick_sg(flops[j], be - bs, 32);
+    const int ntiles = (int)((A.nrows + R - 1) >> tile_log2);
+    smem_zero(reinterpret_cast<unsigned*>(flags), (int)(R >> 2));
+    __syncthreads();
+    long long total = 0;
+    for (int t = 0; t < ntiles; ++t) {
+        const int64_t t0 = int64_t(t) << tile_log2;
+        const int64_t rows = min(R, A.nrows - t0);
+        const int nch = (int)((rows + 511) >> 9);  // 512-byte chunks (32 lanes x 16 B)
+        const int t0i = (int)t0;
+        unsigned char* fl = flags;
+        walk_balanced<4>(A, B, bs, be, sg, t, ntiles, (int)(t0 + rows), cursor + (t & 1) * B.span,
+                         cursor + ((t + 1) & 1) * B.span, int64_t(4) * NT, ws,
+                         per_product([fl, t0i](int64_t, int64_t, int r) { fl[r - t0i] = 1; }));
+        const uint4* f4 = reinterpret_cast<const uint4*>(flags);
+        for (int c = warp; c < nch; c += NW) {
+            int x = __popc(byte_mask16(f4[c * 32 + lane]));
+            x = warp_reduce_sum(x);
+            if (lane == 0) chunk[c] = x;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            int run = 0;
+            for (int b0 = 0; b0 < nch; b0 += 32) {
+                const int c = b0 + lane;
+                const int x = c < nch ? chunk[c] : 0;
+                int tot;
+                const int ex = warp_excl_scan(x, lane, &tot);
+                if (c < nch) chunk[c] = run + ex;
+                run += tot;
+            }
+            if (lane == 0) {
+                tot_sh = run;
+                const unsigned long long off = atomicAdd(scur, (unsigned long long)run);
+                off_sh = off;
+                seg_off[int64_t(blockIdx.x) * T + t] = (int64_t)off;
+                seg_cnt[int64_t(blockIdx.x) * T + t] = run;
+            }
+        }
+        __syncthreads();
+        const int64_t off = (int64_t)off_sh;
+        uint4* fw = reinterpret_cast<uint4*>(flags);
+        for (int c = warp; c < nch; c += NW) {
+            const uint4 v = fw[c * 32 + lane];
+            const unsigned m = byte_mask16(v);
+            emit_rows_coalesced(m, t0i + c * 512 + lane * 16, srows + off + chunk[c], lane);
+            if (m) fw[c * 32 + lane] = make_uint4(0u, 0u, 0u, 0u);  // clear for the next tile
         }
         total += tot_sh;
         __syncthreads();
@@ -256,6 +345,42 @@ __global__ void __launch_bounds__(256)
 
 // ----------------------------------------------------------------------- K3
 
+// Value accumulation for a batch of U products of one B entry: all U value
+// loads are issued before any rank lookup / atomic, so the A-value gathers
+// overlap like the row-id gathers do.
+template <int SRID>
+struct ValueBatch {
+    using S_ = Sr<SRID>;
+    using T = typename S_::T;
+    using Acc = typename S_::Acc;
+    const T* __restrict__ Av;
+    const T* __restrict__ Bv;
+    const unsigned* bm;
+    const uint16_t* pre16;
+    const int* chunk;
+    Acc* vals;
+    int r_lo;
+    template <int U>
+    __device__ __forceinline__ void batch(int64_t p, int width, int64_t i, const int* r, int ok) {
+        if (!ok) return;  // bit 0 set whenever any bit is (the batch stops at the first miss)
+        const T bv = Bv[i];
+        T av[U];
+        // unpredicated loads (a lane past the batch end re-reads position p)
+        // so the compiler issues all U before the first use
+#pragma unroll
+        for (int u = 0; u < U; ++u) av[u] = Av[(ok & (1 << u)) ? p + int64_t(u) * width : p];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (ok & (1 << u)) {
+                const int rr = r[u] - r_lo;
+                const int w = rr >> 5;
+                const int idx = chunk[w >> 5] + pre16[w] + __popc(bm[w] & ((1u << (rr & 31)) - 1u));
+                S_::atomic_acc(&vals[idx], S_::mul(av[u], bv));
+            }
+        }
+    }
+};
+
 // Values of heavy columns for semirings with values: per row tile the bitmap
 // is rebuilt from C's (sorted) rows, popcount prefixes give every row its
 // rank, one pass over the products accumulates at rank in shared memory (or
@@ -274,8 +399,8 @@ __global__ void __launch_bounds__(NT)
     const int WMAX = (int)(R >> 5);
     Acc* vals = reinterpret_cast<Acc*>(sm_raw);
     unsigned* bm = reinterpret_cast<unsigned*>(sm_raw + sizeof(Acc) * cap);
-    int* pre = reinterpret_cast<int*>(bm + WMAX);
-    int* chunk = pre + WMAX;
+    int* chunk = reinterpret_cast<int*>(bm + WMAX);                    // [WMAX/32]
+    uint16_t* pre16 = reinterpret_cast<uint16_t*>(chunk + WMAX / 32);  // [WMAX]
     __shared__ int tot_sh;
     __shared__ int64_t hi_sh;
     __shared__ WalkShared ws;
@@ -319,7 +444,7 @@ __global__ void __launch_bounds__(NT)
             atomicOr(&bm[rr >> 5], 1u << (rr & 31));
         }
         __syncthreads();
-        const int tile_nnz = bitmap_ranks(bm, pre, chunk, W, &tot_sh);
+        const int tile_nnz = bitmap_ranks16(bm, pre16, chunk, W, &tot_sh);
         if (tile_nnz != hi - lo) {
             if (tid == 0) atomicExch(err, 1);
             return;
@@ -327,19 +452,22 @@ __global__ void __launch_bounds__(NT)
         for (int i = tid; i < tile_nnz; i += NT) vals[i] = S_::identity();
         __syncthreads();
         // ntiles = 2 selects the cursor-driven walk (chunk count is data dependent)
-        walk_balanced<4>(A, B, bs, be, sg, t, 2, r_hi, cursor + (t & 1) * B.span, cursor + ((t + 1) & 1) * B.span,
-                         int64_t(4) * NT, ws, [&](int64_t p, int64_t i, int r) {
-                             const int rr = r - r_lo;
-                             const int w = rr >> 5;
-                             const int idx = pre[w] + __popc(bm[w] & ((1u << (rr & 31)) - 1u));
-                             S_::atomic_acc(&vals[idx], S_::mul(Av[p], Bv[i]));
-                         });
+        walk_balanced<8>(A, B, bs, be, sg, t, 2, r_hi, cursor + (t & 1) * B.span, cursor + ((t + 1) & 1) * B.span,
+                         int64_t(8) * NT, ws, ValueBatch<SRID>{Av, Bv, bm, pre16, chunk, vals, r_lo});
         for (int i = tid; i < tile_nnz; i += NT) Cv[lo + i] = S_::out(vals[i]);
         lo = hi;
         r_lo = r_hi;
         __syncthreads();
     }
     if (tid == 0 && lo != ce) atomicExch(err, 1);
+}
+
+__global__ void k_count_ge(int n, const int* __restrict__ list, const int64_t* __restrict__ flops, int64_t thr,
+                           int* __restrict__ out) {
+    int c = 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) c += flops[list[i]] >= thr;
+    c = warp_reduce_sum(c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
 }
 
 // Staging bound: sum_j min(flops_j, nrows) (entries any column can produce).
@@ -357,7 +485,7 @@ __global__ void k_stage_bound(int64_t n, const int64_t* __restrict__ flops, int6
 namespace {
 
 constexpr int kFusedHeavyThreads = 512;
-constexpr int kValuesThreads = 512;
+constexpr int kValuesThreads = 1024;
 
 template <int SRID, bool ONES, int LOG2S, int G, int CPB>
 void launch_fused_light(Ctx& c, const DevCsc& A, const DevCsc& B, const int* list, int n, const int64_t* flops,
@@ -404,6 +532,7 @@ int64_t fused_begin(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int alg,
     resolve(c, A);
     resolve(c, B);
     if ((A.span && !A.v) || (B.span && !B.v)) throw Fail{SLAPCU_ERR_INVALID, "operand values are null"};
+    ctx_settle(c);  // the previous finish() on this context may still be running
     SLAPCU_CUDA(cudaEventRecord(c.ev[0], c.stream));
     FusedState& f = c.fused;
     f.valid = false;
@@ -458,10 +587,27 @@ int64_t fused_begin(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int alg,
     const int nheavy = f.bins.count[spec.nlight];
     f.nlight_bins = spec.nlight;
     f.tile_log2 = heavy_tile_log2(c.opt.sym_tile_rows_log2, A.nrows);
-    f.T = (int)((A.nrows + (int64_t(1) << f.tile_log2) - 1) >> f.tile_log2);
+    const int tb = (int)((A.nrows + (int64_t(1) << f.tile_log2) - 1) >> f.tile_log2);
+    // byte-flag path for the heaviest columns (the heavy list is sorted by
+    // flops, descending, so they are its first `ndense` entries)
+    const int dense_log2 = heavy_tile_log2(std::min(c.opt.dense_tile_rows_log2, 17), A.nrows);
+    const int td = (int)((A.nrows + (int64_t(1) << dense_log2) - 1) >> dense_log2);
+    int ndense = 0;
+    const int64_t dthr = c.opt.dense_flops_min < 0 ? std::max<int64_t>(A.nrows / 4, 1) : c.opt.dense_flops_min;
+    if (nheavy && c.opt.dense_flops_min != 0) {
+        DevBuf nd(sizeof(int), c.stream);
+        SLAPCU_CUDA(cudaMemsetAsync(nd.get(), 0, sizeof(int), c.stream));
+        KScope ks(c, KC_BIN);
+        launch(c, k_count_ge, dim3(grid_for(c, nheavy, 256)), dim3(256), 0, nheavy, L + f.bins.offset[spec.nlight],
+               flops, dthr, nd.as<int>());
+        SLAPCU_CUDA(cudaMemcpyAsync(&ndense, nd.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+        SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+    }
+    f.T = std::max(tb, ndense ? td : 1);
     if (nheavy) {
         f.seg_off.reset(sizeof(int64_t) * int64_t(nheavy) * std::max(f.T, 1), c.stream);
         f.seg_cnt.reset(sizeof(int) * int64_t(nheavy) * std::max(f.T, 1), c.stream);
+        SLAPCU_CUDA(cudaMemsetAsync(f.seg_cnt.get(), 0, sizeof(int) * int64_t(nheavy) * std::max(f.T, 1), c.stream));
     }
     dispatch_sr(sr, [&](auto id) {
         constexpr int ID = decltype(id)::value;
@@ -479,15 +625,36 @@ int64_t fused_begin(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int alg,
             }
         }
     });
-    if (nheavy) {
+    const int* HL = L + f.bins.offset[spec.nlight];
+    if (ndense) {
+        KScope ks(c, KC_SYM_HEAVY);
+        const size_t R = size_t(1) << dense_log2;
+        const size_t smem = R + (R / 512) * 4 + 16;
+        auto k = k_fused_dense<1024>;
+        ensure_smem(k, smem);
+        launch(c, k, dim3(ndense), dim3(1024), smem, A, B, HL, ndense, flops, dense_log2,
+               c.plan.cursor.as<int32_t>(), f.cnt.as<int64_t>(), f.srows.as<int32_t>(),
+               f.scur.as<unsigned long long>(), f.seg_off.as<int64_t>(), f.seg_cnt.as<int>(), f.T);
+    }
+    if (nheavy > ndense) {
         KScope ks(c, KC_SYM_HEAVY);
         const size_t W = size_t(1) << (f.tile_log2 - 5);
         const size_t smem = W * 4 + ((W + 31) / 32) * 4 + 16;
-        auto k = k_fused_heavy<kFusedHeavyThreads>;
-        ensure_smem(k, smem);
-        launch(c, k, dim3(nheavy), dim3(kFusedHeavyThreads), smem, A, B, L + f.bins.offset[spec.nlight], nheavy,
-               flops, f.tile_log2, c.plan.cursor.as<int32_t>(), f.cnt.as<int64_t>(), f.srows.as<int32_t>(),
-               f.scur.as<unsigned long long>(), f.seg_off.as<int64_t>(), f.seg_cnt.as<int>(), f.T);
+        const int nb = nheavy - ndense;
+        // segment slots continue after the dense columns'
+        int64_t* so = f.seg_off.as<int64_t>() + int64_t(ndense) * f.T;
+        int* sc = f.seg_cnt.as<int>() + int64_t(ndense) * f.T;
+        // a bitmap above ~96 KB leaves room for one CTA per SM: give it 1024 threads
+        auto go = [&](auto k, int nt) {
+            ensure_smem(k, smem);
+            launch(c, k, dim3(nb), dim3(nt), smem, A, B, HL + ndense, nb, flops, f.tile_log2,
+                   c.plan.cursor.as<int32_t>(), f.cnt.as<int64_t>(), f.srows.as<int32_t>(),
+                   f.scur.as<unsigned long long>(), so, sc, f.T);
+        };
+        if (smem > 96 * 1024)
+            go(k_fused_heavy<1024>, 1024);
+        else
+            go(k_fused_heavy<kFusedHeavyThreads>, kFusedHeavyThreads);
     }
     {
         KScope ks(c, KC_SCAN);
@@ -555,13 +722,14 @@ void fused_finish(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int32_t* c
                 KScope ks2(c, KC_NUM_HEAVY);
                 // bitmap + ranks for up to 2^17 rows, the rest of ~113 KB (two
                 // CTAs per SM) holds the chunk's values
-                const int tl = heavy_tile_log2(std::min(c.opt.tile_rows_log2, 17), A.nrows);
+                // One CTA of 1024 threads per SM: bitmap + 16-bit ranks for up to
+                // 2^19 rows (98 KB) and the rest of the SM's shared memory for
+                // the chunk's values, so a heavy column needs few chunks (each
+                // chunk re-walks the column's B entries).
+                const int tl = heavy_tile_log2(std::min(c.opt.tile_rows_log2 + 1, 19), A.nrows);
                 const size_t W = size_t(1) << (tl - 5);
-                const size_t fixed = W * 8 + ((W + 31) / 32) * 4 + 64;
-                // 112 KB: two CTAs per SM once the per-CTA reserved 1 KB and the
-                // static shared state are added (228 KB per SM)
-                size_t budget = std::min<size_t>(size_t(c.smem_optin), size_t(108) * 1024);
-                if (budget < fixed + 1024 * sizeof(Acc)) budget = size_t(c.smem_optin);
+                const size_t fixed = W * 4 + ((W + 31) / 32) * 4 + W * 2 + 64;
+                const size_t budget = size_t(c.smem_optin) - 8 * 1024;  // static state + reserve
                 // multiple of 4 entries keeps the bitmap behind the values 16-byte aligned
                 const int cap = (int)((budget - fixed) / sizeof(Acc)) & ~3;
                 const size_t smem = fixed + size_t(cap) * sizeof(Acc);
@@ -572,13 +740,22 @@ void fused_finish(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int32_t* c
             }
         }
     });
-    int herr = 0;
-    SLAPCU_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    if (!c.err_host) SLAPCU_CUDA(cudaMallocHost((void**)&c.err_host, sizeof(int)));
+    SLAPCU_CUDA(cudaMemcpyAsync(c.err_host, err, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
     SLAPCU_CUDA(cudaEventRecord(c.ev[3], c.stream));
+    c.err_pending = true;
+    if (!c.opt.async_finish) ctx_settle(c);
+}
+
+// Completes an asynchronous finish(): waits for the context stream and raises
+// the deferred InternalError, if any.
+void ctx_settle(Ctx& c) {
+    if (!c.err_pending) return;
+    c.err_pending = false;
     SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
     cudaEventElapsedTime(&c.num_ms, c.ev[2], c.ev[3]);
     prof_flush(c);
-    if (herr) throw Fail{SLAPCU_ERR_INTERNAL, "numeric column nnz disagrees with symbolic count"};
+    if (*c.err_host) throw Fail{SLAPCU_ERR_INTERNAL, "numeric column nnz disagrees with symbolic count"};
 }
 
 }  // namespace slapcu

@@ -186,6 +186,22 @@ __device__ __forceinline__ void walk_tile_ilp(const DevCsc& A, const DevCsc& B, 
     }
 }
 
+// Batch functor adapting a per-product callable f(p, i, row).
+template <class F>
+struct PerProduct {
+    F f;
+    template <int U>
+    __device__ __forceinline__ void batch(int64_t p, int width, int64_t i, const int* r, int ok) {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (ok & (1 << u)) f(p + int64_t(u) * width, i, r[u]);
+    }
+};
+template <class F>
+__device__ __forceinline__ PerProduct<F> per_product(F f) {
+    return PerProduct<F>{f};
+}
+
 // Products of ONE B entry i (A column k, entries [start, ae)) restricted to
 // rows < t1, walked by `width` threads of which this is thread `sl`, U loads
 // in flight per thread.  Returns nothing; writes the tile cursor through
@@ -203,15 +219,19 @@ __device__ __forceinline__ void walk_entry(const int32_t* __restrict__ Arw, int6
             const int64_t q = p + int64_t(u) * width;
             r[u] = q < ae ? __ldg(&Arw[q]) : INT_MAX;
         }
+        // hand the whole batch to f so it can issue its own dependent loads
+        // (values) for all U products before consuming any of them
+        int ok = 0;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if (stop < 0) {
                 if (r[u] < t1)
-                    f(p + int64_t(u) * width, i, r[u]);
+                    ok |= 1 << u;
                 else
                     stop = p + int64_t(u) * width;
             }
         }
+        f.template batch<U>(p, width, i, r, ok);
         p += int64_t(U) * width;
     }
     if (cur_out_i) {
@@ -225,7 +245,7 @@ __device__ __forceinline__ void walk_entry(const int32_t* __restrict__ Arw, int6
 struct WalkShared {
     int next;      // dynamic hand-out of short entries
     int nlong;     // long entries collected this round
-    int list[512];  // their B positions (relative to bs)
+    int list[1024];  // their B positions (relative to bs); >= blockDim.x
 };
 
 // Load-balanced walk of all products of column j inside one row tile.  A
@@ -236,7 +256,7 @@ struct WalkShared {
 // products are walked by the whole CTA cooperatively (collected NT at a time
 // into shared memory), and the others are handed out to sub-groups of sg
 // lanes through a shared atomic counter.  Must be called by all threads of
-// the CTA (contains barriers); NT <= 512.
+// the CTA (contains barriers); NT <= 1024.
 template <int U, class F>
 __device__ __forceinline__ void walk_balanced(const DevCsc& A, const DevCsc& B, int64_t bs, int64_t be, int sg,
                                               int t, int ntiles, int t1, const int32_t* __restrict__ cur_in,
@@ -346,6 +366,38 @@ __device__ __forceinline__ int bitmap_ranks(const unsigned* __restrict__ bm, int
     }
     __syncthreads();
     for (int w = tid; w < W; w += blockDim.x) pre[w] += chunk[w >> 5];
+    __syncthreads();
+    return *total_sh;
+}
+
+// bitmap_ranks with half the rank storage: pre16[w] is the exclusive prefix
+// inside w's 32-word chunk (<= 992, fits 16 bits) and chunk[c] the chunk
+// base, so rank(row) = chunk[w>>5] + pre16[w] + popc(low bits of bm[w]).
+__device__ __forceinline__ int bitmap_ranks16(const unsigned* __restrict__ bm, uint16_t* __restrict__ pre16,
+                                              int* __restrict__ chunk, int W, int* total_sh) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    const int nch = (W + 31) >> 5;
+    for (int c = warp; c < nch; c += nw) {
+        const int w = c * 32 + lane;
+        const int x = w < W ? __popc(bm[w]) : 0;
+        int tot;
+        const int ex = warp_excl_scan(x, lane, &tot);
+        if (w < W) pre16[w] = (uint16_t)ex;
+        if (lane == 0) chunk[c] = tot;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        int run = 0;
+        for (int b0 = 0; b0 < nch; b0 += 32) {
+            const int c = b0 + lane;
+            const int x = c < nch ? chunk[c] : 0;
+            int tot;
+            const int ex = warp_excl_scan(x, lane, &tot);
+            if (c < nch) chunk[c] = run + ex;
+            run += tot;
+        }
+        if (lane == 0) *total_sh = run;
+    }
     __syncthreads();
     return *total_sh;
 }

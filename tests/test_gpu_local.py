@@ -141,6 +141,7 @@ def test_multi_tile_paths(port, sr):
     ctx.set_option(L.OPT_SYM_TILE_ROWS_LOG2, 10)
     ctx.set_option(L.OPT_LIGHT_NNZ_MAX, 16)
     ctx.set_option(L.OPT_LIGHT_FLOPS_MAX, 32)
+    ctx.set_option(L.OPT_DENSE_TILE_ROWS_LOG2, 10)
     da = to_device(a)
     for alg in ALGS:
         for method in METHODS:
@@ -201,6 +202,25 @@ def test_thread_count_invariance(port):
     for t in (2, 4, 8):
         c = P.local_spgemm(da, da, P.PlusTimesI64, threads=t).to_host()
         assert np.array_equal(c.rowids, base.rowids) and np.array_equal(c.vals, base.vals)
+
+
+@pytest.mark.parametrize("dense_min", [0, 1, -1])
+def test_fused_pattern_paths(port, dense_min):
+    """Fused pattern pass: bitmap-atomic path only (0), byte-flag path for
+    every heavy column (1), automatic split (-1)."""
+    a = with_values(port, port.gen_rmat(12), oracle.MIN_PLUS_I32)
+    want = port.spgemm(oracle.MIN_PLUS_I32, a, a)
+    ctx = P.Context()
+    ctx.set_option(L.OPT_DENSE_FLOPS_MIN, dense_min)
+    ctx.set_option(L.OPT_DENSE_TILE_ROWS_LOG2, 11)
+    da = to_device(a)
+    for sr, w in ((P.MinPlusI32, want),):
+        got = P.local_spgemm(da, da, sr, ctx=ctx)
+        assert_parity(got, w, sr.id, f"dense_min={dense_min}")
+    ab = a.with_vals(np.ones(a.nnz, np.uint8))
+    wb = port.spgemm(oracle.OR_AND_U8, ab, ab)
+    got = P.local_spgemm(to_device(ab), to_device(ab), P.OrAnd, ctx=ctx)
+    assert_parity(got, wb, oracle.OR_AND_U8, f"bool dense_min={dense_min}")
 
 
 def test_column_window_operand(port):

@@ -1,0 +1,21 @@
+"""The reference-side C++ binding (include/slapcu_slap.hpp) on the GPU: the
+prebuilt build/shim_test (compiled against the reference headers by
+__graft_entry__.build(); the headers do not exist on the GPU box) runs the
+reference template and the drop-in side by side and prints SHIM_OK."""
+import os
+import subprocess
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BIN = os.path.join(ROOT, "build", "shim_test")
+
+
+@pytest.mark.skipif(not torch.cuda.is_available(), reason="no CUDA device")
+@pytest.mark.skipif(not os.path.exists(BIN), reason="build/shim_test not built (needs the reference headers)")
+def test_cpp_dropin_matches_reference():
+    r = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "SHIM_OK" in r.stdout, r.stdout + r.stderr
