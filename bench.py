@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--sym-tile-log2", type=int, default=0, help="row-tile height of the pattern bitmap (0 = default)")
     ap.add_argument("--tile-log2", type=int, default=0, help="row-tile height of the value pass (0 = default)")
     ap.add_argument("--dense-min", type=int, default=None, help="byte-flag pattern path for flops >= this (0 off)")
+    ap.add_argument("--streams", type=int, default=1, choices=[1, 2],
+                    help="2: alternate column batches over two contexts/streams (async finish)")
     return ap.parse_args()
 
 
@@ -219,10 +221,15 @@ def run_ours(args):
     # pass) is still in flight -- slapcu_spgemm_finish is asynchronous
     # (SLAPCU_OPT_ASYNC_FINISH) and the next begin() on the same context
     # settles it.  Each context owns its staging area and output buffers.
-    stream2 = torch.cuda.Stream(device=dev)
-    ctxs = [ctx, P.Context(0, stream2)]
-    apply_options(ctxs[1], args)
-    streams = [stream, stream2]
+    if args.streams == 2:
+        stream2 = torch.cuda.Stream(device=dev)
+        ctxs = [ctx, P.Context(0, stream2)]
+        apply_options(ctxs[1], args)
+        streams = [stream, stream2]
+    else:
+        stream2 = stream
+        ctxs = [ctx]
+        streams = [stream]
     outs = []
     for cx in ctxs:
         cx.set_option(L.OPT_ASYNC_FINISH, 1)
@@ -240,8 +247,8 @@ def run_ours(args):
 
     def step(collect=None):
         for bi, w in enumerate(wins):
-            cx = ctxs[bi % 2]
-            o_cp, o_rw, o_v = outs[bi % 2]
+            cx = ctxs[bi % len(ctxs)]
+            o_cp, o_rw, o_v = outs[bi % len(ctxs)]
             nz = C.c_int64()
             cx.check(lib.slapcu_spgemm_begin(cx.h, C.byref(av), C.byref(w), sr.id, P.SpGemmAlg.hybrid, 0,
                                              o_cp.data_ptr(), C.byref(nz)), "begin")
@@ -273,7 +280,8 @@ def run_ours(args):
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in streams]
     torch.cuda.synchronize()
     ev0.record(stream)
-    stream2.wait_event(ev0)
+    if stream2 is not stream:
+        stream2.wait_event(ev0)
     for _ in range(args.steps):
         step()
     for e, s in zip(ev1, streams):

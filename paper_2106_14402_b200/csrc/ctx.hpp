@@ -105,7 +105,7 @@ struct FusedState {
     int64_t ncols = -1, nnz = 0;
     const int64_t* colptr = nullptr;
     bool ones = false;
-    DevBuf srows, svals, cnt, soff, scur, seg_off, seg_cnt;
+    DevBuf srows, svals, cnt, soff, scur, seg_off, seg_cnt, items;
     Bins bins;
     int nlight_bins = 0, tile_log2 = 0, T = 0;
 };

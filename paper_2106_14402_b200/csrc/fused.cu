@@ -462,6 +462,163 @@ __global__ void __launch_bounds__(NT)
     if (tid == 0 && lo != ce) atomicExch(err, 1);
 }
 
+// ---------------------------------------------------- K3 as independent items
+
+// One work item of the value pass: rows [r_lo, r_hi) of column `col`, whose
+// output entries are C[lo, hi) (at most cap of them, at most R rows).
+struct VItem {
+    int col, r_lo, r_hi, pad;
+    int64_t lo, hi;
+};
+
+// Cuts every heavy column's output into items (one thread per column; C's
+// rows are sorted, so the boundaries are binary searches in C itself).
+// fill == false: counts items per column into nit[h]; fill == true: writes
+// them at items[off[h] ...].
+// Columns with at most `split_flops` multiplies become ONE whole-column item
+// (pad = 1: the CTA walks all its chunks with tile cursors, no searches);
+// heavier ones are cut into independent single-chunk items (pad = 0).
+__global__ void k_values_plan(const int* __restrict__ cols, int n, const int64_t* __restrict__ Ccp,
+                              const int32_t* __restrict__ Crw, int64_t nrows, int64_t R, int cap, bool fill,
+                              int64_t* __restrict__ nit, const int64_t* __restrict__ off, VItem* __restrict__ items,
+                              const int64_t* __restrict__ flops, int64_t split_flops) {
+    for (int h = blockIdx.x * blockDim.x + threadIdx.x; h < n; h += gridDim.x * blockDim.x) {
+        const int j = cols[h];
+        const int64_t ce = Ccp[j + 1];
+        if (flops[j] <= split_flops) {
+            if (fill) items[off[h]] = VItem{j, 0, (int)nrows, 1, Ccp[j], ce};
+            else nit[h] = 1;
+            continue;
+        }
+        int64_t lo = Ccp[j];
+        int r_lo = 0;
+        int64_t k = 0;
+        while (lo < ce) {
+            const int64_t e_cap = lo + cap;
+            const int64_t r_cand = e_cap < ce ? (int64_t)Crw[e_cap] : nrows;
+            const int r_hi = (int)min(min(r_cand, int64_t(r_lo) + R), nrows);
+            int64_t a = lo, b = min(ce, e_cap);
+            while (a < b) {
+                const int64_t mid = (a + b) >> 1;
+                if (Crw[mid] < r_hi)
+                    a = mid + 1;
+                else
+                    b = mid;
+            }
+            if (a > lo) {  // skip row ranges without output (no products either)
+                if (fill) items[off[h] + k] = VItem{j, r_lo, r_hi, 0, lo, a};
+                ++k;
+            }
+            lo = a;
+            r_lo = r_hi;
+        }
+        if (!fill) nit[h] = k;
+    }
+}
+
+// One CTA per item: bitmap of the item's output rows (from C), 16-bit
+// popcount ranks, values accumulated at rank in shared memory over all
+// products with rows in [r_lo, r_hi) (start positions by binary search, so
+// items of one column are independent and spread over SMs -- the heaviest
+// column no longer serialises on one SM).
+template <int SRID, int NT>
+__global__ void __launch_bounds__(NT)
+    k_values_items(DevCsc A, DevCsc B, const VItem* __restrict__ items, const int64_t* __restrict__ flops,
+                   const int32_t* __restrict__ Crw, typename Sr<SRID>::T* __restrict__ Cv, int tile_log2, int cap,
+                   int32_t* __restrict__ cursor, int* __restrict__ err) {
+    using S_ = Sr<SRID>;
+    using T = typename S_::T;
+    using Acc = typename S_::Acc;
+    extern __shared__ __align__(16) unsigned char sm_raw[];
+    const int64_t R = int64_t(1) << tile_log2;
+    const int WMAX = (int)(R >> 5);
+    Acc* vals = reinterpret_cast<Acc*>(sm_raw);
+    unsigned* bm = reinterpret_cast<unsigned*>(sm_raw + ((sizeof(Acc) * size_t(cap) + 15) & ~size_t(15)));
+    int* chunk = reinterpret_cast<int*>(bm + WMAX);
+    uint16_t* pre16 = reinterpret_cast<uint16_t*>(chunk + WMAX / 32);
+    __shared__ int tot_sh, rhi_sh;
+    __shared__ int64_t hi_sh;
+    __shared__ WalkShared ws;
+    const int tid = threadIdx.x;
+    const T* Av = static_cast<const T*>(A.v);
+    const T* Bv = static_cast<const T*>(B.v);
+    const VItem it = items[blockIdx.x];
+    const int j = it.col;
+    const int64_t bs = B.cp[j], be = B.cp[j + 1];
+    const int sg = pick_sg(flops[j], be - bs, 32);
+    const int32_t* Arw = A.rw;
+    const bool whole = it.pad == 1;  // all chunks of the column here, tile cursors between chunks
+    int64_t lo = it.lo;
+    int r_lo = it.r_lo;
+    for (int t = 0; lo < it.hi; ++t) {
+        int64_t hi;
+        int r_hi;
+        if (whole) {
+            if (tid == 0) {
+                const int64_t e_cap = lo + cap;
+                const int64_t r_cand = e_cap < it.hi ? (int64_t)Crw[e_cap] : A.nrows;
+                const int rh = (int)min(min(r_cand, int64_t(r_lo) + R), A.nrows);
+                int64_t a = lo, b = min(it.hi, e_cap);
+                while (a < b) {
+                    const int64_t mid = (a + b) >> 1;
+                    if (Crw[mid] < rh)
+                        a = mid + 1;
+                    else
+                        b = mid;
+                }
+                hi_sh = a;
+                rhi_sh = rh;
+            }
+            __syncthreads();
+            hi = hi_sh;
+            r_hi = rhi_sh;
+        } else {
+            hi = it.hi;
+            r_hi = it.r_hi;
+        }
+        const int W = (r_hi - r_lo + 31) >> 5;
+        smem_zero(bm, W);
+        __syncthreads();
+        for (int64_t e = lo + tid; e < hi; e += NT) {
+            const int rr = Crw[e] - r_lo;
+            atomicOr(&bm[rr >> 5], 1u << (rr & 31));
+        }
+        __syncthreads();
+        const int tile_nnz = bitmap_ranks16(bm, pre16, chunk, W, &tot_sh);
+        if (tile_nnz != hi - lo) {
+            if (tid == 0) atomicExch(err, 1);
+            return;
+        }
+        for (int i = tid; i < tile_nnz; i += NT) vals[i] = S_::identity();
+        __syncthreads();
+        ValueBatch<SRID> vb{Av, Bv, bm, pre16, chunk, vals, r_lo};
+        if (whole) {
+            // cursor-driven like k_fused_heavy's tiles (ntiles = 2: chunk count is data dependent)
+            walk_balanced<8>(A, B, bs, be, sg, t, 2, r_hi, cursor + (t & 1) * B.span,
+                             cursor + ((t + 1) & 1) * B.span, int64_t(8) * NT, ws, vb);
+        } else {
+            const int rl = r_lo;
+            auto start_of = [Arw, rl](int64_t, int64_t as, int64_t ae) -> int64_t {
+                if (rl == 0) return as;
+                int64_t a = as, b = ae;  // first position with row >= rl
+                while (a < b) {
+                    const int64_t mid = (a + b) >> 1;
+                    if (__ldg(&Arw[mid]) < rl)
+                        a = mid + 1;
+                    else
+                        b = mid;
+                }
+                return a;
+            };
+            walk_balanced_from<8>(A, B, bs, be, sg, r_hi, nullptr, int64_t(8) * NT, ws, start_of, vb);
+        }
+        for (int i = tid; i < tile_nnz; i += NT) Cv[lo + i] = S_::out(vals[i]);
+        lo = hi;
+        r_lo = r_hi;
+        __syncthreads();
+    }
+}
+
 __global__ void k_count_ge(int n, const int* __restrict__ list, const int64_t* __restrict__ flops, int64_t thr,
                            int* __restrict__ out) {
     int c = 0;
@@ -720,23 +877,39 @@ void fused_finish(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int32_t* c
                        (const int32_t*)f.srows.as<int32_t>(), (const int64_t*)f.colptr, crw, Cv);
             if (!f.ones) {
                 KScope ks2(c, KC_NUM_HEAVY);
-                // bitmap + ranks for up to 2^17 rows, the rest of ~113 KB (two
-                // CTAs per SM) holds the chunk's values
                 // One CTA of 1024 threads per SM: bitmap + 16-bit ranks for up to
                 // 2^19 rows (98 KB) and the rest of the SM's shared memory for
-                // the chunk's values, so a heavy column needs few chunks (each
-                // chunk re-walks the column's B entries).
+                // the item's values.  Items (<= cap entries, <= 2^19 rows) are
+                // planned from C's rows and processed independently.
                 const int tl = heavy_tile_log2(std::min(c.opt.tile_rows_log2 + 1, 19), A.nrows);
                 const size_t W = size_t(1) << (tl - 5);
                 const size_t fixed = W * 4 + ((W + 31) / 32) * 4 + W * 2 + 64;
                 const size_t budget = size_t(c.smem_optin) - 8 * 1024;  // static state + reserve
-                // multiple of 4 entries keeps the bitmap behind the values 16-byte aligned
                 const int cap = (int)((budget - fixed) / sizeof(Acc)) & ~3;
-                const size_t smem = fixed + size_t(cap) * sizeof(Acc);
-                auto k = k_values_heavy<ID, kValuesThreads>;
+                const size_t smem = fixed + size_t(cap) * sizeof(Acc) + 16;
+                DevBuf nit(sizeof(int64_t) * (nheavy + 1), c.stream), ioff(sizeof(int64_t) * (nheavy + 1), c.stream);
+                SLAPCU_CUDA(cudaMemsetAsync(nit.as<int64_t>() + nheavy, 0, sizeof(int64_t), c.stream));
+                const int pg = grid_for(c, nheavy, 128);
+                // columns above this many multiplies are split over several CTAs
+                const int64_t split = int64_t(4) << 20;
+                launch(c, k_values_plan, dim3(pg), dim3(128), 0, hl, nheavy, (const int64_t*)f.colptr,
+                       (const int32_t*)crw, A.nrows, int64_t(1) << tl, cap, false, nit.as<int64_t>(),
+                       (const int64_t*)nullptr, (VItem*)nullptr, flops, split);
+                exclusive_scan_i64(c, nit.as<int64_t>(), ioff.as<int64_t>(), nheavy + 1);
+                int64_t nitems = 0;
+                SLAPCU_CUDA(cudaMemcpyAsync(&nitems, ioff.as<int64_t>() + nheavy, sizeof(int64_t),
+                                            cudaMemcpyDeviceToHost, c.stream));
+                SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+                if (nitems > INT32_MAX) throw Fail{SLAPCU_ERR_INVALID, "too many value-pass items"};
+                f.items.reset(sizeof(VItem) * std::max<int64_t>(nitems, 1), c.stream);
+                launch(c, k_values_plan, dim3(pg), dim3(128), 0, hl, nheavy, (const int64_t*)f.colptr,
+                       (const int32_t*)crw, A.nrows, int64_t(1) << tl, cap, true, nit.as<int64_t>(),
+                       (const int64_t*)ioff.as<int64_t>(), f.items.as<VItem>(), flops, split);
+                auto k = k_values_items<ID, kValuesThreads>;
                 ensure_smem(k, smem);
-                launch(c, k, dim3(nheavy), dim3(kValuesThreads), smem, A, B, hl, nheavy, flops,
-                       (const int64_t*)f.colptr, (const int32_t*)crw, Cv, tl, cap, c.plan.cursor.as<int32_t>(), err);
+                launch(c, k, dim3((unsigned)nitems), dim3(kValuesThreads), smem, A, B,
+                       (const VItem*)f.items.as<VItem>(), flops, (const int32_t*)crw, Cv, tl, cap,
+                       c.plan.cursor.as<int32_t>(), err);
             }
         }
     });

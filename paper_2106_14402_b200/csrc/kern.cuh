@@ -257,16 +257,32 @@ struct WalkShared {
 // into shared memory), and the others are handed out to sub-groups of sg
 // lanes through a shared atomic counter.  Must be called by all threads of
 // the CTA (contains barriers); NT <= 1024.
+template <int U, class S, class F>
+__device__ __forceinline__ void walk_balanced_from(const DevCsc& A, const DevCsc& B, int64_t bs, int64_t be, int sg,
+                                                   int t1, int32_t* __restrict__ cur_out, int64_t big,
+                                                   WalkShared& ws, S&& start_of, F&& f);
+
 template <int U, class F>
 __device__ __forceinline__ void walk_balanced(const DevCsc& A, const DevCsc& B, int64_t bs, int64_t be, int sg,
                                               int t, int ntiles, int t1, const int32_t* __restrict__ cur_in,
                                               int32_t* __restrict__ cur_out, int64_t big, WalkShared& ws, F&& f) {
-    const int tid = threadIdx.x, nt = blockDim.x;
     const bool tiled = ntiles > 1;
-    const int64_t nb = be - bs;
-    auto start_of = [&](int64_t i, int64_t as) -> int64_t {
+    auto start_of = [&](int64_t i, int64_t as, int64_t) -> int64_t {
         return (!tiled || t == 0) ? as : as + cur_in[i - B.base];
     };
+    walk_balanced_from<U>(A, B, bs, be, sg, t1, tiled ? cur_out : nullptr, big, ws, start_of, f);
+}
+
+// Same walk with a caller-supplied start position per B entry
+// (start_of(i, as, ae) -> first position to visit); cursors are written only
+// when cur_out is non-null.
+template <int U, class S, class F>
+__device__ __forceinline__ void walk_balanced_from(const DevCsc& A, const DevCsc& B, int64_t bs, int64_t be, int sg,
+                                                   int t1, int32_t* __restrict__ cur_out, int64_t big,
+                                                   WalkShared& ws, S&& start_of, F&& f) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const bool tiled = cur_out != nullptr;
+    const int64_t nb = be - bs;
     // phase A: long entries, whole CTA per entry
     for (int64_t base = 0; base < nb; base += nt) {
         if (tid == 0) ws.nlong = 0;
@@ -275,7 +291,7 @@ __device__ __forceinline__ void walk_balanced(const DevCsc& A, const DevCsc& B, 
         if (base + tid < nb) {
             const int k = B.rw[i];
             const int64_t as = A.cp[k], ae = A.cp[k + 1];
-            if (ae - start_of(i, as) >= big) ws.list[atomicAdd(&ws.nlong, 1)] = (int)(base + tid);
+            if (ae - start_of(i, as, ae) >= big) ws.list[atomicAdd(&ws.nlong, 1)] = (int)(base + tid);
         }
         __syncthreads();
         const int nl = ws.nlong;
@@ -283,7 +299,7 @@ __device__ __forceinline__ void walk_balanced(const DevCsc& A, const DevCsc& B, 
             const int64_t ii = bs + ws.list[li];
             const int k = B.rw[ii];
             const int64_t as = A.cp[k], ae = A.cp[k + 1];
-            walk_entry<U>(A.rw, ii, as, start_of(ii, as), ae, tid, nt, t1, tiled ? cur_out + (ii - B.base) : nullptr,
+            walk_entry<U>(A.rw, ii, as, start_of(ii, as, ae), ae, tid, nt, t1, tiled ? cur_out + (ii - B.base) : nullptr,
                           f);
         }
         __syncthreads();
@@ -302,7 +318,7 @@ __device__ __forceinline__ void walk_balanced(const DevCsc& A, const DevCsc& B, 
             const int64_t i = bs + e;
             const int k = B.rw[i];
             const int64_t as = A.cp[k], ae = A.cp[k + 1];
-            const int64_t st = start_of(i, as);
+            const int64_t st = start_of(i, as, ae);
             if (ae - st < big)
                 walk_entry<U>(A.rw, i, as, st, ae, sl, sg, t1, tiled ? cur_out + (i - B.base) : nullptr, f);
         }
