@@ -105,3 +105,15 @@ def test_grid_shapes():
         G.Grid3D.make(6, 2, 0)  # p/c = 3 not square
     assert G.Grid3D.make(8, 2, 0).layer_warning is False  # c=2 <= cbrt(8)
     assert G.Grid3D.make(4, 4, 0).layer_warning is True
+
+
+def test_plan_batches_by_count_matches_reference_rule():
+    # batched.hpp:25-37: remainder one per range from the front
+    from paper_2106_14402_b200 import batched as BT
+
+    p = BT.plan_batches_by_count(10, 4)
+    assert p.col_ranges == [(0, 3), (3, 6), (6, 8), (8, 10)]
+    with pytest.raises(Exception):
+        BT.plan_batches_by_count(10, 0)
+    q = BT.plan_from_counts([1, 2, 3, 4], 16 * 5)
+    assert q.col_ranges == [(0, 2), (2, 3), (3, 4)] and q.est_entries == [3, 3, 4]
