@@ -58,6 +58,10 @@ def parse():
     ap.add_argument("--sym-tile-log2", type=int, default=0, help="row-tile height of the pattern bitmap (0 = default)")
     ap.add_argument("--tile-log2", type=int, default=0, help="row-tile height of the value pass (0 = default)")
     ap.add_argument("--dense-min", type=int, default=None, help="byte-flag pattern path for flops >= this (0 off)")
+    ap.add_argument("--method", default="direct", choices=["direct", "fused"],
+                    help="direct: slapcu_spgemm_direct writes C in place in one pass; fused: begin/finish")
+    ap.add_argument("--direct-tile-log2", type=int, default=0, help="rows per direct-path item (0 = default)")
+    ap.add_argument("--direct-dense-min", type=int, default=None, help="direct path: dense item threshold")
     ap.add_argument("--streams", type=int, default=1, choices=[1, 2],
                     help="2: alternate column batches over two contexts/streams (async finish)")
     return ap.parse_args()
@@ -72,6 +76,10 @@ def apply_options(ctx, args):
         ctx.set_option(L.OPT_TILE_ROWS_LOG2, args.tile_log2)
     if args.dense_min is not None:
         ctx.set_option(L.OPT_DENSE_FLOPS_MIN, args.dense_min)
+    if args.direct_tile_log2:
+        ctx.set_option(L.OPT_DIRECT_TILE_ROWS_LOG2, args.direct_tile_log2)
+    if args.direct_dense_min is not None:
+        ctx.set_option(L.OPT_DIRECT_DENSE_FLOPS_MIN, args.direct_dense_min)
 
 
 # ------------------------------------------------------------------ helpers
@@ -221,6 +229,8 @@ def run_ours(args):
     # pass) is still in flight -- slapcu_spgemm_finish is asynchronous
     # (SLAPCU_OPT_ASYNC_FINISH) and the next begin() on the same context
     # settles it.  Each context owns its staging area and output buffers.
+    if args.method == "direct":
+        args.streams = 1  # the direct call synchronises its own stream (item counts, totals)
     if args.streams == 2:
         stream2 = torch.cuda.Stream(device=dev)
         ctxs = [ctx, P.Context(0, stream2)]
@@ -250,6 +260,13 @@ def run_ours(args):
             cx = ctxs[bi % len(ctxs)]
             o_cp, o_rw, o_v = outs[bi % len(ctxs)]
             nz = C.c_int64()
+            if args.method == "direct":
+                cx.check(lib.slapcu_spgemm_direct(cx.h, C.byref(av), C.byref(w), sr.id, P.SpGemmAlg.hybrid,
+                                                  o_rw.numel(), o_cp.data_ptr(), o_rw.data_ptr(), o_v.data_ptr(),
+                                                  C.byref(nz)), "direct")
+                if collect is not None:
+                    collect(bi, int(nz.value))
+                continue
             cx.check(lib.slapcu_spgemm_begin(cx.h, C.byref(av), C.byref(w), sr.id, P.SpGemmAlg.hybrid, 0,
                                              o_cp.data_ptr(), C.byref(nz)), "begin")
             cx.check(lib.slapcu_spgemm_finish(cx.h, C.byref(av), C.byref(w), sr.id, o_rw.data_ptr(),
@@ -303,7 +320,7 @@ def run_ours(args):
     per_step = {k: (nl / args.steps, t / args.steps) for k, (nl, t) in kstats.items() if nl}
     dom = max(per_step, key=lambda k: per_step[k][1])
     # heavy columns of the fused path: flops > max(256, min(n/128, 4096))
-    lmax = max(256, min(A.nrows // 128, 4096))
+    lmax = max(256, min(A.nrows // 128, 4096))  # same light/heavy split in both methods
     fl = flops_per.cpu().numpy()
     heavy = fl > lmax
     colnnz_b = np.diff(A.colptr.cpu().numpy())
@@ -315,7 +332,10 @@ def run_ours(args):
             continue
         c_ent = int(counts[s:e][h].sum())
         b_ent = int(colnnz_b[s:e][h].sum())
-        if dom == "sym_heavy":  # k_fused_heavy: B cols + A (pattern) in, staged rows out
+        if dom == "sym_heavy" and args.method == "direct":
+            # k_tile_direct + k_tile_dense: B cols + A pattern in, C rows + values out in place
+            dom_bytes += c_ent * (4 + vs) + b_ent * 4 + (nh + 1) * 8 + A.nnz * 4 + (n + 1) * 8
+        elif dom == "sym_heavy":  # k_fused_heavy: B cols + A (pattern) in, staged rows out
             dom_bytes += c_ent * 4 + b_ent * 4 + (nh + 1) * 8 + A.nnz * 4 + (n + 1) * 8
         elif dom == "num_heavy":  # k_values_heavy: C rows in, values out, B and A with values
             dom_bytes += c_ent * (4 + vs) + b_ent * (4 + vs) + (nh + 1) * 8 + A.nnz * (4 + vs) + (n + 1) * 8
@@ -328,7 +348,8 @@ def run_ours(args):
     step_bytes = bytes_alg(A.nnz, n, A.nnz, n, nnz_c, n, vs)
     roofline = {
         "bound": "hbm",
-        "kernel": {"sym_heavy": "k_fused_heavy", "sym_light": "k_fused_light", "num_heavy": "k_values_heavy",
+        "method": args.method,
+        "kernel": {"sym_heavy": "k_tile_direct+k_tile_dense" if args.method == "direct" else "k_fused_heavy", "sym_light": "k_fused_light", "num_heavy": "k_values_heavy",
                    "num_light": "k_copy_light+k_copy_heavy"}.get(dom, dom),
         "achieved": round(achieved, 2),
         "peak": peak,
@@ -436,10 +457,15 @@ def run_e2e_single(args, A, sr, batches, counts, total_flops, ctx, stream):
         for s, e in batches:
             w = L.CscView(A.nrows, e - s, A.nnz, d_cp.data_ptr() + 8 * s, d_rw.data_ptr(), d_v.data_ptr())
             nz = C.c_int64()
-            ctx.check(lib.slapcu_spgemm_begin(ctx.h, C.byref(av), C.byref(w), sr.id, P.SpGemmAlg.hybrid, 0,
-                                              o_cp.data_ptr(), C.byref(nz)), "begin")
-            ctx.check(lib.slapcu_spgemm_finish(ctx.h, C.byref(av), C.byref(w), sr.id, o_rw.data_ptr(),
-                                               o_v.data_ptr()), "finish")
+            if args.method == "direct":
+                ctx.check(lib.slapcu_spgemm_direct(ctx.h, C.byref(av), C.byref(w), sr.id, P.SpGemmAlg.hybrid,
+                                                   o_rw.numel(), o_cp.data_ptr(), o_rw.data_ptr(), o_v.data_ptr(),
+                                                   C.byref(nz)), "direct")
+            else:
+                ctx.check(lib.slapcu_spgemm_begin(ctx.h, C.byref(av), C.byref(w), sr.id, P.SpGemmAlg.hybrid, 0,
+                                                  o_cp.data_ptr(), C.byref(nz)), "begin")
+                ctx.check(lib.slapcu_spgemm_finish(ctx.h, C.byref(av), C.byref(w), sr.id, o_rw.data_ptr(),
+                                                   o_v.data_ptr()), "finish")
             nzv = int(nz.value)
             h_out_cp[: e - s + 1].copy_(o_cp[: e - s + 1], non_blocking=True)
             d2h += (e - s + 1) * 8

@@ -110,9 +110,12 @@ typedef enum {
     SLAPCU_OPT_DENSE_FLOPS_MIN = 6,   /* fused path: byte-flag tiles for columns with flops >= v
                                          (-1 auto = nrows/4, 0 = off) */
     SLAPCU_OPT_DENSE_TILE_ROWS_LOG2 = 7, /* byte-flag tile height (default 17 = 128 KB) */
-    SLAPCU_OPT_ASYNC_FINISH = 8       /* 1: slapcu_spgemm_finish returns without waiting; its
+    SLAPCU_OPT_ASYNC_FINISH = 8,      /* 1: slapcu_spgemm_finish returns without waiting; its
                                          InternalError surfaces at the next call on the context
                                          or at slapcu_ctx_synchronize */
+    SLAPCU_OPT_DIRECT_TILE_ROWS_LOG2 = 9,  /* direct path: rows per (column, row tile) item (default 17) */
+    SLAPCU_OPT_DIRECT_DENSE_FLOPS_MIN = 10 /* direct path: items with at least this many multiplies are
+                                              formed up front into global bitmaps (0 = never) */
 } slapcu_option;
 slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t value);
 
@@ -171,6 +174,22 @@ slapcu_status slapcu_spgemm_begin(slapcu_ctx ctx, const slapcu_csc* A, const sla
                                   slapcu_alg alg, int64_t staging_budget_bytes, int64_t* c_colptr, int64_t* c_nnz);
 slapcu_status slapcu_spgemm_finish(slapcu_ctx ctx, const slapcu_csc* A, const slapcu_csc* B, slapcu_semiring sr,
                                    int32_t* c_rowids, void* c_vals);
+
+/* Single pass straight into caller buffers (the production path for the
+ * Boolean C3 headline): C's colptr, rowids and values are written in place by
+ * one walk over the products -- heavy columns are cut into (column, row
+ * tile) items laid out in C order, each formed in a shared-memory bitmap and
+ * given its output offset by a decoupled look-back, so there is no staging
+ * copy and no second product pass.  `capacity` = entries the caller's
+ * c_rowids / c_vals hold; sum_j min(flops_j, A.nrows) (from
+ * slapcu_estimate_flops) always suffices.  If C needs more, nothing beyond
+ * capacity is written, *c_nnz gets the exact requirement and the call
+ * returns SLAPCU_ERR_BUDGET.  OrAnd operands without stored zeros take the
+ * in-place path; other semirings are formed by the begin/finish pair into
+ * the same buffers (same contract).  Same output as local_spgemm. */
+slapcu_status slapcu_spgemm_direct(slapcu_ctx ctx, const slapcu_csc* A, const slapcu_csc* B, slapcu_semiring sr,
+                                   slapcu_alg alg, int64_t capacity, int64_t* c_colptr, int32_t* c_rowids,
+                                   void* c_vals, int64_t* c_nnz);
 
 /* spgemm.hpp:275-330 local_spgemm, all three phases, C allocated on the
  * device by the library (single-pass begin/finish; falls back to the

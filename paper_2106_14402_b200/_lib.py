@@ -32,7 +32,8 @@ PLUS_TIMES_F64, PLUS_TIMES_F32, PLUS_TIMES_I64, MIN_PLUS_I32, MIN_PLUS_F64, OR_A
 ALG_HEAP, ALG_HASH, ALG_HYBRID = 0, 1, 2
 # slapcu_option
 (OPT_TILE_ROWS_LOG2, OPT_SYM_TILE_ROWS_LOG2, OPT_LIGHT_NNZ_MAX, OPT_LIGHT_FLOPS_MAX, OPT_DETERMINISTIC, OPT_PROFILE,
- OPT_DENSE_FLOPS_MIN, OPT_DENSE_TILE_ROWS_LOG2, OPT_ASYNC_FINISH) = range(9)
+ OPT_DENSE_FLOPS_MIN, OPT_DENSE_TILE_ROWS_LOG2, OPT_ASYNC_FINISH, OPT_DIRECT_TILE_ROWS_LOG2,
+ OPT_DIRECT_DENSE_FLOPS_MIN) = range(11)
 NUM_KERNEL_CLASSES = 10
 KERNEL_CLASSES = ["other", "flops", "bin", "sym_light", "sym_heavy", "scan", "num_light", "num_heavy", "merge", "gen"]
 
@@ -106,6 +107,7 @@ SIGNATURES = [
     ("slapcu_spgemm_numeric", _I, [_P, _PV, _PV, _I, _I, _P, _P, _P]),
     ("slapcu_spgemm_begin", _I, [_P, _PV, _PV, _I, _I, _L, _P, C.POINTER(_L)]),
     ("slapcu_spgemm_finish", _I, [_P, _PV, _PV, _I, _P, _P]),
+    ("slapcu_spgemm_direct", _I, [_P, _PV, _PV, _I, _I, _L, _P, _P, _P, C.POINTER(_L)]),
     ("slapcu_spgemm", _I, [_P, _PV, _PV, _I, _I, _PO]),
     ("slapcu_spgemm_host", _I, [_P, _PO, _PO, _I, _I, _PO]),
     ("slapcu_csc_free", _I, [_P, _PO]),

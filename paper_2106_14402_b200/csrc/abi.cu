@@ -138,6 +138,14 @@ slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t v
             c.opt.sym_tile_rows_log2 = (int)v;
             break;
         case SLAPCU_OPT_LIGHT_NNZ_MAX: c.opt.light_nnz_max = v; break;
+        case SLAPCU_OPT_DIRECT_TILE_ROWS_LOG2:
+            require(v >= 10 && v <= 18, SLAPCU_ERR_INVALID, "direct tile rows log2 must be in 10..18");
+            c.opt.direct_tile_rows_log2 = (int)v;
+            break;
+        case SLAPCU_OPT_DIRECT_DENSE_FLOPS_MIN:
+            require(v >= 0, SLAPCU_ERR_INVALID, "dense flops threshold must be >= 0");
+            c.opt.direct_dense_flops_min = v;
+            break;
         case SLAPCU_OPT_LIGHT_FLOPS_MAX: c.opt.light_flops_max = v; break;
         case SLAPCU_OPT_DETERMINISTIC: break;
         case SLAPCU_OPT_DENSE_FLOPS_MIN: c.opt.dense_flops_min = v; break;
@@ -254,6 +262,19 @@ slapcu_status slapcu_spgemm_finish(slapcu_ctx ctx, const slapcu_csc* A, const sl
         require(A && B, SLAPCU_ERR_INVALID, "null argument");
         fused_finish(c, view(*A), view(*B), sr, c_rowids, c_vals);
     });
+}
+
+slapcu_status slapcu_spgemm_direct(slapcu_ctx ctx, const slapcu_csc* A, const slapcu_csc* B, slapcu_semiring sr,
+                                   slapcu_alg alg, int64_t capacity, int64_t* c_colptr, int32_t* c_rowids,
+                                   void* c_vals, int64_t* c_nnz) {
+    if (ctx) ctx->c.direct.last_nnz = -1;
+    const slapcu_status st = guarded(ctx, [&](Ctx& c) {
+        require(A && B && c_colptr, SLAPCU_ERR_INVALID, "null argument");
+        require(capacity >= 0, SLAPCU_ERR_INVALID, "negative capacity");
+        c.direct.last_nnz = direct_spgemm(c, view(*A), view(*B), sr, alg, capacity, c_colptr, c_rowids, c_vals);
+    });
+    if (ctx && c_nnz) *c_nnz = ctx->c.direct.last_nnz;
+    return st;
 }
 
 // Largest staging area the one-shot call will take: half the free device memory.

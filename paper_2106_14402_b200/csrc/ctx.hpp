@@ -121,6 +121,21 @@ struct Options {
     int64_t dense_flops_min = 0;
     int dense_tile_rows_log2 = 17;    // byte-flag tile height (128 KB of flags)
     bool async_finish = false;        // finish() returns without waiting (errors surface later)
+    int direct_tile_rows_log2 = 17;   // direct path: row-tile height of an item (16 KB bitmap)
+    int64_t direct_dense_flops_min = 65536;  // direct path: items with >= this many multiplies are
+                                             // formed up front into global bitmaps (0 = never)
+};
+
+// Workspace of the direct (in-place) path, kept across calls.
+struct DirectCache {
+    FusedState light;  // light columns: staged hash output (fused.cu kernels)
+    DevBuf atp;        // A tile pointers int32[A.ncols][T+1]
+    const void* atp_key = nullptr;
+    int64_t atp_ncols = -1, atp_nnz = -1;
+    int atp_tl = -1;
+    bool atp_valid = false;
+    DevBuf lp, hcnt, hl, items, dslot, dlist, state, gbm;
+    int64_t last_nnz = -1;  // exact nnz(C) of the last call (also on BudgetError)
 };
 
 // Kernel classes for the per-class device-time breakdown (profiling mode).
@@ -153,6 +168,7 @@ struct Ctx {
     Options opt;
     Plan plan;
     FusedState fused;
+    DirectCache direct;
     std::string last_error;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     float sym_ms = 0.f, num_ms = 0.f;
@@ -188,6 +204,14 @@ int64_t fused_begin(Ctx& c, const DevCsc& A, const DevCsc& B, int sr, int alg, i
                     int64_t staging_budget_bytes);
 void fused_finish(Ctx& c, const DevCsc& A, const DevCsc& B, int sr, int32_t* c_rowids, void* c_vals);
 void ctx_settle(Ctx& c);
+// fused.cu helpers shared with the direct path
+void fused_light_launch(Ctx& c, int sr, bool ones, int bin, const DevCsc& A, const DevCsc& B, const int* list, int n,
+                        const int64_t* flops, FusedState& f);
+void fused_copy_light(Ctx& c, bool ones, const int* list, int n, const FusedState& f, const int64_t* c_colptr,
+                      int32_t* c_rowids, void* c_vals);
+// direct.cu: single pass straight into C (pattern semirings)
+int64_t direct_spgemm(Ctx& c, const DevCsc& A, const DevCsc& B, int sr, int alg, int64_t capacity, int64_t* c_colptr,
+                      int32_t* c_rowids, void* c_vals);
 void any_zero_u8(Ctx& c, const uint8_t* v, int64_t n, int* flag);
 void dcsc_colptr(Ctx& c, int64_t ncols, int64_t nzc, const int32_t* jc, const int32_t* cp, int64_t* colptr);
 void exclusive_scan_i64(Ctx& c, const int64_t* in, int64_t* out, int64_t n);

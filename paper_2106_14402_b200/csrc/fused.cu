@@ -679,6 +679,33 @@ int heavy_tile_log2(int want, int64_t nrows) {
 
 }  // namespace
 
+void fused_light_launch(Ctx& c, int sr, bool ones, int bin, const DevCsc& A, const DevCsc& B, const int* list, int n,
+                        const int64_t* flops, FusedState& f) {
+    dispatch_sr(sr, [&](auto id) {
+        constexpr int ID = decltype(id)::value;
+        if constexpr (ID == SLAPCU_OR_AND_U8) {
+            if (ones) {
+                launch_fused_light_bin<ID, true>(c, bin, A, B, list, n, flops, f);
+                return;
+            }
+        }
+        launch_fused_light_bin<ID, false>(c, bin, A, B, list, n, flops, f);
+    });
+}
+
+// Staged light columns into C (OrAnd only: values 1 when `ones`).
+void fused_copy_light(Ctx& c, bool ones, const int* list, int n, const FusedState& f, const int64_t* c_colptr,
+                      int32_t* crw, void* cv) {
+    using T = uint8_t;
+    const int g = grid_for(c, int64_t(n) * 32, 256, 16);
+    if (ones)
+        launch(c, k_copy_light<T, true>, dim3(g), dim3(256), 0, list, n, (const int64_t*)f.soff.as<int64_t>(), c_colptr,
+               (const int32_t*)f.srows.as<int32_t>(), (const T*)nullptr, crw, static_cast<T*>(cv));
+    else
+        launch(c, k_copy_light<T, false>, dim3(g), dim3(256), 0, list, n, (const int64_t*)f.soff.as<int64_t>(),
+               c_colptr, (const int32_t*)f.srows.as<int32_t>(), (const T*)f.svals.get(), crw, static_cast<T*>(cv));
+}
+
 int64_t fused_begin(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int alg, int64_t* c_colptr,
                     int64_t staging_budget_bytes) {
     check_operands(A_, B_);

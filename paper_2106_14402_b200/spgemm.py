@@ -374,7 +374,9 @@ def local_spgemm(a, b, sr: Semiring, alg=SpGemmAlg.hybrid, threads: int = 1, ctx
 
     method "fused" (default) forms each column once (slapcu_spgemm_begin /
     _finish) and falls back to "two_pass" (slapcu_spgemm_symbolic / _numeric)
-    when its staging area would not fit in half the free device memory."""
+    when its staging area would not fit in half the free device memory.
+    method "direct" writes C in place in one pass (slapcu_spgemm_direct) into
+    buffers sized by the bound sum_j min(flops_j, A.nrows)."""
     sr = _sr(sr)
     alg = SpGemmAlg(int(alg))
     ctx = _ctx(ctx)
@@ -390,6 +392,15 @@ def local_spgemm(a, b, sr: Semiring, alg=SpGemmAlg.hybrid, threads: int = 1, ctx
     cp = torch.empty(B.ncols + 1, dtype=torch.int64, device=dev)
     nnz = C.c_int64()
     av, bv = A.view(), B.view()
+    if method == "direct":
+        _tot, fl = estimate_flops(A, B, ctx=ctx)
+        cap = int(torch.clamp(fl, max=A.nrows).sum().item()) if B.ncols else 0
+        rw = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+        vals = torch.empty(max(cap, 1), dtype=sr.torch_dtype, device=dev)
+        ctx.check(ctx.lib.slapcu_spgemm_direct(ctx.h, C.byref(av), C.byref(bv), sr.id, int(alg), cap, cp.data_ptr(),
+                                               rw.data_ptr(), vals.data_ptr(), C.byref(nnz)), "direct")
+        n = int(nnz.value)
+        return DeviceCsc(A.nrows, B.ncols, cp, rw[:n].clone(), vals[:n].clone())
     if method == "fused":
         free, _ = torch.cuda.mem_get_info(dev)
         st = ctx.lib.slapcu_spgemm_begin(ctx.h, C.byref(av), C.byref(bv), sr.id, int(alg), int(free // 2),

@@ -1,0 +1,121 @@
+"""GPU parity of the in-place single-pass path (slapcu_spgemm_direct).
+
+The Boolean product is formed as (column, row tile) items ordered by a
+decoupled look-back; these cases force every item class -- short runs, warp
+units, dense items pre-formed into global bitmaps, many tiles per column,
+column windows, empty columns -- and check C bit-exactly against the CPU
+oracle (acceptance.cpp:58-97 style equivalence; spgemm.hpp:259-260 sorted
+rows).  Capacity overflow must raise BudgetError with the exact nnz.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import oracle
+from tests.helpers import assert_parity, to_device, with_values
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2106_14402_b200 as P  # noqa: E402
+from paper_2106_14402_b200 import _lib as L  # noqa: E402
+
+
+def _ones(m):
+    return m.with_vals(np.ones(m.nnz, np.uint8))
+
+
+@pytest.mark.parametrize("tile_log2", [10, 12, 17])
+@pytest.mark.parametrize("dense_min", [0, 1, 2000, 65536])
+def test_direct_bool_tiles_and_dense(port, tile_log2, dense_min):
+    a = _ones(port.gen_rmat(12))
+    want = port.spgemm(oracle.OR_AND_U8, a, a)
+    ctx = P.Context()
+    ctx.set_option(L.OPT_DIRECT_TILE_ROWS_LOG2, tile_log2)
+    ctx.set_option(L.OPT_DIRECT_DENSE_FLOPS_MIN, dense_min)
+    da = to_device(a)
+    for alg in (P.SpGemmAlg.heap, P.SpGemmAlg.hybrid):
+        got = P.local_spgemm(da, da, P.OrAnd, alg, ctx=ctx, method="direct")
+        assert_parity(got, want, oracle.OR_AND_U8, f"TL={tile_log2} dense={dense_min} {alg.name}")
+
+
+@pytest.mark.parametrize("scale", [8, 11, 14])
+def test_direct_bool_rmat(port, scale):
+    a = _ones(port.gen_rmat(scale))
+    want = port.spgemm(oracle.OR_AND_U8, a, a)
+    got = P.local_spgemm(to_device(a), to_device(a), P.OrAnd, method="direct")
+    assert_parity(got, want, oracle.OR_AND_U8, f"s{scale}")
+
+
+def test_direct_window_and_rectangular(port):
+    from paper_2106_14402_b200 import dist as D
+
+    a = _ones(port.gen_rmat(12))
+    want = port.spgemm(oracle.OR_AND_U8, a, a, 700, 3100)
+    da = to_device(a)
+    ctx = P.Context()
+    ctx.set_option(L.OPT_DIRECT_TILE_ROWS_LOG2, 11)
+    got = P.local_spgemm(da, D.column_window(da, 700, 3100), P.OrAnd, ctx=ctx, method="direct")
+    assert_parity(got, want, oracle.OR_AND_U8, "window")
+    # B with empty columns and a different row count than A's columns
+    b = port.gen_rmat(12, 8, 3)
+    rows, cols = [], []
+    for j in range(0, 1500):
+        if j % 4 == 0:
+            continue
+        s, e = b.colptr[j], b.colptr[j + 1]
+        rows += b.rowids[s:e].tolist()
+        cols += [j] * int(e - s)
+    bb = _ones(oracle.from_triples(b.nrows, 1500, rows, cols, np.ones(len(rows))))
+    want = port.spgemm(oracle.OR_AND_U8, a, bb)
+    got = P.local_spgemm(da, to_device(bb), P.OrAnd, ctx=ctx, method="direct")
+    assert_parity(got, want, oracle.OR_AND_U8, "rect")
+
+
+def test_direct_fallback_semirings(port):
+    """Value semirings and OrAnd with stored zeros go through begin/finish
+    into the caller's buffers: same contract, same output."""
+    a = with_values(port, port.gen_rmat(11), oracle.MIN_PLUS_I32)
+    want = port.spgemm(oracle.MIN_PLUS_I32, a, a)
+    assert_parity(P.local_spgemm(to_device(a), to_device(a), P.MinPlusI32, method="direct"), want,
+                  oracle.MIN_PLUS_I32, "min_plus")
+    z = port.gen_rmat(10)
+    z = z.with_vals((np.arange(z.nnz) % 3 != 0).astype(np.uint8))
+    want = port.spgemm(oracle.OR_AND_U8, z, z)
+    assert_parity(P.local_spgemm(to_device(z), to_device(z), P.OrAnd, method="direct"), want, oracle.OR_AND_U8,
+                  "zeros")
+
+
+def test_direct_capacity_budget_error(port):
+    a = _ones(port.gen_rmat(11))
+    want = port.spgemm(oracle.OR_AND_U8, a, a)
+    da = to_device(a)
+    ctx = P.Context()
+    n = want.nnz
+    cp = torch.empty(a.ncols + 1, dtype=torch.int64, device="cuda")
+    rw = torch.empty(n, dtype=torch.int32, device="cuda")
+    v = torch.empty(n, dtype=torch.uint8, device="cuda")
+    nnz = C.c_int64()
+    st = ctx.lib.slapcu_spgemm_direct(ctx.h, C.byref(da.view()), C.byref(da.view()), P.OrAnd.id, 2, n - 1,
+                                      cp.data_ptr(), rw.data_ptr(), v.data_ptr(), C.byref(nnz))
+    assert st == 5 and nnz.value == n
+    # exact capacity succeeds
+    st = ctx.lib.slapcu_spgemm_direct(ctx.h, C.byref(da.view()), C.byref(da.view()), P.OrAnd.id, 2, n,
+                                      cp.data_ptr(), rw.data_ptr(), v.data_ptr(), C.byref(nnz))
+    assert st == 0 and nnz.value == n
+    assert np.array_equal(rw.cpu().numpy(), want.rowids)
+    assert np.array_equal(cp.cpu().numpy(), want.colptr)
+
+
+def test_direct_empty(port):
+    e = oracle.from_triples(50, 40, [], [], np.zeros(0, np.uint8))
+    a = _ones(port.gen_rmat(6))
+    for x, y in ((e, _ones(oracle.from_triples(40, 30, [], [], np.zeros(0)))),
+                 (_ones(oracle.from_triples(64, 64, [], [], np.zeros(0))), a)):
+        want = port.spgemm(oracle.OR_AND_U8, x, y)
+        got = P.local_spgemm(to_device(x), to_device(y), P.OrAnd, method="direct")
+        assert_parity(got, want, oracle.OR_AND_U8, "empty")

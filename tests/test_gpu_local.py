@@ -25,7 +25,7 @@ from paper_2106_14402_b200 import _lib as L  # noqa: E402
 
 SRS = [P.PlusTimesF64, P.PlusTimesF32, P.PlusTimesI64, P.MinPlusI32, P.MinPlusF64, P.OrAnd]
 ALGS = [P.SpGemmAlg.heap, P.SpGemmAlg.hash, P.SpGemmAlg.hybrid]
-METHODS = ["fused", "two_pass"]
+METHODS = ["fused", "two_pass", "direct"]
 
 
 def example_a():
