@@ -122,7 +122,7 @@ struct Options {
     int dense_tile_rows_log2 = 17;    // byte-flag tile height (128 KB of flags)
     bool async_finish = false;        // finish() returns without waiting (errors surface later)
     int direct_tile_rows_log2 = 17;   // direct path: row-tile height of an item (16 KB bitmap)
-    int64_t direct_dense_flops_min = 65536;  // direct path: items with >= this many multiplies are
+    int64_t direct_dense_flops_min = 16384;  // direct path: items with >= this many multiplies are
                                              // formed up front into global bitmaps (0 = never)
 };
 

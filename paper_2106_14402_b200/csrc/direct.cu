@@ -42,9 +42,11 @@ constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagIncl = 2ull << 62, kVal
 __device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+// Look-back reads only use the state word itself, so relaxed suffices (an
+// acquire load invalidates L1 on every spin).
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
     unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
 
@@ -78,16 +80,18 @@ struct WalkSm {
     int64_t start[NT];
 };
 
-// Marks row r of the current tile: test before set (a plain shared load is a
-// broadcast for lanes hitting one word; most products of a dense column find
-// their bit already set), first touch of a word also sets its summary bit.
+// Marks row rr of the current tile (bitmap at shared address bmA): test
+// before set (a plain shared load is a broadcast for lanes hitting one word,
+// and most products of a dense column find their bit already set); the first
+// touch of a word also sets its summary bit (summary at sumA).
 template <bool SUMM>
-__device__ __forceinline__ void mark(unsigned* bm, unsigned* summ, int rr) {
+__device__ __forceinline__ void mark(unsigned bmA, unsigned sumA, int rr) {
     const int w = rr >> 5;
+    const unsigned a = bmA + (unsigned(w) << 2);
     const unsigned b = 1u << (rr & 31);
-    if (!(bm[w] & b)) {
-        const unsigned old = atomicOr(&bm[w], b);
-        if (SUMM && old == 0) atomicOr(&summ[w >> 5], 1u << (w & 31));
+    if (!(lds_u32(a) & b)) {
+        const unsigned old = atoms_or(a, b);
+        if (SUMM && old == 0) atoms_or(sumA + (unsigned(w >> 5) << 2), 1u << (w & 31));
     }
 }
 
@@ -102,6 +106,7 @@ __device__ __forceinline__ void tile_walk(const DevCsc& A, const DevCsc& B, cons
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t bs = B.cp[j], be = B.cp[j + 1];
     const int32_t* __restrict__ Arw = A.rw;
+    const unsigned bmA = smem_addr(bm), sumA = SUMM ? smem_addr(summ) : 0u;
     for (int64_t base = bs; base < be; base += NT) {
         const int64_t i = base + tid;
         int units = 0, len = 0;
@@ -113,7 +118,8 @@ __device__ __forceinline__ void tile_walk(const DevCsc& A, const DevCsc& B, cons
             s = A.cp[k] + lo;
             len = hi - lo;
             if (len < kShortRun) {
-                for (int q = 0; q < len; ++q) mark<SUMM>(bm, summ, __ldg(&Arw[s + q]) - t0);
+                const int32_t* q = Arw + s;
+                for (int x = 0; x < len; ++x) mark<SUMM>(bmA, sumA, __ldg(q + x) - t0);
                 len = 0;
             } else {
                 units = (len + kUnit - 1) / kUnit;
@@ -135,18 +141,16 @@ __device__ __forceinline__ void tile_walk(const DevCsc& A, const DevCsc& B, cons
                 else
                     hi = mid - 1;
             }
-            const int64_t ps = sh.start[lo] + int64_t(u - sh.ustart[lo]) * kUnit;
-            const int64_t pe = min(ps + kUnit, sh.start[lo] + sh.len[lo]);
-            for (int64_t p = ps + lane; p < pe; p += 32 * U) {
+            const int c0 = (u - sh.ustart[lo]) * kUnit;
+            const int32_t* run = Arw + sh.start[lo] + c0;
+            const int m = min(kUnit, sh.len[lo] - c0);
+            for (int x = lane; x < m; x += 32 * U) {
                 int r[U];
 #pragma unroll
-                for (int v = 0; v < U; ++v) {
-                    const int64_t q = p + 32 * v;
-                    r[v] = q < pe ? __ldg(&Arw[q]) : -1;
-                }
+                for (int v = 0; v < U; ++v) r[v] = x + 32 * v < m ? __ldg(run + x + 32 * v) : -1;
 #pragma unroll
                 for (int v = 0; v < U; ++v)
-                    if (r[v] >= 0) mark<SUMM>(bm, summ, r[v] - t0);
+                    if (r[v] >= 0) mark<SUMM>(bmA, sumA, r[v] - t0);
             }
         }
         __syncthreads();
@@ -289,14 +293,14 @@ __global__ void __launch_bounds__(NT) k_tile_direct(DirectArgs g) {
                 long long q0 = item - 1;
                 for (;;) {
                     const long long q = q0 - lane;
-                    const unsigned long long s = q >= 0 ? ld_acquire(&g.state[q]) : kFlagIncl;
+                    const unsigned long long s = q >= 0 ? ld_relaxed(&g.state[q]) : kFlagIncl;
                     const unsigned fl = (unsigned)(s >> 62);
                     const unsigned incl = __ballot_sync(0xffffffffu, fl == 2);
                     const unsigned ready = __ballot_sync(0xffffffffu, fl != 0);
                     const int L = incl ? __ffs(incl) - 1 : 31;
                     const unsigned need = L == 31 ? 0xffffffffu : ((2u << L) - 1u);
                     if ((ready & need) != need) {
-                        __nanosleep(64);
+                        __nanosleep(32);
                         continue;
                     }
                     unsigned long long v = lane <= L ? (s & kValMask) : 0ull;

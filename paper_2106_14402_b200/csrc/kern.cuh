@@ -326,10 +326,26 @@ __device__ __forceinline__ void walk_balanced_from(const DevCsc& A, const DevCsc
     __syncthreads();
 }
 
+// Position of the n-th (0-based) set bit of w (n < popc(w)): branch-free
+// halving on popcounts (the __fns intrinsic is a software loop on sm_100).
+__device__ __forceinline__ int nth_set_bit(unsigned w, int n) {
+    int pos = 0;
+#pragma unroll
+    for (int half = 16; half > 0; half >>= 1) {
+        const unsigned lo = w & ((1u << half) - 1u);
+        const int c = __popc(lo);
+        const bool up = n >= c;
+        n -= up ? c : 0;
+        pos += up ? half : 0;
+        w = up ? (w >> half) : lo;
+    }
+    return pos;
+}
+
 // Writes the set bits of a warp's 32 bitmap words (word w0+lane) as row ids
 // rb_lane + bit to out[base ...] in order, 32 consecutive entries per store:
 // output element o is found by a shuffle search for the lane whose exclusive
-// prefix covers o, then __fns for the bit.
+// prefix covers o, then the bit by popcount halving.
 __device__ __forceinline__ void emit_rows_coalesced(unsigned bits, int row_base, int32_t* __restrict__ out,
                                                     int lane) {
     int tot;
@@ -347,8 +363,23 @@ __device__ __forceinline__ void emit_rows_coalesced(unsigned bits, int row_base,
         const unsigned w = __shfl_sync(0xffffffffu, bits, lo);
         const int rb = __shfl_sync(0xffffffffu, row_base, lo);
         const int exl = __shfl_sync(0xffffffffu, ex, lo);
-        if (o < tot) out[o] = rb + (int)__fns(w, 0, o - exl + 1);
+        if (o < tot) out[o] = rb + nth_set_bit(w, o - exl);
     }
+}
+
+// 32-bit shared-window addresses and raw shared loads / atomics: the generic
+// pointer form makes the compiler rebuild the shared base (S2R + LEA) for
+// every product.
+__device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ unsigned lds_u32(unsigned a) {
+    unsigned v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned atoms_or(unsigned a, unsigned v) {
+    unsigned o;
+    asm volatile("atom.shared.or.b32 %0, [%1], %2;" : "=r"(o) : "r"(a), "r"(v) : "memory");
+    return o;
 }
 
 // Per-word exclusive popcount prefix of a W-word bitmap (the rank of every
