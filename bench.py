@@ -61,7 +61,7 @@ def parse():
     ap.add_argument("--method", default="direct", choices=["direct", "fused"],
                     help="direct: slapcu_spgemm_direct writes C in place in one pass; fused: begin/finish")
     ap.add_argument("--direct-tile-log2", type=int, default=0, help="rows per direct-path item (0 = default)")
-    ap.add_argument("--direct-dense-min", type=int, default=None, help="direct path: dense item threshold")
+    ap.add_argument("--direct-split", type=int, default=None, help="direct path: split items above this many flops")
     ap.add_argument("--streams", type=int, default=1, choices=[1, 2],
                     help="2: alternate column batches over two contexts/streams (async finish)")
     return ap.parse_args()
@@ -78,8 +78,8 @@ def apply_options(ctx, args):
         ctx.set_option(L.OPT_DENSE_FLOPS_MIN, args.dense_min)
     if args.direct_tile_log2:
         ctx.set_option(L.OPT_DIRECT_TILE_ROWS_LOG2, args.direct_tile_log2)
-    if args.direct_dense_min is not None:
-        ctx.set_option(L.OPT_DIRECT_DENSE_FLOPS_MIN, args.direct_dense_min)
+    if args.direct_split is not None:
+        ctx.set_option(L.OPT_DIRECT_SPLIT_FLOPS, args.direct_split)
 
 
 # ------------------------------------------------------------------ helpers

@@ -114,8 +114,8 @@ typedef enum {
                                          InternalError surfaces at the next call on the context
                                          or at slapcu_ctx_synchronize */
     SLAPCU_OPT_DIRECT_TILE_ROWS_LOG2 = 9,  /* direct path: rows per (column, row tile) item (default 17) */
-    SLAPCU_OPT_DIRECT_DENSE_FLOPS_MIN = 10 /* direct path: items with at least this many multiplies are
-                                              formed up front into global bitmaps (0 = never) */
+    SLAPCU_OPT_DIRECT_SPLIT_FLOPS = 10     /* direct path: items with more multiplies than this are formed
+                                              by several CTAs over equal-flops parts of B(:,j) (>= 1024) */
 } slapcu_option;
 slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t value);
 
@@ -176,11 +176,12 @@ slapcu_status slapcu_spgemm_finish(slapcu_ctx ctx, const slapcu_csc* A, const sl
                                    int32_t* c_rowids, void* c_vals);
 
 /* Single pass straight into caller buffers (the production path for the
- * Boolean C3 headline): C's colptr, rowids and values are written in place by
- * one walk over the products -- heavy columns are cut into (column, row
- * tile) items laid out in C order, each formed in a shared-memory bitmap and
- * given its output offset by a decoupled look-back, so there is no staging
- * copy and no second product pass.  `capacity` = entries the caller's
+ * Boolean C3 headline): C's colptr, rowids and values are written in place
+ * after one walk over the products -- heavy columns are cut into (column, row
+ * tile) items, each formed in a shared-memory bitmap and kept as a compact
+ * stash (bitmap or non-zero word list, ~1 byte per output entry), then placed
+ * by a scan of the item counts and expanded straight into C; there is no
+ * row-id staging copy and no second product pass.  `capacity` = entries the caller's
  * c_rowids / c_vals hold; sum_j min(flops_j, A.nrows) (from
  * slapcu_estimate_flops) always suffices.  If C needs more, nothing beyond
  * capacity is written, *c_nnz gets the exact requirement and the call

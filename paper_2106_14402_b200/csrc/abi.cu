@@ -142,9 +142,9 @@ slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t v
             require(v >= 10 && v <= 18, SLAPCU_ERR_INVALID, "direct tile rows log2 must be in 10..18");
             c.opt.direct_tile_rows_log2 = (int)v;
             break;
-        case SLAPCU_OPT_DIRECT_DENSE_FLOPS_MIN:
-            require(v >= 0, SLAPCU_ERR_INVALID, "dense flops threshold must be >= 0");
-            c.opt.direct_dense_flops_min = v;
+        case SLAPCU_OPT_DIRECT_SPLIT_FLOPS:
+            require(v >= 1024, SLAPCU_ERR_INVALID, "split threshold must be >= 1024");
+            c.opt.direct_split_flops = v;
             break;
         case SLAPCU_OPT_LIGHT_FLOPS_MAX: c.opt.light_flops_max = v; break;
         case SLAPCU_OPT_DETERMINISTIC: break;

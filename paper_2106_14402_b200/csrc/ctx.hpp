@@ -122,8 +122,8 @@ struct Options {
     int dense_tile_rows_log2 = 17;    // byte-flag tile height (128 KB of flags)
     bool async_finish = false;        // finish() returns without waiting (errors surface later)
     int direct_tile_rows_log2 = 17;   // direct path: row-tile height of an item (16 KB bitmap)
-    int64_t direct_dense_flops_min = 16384;  // direct path: items with >= this many multiplies are
-                                             // formed up front into global bitmaps (0 = never)
+    int64_t direct_split_flops = 262144;  // direct path: items above this many multiplies are
+                                          // formed by several CTAs (equal-flops B-entry parts)
 };
 
 // Workspace of the direct (in-place) path, kept across calls.
@@ -134,7 +134,7 @@ struct DirectCache {
     int64_t atp_ncols = -1, atp_nnz = -1;
     int atp_tl = -1;
     bool atp_valid = false;
-    DevBuf lp, hcnt, hl, items, dslot, dlist, state, gbm;
+    DevBuf lp, hcnt, hl, items, ifl, sres, soff, units, order, stash, partial, cnt, form, hoff;
     int64_t last_nnz = -1;  // exact nnz(C) of the last call (also on BudgetError)
 };
 

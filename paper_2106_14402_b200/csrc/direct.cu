@@ -1,29 +1,33 @@
-// direct.cu -- one-pass SpGEMM that writes C in place (no staging of heavy
-// columns).
+// direct.cu -- single product pass that writes C in place.
 //
 // The reference forms C in two passes, symbolic counts then numeric fill
 // (spgemm.hpp:286-330), so every product is walked twice.  fused.cu walks
-// once but stages every output column and copies it into place, which costs
-// 8 extra bytes of HBM traffic per output entry -- at R-MAT s20 that is more
-// than C itself.  Here heavy columns are cut into (column, row tile) items,
-// laid out in C order, and each item is formed in a shared-memory bitmap,
-// counted, given its output offset by a decoupled look-back over the items
-// before it, and emitted straight into C:
+// once but stages every output row id and copies it into place: 8 extra bytes
+// of HBM traffic per output entry, more than C itself (5 bytes for OrAnd).
+// Here heavy columns are cut into (column, row tile) ITEMS and the product
+// walk is decoupled from placement through a compact per-item stash:
 //
-//   A tile pointers   Atp[k][t] = first position of A(:,k) with row >= t*R
-//                     (per A, cached): an item walks exactly its rows of every
-//                     A(:,k), k in B(:,j), with no cursors and no searches.
-//   light columns     (flops <= L) shared-memory hash + sort (fused.cu), staged;
-//                     they hold ~1% of C and are copied at the end.
-//   dense items       (flops > H) formed first by k_tile_dense, kept as a
-//                     global bitmap (R/8 bytes) with their count pre-published,
-//                     so no item in the ordered pass waits behind a long one.
-//   k_tile_direct     persistent CTAs take items by ticket in C order: walk,
-//                     count (touched-word summary, so sparse items never scan
-//                     the whole bitmap), look back, emit rows + values.
-//   colptr            = exclusive scan of light + heavy per-column counts.
+//   A tile pointers  Atp[k][t] = first position of A(:,k) with row >= t*R
+//                    (per A, cached): an item walks exactly its rows of every
+//                    A(:,k), k in B(:,j) -- no cursors, no searches.
+//   form   (k_tile_form)  one CTA per work unit, heaviest first: shared-memory
+//                    bitmap of the tile (test-before-set atomics), then the
+//                    item's count and its stash in the smaller of two forms:
+//                    the whole bitmap (R/8 bytes) or the list of non-zero
+//                    words (6 bytes each).  Items with more than `split`
+//                    multiplies are cut by B entries into equal-flops parts
+//                    whose partial bitmaps are OR-ed by k_tile_combine.
+//   place  item offsets = exclusive scan of item counts (C order) + the light
+//                    prefix of the column; colptr = scan of per-column counts.
+//   emit   (k_tile_emit)  one CTA per item: expands the stash into sorted row
+//                    ids written straight into C (coalesced), values 1.
+//   light columns (flops <= L) use the shared hash of fused.cu, staged; they
+//                    hold ~1% of C and are copied into place at the end.
 //
-// Pattern semirings only (OrAnd); value semirings use fused.cu.
+// Stash traffic at R-MAT scale 16/20 is ~0.8 bytes per output entry (C's
+// words are dense: ~7 entries per touched 32-row word), against 8 for
+// staging row ids.  Pattern semirings only (OrAnd with all-one operands);
+// other semirings go through fused.cu with the same contract.
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -35,20 +39,10 @@ namespace slapcu {
 
 namespace {
 
-constexpr int kShortRun = 32;   // runs shorter than this are walked by one thread
-constexpr int kUnit = 512;      // products per warp work unit on long runs
-constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagIncl = 2ull << 62, kValMask = (1ull << 62) - 1;
+constexpr int kShortRun = 32;  // runs shorter than this are walked by one thread
+constexpr int kUnit = 1024;    // products per warp work unit on long runs
 
-__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-// Look-back reads only use the state word itself, so relaxed suffices (an
-// acquire load invalidates L1 on every spin).
-__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
+__host__ __device__ __forceinline__ int64_t lmin(int64_t a, int64_t b) { return a < b ? a : b; }
 
 // Exclusive block-wide scan of one int per thread; *total gets the sum.
 template <int NT>
@@ -69,49 +63,52 @@ __device__ __forceinline__ int block_excl_scan(int v, int* wsum, int* total) {
     __syncthreads();
     const int r = ex + wsum[warp];
     *total = wsum[NW];
+    __syncthreads();
     return r;
 }
 
 template <int NT>
 struct WalkSm {
     int wsum[NT / 32 + 1];
-    int ustart[NT];
+    int ustart[NT + 1];
     int len[NT];
     int64_t start[NT];
 };
 
 // Marks row rr of the current tile (bitmap at shared address bmA): test
-// before set (a plain shared load is a broadcast for lanes hitting one word,
-// and most products of a dense column find their bit already set); the first
-// touch of a word also sets its summary bit (summary at sumA).
-template <bool SUMM>
-__device__ __forceinline__ void mark(unsigned bmA, unsigned sumA, int rr) {
-    const int w = rr >> 5;
-    const unsigned a = bmA + (unsigned(w) << 2);
+// before set -- a plain shared load is a broadcast for lanes hitting one word,
+// and most products of a dense column find their bit already set.
+__device__ __forceinline__ void mark(unsigned bmA, int rr) {
+    const unsigned a = bmA + (unsigned(rr >> 5) << 2);
     const unsigned b = 1u << (rr & 31);
-    if (!(lds_u32(a) & b)) {
-        const unsigned old = atoms_or(a, b);
-        if (SUMM && old == 0) atoms_or(sumA + (unsigned(w >> 5) << 2), 1u << (w & 31));
-    }
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b32 x;\n\t"
+        "ld.shared.u32 x, [%0];\n\t"
+        "and.b32 x, x, %1;\n\t"
+        "setp.eq.u32 p, x, 0;\n\t"
+        "@p red.shared.or.b32 [%0], %1;\n\t}" ::"r"(a),
+        "r"(b)
+        : "memory");
 }
 
-// All products of item (column j of B, row tile t) into the tile bitmap.
-// B entries are taken NT at a time; a thread walks its own run when it is
-// short, long runs are cut into units of kUnit products that the warps walk
-// lane-strided with U loads in flight (coalesced, balanced across warps).
-template <int NT, int U, bool SUMM>
+// All products of B entries [b0, b1) (column j) whose rows lie in tile t,
+// into the tile bitmap.  Entries are taken NT at a time; a thread walks its
+// own run when it is short, long runs are cut into units of kUnit products
+// that the warps walk lane-strided with U loads in flight (coalesced,
+// balanced across warps; a warp's units are increasing, so the entry owning
+// a unit is found by advancing, not searching).
+template <int NT, int U>
 __device__ __forceinline__ void tile_walk(const DevCsc& A, const DevCsc& B, const int32_t* __restrict__ Atp, int T,
-                                          int j, int t, int t0, unsigned* bm, unsigned* summ, WalkSm<NT>& sh) {
+                                          int64_t b0, int64_t b1, int t, int t0, unsigned* bm, WalkSm<NT>& sh) {
     constexpr int NW = NT / 32;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t bs = B.cp[j], be = B.cp[j + 1];
     const int32_t* __restrict__ Arw = A.rw;
-    const unsigned bmA = smem_addr(bm), sumA = SUMM ? smem_addr(summ) : 0u;
-    for (int64_t base = bs; base < be; base += NT) {
+    const unsigned bmA = smem_addr(bm) - (unsigned(t0 >> 5) << 2);  // rows index the tile directly
+    for (int64_t base = b0; base < b1; base += NT) {
         const int64_t i = base + tid;
         int units = 0, len = 0;
         int64_t s = 0;
-        if (i < be) {
+        if (i < b1) {
             const int k = B.rw[i];
             const int32_t* tp = Atp + int64_t(k) * (T + 1) + t;
             const int lo = tp[0], hi = tp[1];
@@ -119,7 +116,7 @@ __device__ __forceinline__ void tile_walk(const DevCsc& A, const DevCsc& B, cons
             len = hi - lo;
             if (len < kShortRun) {
                 const int32_t* q = Arw + s;
-                for (int x = 0; x < len; ++x) mark<SUMM>(bmA, sumA, __ldg(q + x) - t0);
+                for (int x = 0; x < len; ++x) mark(bmA, __ldg(q + x));
                 len = 0;
             } else {
                 units = (len + kUnit - 1) / kUnit;
@@ -130,212 +127,246 @@ __device__ __forceinline__ void tile_walk(const DevCsc& A, const DevCsc& B, cons
         sh.ustart[tid] = ex;
         sh.len[tid] = len;
         sh.start[tid] = s;
+        if (tid == 0) sh.ustart[NT] = tot;
         __syncthreads();
+        int e = 0;
         for (int u = warp; u < tot; u += NW) {
-            // entry owning unit u: the last e with ustart[e] <= u
-            int lo = 0, hi = NT - 1;
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (sh.ustart[mid] <= u)
-                    lo = mid;
-                else
-                    hi = mid - 1;
-            }
-            const int c0 = (u - sh.ustart[lo]) * kUnit;
-            const int32_t* run = Arw + sh.start[lo] + c0;
-            const int m = min(kUnit, sh.len[lo] - c0);
-            for (int x = lane; x < m; x += 32 * U) {
+            while (sh.ustart[e + 1] <= u) ++e;  // entry owning unit u
+            const int c0 = (u - sh.ustart[e]) * kUnit;
+            const int32_t* run = Arw + sh.start[e] + c0;
+            const int m = min(kUnit, sh.len[e] - c0);
+            int x = lane;
+            for (; x + 32 * (U - 1) < m; x += 32 * U) {
                 int r[U];
 #pragma unroll
-                for (int v = 0; v < U; ++v) r[v] = x + 32 * v < m ? __ldg(run + x + 32 * v) : -1;
+                for (int v = 0; v < U; ++v) r[v] = __ldg(run + x + 32 * v);
 #pragma unroll
-                for (int v = 0; v < U; ++v)
-                    if (r[v] >= 0) mark<SUMM>(bmA, sumA, r[v] - t0);
+                for (int v = 0; v < U; ++v) mark(bmA, r[v]);
             }
+            for (; x < m; x += 32) mark(bmA, __ldg(run + x));
         }
         __syncthreads();
     }
 }
 
-// ------------------------------------------------------------ dense items
+// ------------------------------------------------------------------- form
 
-// One CTA per dense item: bitmap of the tile -> global (W words), count
-// pre-published into the look-back state as an aggregate.
-template <int NT>
-__global__ void __launch_bounds__(NT)
-    k_tile_dense(DevCsc A, DevCsc B, const int32_t* __restrict__ Atp, int T, int TL, const int2* __restrict__ items,
-                 const int* __restrict__ dlist, unsigned* __restrict__ gbm, unsigned long long* __restrict__ state) {
-    extern __shared__ __align__(16) unsigned bm[];
-    __shared__ WalkSm<NT> sh;
-    __shared__ int red[NT / 32];
-    const int W = 1 << (TL - 5);
-    const int item = dlist[blockIdx.x];
-    const int2 it = items[item];
-    smem_zero(bm, W);
-    __syncthreads();
-    tile_walk<NT, 4, false>(A, B, Atp, T, it.x, it.y, it.y << TL, bm, nullptr, sh);
-    uint4* dst = reinterpret_cast<uint4*>(gbm + int64_t(blockIdx.x) * W);
-    const uint4* src = reinterpret_cast<const uint4*>(bm);
-    int cnt = 0;
-    for (int q = threadIdx.x; q < W / 4; q += NT) {
-        const uint4 x = src[q];
-        dst[q] = x;
-        cnt += __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
-    }
-    cnt = warp_reduce_sum(cnt);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cnt;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        long long s = 0;
-        for (int w = 0; w < NT / 32; ++w) s += red[w];
-        state[item] = kFlagAgg | (unsigned long long)s;
-    }
-}
-
-// ------------------------------------------------------------ ordered pass
-
-struct DirectArgs {
+struct FormArgs {
     DevCsc A, B;
     const int32_t* Atp;
     int T, TL;
-    const int2* items;
-    const int* dslot;  // per item: slot in gbm, or -1
-    int nitems;
-    const unsigned* gbm;
-    unsigned long long* state;
-    int* ticket;
-    const int64_t* lp;  // light prefix per column
-    unsigned long long* hcnt;  // heavy entries per column
-    int32_t* crw;
-    uint8_t* cv;
-    int64_t capacity;
-    int* overflow;
+    const int2* items;      // (column, tile) in C order
+    const int4* units;      // (item, b0, b1 relative to B.cp[j], partial slot or -1)
+    const int* order;       // units, heaviest first
+    unsigned* stash;        // per item: bitmap or word list
+    const int64_t* soff;    // stash offset per item (words)
+    const int64_t* sres;    // stash words reserved per item
+    unsigned* partial;      // partial bitmaps of split items (W words per slot)
+    int64_t* cnt;           // output entries per item
+    int* form;              // -1 bitmap, else number of listed words
+    unsigned long long* hcnt;  // output entries per column (heavy part)
 };
 
+// Count, choose the stash form and write it (whole CTA; bm holds the item's
+// tile bitmap).  `chunk` has W/32 + 1 ints of shared scratch.
 template <int NT>
-__global__ void __launch_bounds__(NT) k_tile_direct(DirectArgs g) {
+__device__ __forceinline__ void stash_bitmap(const unsigned* bm, int W, int* chunk, int* red, int64_t item, int j,
+                                             unsigned* stash, int64_t sres, int64_t* cnt, int* form,
+                                             unsigned long long* hcnt) {
     constexpr int NW = NT / 32;
-    extern __shared__ __align__(16) unsigned char sm_raw[];
-    const int W = 1 << (g.TL - 5), WS = W >> 5;
-    unsigned* bm = reinterpret_cast<unsigned*>(sm_raw);
-    unsigned* summ = bm + W;                                       // [WS]
-    int* chunk = reinterpret_cast<int*>(summ + WS);                // [W/32 + 1] chunk bases
-    uint16_t* tl = reinterpret_cast<uint16_t*>(chunk + W / 32 + 1);  // [W] touched words
-    __shared__ WalkSm<NT> sh;
-    __shared__ int item_sh, ntouch_sh;
-    __shared__ unsigned long long excl_sh;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    smem_zero(bm, W + WS);
+    const int nch = W >> 5;
+    int myc = 0;
+    for (int cc = warp; cc < nch; cc += NW) {
+        const unsigned x = bm[cc * 32 + lane];
+        const unsigned nz = __ballot_sync(0xffffffffu, x != 0u);
+        myc += __popc(x);
+        if (lane == 0) chunk[cc] = __popc(nz);
+    }
+    myc = warp_reduce_sum(myc);
+    if (lane == 0) red[warp] = myc;
     __syncthreads();
-    for (;;) {
-        if (tid == 0) item_sh = atomicAdd(g.ticket, 1);
-        __syncthreads();
-        const int item = item_sh;
-        if (item >= g.nitems) break;
-        const int2 it = g.items[item];
-        const int j = it.x, t = it.y, t0 = t << g.TL;
-        const int ds = g.dslot[item];
-        if (ds < 0) {
-            tile_walk<NT, 4, true>(g.A, g.B, g.Atp, g.T, j, t, t0, bm, summ, sh);
-        } else {
-            const uint4* src = reinterpret_cast<const uint4*>(g.gbm + int64_t(ds) * W);
-            uint4* d4 = reinterpret_cast<uint4*>(bm);
-            for (int q = tid; q < W / 4; q += NT) d4[q] = src[q];
-            for (int q = tid; q < WS; q += NT) summ[q] = ~0u;
-            __syncthreads();
+    if (warp == 0) {
+        int run = 0;
+        for (int b0 = 0; b0 < nch; b0 += 32) {
+            const int cix = b0 + lane;
+            const int x = cix < nch ? chunk[cix] : 0;
+            int tt;
+            const int e = warp_excl_scan(x, lane, &tt);
+            if (cix < nch) chunk[cix] = run + e;
+            run += tt;
         }
-        // touched words in order: summary popcounts -> scan -> list
-        {
-            unsigned s = 0;
-            int c = 0;
-            for (int q = tid; q < WS; q += NT) {  // WS <= NT for TL <= 5 + 5 + log2(NT)
-                s = summ[q];
-                c = __popc(s);
-            }
-            int tot;
-            int base = block_excl_scan<NT>(c, sh.wsum, &tot);
-            if (tid < WS) {
-                while (s) {
-                    const int b = __ffs(s) - 1;
-                    s &= s - 1;
-                    tl[base++] = (uint16_t)(tid * 32 + b);
-                }
-            }
-            if (tid == 0) ntouch_sh = tot;
-            __syncthreads();
-        }
-        const int U = ntouch_sh;
-        const int nch = (U + 31) >> 5;
+        if (lane == 0) chunk[nch] = run;
+    }
+    __syncthreads();
+    const int U = chunk[nch];
+    const int64_t lw = int64_t(U) + (U + 1) / 2;  // words + 16-bit word indices
+    const bool list = lw < W && lw <= sres;
+    if (list) {
+        uint16_t* idx = reinterpret_cast<uint16_t*>(stash + U);
         for (int cc = warp; cc < nch; cc += NW) {
-            const int u = cc * 32 + lane;
-            int x = u < U ? __popc(bm[tl[u]]) : 0;
-            x = warp_reduce_sum(x);
-            if (lane == 0) chunk[cc] = x;
-        }
-        __syncthreads();
-        if (warp == 0) {
-            int run = 0;
-            for (int b0 = 0; b0 < nch; b0 += 32) {
-                const int cix = b0 + lane;
-                const int x = cix < nch ? chunk[cix] : 0;
-                int tt;
-                const int e = warp_excl_scan(x, lane, &tt);
-                if (cix < nch) chunk[cix] = run + e;
-                run += tt;
-            }
-            const unsigned long long cnt = (unsigned long long)run;
-            // decoupled look-back over the items before this one (C order)
-            unsigned long long excl = 0;
-            if (item == 0) {
-                if (lane == 0) st_release(&g.state[0], kFlagIncl | cnt);
-            } else {
-                if (ds < 0 && lane == 0) st_release(&g.state[item], kFlagAgg | cnt);
-                long long q0 = item - 1;
-                for (;;) {
-                    const long long q = q0 - lane;
-                    const unsigned long long s = q >= 0 ? ld_relaxed(&g.state[q]) : kFlagIncl;
-                    const unsigned fl = (unsigned)(s >> 62);
-                    const unsigned incl = __ballot_sync(0xffffffffu, fl == 2);
-                    const unsigned ready = __ballot_sync(0xffffffffu, fl != 0);
-                    const int L = incl ? __ffs(incl) - 1 : 31;
-                    const unsigned need = L == 31 ? 0xffffffffu : ((2u << L) - 1u);
-                    if ((ready & need) != need) {
-                        __nanosleep(32);
-                        continue;
-                    }
-                    unsigned long long v = lane <= L ? (s & kValMask) : 0ull;
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                    excl += v;
-                    if (incl) break;
-                    q0 -= 32;
-                }
-                if (lane == 0) st_release(&g.state[item], kFlagIncl | (excl + cnt));
-            }
-            if (lane == 0) {
-                excl_sh = excl;
-                chunk[nch] = run;
-                atomicAdd(&g.hcnt[j], cnt);
+            const unsigned x = bm[cc * 32 + lane];
+            const unsigned nz = __ballot_sync(0xffffffffu, x != 0u);
+            if (x) {
+                const int pos = chunk[cc] + __popc(nz & ((1u << lane) - 1u));
+                stash[pos] = x;
+                idx[pos] = (uint16_t)(cc * 32 + lane);
             }
         }
-        __syncthreads();
-        const int cnt = chunk[nch];
-        const int64_t off = g.lp[j] + (int64_t)excl_sh;
-        if (off + cnt <= g.capacity) {
-            for (int cc = warp; cc < nch; cc += NW) {
-                const int u = cc * 32 + lane;
-                const int w = u < U ? tl[u] : 0;
-                emit_rows_coalesced(u < U ? bm[w] : 0u, t0 + (w << 5), g.crw + off + chunk[cc], lane);
-            }
-            if (g.cv)
-                for (int q = tid; q < cnt; q += NT) g.cv[off + q] = 1;
-        } else if (tid == 0) {
-            atomicExch(g.overflow, 1);
+    } else {
+        uint4* d4 = reinterpret_cast<uint4*>(stash);
+        const uint4* s4 = reinterpret_cast<const uint4*>(bm);
+        for (int q = tid; q < W / 4; q += NT) d4[q] = s4[q];
+    }
+    if (tid == 0) {
+        long long c = 0;
+        for (int w = 0; w < NW; ++w) c += red[w];
+        cnt[item] = c;
+        form[item] = list ? U : -1;
+        atomicAdd(&hcnt[j], (unsigned long long)c);
+    }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_tile_form(FormArgs g) {
+    extern __shared__ __align__(16) unsigned char sm_raw[];
+    const int W = 1 << (g.TL - 5);
+    unsigned* bm = reinterpret_cast<unsigned*>(sm_raw);
+    int* chunk = reinterpret_cast<int*>(bm + W);  // [W/32 + 1]
+    __shared__ WalkSm<NT> sh;
+    __shared__ int red[NT / 32];
+    const int4 u = g.units[g.order[blockIdx.x]];
+    const int2 it = g.items[u.x];
+    const int64_t bs = g.B.cp[it.x];
+    smem_zero(bm, W);
+    __syncthreads();
+    tile_walk<NT, 4>(g.A, g.B, g.Atp, g.T, bs + u.y, bs + u.z, it.y, it.y << g.TL, bm, sh);
+    if (u.w >= 0) {  // one part of a split item: partial bitmap out
+        uint4* d4 = reinterpret_cast<uint4*>(g.partial + int64_t(u.w) * W);
+        const uint4* s4 = reinterpret_cast<const uint4*>(bm);
+        for (int q = threadIdx.x; q < W / 4; q += NT) d4[q] = s4[q];
+        return;
+    }
+    stash_bitmap<NT>(bm, W, chunk, red, u.x, it.x, g.stash + g.soff[u.x], g.sres[u.x], g.cnt, g.form, g.hcnt);
+}
+
+// OR of the partial bitmaps of each split item -> its stash (bitmap or list).
+template <int NT>
+__global__ void __launch_bounds__(NT)
+    k_tile_combine(int TL, const int2* __restrict__ items, const int* __restrict__ sitems,
+                   const int* __restrict__ spart, const int* __restrict__ snp, const unsigned* __restrict__ partial,
+                   unsigned* __restrict__ stash, const int64_t* __restrict__ soff, const int64_t* __restrict__ sres,
+                   int64_t* __restrict__ cnt, int* __restrict__ form, unsigned long long* __restrict__ hcnt) {
+    extern __shared__ __align__(16) unsigned char sm_raw[];
+    const int W = 1 << (TL - 5);
+    unsigned* bm = reinterpret_cast<unsigned*>(sm_raw);
+    int* chunk = reinterpret_cast<int*>(bm + W);
+    __shared__ int red[NT / 32];
+    const int item = sitems[blockIdx.x];
+    const int np = snp[blockIdx.x];
+    const uint4* p4 = reinterpret_cast<const uint4*>(partial + int64_t(spart[blockIdx.x]) * W);
+    uint4* b4 = reinterpret_cast<uint4*>(bm);
+    for (int q = threadIdx.x; q < W / 4; q += NT) {
+        uint4 x = p4[q];
+        for (int p = 1; p < np; ++p) {
+            const uint4 y = p4[int64_t(p) * (W / 4) + q];
+            x.x |= y.x;
+            x.y |= y.y;
+            x.z |= y.z;
+            x.w |= y.w;
         }
-        __syncthreads();
-        for (int u = tid; u < U; u += NT) bm[tl[u]] = 0u;
-        for (int q = tid; q < WS; q += NT) summ[q] = 0u;
-        __syncthreads();
+        b4[q] = x;
+    }
+    __syncthreads();
+    stash_bitmap<NT>(bm, W, chunk, red, item, items[item].x, stash + soff[item], sres[item], cnt, form, hcnt);
+}
+
+// ------------------------------------------------------------------- emit
+
+struct EmitArgs {
+    const int2* items;
+    const int64_t* cnt;
+    const int* form;
+    const unsigned* stash;
+    const int64_t* soff;
+    const int64_t* hoff;  // exclusive scan of cnt over items
+    const int64_t* lp;    // light prefix per column
+    int TL;
+    int32_t* crw;
+    uint8_t* cv;
+};
+
+// Rows of one chunk of 32 words (lane's word x, rows rb + bit) to out[...] in
+// order.  Dense chunks: word by word, lane b writes bit b (coalesced runs);
+// sparse chunks: one output per lane per step, source found by shuffles.
+__device__ __forceinline__ void emit_chunk(unsigned x, int rb, int tot, int32_t* __restrict__ out, int lane) {
+    if (tot >= 256) {
+        int all;
+        const int ex = warp_excl_scan(__popc(x), lane, &all);
+        const unsigned below = (1u << lane) - 1u;
+        for (int k = 0; k < 32; ++k) {
+            const unsigned wk = __shfl_sync(0xffffffffu, x, k);
+            const int ek = __shfl_sync(0xffffffffu, ex, k);
+            const int rk = __shfl_sync(0xffffffffu, rb, k);
+            if ((wk >> lane) & 1u) out[ek + __popc(wk & below)] = rk + lane;
+        }
+    } else {
+        emit_rows_coalesced(x, rb, out, lane);
+    }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_tile_emit(EmitArgs g) {
+    constexpr int NW = NT / 32;
+    extern __shared__ int chunk[];  // [W/32 + 1]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int item = blockIdx.x;
+    const int2 it = g.items[item];
+    const int64_t c = g.cnt[item];
+    const int64_t off = g.lp[it.x] + g.hoff[item];
+    const int U = g.form[item];
+    const int W = 1 << (g.TL - 5);
+    const int nwords = U >= 0 ? U : W;
+    const unsigned* words = g.stash + g.soff[item];
+    const uint16_t* idx = U >= 0 ? reinterpret_cast<const uint16_t*>(words + U) : nullptr;
+    const int nch = (nwords + 31) >> 5;
+    const int t0 = it.y << g.TL;
+    for (int cc = warp; cc < nch; cc += NW) {
+        const int w = cc * 32 + lane;
+        int x = w < nwords ? __popc(words[w]) : 0;
+        x = warp_reduce_sum(x);
+        if (lane == 0) chunk[cc] = x;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        int run = 0;
+        for (int b0 = 0; b0 < nch; b0 += 32) {
+            const int cix = b0 + lane;
+            const int x = cix < nch ? chunk[cix] : 0;
+            int tt;
+            const int e = warp_excl_scan(x, lane, &tt);
+            if (cix < nch) chunk[cix] = run + e;
+            run += tt;
+        }
+        if (lane == 0) chunk[nch] = run;
+    }
+    __syncthreads();
+    for (int cc = warp; cc < nch; cc += NW) {
+        const int w = cc * 32 + lane;
+        const unsigned x = w < nwords ? words[w] : 0u;
+        const int wi = idx ? (w < nwords ? idx[w] : 0) : w;
+        const int tot = chunk[cc + 1] - chunk[cc];
+        if (tot) emit_chunk(x, t0 + (wi << 5), tot, g.crw + off + chunk[cc], lane);
+    }
+    if (g.cv) {
+        // values: c bytes of 1 (head bytes, 16-byte body, tail bytes)
+        uint8_t* v = g.cv + off;
+        const int64_t head = lmin(c, (16 - (reinterpret_cast<uintptr_t>(v) & 15)) & 15);
+        for (int64_t q = tid; q < head; q += NT) v[q] = 1;
+        const int64_t body = (c - head) >> 4;
+        uint4* v4 = reinterpret_cast<uint4*>(v + head);
+        for (int64_t q = tid; q < body; q += NT) v4[q] = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
+        for (int64_t q = head + (body << 4) + tid; q < c; q += NT) v[q] = 1;
     }
 }
 
@@ -368,10 +399,10 @@ __global__ void k_tile_ptr(DevCsc A, int TL, int T, int32_t* __restrict__ Atp) {
     }
 }
 
-// Per heavy column (in column order) and tile: multiplies, and the number of
-// tiles with work.  One warp per column.
-__global__ void k_item_flops(DevCsc A, DevCsc B, const int32_t* __restrict__ Atp, int T, const int* __restrict__ hl,
-                             int nh, int64_t* __restrict__ iflops, int64_t* __restrict__ nit) {
+// Per heavy column (column order) and tile: multiplies, and the number of
+// tiles with work.  One warp per column, 8 tiles per pass over B(:,j).
+__global__ void k_item_flops(DevCsc B, const int32_t* __restrict__ Atp, int T, const int* __restrict__ hl, int nh,
+                             int64_t* __restrict__ iflops, int64_t* __restrict__ nit) {
     const int lane = threadIdx.x & 31;
     const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -379,49 +410,128 @@ __global__ void k_item_flops(DevCsc A, DevCsc B, const int32_t* __restrict__ Atp
         const int j = hl[h];
         const int64_t bs = B.cp[j], be = B.cp[j + 1];
         int64_t items = 0;
-        for (int t = 0; t < T; ++t) {
-            long long f = 0;
+        for (int tb = 0; tb < T; tb += 8) {
+            long long f[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            const int nt = min(8, T - tb);
             for (int64_t i = bs + lane; i < be; i += 32) {
-                const int32_t* tp = Atp + int64_t(B.rw[i]) * (T + 1) + t;
-                f += tp[1] - tp[0];
+                const int32_t* tp = Atp + int64_t(B.rw[i]) * (T + 1) + tb;
+                int prev = tp[0];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if (q < nt) {
+                        const int nx = tp[q + 1];
+                        f[q] += nx - prev;
+                        prev = nx;
+                    }
+                }
             }
-            f = warp_reduce_sum64(f);
-            if (lane == 0) iflops[h * T + t] = f;
-            items += f > 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                if (q < nt) {
+                    const long long s = warp_reduce_sum64(f[q]);
+                    if (lane == 0) iflops[h * T + tb + q] = s;
+                    items += s > 0;
+                }
+            }
         }
         if (lane == 0) nit[h] = items;
     }
 }
 
-__global__ void k_item_fill(const int* __restrict__ hl, int nh, int T, const int64_t* __restrict__ iflops,
-                            const int64_t* __restrict__ ioff, int64_t dense_min, int2* __restrict__ items,
-                            int* __restrict__ dflag) {
+// Items in C order; per item its work-unit count (split when above `split`
+// multiplies), stash reservation and partial-slot count.
+__global__ void k_item_fill(const int* __restrict__ hl, int nh, int T, int W, const int64_t* __restrict__ iflops,
+                            const int64_t* __restrict__ ioff, int64_t split, int max_parts, int2* __restrict__ items,
+                            int64_t* __restrict__ ifl, int64_t* __restrict__ np, int64_t* __restrict__ sres,
+                            int64_t* __restrict__ pslots) {
     for (int64_t h = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; h < nh; h += int64_t(gridDim.x) * blockDim.x) {
         int64_t o = ioff[h];
         const int j = hl[h];
         for (int t = 0; t < T; ++t) {
             const int64_t f = iflops[h * T + t];
-            if (f > 0) {
-                items[o] = make_int2(j, t);
-                dflag[o] = f >= dense_min ? 1 : 0;
-                ++o;
-            }
+            if (f <= 0) continue;
+            items[o] = make_int2(j, t);
+            ifl[o] = f;
+            const int64_t p = f > split ? lmin(max_parts, (f + split - 1) / split) : 1;
+            np[o] = p;
+            pslots[o] = p > 1 ? p : 0;
+            // 4-word multiples keep every stash 16-byte aligned (bitmap copies are uint4)
+            sres[o] = p > 1 ? W : (lmin(W, (3 * lmin(f, W) + 1) / 2 + 1) + 3) & ~int64_t(3);
+            ++o;
         }
     }
 }
 
-// dslot[i] = exclusive prefix of dflag at dense items, -1 elsewhere; dlist
-// inverts it.
-__global__ void k_dense_slots(int n, const int* __restrict__ dflag, const int* __restrict__ dpre,
-                              int* __restrict__ dslot, int* __restrict__ dlist) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        if (dflag[i]) {
-            dslot[i] = dpre[i];
-            dlist[dpre[i]] = i;
-        } else {
-            dslot[i] = -1;
+// Work units: split items get equal-flops B-entry ranges (one CTA per split
+// item scans its column's run lengths); others one unit for the whole column.
+template <int NT>
+__global__ void __launch_bounds__(NT)
+    k_unit_fill(DevCsc B, const int32_t* __restrict__ Atp, int T, int nitems, const int2* __restrict__ items,
+                const int64_t* __restrict__ ifl, const int64_t* __restrict__ np, const int64_t* __restrict__ uoff,
+                const int64_t* __restrict__ poff, int4* __restrict__ units, int64_t* __restrict__ ukey) {
+    __shared__ int wsum[NT / 32 + 1];
+    __shared__ long long run_sh;
+    const int item = blockIdx.x;
+    const int2 it = items[item];
+    const int64_t p = np[item];
+    const int64_t bs = B.cp[it.x], be = B.cp[it.x + 1];
+    const int64_t u0 = uoff[item];
+    const int64_t f = ifl[item];
+    if (p == 1) {
+        if (threadIdx.x == 0) {
+            units[u0] = make_int4(item, 0, (int)(be - bs), -1);
+            ukey[u0] = f;
+        }
+        return;
+    }
+    // boundaries: part q ends after the entry whose inclusive flops prefix first reaches ceil(q*f/p)
+    if (threadIdx.x == 0) run_sh = 0;
+    __shared__ int bnd[65];
+    if (threadIdx.x <= p) bnd[threadIdx.x] = threadIdx.x == p ? (int)(be - bs) : 0;
+    __syncthreads();
+    for (int64_t base = bs; base < be; base += NT) {
+        const int64_t i = base + threadIdx.x;
+        int len = 0;
+        if (i < be) {
+            const int32_t* tp = Atp + int64_t(B.rw[i]) * (T + 1) + it.y;
+            len = tp[1] - tp[0];
+        }
+        int tot;
+        const long long ex = (long long)block_excl_scan<NT>(len, wsum, &tot) + run_sh;
+        const long long in = ex + len;
+        if (len > 0) {
+            // parts q (1..p-1) with target in (ex, in]
+            for (int64_t q = 1; q < p; ++q) {
+                const long long tg = (q * f + p - 1) / p;
+                if (tg > ex && tg <= in) bnd[q] = (int)(i - bs + 1);
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) run_sh += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x < p) {
+        const int lo = bnd[threadIdx.x], hi = max(lo, bnd[threadIdx.x + 1]);
+        units[u0 + threadIdx.x] = make_int4(item, lo, hi, (int)(poff[item] + threadIdx.x));
+        ukey[u0 + threadIdx.x] = f / p;
+    }
+}
+
+__global__ void k_split_list(int nitems, const int64_t* __restrict__ np, const int64_t* __restrict__ poff,
+                             int* __restrict__ sitems, int* __restrict__ spart, int* __restrict__ snp,
+                             int* __restrict__ nsplit) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nitems; i += gridDim.x * blockDim.x) {
+        if (np[i] > 1) {
+            const int s = atomicAdd(nsplit, 1);
+            sitems[s] = i;
+            spart[s] = (int)poff[i];
+            snp[s] = (int)np[i];
         }
     }
+}
+
+__global__ void k_iota(int n, int* __restrict__ v) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) v[i] = i;
 }
 
 __global__ void k_add_counts(int64_t n, const int64_t* __restrict__ a, const unsigned long long* __restrict__ b,
@@ -458,13 +568,14 @@ T d2h(Ctx& c, const T* p) {
     return v;
 }
 
-constexpr int kDirectThreads = 256;
-constexpr int kDenseThreads = 512;
+constexpr int kFormThreads = 256;
+constexpr int kEmitThreads = 256;
+constexpr int kMaxParts = 64;
 
 }  // namespace
 
 int direct_tile_log2(const Ctx& c, int64_t nrows) {
-    int tl = std::min(c.opt.direct_tile_rows_log2, 18);  // summary words <= threads per CTA
+    int tl = c.opt.direct_tile_rows_log2;
     while (tl > 10 && (int64_t(1) << (tl - 1)) >= nrows) --tl;
     return tl;
 }
@@ -519,7 +630,6 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
     any_zero_u8(c, (const uint8_t*)A.v + A.base, A.span, fl + 1);
     any_zero_u8(c, (const uint8_t*)B.v + B.base, B.span, fl + 1);
     if (d2h(c, fl + 1) != 0) return direct_fallback(c, A_, B_, sr, alg, capacity, c_colptr, crw, cv);
-    const bool ones = true;
     SLAPCU_CUDA(cudaEventRecord(c.ev[0], c.stream));
     DirectCache& d = c.direct;
     FusedState& f = d.light;
@@ -554,7 +664,7 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
         const int nb = f.bins.count[b];
         if (!nb) continue;
         KScope ks(c, KC_SYM_LIGHT);
-        fused_light_launch(c, sr, ones, b, A, B, L + f.bins.offset[b], nb, flops, f);
+        fused_light_launch(c, sr, true, b, A, B, L + f.bins.offset[b], nb, flops, f);
     }
     // light prefix per column (heavy columns count 0 here)
     d.lp.reset(sizeof(int64_t) * (n + 1), c.stream);
@@ -570,10 +680,7 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
     const int W = 1 << (TL - 5);
     d.hcnt.reset(sizeof(unsigned long long) * std::max<int64_t>(n, 1), c.stream);
     SLAPCU_CUDA(cudaMemsetAsync(d.hcnt.get(), 0, sizeof(unsigned long long) * std::max<int64_t>(n, 1), c.stream));
-    DevBuf misc(sizeof(int) * 4, c.stream);
-    SLAPCU_CUDA(cudaMemsetAsync(misc.get(), 0, sizeof(int) * 4, c.stream));
-    int* ticket = misc.as<int>();
-    int* overflow = misc.as<int>() + 1;
+    int nitems = 0;
     if (nh > 0) {
         const int32_t* Atp = tile_pointers(c, A, TL, T);
         KScope ks(c, KC_BIN);
@@ -587,53 +694,95 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
         DevBuf iflops(sizeof(int64_t) * int64_t(nh) * T, c.stream);
         DevBuf nit(sizeof(int64_t) * (nh + 1), c.stream), ioff(sizeof(int64_t) * (nh + 1), c.stream);
         SLAPCU_CUDA(cudaMemsetAsync(nit.as<int64_t>() + nh, 0, sizeof(int64_t), c.stream));
-        launch(c, k_item_flops, dim3(grid_for(c, int64_t(nh) * 32, 256)), dim3(256), 0, A, B, Atp, T,
+        launch(c, k_item_flops, dim3(grid_for(c, int64_t(nh) * 32, 256)), dim3(256), 0, B, Atp, T,
                (const int*)d.hl.as<int>(), nh, iflops.as<int64_t>(), nit.as<int64_t>());
         exclusive_scan_i64(c, nit.as<int64_t>(), ioff.as<int64_t>(), nh + 1);
         const int64_t nitems64 = d2h(c, ioff.as<int64_t>() + nh);
         if (nitems64 > INT32_MAX) throw Fail{SLAPCU_ERR_INVALID, "too many tile items"};
-        const int nitems = (int)nitems64;
-        d.items.reset(sizeof(int2) * std::max(nitems, 1), c.stream);
-        DevBuf dflag(sizeof(int) * (nitems + 1), c.stream), dpre(sizeof(int) * (nitems + 1), c.stream);
-        SLAPCU_CUDA(cudaMemsetAsync(dflag.as<int>() + nitems, 0, sizeof(int), c.stream));
-        const int64_t dense_min = c.opt.direct_dense_flops_min > 0 ? c.opt.direct_dense_flops_min : INT64_MAX;
-        launch(c, k_item_fill, dim3(grid_for(c, nh, 256)), dim3(256), 0, (const int*)d.hl.as<int>(), nh, T,
-               (const int64_t*)iflops.as<int64_t>(), (const int64_t*)ioff.as<int64_t>(), dense_min,
-               d.items.as<int2>(), dflag.as<int>());
-        excl_scan_i32(c, dflag.as<int>(), dpre.as<int>(), nitems + 1);
-        const int ndense = d2h(c, dpre.as<int>() + nitems);
-        d.dslot.reset(sizeof(int) * std::max(nitems, 1), c.stream);
-        d.dlist.reset(sizeof(int) * std::max(ndense, 1), c.stream);
-        launch(c, k_dense_slots, dim3(grid_for(c, nitems, 256)), dim3(256), 0, nitems, (const int*)dflag.as<int>(),
-               (const int*)dpre.as<int>(), d.dslot.as<int>(), d.dlist.as<int>());
-        d.state.reset(sizeof(unsigned long long) * std::max(nitems, 1), c.stream);
-        SLAPCU_CUDA(cudaMemsetAsync(d.state.get(), 0, sizeof(unsigned long long) * std::max(nitems, 1), c.stream));
-        d.gbm.reset(sizeof(unsigned) * size_t(W) * std::max(ndense, 1), c.stream);
-        KScope ks2(c, KC_SYM_HEAVY);
-        if (ndense > 0) {
-            const size_t smem = sizeof(unsigned) * W;
-            auto go = [&](auto k) {
-                ensure_smem(k, smem);
-                launch(c, k, dim3(ndense), dim3(kDenseThreads), smem, A, B, Atp, T, TL, (const int2*)d.items.as<int2>(),
-                       (const int*)d.dlist.as<int>(), d.gbm.as<unsigned>(), d.state.as<unsigned long long>());
-            };
-            go(k_tile_dense<kDenseThreads>);
+        nitems = (int)nitems64;
+        const size_t ni1 = size_t(nitems) + 1;
+        d.items.reset(sizeof(int2) * ni1, c.stream);
+        d.ifl.reset(sizeof(int64_t) * ni1, c.stream);
+        DevBuf np(sizeof(int64_t) * ni1, c.stream), uoff(sizeof(int64_t) * ni1, c.stream);
+        DevBuf psl(sizeof(int64_t) * ni1, c.stream), poff(sizeof(int64_t) * ni1, c.stream);
+        d.sres.reset(sizeof(int64_t) * ni1, c.stream);
+        d.soff.reset(sizeof(int64_t) * ni1, c.stream);
+        SLAPCU_CUDA(cudaMemsetAsync(np.as<int64_t>() + nitems, 0, sizeof(int64_t), c.stream));
+        SLAPCU_CUDA(cudaMemsetAsync(psl.as<int64_t>() + nitems, 0, sizeof(int64_t), c.stream));
+        SLAPCU_CUDA(cudaMemsetAsync(d.sres.as<int64_t>() + nitems, 0, sizeof(int64_t), c.stream));
+        const int64_t split = std::max<int64_t>(c.opt.direct_split_flops, 1024);
+        launch(c, k_item_fill, dim3(grid_for(c, nh, 256)), dim3(256), 0, (const int*)d.hl.as<int>(), nh, T, W,
+               (const int64_t*)iflops.as<int64_t>(), (const int64_t*)ioff.as<int64_t>(), split, kMaxParts,
+               d.items.as<int2>(), d.ifl.as<int64_t>(), np.as<int64_t>(), d.sres.as<int64_t>(), psl.as<int64_t>());
+        exclusive_scan_i64(c, np.as<int64_t>(), uoff.as<int64_t>(), nitems + 1);
+        exclusive_scan_i64(c, psl.as<int64_t>(), poff.as<int64_t>(), nitems + 1);
+        exclusive_scan_i64(c, d.sres.as<int64_t>(), d.soff.as<int64_t>(), nitems + 1);
+        int64_t tail[3];
+        SLAPCU_CUDA(cudaMemcpyAsync(&tail[0], uoff.as<int64_t>() + nitems, 8, cudaMemcpyDeviceToHost, c.stream));
+        SLAPCU_CUDA(cudaMemcpyAsync(&tail[1], poff.as<int64_t>() + nitems, 8, cudaMemcpyDeviceToHost, c.stream));
+        SLAPCU_CUDA(cudaMemcpyAsync(&tail[2], d.soff.as<int64_t>() + nitems, 8, cudaMemcpyDeviceToHost, c.stream));
+        SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+        const int64_t nunits = tail[0], nslots = tail[1], swords = tail[2];
+        if (nunits > INT32_MAX || nslots > INT32_MAX) throw Fail{SLAPCU_ERR_INVALID, "too many work units"};
+        d.units.reset(sizeof(int4) * std::max<int64_t>(nunits, 1), c.stream);
+        DevBuf ukey(sizeof(int64_t) * std::max<int64_t>(nunits, 1), c.stream);
+        launch(c, k_unit_fill<256>, dim3(nitems), dim3(256), 0, B, Atp, T, nitems, (const int2*)d.items.as<int2>(),
+               (const int64_t*)d.ifl.as<int64_t>(), (const int64_t*)np.as<int64_t>(),
+               (const int64_t*)uoff.as<int64_t>(), (const int64_t*)poff.as<int64_t>(), d.units.as<int4>(),
+               ukey.as<int64_t>());
+        // heaviest units first (LPT)
+        d.order.reset(sizeof(int) * std::max<int64_t>(nunits, 1), c.stream);
+        {
+            DevBuf idx(sizeof(int) * std::max<int64_t>(nunits, 1), c.stream),
+                kout(sizeof(int64_t) * std::max<int64_t>(nunits, 1), c.stream);
+            launch(c, k_iota, dim3(grid_for(c, nunits, 256)), dim3(256), 0, (int)nunits, idx.as<int>());
+            size_t tb = 0;
+            SLAPCU_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, ukey.as<int64_t>(), kout.as<int64_t>(),
+                                                                  idx.as<int>(), d.order.as<int>(), (int)nunits, 0,
+                                                                  40, c.stream));
+            DevBuf tmp(tb, c.stream);
+            timed(c, KC_BIN, [&] {
+                SLAPCU_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp.get(), tb, ukey.as<int64_t>(),
+                                                                      kout.as<int64_t>(), idx.as<int>(),
+                                                                      d.order.as<int>(), (int)nunits, 0, 40,
+                                                                      c.stream));
+            });
+            ++c.launches;
         }
-        DirectArgs g{A, B, Atp, T, TL, (const int2*)d.items.as<int2>(), (const int*)d.dslot.as<int>(), nitems,
-                     (const unsigned*)d.gbm.as<unsigned>(), d.state.as<unsigned long long>(), ticket,
-                     (const int64_t*)d.lp.as<int64_t>(), d.hcnt.as<unsigned long long>(), crw,
-                     static_cast<uint8_t*>(cv), capacity, overflow};
-        const size_t smem = sizeof(unsigned) * (W + W / 32) + sizeof(int) * (W / 32 + 1) + sizeof(uint16_t) * W + 16;
-        auto go = [&](auto k) {
-            ensure_smem(k, smem);
-            int per_sm = 0;
-            SLAPCU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kDirectThreads, smem));
-            const int grid = std::max(1, std::min(nitems, per_sm * c.num_sms));
-            launch(c, k, dim3(grid), dim3(kDirectThreads), smem, g);
-        };
-        go(k_tile_direct<kDirectThreads>);
+        d.stash.reset(sizeof(unsigned) * std::max<int64_t>(swords, 4), c.stream);
+        d.partial.reset(sizeof(unsigned) * size_t(W) * std::max<int64_t>(nslots, 1), c.stream);
+        d.cnt.reset(sizeof(int64_t) * ni1, c.stream);
+        d.form.reset(sizeof(int) * ni1, c.stream);
+        d.hoff.reset(sizeof(int64_t) * ni1, c.stream);
+        SLAPCU_CUDA(cudaMemsetAsync(d.cnt.as<int64_t>() + nitems, 0, sizeof(int64_t), c.stream));
+        KScope ks2(c, KC_SYM_HEAVY);
+        FormArgs g{A, B, Atp, T, TL, (const int2*)d.items.as<int2>(), (const int4*)d.units.as<int4>(),
+                   (const int*)d.order.as<int>(), d.stash.as<unsigned>(), (const int64_t*)d.soff.as<int64_t>(),
+                   (const int64_t*)d.sres.as<int64_t>(), d.partial.as<unsigned>(), d.cnt.as<int64_t>(),
+                   d.form.as<int>(), d.hcnt.as<unsigned long long>()};
+        const size_t smem = sizeof(unsigned) * W + sizeof(int) * (W / 32 + 1);
+        auto kf = k_tile_form<kFormThreads>;
+        ensure_smem(kf, smem);
+        launch(c, kf, dim3((unsigned)nunits), dim3(kFormThreads), smem, g);
+        if (nslots > 0) {
+            DevBuf sl(sizeof(int) * 3 * nitems + 16, c.stream), ns(sizeof(int), c.stream);
+            SLAPCU_CUDA(cudaMemsetAsync(ns.get(), 0, sizeof(int), c.stream));
+            int* si = sl.as<int>();
+            launch(c, k_split_list, dim3(grid_for(c, nitems, 256)), dim3(256), 0, nitems,
+                   (const int64_t*)np.as<int64_t>(), (const int64_t*)poff.as<int64_t>(), si, si + nitems,
+                   si + 2 * nitems, ns.as<int>());
+            const int nsplit = d2h(c, ns.as<int>());
+            auto kc = k_tile_combine<kFormThreads>;
+            ensure_smem(kc, smem);
+            launch(c, kc, dim3(nsplit), dim3(kFormThreads), smem, TL, (const int2*)d.items.as<int2>(),
+                   (const int*)si, (const int*)(si + nitems), (const int*)(si + 2 * nitems),
+                   (const unsigned*)d.partial.as<unsigned>(), d.stash.as<unsigned>(),
+                   (const int64_t*)d.soff.as<int64_t>(), (const int64_t*)d.sres.as<int64_t>(), d.cnt.as<int64_t>(),
+                   d.form.as<int>(), d.hcnt.as<unsigned long long>());
+        }
+        exclusive_scan_i64(c, d.cnt.as<int64_t>(), d.hoff.as<int64_t>(), nitems + 1);
     }
-    // ---- colptr = scan(light + heavy counts); light columns copied into place
+    // ---- colptr = scan(light + heavy counts)
     {
         KScope ks(c, KC_SCAN);
         DevBuf tot(sizeof(int64_t) * (n + 1), c.stream);
@@ -643,14 +792,24 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
         exclusive_scan_i64(c, tot.as<int64_t>(), c_colptr, n + 1);
     }
     const int64_t total = d2h(c, c_colptr + n);
-    const int ovf = d2h(c, overflow);
     d.last_nnz = total;
-    if (ovf || total > capacity)
+    if (total > capacity)
         throw Fail{SLAPCU_ERR_BUDGET, "output needs " + std::to_string(total) + " entries, capacity " +
                                           std::to_string(capacity)};
+    if (nitems > 0) {
+        KScope ks(c, KC_NUM_HEAVY);
+        EmitArgs e{(const int2*)d.items.as<int2>(), (const int64_t*)d.cnt.as<int64_t>(), (const int*)d.form.as<int>(),
+                   (const unsigned*)d.stash.as<unsigned>(), (const int64_t*)d.soff.as<int64_t>(),
+                   (const int64_t*)d.hoff.as<int64_t>(), (const int64_t*)d.lp.as<int64_t>(), TL, crw,
+                   static_cast<uint8_t*>(cv)};
+        const size_t smem = sizeof(int) * (W / 32 + 2);
+        auto ke = k_tile_emit<kEmitThreads>;
+        ensure_smem(ke, smem);
+        launch(c, ke, dim3(nitems), dim3(kEmitThreads), smem, e);
+    }
     if (nlight) {
         KScope ks(c, KC_NUM_LIGHT);
-        fused_copy_light(c, ones, L, nlight, f, c_colptr, crw, cv);
+        fused_copy_light(c, true, L, nlight, f, c_colptr, crw, cv);
     }
     SLAPCU_CUDA(cudaEventRecord(c.ev[1], c.stream));
     SLAPCU_CUDA(cudaStreamSynchronize(c.stream));

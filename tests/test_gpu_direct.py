@@ -1,9 +1,10 @@
 """GPU parity of the in-place single-pass path (slapcu_spgemm_direct).
 
-The Boolean product is formed as (column, row tile) items ordered by a
-decoupled look-back; these cases force every item class -- short runs, warp
-units, dense items pre-formed into global bitmaps, many tiles per column,
-column windows, empty columns -- and check C bit-exactly against the CPU
+The Boolean product is formed as (column, row tile) items, stashed as a
+bitmap or a word list, placed by a scan and expanded into C; these cases
+force every item class -- short runs, warp units, items split over several
+CTAs, both stash forms, many tiles per column, column windows, empty
+columns -- and check C bit-exactly against the CPU
 oracle (acceptance.cpp:58-97 style equivalence; spgemm.hpp:259-260 sorted
 rows).  Capacity overflow must raise BudgetError with the exact nnz.
 """
@@ -30,17 +31,17 @@ def _ones(m):
 
 
 @pytest.mark.parametrize("tile_log2", [10, 12, 17])
-@pytest.mark.parametrize("dense_min", [0, 1, 2000, 65536])
-def test_direct_bool_tiles_and_dense(port, tile_log2, dense_min):
+@pytest.mark.parametrize("split", [1024, 5000, 262144])
+def test_direct_bool_tiles_and_splits(port, tile_log2, split):
     a = _ones(port.gen_rmat(12))
     want = port.spgemm(oracle.OR_AND_U8, a, a)
     ctx = P.Context()
     ctx.set_option(L.OPT_DIRECT_TILE_ROWS_LOG2, tile_log2)
-    ctx.set_option(L.OPT_DIRECT_DENSE_FLOPS_MIN, dense_min)
+    ctx.set_option(L.OPT_DIRECT_SPLIT_FLOPS, split)
     da = to_device(a)
     for alg in (P.SpGemmAlg.heap, P.SpGemmAlg.hybrid):
         got = P.local_spgemm(da, da, P.OrAnd, alg, ctx=ctx, method="direct")
-        assert_parity(got, want, oracle.OR_AND_U8, f"TL={tile_log2} dense={dense_min} {alg.name}")
+        assert_parity(got, want, oracle.OR_AND_U8, f"TL={tile_log2} split={split} {alg.name}")
 
 
 @pytest.mark.parametrize("scale", [8, 11, 14])
