@@ -62,6 +62,7 @@ def parse():
                     help="direct: slapcu_spgemm_direct writes C in place in one pass; fused: begin/finish")
     ap.add_argument("--direct-tile-log2", type=int, default=0, help="rows per direct-path item (0 = default)")
     ap.add_argument("--direct-split", type=int, default=None, help="direct path: split items above this many flops")
+    ap.add_argument("--mark-mode", type=int, default=None, help="direct path bitmap update mode (0/1/2)")
     ap.add_argument("--streams", type=int, default=1, choices=[1, 2],
                     help="2: alternate column batches over two contexts/streams (async finish)")
     return ap.parse_args()
@@ -80,6 +81,8 @@ def apply_options(ctx, args):
         ctx.set_option(L.OPT_DIRECT_TILE_ROWS_LOG2, args.direct_tile_log2)
     if args.direct_split is not None:
         ctx.set_option(L.OPT_DIRECT_SPLIT_FLOPS, args.direct_split)
+    if args.mark_mode is not None:
+        ctx.set_option(L.OPT_DIRECT_MARK_MODE, args.mark_mode)
 
 
 # ------------------------------------------------------------------ helpers

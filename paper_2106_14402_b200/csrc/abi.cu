@@ -142,6 +142,10 @@ slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t v
             require(v >= 10 && v <= 18, SLAPCU_ERR_INVALID, "direct tile rows log2 must be in 10..18");
             c.opt.direct_tile_rows_log2 = (int)v;
             break;
+        case SLAPCU_OPT_DIRECT_MARK_MODE:
+            require(v >= 0 && v <= 2, SLAPCU_ERR_INVALID, "mark mode must be 0, 1 or 2");
+            c.opt.direct_mark_mode = (int)v;
+            break;
         case SLAPCU_OPT_DIRECT_SPLIT_FLOPS:
             require(v >= 1024, SLAPCU_ERR_INVALID, "split threshold must be >= 1024");
             c.opt.direct_split_flops = v;

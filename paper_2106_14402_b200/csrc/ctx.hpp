@@ -122,6 +122,7 @@ struct Options {
     int dense_tile_rows_log2 = 17;    // byte-flag tile height (128 KB of flags)
     bool async_finish = false;        // finish() returns without waiting (errors surface later)
     int direct_tile_rows_log2 = 17;   // direct path: row-tile height of an item (16 KB bitmap)
+    int direct_mark_mode = 0;  // direct path product update: 0 test+set, 1 atomic only, 2 quad-merged
     int64_t direct_split_flops = 262144;  // direct path: items above this many multiplies are
                                           // formed by several CTAs (equal-flops B-entry parts)
 };

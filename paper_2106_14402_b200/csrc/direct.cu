@@ -75,20 +75,30 @@ struct WalkSm {
     int64_t start[NT];
 };
 
-// Marks row rr of the current tile (bitmap at shared address bmA): test
-// before set -- a plain shared load is a broadcast for lanes hitting one word,
-// and most products of a dense column find their bit already set.
+// Sets bits `b` of word address `a` (shared window): test before set -- a
+// plain shared load is a broadcast for lanes hitting one word, and most
+// products of a dense column find their bits already set.  MODE 1 skips the
+// test (one shared atomic per product).
+template <int MODE>
+__device__ __forceinline__ void set_bits(unsigned a, unsigned b) {
+    if (MODE == 1) {
+        asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(b) : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t.reg .b32 x;\n\t"
+            "ld.shared.u32 x, [%0];\n\t"
+            "and.b32 x, x, %1;\n\t"
+            "setp.ne.u32 p, x, %1;\n\t"
+            "@p red.shared.or.b32 [%0], %1;\n\t}" ::"r"(a),
+            "r"(b)
+            : "memory");
+    }
+}
+
+// Marks row rr of the current tile (bitmap at shared address bmA).
+template <int MODE>
 __device__ __forceinline__ void mark(unsigned bmA, int rr) {
-    const unsigned a = bmA + (unsigned(rr >> 5) << 2);
-    const unsigned b = 1u << (rr & 31);
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t.reg .b32 x;\n\t"
-        "ld.shared.u32 x, [%0];\n\t"
-        "and.b32 x, x, %1;\n\t"
-        "setp.eq.u32 p, x, 0;\n\t"
-        "@p red.shared.or.b32 [%0], %1;\n\t}" ::"r"(a),
-        "r"(b)
-        : "memory");
+    set_bits<MODE>(bmA + (unsigned(rr >> 5) << 2), 1u << (rr & 31));
 }
 
 // All products of B entries [b0, b1) (column j) whose rows lie in tile t,
@@ -97,7 +107,7 @@ __device__ __forceinline__ void mark(unsigned bmA, int rr) {
 // that the warps walk lane-strided with U loads in flight (coalesced,
 // balanced across warps; a warp's units are increasing, so the entry owning
 // a unit is found by advancing, not searching).
-template <int NT, int U>
+template <int NT, int U, int MODE>
 __device__ __forceinline__ void tile_walk(const DevCsc& A, const DevCsc& B, const int32_t* __restrict__ Atp, int T,
                                           int64_t b0, int64_t b1, int t, int t0, unsigned* bm, WalkSm<NT>& sh) {
     constexpr int NW = NT / 32;
@@ -116,7 +126,7 @@ __device__ __forceinline__ void tile_walk(const DevCsc& A, const DevCsc& B, cons
             len = hi - lo;
             if (len < kShortRun) {
                 const int32_t* q = Arw + s;
-                for (int x = 0; x < len; ++x) mark(bmA, __ldg(q + x));
+                for (int x = 0; x < len; ++x) mark<MODE & 1>(bmA, __ldg(q + x));
                 len = 0;
             } else {
                 units = (len + kUnit - 1) / kUnit;
@@ -129,21 +139,65 @@ __device__ __forceinline__ void tile_walk(const DevCsc& A, const DevCsc& B, cons
         sh.start[tid] = s;
         if (tid == 0) sh.ustart[NT] = tot;
         __syncthreads();
+        // warp w takes the contiguous unit range [u0, u1): one search for the
+        // owning entry, then it only advances
+        const int u0 = (int)((int64_t(tot) * warp) / NW), u1 = (int)((int64_t(tot) * (warp + 1)) / NW);
         int e = 0;
-        for (int u = warp; u < tot; u += NW) {
+        if (u0 < u1) {
+            int lo = 0, hi = NT - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (sh.ustart[mid] <= u0)
+                    lo = mid;
+                else
+                    hi = mid - 1;
+            }
+            e = lo;
+        }
+        for (int u = u0; u < u1; ++u) {
             while (sh.ustart[e + 1] <= u) ++e;  // entry owning unit u
             const int c0 = (u - sh.ustart[e]) * kUnit;
             const int32_t* run = Arw + sh.start[e] + c0;
             const int m = min(kUnit, sh.len[e] - c0);
-            int x = lane;
-            for (; x + 32 * (U - 1) < m; x += 32 * U) {
-                int r[U];
+            if (MODE == 2) {
+                // lane-contiguous quads (16-byte loads from the aligned-down
+                // run start); rows of a quad sharing a word are OR-ed in
+                // registers first, so a dense run costs one shared update per
+                // word instead of one per product
+                const int mis = (int)((reinterpret_cast<uintptr_t>(run) >> 2) & 3);
+                const int4* q4 = reinterpret_cast<const int4*>(run - mis);
+                const int total = m + mis;
+                for (int x = 4 * lane; x < total; x += 128) {
+                    const int4 q = __ldg(q4 + (x >> 2));
+                    const int rv[4] = {q.x, q.y, q.z, q.w};
+                    int cw = -1;
+                    unsigned acc = 0;
 #pragma unroll
-                for (int v = 0; v < U; ++v) r[v] = __ldg(run + x + 32 * v);
+                    for (int v = 0; v < 4; ++v) {
+                        const int pos = x + v - mis;
+                        if (pos >= 0 && pos < m) {
+                            const int w = rv[v] >> 5;
+                            if (w != cw) {
+                                if (cw >= 0) set_bits<0>(bmA + (unsigned(cw) << 2), acc);
+                                cw = w;
+                                acc = 0;
+                            }
+                            acc |= 1u << (rv[v] & 31);
+                        }
+                    }
+                    if (cw >= 0) set_bits<0>(bmA + (unsigned(cw) << 2), acc);
+                }
+            } else {
+                int x = lane;
+                for (; x + 32 * (U - 1) < m; x += 32 * U) {
+                    int r[U];
 #pragma unroll
-                for (int v = 0; v < U; ++v) mark(bmA, r[v]);
+                    for (int v = 0; v < U; ++v) r[v] = __ldg(run + x + 32 * v);
+#pragma unroll
+                    for (int v = 0; v < U; ++v) mark<MODE>(bmA, r[v]);
+                }
+                for (; x < m; x += 32) mark<MODE>(bmA, __ldg(run + x));
             }
-            for (; x < m; x += 32) mark(bmA, __ldg(run + x));
         }
         __syncthreads();
     }
@@ -227,7 +281,7 @@ __device__ __forceinline__ void stash_bitmap(const unsigned* bm, int W, int* chu
     }
 }
 
-template <int NT>
+template <int NT, int MODE>
 __global__ void __launch_bounds__(NT) k_tile_form(FormArgs g) {
     extern __shared__ __align__(16) unsigned char sm_raw[];
     const int W = 1 << (g.TL - 5);
@@ -240,7 +294,7 @@ __global__ void __launch_bounds__(NT) k_tile_form(FormArgs g) {
     const int64_t bs = g.B.cp[it.x];
     smem_zero(bm, W);
     __syncthreads();
-    tile_walk<NT, 4>(g.A, g.B, g.Atp, g.T, bs + u.y, bs + u.z, it.y, it.y << g.TL, bm, sh);
+    tile_walk<NT, 4, MODE>(g.A, g.B, g.Atp, g.T, bs + u.y, bs + u.z, it.y, it.y << g.TL, bm, sh);
     if (u.w >= 0) {  // one part of a split item: partial bitmap out
         uint4* d4 = reinterpret_cast<uint4*>(g.partial + int64_t(u.w) * W);
         const uint4* s4 = reinterpret_cast<const uint4*>(bm);
@@ -296,29 +350,59 @@ struct EmitArgs {
     uint8_t* cv;
 };
 
-// Rows of one chunk of 32 words (lane's word x, rows rb + bit) to out[...] in
-// order.  Dense chunks: word by word, lane b writes bit b (coalesced runs);
-// sparse chunks: one output per lane per step, source found by shuffles.
-__device__ __forceinline__ void emit_chunk(unsigned x, int rb, int tot, int32_t* __restrict__ out, int lane) {
-    if (tot >= 256) {
-        int all;
-        const int ex = warp_excl_scan(__popc(x), lane, &all);
-        const unsigned below = (1u << lane) - 1u;
-        for (int k = 0; k < 32; ++k) {
-            const unsigned wk = __shfl_sync(0xffffffffu, x, k);
-            const int ek = __shfl_sync(0xffffffffu, ex, k);
-            const int rk = __shfl_sync(0xffffffffu, rb, k);
-            if ((wk >> lane) & 1u) out[ek + __popc(wk & below)] = rk + lane;
-        }
-    } else {
-        emit_rows_coalesced(x, rb, out, lane);
+// Rows of one chunk of 32 words (lane's word x, rows rb + bit; E set bits in
+// all) to out[0, E) in order.  Each lane produces a contiguous share of the
+// outputs (one search for its first word and bit, then it walks bits
+// serially: ~10 instructions per entry spread over all 32 lanes) into a
+// per-warp shared stage, which is then stored to global memory coalesced.
+__device__ __forceinline__ void emit_chunk(unsigned x, int rb, int E, int32_t* __restrict__ out, unsigned* wsm,
+                                           int* rsm, int* esm, int* stage, int lane) {
+    int all;
+    const int ex = warp_excl_scan(__popc(x), lane, &all);
+    wsm[lane] = x;
+    rsm[lane] = rb;
+    esm[lane] = ex;
+    __syncwarp();
+    const int per = (E + 31) >> 5;
+    const int my0 = min(lane * per, E), my1 = min(my0 + per, E);
+    // the largest l with ex_l <= my0 (ex is non-decreasing across lanes)
+    int src = 0;
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1) {
+        const int cand = src + step;
+        const int exc = __shfl_sync(0xffffffffu, ex, cand & 31);
+        if (cand < 32 && exc <= my0) src = cand;
     }
+    if (my0 < my1) {
+        // an empty word shares ex with the following ones: if src's word is
+        // empty, my0's owner is an earlier lane -- step back to it
+        unsigned w = wsm[src];
+        while (w == 0u) w = wsm[--src];
+        int r0 = rsm[src];
+        const int k = my0 - esm[src];
+        if (k) w &= ~((1u << nth_set_bit(w, k)) - 1u);  // drop the k lowest set bits
+        for (int o = my0; o < my1; ++o) {
+            while (w == 0u) {
+                ++src;
+                w = wsm[src];
+                r0 = rsm[src];
+            }
+            stage[o] = r0 + (__ffs(w) - 1);
+            w &= w - 1u;
+        }
+    }
+    __syncwarp();
+    for (int i = lane; i < E; i += 32) out[i] = stage[i];
+    __syncwarp();
 }
 
 template <int NT>
 __global__ void __launch_bounds__(NT) k_tile_emit(EmitArgs g) {
     constexpr int NW = NT / 32;
-    extern __shared__ int chunk[];  // [W/32 + 1]
+    extern __shared__ int chunk[];  // [W/32 + 2]
+    __shared__ unsigned wsm[NW][32];
+    __shared__ int rsm[NW][32], esm[NW][32];
+    __shared__ int stage[NW][1024];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int item = blockIdx.x;
     const int2 it = g.items[item];
@@ -356,7 +440,9 @@ __global__ void __launch_bounds__(NT) k_tile_emit(EmitArgs g) {
         const unsigned x = w < nwords ? words[w] : 0u;
         const int wi = idx ? (w < nwords ? idx[w] : 0) : w;
         const int tot = chunk[cc + 1] - chunk[cc];
-        if (tot) emit_chunk(x, t0 + (wi << 5), tot, g.crw + off + chunk[cc], lane);
+        if (tot)
+            emit_chunk(x, t0 + (wi << 5), tot, g.crw + off + chunk[cc], wsm[warp], rsm[warp], esm[warp],
+                       stage[warp], lane);
     }
     if (g.cv) {
         // values: c bytes of 1 (head bytes, 16-byte body, tail bytes)
@@ -462,31 +548,38 @@ __global__ void k_item_fill(const int* __restrict__ hl, int nh, int T, int W, co
     }
 }
 
-// Work units: split items get equal-flops B-entry ranges (one CTA per split
-// item scans its column's run lengths); others one unit for the whole column.
+// Work units of unsplit items: the whole column range, in item order.
+__global__ void k_unit_fill_whole(const DevCsc B, int nitems, const int2* __restrict__ items,
+                                  const int64_t* __restrict__ ifl, const int64_t* __restrict__ np,
+                                  const int64_t* __restrict__ uoff, int4* __restrict__ units,
+                                  int64_t* __restrict__ ukey) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nitems; i += gridDim.x * blockDim.x) {
+        if (np[i] != 1) continue;
+        const int j = items[i].x;
+        units[uoff[i]] = make_int4(i, 0, (int)(B.cp[j + 1] - B.cp[j]), -1);
+        ukey[uoff[i]] = ifl[i];
+    }
+}
+
+// Work units of split items: equal-flops B-entry ranges (one CTA per split
+// item scans its column's run lengths in this tile).
 template <int NT>
 __global__ void __launch_bounds__(NT)
-    k_unit_fill(DevCsc B, const int32_t* __restrict__ Atp, int T, int nitems, const int2* __restrict__ items,
-                const int64_t* __restrict__ ifl, const int64_t* __restrict__ np, const int64_t* __restrict__ uoff,
-                const int64_t* __restrict__ poff, int4* __restrict__ units, int64_t* __restrict__ ukey) {
+    k_unit_fill_split(DevCsc B, const int32_t* __restrict__ Atp, int T, const int* __restrict__ sitems,
+                      const int2* __restrict__ items, const int64_t* __restrict__ ifl, const int64_t* __restrict__ np,
+                      const int64_t* __restrict__ uoff, const int64_t* __restrict__ poff, int4* __restrict__ units,
+                      int64_t* __restrict__ ukey) {
     __shared__ int wsum[NT / 32 + 1];
     __shared__ long long run_sh;
-    const int item = blockIdx.x;
+    __shared__ int bnd[65];
+    const int item = sitems[blockIdx.x];
     const int2 it = items[item];
     const int64_t p = np[item];
     const int64_t bs = B.cp[it.x], be = B.cp[it.x + 1];
     const int64_t u0 = uoff[item];
     const int64_t f = ifl[item];
-    if (p == 1) {
-        if (threadIdx.x == 0) {
-            units[u0] = make_int4(item, 0, (int)(be - bs), -1);
-            ukey[u0] = f;
-        }
-        return;
-    }
-    // boundaries: part q ends after the entry whose inclusive flops prefix first reaches ceil(q*f/p)
+    // part q ends after the entry whose inclusive flops prefix first reaches ceil(q*f/p)
     if (threadIdx.x == 0) run_sh = 0;
-    __shared__ int bnd[65];
     if (threadIdx.x <= p) bnd[threadIdx.x] = threadIdx.x == p ? (int)(be - bs) : 0;
     __syncthreads();
     for (int64_t base = bs; base < be; base += NT) {
@@ -500,7 +593,6 @@ __global__ void __launch_bounds__(NT)
         const long long ex = (long long)block_excl_scan<NT>(len, wsum, &tot) + run_sh;
         const long long in = ex + len;
         if (len > 0) {
-            // parts q (1..p-1) with target in (ex, in]
             for (int64_t q = 1; q < p; ++q) {
                 const long long tg = (q * f + p - 1) / p;
                 if (tg > ex && tg <= in) bnd[q] = (int)(i - bs + 1);
@@ -726,10 +818,25 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
         if (nunits > INT32_MAX || nslots > INT32_MAX) throw Fail{SLAPCU_ERR_INVALID, "too many work units"};
         d.units.reset(sizeof(int4) * std::max<int64_t>(nunits, 1), c.stream);
         DevBuf ukey(sizeof(int64_t) * std::max<int64_t>(nunits, 1), c.stream);
-        launch(c, k_unit_fill<256>, dim3(nitems), dim3(256), 0, B, Atp, T, nitems, (const int2*)d.items.as<int2>(),
-               (const int64_t*)d.ifl.as<int64_t>(), (const int64_t*)np.as<int64_t>(),
-               (const int64_t*)uoff.as<int64_t>(), (const int64_t*)poff.as<int64_t>(), d.units.as<int4>(),
-               ukey.as<int64_t>());
+        // split items (parts of one item are formed by several CTAs, then OR-ed)
+        DevBuf sl(sizeof(int) * 3 * (size_t(nitems) + 1), c.stream), ns(sizeof(int), c.stream);
+        SLAPCU_CUDA(cudaMemsetAsync(ns.get(), 0, sizeof(int), c.stream));
+        int* si = sl.as<int>();
+        int nsplit = 0;
+        if (nslots > 0) {
+            launch(c, k_split_list, dim3(grid_for(c, nitems, 256)), dim3(256), 0, nitems,
+                   (const int64_t*)np.as<int64_t>(), (const int64_t*)poff.as<int64_t>(), si, si + nitems,
+                   si + 2 * nitems, ns.as<int>());
+            nsplit = d2h(c, ns.as<int>());
+        }
+        launch(c, k_unit_fill_whole, dim3(grid_for(c, nitems, 256)), dim3(256), 0, B, nitems,
+               (const int2*)d.items.as<int2>(), (const int64_t*)d.ifl.as<int64_t>(), (const int64_t*)np.as<int64_t>(),
+               (const int64_t*)uoff.as<int64_t>(), d.units.as<int4>(), ukey.as<int64_t>());
+        if (nsplit > 0)
+            launch(c, k_unit_fill_split<256>, dim3(nsplit), dim3(256), 0, B, Atp, T, (const int*)si,
+                   (const int2*)d.items.as<int2>(), (const int64_t*)d.ifl.as<int64_t>(),
+                   (const int64_t*)np.as<int64_t>(), (const int64_t*)uoff.as<int64_t>(),
+                   (const int64_t*)poff.as<int64_t>(), d.units.as<int4>(), ukey.as<int64_t>());
         // heaviest units first (LPT)
         d.order.reset(sizeof(int) * std::max<int64_t>(nunits, 1), c.stream);
         {
@@ -761,17 +868,16 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
                    (const int64_t*)d.sres.as<int64_t>(), d.partial.as<unsigned>(), d.cnt.as<int64_t>(),
                    d.form.as<int>(), d.hcnt.as<unsigned long long>()};
         const size_t smem = sizeof(unsigned) * W + sizeof(int) * (W / 32 + 1);
-        auto kf = k_tile_form<kFormThreads>;
-        ensure_smem(kf, smem);
-        launch(c, kf, dim3((unsigned)nunits), dim3(kFormThreads), smem, g);
-        if (nslots > 0) {
-            DevBuf sl(sizeof(int) * 3 * nitems + 16, c.stream), ns(sizeof(int), c.stream);
-            SLAPCU_CUDA(cudaMemsetAsync(ns.get(), 0, sizeof(int), c.stream));
-            int* si = sl.as<int>();
-            launch(c, k_split_list, dim3(grid_for(c, nitems, 256)), dim3(256), 0, nitems,
-                   (const int64_t*)np.as<int64_t>(), (const int64_t*)poff.as<int64_t>(), si, si + nitems,
-                   si + 2 * nitems, ns.as<int>());
-            const int nsplit = d2h(c, ns.as<int>());
+        auto form = [&](auto kf) {
+            ensure_smem(kf, smem);
+            launch(c, kf, dim3((unsigned)nunits), dim3(kFormThreads), smem, g);
+        };
+        switch (c.opt.direct_mark_mode) {
+        case 1: form(k_tile_form<kFormThreads, 1>); break;
+        case 2: form(k_tile_form<kFormThreads, 2>); break;
+        default: form(k_tile_form<kFormThreads, 0>); break;
+        }
+        if (nsplit > 0) {
             auto kc = k_tile_combine<kFormThreads>;
             ensure_smem(kc, smem);
             launch(c, kc, dim3(nsplit), dim3(kFormThreads), smem, TL, (const int2*)d.items.as<int2>(),

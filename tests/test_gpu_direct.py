@@ -44,12 +44,15 @@ def test_direct_bool_tiles_and_splits(port, tile_log2, split):
         assert_parity(got, want, oracle.OR_AND_U8, f"TL={tile_log2} split={split} {alg.name}")
 
 
+@pytest.mark.parametrize("mode", [0, 1, 2])
 @pytest.mark.parametrize("scale", [8, 11, 14])
-def test_direct_bool_rmat(port, scale):
+def test_direct_bool_rmat(port, scale, mode):
     a = _ones(port.gen_rmat(scale))
     want = port.spgemm(oracle.OR_AND_U8, a, a)
-    got = P.local_spgemm(to_device(a), to_device(a), P.OrAnd, method="direct")
-    assert_parity(got, want, oracle.OR_AND_U8, f"s{scale}")
+    ctx = P.Context()
+    ctx.set_option(L.OPT_DIRECT_MARK_MODE, mode)
+    got = P.local_spgemm(to_device(a), to_device(a), P.OrAnd, ctx=ctx, method="direct")
+    assert_parity(got, want, oracle.OR_AND_U8, f"s{scale} mode {mode}")
 
 
 def test_direct_window_and_rectangular(port):
