@@ -350,59 +350,83 @@ struct EmitArgs {
     uint8_t* cv;
 };
 
-// Rows of one chunk of 32 words (lane's word x, rows rb + bit; E set bits in
-// all) to out[0, E) in order.  Each lane produces a contiguous share of the
-// outputs (one search for its first word and bit, then it walks bits
-// serially: ~10 instructions per entry spread over all 32 lanes) into a
-// per-warp shared stage, which is then stored to global memory coalesced.
-__device__ __forceinline__ void emit_chunk(unsigned x, int rb, int E, int32_t* __restrict__ out, unsigned* wsm,
-                                           int* rsm, int* esm, int* stage, int lane) {
+constexpr int kEmitWPL = 4;                    // stash words per lane in a warp block
+constexpr int kEmitBlock = 32 * kEmitWPL;      // words per warp block
+constexpr int kEmitStage = 1024;               // entries per staging round
+
+// Per-warp shared state of the emission.
+struct EmitWarp {
+    unsigned w[kEmitBlock];
+    int rb[kEmitBlock];
+    int stage[kEmitStage + 4];
+};
+
+// Rows of one warp block (lane l holds words 4l..4l+3 in ws->w, row bases in
+// ws->rb; E set bits in all) written to out[0, E) in order.  Outputs go in
+// rounds of kEmitStage: lane l produces a contiguous 1/32 of the round (one
+// search for its first word and bit, then it walks bits serially) into a
+// shared stage co-aligned with `out`, then the round is stored with 16-byte
+// coalesced stores.
+__device__ __forceinline__ void emit_block(EmitWarp* ws, int cnt, int E, int32_t* __restrict__ out, int lane) {
     int all;
-    const int ex = warp_excl_scan(__popc(x), lane, &all);
-    wsm[lane] = x;
-    rsm[lane] = rb;
-    esm[lane] = ex;
-    __syncwarp();
-    const int per = (E + 31) >> 5;
-    const int my0 = min(lane * per, E), my1 = min(my0 + per, E);
-    // the largest l with ex_l <= my0 (ex is non-decreasing across lanes)
-    int src = 0;
+    const int ex = warp_excl_scan(cnt, lane, &all);
+    const int shift = (int)((reinterpret_cast<uintptr_t>(out) >> 2) & 3);
+    for (int R0 = 0; R0 < E; R0 += kEmitStage) {
+        const int RE = min(kEmitStage, E - R0);
+        const int per = (RE + 31) >> 5;
+        const int my0 = R0 + min(lane * per, RE), my1 = R0 + min(lane * per + per, RE);
+        // owner lane of output my0: the largest l with ex_l <= my0
+        int src = 0;
 #pragma unroll
-    for (int step = 16; step > 0; step >>= 1) {
-        const int cand = src + step;
-        const int exc = __shfl_sync(0xffffffffu, ex, cand & 31);
-        if (cand < 32 && exc <= my0) src = cand;
-    }
-    if (my0 < my1) {
-        // an empty word shares ex with the following ones: if src's word is
-        // empty, my0's owner is an earlier lane -- step back to it
-        unsigned w = wsm[src];
-        while (w == 0u) w = wsm[--src];
-        int r0 = rsm[src];
-        const int k = my0 - esm[src];
-        if (k) w &= ~((1u << nth_set_bit(w, k)) - 1u);  // drop the k lowest set bits
-        for (int o = my0; o < my1; ++o) {
-            while (w == 0u) {
-                ++src;
-                w = wsm[src];
-                r0 = rsm[src];
-            }
-            stage[o] = r0 + (__ffs(w) - 1);
-            w &= w - 1u;
+        for (int step = 16; step > 0; step >>= 1) {
+            const int cand = src + step;
+            const int exc = __shfl_sync(0xffffffffu, ex, cand & 31);
+            if (cand < 32 && exc <= my0) src = cand;
         }
+        const int exs = __shfl_sync(0xffffffffu, ex, src);
+        if (my0 < my1) {
+            int k = my0 - exs;
+            int wi = src * kEmitWPL;
+            unsigned w = ws->w[wi];
+            for (;;) {  // word of the owner lane holding output my0
+                const int c = __popc(w);
+                if (k < c) break;
+                k -= c;
+                w = ws->w[++wi];
+            }
+            if (k) w &= ~((1u << nth_set_bit(w, k)) - 1u);  // drop the k lowest set bits
+            int rb = ws->rb[wi];
+            int* st = ws->stage + shift - R0;
+            for (int o = my0; o < my1; ++o) {
+                while (w == 0u) {
+                    ++wi;
+                    w = ws->w[wi];
+                    rb = ws->rb[wi];
+                }
+                st[o] = rb + (__ffs(w) - 1);
+                w &= w - 1u;
+            }
+        }
+        __syncwarp();
+        // stage[shift + i] -> out[R0 + i]; both 16-byte aligned where (shift + i) % 4 == 0
+        int32_t* dst = out + R0;
+        const int h = min(RE, (4 - shift) & 3);
+        if (lane < h) dst[lane] = ws->stage[shift + lane];
+        const int nb = (RE - h) >> 2;
+        const uint4* s4 = reinterpret_cast<const uint4*>(ws->stage + shift + h);
+        uint4* d4 = reinterpret_cast<uint4*>(dst + h);
+        for (int q = lane; q < nb; q += 32) d4[q] = s4[q];
+        const int tl = h + (nb << 2);
+        if (tl + lane < RE) dst[tl + lane] = ws->stage[shift + tl + lane];
+        __syncwarp();
     }
-    __syncwarp();
-    for (int i = lane; i < E; i += 32) out[i] = stage[i];
-    __syncwarp();
 }
 
 template <int NT>
 __global__ void __launch_bounds__(NT) k_tile_emit(EmitArgs g) {
     constexpr int NW = NT / 32;
-    extern __shared__ int chunk[];  // [W/32 + 2]
-    __shared__ unsigned wsm[NW][32];
-    __shared__ int rsm[NW][32], esm[NW][32];
-    __shared__ int stage[NW][1024];
+    extern __shared__ int blk[];  // [W/128 + 2] block counts -> bases
+    __shared__ EmitWarp wsm[NW];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int item = blockIdx.x;
     const int2 it = g.items[item];
@@ -413,36 +437,48 @@ __global__ void __launch_bounds__(NT) k_tile_emit(EmitArgs g) {
     const int nwords = U >= 0 ? U : W;
     const unsigned* words = g.stash + g.soff[item];
     const uint16_t* idx = U >= 0 ? reinterpret_cast<const uint16_t*>(words + U) : nullptr;
-    const int nch = (nwords + 31) >> 5;
+    const int nblk = (nwords + kEmitBlock - 1) / kEmitBlock;
     const int t0 = it.y << g.TL;
-    for (int cc = warp; cc < nch; cc += NW) {
-        const int w = cc * 32 + lane;
-        int x = w < nwords ? __popc(words[w]) : 0;
+    for (int b = warp; b < nblk; b += NW) {
+        int x = 0;
+#pragma unroll
+        for (int q = 0; q < kEmitWPL; ++q) {
+            const int w = b * kEmitBlock + q * 32 + lane;
+            x += w < nwords ? __popc(words[w]) : 0;
+        }
         x = warp_reduce_sum(x);
-        if (lane == 0) chunk[cc] = x;
+        if (lane == 0) blk[b] = x;
     }
     __syncthreads();
     if (warp == 0) {
         int run = 0;
-        for (int b0 = 0; b0 < nch; b0 += 32) {
+        for (int b0 = 0; b0 < nblk; b0 += 32) {
             const int cix = b0 + lane;
-            const int x = cix < nch ? chunk[cix] : 0;
+            const int x = cix < nblk ? blk[cix] : 0;
             int tt;
             const int e = warp_excl_scan(x, lane, &tt);
-            if (cix < nch) chunk[cix] = run + e;
+            if (cix < nblk) blk[cix] = run + e;
             run += tt;
         }
-        if (lane == 0) chunk[nch] = run;
+        if (lane == 0) blk[nblk] = run;
     }
     __syncthreads();
-    for (int cc = warp; cc < nch; cc += NW) {
-        const int w = cc * 32 + lane;
-        const unsigned x = w < nwords ? words[w] : 0u;
-        const int wi = idx ? (w < nwords ? idx[w] : 0) : w;
-        const int tot = chunk[cc + 1] - chunk[cc];
-        if (tot)
-            emit_chunk(x, t0 + (wi << 5), tot, g.crw + off + chunk[cc], wsm[warp], rsm[warp], esm[warp],
-                       stage[warp], lane);
+    EmitWarp* ws = &wsm[warp];
+    for (int b = warp; b < nblk; b += NW) {
+        const int E = blk[b + 1] - blk[b];
+        if (!E) continue;
+        int cnt = 0;
+#pragma unroll
+        for (int q = 0; q < kEmitWPL; ++q) {
+            const int li = lane * kEmitWPL + q;
+            const int w = b * kEmitBlock + li;
+            const unsigned x = w < nwords ? words[w] : 0u;
+            ws->w[li] = x;
+            ws->rb[li] = t0 + ((idx ? (w < nwords ? (int)idx[w] : 0) : w) << 5);
+            cnt += __popc(x);
+        }
+        __syncwarp();
+        emit_block(ws, cnt, E, g.crw + off + blk[b], lane);
     }
     if (g.cv) {
         // values: c bytes of 1 (head bytes, 16-byte body, tail bytes)
@@ -908,7 +944,7 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
                    (const unsigned*)d.stash.as<unsigned>(), (const int64_t*)d.soff.as<int64_t>(),
                    (const int64_t*)d.hoff.as<int64_t>(), (const int64_t*)d.lp.as<int64_t>(), TL, crw,
                    static_cast<uint8_t*>(cv)};
-        const size_t smem = sizeof(int) * (W / 32 + 2);
+        const size_t smem = sizeof(int) * (W / kEmitBlock + 2);
         auto ke = k_tile_emit<kEmitThreads>;
         ensure_smem(ke, smem);
         launch(c, ke, dim3(nitems), dim3(kEmitThreads), smem, e);
