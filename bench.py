@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--direct-tile-log2", type=int, default=0, help="rows per direct-path item (0 = default)")
     ap.add_argument("--direct-split", type=int, default=None, help="direct path: split items above this many flops")
     ap.add_argument("--mark-mode", type=int, default=None, help="direct path bitmap update mode (0/1/2)")
+    ap.add_argument("--form-threads", type=int, default=None, help="direct path form CTA size")
+    ap.add_argument("--emit-threads", type=int, default=None, help="direct path emit CTA size")
     ap.add_argument("--streams", type=int, default=1, choices=[1, 2],
                     help="2: alternate column batches over two contexts/streams (async finish)")
     return ap.parse_args()
@@ -83,6 +85,10 @@ def apply_options(ctx, args):
         ctx.set_option(L.OPT_DIRECT_SPLIT_FLOPS, args.direct_split)
     if args.mark_mode is not None:
         ctx.set_option(L.OPT_DIRECT_MARK_MODE, args.mark_mode)
+    if args.form_threads is not None:
+        ctx.set_option(L.OPT_DIRECT_FORM_THREADS, args.form_threads)
+    if args.emit_threads is not None:
+        ctx.set_option(L.OPT_DIRECT_EMIT_THREADS, args.emit_threads)
 
 
 # ------------------------------------------------------------------ helpers
@@ -323,7 +329,7 @@ def run_ours(args):
     per_step = {k: (nl / args.steps, t / args.steps) for k, (nl, t) in kstats.items() if nl}
     dom = max(per_step, key=lambda k: per_step[k][1])
     # heavy columns of the fused path: flops > max(256, min(n/128, 4096))
-    lmax = max(256, min(A.nrows // 128, 4096))  # same light/heavy split in both methods
+    lmax = 1024 if args.method == "direct" else max(256, min(A.nrows // 128, 4096))  # light/heavy split
     fl = flops_per.cpu().numpy()
     heavy = fl > lmax
     colnnz_b = np.diff(A.colptr.cpu().numpy())
@@ -336,8 +342,13 @@ def run_ours(args):
         c_ent = int(counts[s:e][h].sum())
         b_ent = int(colnnz_b[s:e][h].sum())
         if dom == "sym_heavy" and args.method == "direct":
-            # k_tile_direct + k_tile_dense: B cols + A pattern in, C rows + values out in place
-            dom_bytes += c_ent * (4 + vs) + b_ent * 4 + (nh + 1) * 8 + A.nnz * 4 + (n + 1) * 8
+            # k_tile_form: B columns + the A pattern in (compulsory once per batch);
+            # its per-product A gathers are L2 traffic, its limiter is the
+            # shared-memory bitmap update
+            dom_bytes += b_ent * 4 + (nh + 1) * 8 + A.nnz * 4 + (n + 1) * 8
+        elif dom == "num_heavy" and args.method == "direct":
+            # k_tile_emit: C rows + values of the heavy columns written in place
+            dom_bytes += c_ent * (4 + vs) + (nh + 1) * 8
         elif dom == "sym_heavy":  # k_fused_heavy: B cols + A (pattern) in, staged rows out
             dom_bytes += c_ent * 4 + b_ent * 4 + (nh + 1) * 8 + A.nnz * 4 + (n + 1) * 8
         elif dom == "num_heavy":  # k_values_heavy: C rows in, values out, B and A with values
@@ -352,8 +363,10 @@ def run_ours(args):
     roofline = {
         "bound": "hbm",
         "method": args.method,
-        "kernel": {"sym_heavy": "k_tile_direct+k_tile_dense" if args.method == "direct" else "k_fused_heavy", "sym_light": "k_fused_light", "num_heavy": "k_values_heavy",
-                   "num_light": "k_copy_light+k_copy_heavy"}.get(dom, dom),
+        "kernel": ({"sym_heavy": "k_tile_form", "sym_light": "k_fused_light", "num_heavy": "k_tile_emit",
+                    "num_light": "k_copy_light"} if args.method == "direct" else
+                   {"sym_heavy": "k_fused_heavy", "sym_light": "k_fused_light", "num_heavy": "k_values_heavy",
+                    "num_light": "k_copy_light+k_copy_heavy"}).get(dom, dom),
         "achieved": round(achieved, 2),
         "peak": peak,
         "unit": "GB/s",

@@ -116,9 +116,11 @@ typedef enum {
     SLAPCU_OPT_DIRECT_TILE_ROWS_LOG2 = 9,  /* direct path: rows per (column, row tile) item (default 17) */
     SLAPCU_OPT_DIRECT_SPLIT_FLOPS = 10,    /* direct path: items with more multiplies than this are formed
                                               by several CTAs over equal-flops parts of B(:,j) (>= 1024) */
-    SLAPCU_OPT_DIRECT_MARK_MODE = 11       /* direct path bitmap update: 0 test-then-set per product,
+    SLAPCU_OPT_DIRECT_MARK_MODE = 11,      /* direct path bitmap update: 0 test-then-set per product,
                                               1 shared atomic per product, 2 lane-contiguous quads merged
                                               per 32-row word before the update */
+    SLAPCU_OPT_DIRECT_FORM_THREADS = 12,   /* direct path: threads per form CTA (128, 256, 512) */
+    SLAPCU_OPT_DIRECT_EMIT_THREADS = 13    /* direct path: threads per emit CTA (128, 256) */
 } slapcu_option;
 slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t value);
 

@@ -146,11 +146,22 @@ slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t v
             require(v >= 0 && v <= 2, SLAPCU_ERR_INVALID, "mark mode must be 0, 1 or 2");
             c.opt.direct_mark_mode = (int)v;
             break;
+        case SLAPCU_OPT_DIRECT_FORM_THREADS:
+            require(v == 128 || v == 256 || v == 512, SLAPCU_ERR_INVALID, "form threads: 128, 256 or 512");
+            c.opt.direct_form_threads = (int)v;
+            break;
+        case SLAPCU_OPT_DIRECT_EMIT_THREADS:
+            require(v == 128 || v == 256, SLAPCU_ERR_INVALID, "emit threads: 128 or 256");
+            c.opt.direct_emit_threads = (int)v;
+            break;
         case SLAPCU_OPT_DIRECT_SPLIT_FLOPS:
             require(v >= 1024, SLAPCU_ERR_INVALID, "split threshold must be >= 1024");
             c.opt.direct_split_flops = v;
             break;
-        case SLAPCU_OPT_LIGHT_FLOPS_MAX: c.opt.light_flops_max = v; break;
+        case SLAPCU_OPT_LIGHT_FLOPS_MAX:
+            c.opt.light_flops_max = v;
+            c.opt.direct_light_flops_max = v;
+            break;
         case SLAPCU_OPT_DETERMINISTIC: break;
         case SLAPCU_OPT_DENSE_FLOPS_MIN: c.opt.dense_flops_min = v; break;
         case SLAPCU_OPT_ASYNC_FINISH: c.opt.async_finish = v != 0; break;

@@ -122,8 +122,11 @@ struct Options {
     int dense_tile_rows_log2 = 17;    // byte-flag tile height (128 KB of flags)
     bool async_finish = false;        // finish() returns without waiting (errors surface later)
     int direct_tile_rows_log2 = 17;   // direct path: row-tile height of an item (16 KB bitmap)
-    int direct_mark_mode = 0;  // direct path product update: 0 test+set, 1 atomic only, 2 quad-merged
-    int64_t direct_split_flops = 262144;  // direct path: items above this many multiplies are
+    int64_t direct_light_flops_max = 1024;  // direct path: hash path for columns up to this many flops
+    int direct_mark_mode = 0;               // product update: 0 test+set, 1 atomic only, 2 quad-merged
+    int direct_form_threads = 256;          // CTA size of the form kernel (128, 256, 512)
+    int direct_emit_threads = 128;          // CTA size of the emit kernel (128, 256)
+    int64_t direct_split_flops = 1 << 20;  // direct path: items above this many multiplies are
                                           // formed by several CTAs (equal-flops B-entry parts)
 };
 

@@ -356,26 +356,25 @@ constexpr int kEmitStage = 1024;               // entries per staging round
 
 // Per-warp shared state of the emission.
 struct EmitWarp {
-    unsigned w[kEmitBlock];
-    int rb[kEmitBlock];
-    int stage[kEmitStage + 4];
+    unsigned w[kEmitBlock];             // the block's non-zero words, compacted in order
+    int rb[kEmitBlock];                 // their row bases
+    int stage[kEmitStage + kEmitStage / 32];  // one pad word per 32 entries (conflict-free)
 };
 
-// Rows of one warp block (lane l holds words 4l..4l+3 in ws->w, row bases in
-// ws->rb; E set bits in all) written to out[0, E) in order.  Outputs go in
+// Rows of one warp block written to out[0, E) in order.  Lane l's non-zero
+// words are ws->w[pos, pos + nzc) holding cnt set bits.  Outputs go in
 // rounds of kEmitStage: lane l produces a contiguous 1/32 of the round (one
 // search for its first word and bit, then it walks bits serially) into a
-// shared stage co-aligned with `out`, then the round is stored with 16-byte
-// coalesced stores.
-__device__ __forceinline__ void emit_block(EmitWarp* ws, int cnt, int E, int32_t* __restrict__ out, int lane) {
+// padded shared stage, then the round is stored coalesced.
+__device__ __forceinline__ void emit_block(EmitWarp* ws, int pos, int cnt, int E, int32_t* __restrict__ out,
+                                           int lane) {
     int all;
     const int ex = warp_excl_scan(cnt, lane, &all);
-    const int shift = (int)((reinterpret_cast<uintptr_t>(out) >> 2) & 3);
     for (int R0 = 0; R0 < E; R0 += kEmitStage) {
         const int RE = min(kEmitStage, E - R0);
         const int per = (RE + 31) >> 5;
         const int my0 = R0 + min(lane * per, RE), my1 = R0 + min(lane * per + per, RE);
-        // owner lane of output my0: the largest l with ex_l <= my0
+        // owner lane of output my0: the largest l with ex_l <= my0 and cnt_l > 0
         int src = 0;
 #pragma unroll
         for (int step = 16; step > 0; step >>= 1) {
@@ -384,11 +383,12 @@ __device__ __forceinline__ void emit_block(EmitWarp* ws, int cnt, int E, int32_t
             if (cand < 32 && exc <= my0) src = cand;
         }
         const int exs = __shfl_sync(0xffffffffu, ex, src);
+        const int poss = __shfl_sync(0xffffffffu, pos, src);
         if (my0 < my1) {
             int k = my0 - exs;
-            int wi = src * kEmitWPL;
+            int wi = poss;
             unsigned w = ws->w[wi];
-            for (;;) {  // word of the owner lane holding output my0
+            for (;;) {  // word of the owner lane holding output my0 (all words non-zero)
                 const int c = __popc(w);
                 if (k < c) break;
                 k -= c;
@@ -396,28 +396,19 @@ __device__ __forceinline__ void emit_block(EmitWarp* ws, int cnt, int E, int32_t
             }
             if (k) w &= ~((1u << nth_set_bit(w, k)) - 1u);  // drop the k lowest set bits
             int rb = ws->rb[wi];
-            int* st = ws->stage + shift - R0;
-            for (int o = my0; o < my1; ++o) {
-                while (w == 0u) {
+            for (int o = my0 - R0; o < my1 - R0; ++o) {
+                if (w == 0u) {
                     ++wi;
                     w = ws->w[wi];
                     rb = ws->rb[wi];
                 }
-                st[o] = rb + (__ffs(w) - 1);
+                ws->stage[o + (o >> 5)] = rb + (__ffs(w) - 1);
                 w &= w - 1u;
             }
         }
         __syncwarp();
-        // stage[shift + i] -> out[R0 + i]; both 16-byte aligned where (shift + i) % 4 == 0
         int32_t* dst = out + R0;
-        const int h = min(RE, (4 - shift) & 3);
-        if (lane < h) dst[lane] = ws->stage[shift + lane];
-        const int nb = (RE - h) >> 2;
-        const uint4* s4 = reinterpret_cast<const uint4*>(ws->stage + shift + h);
-        uint4* d4 = reinterpret_cast<uint4*>(dst + h);
-        for (int q = lane; q < nb; q += 32) d4[q] = s4[q];
-        const int tl = h + (nb << 2);
-        if (tl + lane < RE) dst[tl + lane] = ws->stage[shift + tl + lane];
+        for (int i = lane; i < RE; i += 32) dst[i] = ws->stage[i + (i >> 5)];
         __syncwarp();
     }
 }
@@ -467,18 +458,29 @@ __global__ void __launch_bounds__(NT) k_tile_emit(EmitArgs g) {
     for (int b = warp; b < nblk; b += NW) {
         const int E = blk[b + 1] - blk[b];
         if (!E) continue;
-        int cnt = 0;
+        unsigned xs[kEmitWPL];
+        int cnt = 0, nz = 0;
 #pragma unroll
         for (int q = 0; q < kEmitWPL; ++q) {
-            const int li = lane * kEmitWPL + q;
-            const int w = b * kEmitBlock + li;
-            const unsigned x = w < nwords ? words[w] : 0u;
-            ws->w[li] = x;
-            ws->rb[li] = t0 + ((idx ? (w < nwords ? (int)idx[w] : 0) : w) << 5);
-            cnt += __popc(x);
+            const int w = b * kEmitBlock + lane * kEmitWPL + q;
+            xs[q] = w < nwords ? words[w] : 0u;
+            cnt += __popc(xs[q]);
+            nz += xs[q] != 0u;
+        }
+        int nzt;
+        const int pos = warp_excl_scan(nz, lane, &nzt);
+        int p = pos;
+#pragma unroll
+        for (int q = 0; q < kEmitWPL; ++q) {
+            if (xs[q]) {
+                const int w = b * kEmitBlock + lane * kEmitWPL + q;
+                ws->w[p] = xs[q];
+                ws->rb[p] = t0 + ((idx ? (int)idx[w] : w) << 5);
+                ++p;
+            }
         }
         __syncwarp();
-        emit_block(ws, cnt, E, g.crw + off + blk[b], lane);
+        emit_block(ws, pos, cnt, E, g.crw + off + blk[b], lane);
     }
     if (g.cv) {
         // values: c bytes of 1 (head bytes, 16-byte body, tail bytes)
@@ -696,8 +698,7 @@ T d2h(Ctx& c, const T* p) {
     return v;
 }
 
-constexpr int kFormThreads = 256;
-constexpr int kEmitThreads = 256;
+constexpr int kFormThreads = 256;  // split-item combine
 constexpr int kMaxParts = 64;
 
 }  // namespace
@@ -770,8 +771,9 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
     BinSpec spec{};
     spec.nlight = 8;
     for (int b = 0; b < 8; ++b) spec.thr[b] = int64_t(32) << b;
-    int64_t lmax = std::max<int64_t>(256, std::min<int64_t>(A.nrows / 128, 4096));
-    if (c.opt.light_flops_max != Options{}.light_flops_max) lmax = std::min<int64_t>(c.opt.light_flops_max, 4096);
+    // columns above 1024 multiplies go to the tile items: the hash kernels'
+    // block-wide sorts of 2-8K keys cost more than a few small tile items
+    int64_t lmax = std::min<int64_t>(c.opt.direct_light_flops_max, 4096);
     spec.light_max = lmax;
     spec.all_heavy = alg == SLAPCU_ALG_HEAP;
     f.cnt.reset(sizeof(int64_t) * (n + 1), c.stream);
@@ -904,15 +906,21 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
                    (const int64_t*)d.sres.as<int64_t>(), d.partial.as<unsigned>(), d.cnt.as<int64_t>(),
                    d.form.as<int>(), d.hcnt.as<unsigned long long>()};
         const size_t smem = sizeof(unsigned) * W + sizeof(int) * (W / 32 + 1);
-        auto form = [&](auto kf) {
+        auto form = [&](auto kf, int nt) {
             ensure_smem(kf, smem);
-            launch(c, kf, dim3((unsigned)nunits), dim3(kFormThreads), smem, g);
+            launch(c, kf, dim3((unsigned)nunits), dim3(nt), smem, g);
         };
-        switch (c.opt.direct_mark_mode) {
-        case 1: form(k_tile_form<kFormThreads, 1>); break;
-        case 2: form(k_tile_form<kFormThreads, 2>); break;
-        default: form(k_tile_form<kFormThreads, 0>); break;
-        }
+        const int ft = c.opt.direct_form_threads;
+        if (c.opt.direct_mark_mode == 2)
+            form(k_tile_form<256, 2>, 256);
+        else if (c.opt.direct_mark_mode == 1)
+            form(k_tile_form<256, 1>, 256);
+        else if (ft == 128)
+            form(k_tile_form<128, 0>, 128);
+        else if (ft == 512)
+            form(k_tile_form<512, 0>, 512);
+        else
+            form(k_tile_form<256, 0>, 256);
         if (nsplit > 0) {
             auto kc = k_tile_combine<kFormThreads>;
             ensure_smem(kc, smem);
@@ -945,9 +953,14 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
                    (const int64_t*)d.hoff.as<int64_t>(), (const int64_t*)d.lp.as<int64_t>(), TL, crw,
                    static_cast<uint8_t*>(cv)};
         const size_t smem = sizeof(int) * (W / kEmitBlock + 2);
-        auto ke = k_tile_emit<kEmitThreads>;
-        ensure_smem(ke, smem);
-        launch(c, ke, dim3(nitems), dim3(kEmitThreads), smem, e);
+        auto emit = [&](auto ke, int nt) {
+            ensure_smem(ke, smem);
+            launch(c, ke, dim3(nitems), dim3(nt), smem, e);
+        };
+        if (c.opt.direct_emit_threads == 128)
+            emit(k_tile_emit<128>, 128);
+        else
+            emit(k_tile_emit<256>, 256);
     }
     if (nlight) {
         KScope ks(c, KC_NUM_LIGHT);
