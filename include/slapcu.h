@@ -120,7 +120,14 @@ typedef enum {
                                               1 shared atomic per product, 2 lane-contiguous quads merged
                                               per 32-row word before the update */
     SLAPCU_OPT_DIRECT_FORM_THREADS = 12,   /* direct path: threads per form CTA (128, 256, 512) */
-    SLAPCU_OPT_DIRECT_EMIT_THREADS = 13    /* direct path: threads per emit CTA (128, 256) */
+    SLAPCU_OPT_DIRECT_EMIT_THREADS = 13,   /* direct path: threads per emit CTA (128, 256) */
+    SLAPCU_OPT_DIRECT_DENSE_RUN_MIN = 14,  /* direct path: A(:,k) runs inside one row tile with at least
+                                              this many entries are OR-ed as cached tile bitmaps
+                                              (default 2048, 0 = never) */
+    SLAPCU_OPT_DIRECT_PERSISTENT = 15,     /* direct path form kernel: 1 persistent CTAs taking units by
+                                              ticket, 0 one CTA per unit */
+    SLAPCU_OPT_DIRECT_SPARSE_RUN_MAX = 16  /* direct path: A runs shorter than this update the bitmap
+                                              without the test load (default 0 = never) */
 } slapcu_option;
 slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t value);
 

@@ -143,8 +143,13 @@ slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t v
             c.opt.direct_tile_rows_log2 = (int)v;
             break;
         case SLAPCU_OPT_DIRECT_MARK_MODE:
-            require(v >= 0 && v <= 2, SLAPCU_ERR_INVALID, "mark mode must be 0, 1 or 2");
+            require(v >= 0 && v <= 3, SLAPCU_ERR_INVALID, "mark mode must be 0..3 (3: timing experiment, no update)");
             c.opt.direct_mark_mode = (int)v;
+            break;
+        case SLAPCU_OPT_DIRECT_PERSISTENT: c.opt.direct_persistent = v != 0; break;
+        case SLAPCU_OPT_DIRECT_SPARSE_RUN_MAX:
+            require(v >= 0, SLAPCU_ERR_INVALID, "sparse run threshold must be >= 0");
+            c.opt.direct_sparse_run_max = v;
             break;
         case SLAPCU_OPT_DIRECT_FORM_THREADS:
             require(v == 128 || v == 256 || v == 512, SLAPCU_ERR_INVALID, "form threads: 128, 256 or 512");
@@ -153,6 +158,10 @@ slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t v
         case SLAPCU_OPT_DIRECT_EMIT_THREADS:
             require(v == 128 || v == 256, SLAPCU_ERR_INVALID, "emit threads: 128 or 256");
             c.opt.direct_emit_threads = (int)v;
+            break;
+        case SLAPCU_OPT_DIRECT_DENSE_RUN_MIN:
+            require(v >= 0, SLAPCU_ERR_INVALID, "dense run threshold must be >= 0");
+            c.opt.direct_dense_run_min = v;
             break;
         case SLAPCU_OPT_DIRECT_SPLIT_FLOPS:
             require(v >= 1024, SLAPCU_ERR_INVALID, "split threshold must be >= 1024");

@@ -123,7 +123,11 @@ struct Options {
     bool async_finish = false;        // finish() returns without waiting (errors surface later)
     int direct_tile_rows_log2 = 17;   // direct path: row-tile height of an item (16 KB bitmap)
     int64_t direct_light_flops_max = 1024;  // direct path: hash path for columns up to this many flops
+    int64_t direct_dense_run_min = 2048;    // direct path: A runs (column x tile) this long are OR-ed
+                                            // as precomputed tile bitmaps (0 = never)
     int direct_mark_mode = 0;               // product update: 0 test+set, 1 atomic only, 2 quad-merged
+    int64_t direct_sparse_run_max = 0;      // direct path: runs shorter than this update without a test
+    int direct_persistent = 1;              // form kernel: persistent CTAs (1) or one CTA per unit (0)
     int direct_form_threads = 256;          // CTA size of the form kernel (128, 256, 512)
     int direct_emit_threads = 128;          // CTA size of the emit kernel (128, 256)
     int64_t direct_split_flops = 1 << 20;  // direct path: items above this many multiplies are
@@ -138,6 +142,8 @@ struct DirectCache {
     int64_t atp_ncols = -1, atp_nnz = -1;
     int atp_tl = -1;
     bool atp_valid = false;
+    DevBuf dslot, dbm;  // dense A runs: slot per (k, tile), tile bitmaps
+    int ndense = 0, dense_min = -1;
     DevBuf lp, hcnt, hl, items, ifl, sres, soff, units, order, stash, partial, cnt, form, hoff;
     int64_t last_nnz = -1;  // exact nnz(C) of the last call (also on BudgetError)
 };

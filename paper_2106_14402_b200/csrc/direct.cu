@@ -40,7 +40,7 @@ namespace slapcu {
 namespace {
 
 constexpr int kShortRun = 32;  // runs shorter than this are walked by one thread
-constexpr int kUnit = 1024;    // products per warp work unit on long runs
+constexpr int kUnit = 256;     // products per warp work unit on long runs
 
 __host__ __device__ __forceinline__ int64_t lmin(int64_t a, int64_t b) { return a < b ? a : b; }
 
@@ -73,32 +73,63 @@ struct WalkSm {
     int ustart[NT + 1];
     int len[NT];
     int64_t start[NT];
+    int ndense, nlong;
+    int dense[NT];  // dense-run bitmap slots met in this batch of B entries
+};
+
+// Dense A runs: A(:,k) restricted to row tile t with at least `dmin` entries
+// is kept (per A, cached) as a bitmap of the tile, so an item OR-s whole words
+// (one coalesced load + one conflict-free shared update per 32 rows) instead
+// of marking each product.  slot[k*T + t] = bitmap index or -1.
+struct DenseRuns {
+    const int* slot;
+    const unsigned* bm;
+    int dmin;  // 0: none
 };
 
 // Sets bits `b` of word address `a` (shared window): test before set -- a
 // plain shared load is a broadcast for lanes hitting one word, and most
 // products of a dense column find their bits already set.  MODE 1 skips the
 // test (one shared atomic per product).
+// Sets bits `b` of the bitmap word at shared address `a`; the first setter of
+// a word (it read the word as 0) also sets the word's bit `sb` in the
+// summary word at `sa`, so the passes after the walk visit touched words only.
+// Test before set: a plain shared load is a broadcast for lanes hitting one
+// word, and most products of a dense column find their bits already set.
+// (No "memory" clobber: the bitmap is only read back after a __syncthreads,
+// and a clobber would stop the compiler from issuing the next products'
+// global loads ahead of these shared updates.)
 template <int MODE>
-__device__ __forceinline__ void set_bits(unsigned a, unsigned b) {
-    if (MODE == 1) {
-        asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(b) : "memory");
-    } else {
+__device__ __forceinline__ void set_bits(unsigned a, unsigned b, unsigned sa, unsigned sb) {
+    if (MODE == 3) {  // timing experiment only: no update (wrong results)
+        asm volatile("" ::"r"(a), "r"(b), "r"(sa), "r"(sb));
+    } else if (MODE == 0) {  // bitmap only; the summary is rebuilt by a ballot pass
         asm volatile(
             "{\n\t.reg .pred p;\n\t.reg .b32 x;\n\t"
             "ld.shared.u32 x, [%0];\n\t"
             "and.b32 x, x, %1;\n\t"
             "setp.ne.u32 p, x, %1;\n\t"
             "@p red.shared.or.b32 [%0], %1;\n\t}" ::"r"(a),
-            "r"(b)
-            : "memory");
+            "r"(b));
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred p, q;\n\t.reg .b32 x, y;\n\t"
+            "ld.shared.u32 x, [%0];\n\t"
+            "and.b32 y, x, %1;\n\t"
+            "setp.ne.u32 p, y, %1;\n\t"
+            "setp.eq.and.u32 q, x, 0, p;\n\t"
+            "@p red.shared.or.b32 [%0], %1;\n\t"
+            "@q red.shared.or.b32 [%2], %3;\n\t}" ::"r"(a),
+            "r"(b), "r"(sa), "r"(sb));
     }
 }
 
-// Marks row rr of the current tile (bitmap at shared address bmA).
+// Marks absolute row rr: bmA / sumA are the bitmap / summary base addresses
+// shifted by the tile origin so that rows index them directly.
 template <int MODE>
-__device__ __forceinline__ void mark(unsigned bmA, int rr) {
-    set_bits<MODE>(bmA + (unsigned(rr >> 5) << 2), 1u << (rr & 31));
+__device__ __forceinline__ void mark(unsigned bmA, unsigned sumA, int rr) {
+    set_bits<MODE>(bmA + (unsigned(rr >> 5) << 2), 1u << (rr & 31), sumA + (unsigned(rr >> 10) << 2),
+                   1u << ((rr >> 5) & 31));
 }
 
 // All products of B entries [b0, b1) (column j) whose rows lie in tile t,
@@ -109,14 +140,18 @@ __device__ __forceinline__ void mark(unsigned bmA, int rr) {
 // a unit is found by advancing, not searching).
 template <int NT, int U, int MODE>
 __device__ __forceinline__ void tile_walk(const DevCsc& A, const DevCsc& B, const int32_t* __restrict__ Atp, int T,
-                                          int64_t b0, int64_t b1, int t, int t0, unsigned* bm, WalkSm<NT>& sh) {
+                                          int64_t b0, int64_t b1, int t, int t0, unsigned* bm, unsigned* summ,
+                                          WalkSm<NT>& sh, const DenseRuns& dr, int W, int sparse_max) {
     constexpr int NW = NT / 32;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int32_t* __restrict__ Arw = A.rw;
-    const unsigned bmA = smem_addr(bm) - (unsigned(t0 >> 5) << 2);  // rows index the tile directly
+    const unsigned bm0 = smem_addr(bm), sum0 = smem_addr(summ);
+    const unsigned bmA = bm0 - (unsigned(t0 >> 5) << 2);  // rows index the tile directly
+    const unsigned sumA = sum0 - (unsigned(t0 >> 10) << 2);
+    // (sh.ndense and sh.nlong are zeroed by the caller before a barrier)
     for (int64_t base = b0; base < b1; base += NT) {
         const int64_t i = base + tid;
-        int units = 0, len = 0;
+        int len = 0;
         int64_t s = 0;
         if (i < b1) {
             const int k = B.rw[i];
@@ -124,27 +159,47 @@ __device__ __forceinline__ void tile_walk(const DevCsc& A, const DevCsc& B, cons
             const int lo = tp[0], hi = tp[1];
             s = A.cp[k] + lo;
             len = hi - lo;
-            if (len < kShortRun) {
+            if (dr.dmin && len >= dr.dmin) {
+                sh.dense[atomicAdd(&sh.ndense, 1)] = dr.slot[int64_t(k) * T + t];
+                len = 0;
+            } else if (len < kShortRun) {
+                // loads in groups of 4 so a short run is not a chain of L2 round trips
                 const int32_t* q = Arw + s;
-                for (int x = 0; x < len; ++x) mark<MODE & 1>(bmA, __ldg(q + x));
+                int x = 0;
+                for (; x + 4 <= len; x += 4) {
+                    const int r0 = __ldg(q + x), r1 = __ldg(q + x + 1), r2 = __ldg(q + x + 2), r3 = __ldg(q + x + 3);
+                    mark<MODE>(bmA, sumA, r0);
+                    mark<MODE>(bmA, sumA, r1);
+                    mark<MODE>(bmA, sumA, r2);
+                    mark<MODE>(bmA, sumA, r3);
+                }
+                for (; x < len; ++x) mark<MODE>(bmA, sumA, __ldg(q + x));
                 len = 0;
             } else {
-                units = (len + kUnit - 1) / kUnit;
+                // long run: into the compact list (order is irrelevant)
+                const unsigned peers = __activemask();
+                const int leader = __ffs(peers) - 1;
+                int pos = 0;
+                if (lane == leader) pos = atomicAdd(&sh.nlong, __popc(peers));
+                pos = __shfl_sync(peers, pos, leader) + __popc(peers & ((1u << lane) - 1u));
+                sh.len[pos] = len;
+                sh.start[pos] = s;
             }
         }
+        __syncthreads();
+        const int nl = sh.nlong;
+        const int units = tid < nl ? (sh.len[tid] + kUnit - 1) / kUnit : 0;
         int tot;
         const int ex = block_excl_scan<NT>(units, sh.wsum, &tot);
         sh.ustart[tid] = ex;
-        sh.len[tid] = len;
-        sh.start[tid] = s;
-        if (tid == 0) sh.ustart[NT] = tot;
+        if (tid == 0) sh.ustart[nl] = tot;
         __syncthreads();
         // warp w takes the contiguous unit range [u0, u1): one search for the
-        // owning entry, then it only advances
+        // owning long run, then it only advances (every long run has units)
         const int u0 = (int)((int64_t(tot) * warp) / NW), u1 = (int)((int64_t(tot) * (warp + 1)) / NW);
         int e = 0;
         if (u0 < u1) {
-            int lo = 0, hi = NT - 1;
+            int lo = 0, hi = nl - 1;
             while (lo < hi) {
                 const int mid = (lo + hi + 1) >> 1;
                 if (sh.ustart[mid] <= u0)
@@ -155,49 +210,52 @@ __device__ __forceinline__ void tile_walk(const DevCsc& A, const DevCsc& B, cons
             e = lo;
         }
         for (int u = u0; u < u1; ++u) {
-            while (sh.ustart[e + 1] <= u) ++e;  // entry owning unit u
+            if (sh.ustart[e + 1] <= u) ++e;
             const int c0 = (u - sh.ustart[e]) * kUnit;
             const int32_t* run = Arw + sh.start[e] + c0;
             const int m = min(kUnit, sh.len[e] - c0);
-            if (MODE == 2) {
-                // lane-contiguous quads (16-byte loads from the aligned-down
-                // run start); rows of a quad sharing a word are OR-ed in
-                // registers first, so a dense run costs one shared update per
-                // word instead of one per product
-                const int mis = (int)((reinterpret_cast<uintptr_t>(run) >> 2) & 3);
-                const int4* q4 = reinterpret_cast<const int4*>(run - mis);
-                const int total = m + mis;
-                for (int x = 4 * lane; x < total; x += 128) {
-                    const int4 q = __ldg(q4 + (x >> 2));
-                    const int rv[4] = {q.x, q.y, q.z, q.w};
-                    int cw = -1;
-                    unsigned acc = 0;
-#pragma unroll
-                    for (int v = 0; v < 4; ++v) {
-                        const int pos = x + v - mis;
-                        if (pos >= 0 && pos < m) {
-                            const int w = rv[v] >> 5;
-                            if (w != cw) {
-                                if (cw >= 0) set_bits<0>(bmA + (unsigned(cw) << 2), acc);
-                                cw = w;
-                                acc = 0;
-                            }
-                            acc |= 1u << (rv[v] & 31);
-                        }
-                    }
-                    if (cw >= 0) set_bits<0>(bmA + (unsigned(cw) << 2), acc);
-                }
-            } else {
-                int x = lane;
+            int x = lane;
+            if (sparse_max && sh.len[e] < sparse_max) {
+                // sparse run: consecutive entries fall in different words and
+                // their bits are mostly unset -- skip the test load
                 for (; x + 32 * (U - 1) < m; x += 32 * U) {
                     int r[U];
 #pragma unroll
                     for (int v = 0; v < U; ++v) r[v] = __ldg(run + x + 32 * v);
 #pragma unroll
-                    for (int v = 0; v < U; ++v) mark<MODE>(bmA, r[v]);
+                    for (int v = 0; v < U; ++v) mark<1>(bmA, sumA, r[v]);
                 }
-                for (; x < m; x += 32) mark<MODE>(bmA, __ldg(run + x));
+                for (; x < m; x += 32) mark<1>(bmA, sumA, __ldg(run + x));
+                continue;
             }
+            for (; x + 32 * (U - 1) < m; x += 32 * U) {
+                int r[U];
+#pragma unroll
+                for (int v = 0; v < U; ++v) r[v] = __ldg(run + x + 32 * v);
+#pragma unroll
+                for (int v = 0; v < U; ++v) mark<MODE>(bmA, sumA, r[v]);
+            }
+            for (; x < m; x += 32) mark<MODE>(bmA, sumA, __ldg(run + x));
+        }
+        // dense runs of this batch: OR whole words of their tile bitmaps
+        const int nd = sh.ndense;
+        for (int di = 0; di < nd; ++di) {
+            const uint4* src = reinterpret_cast<const uint4*>(dr.bm + int64_t(sh.dense[di]) * W);
+            for (int q = tid; q < (W >> 2); q += NT) {
+                const uint4 v = __ldg(src + q);
+                const unsigned a = bm0 + (unsigned(q) << 4);
+                const unsigned sa = sum0 + (unsigned(q >> 3) << 2);
+                const unsigned sb = 1u << ((q << 2) & 31);
+                if (v.x) set_bits<MODE>(a, v.x, sa, sb);
+                if (v.y) set_bits<MODE>(a + 4, v.y, sa, sb << 1);
+                if (v.z) set_bits<MODE>(a + 8, v.z, sa, sb << 2);
+                if (v.w) set_bits<MODE>(a + 12, v.w, sa, sb << 3);
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            sh.ndense = 0;
+            sh.nlong = 0;
         }
         __syncthreads();
     }
@@ -208,6 +266,7 @@ __device__ __forceinline__ void tile_walk(const DevCsc& A, const DevCsc& B, cons
 struct FormArgs {
     DevCsc A, B;
     const int32_t* Atp;
+    DenseRuns dr;
     int T, TL;
     const int2* items;      // (column, tile) in C order
     const int4* units;      // (item, b0, b1 relative to B.cp[j], partial slot or -1)
@@ -219,59 +278,60 @@ struct FormArgs {
     int64_t* cnt;           // output entries per item
     int* form;              // -1 bitmap, else number of listed words
     unsigned long long* hcnt;  // output entries per column (heavy part)
+    int* ticket;
+    int nunits;
+    int sparse_max;  // runs shorter than this skip the test-before-set (0 = never)
 };
 
-// Count, choose the stash form and write it (whole CTA; bm holds the item's
-// tile bitmap).  `chunk` has W/32 + 1 ints of shared scratch.
+// Count, choose the stash form and write it, then clear the bitmap (whole
+// CTA).  bm holds the item's tile bitmap and summ its touched-word summary
+// (W/32 words); tl is shared scratch for W word indices.
 template <int NT>
-__device__ __forceinline__ void stash_bitmap(const unsigned* bm, int W, int* chunk, int* red, int64_t item, int j,
-                                             unsigned* stash, int64_t sres, int64_t* cnt, int* form,
-                                             unsigned long long* hcnt) {
+__device__ __forceinline__ void stash_bitmap(unsigned* bm, unsigned* summ, uint16_t* tl, int W, int* wsum, int* red,
+                                             int64_t item, int j, unsigned* stash, int64_t sres, int64_t* cnt,
+                                             int* form, unsigned long long* hcnt) {
     constexpr int NW = NT / 32;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int nch = W >> 5;
+    const int WS = W >> 5;
+    // touched words in order: summary popcounts -> scan -> list (WS <= NT)
+    unsigned sw = 0;
+    if (tid < WS) {
+        sw = summ[tid];
+        summ[tid] = 0u;
+    }
+    int U;
+    int base = block_excl_scan<NT>(__popc(sw), wsum, &U);
+    while (sw) {
+        tl[base++] = (uint16_t)(tid * 32 + __ffs(sw) - 1);
+        sw &= sw - 1u;
+    }
+    __syncthreads();
+    const int64_t lw = int64_t(U) + (U + 1) / 2;  // words + 16-bit word indices
+    const bool list = lw < W && lw <= sres;
     int myc = 0;
-    for (int cc = warp; cc < nch; cc += NW) {
-        const unsigned x = bm[cc * 32 + lane];
-        const unsigned nz = __ballot_sync(0xffffffffu, x != 0u);
-        myc += __popc(x);
-        if (lane == 0) chunk[cc] = __popc(nz);
+    if (list) {
+        uint16_t* idx = reinterpret_cast<uint16_t*>(stash + U);
+        for (int q = tid; q < U; q += NT) {
+            const int w = tl[q];
+            const unsigned x = bm[w];
+            bm[w] = 0u;
+            stash[q] = x;
+            idx[q] = (uint16_t)w;
+            myc += __popc(x);
+        }
+    } else {
+        uint4* d4 = reinterpret_cast<uint4*>(stash);
+        uint4* s4 = reinterpret_cast<uint4*>(bm);
+        for (int q = tid; q < W / 4; q += NT) {
+            const uint4 x = s4[q];
+            d4[q] = x;
+            s4[q] = make_uint4(0u, 0u, 0u, 0u);
+            myc += __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
+        }
     }
     myc = warp_reduce_sum(myc);
     if (lane == 0) red[warp] = myc;
     __syncthreads();
-    if (warp == 0) {
-        int run = 0;
-        for (int b0 = 0; b0 < nch; b0 += 32) {
-            const int cix = b0 + lane;
-            const int x = cix < nch ? chunk[cix] : 0;
-            int tt;
-            const int e = warp_excl_scan(x, lane, &tt);
-            if (cix < nch) chunk[cix] = run + e;
-            run += tt;
-        }
-        if (lane == 0) chunk[nch] = run;
-    }
-    __syncthreads();
-    const int U = chunk[nch];
-    const int64_t lw = int64_t(U) + (U + 1) / 2;  // words + 16-bit word indices
-    const bool list = lw < W && lw <= sres;
-    if (list) {
-        uint16_t* idx = reinterpret_cast<uint16_t*>(stash + U);
-        for (int cc = warp; cc < nch; cc += NW) {
-            const unsigned x = bm[cc * 32 + lane];
-            const unsigned nz = __ballot_sync(0xffffffffu, x != 0u);
-            if (x) {
-                const int pos = chunk[cc] + __popc(nz & ((1u << lane) - 1u));
-                stash[pos] = x;
-                idx[pos] = (uint16_t)(cc * 32 + lane);
-            }
-        }
-    } else {
-        uint4* d4 = reinterpret_cast<uint4*>(stash);
-        const uint4* s4 = reinterpret_cast<const uint4*>(bm);
-        for (int q = tid; q < W / 4; q += NT) d4[q] = s4[q];
-    }
     if (tid == 0) {
         long long c = 0;
         for (int w = 0; w < NW; ++w) c += red[w];
@@ -281,27 +341,53 @@ __device__ __forceinline__ void stash_bitmap(const unsigned* bm, int W, int* chu
     }
 }
 
+// Persistent: each CTA takes work units (heaviest first) by ticket.
 template <int NT, int MODE>
 __global__ void __launch_bounds__(NT) k_tile_form(FormArgs g) {
     extern __shared__ __align__(16) unsigned char sm_raw[];
     const int W = 1 << (g.TL - 5);
     unsigned* bm = reinterpret_cast<unsigned*>(sm_raw);
-    int* chunk = reinterpret_cast<int*>(bm + W);  // [W/32 + 1]
+    unsigned* summ = bm + W;                                // [W/32]
+    uint16_t* tl = reinterpret_cast<uint16_t*>(summ + W / 32);  // [W]
     __shared__ WalkSm<NT> sh;
     __shared__ int red[NT / 32];
-    const int4 u = g.units[g.order[blockIdx.x]];
-    const int2 it = g.items[u.x];
-    const int64_t bs = g.B.cp[it.x];
-    smem_zero(bm, W);
-    __syncthreads();
-    tile_walk<NT, 4, MODE>(g.A, g.B, g.Atp, g.T, bs + u.y, bs + u.z, it.y, it.y << g.TL, bm, sh);
-    if (u.w >= 0) {  // one part of a split item: partial bitmap out
-        uint4* d4 = reinterpret_cast<uint4*>(g.partial + int64_t(u.w) * W);
-        const uint4* s4 = reinterpret_cast<const uint4*>(bm);
-        for (int q = threadIdx.x; q < W / 4; q += NT) d4[q] = s4[q];
-        return;
+    __shared__ int ticket_sh;
+    smem_zero(bm, W + W / 32);
+    for (;;) {
+        if (threadIdx.x == 0) {
+            ticket_sh = atomicAdd(g.ticket, 1);
+            sh.ndense = 0;
+            sh.nlong = 0;
+        }
+        __syncthreads();
+        const int ui = ticket_sh;
+        if (ui >= g.nunits) break;
+        const int4 u = g.units[g.order[ui]];
+        const int2 it = g.items[u.x];
+        const int64_t bs = g.B.cp[it.x];
+        tile_walk<NT, 4, MODE>(g.A, g.B, g.Atp, g.T, bs + u.y, bs + u.z, it.y, it.y << g.TL, bm, summ, sh, g.dr, W, g.sparse_max);
+        if (MODE != 2 && u.w < 0) {  // summary by ballots over the bitmap
+            const int lane = threadIdx.x & 31;
+            for (int cc = threadIdx.x >> 5; cc < W / 32; cc += NT / 32) {
+                const unsigned nz = __ballot_sync(0xffffffffu, bm[cc * 32 + lane] != 0u);
+                if (lane == 0) summ[cc] = nz;
+            }
+            __syncthreads();
+        }
+        if (u.w >= 0) {  // one part of a split item: partial bitmap out, then clear
+            uint4* d4 = reinterpret_cast<uint4*>(g.partial + int64_t(u.w) * W);
+            uint4* s4 = reinterpret_cast<uint4*>(bm);
+            for (int q = threadIdx.x; q < W / 4; q += NT) {
+                d4[q] = s4[q];
+                s4[q] = make_uint4(0u, 0u, 0u, 0u);
+            }
+            for (int q = threadIdx.x; q < W / 32; q += NT) summ[q] = 0u;
+        } else {
+            stash_bitmap<NT>(bm, summ, tl, W, sh.wsum, red, u.x, it.x, g.stash + g.soff[u.x], g.sres[u.x], g.cnt,
+                             g.form, g.hcnt);
+        }
+        __syncthreads();
     }
-    stash_bitmap<NT>(bm, W, chunk, red, u.x, it.x, g.stash + g.soff[u.x], g.sres[u.x], g.cnt, g.form, g.hcnt);
 }
 
 // OR of the partial bitmaps of each split item -> its stash (bitmap or list).
@@ -311,28 +397,29 @@ __global__ void __launch_bounds__(NT)
                    const int* __restrict__ spart, const int* __restrict__ snp, const unsigned* __restrict__ partial,
                    unsigned* __restrict__ stash, const int64_t* __restrict__ soff, const int64_t* __restrict__ sres,
                    int64_t* __restrict__ cnt, int* __restrict__ form, unsigned long long* __restrict__ hcnt) {
+    constexpr int NW = NT / 32;
     extern __shared__ __align__(16) unsigned char sm_raw[];
     const int W = 1 << (TL - 5);
     unsigned* bm = reinterpret_cast<unsigned*>(sm_raw);
-    int* chunk = reinterpret_cast<int*>(bm + W);
-    __shared__ int red[NT / 32];
+    unsigned* summ = bm + W;
+    uint16_t* tl = reinterpret_cast<uint16_t*>(summ + W / 32);
+    __shared__ int red[NW];
+    __shared__ int wsum[NW + 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int item = sitems[blockIdx.x];
     const int np = snp[blockIdx.x];
-    const uint4* p4 = reinterpret_cast<const uint4*>(partial + int64_t(spart[blockIdx.x]) * W);
-    uint4* b4 = reinterpret_cast<uint4*>(bm);
-    for (int q = threadIdx.x; q < W / 4; q += NT) {
-        uint4 x = p4[q];
-        for (int p = 1; p < np; ++p) {
-            const uint4 y = p4[int64_t(p) * (W / 4) + q];
-            x.x |= y.x;
-            x.y |= y.y;
-            x.z |= y.z;
-            x.w |= y.w;
-        }
-        b4[q] = x;
+    const unsigned* p0 = partial + int64_t(spart[blockIdx.x]) * W;
+    for (int cc = warp; cc < W / 32; cc += NW) {
+        const int w = cc * 32 + lane;
+        unsigned x = 0;
+        for (int p = 0; p < np; ++p) x |= p0[int64_t(p) * W + w];
+        bm[w] = x;
+        const unsigned nz = __ballot_sync(0xffffffffu, x != 0u);
+        if (lane == 0) summ[cc] = nz;
     }
     __syncthreads();
-    stash_bitmap<NT>(bm, W, chunk, red, item, items[item].x, stash + soff[item], sres[item], cnt, form, hcnt);
+    stash_bitmap<NT>(bm, summ, tl, W, wsum, red, item, items[item].x, stash + soff[item], sres[item], cnt, form,
+                     hcnt);
 }
 
 // ------------------------------------------------------------------- emit
@@ -521,6 +608,50 @@ __global__ void k_tile_ptr(DevCsc A, int TL, int T, int32_t* __restrict__ Atp) {
         }
         Atp[x] = (int32_t)(lo - as);
     }
+}
+
+__global__ void k_dense_flag(int64_t nkt, int T, const int32_t* __restrict__ Atp, int dmin, int* __restrict__ flag) {
+    for (int64_t x = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < nkt; x += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t k = x / T;
+        const int t = (int)(x - k * T);
+        const int32_t* tp = Atp + k * (T + 1) + t;
+        flag[x] = (tp[1] - tp[0]) >= dmin;
+    }
+}
+
+__global__ void k_dense_slot(int64_t nkt, const int* __restrict__ flag, const int* __restrict__ pre,
+                             int* __restrict__ slot, int2* __restrict__ runs, int T) {
+    for (int64_t x = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < nkt; x += int64_t(gridDim.x) * blockDim.x) {
+        if (flag[x]) {
+            slot[x] = pre[x];
+            runs[pre[x]] = make_int2((int)(x / T), (int)(x % T));
+        } else {
+            slot[x] = -1;
+        }
+    }
+}
+
+// One CTA per dense run: its rows of the tile as a bitmap.
+template <int NT>
+__global__ void __launch_bounds__(NT)
+    k_dense_build(DevCsc A, const int32_t* __restrict__ Atp, int T, int TL, const int2* __restrict__ runs,
+                  unsigned* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned bmd[];
+    const int W = 1 << (TL - 5);
+    const int2 r = runs[blockIdx.x];
+    smem_zero(bmd, W);
+    __syncthreads();
+    const int32_t* tp = Atp + int64_t(r.x) * (T + 1) + r.y;
+    const int64_t s = A.cp[r.x] + tp[0], e = A.cp[r.x] + tp[1];
+    const int t0 = r.y << TL;
+    for (int64_t p = s + threadIdx.x; p < e; p += NT) {
+        const int rr = A.rw[p] - t0;
+        atomicOr(&bmd[rr >> 5], 1u << (rr & 31));
+    }
+    __syncthreads();
+    uint4* d4 = reinterpret_cast<uint4*>(out + int64_t(blockIdx.x) * W);
+    const uint4* s4 = reinterpret_cast<const uint4*>(bmd);
+    for (int q = threadIdx.x; q < W / 4; q += NT) d4[q] = s4[q];
 }
 
 // Per heavy column (column order) and tile: multiplies, and the number of
@@ -712,11 +843,36 @@ int direct_tile_log2(const Ctx& c, int64_t nrows) {
 // Tile pointers of A for row tiles of 2^TL rows (cached on the context).
 static const int32_t* tile_pointers(Ctx& c, const DevCsc& A, int TL, int T) {
     DirectCache& d = c.direct;
-    if (d.atp_valid && d.atp_key == A.cp && d.atp_ncols == A.ncols && d.atp_tl == TL && d.atp_nnz == A.nnz)
+    const int dmin = (int)std::min<int64_t>(c.opt.direct_dense_run_min, INT32_MAX);
+    if (d.atp_valid && d.atp_key == A.cp && d.atp_ncols == A.ncols && d.atp_tl == TL && d.atp_nnz == A.nnz &&
+        d.dense_min == dmin)
         return d.atp.as<int32_t>();
     d.atp.reset(sizeof(int32_t) * size_t(A.ncols) * (T + 1), c.stream);
     KScope ks(c, KC_BIN);
     launch(c, k_tile_ptr, dim3(grid_for(c, A.ncols * (T + 1), 256)), dim3(256), 0, A, TL, T, d.atp.as<int32_t>());
+    d.ndense = 0;
+    d.dense_min = dmin;
+    if (dmin > 0) {
+        const int64_t nkt = A.ncols * int64_t(T);
+        DevBuf flag(sizeof(int) * (nkt + 1), c.stream), pre(sizeof(int) * (nkt + 1), c.stream);
+        SLAPCU_CUDA(cudaMemsetAsync(flag.as<int>() + nkt, 0, sizeof(int), c.stream));
+        launch(c, k_dense_flag, dim3(grid_for(c, nkt, 256)), dim3(256), 0, nkt, T, (const int32_t*)d.atp.as<int32_t>(),
+               dmin, flag.as<int>());
+        excl_scan_i32(c, flag.as<int>(), pre.as<int>(), nkt + 1);
+        d.ndense = d2h(c, pre.as<int>() + nkt);
+        d.dslot.reset(sizeof(int) * std::max<int64_t>(nkt, 1), c.stream);
+        DevBuf runs(sizeof(int2) * std::max(d.ndense, 1), c.stream);
+        launch(c, k_dense_slot, dim3(grid_for(c, nkt, 256)), dim3(256), 0, nkt, (const int*)flag.as<int>(),
+               (const int*)pre.as<int>(), d.dslot.as<int>(), runs.as<int2>(), T);
+        const int W = 1 << (TL - 5);
+        d.dbm.reset(sizeof(unsigned) * size_t(W) * std::max(d.ndense, 1), c.stream);
+        if (d.ndense > 0) {
+            auto k = k_dense_build<256>;
+            ensure_smem(k, sizeof(unsigned) * W);
+            launch(c, k, dim3(d.ndense), dim3(256), sizeof(unsigned) * W, A, (const int32_t*)d.atp.as<int32_t>(), T,
+                   TL, (const int2*)runs.as<int2>(), d.dbm.as<unsigned>());
+        }
+    }
     d.atp_key = A.cp;
     d.atp_ncols = A.ncols;
     d.atp_nnz = A.nnz;
@@ -901,20 +1057,31 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
         d.hoff.reset(sizeof(int64_t) * ni1, c.stream);
         SLAPCU_CUDA(cudaMemsetAsync(d.cnt.as<int64_t>() + nitems, 0, sizeof(int64_t), c.stream));
         KScope ks2(c, KC_SYM_HEAVY);
-        FormArgs g{A, B, Atp, T, TL, (const int2*)d.items.as<int2>(), (const int4*)d.units.as<int4>(),
+        const DenseRuns dr{d.ndense > 0 ? (const int*)d.dslot.as<int>() : nullptr,
+                           (const unsigned*)d.dbm.as<unsigned>(), d.ndense > 0 ? d.dense_min : 0};
+        FormArgs g{A, B, Atp, dr, T, TL, (const int2*)d.items.as<int2>(), (const int4*)d.units.as<int4>(),
                    (const int*)d.order.as<int>(), d.stash.as<unsigned>(), (const int64_t*)d.soff.as<int64_t>(),
                    (const int64_t*)d.sres.as<int64_t>(), d.partial.as<unsigned>(), d.cnt.as<int64_t>(),
-                   d.form.as<int>(), d.hcnt.as<unsigned long long>()};
-        const size_t smem = sizeof(unsigned) * W + sizeof(int) * (W / 32 + 1);
+                   d.form.as<int>(), d.hcnt.as<unsigned long long>(), nullptr, 0,
+                   (int)std::min<int64_t>(c.opt.direct_sparse_run_max, INT32_MAX)};
+        const size_t smem = sizeof(unsigned) * (W + W / 32) + sizeof(uint16_t) * W;
+        DevBuf tick(sizeof(int), c.stream);
+        SLAPCU_CUDA(cudaMemsetAsync(tick.get(), 0, sizeof(int), c.stream));
+        g.ticket = tick.as<int>();
+        g.nunits = (int)nunits;
         auto form = [&](auto kf, int nt) {
             ensure_smem(kf, smem);
-            launch(c, kf, dim3((unsigned)nunits), dim3(nt), smem, g);
+            int per_sm = 0;
+            SLAPCU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kf, nt, smem));
+            const int64_t grid = c.opt.direct_persistent ? std::max<int64_t>(1, std::min<int64_t>(nunits, int64_t(per_sm) * c.num_sms))
+                                                         : nunits;
+            launch(c, kf, dim3((unsigned)grid), dim3(nt), smem, g);
         };
         const int ft = c.opt.direct_form_threads;
-        if (c.opt.direct_mark_mode == 2)
+        if (c.opt.direct_mark_mode == 3)
+            form(k_tile_form<256, 3>, 256);
+        else if (c.opt.direct_mark_mode == 2)
             form(k_tile_form<256, 2>, 256);
-        else if (c.opt.direct_mark_mode == 1)
-            form(k_tile_form<256, 1>, 256);
         else if (ft == 128)
             form(k_tile_form<128, 0>, 128);
         else if (ft == 512)

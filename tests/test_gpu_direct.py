@@ -32,12 +32,14 @@ def _ones(m):
 
 @pytest.mark.parametrize("tile_log2", [10, 12, 17])
 @pytest.mark.parametrize("split", [1024, 5000, 262144])
-def test_direct_bool_tiles_and_splits(port, tile_log2, split):
+@pytest.mark.parametrize("dense_run", [0, 16, 2048])
+def test_direct_bool_tiles_and_splits(port, tile_log2, split, dense_run):
     a = _ones(port.gen_rmat(12))
     want = port.spgemm(oracle.OR_AND_U8, a, a)
     ctx = P.Context()
     ctx.set_option(L.OPT_DIRECT_TILE_ROWS_LOG2, tile_log2)
     ctx.set_option(L.OPT_DIRECT_SPLIT_FLOPS, split)
+    ctx.set_option(L.OPT_DIRECT_DENSE_RUN_MIN, dense_run)
     da = to_device(a)
     for alg in (P.SpGemmAlg.heap, P.SpGemmAlg.hybrid):
         got = P.local_spgemm(da, da, P.OrAnd, alg, ctx=ctx, method="direct")
