@@ -44,6 +44,19 @@ constexpr int kUnit = 256;     // products per warp work unit on long runs
 
 __host__ __device__ __forceinline__ int64_t lmin(int64_t a, int64_t b) { return a < b ? a : b; }
 
+constexpr int kEmitWPL = 4;                    // stash words per lane in a warp block
+constexpr int kEmitBlock = 32 * kEmitWPL;      // words per warp block
+constexpr int kEmitStage = 1024;               // entries per staging round
+constexpr int kMaxBlocks = 128;                // W / kEmitBlock for row tiles up to 2^19
+
+// Every item's stash starts with a header of per-block output counts (one
+// int per kEmitBlock words of the stash body), so the emitter needs no
+// counting pass; padded to 16 bytes.
+__host__ __device__ __forceinline__ int stash_header_words(int W) {
+    const int nb = (W + kEmitBlock - 1) / kEmitBlock;
+    return (nb + 3) & ~3;
+}
+
 // Exclusive block-wide scan of one int per thread; *total gets the sum.
 template <int NT>
 __device__ __forceinline__ int block_excl_scan(int v, int* wsum, int* total) {
@@ -288,8 +301,8 @@ struct FormArgs {
 // (W/32 words); tl is shared scratch for W word indices.
 template <int NT>
 __device__ __forceinline__ void stash_bitmap(unsigned* bm, unsigned* summ, uint16_t* tl, int W, int* wsum, int* red,
-                                             int64_t item, int j, unsigned* stash, int64_t sres, int64_t* cnt,
-                                             int* form, unsigned long long* hcnt) {
+                                             int* bcs, int64_t item, int j, unsigned* stash, int64_t sres,
+                                             int64_t* cnt, int* form, unsigned long long* hcnt) {
     constexpr int NW = NT / 32;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int WS = W >> 5;
@@ -306,32 +319,55 @@ __device__ __forceinline__ void stash_bitmap(unsigned* bm, unsigned* summ, uint1
         sw &= sw - 1u;
     }
     __syncthreads();
+    const int HB = stash_header_words(W);
     const int64_t lw = int64_t(U) + (U + 1) / 2;  // words + 16-bit word indices
-    const bool list = lw < W && lw <= sres;
+    const bool list = lw < W && lw <= sres - HB;
+    unsigned* body = stash + HB;
     int myc = 0;
     if (list) {
-        uint16_t* idx = reinterpret_cast<uint16_t*>(stash + U);
-        for (int q = tid; q < U; q += NT) {
-            const int w = tl[q];
-            const unsigned x = bm[w];
-            bm[w] = 0u;
-            stash[q] = x;
-            idx[q] = (uint16_t)w;
-            myc += __popc(x);
+        // a warp covers 32 consecutive list positions: one warp sum per group
+        uint16_t* idx = reinterpret_cast<uint16_t*>(body + U);
+        for (int q0 = 0; q0 < U; q0 += NT) {
+            const int q = q0 + tid;
+            int c = 0;
+            if (q < U) {
+                const int w = tl[q];
+                const unsigned x = bm[w];
+                bm[w] = 0u;
+                body[q] = x;
+                idx[q] = (uint16_t)w;
+                c = __popc(x);
+            }
+            myc += c;
+            c = warp_reduce_sum(c);
+            if (lane == 0 && c) atomicAdd(&bcs[(q0 + warp * 32) / kEmitBlock], c);
         }
     } else {
-        uint4* d4 = reinterpret_cast<uint4*>(stash);
+        // a warp covers 32 consecutive uint4 = one block of 128 words
+        uint4* d4 = reinterpret_cast<uint4*>(body);
         uint4* s4 = reinterpret_cast<uint4*>(bm);
-        for (int q = tid; q < W / 4; q += NT) {
-            const uint4 x = s4[q];
-            d4[q] = x;
-            s4[q] = make_uint4(0u, 0u, 0u, 0u);
-            myc += __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
+        for (int q0 = 0; q0 < W / 4; q0 += NT) {
+            const int q = q0 + tid;
+            int c = 0;
+            if (q < W / 4) {
+                const uint4 x = s4[q];
+                d4[q] = x;
+                s4[q] = make_uint4(0u, 0u, 0u, 0u);
+                c = __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
+            }
+            myc += c;
+            c = warp_reduce_sum(c);
+            if (lane == 0 && c) atomicAdd(&bcs[((q0 + warp * 32) * 4) / kEmitBlock], c);
         }
     }
     myc = warp_reduce_sum(myc);
     if (lane == 0) red[warp] = myc;
     __syncthreads();
+    const int nb = ((list ? U : W) + kEmitBlock - 1) / kEmitBlock;
+    for (int b = tid; b < nb; b += NT) {
+        stash[b] = (unsigned)bcs[b];
+        bcs[b] = 0;
+    }
     if (tid == 0) {
         long long c = 0;
         for (int w = 0; w < NW; ++w) c += red[w];
@@ -352,7 +388,9 @@ __global__ void __launch_bounds__(NT) k_tile_form(FormArgs g) {
     __shared__ WalkSm<NT> sh;
     __shared__ int red[NT / 32];
     __shared__ int ticket_sh;
+    __shared__ int bcs[kMaxBlocks];
     smem_zero(bm, W + W / 32);
+    for (int b = threadIdx.x; b < kMaxBlocks; b += NT) bcs[b] = 0;
     for (;;) {
         if (threadIdx.x == 0) {
             ticket_sh = atomicAdd(g.ticket, 1);
@@ -383,7 +421,7 @@ __global__ void __launch_bounds__(NT) k_tile_form(FormArgs g) {
             }
             for (int q = threadIdx.x; q < W / 32; q += NT) summ[q] = 0u;
         } else {
-            stash_bitmap<NT>(bm, summ, tl, W, sh.wsum, red, u.x, it.x, g.stash + g.soff[u.x], g.sres[u.x], g.cnt,
+            stash_bitmap<NT>(bm, summ, tl, W, sh.wsum, red, bcs, u.x, it.x, g.stash + g.soff[u.x], g.sres[u.x], g.cnt,
                              g.form, g.hcnt);
         }
         __syncthreads();
@@ -405,6 +443,8 @@ __global__ void __launch_bounds__(NT)
     uint16_t* tl = reinterpret_cast<uint16_t*>(summ + W / 32);
     __shared__ int red[NW];
     __shared__ int wsum[NW + 1];
+    __shared__ int bcs[kMaxBlocks];
+    for (int b = threadIdx.x; b < kMaxBlocks; b += NT) bcs[b] = 0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int item = sitems[blockIdx.x];
     const int np = snp[blockIdx.x];
@@ -418,7 +458,7 @@ __global__ void __launch_bounds__(NT)
         if (lane == 0) summ[cc] = nz;
     }
     __syncthreads();
-    stash_bitmap<NT>(bm, summ, tl, W, wsum, red, item, items[item].x, stash + soff[item], sres[item], cnt, form,
+    stash_bitmap<NT>(bm, summ, tl, W, wsum, red, bcs, item, items[item].x, stash + soff[item], sres[item], cnt, form,
                      hcnt);
 }
 
@@ -437,31 +477,28 @@ struct EmitArgs {
     uint8_t* cv;
 };
 
-constexpr int kEmitWPL = 4;                    // stash words per lane in a warp block
-constexpr int kEmitBlock = 32 * kEmitWPL;      // words per warp block
-constexpr int kEmitStage = 1024;               // entries per staging round
-
 // Per-warp shared state of the emission.
 struct EmitWarp {
-    unsigned w[kEmitBlock];             // the block's non-zero words, compacted in order
-    int rb[kEmitBlock];                 // their row bases
-    int stage[kEmitStage + kEmitStage / 32];  // one pad word per 32 entries (conflict-free)
+    uint2 wr[kEmitBlock];         // the block's non-zero words (x) and their row bases (y), in order
+    int stage[kEmitStage + 8];    // one round of outputs, co-aligned with the destination
 };
 
 // Rows of one warp block written to out[0, E) in order.  Lane l's non-zero
-// words are ws->w[pos, pos + nzc) holding cnt set bits.  Outputs go in
-// rounds of kEmitStage: lane l produces a contiguous 1/32 of the round (one
-// search for its first word and bit, then it walks bits serially) into a
-// padded shared stage, then the round is stored coalesced.
+// words are ws->wr[pos, pos + nz) holding cnt set bits.  Outputs go in
+// rounds of kEmitStage: lane l produces a contiguous run of `per` outputs
+// (per odd, so the lanes' stage writes hit distinct banks) -- one search for
+// its first word and bit, then it walks bits serially -- into a stage
+// co-aligned with `out`, then the round is stored with 16-byte stores.
 __device__ __forceinline__ void emit_block(EmitWarp* ws, int pos, int cnt, int E, int32_t* __restrict__ out,
                                            int lane) {
     int all;
     const int ex = warp_excl_scan(cnt, lane, &all);
+    const int shift = (int)((reinterpret_cast<uintptr_t>(out) >> 2) & 3);
     for (int R0 = 0; R0 < E; R0 += kEmitStage) {
         const int RE = min(kEmitStage, E - R0);
-        const int per = (RE + 31) >> 5;
+        const int per = ((RE + 31) >> 5) | 1;
         const int my0 = R0 + min(lane * per, RE), my1 = R0 + min(lane * per + per, RE);
-        // owner lane of output my0: the largest l with ex_l <= my0 and cnt_l > 0
+        // owner lane of output my0: the largest l with ex_l <= my0
         int src = 0;
 #pragma unroll
         for (int step = 16; step > 0; step >>= 1) {
@@ -474,28 +511,38 @@ __device__ __forceinline__ void emit_block(EmitWarp* ws, int pos, int cnt, int E
         if (my0 < my1) {
             int k = my0 - exs;
             int wi = poss;
-            unsigned w = ws->w[wi];
+            uint2 cur = ws->wr[wi];
             for (;;) {  // word of the owner lane holding output my0 (all words non-zero)
-                const int c = __popc(w);
+                const int c = __popc(cur.x);
                 if (k < c) break;
                 k -= c;
-                w = ws->w[++wi];
+                cur = ws->wr[++wi];
             }
+            unsigned w = cur.x;
             if (k) w &= ~((1u << nth_set_bit(w, k)) - 1u);  // drop the k lowest set bits
-            int rb = ws->rb[wi];
-            for (int o = my0 - R0; o < my1 - R0; ++o) {
+            int rb = (int)cur.y;
+            int* st = ws->stage + shift - R0;
+            for (int o = my0; o < my1; ++o) {
                 if (w == 0u) {
-                    ++wi;
-                    w = ws->w[wi];
-                    rb = ws->rb[wi];
+                    cur = ws->wr[++wi];
+                    w = cur.x;
+                    rb = (int)cur.y;
                 }
-                ws->stage[o + (o >> 5)] = rb + (__ffs(w) - 1);
+                st[o] = rb + (__ffs(w) - 1);
                 w &= w - 1u;
             }
         }
         __syncwarp();
+        // stage[shift + i] -> out[R0 + i]; both 16-byte aligned where (shift + i) % 4 == 0
         int32_t* dst = out + R0;
-        for (int i = lane; i < RE; i += 32) dst[i] = ws->stage[i + (i >> 5)];
+        const int h = min(RE, (4 - shift) & 3);
+        if (lane < h) dst[lane] = ws->stage[shift + lane];
+        const int nb = (RE - h) >> 2;
+        const uint4* s4 = reinterpret_cast<const uint4*>(ws->stage + shift + h);
+        uint4* d4 = reinterpret_cast<uint4*>(dst + h);
+        for (int q = lane; q < nb; q += 32) d4[q] = s4[q];
+        const int tl = h + (nb << 2);
+        if (tl + lane < RE) dst[tl + lane] = ws->stage[shift + tl + lane];
         __syncwarp();
     }
 }
@@ -503,7 +550,6 @@ __device__ __forceinline__ void emit_block(EmitWarp* ws, int pos, int cnt, int E
 template <int NT>
 __global__ void __launch_bounds__(NT) k_tile_emit(EmitArgs g) {
     constexpr int NW = NT / 32;
-    extern __shared__ int blk[];  // [W/128 + 2] block counts -> bases
     __shared__ EmitWarp wsm[NW];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int item = blockIdx.x;
@@ -513,61 +559,46 @@ __global__ void __launch_bounds__(NT) k_tile_emit(EmitArgs g) {
     const int U = g.form[item];
     const int W = 1 << (g.TL - 5);
     const int nwords = U >= 0 ? U : W;
-    const unsigned* words = g.stash + g.soff[item];
+    const unsigned* hdr = g.stash + g.soff[item];
+    const unsigned* words = hdr + stash_header_words(W);
     const uint16_t* idx = U >= 0 ? reinterpret_cast<const uint16_t*>(words + U) : nullptr;
     const int nblk = (nwords + kEmitBlock - 1) / kEmitBlock;
     const int t0 = it.y << g.TL;
-    for (int b = warp; b < nblk; b += NW) {
-        int x = 0;
-#pragma unroll
-        for (int q = 0; q < kEmitWPL; ++q) {
-            const int w = b * kEmitBlock + q * 32 + lane;
-            x += w < nwords ? __popc(words[w]) : 0;
-        }
-        x = warp_reduce_sum(x);
-        if (lane == 0) blk[b] = x;
-    }
-    __syncthreads();
-    if (warp == 0) {
-        int run = 0;
-        for (int b0 = 0; b0 < nblk; b0 += 32) {
-            const int cix = b0 + lane;
-            const int x = cix < nblk ? blk[cix] : 0;
-            int tt;
-            const int e = warp_excl_scan(x, lane, &tt);
-            if (cix < nblk) blk[cix] = run + e;
-            run += tt;
-        }
-        if (lane == 0) blk[nblk] = run;
-    }
-    __syncthreads();
     EmitWarp* ws = &wsm[warp];
-    for (int b = warp; b < nblk; b += NW) {
-        const int E = blk[b + 1] - blk[b];
-        if (!E) continue;
-        unsigned xs[kEmitWPL];
-        int cnt = 0, nz = 0;
+    int run = 0;
+    for (int c0 = 0; c0 < nblk; c0 += 32) {  // header chunks of 32 block counts (warp-level scan)
+        const int v = c0 + lane < nblk ? (int)hdr[c0 + lane] : 0;
+        int tot;
+        const int ex = warp_excl_scan(v, lane, &tot);
+        const int cend = min(c0 + 32, nblk);
+        for (int b = c0 + warp; b < cend; b += NW) {
+            const int E = __shfl_sync(0xffffffffu, v, b - c0);
+            const int bbase = run + __shfl_sync(0xffffffffu, ex, b - c0);
+            if (!E) continue;
+            unsigned xs[kEmitWPL];
+            int cnt = 0, nz = 0;
 #pragma unroll
-        for (int q = 0; q < kEmitWPL; ++q) {
-            const int w = b * kEmitBlock + lane * kEmitWPL + q;
-            xs[q] = w < nwords ? words[w] : 0u;
-            cnt += __popc(xs[q]);
-            nz += xs[q] != 0u;
-        }
-        int nzt;
-        const int pos = warp_excl_scan(nz, lane, &nzt);
-        int p = pos;
-#pragma unroll
-        for (int q = 0; q < kEmitWPL; ++q) {
-            if (xs[q]) {
+            for (int q = 0; q < kEmitWPL; ++q) {
                 const int w = b * kEmitBlock + lane * kEmitWPL + q;
-                ws->w[p] = xs[q];
-                ws->rb[p] = t0 + ((idx ? (int)idx[w] : w) << 5);
-                ++p;
+                xs[q] = w < nwords ? words[w] : 0u;
+                cnt += __popc(xs[q]);
+                nz += xs[q] != 0u;
             }
+            int nzt;
+            const int pos = warp_excl_scan(nz, lane, &nzt);
+            int p = pos;
+#pragma unroll
+            for (int q = 0; q < kEmitWPL; ++q) {
+                if (xs[q]) {
+                    const int w = b * kEmitBlock + lane * kEmitWPL + q;
+                    ws->wr[p] = make_uint2(xs[q], (unsigned)(t0 + ((idx ? (int)idx[w] : w) << 5)));
+                    ++p;
+                }
+            }
+            __syncwarp();
+            emit_block(ws, pos, cnt, E, g.crw + off + bbase, lane);
         }
-        __syncwarp();
-        emit_block(ws, pos, cnt, E, g.crw + off + blk[b], lane);
+        run += tot;
     }
     if (g.cv) {
         // values: c bytes of 1 (head bytes, 16-byte body, tail bytes)
@@ -711,7 +742,8 @@ __global__ void k_item_fill(const int* __restrict__ hl, int nh, int T, int W, co
             np[o] = p;
             pslots[o] = p > 1 ? p : 0;
             // 4-word multiples keep every stash 16-byte aligned (bitmap copies are uint4)
-            sres[o] = p > 1 ? W : (lmin(W, (3 * lmin(f, W) + 1) / 2 + 1) + 3) & ~int64_t(3);
+            sres[o] = stash_header_words(W) +
+                      (p > 1 ? W : (lmin(W, (3 * lmin(f, W) + 1) / 2 + 1) + 3) & ~int64_t(3));
             ++o;
         }
     }
@@ -1119,7 +1151,7 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
                    (const unsigned*)d.stash.as<unsigned>(), (const int64_t*)d.soff.as<int64_t>(),
                    (const int64_t*)d.hoff.as<int64_t>(), (const int64_t*)d.lp.as<int64_t>(), TL, crw,
                    static_cast<uint8_t*>(cv)};
-        const size_t smem = sizeof(int) * (W / kEmitBlock + 2);
+        const size_t smem = 0;
         auto emit = [&](auto ke, int nt) {
             ensure_smem(ke, smem);
             launch(c, ke, dim3(nitems), dim3(nt), smem, e);
