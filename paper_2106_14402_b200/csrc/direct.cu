@@ -47,7 +47,7 @@ __host__ __device__ __forceinline__ int64_t lmin(int64_t a, int64_t b) { return 
 constexpr int kEmitWPL = 4;                    // stash words per lane in a warp block
 constexpr int kEmitBlock = 32 * kEmitWPL;      // words per warp block
 constexpr int kEmitStage = 1024;               // entries per staging round
-constexpr int kMaxBlocks = 128;                // W / kEmitBlock for row tiles up to 2^19
+constexpr int kMaxBlocks = 128;                // W / kEmitBlock for row tiles up to 2^19 (emit holds 4 x 32)
 
 // Every item's stash starts with a header of per-block output counts (one
 // int per kEmitBlock words of the stash body), so the emitter needs no
@@ -565,22 +565,42 @@ __global__ void __launch_bounds__(NT) k_tile_emit(EmitArgs g) {
     const int nblk = (nwords + kEmitBlock - 1) / kEmitBlock;
     const int t0 = it.y << g.TL;
     EmitWarp* ws = &wsm[warp];
+    // block counts -> exclusive block bases, held as 4 registers per lane
+    // (block b at lane b % 32, register b / 32; up to 128 blocks)
+    int hv[4], hb[4];
     int run = 0;
-    for (int c0 = 0; c0 < nblk; c0 += 32) {  // header chunks of 32 block counts (warp-level scan)
-        const int v = c0 + lane < nblk ? (int)hdr[c0 + lane] : 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int bi = k * 32 + lane;
+        hv[k] = bi < nblk ? (int)hdr[bi] : 0;
         int tot;
-        const int ex = warp_excl_scan(v, lane, &tot);
-        const int cend = min(c0 + 32, nblk);
-        for (int b = c0 + warp; b < cend; b += NW) {
-            const int E = __shfl_sync(0xffffffffu, v, b - c0);
-            const int bbase = run + __shfl_sync(0xffffffffu, ex, b - c0);
-            if (!E) continue;
-            unsigned xs[kEmitWPL];
+        hb[k] = run + warp_excl_scan(hv[k], lane, &tot);
+        run += tot;
+    }
+    auto sel = [](const int (&r)[4], int k) { return k == 0 ? r[0] : k == 1 ? r[1] : k == 2 ? r[2] : r[3]; };
+    // words of block b (4 per lane), prefetched one block ahead
+    auto load = [&](int b, unsigned (&xs)[kEmitWPL], int (&wi)[kEmitWPL]) {
+#pragma unroll
+        for (int q = 0; q < kEmitWPL; ++q) {
+            const int w = b * kEmitBlock + lane * kEmitWPL + q;
+            const bool ok = b < nblk && w < nwords;
+            xs[q] = ok ? words[w] : 0u;
+            wi[q] = ok ? (idx ? (int)idx[w] : w) : 0;
+        }
+    };
+    unsigned xs[kEmitWPL];
+    int wi[kEmitWPL];
+    load(warp, xs, wi);
+    for (int b = warp; b < nblk; b += NW) {
+        unsigned xn[kEmitWPL];
+        int wn[kEmitWPL];
+        load(b + NW, xn, wn);
+        const int E = __shfl_sync(0xffffffffu, sel(hv, b >> 5), b & 31);
+        const int bbase = __shfl_sync(0xffffffffu, sel(hb, b >> 5), b & 31);
+        if (E) {
             int cnt = 0, nz = 0;
 #pragma unroll
             for (int q = 0; q < kEmitWPL; ++q) {
-                const int w = b * kEmitBlock + lane * kEmitWPL + q;
-                xs[q] = w < nwords ? words[w] : 0u;
                 cnt += __popc(xs[q]);
                 nz += xs[q] != 0u;
             }
@@ -590,15 +610,18 @@ __global__ void __launch_bounds__(NT) k_tile_emit(EmitArgs g) {
 #pragma unroll
             for (int q = 0; q < kEmitWPL; ++q) {
                 if (xs[q]) {
-                    const int w = b * kEmitBlock + lane * kEmitWPL + q;
-                    ws->wr[p] = make_uint2(xs[q], (unsigned)(t0 + ((idx ? (int)idx[w] : w) << 5)));
+                    ws->wr[p] = make_uint2(xs[q], (unsigned)(t0 + (wi[q] << 5)));
                     ++p;
                 }
             }
             __syncwarp();
             emit_block(ws, pos, cnt, E, g.crw + off + bbase, lane);
         }
-        run += tot;
+#pragma unroll
+        for (int q = 0; q < kEmitWPL; ++q) {
+            xs[q] = xn[q];
+            wi[q] = wn[q];
+        }
     }
     if (g.cv) {
         // values: c bytes of 1 (head bytes, 16-byte body, tail bytes)
