@@ -67,7 +67,7 @@ def parse():
     ap.add_argument("--emit-threads", type=int, default=None, help="direct path emit CTA size")
     ap.add_argument("--dense-run", type=int, default=None, help="direct path dense A-run threshold (0 off)")
     ap.add_argument("--persistent", type=int, default=None, help="direct path form kernel persistent (1) or not (0)")
-    ap.add_argument("--sparse-run", type=int, default=None, help="direct path: runs shorter than this skip the test")
+    ap.add_argument("--quads", type=int, default=None, help="direct path: lane-contiguous quads (1) or strided (0)")
     ap.add_argument("--streams", type=int, default=1, choices=[1, 2],
                     help="2: alternate column batches over two contexts/streams (async finish)")
     return ap.parse_args()
@@ -96,8 +96,8 @@ def apply_options(ctx, args):
         ctx.set_option(L.OPT_DIRECT_DENSE_RUN_MIN, args.dense_run)
     if args.persistent is not None:
         ctx.set_option(L.OPT_DIRECT_PERSISTENT, args.persistent)
-    if args.sparse_run is not None:
-        ctx.set_option(L.OPT_DIRECT_SPARSE_RUN_MAX, args.sparse_run)
+    if args.quads is not None:
+        ctx.set_option(L.OPT_DIRECT_QUADS, args.quads)
 
 
 # ------------------------------------------------------------------ helpers

@@ -126,8 +126,9 @@ typedef enum {
                                               (default 2048, 0 = never) */
     SLAPCU_OPT_DIRECT_PERSISTENT = 15,     /* direct path form kernel: 1 persistent CTAs taking units by
                                               ticket, 0 one CTA per unit */
-    SLAPCU_OPT_DIRECT_SPARSE_RUN_MAX = 16  /* direct path: A runs shorter than this update the bitmap
-                                              without the test load (default 0 = never) */
+    SLAPCU_OPT_DIRECT_QUADS = 16           /* direct path: 1 = each lane takes 4 consecutive entries of a
+                                              run (16-byte loads) and merges rows sharing a word before
+                                              the shared-memory update */
 } slapcu_option;
 slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t value);
 

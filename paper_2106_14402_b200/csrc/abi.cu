@@ -147,10 +147,7 @@ slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t v
             c.opt.direct_mark_mode = (int)v;
             break;
         case SLAPCU_OPT_DIRECT_PERSISTENT: c.opt.direct_persistent = v != 0; break;
-        case SLAPCU_OPT_DIRECT_SPARSE_RUN_MAX:
-            require(v >= 0, SLAPCU_ERR_INVALID, "sparse run threshold must be >= 0");
-            c.opt.direct_sparse_run_max = v;
-            break;
+        case SLAPCU_OPT_DIRECT_QUADS: c.opt.direct_quads = v != 0; break;
         case SLAPCU_OPT_DIRECT_FORM_THREADS:
             require(v == 128 || v == 256 || v == 512, SLAPCU_ERR_INVALID, "form threads: 128, 256 or 512");
             c.opt.direct_form_threads = (int)v;

@@ -126,7 +126,7 @@ struct Options {
     int64_t direct_dense_run_min = 2048;    // direct path: A runs (column x tile) this long are OR-ed
                                             // as precomputed tile bitmaps (0 = never)
     int direct_mark_mode = 0;               // product update: 0 test+set, 1 atomic only, 2 quad-merged
-    int64_t direct_sparse_run_max = 0;      // direct path: runs shorter than this update without a test
+    int direct_quads = 0;                   // direct path: lane-contiguous quads merged per word
     int direct_persistent = 1;              // form kernel: persistent CTAs (1) or one CTA per unit (0)
     int direct_form_threads = 256;          // CTA size of the form kernel (128, 256, 512)
     int direct_emit_threads = 128;          // CTA size of the emit kernel (128, 256)

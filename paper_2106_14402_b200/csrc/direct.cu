@@ -154,7 +154,7 @@ __device__ __forceinline__ void mark(unsigned bmA, unsigned sumA, int rr) {
 template <int NT, int U, int MODE>
 __device__ __forceinline__ void tile_walk(const DevCsc& A, const DevCsc& B, const int32_t* __restrict__ Atp, int T,
                                           int64_t b0, int64_t b1, int t, int t0, unsigned* bm, unsigned* summ,
-                                          WalkSm<NT>& sh, const DenseRuns& dr, int W, int sparse_max) {
+                                          WalkSm<NT>& sh, const DenseRuns& dr, int W, int quads) {
     constexpr int NW = NT / 32;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int32_t* __restrict__ Arw = A.rw;
@@ -228,17 +228,31 @@ __device__ __forceinline__ void tile_walk(const DevCsc& A, const DevCsc& B, cons
             const int32_t* run = Arw + sh.start[e] + c0;
             const int m = min(kUnit, sh.len[e] - c0);
             int x = lane;
-            if (sparse_max && sh.len[e] < sparse_max) {
-                // sparse run: consecutive entries fall in different words and
-                // their bits are mostly unset -- skip the test load
-                for (; x + 32 * (U - 1) < m; x += 32 * U) {
-                    int r[U];
-#pragma unroll
-                    for (int v = 0; v < U; ++v) r[v] = __ldg(run + x + 32 * v);
-#pragma unroll
-                    for (int v = 0; v < U; ++v) mark<1>(bmA, sumA, r[v]);
+            if (quads) {
+                // lane-contiguous quads (16-byte loads from the aligned-down
+                // unit start): rows of a quad that share a word are OR-ed in
+                // registers, so a dense run touches shared memory once per
+                // word run instead of once per product (branch-free heads)
+                const int mis = (int)((reinterpret_cast<uintptr_t>(run) >> 2) & 3);
+                const int4* q4 = reinterpret_cast<const int4*>(run - mis);
+                const int total = m + mis;
+                for (int y = 4 * lane; y < total; y += 128) {
+                    const int4 q = __ldg(q4 + (y >> 2));
+                    const int p0 = y - mis;
+                    const bool v0 = p0 >= 0 && p0 < m, v1 = p0 + 1 >= 0 && p0 + 1 < m;
+                    const bool v2 = p0 + 2 >= 0 && p0 + 2 < m, v3 = p0 + 3 < m;
+                    const int w0 = q.x >> 5, w1 = q.y >> 5, w2 = q.z >> 5, w3 = q.w >> 5;
+                    const bool m1 = v0 && v1 && w1 == w0, m2 = v1 && v2 && w2 == w1, m3 = v2 && v3 && w3 == w2;
+                    const unsigned b3 = 1u << (q.w & 31);
+                    const unsigned a3 = b3;
+                    const unsigned a2 = (1u << (q.z & 31)) | (m3 ? a3 : 0u);
+                    const unsigned a1 = (1u << (q.y & 31)) | (m2 ? a2 : 0u);
+                    const unsigned a0 = (1u << (q.x & 31)) | (m1 ? a1 : 0u);
+                    if (v0) set_bits<MODE>(bmA + (unsigned(w0) << 2), a0, sumA + (unsigned(q.x >> 10) << 2), 1u << (w0 & 31));
+                    if (v1 && !m1) set_bits<MODE>(bmA + (unsigned(w1) << 2), a1, sumA + (unsigned(q.y >> 10) << 2), 1u << (w1 & 31));
+                    if (v2 && !m2) set_bits<MODE>(bmA + (unsigned(w2) << 2), a2, sumA + (unsigned(q.z >> 10) << 2), 1u << (w2 & 31));
+                    if (v3 && !m3) set_bits<MODE>(bmA + (unsigned(w3) << 2), a3, sumA + (unsigned(q.w >> 10) << 2), 1u << (w3 & 31));
                 }
-                for (; x < m; x += 32) mark<1>(bmA, sumA, __ldg(run + x));
                 continue;
             }
             for (; x + 32 * (U - 1) < m; x += 32 * U) {
@@ -293,7 +307,7 @@ struct FormArgs {
     unsigned long long* hcnt;  // output entries per column (heavy part)
     int* ticket;
     int nunits;
-    int sparse_max;  // runs shorter than this skip the test-before-set (0 = never)
+    int quads;  // 1: lane-contiguous quads merged per word before the shared update
 };
 
 // Count, choose the stash form and write it, then clear the bitmap (whole
@@ -403,7 +417,7 @@ __global__ void __launch_bounds__(NT) k_tile_form(FormArgs g) {
         const int4 u = g.units[g.order[ui]];
         const int2 it = g.items[u.x];
         const int64_t bs = g.B.cp[it.x];
-        tile_walk<NT, 4, MODE>(g.A, g.B, g.Atp, g.T, bs + u.y, bs + u.z, it.y, it.y << g.TL, bm, summ, sh, g.dr, W, g.sparse_max);
+        tile_walk<NT, 4, MODE>(g.A, g.B, g.Atp, g.T, bs + u.y, bs + u.z, it.y, it.y << g.TL, bm, summ, sh, g.dr, W, g.quads);
         if (MODE != 2 && u.w < 0) {  // summary by ballots over the bitmap
             const int lane = threadIdx.x & 31;
             for (int cc = threadIdx.x >> 5; cc < W / 32; cc += NT / 32) {
@@ -1118,7 +1132,7 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
                    (const int*)d.order.as<int>(), d.stash.as<unsigned>(), (const int64_t*)d.soff.as<int64_t>(),
                    (const int64_t*)d.sres.as<int64_t>(), d.partial.as<unsigned>(), d.cnt.as<int64_t>(),
                    d.form.as<int>(), d.hcnt.as<unsigned long long>(), nullptr, 0,
-                   (int)std::min<int64_t>(c.opt.direct_sparse_run_max, INT32_MAX)};
+                   c.opt.direct_quads};
         const size_t smem = sizeof(unsigned) * (W + W / 32) + sizeof(uint16_t) * W;
         DevBuf tick(sizeof(int), c.stream);
         SLAPCU_CUDA(cudaMemsetAsync(tick.get(), 0, sizeof(int), c.stream));
