@@ -68,6 +68,9 @@ def parse():
     ap.add_argument("--dense-run", type=int, default=None, help="direct path dense A-run threshold (0 off)")
     ap.add_argument("--persistent", type=int, default=None, help="direct path form kernel persistent (1) or not (0)")
     ap.add_argument("--quads", type=int, default=None, help="direct path: lane-contiguous quads (1) or strided (0)")
+    ap.add_argument("--dist", default="1d", choices=["1d", "summa"],
+                    help="N>1: 1d = flops-balanced column blocks with A replicated (no data-path collective); "
+                         "summa = the 2D SUMMA / 3D drivers (NCCL stage broadcasts, fiber exchange, merge)")
     ap.add_argument("--streams", type=int, default=1, choices=[1, 2],
                     help="2: alternate column batches over two contexts/streams (async finish)")
     return ap.parse_args()
@@ -183,6 +186,16 @@ def plan_batches(counts: np.ndarray, entry_bytes: int, budget: int):
     return ranges
 
 
+def flops_balanced_blocks(flops: np.ndarray, parts: int):
+    """Column boundaries [b_0 = 0, ..., b_parts = n] splitting the columns into
+    `parts` contiguous blocks of (nearly) equal multiplies."""
+    n = len(flops)
+    cum = np.cumsum(flops)
+    total = int(cum[-1]) if n else 0
+    inner = [int(np.searchsorted(cum, total * r / parts)) for r in range(1, parts)]
+    return [0] + [min(max(b, 0), n) for b in inner] + [n]
+
+
 def cpu_sample_offsets(n, w):
     # the survey's four slices (probe8: 0, n/4+12345, n/2+777, n-4096), width w
     return [0, min(n // 4 + 12345, n - w), min(n // 2 + 777, n - w), n - w]
@@ -214,6 +227,8 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if world > 1:
+        if args.dist == "1d":
+            return run_ours_1d(args, world, rank)
         return run_ours_dist(args, world, rank)
     torch.cuda.set_device(0)
     dev = torch.device("cuda", 0)
@@ -528,6 +543,162 @@ def dist_shape(world: int):
         if world % (q * q) == 0:
             return "ca3d", world // (q * q)
     return "ca3d", world
+
+
+def run_ours_1d(args, world, rank):
+    """N GPUs, one process each, C = A*A split by flops-balanced column
+    blocks: every rank holds A (the replicated operand of CombBLAS's in-node
+    GPU scheme) and forms C(:, J_rank) with the direct path in
+    column batches.  No collective on the data path; the time is the max over
+    ranks of CUDA-event time."""
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2106_14402_b200 as P
+    from paper_2106_14402_b200 import _lib as L
+
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.current_stream()
+    ctx = P.Context(local, stream)
+    apply_options(ctx, args)
+    lib = ctx.lib
+    sr = P.OrAnd if args.semiring == "or_and" else P.MinPlusI32
+    kind = 0 if sr is P.OrAnd else 3
+    vs = 1 if sr is P.OrAnd else 4
+    A = P.fill_values(P.gen_rmat(args.scale, args.edge_factor, 1, ctx=ctx), sr, kind, ctx=ctx)
+    n = A.ncols
+    total_flops, flops_per = P.estimate_flops(A, A, ctx=ctx)
+    fl = flops_per.cpu().numpy()
+    bnd = flops_balanced_blocks(fl, world)
+    c0, c1 = bnd[rank], bnd[rank + 1]
+    bound = np.minimum(fl[c0:c1], A.nrows)
+    free, _tot = torch.cuda.mem_get_info()
+    budget = int(args.budget_gb * 2**30) if args.budget_gb > 0 else int(min(0.15 * free, 24 * 2**30))
+    batches = [(s + c0, e + c0) for s, e in plan_batches(bound, 4, budget)] if c1 > c0 else []
+    max_cap = max([int(bound[s - c0:e - c0].sum()) for s, e in batches] + [1])
+    max_cols = max([e - s for s, e in batches] + [1])
+    o_cp = torch.empty(max_cols + 1, dtype=torch.int64, device=dev)
+    o_rw = torch.empty(max_cap, dtype=torch.int32, device=dev)
+    o_v = torch.empty(max_cap, dtype=sr.torch_dtype, device=dev)
+
+    def step(Ad, collect=None, d2h=None):
+        av = L.CscView(A.nrows, n, A.nnz, Ad[0].data_ptr(), Ad[1].data_ptr(), Ad[2].data_ptr())
+        for s, e in batches:
+            w = L.CscView(A.nrows, e - s, A.nnz, Ad[0].data_ptr() + 8 * s, Ad[1].data_ptr(), Ad[2].data_ptr())
+            nz = C.c_int64()
+            ctx.check(lib.slapcu_spgemm_direct(ctx.h, C.byref(av), C.byref(w), sr.id, P.SpGemmAlg.hybrid,
+                                               o_rw.numel(), o_cp.data_ptr(), o_rw.data_ptr(), o_v.data_ptr(),
+                                               C.byref(nz)), "direct")
+            if collect is not None:
+                collect.append(int(nz.value))
+            if d2h is not None:
+                d2h(e - s, int(nz.value))
+
+    Adev = (A.colptr, A.rowids, A.vals)
+    got = []
+    step(Adev, collect=got)
+    nnz_local = sum(got)
+    for _ in range(args.warmup - 1):
+        step(Adev)
+    torch.cuda.synchronize()
+    launches0 = ctx.launches
+    clocks = ClockSampler(local) if rank == 0 else None
+    if clocks:
+        clocks.start()
+    dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step(Adev)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk = clocks.stop() if clocks else None
+    ms_rank = ev0.elapsed_time(ev1) / args.steps
+    launches = (ctx.launches - launches0) // args.steps
+
+    # ---- e2e: A from pinned host memory, every output batch back to pinned host memory
+    e2e_ms, h2d, d2h_bytes = 0.0, 0, 0
+    if not args.no_e2e:
+        hA = [x.cpu().pin_memory() for x in Adev]
+        dA = [torch.empty_like(x) for x in Adev]
+        chunk = 1 << 28
+        h_rw = torch.empty(chunk, dtype=torch.int32).pin_memory()
+        h_v = torch.empty(chunk, dtype=sr.torch_dtype).pin_memory()
+        h_cp = torch.empty(max_cols + 1, dtype=torch.int64).pin_memory()
+        h2d = sum(x.numel() * x.element_size() for x in hA)
+        moved = [0]
+
+        def pull(ncols, nzv):
+            h_cp[:ncols + 1].copy_(o_cp[:ncols + 1], non_blocking=True)
+            moved[0] += (ncols + 1) * 8
+            for o in range(0, nzv, chunk):
+                m = min(chunk, nzv - o)
+                h_rw[:m].copy_(o_rw[o:o + m], non_blocking=True)
+                h_v[:m].copy_(o_v[o:o + m], non_blocking=True)
+                moved[0] += m * (4 + vs)
+
+        def e2e_step():
+            moved[0] = 0
+            for d, h in zip(dA, hA):
+                d.copy_(h, non_blocking=True)
+            step(dA, d2h=pull)
+            torch.cuda.current_stream().synchronize()
+
+        e2e_step()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(max(args.e2e_steps, 1)):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = e0.elapsed_time(e1) / max(args.e2e_steps, 1)
+        d2h_bytes = moved[0]
+        dist.barrier()
+    tm = torch.tensor([ms_rank, e2e_ms, float(nnz_local), float(h2d), float(d2h_bytes)], device=dev,
+                      dtype=torch.float64)
+    mx = tm.clone()
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    sm = tm.clone()
+    dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+    if rank == 0:
+        ms = float(mx[0])
+        nnz_c = int(sm[2])
+        peak, peak_kind = measured_peak_gbs()
+        step_bytes = bytes_alg(A.nnz, n, A.nnz, n, nnz_c, n, vs)
+        per_gpu = step_bytes / world / (ms / 1e3) / 1e9
+        line = {
+            "metric": METRIC, "value": round(2.0 * total_flops / (ms / 1e3) / 1e9, 3), "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": sr.dtype,
+            "data": "synthetic",
+            "config": {
+                "workload": f"C3: R-MAT scale {args.scale} ef {args.edge_factor} seed 1, C = A*A, {sr.name} {sr.dtype}",
+                "semiring": f"{sr.name}_{sr.dtype}", "n": n, "nnz_A": A.nnz, "multiplies": total_flops,
+                "nnz_C": nnz_c, "parallelism": f"1D column blocks x{world} (A replicated, flops-balanced)",
+                "column_blocks": bnd, "column_batches_rank0": len(batches),
+                "l2": "inputs/outputs larger than L2; no flush"},
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "roofline": {"bound": "hbm", "kernel": "whole local multiply per GPU", "achieved": round(per_gpu, 2),
+                         "peak": peak, "unit": "GB/s", "frac": round(per_gpu / peak, 5), "traffic": None,
+                         "peak_source": peak_kind, "algorithmic_bytes_per_step": step_bytes},
+            "e2e": None if args.no_e2e else {
+                "value": round(2.0 * total_flops / (float(mx[1]) / 1e3) / 1e9, 3), "unit": UNIT,
+                "h2d_bytes_per_step": int(sm[3]), "d2h_bytes_per_step": int(sm[4]),
+                "ms_per_step": round(float(mx[1]), 3), "steps": max(args.e2e_steps, 1)},
+            "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
 
 
 def run_ours_dist(args, world, rank):
