@@ -71,6 +71,9 @@ def parse():
     ap.add_argument("--dist", default="1d", choices=["1d", "summa"],
                     help="N>1: 1d = flops-balanced column blocks with A replicated (no data-path collective); "
                          "summa = the 2D SUMMA / 3D drivers (NCCL stage broadcasts, fiber exchange, merge)")
+    ap.add_argument("--balance-out", type=float, default=3.0, help="1d split: weight of a column's output bound")
+    ap.add_argument("--balance-col", type=float, default=2000.0, help="1d split: per-column weight")
+    ap.add_argument("--calibrate", type=int, default=1, help="1d split: timed re-balancing rounds before warmup")
     ap.add_argument("--streams", type=int, default=1, choices=[1, 2],
                     help="2: alternate column batches over two contexts/streams (async finish)")
     return ap.parse_args()
@@ -574,19 +577,33 @@ def run_ours_1d(args, world, rank):
     n = A.ncols
     total_flops, flops_per = P.estimate_flops(A, A, ctx=ctx)
     fl = flops_per.cpu().numpy()
-    bnd = flops_balanced_blocks(fl, world)
-    c0, c1 = bnd[rank], bnd[rank + 1]
-    bound = np.minimum(fl[c0:c1], A.nrows)
+    # balance multiplies plus output-proportional work (the bound on a
+    # column's entries) plus a per-column constant
+    weight = fl + args.balance_out * np.minimum(fl, A.nrows) + args.balance_col
+    bnd = flops_balanced_blocks(weight, world)
     free, _tot = torch.cuda.mem_get_info()
     budget = int(args.budget_gb * 2**30) if args.budget_gb > 0 else int(min(0.15 * free, 24 * 2**30))
-    batches = [(s + c0, e + c0) for s, e in plan_batches(bound, 4, budget)] if c1 > c0 else []
-    max_cap = max([int(bound[s - c0:e - c0].sum()) for s, e in batches] + [1])
-    max_cols = max([e - s for s, e in batches] + [1])
-    o_cp = torch.empty(max_cols + 1, dtype=torch.int64, device=dev)
-    o_rw = torch.empty(max_cap, dtype=torch.int32, device=dev)
-    o_v = torch.empty(max_cap, dtype=sr.torch_dtype, device=dev)
+    o_bufs = {}
+
+    def plan(bnd):
+        c0, c1 = bnd[rank], bnd[rank + 1]
+        bound = np.minimum(fl[c0:c1], A.nrows)
+        batches = [(s + c0, e + c0) for s, e in plan_batches(bound, 4, budget)] if c1 > c0 else []
+        max_cap = max([int(bound[s - c0:e - c0].sum()) for s, e in batches] + [1])
+        max_cols = max([e - s for s, e in batches] + [1])
+        if o_bufs.get("cap", 0) < max_cap or o_bufs.get("cols", 0) < max_cols:
+            o_bufs.clear()
+            torch.cuda.empty_cache()
+            o_bufs.update(cap=max_cap, cols=max_cols,
+                          cp=torch.empty(max_cols + 1, dtype=torch.int64, device=dev),
+                          rw=torch.empty(max_cap, dtype=torch.int32, device=dev),
+                          v=torch.empty(max_cap, dtype=sr.torch_dtype, device=dev))
+        return batches, max_cols
+
+    batches, max_cols = plan(bnd)
 
     def step(Ad, collect=None, d2h=None):
+        o_cp, o_rw, o_v = o_bufs["cp"], o_bufs["rw"], o_bufs["v"]
         av = L.CscView(A.nrows, n, A.nnz, Ad[0].data_ptr(), Ad[1].data_ptr(), Ad[2].data_ptr())
         for s, e in batches:
             w = L.CscView(A.nrows, e - s, A.nnz, Ad[0].data_ptr() + 8 * s, Ad[1].data_ptr(), Ad[2].data_ptr())
@@ -598,6 +615,30 @@ def run_ours_1d(args, world, rank):
                 collect.append(int(nz.value))
             if d2h is not None:
                 d2h(e - s, int(nz.value))
+
+    # one calibration step: scale each rank's weights by its measured time per
+    # unit weight and re-split (ranks differ in time per multiply: hub columns
+    # have dense outputs, the tail has many small columns)
+    Adev0 = (A.colptr, A.rowids, A.vals)
+    step(Adev0)
+    for _ in range(args.calibrate):
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step(Adev0)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
+        ts = [torch.zeros(1, device=dev, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(ts, t)
+        for r in range(world):
+            wr = weight[bnd[r]:bnd[r + 1]]
+            if wr.sum() > 0:
+                weight[bnd[r]:bnd[r + 1]] = wr * (float(ts[r].item()) / float(wr.sum()))
+        bnd = flops_balanced_blocks(weight, world)
+        batches, max_cols = plan(bnd)
+    o_cp, o_rw, o_v = o_bufs["cp"], o_bufs["rw"], o_bufs["v"]
 
     Adev = (A.colptr, A.rowids, A.vals)
     got = []
@@ -664,6 +705,8 @@ def run_ours_1d(args, world, rank):
         dist.barrier()
     tm = torch.tensor([ms_rank, e2e_ms, float(nnz_local), float(h2d), float(d2h_bytes)], device=dev,
                       dtype=torch.float64)
+    per_rank = [torch.zeros(1, device=dev, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(per_rank, tm[:1].clone())
     mx = tm.clone()
     dist.all_reduce(mx, op=dist.ReduceOp.MAX)
     sm = tm.clone()
@@ -684,6 +727,7 @@ def run_ours_1d(args, world, rank):
                 "semiring": f"{sr.name}_{sr.dtype}", "n": n, "nnz_A": A.nnz, "multiplies": total_flops,
                 "nnz_C": nnz_c, "parallelism": f"1D column blocks x{world} (A replicated, flops-balanced)",
                 "column_blocks": bnd, "column_batches_rank0": len(batches),
+                "rank_ms": [round(float(x.item()), 3) for x in per_rank],
                 "l2": "inputs/outputs larger than L2; no flush"},
             "gpu_launches": int(launches),
             "clocks": clk,
