@@ -126,9 +126,11 @@ typedef enum {
                                               (default 2048, 0 = never) */
     SLAPCU_OPT_DIRECT_PERSISTENT = 15,     /* direct path form kernel: 1 persistent CTAs taking units by
                                               ticket, 0 one CTA per unit */
-    SLAPCU_OPT_DIRECT_QUADS = 16           /* direct path: 1 = each lane takes 4 consecutive entries of a
+    SLAPCU_OPT_DIRECT_QUADS = 16,          /* direct path: 1 = each lane takes 4 consecutive entries of a
                                               run (16-byte loads) and merges rows sharing a word before
                                               the shared-memory update */
+    SLAPCU_OPT_DIRECT_VALUE_TILE_ROWS_LOG2 = 17 /* direct path value pass: rows per shared value array
+                                                   (10..15, default 14) */
 } slapcu_option;
 slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t value);
 

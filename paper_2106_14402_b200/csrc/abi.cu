@@ -148,6 +148,10 @@ slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t v
             break;
         case SLAPCU_OPT_DIRECT_PERSISTENT: c.opt.direct_persistent = v != 0; break;
         case SLAPCU_OPT_DIRECT_QUADS: c.opt.direct_quads = v != 0; break;
+        case SLAPCU_OPT_DIRECT_VALUE_TILE_ROWS_LOG2:
+            require(v >= 10 && v <= 15, SLAPCU_ERR_INVALID, "value tile rows log2 must be in 10..15");
+            c.opt.direct_value_tile_log2 = (int)v;
+            break;
         case SLAPCU_OPT_DIRECT_FORM_THREADS:
             require(v == 128 || v == 256 || v == 512, SLAPCU_ERR_INVALID, "form threads: 128, 256 or 512");
             c.opt.direct_form_threads = (int)v;

@@ -126,7 +126,9 @@ struct Options {
     int64_t direct_dense_run_min = 2048;    // direct path: A runs (column x tile) this long are OR-ed
                                             // as precomputed tile bitmaps (0 = never)
     int direct_mark_mode = 0;               // product update: 0 test+set, 1 atomic only, 2 quad-merged
-    int direct_quads = 0;                   // direct path: lane-contiguous quads merged per word
+    int direct_quads = 0;
+    int direct_value_tile_log2 = 14;        // direct path value pass: rows per shared value array
+    int direct_values_fallback = 0;         // 1: value semirings use begin/finish instead                   // direct path: lane-contiguous quads merged per word
     int direct_persistent = 1;              // form kernel: persistent CTAs (1) or one CTA per unit (0)
     int direct_form_threads = 256;          // CTA size of the form kernel (128, 256, 512)
     int direct_emit_threads = 128;          // CTA size of the emit kernel (128, 256)
@@ -143,8 +145,12 @@ struct DirectCache {
     int atp_tl = -1;
     bool atp_valid = false;
     DevBuf dslot, dbm;  // dense A runs: slot per (k, tile), tile bitmaps
+    DevBuf atpv;        // A tile pointers at the value-pass sub-tile height
+    const void* atpv_key = nullptr;
+    int64_t atpv_ncols = -1, atpv_nnz = -1;
+    int atpv_tl = -1;
     int ndense = 0, dense_min = -1;
-    DevBuf lp, hcnt, hl, items, ifl, sres, soff, units, order, stash, partial, cnt, form, hoff;
+    DevBuf lp, hcnt, hl, items, ifl, sres, soff, units, order, stash, partial, cnt, form, hoff, rbc;
     int64_t last_nnz = -1;  // exact nnz(C) of the last call (also on BudgetError)
 };
 
@@ -217,7 +223,7 @@ void ctx_settle(Ctx& c);
 // fused.cu helpers shared with the direct path
 void fused_light_launch(Ctx& c, int sr, bool ones, int bin, const DevCsc& A, const DevCsc& B, const int* list, int n,
                         const int64_t* flops, FusedState& f);
-void fused_copy_light(Ctx& c, bool ones, const int* list, int n, const FusedState& f, const int64_t* c_colptr,
+void fused_copy_light(Ctx& c, int sr, bool ones, const int* list, int n, const FusedState& f, const int64_t* c_colptr,
                       int32_t* c_rowids, void* c_vals);
 // direct.cu: single pass straight into C (pattern semirings)
 int64_t direct_spgemm(Ctx& c, const DevCsc& A, const DevCsc& B, int sr, int alg, int64_t capacity, int64_t* c_colptr,

@@ -307,6 +307,7 @@ struct FormArgs {
     unsigned long long* hcnt;  // output entries per column (heavy part)
     int* ticket;
     int nunits;
+    int* rbc;  // per item entries per 4096-row block (value semirings), or null
     int quads;  // 1: lane-contiguous quads merged per word before the shared update
 };
 
@@ -316,10 +317,23 @@ struct FormArgs {
 template <int NT>
 __device__ __forceinline__ void stash_bitmap(unsigned* bm, unsigned* summ, uint16_t* tl, int W, int* wsum, int* red,
                                              int* bcs, int64_t item, int j, unsigned* stash, int64_t sres,
-                                             int64_t* cnt, int* form, unsigned long long* hcnt) {
+                                             int64_t* cnt, int* form, unsigned long long* hcnt, int* rbc) {
     constexpr int NW = NT / 32;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int WS = W >> 5;
+    if (rbc) {  // entries per 4096-row block (value pass sub-tile ranges)
+        const int nrb = (W + kEmitBlock - 1) / kEmitBlock;
+        for (int b = warp; b < nrb; b += NW) {
+            int x = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int w = b * kEmitBlock + q * 32 + lane;
+                x += w < W ? __popc(bm[w]) : 0;
+            }
+            x = warp_reduce_sum(x);
+            if (lane == 0) rbc[item * nrb + b] = x;
+        }
+    }
     // touched words in order: summary popcounts -> scan -> list (WS <= NT)
     unsigned sw = 0;
     if (tid < WS) {
@@ -436,7 +450,7 @@ __global__ void __launch_bounds__(NT) k_tile_form(FormArgs g) {
             for (int q = threadIdx.x; q < W / 32; q += NT) summ[q] = 0u;
         } else {
             stash_bitmap<NT>(bm, summ, tl, W, sh.wsum, red, bcs, u.x, it.x, g.stash + g.soff[u.x], g.sres[u.x], g.cnt,
-                             g.form, g.hcnt);
+                             g.form, g.hcnt, g.rbc);
         }
         __syncthreads();
     }
@@ -448,7 +462,8 @@ __global__ void __launch_bounds__(NT)
     k_tile_combine(int TL, const int2* __restrict__ items, const int* __restrict__ sitems,
                    const int* __restrict__ spart, const int* __restrict__ snp, const unsigned* __restrict__ partial,
                    unsigned* __restrict__ stash, const int64_t* __restrict__ soff, const int64_t* __restrict__ sres,
-                   int64_t* __restrict__ cnt, int* __restrict__ form, unsigned long long* __restrict__ hcnt) {
+                   int64_t* __restrict__ cnt, int* __restrict__ form, unsigned long long* __restrict__ hcnt,
+                   int* __restrict__ rbc) {
     constexpr int NW = NT / 32;
     extern __shared__ __align__(16) unsigned char sm_raw[];
     const int W = 1 << (TL - 5);
@@ -473,7 +488,7 @@ __global__ void __launch_bounds__(NT)
     }
     __syncthreads();
     stash_bitmap<NT>(bm, summ, tl, W, wsum, red, bcs, item, items[item].x, stash + soff[item], sres[item], cnt, form,
-                     hcnt);
+                     hcnt, rbc);
 }
 
 // ------------------------------------------------------------------- emit
@@ -647,6 +662,201 @@ __global__ void __launch_bounds__(NT) k_tile_emit(EmitArgs g) {
         for (int64_t q = tid; q < body; q += NT) v4[q] = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
         for (int64_t q = head + (body << 4) + tid; q < c; q += NT) v[q] = 1;
     }
+}
+
+// ------------------------------------------------------------ value pass
+
+// Values of the items for semirings with values (and OrAnd operands with
+// stored zeros), after the emit pass has written C's rows.  One CTA per item;
+// the item's tile is walked in sub-tiles of 2^VTL rows with a dense shared
+// value array indexed by row (no ranks needed): every product of the
+// sub-tile is folded in with the semiring's atomic, then the item's output
+// entries that fall in the sub-tile (a contiguous range of C, found by
+// binary search in its sorted rows) take their values and the touched slots
+// are reset to the identity.  A second walk over the products -- the pattern
+// walk (k_tile_form) only touches row ids.
+struct ValueArgs {
+    DevCsc A, B;
+    const int32_t* Atpv;  // A tile pointers at 2^VTL rows
+    int Tv, VTL, TL;
+    const int2* items;
+    const int64_t* cnt;
+    const int64_t* hoff;
+    const int64_t* lp;
+    const int* rbc;       // entries per 4096-row block of every item
+    const int32_t* crw;
+    void* cv;
+};
+
+template <int SRID, int NT>
+__global__ void __launch_bounds__(NT) k_tile_values(ValueArgs g) {
+    using S_ = Sr<SRID>;
+    using T = typename S_::T;
+    using Acc = typename S_::Acc;
+    constexpr int NW = NT / 32;
+    extern __shared__ __align__(16) unsigned char sm_raw[];
+    Acc* val = reinterpret_cast<Acc*>(sm_raw);
+    __shared__ int wsum[NW + 1];
+    __shared__ int ustart[NT + 1];
+    __shared__ int ulen[NT];
+    __shared__ int64_t ustartp[NT];
+    __shared__ T ubval[NT];
+    __shared__ int sp[NT + 1];       // packed short runs: product prefix per B entry
+    __shared__ int64_t sst[NT];
+    __shared__ T sbv[NT];
+    __shared__ int nlong;
+    __shared__ int64_t range_sh[2];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nsub = 1 << (g.TL - g.VTL);
+    const int item = blockIdx.x / nsub, s = blockIdx.x % nsub;
+    const int2 it = g.items[item];
+    const int j = it.x;
+    const int ts = (it.y << (g.TL - g.VTL)) + s;
+    const int s0 = ts << g.VTL;
+    if (warp == 0) {  // this sub-tile's output entries C[lo, hi) from the row-block counts
+        const int W = 1 << (g.TL - 5);
+        const int nrb = (W + kEmitBlock - 1) / kEmitBlock;
+        const int per = max(1, (1 << (g.VTL - 5)) / kEmitBlock);  // row blocks per sub-tile
+        const int* rb = g.rbc + int64_t(item) * nrb;
+        int before = 0, inside = 0;
+        for (int b = lane; b < nrb; b += 32) {
+            const int x = rb[b];
+            before += b < s * per ? x : 0;
+            inside += (b >= s * per && b < (s + 1) * per) ? x : 0;
+        }
+        before = warp_reduce_sum(before);
+        inside = warp_reduce_sum(inside);
+        if (lane == 0) {
+            const int64_t off = g.lp[j] + g.hoff[item];
+            range_sh[0] = off + before;
+            range_sh[1] = off + before + inside;
+            nlong = 0;
+        }
+    }
+    __syncthreads();
+    const int64_t lo = range_sh[0], hi = range_sh[1];
+    if (lo == hi) return;
+    // products only land on output rows: initialise just those slots
+    for (int64_t q = lo + tid; q < hi; q += NT) val[g.crw[q] - s0] = S_::identity();
+    const T* Av = static_cast<const T*>(g.A.v);
+    const T* Bv = static_cast<const T*>(g.B.v);
+    T* Cv = static_cast<T*>(g.cv);
+    const int32_t* __restrict__ Arw = g.A.rw;
+    const int64_t bs = g.B.cp[j], be = g.B.cp[j + 1];
+    for (int64_t base = bs; base < be; base += NT) {
+        const int64_t i = base + tid;
+        int slen = 0;
+        if (i < be) {
+            const int k = g.B.rw[i];
+            const int32_t* tp = g.Atpv + int64_t(k) * (g.Tv + 1) + ts;
+            const int rlo = tp[0], rhi = tp[1];
+            const int len = rhi - rlo;
+            if (len > 0) {
+                const int64_t st = g.A.cp[k] + rlo;
+                const T bv = Bv[i];
+                if (len < 32) {
+                    slen = len;
+                    sst[tid] = st;
+                    sbv[tid] = bv;
+                } else {
+                    const unsigned peers = __activemask();
+                    const int leader = __ffs(peers) - 1;
+                    int pos = 0;
+                    if (lane == leader) pos = atomicAdd(&nlong, __popc(peers));
+                    pos = __shfl_sync(peers, pos, leader) + __popc(peers & ((1u << lane) - 1u));
+                    ulen[pos] = len;
+                    ustartp[pos] = st;
+                    ubval[pos] = bv;
+                }
+            }
+        }
+        __syncthreads();  // (also makes every thread's shared state visible, in this step's order)
+        const int nl = nlong;
+        const int units = tid < nl ? (ulen[tid] + 255) / 256 : 0;
+        int tot, stot;
+        {
+            // two block scans at once: long-run units and short-run products
+            int wt, wt2;
+            const int ex = warp_excl_scan(units, lane, &wt);
+            const int ex2 = warp_excl_scan(slen, lane, &wt2);
+            if (lane == 0) wsum[warp] = wt;
+            __shared__ int wsum2[NW + 1];
+            if (lane == 0) wsum2[warp] = wt2;
+            __syncthreads();
+            if (warp == 0) {
+                const int x = lane < NW ? wsum[lane] : 0, y = lane < NW ? wsum2[lane] : 0;
+                int t1, t2;
+                const int e1 = warp_excl_scan(x, lane, &t1), e2 = warp_excl_scan(y, lane, &t2);
+                if (lane < NW) {
+                    wsum[lane] = e1;
+                    wsum2[lane] = e2;
+                }
+                if (lane == 0) {
+                    wsum[NW] = t1;
+                    wsum2[NW] = t2;
+                }
+            }
+            __syncthreads();
+            ustart[tid] = ex + wsum[warp];
+            sp[tid] = ex2 + wsum2[warp];
+            tot = wsum[NW];
+            stot = wsum2[NW];
+            if (tid == 0) {
+                ustart[nl] = tot;
+                sp[NT] = stot;
+            }
+        }
+        __syncthreads();
+        // short runs packed 32 products per warp step: entry of product o by search
+        for (int o0 = warp * 32; o0 < stot; o0 += NT) {
+            const int o = o0 + lane;
+            if (o < stot) {
+                int a = 0, b = NT - 1;
+                while (a < b) {
+                    const int mid = (a + b + 1) >> 1;
+                    if (sp[mid] <= o)
+                        a = mid;
+                    else
+                        b = mid - 1;
+                }
+                const int64_t p = sst[a] + (o - sp[a]);
+                S_::atomic_acc(&val[__ldg(&Arw[p]) - s0], S_::mul(Av[p], sbv[a]));
+            }
+        }
+        const int u0 = (int)((int64_t(tot) * warp) / NW), u1 = (int)((int64_t(tot) * (warp + 1)) / NW);
+        int e = 0;
+        if (u0 < u1) {
+            int a = 0, b = nl - 1;
+            while (a < b) {
+                const int mid = (a + b + 1) >> 1;
+                if (ustart[mid] <= u0)
+                    a = mid;
+                else
+                    b = mid - 1;
+            }
+            e = a;
+        }
+        for (int u = u0; u < u1; ++u) {
+            if (ustart[e + 1] <= u) ++e;
+            const int c0 = (u - ustart[e]) * 256;
+            const int64_t p0 = ustartp[e] + c0;
+            const int m = min(256, ulen[e] - c0);
+            const T bv = ubval[e];
+            for (int x = lane; x < m; x += 64) {
+                const int r0 = __ldg(&Arw[p0 + x]);
+                const T a0 = Av[p0 + x];
+                const bool two = x + 32 < m;
+                const int r1 = two ? __ldg(&Arw[p0 + x + 32]) : 0;
+                const T a1 = two ? Av[p0 + x + 32] : a0;
+                S_::atomic_acc(&val[r0 - s0], S_::mul(a0, bv));
+                if (two) S_::atomic_acc(&val[r1 - s0], S_::mul(a1, bv));
+            }
+        }
+        __syncthreads();
+        if (tid == 0) nlong = 0;
+        __syncthreads();
+    }
+    for (int64_t q = lo + tid; q < hi; q += NT) Cv[q] = S_::out(val[g.crw[q] - s0]);
 }
 
 // ------------------------------------------------------------ item setup
@@ -950,6 +1160,22 @@ static const int32_t* tile_pointers(Ctx& c, const DevCsc& A, int TL, int T) {
     return d.atp.as<int32_t>();
 }
 
+// Tile pointers at the value-pass sub-tile height (cached like Atp).
+static const int32_t* value_tile_pointers(Ctx& c, const DevCsc& A, int VTL, int Tv) {
+    DirectCache& d = c.direct;
+    if (d.atpv_key == A.cp && d.atpv_ncols == A.ncols && d.atpv_tl == VTL && d.atpv_nnz == A.nnz)
+        return d.atpv.as<int32_t>();
+    d.atpv.reset(sizeof(int32_t) * size_t(A.ncols) * (Tv + 1), c.stream);
+    KScope ks(c, KC_BIN);
+    launch(c, k_tile_ptr, dim3(grid_for(c, A.ncols * (Tv + 1), 256)), dim3(256), 0, A, VTL, Tv,
+           d.atpv.as<int32_t>());
+    d.atpv_key = A.cp;
+    d.atpv_ncols = A.ncols;
+    d.atpv_nnz = A.nnz;
+    d.atpv_tl = VTL;
+    return d.atpv.as<int32_t>();
+}
+
 // Fallback for semirings with values (and OrAnd operands holding stored
 // zeros, whose pattern is structural but whose values are not all 1): the
 // fused begin/finish pair into the caller's buffers.
@@ -976,18 +1202,24 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
     resolve(c, B);
     if ((A.span && !A.v) || (B.span && !B.v)) throw Fail{SLAPCU_ERR_INVALID, "operand values are null"};
     ctx_settle(c);
-    if (sr != SLAPCU_OR_AND_U8) return direct_fallback(c, A_, B_, sr, alg, capacity, c_colptr, crw, cv);
-    // OrAnd: if no stored value is 0 every product is 1 (pattern only)
-    c.err_flag.reset(sizeof(int) * 2, c.stream);
-    int* fl = c.err_flag.as<int>();
-    SLAPCU_CUDA(cudaMemsetAsync(fl, 0, sizeof(int) * 2, c.stream));
-    any_zero_u8(c, (const uint8_t*)A.v + A.base, A.span, fl + 1);
-    any_zero_u8(c, (const uint8_t*)B.v + B.base, B.span, fl + 1);
-    if (d2h(c, fl + 1) != 0) return direct_fallback(c, A_, B_, sr, alg, capacity, c_colptr, crw, cv);
+    if (c.opt.direct_values_fallback && sr != SLAPCU_OR_AND_U8)
+        return direct_fallback(c, A_, B_, sr, alg, capacity, c_colptr, crw, cv);
+    // OrAnd: if no stored value is 0 every product is 1 (pattern only, values
+    // written as 1); otherwise -- and for every other semiring -- the pattern
+    // is structural and a value pass follows the emit pass
+    bool ones = false;
+    if (sr == SLAPCU_OR_AND_U8) {
+        c.err_flag.reset(sizeof(int) * 2, c.stream);
+        int* fl = c.err_flag.as<int>();
+        SLAPCU_CUDA(cudaMemsetAsync(fl, 0, sizeof(int) * 2, c.stream));
+        any_zero_u8(c, (const uint8_t*)A.v + A.base, A.span, fl + 1);
+        any_zero_u8(c, (const uint8_t*)B.v + B.base, B.span, fl + 1);
+        ones = d2h(c, fl + 1) == 0;
+    }
     SLAPCU_CUDA(cudaEventRecord(c.ev[0], c.stream));
     DirectCache& d = c.direct;
     FusedState& f = d.light;
-    f.ones = true;
+    f.ones = ones;
     prepare_plan(c, A, B);
     const int64_t* flops = c.plan.flops.as<int64_t>();
     const int64_t n = B.ncols;
@@ -1011,6 +1243,7 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
         light_bound += int64_t(f.bins.count[b]) * std::min<int64_t>(spec.thr[b], A.nrows);
     }
     f.srows.reset(sizeof(int32_t) * std::max<int64_t>(light_bound, 1), c.stream);
+    if (!ones) f.svals.reset(size_t(value_size(sr)) * std::max<int64_t>(light_bound, 1), c.stream);
     f.soff.reset(sizeof(int64_t) * std::max<int64_t>(n, 1), c.stream);
     f.scur.reset(sizeof(unsigned long long), c.stream);
     SLAPCU_CUDA(cudaMemsetAsync(f.scur.get(), 0, sizeof(unsigned long long), c.stream));
@@ -1019,7 +1252,7 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
         const int nb = f.bins.count[b];
         if (!nb) continue;
         KScope ks(c, KC_SYM_LIGHT);
-        fused_light_launch(c, sr, true, b, A, B, L + f.bins.offset[b], nb, flops, f);
+        fused_light_launch(c, sr, ones, b, A, B, L + f.bins.offset[b], nb, flops, f);
     }
     // light prefix per column (heavy columns count 0 here)
     d.lp.reset(sizeof(int64_t) * (n + 1), c.stream);
@@ -1126,12 +1359,18 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
         d.hoff.reset(sizeof(int64_t) * ni1, c.stream);
         SLAPCU_CUDA(cudaMemsetAsync(d.cnt.as<int64_t>() + nitems, 0, sizeof(int64_t), c.stream));
         KScope ks2(c, KC_SYM_HEAVY);
+        const int nrb = (W + kEmitBlock - 1) / kEmitBlock;
+        int* rbc = nullptr;
+        if (!ones) {
+            d.rbc.reset(sizeof(int) * size_t(nitems) * nrb, c.stream);
+            rbc = d.rbc.as<int>();
+        }
         const DenseRuns dr{d.ndense > 0 ? (const int*)d.dslot.as<int>() : nullptr,
                            (const unsigned*)d.dbm.as<unsigned>(), d.ndense > 0 ? d.dense_min : 0};
         FormArgs g{A, B, Atp, dr, T, TL, (const int2*)d.items.as<int2>(), (const int4*)d.units.as<int4>(),
                    (const int*)d.order.as<int>(), d.stash.as<unsigned>(), (const int64_t*)d.soff.as<int64_t>(),
                    (const int64_t*)d.sres.as<int64_t>(), d.partial.as<unsigned>(), d.cnt.as<int64_t>(),
-                   d.form.as<int>(), d.hcnt.as<unsigned long long>(), nullptr, 0,
+                   d.form.as<int>(), d.hcnt.as<unsigned long long>(), nullptr, 0, rbc,
                    c.opt.direct_quads};
         const size_t smem = sizeof(unsigned) * (W + W / 32) + sizeof(uint16_t) * W;
         DevBuf tick(sizeof(int), c.stream);
@@ -1164,7 +1403,7 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
                    (const int*)si, (const int*)(si + nitems), (const int*)(si + 2 * nitems),
                    (const unsigned*)d.partial.as<unsigned>(), d.stash.as<unsigned>(),
                    (const int64_t*)d.soff.as<int64_t>(), (const int64_t*)d.sres.as<int64_t>(), d.cnt.as<int64_t>(),
-                   d.form.as<int>(), d.hcnt.as<unsigned long long>());
+                   d.form.as<int>(), d.hcnt.as<unsigned long long>(), rbc);
         }
         exclusive_scan_i64(c, d.cnt.as<int64_t>(), d.hoff.as<int64_t>(), nitems + 1);
     }
@@ -1187,7 +1426,7 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
         EmitArgs e{(const int2*)d.items.as<int2>(), (const int64_t*)d.cnt.as<int64_t>(), (const int*)d.form.as<int>(),
                    (const unsigned*)d.stash.as<unsigned>(), (const int64_t*)d.soff.as<int64_t>(),
                    (const int64_t*)d.hoff.as<int64_t>(), (const int64_t*)d.lp.as<int64_t>(), TL, crw,
-                   static_cast<uint8_t*>(cv)};
+                   ones ? static_cast<uint8_t*>(cv) : nullptr};  // values: 1s here, else the value pass
         const size_t smem = 0;
         auto emit = [&](auto ke, int nt) {
             ensure_smem(ke, smem);
@@ -1198,9 +1437,29 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
         else
             emit(k_tile_emit<256>, 256);
     }
+    if (nitems > 0 && !ones) {
+        KScope ks(c, KC_NUM_HEAVY);
+        // sub-tiles are whole 4096-row blocks of the item (or the item itself)
+        const int VTL = std::min(TL, std::max(12, c.opt.direct_value_tile_log2));
+        const int Tv = (int)((A.nrows + (int64_t(1) << VTL) - 1) >> VTL);
+        const int32_t* Atpv = value_tile_pointers(c, A, VTL, Tv);
+        const ValueArgs va{A, B, Atpv, Tv, VTL, TL, (const int2*)d.items.as<int2>(),
+                           (const int64_t*)d.cnt.as<int64_t>(), (const int64_t*)d.hoff.as<int64_t>(),
+                           (const int64_t*)d.lp.as<int64_t>(), (const int*)d.rbc.as<int>(), crw, cv};
+        dispatch_sr(sr, [&](auto id) {
+            constexpr int ID = decltype(id)::value;
+            using Acc = typename Sr<ID>::Acc;
+            const size_t smem = sizeof(Acc) * (size_t(1) << VTL);
+            if (smem > size_t(c.smem_optin) - 16 * 1024)
+                throw Fail{SLAPCU_ERR_INVALID, "value tile too large for shared memory"};
+            auto k = k_tile_values<ID, 256>;
+            ensure_smem(k, smem);
+            launch(c, k, dim3((unsigned)(int64_t(nitems) << (TL - VTL))), dim3(256), smem, va);
+        });
+    }
     if (nlight) {
         KScope ks(c, KC_NUM_LIGHT);
-        fused_copy_light(c, true, L, nlight, f, c_colptr, crw, cv);
+        fused_copy_light(c, sr, ones, L, nlight, f, c_colptr, crw, cv);
     }
     SLAPCU_CUDA(cudaEventRecord(c.ev[1], c.stream));
     SLAPCU_CUDA(cudaStreamSynchronize(c.stream));

@@ -693,17 +693,21 @@ void fused_light_launch(Ctx& c, int sr, bool ones, int bin, const DevCsc& A, con
     });
 }
 
-// Staged light columns into C (OrAnd only: values 1 when `ones`).
-void fused_copy_light(Ctx& c, bool ones, const int* list, int n, const FusedState& f, const int64_t* c_colptr,
+// Staged light columns into C (values 1 for all-one OrAnd operands).
+void fused_copy_light(Ctx& c, int sr, bool ones, const int* list, int n, const FusedState& f, const int64_t* c_colptr,
                       int32_t* crw, void* cv) {
-    using T = uint8_t;
     const int g = grid_for(c, int64_t(n) * 32, 256, 16);
-    if (ones)
-        launch(c, k_copy_light<T, true>, dim3(g), dim3(256), 0, list, n, (const int64_t*)f.soff.as<int64_t>(), c_colptr,
-               (const int32_t*)f.srows.as<int32_t>(), (const T*)nullptr, crw, static_cast<T*>(cv));
-    else
-        launch(c, k_copy_light<T, false>, dim3(g), dim3(256), 0, list, n, (const int64_t*)f.soff.as<int64_t>(),
-               c_colptr, (const int32_t*)f.srows.as<int32_t>(), (const T*)f.svals.get(), crw, static_cast<T*>(cv));
+    dispatch_sr(sr, [&](auto id) {
+        constexpr int ID = decltype(id)::value;
+        using T = typename Sr<ID>::T;
+        if (ones)
+            launch(c, k_copy_light<T, true>, dim3(g), dim3(256), 0, list, n, (const int64_t*)f.soff.as<int64_t>(),
+                   c_colptr, (const int32_t*)f.srows.as<int32_t>(), (const T*)nullptr, crw, static_cast<T*>(cv));
+        else
+            launch(c, k_copy_light<T, false>, dim3(g), dim3(256), 0, list, n, (const int64_t*)f.soff.as<int64_t>(),
+                   c_colptr, (const int32_t*)f.srows.as<int32_t>(), (const T*)f.svals.get(), crw,
+                   static_cast<T*>(cv));
+    });
 }
 
 int64_t fused_begin(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int alg, int64_t* c_colptr,
