@@ -130,7 +130,7 @@ typedef enum {
                                               run (16-byte loads) and merges rows sharing a word before
                                               the shared-memory update */
     SLAPCU_OPT_DIRECT_VALUE_TILE_ROWS_LOG2 = 17 /* direct path value pass: rows per shared value array
-                                                   (10..15, default 14) */
+                                                   (12..15, default 14) */
 } slapcu_option;
 slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t value);
 

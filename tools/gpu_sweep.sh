@@ -5,7 +5,7 @@ mkdir -p gpurun_out
 IFS=';' read -ra SETS <<< "$1"
 i=0
 for a in "${SETS[@]}"; do
-  timeout 300 python bench.py --no-cpu --no-e2e --steps 2 --warmup 3 $a > gpurun_out/sweep$i.log 2>&1
+  timeout ${RUN_TIMEOUT:-240} python bench.py --no-cpu --no-e2e --steps 2 --warmup 3 $a > gpurun_out/sweep$i.log 2>&1
   python tools/sweep_line.py "$a" gpurun_out/sweep$i.log
   i=$((i+1))
 done
