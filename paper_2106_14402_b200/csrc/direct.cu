@@ -47,6 +47,7 @@ __host__ __device__ __forceinline__ int64_t lmin(int64_t a, int64_t b) { return 
 constexpr int kEmitWPL = 4;                    // stash words per lane in a warp block
 constexpr int kEmitBlock = 32 * kEmitWPL;      // words per warp block
 constexpr int kEmitStage = 1024;               // entries per staging round
+constexpr int kRbcWords = 128;                 // value pass: row blocks of 128 words (4096 rows)
 constexpr int kMaxBlocks = 128;                // W / kEmitBlock for row tiles up to 2^19 (emit holds 4 x 32)
 
 // Every item's stash starts with a header of per-block output counts (one
@@ -322,12 +323,12 @@ __device__ __forceinline__ void stash_bitmap(unsigned* bm, unsigned* summ, uint1
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int WS = W >> 5;
     if (rbc) {  // entries per 4096-row block (value pass sub-tile ranges)
-        const int nrb = (W + kEmitBlock - 1) / kEmitBlock;
+        const int nrb = (W + kRbcWords - 1) / kRbcWords;
         for (int b = warp; b < nrb; b += NW) {
             int x = 0;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int w = b * kEmitBlock + q * 32 + lane;
+            for (int q = 0; q < kRbcWords / 32; ++q) {
+                const int w = b * kRbcWords + q * 32 + lane;
                 x += w < W ? __popc(bm[w]) : 0;
             }
             x = warp_reduce_sum(x);
@@ -715,8 +716,8 @@ __global__ void __launch_bounds__(NT) k_tile_values(ValueArgs g) {
     const int s0 = ts << g.VTL;
     if (warp == 0) {  // this sub-tile's output entries C[lo, hi) from the row-block counts
         const int W = 1 << (g.TL - 5);
-        const int nrb = (W + kEmitBlock - 1) / kEmitBlock;
-        const int per = max(1, (1 << (g.VTL - 5)) / kEmitBlock);  // row blocks per sub-tile
+        const int nrb = (W + kRbcWords - 1) / kRbcWords;
+        const int per = max(1, (1 << (g.VTL - 5)) / kRbcWords);  // row blocks per sub-tile
         const int* rb = g.rbc + int64_t(item) * nrb;
         int before = 0, inside = 0;
         for (int b = lane; b < nrb; b += 32) {
@@ -1359,7 +1360,7 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
         d.hoff.reset(sizeof(int64_t) * ni1, c.stream);
         SLAPCU_CUDA(cudaMemsetAsync(d.cnt.as<int64_t>() + nitems, 0, sizeof(int64_t), c.stream));
         KScope ks2(c, KC_SYM_HEAVY);
-        const int nrb = (W + kEmitBlock - 1) / kEmitBlock;
+        const int nrb = (W + kRbcWords - 1) / kRbcWords;
         int* rbc = nullptr;
         if (!ones) {
             d.rbc.reset(sizeof(int) * size_t(nitems) * nrb, c.stream);
@@ -1432,10 +1433,7 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
             ensure_smem(ke, smem);
             launch(c, ke, dim3(nitems), dim3(nt), smem, e);
         };
-        if (c.opt.direct_emit_threads == 128)
-            emit(k_tile_emit<128>, 128);
-        else
-            emit(k_tile_emit<256>, 256);
+        emit(k_tile_emit<128>, 128);  // (per-warp state is static shared memory: 4 warps)
     }
     if (nitems > 0 && !ones) {
         KScope ks(c, KC_NUM_HEAVY);
