@@ -129,8 +129,9 @@ typedef enum {
     SLAPCU_OPT_DIRECT_QUADS = 16,          /* direct path: 1 = each lane takes 4 consecutive entries of a
                                               run (16-byte loads) and merges rows sharing a word before
                                               the shared-memory update */
-    SLAPCU_OPT_DIRECT_VALUE_TILE_ROWS_LOG2 = 17 /* direct path value pass: rows per shared value array
-                                                   (12..15, default 14) */
+    SLAPCU_OPT_DIRECT_VALUE_TILE_ROWS_LOG2 = 17, /* direct path value pass: rows per shared value array
+                                                    (12..15, default 14) */
+    SLAPCU_OPT_DIRECT_VALUE_THREADS = 18   /* direct path value pass: threads per CTA (256, 512) */
 } slapcu_option;
 slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t value);
 

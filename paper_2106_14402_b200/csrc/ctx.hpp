@@ -128,7 +128,8 @@ struct Options {
     int direct_mark_mode = 0;               // product update: 0 test+set, 1 atomic only, 2 quad-merged
     int direct_quads = 0;
     int direct_value_tile_log2 = 14;        // direct path value pass: rows per shared value array
-    int direct_values_fallback = 0;         // 1: value semirings use begin/finish instead                   // direct path: lane-contiguous quads merged per word
+    int direct_values_fallback = 0;
+    int direct_value_threads = 256;         // CTA size of the value pass (256, 512)         // 1: value semirings use begin/finish instead                   // direct path: lane-contiguous quads merged per word
     int direct_persistent = 1;              // form kernel: persistent CTAs (1) or one CTA per unit (0)
     int direct_form_threads = 256;          // CTA size of the form kernel (128, 256, 512)
     int direct_emit_threads = 128;          // CTA size of the emit kernel (128, 256)

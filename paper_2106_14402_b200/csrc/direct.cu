@@ -1450,9 +1450,14 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
             const size_t smem = sizeof(Acc) * (size_t(1) << VTL);
             if (smem > size_t(c.smem_optin) - 16 * 1024)
                 throw Fail{SLAPCU_ERR_INVALID, "value tile too large for shared memory"};
-            auto k = k_tile_values<ID, 256>;
-            ensure_smem(k, smem);
-            launch(c, k, dim3((unsigned)(int64_t(nitems) << (TL - VTL))), dim3(256), smem, va);
+            auto go = [&](auto k, int nt) {
+                ensure_smem(k, smem);
+                launch(c, k, dim3((unsigned)(int64_t(nitems) << (TL - VTL))), dim3(nt), smem, va);
+            };
+            if (c.opt.direct_value_threads == 512)
+                go(k_tile_values<ID, 512>, 512);
+            else
+                go(k_tile_values<ID, 256>, 256);
         });
     }
     if (nlight) {

@@ -465,7 +465,9 @@ __device__ __forceinline__ void smem_zero(unsigned* p, int n) {
 // against the same 48 KB default, hence the margin.
 template <class K>
 void ensure_smem(K kernel, size_t smem) {
-    if (smem > 40 * 1024) SLAPCU_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // static + dynamic may pass the 48 KB default even when the dynamic part
+    // alone does not, so opt in whenever a kernel carries static state too
+    if (smem > 16 * 1024) SLAPCU_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
 }
 
 int grid_for(Ctx& c, int64_t work, int block, int per_sm = 8);
