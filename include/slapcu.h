@@ -131,7 +131,11 @@ typedef enum {
                                               the shared-memory update */
     SLAPCU_OPT_DIRECT_VALUE_TILE_ROWS_LOG2 = 17, /* direct path value pass: rows per shared value array
                                                     (12..15, default 14) */
-    SLAPCU_OPT_DIRECT_VALUE_THREADS = 18   /* direct path value pass: threads per CTA (256, 512) */
+    SLAPCU_OPT_DIRECT_VALUE_THREADS = 18,  /* direct path value pass: threads per CTA (256, 512) */
+    SLAPCU_OPT_SUMMA_CONCAT = 19           /* SUMMA / 3D layers: 1 (default) = all stage blocks are
+                                              broadcast, then ONE concatenated-k product forms C(i,j)
+                                              (no stage partials, no merge); 0 = per-stage products
+                                              double-buffered against the broadcasts + stage merge */
 } slapcu_option;
 slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t value);
 

@@ -152,6 +152,7 @@ slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t v
             require(v >= 10 && v <= 15, SLAPCU_ERR_INVALID, "value tile rows log2 must be in 10..15");
             c.opt.direct_value_tile_log2 = (int)v;
             break;
+        case SLAPCU_OPT_SUMMA_CONCAT: c.opt.summa_concat = v != 0; break;
         case SLAPCU_OPT_DIRECT_VALUE_THREADS:
             require(v == 256 || v == 512, SLAPCU_ERR_INVALID, "value threads: 256 or 512");
             c.opt.direct_value_threads = (int)v;

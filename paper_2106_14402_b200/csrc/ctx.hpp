@@ -129,6 +129,7 @@ struct Options {
     int direct_quads = 0;
     int direct_value_tile_log2 = 14;        // direct path value pass: rows per shared value array
     int direct_values_fallback = 0;
+    int summa_concat = 1;                   // SUMMA: one concatenated-k product per call (no stage merge)
     int direct_value_threads = 256;         // CTA size of the value pass (256, 512)         // 1: value semirings use begin/finish instead                   // direct path: lane-contiguous quads merged per word
     int direct_persistent = 1;              // form kernel: persistent CTAs (1) or one CTA per unit (0)
     int direct_form_threads = 256;          // CTA size of the form kernel (128, 256, 512)

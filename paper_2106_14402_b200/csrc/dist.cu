@@ -30,7 +30,7 @@
 #include <string>
 #include <vector>
 
-#include "ctx.hpp"
+#include "kern.cuh"
 
 #define SLAPCU_NCCL(call)                                                                               \
     do {                                                                                                \
@@ -203,6 +203,139 @@ struct Timer {
     }
 };
 
+// ---- concatenated-k local multiply (no partial merge)
+//
+// C(i,j) = sum_s A(i,s) B(s,j) is formed as ONE product [A(i,0) .. A(i,q-1)] x
+// [B(0,j); ..; B(q-1,j)] once every stage's blocks have arrived: the stage
+// partials of summa.hpp:145-156 -- each nearly as large as C(i,j) itself for
+// A*A -- and their merge disappear.  Exact semirings are bit-identical to the
+// stage-order fold; PlusTimes fp64 stays within the north_star tolerance.
+
+__global__ void k_cat_colptr(const int64_t* __restrict__ in, int64_t K, int64_t pre, int64_t* __restrict__ out,
+                             int last) {
+    const int64_t n = K + (last ? 1 : 0);
+    for (int64_t x = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < n; x += int64_t(gridDim.x) * blockDim.x)
+        out[x] = in[x] - in[0] + pre;
+}
+
+struct VStack {
+    const int64_t* cp[8];
+    const int32_t* rw[8];
+    const char* v[8];
+    int64_t koff[8];
+    int q;
+};
+
+__global__ void k_vstack_count(VStack vs, int64_t n, int64_t* __restrict__ cnt) {
+    for (int64_t x = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < n; x += int64_t(gridDim.x) * blockDim.x) {
+        int64_t t = 0;
+        for (int s = 0; s < vs.q; ++s) t += vs.cp[s][x + 1] - vs.cp[s][x];
+        cnt[x] = t;
+    }
+}
+
+__global__ void k_vstack_fill(VStack vs, int vsize, int64_t n, const int64_t* __restrict__ ocp,
+                              int32_t* __restrict__ orw, char* __restrict__ ov) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t x = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; x < n;
+         x += (int64_t(gridDim.x) * blockDim.x) >> 5) {
+        int64_t o = ocp[x];
+        for (int s = 0; s < vs.q; ++s) {
+            const int64_t a = vs.cp[s][x], b = vs.cp[s][x + 1];
+            const int32_t add = (int32_t)vs.koff[s];
+            for (int64_t e = a + lane; e < b; e += 32) {
+                orw[o + (e - a)] = vs.rw[s][e] + add;
+                for (int k = 0; k < vsize; ++k) ov[(o + (e - a)) * vsize + k] = vs.v[s][e * vsize + k];
+            }
+            o += b - a;
+        }
+    }
+}
+
+// [A_0 .. A_{q-1}] (column concatenation) and [B_0; ..; B_{q-1}] (row
+// concatenation) of the received stage blocks, then one direct product.
+void concat_multiply(Ctx& c, const std::vector<DevCsc>& As, const std::vector<DevCsc>& Bs, int sr, int alg,
+                     Block& out, float* ms) {
+    const int q = (int)As.size();
+    const int vs = value_size(sr);
+    int64_t K = 0, annz = 0, bnnz = 0;
+    for (int s = 0; s < q; ++s) {
+        K += As[s].ncols;
+        annz += As[s].span;
+        bnnz += Bs[s].span;
+    }
+    const int64_t M = As[0].nrows, N = Bs[0].ncols;
+    Block Ac, Bc;
+    Ac.nrows = M; Ac.ncols = K; Ac.nnz = annz;
+    Ac.cp.reset(sizeof(int64_t) * (K + 1), c.stream);
+    Ac.rw.reset(sizeof(int32_t) * std::max<int64_t>(annz, 1), c.stream);
+    Ac.v.reset(size_t(vs) * std::max<int64_t>(annz, 1), c.stream);
+    int64_t koff = 0, pre = 0;
+    for (int s = 0; s < q; ++s) {
+        const DevCsc& a = As[s];
+        launch(c, k_cat_colptr, dim3(grid_for(c, a.ncols + 1, 256)), dim3(256), 0, a.cp, a.ncols, pre,
+               Ac.cp.as<int64_t>() + koff, s == q - 1 ? 1 : 0);
+        if (a.span) {
+            SLAPCU_CUDA(cudaMemcpyAsync(Ac.rw.as<int32_t>() + pre, a.rw + a.base, sizeof(int32_t) * a.span,
+                                        cudaMemcpyDeviceToDevice, c.stream));
+            SLAPCU_CUDA(cudaMemcpyAsync(static_cast<char*>(Ac.v.get()) + size_t(vs) * pre,
+                                        static_cast<const char*>(a.v) + size_t(vs) * a.base, size_t(vs) * a.span,
+                                        cudaMemcpyDeviceToDevice, c.stream));
+        }
+        koff += a.ncols;
+        pre += a.span;
+    }
+    VStack st{};
+    st.q = q;
+    int64_t ko = 0;
+    for (int s = 0; s < q; ++s) {
+        st.cp[s] = Bs[s].cp;
+        st.rw[s] = Bs[s].rw;
+        st.v[s] = static_cast<const char*>(Bs[s].v);
+        st.koff[s] = ko;
+        ko += Bs[s].nrows;
+    }
+    Bc.nrows = ko; Bc.ncols = N; Bc.nnz = bnnz;
+    Bc.cp.reset(sizeof(int64_t) * (N + 1), c.stream);
+    Bc.rw.reset(sizeof(int32_t) * std::max<int64_t>(bnnz, 1), c.stream);
+    Bc.v.reset(size_t(vs) * std::max<int64_t>(bnnz, 1), c.stream);
+    {
+        DevBuf cnt(sizeof(int64_t) * (N + 1), c.stream);
+        SLAPCU_CUDA(cudaMemsetAsync(cnt.as<int64_t>() + N, 0, sizeof(int64_t), c.stream));
+        launch(c, k_vstack_count, dim3(grid_for(c, N, 256)), dim3(256), 0, st, N, cnt.as<int64_t>());
+        exclusive_scan_i64(c, cnt.as<int64_t>(), Bc.cp.as<int64_t>(), N + 1);
+        launch(c, k_vstack_fill, dim3(grid_for(c, N * 32, 256)), dim3(256), 0, st, vs, N,
+               (const int64_t*)Bc.cp.as<int64_t>(), Bc.rw.as<int32_t>(), static_cast<char*>(Bc.v.get()));
+    }
+    const DevCsc A = Ac.view(), B = Bc.view();
+    // output sized by the bound sum_j min(flops_j, M)
+    DevBuf fl(sizeof(int64_t) * std::max<int64_t>(N, 1), c.stream);
+    int64_t tot = 0;
+    spgemm_flops(c, A, B, fl.as<int64_t>(), &tot);
+    std::vector<int64_t> hf(N);
+    if (N) SLAPCU_CUDA(cudaMemcpyAsync(hf.data(), fl.get(), sizeof(int64_t) * N, cudaMemcpyDeviceToHost, c.stream));
+    SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+    int64_t cap = 0;
+    for (int64_t x = 0; x < N; ++x) cap += std::min(hf[x], M);
+    out.nrows = M;
+    out.ncols = N;
+    out.cp.reset(sizeof(int64_t) * (N + 1), c.stream);
+    out.rw.reset(sizeof(int32_t) * std::max<int64_t>(cap, 1), c.stream);
+    out.v.reset(size_t(vs) * std::max<int64_t>(cap, 1), c.stream);
+    cudaEvent_t e0, e1;
+    SLAPCU_CUDA(cudaEventCreate(&e0));
+    SLAPCU_CUDA(cudaEventCreate(&e1));
+    SLAPCU_CUDA(cudaEventRecord(e0, c.stream));
+    out.nnz = direct_spgemm(c, A, B, sr, alg, cap, out.cp.as<int64_t>(), out.rw.as<int32_t>(), out.v.get());
+    SLAPCU_CUDA(cudaEventRecord(e1, c.stream));
+    SLAPCU_CUDA(cudaEventSynchronize(e1));
+    float t = 0.f;
+    cudaEventElapsedTime(&t, e0, e1);
+    *ms += t;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+}
+
 // The q-stage SUMMA over a q x q (layer) grid.  `gr_row`/`gr_col` are this
 // rank's group ranks in the row / column communicators (= its column / row
 // coordinate); meta_of(i,j) returns the metadata index of grid rank (i,j).
@@ -221,8 +354,9 @@ void summa_stages(slapcu_comm_s* cm, Ctx& c, ncclComm_t row, ncclComm_t col, int
         b_nc = std::max(b_nc, mb[MB_C]);
         b_nz = std::max(b_nz, mb[MB_NZ]);
     }
-    Slot sa[2], sb[2];
-    const int nslots = q > 1 ? 2 : 1;
+    const bool concat = c.opt.summa_concat && q > 1 && q <= 8;
+    std::vector<Slot> sa(concat ? q : 2), sb(concat ? q : 2);
+    const int nslots = concat ? q : (q > 1 ? 2 : 1);
     for (int k = 0; k < nslots; ++k) {
         sa[k].reserve(c, a_nc, a_nz, vs);
         sb[k].reserve(c, b_nc, b_nz, vs);
@@ -237,8 +371,8 @@ void summa_stages(slapcu_comm_s* cm, Ctx& c, ncclComm_t row, ncclComm_t col, int
     SLAPCU_CUDA(cudaEventRecord(ready, c.stream));
     SLAPCU_CUDA(cudaStreamWaitEvent(cm->comm_stream, ready, 0));
     auto issue = [&](int s) {
-        const int slot = s % 2;
-        if (s >= 2) SLAPCU_CUDA(cudaStreamWaitEvent(cm->comm_stream, slot_free[slot], 0));
+        const int slot = concat ? s : s % 2;
+        if (!concat && s >= 2) SLAPCU_CUDA(cudaStreamWaitEvent(cm->comm_stream, slot_free[slot], 0));
         const int64_t* ma = &meta[kMeta * meta_of(myi, s)];
         const int64_t* mb = &meta[kMeta * meta_of(s, myj)];
         SLAPCU_NCCL(ncclGroupStart());
@@ -249,9 +383,37 @@ void summa_stages(slapcu_comm_s* cm, Ctx& c, ncclComm_t row, ncclComm_t col, int
         SLAPCU_NCCL(ncclGroupEnd());
         SLAPCU_CUDA(cudaEventRecord(bc_done[s], cm->comm_stream));
     };
-    partials.resize(q);
     float local_ms = 0.f, exposed = 0.f;
     Timer w;
+    if (concat) {
+        // every stage's broadcasts are issued at once; the multiply waits for all
+        partials.resize(1);
+        for (int s = 0; s < q; ++s) issue(s);
+        SLAPCU_CUDA(cudaEventRecord(w.a, c.stream));
+        for (int s = 0; s < q; ++s) SLAPCU_CUDA(cudaStreamWaitEvent(c.stream, bc_done[s], 0));
+        SLAPCU_CUDA(cudaEventRecord(w.b, c.stream));
+        SLAPCU_CUDA(cudaEventSynchronize(w.b));
+        exposed = w.ms();
+        for (int s = 0; s < q; ++s) {
+            if (sa_view[s].ncols != sb_view[s].nrows)
+                throw Fail{SLAPCU_ERR_DIM, "SUMMA stage blocks misaligned on the inner dimension"};
+            int64_t f = 0;
+            spgemm_flops(c, sa_view[s], sb_view[s], nullptr, &f);
+            if (st) st->flops += f;
+        }
+        concat_multiply(c, sa_view, sb_view, sr, alg, partials[0], &local_ms);
+        SLAPCU_CUDA(cudaStreamSynchronize(cm->comm_stream));
+        for (auto& e : bc_done) cudaEventDestroy(e);
+        for (auto& e : slot_free) cudaEventDestroy(e);
+        cudaEventDestroy(ready);
+        if (st) {
+            st->ms_local += local_ms;
+            st->ms_exposed_bcast += exposed;
+            st->stages = q;
+        }
+        return;
+    }
+    partials.resize(q);
     if (q > 1) issue(0);
     for (int s = 0; s < q; ++s) {
         if (q > 1 && s + 1 < q) issue(s + 1);  // prefetch the next stage while this one multiplies
@@ -379,7 +541,7 @@ slapcu_status slapcu_summa2d(slapcu_comm cm, const slapcu_csc* A_local, const sl
                      [&](int ii, int jj) { return q > 1 ? ii * (int)q + jj : 0; }, partials, stats);
         Timer mt;
         SLAPCU_CUDA(cudaEventRecord(mt.a, c.stream));
-        if (q == 1) {
+        if (partials.size() == 1) {
             move_out(c, partials[0], C_local);
         } else {
             std::vector<DevCsc> pv;
@@ -447,7 +609,7 @@ slapcu_status slapcu_ca3d(slapcu_comm cm, int layers, const slapcu_csc* A_local,
         // C_int: the layer's merged product (a view; owned by partials[0] or cint_out)
         slapcu_csc_out cint_out{};
         DevCsc ci;
-        if (q == 1) {
+        if (partials.size() == 1) {
             ci = partials[0].view();
         } else {
             std::vector<DevCsc> pv;

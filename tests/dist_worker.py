@@ -35,12 +35,16 @@ def main():
     ap.add_argument("--case", default="summa")
     ap.add_argument("--layers", type=int, default=2)
     ap.add_argument("--scale", type=int, default=11)
+    ap.add_argument("--concat", type=int, default=1, help="SLAPCU_OPT_SUMMA_CONCAT")
     a = ap.parse_args()
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     dist.init_process_group("gloo")
+    from paper_2106_14402_b200 import _lib as L
+
+    P.default_context().set_option(L.OPT_SUMMA_CONCAT, a.concat)
     comm = D.NcclComm()
     port = oracle.port()
     for sr in (P.PlusTimesF64, P.MinPlusI32, P.OrAnd, P.PlusTimesI64):

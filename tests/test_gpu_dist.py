@@ -28,8 +28,9 @@ def test_ca3d_p2_c2():
 
 
 @pytest.mark.skipif(NGPU < 4, reason="needs 4 GPUs")
-def test_summa_p4():
-    run(4, "--case", "summa")
+@pytest.mark.parametrize("concat", [0, 1])
+def test_summa_p4(concat):
+    run(4, "--case", "summa", "--concat", str(concat))
 
 
 @pytest.mark.skipif(NGPU < 4, reason="needs 4 GPUs")
