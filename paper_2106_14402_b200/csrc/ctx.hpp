@@ -153,6 +153,7 @@ struct DirectCache {
     int atpv_tl = -1;
     int ndense = 0, dense_min = -1;
     DevBuf lp, hcnt, hl, items, ifl, sres, soff, units, order, stash, partial, cnt, form, hoff, rbc;
+    DevBuf dist_rw, dist_v;  // SUMMA concatenated product: bound-sized output scratch
     int64_t last_nnz = -1;  // exact nnz(C) of the last call (also on BudgetError)
 };
 

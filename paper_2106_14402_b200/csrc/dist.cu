@@ -320,13 +320,24 @@ void concat_multiply(Ctx& c, const std::vector<DevCsc>& As, const std::vector<De
     out.nrows = M;
     out.ncols = N;
     out.cp.reset(sizeof(int64_t) * (N + 1), c.stream);
-    out.rw.reset(sizeof(int32_t) * std::max<int64_t>(cap, 1), c.stream);
-    out.v.reset(size_t(vs) * std::max<int64_t>(cap, 1), c.stream);
+    // the product lands in a bound-sized scratch kept on the context (no
+    // per-call allocation of ~3x the output), then moves into exact buffers
+    DirectCache& d = c.direct;
+    d.dist_rw.reset(sizeof(int32_t) * std::max<int64_t>(cap, 1), c.stream);
+    d.dist_v.reset(size_t(vs) * std::max<int64_t>(cap, 1), c.stream);
     cudaEvent_t e0, e1;
     SLAPCU_CUDA(cudaEventCreate(&e0));
     SLAPCU_CUDA(cudaEventCreate(&e1));
     SLAPCU_CUDA(cudaEventRecord(e0, c.stream));
-    out.nnz = direct_spgemm(c, A, B, sr, alg, cap, out.cp.as<int64_t>(), out.rw.as<int32_t>(), out.v.get());
+    out.nnz = direct_spgemm(c, A, B, sr, alg, cap, out.cp.as<int64_t>(), d.dist_rw.as<int32_t>(), d.dist_v.get());
+    out.rw.reset(sizeof(int32_t) * std::max<int64_t>(out.nnz, 1), c.stream);
+    out.v.reset(size_t(vs) * std::max<int64_t>(out.nnz, 1), c.stream);
+    if (out.nnz) {
+        SLAPCU_CUDA(cudaMemcpyAsync(out.rw.get(), d.dist_rw.get(), sizeof(int32_t) * out.nnz, cudaMemcpyDeviceToDevice,
+                                    c.stream));
+        SLAPCU_CUDA(cudaMemcpyAsync(out.v.get(), d.dist_v.get(), size_t(vs) * out.nnz, cudaMemcpyDeviceToDevice,
+                                    c.stream));
+    }
     SLAPCU_CUDA(cudaEventRecord(e1, c.stream));
     SLAPCU_CUDA(cudaEventSynchronize(e1));
     float t = 0.f;
