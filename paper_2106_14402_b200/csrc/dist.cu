@@ -347,6 +347,59 @@ void concat_multiply(Ctx& c, const std::vector<DevCsc>& As, const std::vector<De
     cudaEventDestroy(e1);
 }
 
+// Multiplicative identity of each semiring (one ⊗ id = id ⊗ one = value).
+template <int ID>
+typename Sr<ID>::T mul_one() {
+    if constexpr (ID == SLAPCU_MIN_PLUS_I32 || ID == SLAPCU_MIN_PLUS_F64)
+        return typename Sr<ID>::T(0);
+    else
+        return typename Sr<ID>::T(1);
+}
+
+__global__ void k_identity(int64_t n, int64_t* __restrict__ cp, int32_t* __restrict__ rw, char* __restrict__ v,
+                           const char* __restrict__ one, int vsize) {
+    for (int64_t x = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; x <= n; x += int64_t(gridDim.x) * blockDim.x) {
+        cp[x] = x;
+        if (x < n) {
+            rw[x] = (int32_t)x;
+            for (int k = 0; k < vsize; ++k) v[x * vsize + k] = one[k];
+        }
+    }
+}
+
+// C = P0 (+) P1 (+) ... as the product [P0 .. Pq-1] x [I; ..; I] on the direct
+// path (bitmap union per row tile instead of per-entry binary searches).
+// Exact semirings are bit-identical to the stage-order fold; PlusTimes fp64
+// folds in atomic order (north_star tolerance 1e-12).
+void fast_merge(Ctx& c, std::vector<DevCsc> parts, int sr, int alg, slapcu_csc_out* C, float* ms) {
+    const int vs = value_size(sr);
+    for (auto& p : parts) resolve(c, p);
+    const int64_t N = parts[0].ncols;
+    Block id;
+    id.nrows = N;
+    id.ncols = N;
+    id.nnz = N;
+    id.cp.reset(sizeof(int64_t) * (N + 1), c.stream);
+    id.rw.reset(sizeof(int32_t) * std::max<int64_t>(N, 1), c.stream);
+    id.v.reset(size_t(vs) * std::max<int64_t>(N, 1), c.stream);
+    char one[8] = {0};
+    dispatch_sr(sr, [&](auto idc) {
+        constexpr int ID = decltype(idc)::value;
+        const auto o = mul_one<ID>();
+        std::memcpy(one, &o, sizeof(o));
+    });
+    DevBuf done(8, c.stream);
+    SLAPCU_CUDA(cudaMemcpyAsync(done.get(), one, 8, cudaMemcpyHostToDevice, c.stream));
+    launch(c, k_identity, dim3(grid_for(c, N + 1, 256)), dim3(256), 0, N, id.cp.as<int64_t>(), id.rw.as<int32_t>(),
+           static_cast<char*>(id.v.get()), (const char*)done.get(), vs);
+    DevCsc iv = id.view();
+    resolve(c, iv);
+    std::vector<DevCsc> ids(parts.size(), iv);
+    Block out;
+    concat_multiply(c, parts, ids, sr, alg, out, ms);
+    move_out(c, out, C);
+}
+
 // The q-stage SUMMA over a q x q (layer) grid.  `gr_row`/`gr_col` are this
 // rank's group ranks in the row / column communicators (= its column / row
 // coordinate); meta_of(i,j) returns the metadata index of grid rank (i,j).
@@ -364,6 +417,20 @@ void summa_stages(slapcu_comm_s* cm, Ctx& c, ncclComm_t row, ncclComm_t col, int
         a_nz = std::max(a_nz, ma[MA_NZ]);
         b_nc = std::max(b_nc, mb[MB_C]);
         b_nz = std::max(b_nz, mb[MB_NZ]);
+    }
+    if (q == 1 && c.opt.summa_concat) {  // one stage: the local product alone, on the direct path
+        float local_ms = 0.f;
+        if (A.ncols != B.nrows) throw Fail{SLAPCU_ERR_DIM, "SUMMA inner dims disagree"};
+        int64_t f = 0;
+        spgemm_flops(c, A, B, nullptr, &f);
+        if (st) st->flops += f;
+        partials.resize(1);
+        concat_multiply(c, {A}, {B}, sr, alg, partials[0], &local_ms);
+        if (st) {
+            st->ms_local += local_ms;
+            st->stages = 1;
+        }
+        return;
     }
     const bool concat = c.opt.summa_concat && q > 1 && q <= 8;
     std::vector<Slot> sa(concat ? q : 2), sb(concat ? q : 2);
@@ -625,7 +692,11 @@ slapcu_status slapcu_ca3d(slapcu_comm cm, int layers, const slapcu_csc* A_local,
         } else {
             std::vector<DevCsc> pv;
             for (auto& pp : partials) pv.push_back(pp.view());
-            merge_blocks(c, pv, sr, &cint_out);
+            float fm = 0.f;
+            if (c.opt.summa_concat)
+                fast_merge(c, pv, sr, alg, &cint_out, &fm);
+            else
+                merge_blocks(c, pv, sr, &cint_out);
             partials.clear();
             ci = DevCsc{cint_out.nrows, cint_out.ncols, cint_out.nnz, cint_out.colptr, cint_out.rowids, cint_out.vals};
         }
@@ -715,7 +786,11 @@ slapcu_status slapcu_ca3d(slapcu_comm cm, int layers, const slapcu_csc* A_local,
             else
                 pv[k] = pieces[k].view();
         }
-        merge_blocks(c, pv, sr, C_local);
+        float fm = 0.f;
+        if (c.opt.summa_concat)
+            fast_merge(c, pv, sr, alg, C_local, &fm);
+        else
+            merge_blocks(c, pv, sr, C_local);
         SLAPCU_CUDA(cudaEventRecord(mt.b, c.stream));
         SLAPCU_CUDA(cudaEventRecord(total.b, c.stream));
         SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
