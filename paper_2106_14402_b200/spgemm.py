@@ -367,16 +367,17 @@ def symbolic_nnz(a, b, threads: int = 1, alg=SpGemmAlg.hybrid, ctx: Context | No
 
 
 def local_spgemm(a, b, sr: Semiring, alg=SpGemmAlg.hybrid, threads: int = 1, ctx: Context | None = None,
-                 method: str = "fused"):
+                 method: str = "direct"):
     """spgemm.hpp:275-330 local_spgemm.  Returns a DeviceCsc for device
     operands and a host CscMatrix for host operands (the host call runs the
     H2D copies, the three GPU phases and the D2H copies inside the library).
 
-    method "fused" (default) forms each column once (slapcu_spgemm_begin /
+    method "direct" (default) writes C in place in one product pass
+    (slapcu_spgemm_direct) into buffers sized by the bound
+    sum_j min(flops_j, A.nrows), then trims them.
+    method "fused" forms each column once (slapcu_spgemm_begin /
     _finish) and falls back to "two_pass" (slapcu_spgemm_symbolic / _numeric)
-    when its staging area would not fit in half the free device memory.
-    method "direct" writes C in place in one pass (slapcu_spgemm_direct) into
-    buffers sized by the bound sum_j min(flops_j, A.nrows)."""
+    when its staging area would not fit in half the free device memory."""
     sr = _sr(sr)
     alg = SpGemmAlg(int(alg))
     ctx = _ctx(ctx)
