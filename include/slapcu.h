@@ -132,10 +132,14 @@ typedef enum {
     SLAPCU_OPT_DIRECT_VALUE_TILE_ROWS_LOG2 = 17, /* direct path value pass: rows per shared value array
                                                     (12..15, default 14) */
     SLAPCU_OPT_DIRECT_VALUE_THREADS = 18,  /* direct path value pass: threads per CTA (256, 512) */
-    SLAPCU_OPT_SUMMA_CONCAT = 19           /* SUMMA / 3D layers: 1 (default) = all stage blocks are
+    SLAPCU_OPT_SUMMA_CONCAT = 19,          /* SUMMA / 3D layers: 1 (default) = all stage blocks are
                                               broadcast, then ONE concatenated-k product forms C(i,j)
                                               (no stage partials, no merge); 0 = per-stage products
                                               double-buffered against the broadcasts + stage merge */
+    SLAPCU_OPT_DIRECT_VALUE_HASH = 20      /* direct path value pass: 1 (default, = 13) / 13 / 14 = items
+                                              with <= 2^(v-1) outputs take one walk into a shared hash
+                                              table of 2^v slots keyed by their rows; 0 = every item
+                                              takes the row sub-tile pass */
 } slapcu_option;
 slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t value);
 

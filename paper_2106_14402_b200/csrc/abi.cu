@@ -139,7 +139,7 @@ slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t v
             break;
         case SLAPCU_OPT_LIGHT_NNZ_MAX: c.opt.light_nnz_max = v; break;
         case SLAPCU_OPT_DIRECT_TILE_ROWS_LOG2:
-            require(v >= 10 && v <= 18, SLAPCU_ERR_INVALID, "direct tile rows log2 must be in 10..18");
+            require(v == 0 || (v >= 10 && v <= 18), SLAPCU_ERR_INVALID, "direct tile rows log2: 0 (auto) or 10..18");
             c.opt.direct_tile_rows_log2 = (int)v;
             break;
         case SLAPCU_OPT_DIRECT_MARK_MODE:
@@ -153,6 +153,10 @@ slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t v
             c.opt.direct_value_tile_log2 = (int)v;
             break;
         case SLAPCU_OPT_SUMMA_CONCAT: c.opt.summa_concat = v != 0; break;
+        case SLAPCU_OPT_DIRECT_VALUE_HASH:
+            require(v == 0 || v == 1 || v == 13 || v == 14, SLAPCU_ERR_INVALID, "value hash: 0, 1, 13 or 14");
+            c.opt.direct_value_hash = (int)v;
+            break;
         case SLAPCU_OPT_DIRECT_VALUE_THREADS:
             require(v == 256 || v == 512, SLAPCU_ERR_INVALID, "value threads: 256 or 512");
             c.opt.direct_value_threads = (int)v;

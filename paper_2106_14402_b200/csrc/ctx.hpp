@@ -121,16 +121,17 @@ struct Options {
     int64_t dense_flops_min = 0;
     int dense_tile_rows_log2 = 17;    // byte-flag tile height (128 KB of flags)
     bool async_finish = false;        // finish() returns without waiting (errors surface later)
-    int direct_tile_rows_log2 = 17;   // direct path: row-tile height of an item (16 KB bitmap)
+    int direct_tile_rows_log2 = 0;    // direct path: row-tile height of an item (0 = auto: 17, 18 above 2^20 rows)
     int64_t direct_light_flops_max = 1024;  // direct path: hash path for columns up to this many flops
     int64_t direct_dense_run_min = 2048;    // direct path: A runs (column x tile) this long are OR-ed
                                             // as precomputed tile bitmaps (0 = never)
     int direct_mark_mode = 0;               // product update: 0 test+set, 1 atomic only, 2 quad-merged
     int direct_quads = 0;
-    int direct_value_tile_log2 = 14;        // direct path value pass: rows per shared value array
+    int direct_value_tile_log2 = 13;        // direct path value pass: rows per shared value array
     int direct_values_fallback = 0;
     int summa_concat = 1;                   // SUMMA: one concatenated-k product per call (no stage merge)
-    int direct_value_threads = 256;         // CTA size of the value pass (256, 512)         // 1: value semirings use begin/finish instead                   // direct path: lane-contiguous quads merged per word
+    int direct_value_threads = 256;
+    int direct_value_hash = 1;              // value pass: small items through the one-walk hash kernel         // CTA size of the value pass (256, 512)         // 1: value semirings use begin/finish instead                   // direct path: lane-contiguous quads merged per word
     int direct_persistent = 1;              // form kernel: persistent CTAs (1) or one CTA per unit (0)
     int direct_form_threads = 256;          // CTA size of the form kernel (128, 256, 512)
     int direct_emit_threads = 128;          // CTA size of the emit kernel (128, 256)

@@ -680,7 +680,10 @@ struct ValueArgs {
     DevCsc A, B;
     const int32_t* Atpv;  // A tile pointers at 2^VTL rows
     int Tv, VTL, TL;
+    const int32_t* Atp;   // A tile pointers at 2^TL rows (the items' tiles)
+    int T;
     const int2* items;
+    const int* list;      // the items this launch handles
     const int64_t* cnt;
     const int64_t* hoff;
     const int64_t* lp;
@@ -690,26 +693,166 @@ struct ValueArgs {
 };
 
 template <int SRID, int NT>
+struct ValueWalkSm {
+    using T = typename Sr<SRID>::T;
+    int wsum[NT / 32 + 1], wsum2[NT / 32 + 1];
+    int ustart[NT + 1];
+    int ulen[NT];
+    int64_t ustartp[NT];
+    T ubval[NT];
+    int sp[NT + 1];  // packed short runs: product prefix per B entry
+    int64_t sst[NT];
+    T sbv[NT];
+    int nlong;
+};
+
+// Every product of B(:,j) whose A row lies in tile `t` of the pointer table
+// `tp0` (T+1 entries per A column) is folded into *slot(row) with the
+// semiring's atomic.  Runs of >= 32 products are cut into 256-product warp
+// units; shorter runs are packed 32 products per warp step (the owning B
+// entry found by a search over the batch's product prefix), so no thread
+// walks a run alone through a chain of dependent loads.
+template <int SRID, int NT, class Slot>
+__device__ __forceinline__ void value_walk(const DevCsc& A, const DevCsc& B, const int32_t* __restrict__ Atab, int T,
+                                           int t, int j, ValueWalkSm<SRID, NT>& sh, Slot slot) {
+    using S_ = Sr<SRID>;
+    using T_ = typename S_::T;
+    constexpr int NW = NT / 32;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const T_* Av = static_cast<const T_*>(A.v);
+    const T_* Bv = static_cast<const T_*>(B.v);
+    const int32_t* __restrict__ Arw = A.rw;
+    const int64_t bs = B.cp[j], be = B.cp[j + 1];
+    for (int64_t base = bs; base < be; base += NT) {
+        const int64_t i = base + tid;
+        int slen = 0;
+        if (i < be) {
+            const int k = B.rw[i];
+            const int32_t* tp = Atab + int64_t(k) * (T + 1) + t;
+            const int rlo = tp[0], rhi = tp[1];
+            const int len = rhi - rlo;
+            if (len > 0) {
+                const int64_t st = A.cp[k] + rlo;
+                const T_ bv = Bv[i];
+                if (len < 32) {
+                    slen = len;
+                    sh.sst[tid] = st;
+                    sh.sbv[tid] = bv;
+                } else {
+                    const unsigned peers = __activemask();
+                    const int leader = __ffs(peers) - 1;
+                    int pos = 0;
+                    if (lane == leader) pos = atomicAdd(&sh.nlong, __popc(peers));
+                    pos = __shfl_sync(peers, pos, leader) + __popc(peers & ((1u << lane) - 1u));
+                    sh.ulen[pos] = len;
+                    sh.ustartp[pos] = st;
+                    sh.ubval[pos] = bv;
+                }
+            }
+        }
+        __syncthreads();
+        const int nl = sh.nlong;
+        const int units = tid < nl ? (sh.ulen[tid] + 255) / 256 : 0;
+        int tot, stot;
+        {
+            int wt, wt2;
+            const int ex = warp_excl_scan(units, lane, &wt);
+            const int ex2 = warp_excl_scan(slen, lane, &wt2);
+            if (lane == 0) {
+                sh.wsum[warp] = wt;
+                sh.wsum2[warp] = wt2;
+            }
+            __syncthreads();
+            if (warp == 0) {
+                const int x = lane < NW ? sh.wsum[lane] : 0, y = lane < NW ? sh.wsum2[lane] : 0;
+                int t1, t2;
+                const int e1 = warp_excl_scan(x, lane, &t1), e2 = warp_excl_scan(y, lane, &t2);
+                if (lane < NW) {
+                    sh.wsum[lane] = e1;
+                    sh.wsum2[lane] = e2;
+                }
+                if (lane == 0) {
+                    sh.wsum[NW] = t1;
+                    sh.wsum2[NW] = t2;
+                }
+            }
+            __syncthreads();
+            sh.ustart[tid] = ex + sh.wsum[warp];
+            sh.sp[tid] = ex2 + sh.wsum2[warp];
+            tot = sh.wsum[NW];
+            stot = sh.wsum2[NW];
+            if (tid == 0) {
+                sh.ustart[nl] = tot;
+                sh.sp[NT] = stot;
+            }
+        }
+        __syncthreads();
+        for (int o0 = warp * 32; o0 < stot; o0 += NT) {
+            const int o = o0 + lane;
+            if (o < stot) {
+                int a = 0, b = NT - 1;
+                while (a < b) {
+                    const int mid = (a + b + 1) >> 1;
+                    if (sh.sp[mid] <= o)
+                        a = mid;
+                    else
+                        b = mid - 1;
+                }
+                const int64_t p = sh.sst[a] + (o - sh.sp[a]);
+                S_::atomic_acc(slot(__ldg(&Arw[p])), S_::mul(Av[p], sh.sbv[a]));
+            }
+        }
+        const int u0 = (int)((int64_t(tot) * warp) / NW), u1 = (int)((int64_t(tot) * (warp + 1)) / NW);
+        int e = 0;
+        if (u0 < u1) {
+            int a = 0, b = nl - 1;
+            while (a < b) {
+                const int mid = (a + b + 1) >> 1;
+                if (sh.ustart[mid] <= u0)
+                    a = mid;
+                else
+                    b = mid - 1;
+            }
+            e = a;
+        }
+        for (int u = u0; u < u1; ++u) {
+            if (sh.ustart[e + 1] <= u) ++e;
+            const int c0 = (u - sh.ustart[e]) * 256;
+            const int64_t p0 = sh.ustartp[e] + c0;
+            const int m = min(256, sh.ulen[e] - c0);
+            const T_ bv = sh.ubval[e];
+            for (int x = lane; x < m; x += 64) {
+                const int r0 = __ldg(&Arw[p0 + x]);
+                const T_ a0 = Av[p0 + x];
+                const bool two = x + 32 < m;
+                const int r1 = two ? __ldg(&Arw[p0 + x + 32]) : 0;
+                const T_ a1 = two ? Av[p0 + x + 32] : a0;
+                S_::atomic_acc(slot(r0), S_::mul(a0, bv));
+                if (two) S_::atomic_acc(slot(r1), S_::mul(a1, bv));
+            }
+        }
+        __syncthreads();
+        if (tid == 0) sh.nlong = 0;
+        __syncthreads();
+    }
+}
+
+// Values of the large items: one CTA per (item, sub-tile of 2^VTL rows) with
+// a dense shared value array indexed by row.  The sub-tile's output entries
+// are a contiguous range of C (from the item's row-block counts); products
+// only land on those rows, so only they are initialised.
+template <int SRID, int NT>
 __global__ void __launch_bounds__(NT) k_tile_values(ValueArgs g) {
     using S_ = Sr<SRID>;
     using T = typename S_::T;
     using Acc = typename S_::Acc;
-    constexpr int NW = NT / 32;
     extern __shared__ __align__(16) unsigned char sm_raw[];
     Acc* val = reinterpret_cast<Acc*>(sm_raw);
-    __shared__ int wsum[NW + 1];
-    __shared__ int ustart[NT + 1];
-    __shared__ int ulen[NT];
-    __shared__ int64_t ustartp[NT];
-    __shared__ T ubval[NT];
-    __shared__ int sp[NT + 1];       // packed short runs: product prefix per B entry
-    __shared__ int64_t sst[NT];
-    __shared__ T sbv[NT];
-    __shared__ int nlong;
+    __shared__ ValueWalkSm<SRID, NT> sh;
     __shared__ int64_t range_sh[2];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nsub = 1 << (g.TL - g.VTL);
-    const int item = blockIdx.x / nsub, s = blockIdx.x % nsub;
+    const int item = g.list[blockIdx.x / nsub], s = blockIdx.x % nsub;
     const int2 it = g.items[item];
     const int j = it.x;
     const int ts = (it.y << (g.TL - g.VTL)) + s;
@@ -731,133 +874,68 @@ __global__ void __launch_bounds__(NT) k_tile_values(ValueArgs g) {
             const int64_t off = g.lp[j] + g.hoff[item];
             range_sh[0] = off + before;
             range_sh[1] = off + before + inside;
-            nlong = 0;
+            sh.nlong = 0;
         }
     }
     __syncthreads();
     const int64_t lo = range_sh[0], hi = range_sh[1];
     if (lo == hi) return;
-    // products only land on output rows: initialise just those slots
     for (int64_t q = lo + tid; q < hi; q += NT) val[g.crw[q] - s0] = S_::identity();
-    const T* Av = static_cast<const T*>(g.A.v);
-    const T* Bv = static_cast<const T*>(g.B.v);
+    __syncthreads();
+    value_walk<SRID, NT>(g.A, g.B, g.Atpv, g.Tv, ts, j, sh, [val, s0](int r) { return &val[r - s0]; });
     T* Cv = static_cast<T*>(g.cv);
-    const int32_t* __restrict__ Arw = g.A.rw;
-    const int64_t bs = g.B.cp[j], be = g.B.cp[j + 1];
-    for (int64_t base = bs; base < be; base += NT) {
-        const int64_t i = base + tid;
-        int slen = 0;
-        if (i < be) {
-            const int k = g.B.rw[i];
-            const int32_t* tp = g.Atpv + int64_t(k) * (g.Tv + 1) + ts;
-            const int rlo = tp[0], rhi = tp[1];
-            const int len = rhi - rlo;
-            if (len > 0) {
-                const int64_t st = g.A.cp[k] + rlo;
-                const T bv = Bv[i];
-                if (len < 32) {
-                    slen = len;
-                    sst[tid] = st;
-                    sbv[tid] = bv;
-                } else {
-                    const unsigned peers = __activemask();
-                    const int leader = __ffs(peers) - 1;
-                    int pos = 0;
-                    if (lane == leader) pos = atomicAdd(&nlong, __popc(peers));
-                    pos = __shfl_sync(peers, pos, leader) + __popc(peers & ((1u << lane) - 1u));
-                    ulen[pos] = len;
-                    ustartp[pos] = st;
-                    ubval[pos] = bv;
-                }
-            }
-        }
-        __syncthreads();  // (also makes every thread's shared state visible, in this step's order)
-        const int nl = nlong;
-        const int units = tid < nl ? (ulen[tid] + 255) / 256 : 0;
-        int tot, stot;
-        {
-            // two block scans at once: long-run units and short-run products
-            int wt, wt2;
-            const int ex = warp_excl_scan(units, lane, &wt);
-            const int ex2 = warp_excl_scan(slen, lane, &wt2);
-            if (lane == 0) wsum[warp] = wt;
-            __shared__ int wsum2[NW + 1];
-            if (lane == 0) wsum2[warp] = wt2;
-            __syncthreads();
-            if (warp == 0) {
-                const int x = lane < NW ? wsum[lane] : 0, y = lane < NW ? wsum2[lane] : 0;
-                int t1, t2;
-                const int e1 = warp_excl_scan(x, lane, &t1), e2 = warp_excl_scan(y, lane, &t2);
-                if (lane < NW) {
-                    wsum[lane] = e1;
-                    wsum2[lane] = e2;
-                }
-                if (lane == 0) {
-                    wsum[NW] = t1;
-                    wsum2[NW] = t2;
-                }
-            }
-            __syncthreads();
-            ustart[tid] = ex + wsum[warp];
-            sp[tid] = ex2 + wsum2[warp];
-            tot = wsum[NW];
-            stot = wsum2[NW];
-            if (tid == 0) {
-                ustart[nl] = tot;
-                sp[NT] = stot;
-            }
-        }
-        __syncthreads();
-        // short runs packed 32 products per warp step: entry of product o by search
-        for (int o0 = warp * 32; o0 < stot; o0 += NT) {
-            const int o = o0 + lane;
-            if (o < stot) {
-                int a = 0, b = NT - 1;
-                while (a < b) {
-                    const int mid = (a + b + 1) >> 1;
-                    if (sp[mid] <= o)
-                        a = mid;
-                    else
-                        b = mid - 1;
-                }
-                const int64_t p = sst[a] + (o - sp[a]);
-                S_::atomic_acc(&val[__ldg(&Arw[p]) - s0], S_::mul(Av[p], sbv[a]));
-            }
-        }
-        const int u0 = (int)((int64_t(tot) * warp) / NW), u1 = (int)((int64_t(tot) * (warp + 1)) / NW);
-        int e = 0;
-        if (u0 < u1) {
-            int a = 0, b = nl - 1;
-            while (a < b) {
-                const int mid = (a + b + 1) >> 1;
-                if (ustart[mid] <= u0)
-                    a = mid;
-                else
-                    b = mid - 1;
-            }
-            e = a;
-        }
-        for (int u = u0; u < u1; ++u) {
-            if (ustart[e + 1] <= u) ++e;
-            const int c0 = (u - ustart[e]) * 256;
-            const int64_t p0 = ustartp[e] + c0;
-            const int m = min(256, ulen[e] - c0);
-            const T bv = ubval[e];
-            for (int x = lane; x < m; x += 64) {
-                const int r0 = __ldg(&Arw[p0 + x]);
-                const T a0 = Av[p0 + x];
-                const bool two = x + 32 < m;
-                const int r1 = two ? __ldg(&Arw[p0 + x + 32]) : 0;
-                const T a1 = two ? Av[p0 + x + 32] : a0;
-                S_::atomic_acc(&val[r0 - s0], S_::mul(a0, bv));
-                if (two) S_::atomic_acc(&val[r1 - s0], S_::mul(a1, bv));
-            }
-        }
-        __syncthreads();
-        if (tid == 0) nlong = 0;
-        __syncthreads();
-    }
     for (int64_t q = lo + tid; q < hi; q += NT) Cv[q] = S_::out(val[g.crw[q] - s0]);
+}
+
+// Values of the small items (at most HS/2 output entries): one CTA per item,
+// one walk over its products, values in a shared open-addressing table keyed
+// by the item's output rows (built first from C's rows, so a product only
+// probes -- it never inserts).
+template <int SRID, int NT, int LOG2HS>
+__global__ void __launch_bounds__(NT) k_item_values_hash(ValueArgs g) {
+    using S_ = Sr<SRID>;
+    using T = typename S_::T;
+    using Acc = typename S_::Acc;
+    constexpr int HS = 1 << LOG2HS;
+    extern __shared__ __align__(16) unsigned char sm_raw[];
+    Acc* val = reinterpret_cast<Acc*>(sm_raw);
+    int* key = reinterpret_cast<int*>(sm_raw + sizeof(Acc) * HS);
+    __shared__ ValueWalkSm<SRID, NT> sh;
+    const int tid = threadIdx.x;
+    const int item = g.list[blockIdx.x];
+    const int2 it = g.items[item];
+    const int j = it.x;
+    const int64_t off = g.lp[j] + g.hoff[item];
+    const int64_t c = g.cnt[item];
+    for (int q = tid; q < HS; q += NT) key[q] = -1;
+    if (tid == 0) sh.nlong = 0;
+    __syncthreads();
+    auto home = [](int r) { return (int)(((unsigned)r * 0x9E3779B1u) >> (32 - LOG2HS)); };
+    for (int64_t q = tid; q < c; q += NT) {
+        const int r = g.crw[off + q];
+        int h = home(r);
+        while (atomicCAS(&key[h], -1, r) != -1) h = (h + 1) & (HS - 1);
+        val[h] = S_::identity();
+    }
+    __syncthreads();
+    auto slot = [key, val, home](int r) {
+        int h = home(r);
+        while (key[h] != r) h = (h + 1) & (HS - 1);
+        return &val[h];
+    };
+    value_walk<SRID, NT>(g.A, g.B, g.Atp, g.T, it.y, j, sh, slot);
+    T* Cv = static_cast<T*>(g.cv);
+    for (int64_t q = tid; q < c; q += NT) Cv[off + q] = S_::out(*slot(g.crw[off + q]));
+}
+
+__global__ void k_value_split(int nitems, const int64_t* __restrict__ cnt, int64_t hcap, int* __restrict__ small,
+                              int* __restrict__ large, int* __restrict__ counts) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nitems; i += gridDim.x * blockDim.x) {
+        if (cnt[i] <= hcap)
+            small[atomicAdd(&counts[0], 1)] = i;
+        else
+            large[atomicAdd(&counts[1], 1)] = i;
+    }
 }
 
 // ------------------------------------------------------------ item setup
@@ -1115,7 +1193,9 @@ constexpr int kMaxParts = 64;
 }  // namespace
 
 int direct_tile_log2(const Ctx& c, int64_t nrows) {
-    int tl = c.opt.direct_tile_rows_log2;
+    // auto: 2^17-row tiles up to 2^20 rows, 2^18 above (fewer items walking
+    // the same B columns when rows are many and columns sparse)
+    int tl = c.opt.direct_tile_rows_log2 > 0 ? c.opt.direct_tile_rows_log2 : (nrows > (int64_t(1) << 20) ? 18 : 17);
     while (tl > 10 && (int64_t(1) << (tl - 1)) >= nrows) --tl;
     return tl;
 }
@@ -1441,23 +1521,51 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
         const int VTL = std::min(TL, std::max(12, c.opt.direct_value_tile_log2));
         const int Tv = (int)((A.nrows + (int64_t(1) << VTL) - 1) >> VTL);
         const int32_t* Atpv = value_tile_pointers(c, A, VTL, Tv);
-        const ValueArgs va{A, B, Atpv, Tv, VTL, TL, (const int2*)d.items.as<int2>(),
-                           (const int64_t*)d.cnt.as<int64_t>(), (const int64_t*)d.hoff.as<int64_t>(),
-                           (const int64_t*)d.lp.as<int64_t>(), (const int*)d.rbc.as<int>(), crw, cv};
+        const int32_t* Atp = tile_pointers(c, A, TL, T);
+        // small items (<= kHashCap outputs) take the one-walk hash kernel
+        const int hlog2 = c.opt.direct_value_hash >= 14 ? 14 : 13;  // table slots (load <= 1/2)
+        const int64_t hcap = c.opt.direct_value_hash ? (int64_t(1) << hlog2) / 2 : -1;
+        DevBuf lists(sizeof(int) * (2 * size_t(nitems) + 2), c.stream), lc(sizeof(int) * 2, c.stream);
+        SLAPCU_CUDA(cudaMemsetAsync(lc.get(), 0, sizeof(int) * 2, c.stream));
+        int* small = lists.as<int>();
+        int* large = small + nitems;
+        launch(c, k_value_split, dim3(grid_for(c, nitems, 256)), dim3(256), 0, nitems,
+               (const int64_t*)d.cnt.as<int64_t>(), hcap, small, large, lc.as<int>());
+        int nsl[2];
+        SLAPCU_CUDA(cudaMemcpyAsync(nsl, lc.get(), sizeof(nsl), cudaMemcpyDeviceToHost, c.stream));
+        SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+        ValueArgs va{A, B, Atpv, Tv, VTL, TL, Atp, T, (const int2*)d.items.as<int2>(), nullptr,
+                     (const int64_t*)d.cnt.as<int64_t>(), (const int64_t*)d.hoff.as<int64_t>(),
+                     (const int64_t*)d.lp.as<int64_t>(), (const int*)d.rbc.as<int>(), crw, cv};
         dispatch_sr(sr, [&](auto id) {
             constexpr int ID = decltype(id)::value;
             using Acc = typename Sr<ID>::Acc;
-            const size_t smem = sizeof(Acc) * (size_t(1) << VTL);
-            if (smem > size_t(c.smem_optin) - 16 * 1024)
-                throw Fail{SLAPCU_ERR_INVALID, "value tile too large for shared memory"};
-            auto go = [&](auto k, int nt) {
-                ensure_smem(k, smem);
-                launch(c, k, dim3((unsigned)(int64_t(nitems) << (TL - VTL))), dim3(nt), smem, va);
-            };
-            if (c.opt.direct_value_threads == 512)
-                go(k_tile_values<ID, 512>, 512);
-            else
-                go(k_tile_values<ID, 256>, 256);
+            if (nsl[0] > 0) {
+                va.list = small;
+                const size_t smem = (sizeof(Acc) + sizeof(int)) << hlog2;
+                auto go = [&](auto k) {
+                    ensure_smem(k, smem);
+                    launch(c, k, dim3(nsl[0]), dim3(256), smem, va);
+                };
+                if (hlog2 == 14)
+                    go(k_item_values_hash<ID, 256, 14>);
+                else
+                    go(k_item_values_hash<ID, 256, 13>);
+            }
+            if (nsl[1] > 0) {
+                va.list = large;
+                const size_t smem = sizeof(Acc) * (size_t(1) << VTL);
+                if (smem > size_t(c.smem_optin) - 16 * 1024)
+                    throw Fail{SLAPCU_ERR_INVALID, "value tile too large for shared memory"};
+                auto go = [&](auto k, int nt) {
+                    ensure_smem(k, smem);
+                    launch(c, k, dim3((unsigned)(int64_t(nsl[1]) << (TL - VTL))), dim3(nt), smem, va);
+                };
+                if (c.opt.direct_value_threads == 512)
+                    go(k_tile_values<ID, 512>, 512);
+                else
+                    go(k_tile_values<ID, 256>, 256);
+            }
         });
     }
     if (nlight) {

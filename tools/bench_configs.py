@@ -45,6 +45,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--cpu-cols", type=int, default=256)
+    ap.add_argument("--method", default="direct", choices=["direct", "fused", "two_pass"])
     args = ap.parse_args()
     torch.cuda.set_device(0)
     stream = torch.cuda.current_stream()
@@ -53,16 +54,16 @@ def main():
     for name in args.configs.split(","):
         desc, A, B, sr = workload(name, ctx)
         flops, _ = P.estimate_flops(A, B, ctx=ctx)
-        C = P.local_spgemm(A, B, sr, ctx=ctx)
+        C = P.local_spgemm(A, B, sr, ctx=ctx, method=args.method)
         nnz = C.nnz
         del C
         for _ in range(args.warmup):
-            P.local_spgemm(A, B, sr, ctx=ctx)
+            P.local_spgemm(A, B, sr, ctx=ctx, method=args.method)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.steps):
-            P.local_spgemm(A, B, sr, ctx=ctx)
+            P.local_spgemm(A, B, sr, ctx=ctx, method=args.method)
         e1.record(stream)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / args.steps
@@ -72,7 +73,7 @@ def main():
         ha, hb = A.to_host(), B.to_host()
         oa = oracle.Csc(ha.nrows, ha.ncols, ha.colptr, ha.rowids, ha.vals)
         ob = oracle.Csc(hb.nrows, hb.ncols, hb.colptr, hb.rowids, hb.vals)
-        gpu_slice = P.local_spgemm(A, BT.column_window(B, c0, c0 + w), sr, ctx=ctx).to_host()
+        gpu_slice = P.local_spgemm(A, BT.column_window(B, c0, c0 + w), sr, ctx=ctx, method=args.method).to_host()
         secs, ref_nnz, ref_fl = oracle.ref().time_local_spgemm(sr.id, oa, ob, c0, c0 + w, threads)
         want = oracle.port().spgemm(sr.id, oa, ob, c0, c0 + w)
         same_pattern = bool(np.array_equal(gpu_slice.colptr, want.colptr) and
