@@ -1014,13 +1014,15 @@ __global__ void __launch_bounds__(NT)
 // Per heavy column (column order) and tile: multiplies, and the number of
 // tiles with work.  One warp per column, 8 tiles per pass over B(:,j).
 __global__ void k_item_flops(DevCsc B, const int32_t* __restrict__ Atp, int T, const int* __restrict__ hl, int nh,
-                             int64_t* __restrict__ iflops, int64_t* __restrict__ nit) {
+                             const int64_t* __restrict__ flops, int64_t* __restrict__ iflops,
+                             int64_t* __restrict__ nit) {
     const int lane = threadIdx.x & 31;
     const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
     for (int64_t h = w0; h < nh; h += nw) {
         const int j = hl[h];
         const int64_t bs = B.cp[j], be = B.cp[j + 1];
+        const bool small = flops[j] < (int64_t(1) << 31);  // 32-bit sums: one redux per tile
         int64_t items = 0;
         for (int tb = 0; tb < T; tb += 8) {
             long long f[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -1040,9 +1042,10 @@ __global__ void k_item_flops(DevCsc B, const int32_t* __restrict__ Atp, int T, c
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
                 if (q < nt) {
-                    const long long s = warp_reduce_sum64(f[q]);
-                    if (lane == 0) iflops[h * T + tb + q] = s;
-                    items += s > 0;
+                    const long long sum =
+                        small ? (long long)__reduce_add_sync(0xffffffffu, (unsigned)f[q]) : warp_reduce_sum64(f[q]);
+                    if (lane == 0) iflops[h * T + tb + q] = sum;
+                    items += sum > 0;
                 }
             }
         }
@@ -1364,7 +1367,7 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
         DevBuf nit(sizeof(int64_t) * (nh + 1), c.stream), ioff(sizeof(int64_t) * (nh + 1), c.stream);
         SLAPCU_CUDA(cudaMemsetAsync(nit.as<int64_t>() + nh, 0, sizeof(int64_t), c.stream));
         launch(c, k_item_flops, dim3(grid_for(c, int64_t(nh) * 32, 256)), dim3(256), 0, B, Atp, T,
-               (const int*)d.hl.as<int>(), nh, iflops.as<int64_t>(), nit.as<int64_t>());
+               (const int*)d.hl.as<int>(), nh, flops, iflops.as<int64_t>(), nit.as<int64_t>());
         exclusive_scan_i64(c, nit.as<int64_t>(), ioff.as<int64_t>(), nh + 1);
         const int64_t nitems64 = d2h(c, ioff.as<int64_t>() + nh);
         if (nitems64 > INT32_MAX) throw Fail{SLAPCU_ERR_INVALID, "too many tile items"};
