@@ -120,7 +120,8 @@ typedef enum {
                                               1 shared atomic per product, 2 lane-contiguous quads merged
                                               per 32-row word before the update */
     SLAPCU_OPT_DIRECT_FORM_THREADS = 12,   /* direct path: threads per form CTA (128, 256, 512) */
-    SLAPCU_OPT_DIRECT_EMIT_THREADS = 13,   /* direct path: threads per emit CTA (128, 256) */
+    SLAPCU_OPT_DIRECT_EMIT_THREADS = 13,   /* direct path emit granularity: 128 (default) = one 4-warp
+                                              CTA per item; 32 = one warp per (item, 128-word block) */
     SLAPCU_OPT_DIRECT_DENSE_RUN_MIN = 14,  /* direct path: A(:,k) runs inside one row tile with at least
                                               this many entries are OR-ed as cached tile bitmaps
                                               (default 2048, 0 = never) */

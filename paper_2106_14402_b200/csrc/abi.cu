@@ -166,8 +166,9 @@ slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t v
             c.opt.direct_form_threads = (int)v;
             break;
         case SLAPCU_OPT_DIRECT_EMIT_THREADS:
-            require(v == 128 || v == 256, SLAPCU_ERR_INVALID, "emit threads: 128 or 256");
-            c.opt.direct_emit_threads = (int)v;
+            // 0: one CTA per item; 32: one warp per (item, 128-word block) (default)
+            require(v == 0 || v == 32 || v == 128, SLAPCU_ERR_INVALID, "emit mode: 0/128 (CTA per item) or 32 (warp per block)");
+            c.opt.direct_emit_blocks = v == 32;
             break;
         case SLAPCU_OPT_DIRECT_DENSE_RUN_MIN:
             require(v >= 0, SLAPCU_ERR_INVALID, "dense run threshold must be >= 0");

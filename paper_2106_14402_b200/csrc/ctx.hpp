@@ -131,7 +131,8 @@ struct Options {
     int direct_values_fallback = 0;
     int summa_concat = 1;                   // SUMMA: one concatenated-k product per call (no stage merge)
     int direct_value_threads = 256;
-    int direct_value_hash = 1;              // value pass: small items through the one-walk hash kernel         // CTA size of the value pass (256, 512)         // 1: value semirings use begin/finish instead                   // direct path: lane-contiguous quads merged per word
+    int direct_value_hash = 1;
+    int direct_emit_blocks = 0;             // emit: one warp per (item, block) (1) or one CTA per item (0)              // value pass: small items through the one-walk hash kernel         // CTA size of the value pass (256, 512)         // 1: value semirings use begin/finish instead                   // direct path: lane-contiguous quads merged per word
     int direct_persistent = 1;              // form kernel: persistent CTAs (1) or one CTA per unit (0)
     int direct_form_threads = 256;          // CTA size of the form kernel (128, 256, 512)
     int direct_emit_threads = 128;          // CTA size of the emit kernel (128, 256)
@@ -155,6 +156,7 @@ struct DirectCache {
     int ndense = 0, dense_min = -1;
     DevBuf lp, hcnt, hl, items, ifl, sres, soff, units, order, stash, partial, cnt, form, hoff, rbc;
     DevBuf dist_rw, dist_v;  // SUMMA concatenated product: bound-sized output scratch
+    DevBuf eblocks;          // emit work list: (item, block) pairs
     int64_t last_nnz = -1;  // exact nnz(C) of the last call (also on BudgetError)
 };
 

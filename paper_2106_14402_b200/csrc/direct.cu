@@ -665,6 +665,79 @@ __global__ void __launch_bounds__(NT) k_tile_emit(EmitArgs g) {
     }
 }
 
+// Block-granular emission: one warp per (item, 128-word block) pair from a
+// flat list, so small items (one block) do not leave a CTA's other warps
+// idle.  The block's output base is the item's offset plus the header
+// counts of the blocks before it.
+__global__ void __launch_bounds__(128) k_tile_emit_blocks(EmitArgs g, const int2* __restrict__ blocks, int64_t nblocks) {
+    __shared__ EmitWarp wsm[4];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t bi = int64_t(blockIdx.x) * 4 + warp;
+    if (bi >= nblocks) return;
+    const int2 ib = blocks[bi];
+    const int item = ib.x, b = ib.y;
+    const int2 it = g.items[item];
+    const int U = g.form[item];
+    const int W = 1 << (g.TL - 5);
+    const int nwords = U >= 0 ? U : W;
+    const unsigned* hdr = g.stash + g.soff[item];
+    const unsigned* words = hdr + stash_header_words(W);
+    const uint16_t* idx = U >= 0 ? reinterpret_cast<const uint16_t*>(words + U) : nullptr;
+    const int t0 = it.y << g.TL;
+    // this block's words (4 per lane) and the item's header prefix up to b
+    unsigned xs[kEmitWPL];
+    int cnt = 0, nz = 0;
+#pragma unroll
+    for (int q = 0; q < kEmitWPL; ++q) {
+        const int w = b * kEmitBlock + lane * kEmitWPL + q;
+        xs[q] = w < nwords ? words[w] : 0u;
+        cnt += __popc(xs[q]);
+        nz += xs[q] != 0u;
+    }
+    int before = 0;
+    for (int k = lane; k < b; k += 32) before += (int)hdr[k];
+    before = warp_reduce_sum(before);
+    const int E = __reduce_add_sync(0xffffffffu, (unsigned)cnt);
+    if (!E) return;
+    const int64_t off = g.lp[it.x] + g.hoff[item] + before;
+    EmitWarp* ws = &wsm[warp];
+    int nzt;
+    const int pos = warp_excl_scan(nz, lane, &nzt);
+    int p = pos;
+#pragma unroll
+    for (int q = 0; q < kEmitWPL; ++q) {
+        if (xs[q]) {
+            const int w = b * kEmitBlock + lane * kEmitWPL + q;
+            ws->wr[p] = make_uint2(xs[q], (unsigned)(t0 + ((idx ? (int)idx[w] : w) << 5)));
+            ++p;
+        }
+    }
+    __syncwarp();
+    emit_block(ws, pos, cnt, E, g.crw + off, lane);
+    if (g.cv) {  // values: E bytes of 1
+        uint8_t* v = g.cv + off;
+        const int head = (int)lmin(E, (16 - (reinterpret_cast<uintptr_t>(v) & 15)) & 15);
+        if (lane < head) v[lane] = 1;
+        const int body = (E - head) >> 4;
+        uint4* v4 = reinterpret_cast<uint4*>(v + head);
+        for (int q = lane; q < body; q += 32) v4[q] = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
+        for (int q = head + (body << 4) + lane; q < E; q += 32) v[q] = 1;
+    }
+}
+
+__global__ void k_emit_nblk(int nitems, const int* __restrict__ form, int W, int64_t* __restrict__ nb) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nitems; i += gridDim.x * blockDim.x) {
+        const int nw = form[i] >= 0 ? form[i] : W;
+        nb[i] = (nw + kEmitBlock - 1) / kEmitBlock;
+    }
+}
+
+__global__ void k_emit_fill(int nitems, const int64_t* __restrict__ nb, const int64_t* __restrict__ boff,
+                            int2* __restrict__ blocks) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nitems; i += gridDim.x * blockDim.x)
+        for (int64_t b = 0; b < nb[i]; ++b) blocks[boff[i] + b] = make_int2(i, (int)b);
+}
+
 // ------------------------------------------------------------ value pass
 
 // Values of the items for semirings with values (and OrAnd operands with
@@ -1512,11 +1585,26 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
                    (const int64_t*)d.hoff.as<int64_t>(), (const int64_t*)d.lp.as<int64_t>(), TL, crw,
                    ones ? static_cast<uint8_t*>(cv) : nullptr};  // values: 1s here, else the value pass
         const size_t smem = 0;
-        auto emit = [&](auto ke, int nt) {
-            ensure_smem(ke, smem);
-            launch(c, ke, dim3(nitems), dim3(nt), smem, e);
-        };
-        emit(k_tile_emit<128>, 128);  // (per-warp state is static shared memory: 4 warps)
+        if (c.opt.direct_emit_blocks) {
+            DevBuf nb(sizeof(int64_t) * (size_t(nitems) + 1), c.stream), boff(sizeof(int64_t) * (size_t(nitems) + 1),
+                                                                                c.stream);
+            SLAPCU_CUDA(cudaMemsetAsync(nb.as<int64_t>() + nitems, 0, sizeof(int64_t), c.stream));
+            launch(c, k_emit_nblk, dim3(grid_for(c, nitems, 256)), dim3(256), 0, nitems, (const int*)d.form.as<int>(),
+                   W, nb.as<int64_t>());
+            exclusive_scan_i64(c, nb.as<int64_t>(), boff.as<int64_t>(), nitems + 1);
+            const int64_t nblocks = d2h(c, boff.as<int64_t>() + nitems);
+            d.eblocks.reset(sizeof(int2) * std::max<int64_t>(nblocks, 1), c.stream);
+            launch(c, k_emit_fill, dim3(grid_for(c, nitems, 256)), dim3(256), 0, nitems,
+                   (const int64_t*)nb.as<int64_t>(), (const int64_t*)boff.as<int64_t>(), d.eblocks.as<int2>());
+            launch(c, k_tile_emit_blocks, dim3((unsigned)((nblocks + 3) / 4)), dim3(128), 0, e,
+                   (const int2*)d.eblocks.as<int2>(), nblocks);
+        } else {
+            auto emit = [&](auto ke, int nt) {
+                ensure_smem(ke, smem);
+                launch(c, ke, dim3(nitems), dim3(nt), smem, e);
+            };
+            emit(k_tile_emit<128>, 128);  // (per-warp state is static shared memory: 4 warps)
+        }
     }
     if (nitems > 0 && !ones) {
         KScope ks(c, KC_NUM_HEAVY);

@@ -48,15 +48,17 @@ def test_direct_bool_tiles_and_splits(port, tile_log2, split, dense_run):
 
 @pytest.mark.parametrize("mode", [0, 1, 2])
 @pytest.mark.parametrize("quads", [0, 1])
+@pytest.mark.parametrize("emit", [32, 128])
 @pytest.mark.parametrize("scale", [8, 11, 14])
-def test_direct_bool_rmat(port, scale, mode, quads):
+def test_direct_bool_rmat(port, scale, mode, quads, emit):
     a = _ones(port.gen_rmat(scale))
     want = port.spgemm(oracle.OR_AND_U8, a, a)
     ctx = P.Context()
     ctx.set_option(L.OPT_DIRECT_MARK_MODE, mode)
     ctx.set_option(L.OPT_DIRECT_QUADS, quads)
+    ctx.set_option(L.OPT_DIRECT_EMIT_THREADS, emit)
     got = P.local_spgemm(to_device(a), to_device(a), P.OrAnd, ctx=ctx, method="direct")
-    assert_parity(got, want, oracle.OR_AND_U8, f"s{scale} mode {mode}")
+    assert_parity(got, want, oracle.OR_AND_U8, f"s{scale} mode {mode} quads {quads} emit {emit}")
 
 
 def test_direct_window_and_rectangular(port):
