@@ -137,10 +137,13 @@ typedef enum {
                                               broadcast, then ONE concatenated-k product forms C(i,j)
                                               (no stage partials, no merge); 0 = per-stage products
                                               double-buffered against the broadcasts + stage merge */
-    SLAPCU_OPT_DIRECT_VALUE_HASH = 20      /* direct path value pass: 1 (default, = 13) / 13 / 14 = items
+    SLAPCU_OPT_DIRECT_VALUE_HASH = 20,     /* direct path value pass: 1 (default, = 13) / 13 / 14 = items
                                               with <= 2^(v-1) outputs take one walk into a shared hash
                                               table of 2^v slots keyed by their rows; 0 = every item
                                               takes the row sub-tile pass */
+    SLAPCU_OPT_DIRECT_VALUE_RANK = 21      /* direct path value pass: larger items are folded in rank
+                                              chunks of at most this many outputs (4096..16384, default
+                                              4096); 0 = row sub-tiles of 2^VTL rows */
 } slapcu_option;
 slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t value);
 

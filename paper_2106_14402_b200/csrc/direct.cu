@@ -787,7 +787,7 @@ struct ValueWalkSm {
 // walks a run alone through a chain of dependent loads.
 template <int SRID, int NT, class Slot>
 __device__ __forceinline__ void value_walk(const DevCsc& A, const DevCsc& B, const int32_t* __restrict__ Atab, int T,
-                                           int t, int j, ValueWalkSm<SRID, NT>& sh, Slot slot) {
+                                           int t, int j, ValueWalkSm<SRID, NT>& sh, Slot slot, int t_hi = -1) {
     using S_ = Sr<SRID>;
     using T_ = typename S_::T;
     constexpr int NW = NT / 32;
@@ -801,8 +801,8 @@ __device__ __forceinline__ void value_walk(const DevCsc& A, const DevCsc& B, con
         int slen = 0;
         if (i < be) {
             const int k = B.rw[i];
-            const int32_t* tp = Atab + int64_t(k) * (T + 1) + t;
-            const int rlo = tp[0], rhi = tp[1];
+            const int32_t* tp = Atab + int64_t(k) * (T + 1);
+            const int rlo = tp[t], rhi = tp[t_hi < 0 ? t + 1 : t_hi];  // tiles [t, t_hi) of the table
             const int len = rhi - rlo;
             if (len > 0) {
                 const int64_t st = A.cp[k] + rlo;
@@ -999,6 +999,126 @@ __global__ void __launch_bounds__(NT) k_item_values_hash(ValueArgs g) {
     value_walk<SRID, NT>(g.A, g.B, g.Atp, g.T, it.y, j, sh, slot);
     T* Cv = static_cast<T*>(g.cv);
     for (int64_t q = tid; q < c; q += NT) Cv[off + q] = S_::out(*slot(g.crw[off + q]));
+}
+
+// Values of the large items by rank chunks: an item's 4096-row blocks are
+// grouped greedily into chunks of at most `cap` output entries; one CTA per
+// chunk rebuilds the chunk's row bitmap from C's rows, turns it into ranks
+// (16-bit prefixes inside 32-word groups + group bases) and folds every
+// product of the chunk's rows into a rank-indexed shared value array -- one
+// walk over B(:,j) per chunk instead of one per fixed row sub-tile.
+struct RankChunk {
+    int item, b0, b1, pad;
+};
+
+template <int SRID, int NT>
+__global__ void __launch_bounds__(NT) k_item_values_rank(ValueArgs g, const RankChunk* __restrict__ chunks, int cap) {
+    using S_ = Sr<SRID>;
+    using T = typename S_::T;
+    using Acc = typename S_::Acc;
+    constexpr int NW = NT / 32;
+    constexpr int kBlkRows = kRbcWords * 32;  // 4096
+    extern __shared__ __align__(16) unsigned char sm_raw[];
+    const int W = 1 << (g.TL - 5);
+    Acc* val = reinterpret_cast<Acc*>(sm_raw);
+    unsigned* bm = reinterpret_cast<unsigned*>(sm_raw + ((sizeof(Acc) * size_t(cap) + 15) & ~size_t(15)));
+    uint16_t* pre16 = reinterpret_cast<uint16_t*>(bm + W);  // [W]
+    int* gbase = reinterpret_cast<int*>(pre16 + W);         // [W / 32]
+    __shared__ ValueWalkSm<SRID, NT> sh;
+    __shared__ int64_t range_sh[2];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const RankChunk ch = chunks[blockIdx.x];
+    const int2 it = g.items[ch.item];
+    const int j = it.x;
+    const int r0 = (it.y << g.TL) + ch.b0 * kBlkRows;
+    const int nwords = (ch.b1 - ch.b0) * kRbcWords;
+    if (warp == 0) {
+        const int nrb = (W + kRbcWords - 1) / kRbcWords;
+        const int* rb = g.rbc + int64_t(ch.item) * nrb;
+        int before = 0, inside = 0;
+        for (int b = lane; b < nrb; b += 32) {
+            const int x = rb[b];
+            before += b < ch.b0 ? x : 0;
+            inside += (b >= ch.b0 && b < ch.b1) ? x : 0;
+        }
+        before = warp_reduce_sum(before);
+        inside = warp_reduce_sum(inside);
+        if (lane == 0) {
+            const int64_t off = g.lp[j] + g.hoff[ch.item];
+            range_sh[0] = off + before;
+            range_sh[1] = off + before + inside;
+            sh.nlong = 0;
+        }
+    }
+    for (int q = tid; q < nwords; q += NT) bm[q] = 0u;
+    __syncthreads();
+    const int64_t lo = range_sh[0], hi = range_sh[1];
+    const int n = (int)(hi - lo);
+    for (int q = tid; q < n; q += NT) {
+        const int rr = g.crw[lo + q] - r0;
+        atomicOr(&bm[rr >> 5], 1u << (rr & 31));
+        val[q] = S_::identity();
+    }
+    __syncthreads();
+    // ranks: per 32-word group a warp scan (16-bit prefixes), then group bases
+    const int ng = (nwords + 31) >> 5;
+    for (int gi = warp; gi < ng; gi += NW) {
+        const int w = gi * 32 + lane;
+        const int x = w < nwords ? __popc(bm[w]) : 0;
+        int tot;
+        const int ex = warp_excl_scan(x, lane, &tot);
+        if (w < nwords) pre16[w] = (uint16_t)ex;
+        if (lane == 0) gbase[gi] = tot;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        int run = 0;
+        for (int b0 = 0; b0 < ng; b0 += 32) {
+            const int gi = b0 + lane;
+            const int x = gi < ng ? gbase[gi] : 0;
+            int tt;
+            const int e = warp_excl_scan(x, lane, &tt);
+            if (gi < ng) gbase[gi] = run + e;
+            run += tt;
+        }
+    }
+    __syncthreads();
+    auto slot = [bm, pre16, gbase, val, r0](int r) {
+        const int rr = r - r0;
+        const int w = rr >> 5;
+        return &val[gbase[w >> 5] + pre16[w] + __popc(bm[w] & ((1u << (rr & 31)) - 1u))];
+    };
+    const int ts0 = (it.y << (g.TL - g.VTL)) + ch.b0, ts1 = (it.y << (g.TL - g.VTL)) + ch.b1;
+    value_walk<SRID, NT>(g.A, g.B, g.Atpv, g.Tv, ts0, j, sh, slot, ts1);
+    T* Cv = static_cast<T*>(g.cv);
+    for (int q = tid; q < n; q += NT) Cv[lo + q] = S_::out(val[q]);
+}
+
+// Rank chunks of the large items (thread per item, greedy over row blocks).
+__global__ void k_rank_chunks(int n, const int* __restrict__ list, const int* __restrict__ rbc, int nrb, int cap,
+                              const int64_t* __restrict__ coff, int64_t* __restrict__ ccount,
+                              RankChunk* __restrict__ out) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int item = list[i];
+        const int* rb = rbc + int64_t(item) * nrb;
+        int64_t k = 0, acc = 0;
+        int b0 = 0;
+        for (int b = 0; b < nrb; ++b) {
+            const int x = rb[b];
+            if (acc > 0 && acc + x > cap) {
+                if (out) out[coff[i] + k] = RankChunk{item, b0, b, 0};
+                ++k;
+                b0 = b;
+                acc = 0;
+            }
+            acc += x;
+        }
+        if (acc > 0) {
+            if (out) out[coff[i] + k] = RankChunk{item, b0, nrb, 0};
+            ++k;
+        }
+        if (!out) ccount[i] = k;
+    }
 }
 
 __global__ void k_value_split(int nitems, const int64_t* __restrict__ cnt, int64_t hcap, int* __restrict__ small,
@@ -1611,7 +1731,9 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
         // sub-tiles are whole 4096-row blocks of the item (or the item itself)
         const int VTL = std::min(TL, std::max(12, c.opt.direct_value_tile_log2));
         const int Tv = (int)((A.nrows + (int64_t(1) << VTL) - 1) >> VTL);
-        const int32_t* Atpv = value_tile_pointers(c, A, VTL, Tv);
+        const bool rank_path = c.opt.direct_value_rank > 0 && TL >= 12;
+        // (one cached table at a time: only the sub-tile path needs 2^VTL rows)
+        const int32_t* Atpv = rank_path ? nullptr : value_tile_pointers(c, A, VTL, Tv);
         const int32_t* Atp = tile_pointers(c, A, TL, T);
         // small items (<= kHashCap outputs) take the one-walk hash kernel
         const int hlog2 = c.opt.direct_value_hash >= 14 ? 14 : 13;  // table slots (load <= 1/2)
@@ -1643,7 +1765,33 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
                 else
                     go(k_item_values_hash<ID, 256, 13>);
             }
-            if (nsl[1] > 0) {
+            if (nsl[1] > 0 && rank_path) {
+                // large items by rank chunks over 4096-row blocks (tile pointers at 2^12 rows)
+                const int cap = c.opt.direct_value_rank;
+                const int T12 = (int)((A.nrows + 4095) >> 12);
+                ValueArgs vr = va;
+                vr.Atpv = value_tile_pointers(c, A, 12, T12);
+                vr.Tv = T12;
+                vr.VTL = 12;
+                const int nrb = (W + kRbcWords - 1) / kRbcWords;
+                DevBuf ccount(sizeof(int64_t) * (size_t(nsl[1]) + 1), c.stream),
+                    coff(sizeof(int64_t) * (size_t(nsl[1]) + 1), c.stream);
+                SLAPCU_CUDA(cudaMemsetAsync(ccount.as<int64_t>() + nsl[1], 0, sizeof(int64_t), c.stream));
+                launch(c, k_rank_chunks, dim3(grid_for(c, nsl[1], 256)), dim3(256), 0, nsl[1], (const int*)large,
+                       (const int*)d.rbc.as<int>(), nrb, cap, (const int64_t*)nullptr, ccount.as<int64_t>(),
+                       (RankChunk*)nullptr);
+                exclusive_scan_i64(c, ccount.as<int64_t>(), coff.as<int64_t>(), nsl[1] + 1);
+                const int64_t nch = d2h(c, coff.as<int64_t>() + nsl[1]);
+                DevBuf chunks(sizeof(RankChunk) * std::max<int64_t>(nch, 1), c.stream);
+                launch(c, k_rank_chunks, dim3(grid_for(c, nsl[1], 256)), dim3(256), 0, nsl[1], (const int*)large,
+                       (const int*)d.rbc.as<int>(), nrb, cap, (const int64_t*)coff.as<int64_t>(), ccount.as<int64_t>(),
+                       chunks.as<RankChunk>());
+                const size_t smem = ((sizeof(Acc) * size_t(cap) + 15) & ~size_t(15)) + sizeof(unsigned) * W +
+                                    sizeof(uint16_t) * W + sizeof(int) * (W / 32) + 16;
+                auto k = k_item_values_rank<ID, 256>;
+                ensure_smem(k, smem);
+                launch(c, k, dim3((unsigned)nch), dim3(256), smem, vr, (const RankChunk*)chunks.as<RankChunk>(), cap);
+            } else if (nsl[1] > 0) {
                 va.list = large;
                 const size_t smem = sizeof(Acc) * (size_t(1) << VTL);
                 if (smem > size_t(c.smem_optin) - 16 * 1024)

@@ -87,10 +87,11 @@ def test_direct_window_and_rectangular(port):
 
 
 @pytest.mark.parametrize("vtl", [10, 12, 14])
+@pytest.mark.parametrize("rank", [0, 4096])
 @pytest.mark.parametrize("hash_", [0, 1])
 @pytest.mark.parametrize("sr", [P.PlusTimesF64, P.PlusTimesF32, P.PlusTimesI64, P.MinPlusI32, P.MinPlusF64],
                          ids=lambda s: f"{s.name}_{s.dtype}")
-def test_direct_value_pass(port, sr, vtl, hash_):
+def test_direct_value_pass(port, sr, vtl, hash_, rank):
     """Semirings with values: pattern walk + emit, then the value pass --
     small items through the hash kernel, large ones over sub-tiles of 2^vtl
     rows (several per item when vtl < the item tile)."""
@@ -100,6 +101,7 @@ def test_direct_value_pass(port, sr, vtl, hash_):
     ctx.set_option(L.OPT_DIRECT_TILE_ROWS_LOG2, 14 if hash_ else 12)
     ctx.set_option(L.OPT_DIRECT_VALUE_TILE_ROWS_LOG2, vtl)
     ctx.set_option(L.OPT_DIRECT_VALUE_HASH, hash_)
+    ctx.set_option(L.OPT_DIRECT_VALUE_RANK, rank)
     ctx.set_option(L.OPT_DIRECT_SPLIT_FLOPS, 4096)
     got = P.local_spgemm(to_device(a), to_device(a), sr, ctx=ctx, method="direct")
     assert_parity(got, want, sr.id, f"{sr.name} vtl={vtl}")
