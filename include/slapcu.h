@@ -221,8 +221,9 @@ slapcu_status slapcu_spgemm_direct(slapcu_ctx ctx, const slapcu_csc* A, const sl
                                    void* c_vals, int64_t* c_nnz);
 
 /* spgemm.hpp:275-330 local_spgemm, all three phases, C allocated on the
- * device by the library (single-pass begin/finish; falls back to the
- * symbolic/numeric pair when the staging area does not fit). */
+ * device by the library: the direct single pass into a bound-sized scratch,
+ * then exactly sized buffers; falls back to begin/finish, then to the
+ * symbolic/numeric pair, when that scratch / the staging area does not fit. */
 slapcu_status slapcu_spgemm(slapcu_ctx ctx, const slapcu_csc* A, const slapcu_csc* B, slapcu_semiring sr,
                             slapcu_alg alg, slapcu_csc_out* C);
 

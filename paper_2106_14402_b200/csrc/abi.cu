@@ -330,9 +330,22 @@ slapcu_status slapcu_spgemm(slapcu_ctx ctx, const slapcu_csc* A, const slapcu_cs
         const int vs = value_size(sr);
         require(vs > 0, SLAPCU_ERR_INVALID, "unknown semiring");
         const DevCsc a = view(*A), b = view(*B);
+        // production path: one product pass into an exactly sized C
+        int64_t nnz = 0;
+        int64_t* dcp = nullptr;
+        int32_t* drw = nullptr;
+        void* dv = nullptr;
+        if (direct_exact(c, a, b, sr, alg, default_staging_budget(c), &dcp, &drw, &dv, &nnz)) {
+            C->nrows = a.nrows;
+            C->ncols = b.ncols;
+            C->nnz = nnz;
+            C->colptr = dcp;
+            C->rowids = drw;
+            C->vals = dv;
+            return;
+        }
         int64_t* cp = nullptr;
         SLAPCU_CUDA(cudaMallocAsync((void**)&cp, sizeof(int64_t) * (b.ncols + 1), c.stream));
-        int64_t nnz = 0;
         bool fused = true;
         try {
             try {
@@ -393,11 +406,15 @@ slapcu_status slapcu_spgemm_host(slapcu_ctx ctx, const slapcu_host_csc* A, const
         };
         try {
             const DevCsc av = view(a), bv = view(b);
-            SLAPCU_CUDA(cudaMallocAsync((void**)&dC.colptr, sizeof(int64_t) * (bv.ncols + 1), c.stream));
-            const int64_t nnz = spgemm_symbolic(c, av, bv, alg, dC.colptr);
-            SLAPCU_CUDA(cudaMallocAsync((void**)&dC.rowids, sizeof(int32_t) * std::max<int64_t>(nnz, 1), c.stream));
-            SLAPCU_CUDA(cudaMallocAsync(&dC.vals, size_t(vs) * std::max<int64_t>(nnz, 1), c.stream));
-            spgemm_numeric(c, av, bv, sr, alg, dC.colptr, dC.rowids, dC.vals);
+            int64_t nnz = 0;
+            if (!direct_exact(c, av, bv, sr, alg, default_staging_budget(c), &dC.colptr, &dC.rowids, &dC.vals,
+                              &nnz)) {
+                SLAPCU_CUDA(cudaMallocAsync((void**)&dC.colptr, sizeof(int64_t) * (bv.ncols + 1), c.stream));
+                nnz = spgemm_symbolic(c, av, bv, alg, dC.colptr);
+                SLAPCU_CUDA(cudaMallocAsync((void**)&dC.rowids, sizeof(int32_t) * std::max<int64_t>(nnz, 1), c.stream));
+                SLAPCU_CUDA(cudaMallocAsync(&dC.vals, size_t(vs) * std::max<int64_t>(nnz, 1), c.stream));
+                spgemm_numeric(c, av, bv, sr, alg, dC.colptr, dC.rowids, dC.vals);
+            }
             C->nrows = av.nrows;
             C->ncols = bv.ncols;
             C->nnz = nnz;

@@ -123,7 +123,7 @@ struct Options {
     bool async_finish = false;        // finish() returns without waiting (errors surface later)
     int direct_tile_rows_log2 = 0;    // direct path: row-tile height of an item (0 = auto: 17, 18 above 2^20 rows)
     int64_t direct_light_flops_max = 1024;  // direct path: hash path for columns up to this many flops
-    int64_t direct_dense_run_min = 2048;    // direct path: A runs (column x tile) this long are OR-ed
+    int64_t direct_dense_run_min = 4096;    // direct path: A runs (column x tile) this long are OR-ed
                                             // as precomputed tile bitmaps (0 = never)
     int direct_mark_mode = 0;               // product update: 0 test+set, 1 atomic only, 2 quad-merged
     int direct_quads = 0;
@@ -232,7 +232,10 @@ void fused_light_launch(Ctx& c, int sr, bool ones, int bin, const DevCsc& A, con
                         const int64_t* flops, FusedState& f);
 void fused_copy_light(Ctx& c, int sr, bool ones, const int* list, int n, const FusedState& f, const int64_t* c_colptr,
                       int32_t* c_rowids, void* c_vals);
-// direct.cu: single pass straight into C (pattern semirings)
+// direct.cu: single product pass straight into C; direct_exact returns exactly
+// sized library-owned buffers (false when the bound-sized scratch exceeds budget)
+bool direct_exact(Ctx& c, const DevCsc& A, const DevCsc& B, int sr, int alg, int64_t budget, int64_t** colptr,
+                  int32_t** rowids, void** vals, int64_t* nnz);
 int64_t direct_spgemm(Ctx& c, const DevCsc& A, const DevCsc& B, int sr, int alg, int64_t capacity, int64_t* c_colptr,
                       int32_t* c_rowids, void* c_vals);
 void any_zero_u8(Ctx& c, const uint8_t* v, int64_t n, int* flag);

@@ -1818,4 +1818,46 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
     return total;
 }
 
+// The direct product into library-owned, exactly sized buffers (the
+// one-shot / host / distributed entry points): C lands in a bound-sized
+// scratch kept on the context, then moves into cudaMallocAsync'd buffers of
+// nnz entries.  Returns false (nothing allocated) when the scratch would not
+// fit in `budget` bytes -- callers then take the staged or two-pass path.
+bool direct_exact(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int alg, int64_t budget, int64_t** cp,
+                  int32_t** rw, void** v, int64_t* nnz) {
+    check_operands(A_, B_);
+    const int vs = value_size(sr);
+    DevCsc A = A_, B = B_;
+    resolve(c, A);
+    resolve(c, B);
+    const int64_t N = B.ncols;
+    DevBuf fl(sizeof(int64_t) * std::max<int64_t>(N, 1), c.stream);
+    int64_t tot = 0;
+    spgemm_flops(c, A, B, fl.as<int64_t>(), &tot);
+    std::vector<int64_t> hf(N);
+    if (N) SLAPCU_CUDA(cudaMemcpyAsync(hf.data(), fl.get(), sizeof(int64_t) * N, cudaMemcpyDeviceToHost, c.stream));
+    SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+    int64_t cap = 0;
+    for (int64_t x = 0; x < N; ++x) cap += std::min(hf[x], A.nrows);
+    if (budget > 0 && cap * (4 + vs) > budget) return false;
+    DirectCache& d = c.direct;
+    d.dist_rw.reset(sizeof(int32_t) * std::max<int64_t>(cap, 1), c.stream);
+    d.dist_v.reset(size_t(vs) * std::max<int64_t>(cap, 1), c.stream);
+    SLAPCU_CUDA(cudaMallocAsync((void**)cp, sizeof(int64_t) * (N + 1), c.stream));
+    try {
+        *nnz = direct_spgemm(c, A_, B_, sr, alg, cap, *cp, d.dist_rw.as<int32_t>(), d.dist_v.get());
+    } catch (...) {
+        cudaFreeAsync(*cp, c.stream);
+        *cp = nullptr;
+        throw;
+    }
+    SLAPCU_CUDA(cudaMallocAsync((void**)rw, sizeof(int32_t) * std::max<int64_t>(*nnz, 1), c.stream));
+    SLAPCU_CUDA(cudaMallocAsync(v, size_t(vs) * std::max<int64_t>(*nnz, 1), c.stream));
+    if (*nnz) {
+        SLAPCU_CUDA(cudaMemcpyAsync(*rw, d.dist_rw.get(), sizeof(int32_t) * *nnz, cudaMemcpyDeviceToDevice, c.stream));
+        SLAPCU_CUDA(cudaMemcpyAsync(*v, d.dist_v.get(), size_t(vs) * *nnz, cudaMemcpyDeviceToDevice, c.stream));
+    }
+    return true;
+}
+
 }  // namespace slapcu
