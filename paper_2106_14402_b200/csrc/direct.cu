@@ -1756,14 +1756,15 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
             if (nsl[0] > 0) {
                 va.list = small;
                 const size_t smem = (sizeof(Acc) + sizeof(int)) << hlog2;
-                auto go = [&](auto k) {
+                auto go = [&](auto k, int nt) {
                     ensure_smem(k, smem);
-                    launch(c, k, dim3(nsl[0]), dim3(256), smem, va);
+                    launch(c, k, dim3(nsl[0]), dim3(nt), smem, va);
                 };
+                const bool wide = c.opt.direct_value_threads == 512;
                 if (hlog2 == 14)
-                    go(k_item_values_hash<ID, 256, 14>);
+                    wide ? go(k_item_values_hash<ID, 512, 14>, 512) : go(k_item_values_hash<ID, 256, 14>, 256);
                 else
-                    go(k_item_values_hash<ID, 256, 13>);
+                    wide ? go(k_item_values_hash<ID, 512, 13>, 512) : go(k_item_values_hash<ID, 256, 13>, 256);
             }
             if (nsl[1] > 0 && rank_path) {
                 // large items by rank chunks over 4096-row blocks (tile pointers at 2^12 rows)
@@ -1788,9 +1789,15 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
                        chunks.as<RankChunk>());
                 const size_t smem = ((sizeof(Acc) * size_t(cap) + 15) & ~size_t(15)) + sizeof(unsigned) * W +
                                     sizeof(uint16_t) * W + sizeof(int) * (W / 32) + 16;
-                auto k = k_item_values_rank<ID, 256>;
-                ensure_smem(k, smem);
-                launch(c, k, dim3((unsigned)nch), dim3(256), smem, vr, (const RankChunk*)chunks.as<RankChunk>(), cap);
+                auto gor = [&](auto k, int nt) {
+                    ensure_smem(k, smem);
+                    launch(c, k, dim3((unsigned)nch), dim3(nt), smem, vr, (const RankChunk*)chunks.as<RankChunk>(),
+                           cap);
+                };
+                if (c.opt.direct_value_threads == 512)
+                    gor(k_item_values_rank<ID, 512>, 512);
+                else
+                    gor(k_item_values_rank<ID, 256>, 256);
             } else if (nsl[1] > 0) {
                 va.list = large;
                 const size_t smem = sizeof(Acc) * (size_t(1) << VTL);
