@@ -43,7 +43,8 @@ typedef enum {
     SLAPCU_ERR_INVALID = 7,  /* bad argument (null pointer, unsupported id)        */
     SLAPCU_ERR_CUDA = 8,     /* CUDA runtime failure                               */
     SLAPCU_ERR_NOMEM = 9,    /* device allocation failure                          */
-    SLAPCU_ERR_COMM = 10     /* NCCL failure / collective mismatch (DeadlockError) */
+    SLAPCU_ERR_COMM = 10,    /* NCCL failure / collective mismatch (DeadlockError) */
+    SLAPCU_ERR_STOCHASTIC = 11 /* StochasticityError (algorithms.cpp:271-275, mcl_step input) */
 } slapcu_status;
 
 /* semiring.hpp:36-93.  Ids are stable (shared with oracle/oracle.h). */
@@ -235,6 +236,16 @@ slapcu_status slapcu_spgemm_host(slapcu_ctx ctx, const slapcu_host_csc* A, const
 
 slapcu_status slapcu_csc_free(slapcu_ctx ctx, slapcu_csc_out* C);
 void slapcu_host_free(slapcu_host_csc* C);
+
+/* algorithms.cpp:267-293 mcl_step on one device: expansion
+ * C = A*A (the direct single pass), inflation v -> v^inflation, pruning of
+ * entries with v < prune_threshold, column renormalisation (a column whose
+ * kept sum is 0 is left as is).  sr: PlusTimes f64 (the reference's type) or
+ * f32 (config C4).  Input columns must sum to 1 within 1e-9 (f64) / 1e-5
+ * (f32), else SLAPCU_ERR_STOCHASTIC; non-square A or inflation <= 0 give
+ * SLAPCU_ERR_SHAPE.  C is allocated by the library (slapcu_csc_free). */
+slapcu_status slapcu_mcl_step(slapcu_ctx ctx, const slapcu_csc* A, slapcu_semiring sr, double inflation,
+                              double prune_threshold, slapcu_csc_out* C);
 
 /* ------------------------------------------------------- format adapters */
 

@@ -195,6 +195,7 @@ class _Ref:
         L.ref_ca3d.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P, P, P]
         L.ref_plan_batches.argtypes = [C.c_int, C.c_int, P, P, C.c_int64, C.c_void_p, C.c_void_p, C.c_int]
         L.ref_merge.argtypes = [C.c_int, C.c_int, P, P]
+        L.ref_mcl_step.argtypes = [C.c_int, C.c_int, P, C.c_double, C.c_double, P]
         L.ref_free.argtypes = [C.c_void_p]
         L.ref_time_local_spgemm.argtypes = [C.c_int, C.c_int, C.c_int, P, P, C.c_int64, C.c_int64,
                                             C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
@@ -237,6 +238,18 @@ class _Ref:
         rc = self.lib.ref_gen_rmat(scale, edge_factor, seed, C.byref(out))
         assert rc == 0, rc
         return _from_c(out, None, self.lib.ref_free)
+
+    def mcl_step(self, a: Csc, inflation=2.0, prune=1e-4, p=1, layers=1) -> Csc:
+        """algorithms.cpp:267-293 mcl_step (PlusTimes<double>) on p rank threads.
+        Raises ValueError("StochasticityError") when a column sum is off by > 1e-9."""
+        keep = []
+        out = _CCsc()
+        rc = self.lib.ref_mcl_step(p, layers, C.byref(_as_c(a, keep)), inflation, prune, C.byref(out))
+        if rc == -8:
+            raise ValueError("StochasticityError")
+        if rc != 0:
+            raise RuntimeError(f"ref_mcl_step failed: {rc}")
+        return _from_c(out, DTYPES[PLUS_TIMES_F64], self.lib.ref_free)
 
     def summa2d(self, sr, a: Csc, b: Csc, p=4, alg=HYBRID, threads=1):
         keep = []

@@ -132,6 +132,7 @@ int error_code(const std::exception& e) {
         if (err->kind() == "ShapeError") return -6;
         if (err->kind() == "BudgetError") return -7;
         if (err->kind() == "InternalError") return -4;
+        if (err->kind() == "StochasticityError") return -8;
     }
     return -1;
 }
@@ -247,6 +248,34 @@ int ref_gen_rmat(int scale, int edge_factor, uint64_t seed, ref_csc* out) {
             out->vals = nullptr;
         });
         return rc;
+    } catch (const std::exception& e) {
+        return error_code(e);
+    }
+}
+
+/// algorithms.cpp:267-293 mcl_step (expansion A*A in PlusTimes<double>,
+/// inflation pow, prune below the threshold, column renormalisation) on a
+/// sqrt(p) x sqrt(p) grid of rank threads (layers > 1: the 3D expansion).
+int ref_mcl_step(int p, int layers, const ref_csc* a, double inflation, double prune, ref_csc* c) {
+    try {
+        auto ta = to_triples64<double>(*a);
+        run_world(p, [&](Comm& w) {
+            auto g = make_square_grid2d(w);
+            auto first = [](const double& x, const double&) { return x; };
+            Triples<GlobalIdx, double> ma;
+            ma.nrows = ta.nrows;
+            ma.ncols = ta.ncols;
+            if (w.rank() == 0) ma = ta;
+            auto da = distribute_triples(ma, g, ta.nrows, ta.ncols, first);
+            MclOptions opt;
+            opt.inflation = inflation;
+            opt.prune_threshold = prune;
+            opt.layers = layers;
+            auto dc = mcl_step(da, opt);
+            auto got = gather_matrix(dc);
+            if (w.rank() == 0) from_triples64(got, c);
+        });
+        return 0;
     } catch (const std::exception& e) {
         return error_code(e);
     }

@@ -30,6 +30,7 @@ from .spgemm import (
     gen_one_per_row,
     gen_rmat,
     local_spgemm,
+    mcl_step,
     merge,
     permute_symmetric,
     semiring_from_name,

@@ -114,6 +114,7 @@ SIGNATURES = [
     ("slapcu_spgemm", _I, [_P, _PV, _PV, _I, _I, _PO]),
     ("slapcu_spgemm_host", _I, [_P, _PO, _PO, _I, _I, _PO]),
     ("slapcu_csc_free", _I, [_P, _PO]),
+    ("slapcu_mcl_step", _I, [_P, _PV, _I, C.c_double, C.c_double, _PO]),
     ("slapcu_host_free", None, [_PO]),
     ("slapcu_dcsc_colptr", _I, [_P, _L, _L, _P, _P, _P]),
     ("slapcu_merge_symbolic", _I, [_P, _I, _PV, _P, C.POINTER(_L)]),

@@ -76,6 +76,7 @@ const char* slapcu_status_name(slapcu_status s) {
     case SLAPCU_ERR_CUDA: return "CudaError";
     case SLAPCU_ERR_NOMEM: return "OutOfMemory";
     case SLAPCU_ERR_COMM: return "DeadlockError";
+    case SLAPCU_ERR_STOCHASTIC: return "StochasticityError";
     }
     return "Unknown";
 }
@@ -434,6 +435,15 @@ slapcu_status slapcu_spgemm_host(slapcu_ctx ctx, const slapcu_host_csc* A, const
             throw;
         }
         cleanup();
+    });
+}
+
+slapcu_status slapcu_mcl_step(slapcu_ctx ctx, const slapcu_csc* A, slapcu_semiring sr, double inflation,
+                              double prune_threshold, slapcu_csc_out* C) {
+    return guarded(ctx, [&](Ctx& c) {
+        require(A && C, SLAPCU_ERR_INVALID, "null argument");
+        *C = slapcu_csc_out{};
+        mcl_step(c, view(*A), sr, inflation, prune_threshold, C);
     });
 }
 

@@ -242,6 +242,9 @@ void any_zero_u8(Ctx& c, const uint8_t* v, int64_t n, int* flag);
 void dcsc_colptr(Ctx& c, int64_t ncols, int64_t nzc, const int32_t* jc, const int32_t* cp, int64_t* colptr);
 void exclusive_scan_i64(Ctx& c, const int64_t* in, int64_t* out, int64_t n);
 
+// mcl.cu: algorithms.cpp:267-293 mcl_step around the direct product
+void mcl_step(Ctx& c, const DevCsc& A, int sr, double inflation, double prune, slapcu_csc_out* out);
+
 // merge.cu
 int64_t merge_symbolic(Ctx& c, int nparts, const DevCsc* parts, int64_t* c_colptr);
 void merge_numeric(Ctx& c, int nparts, const DevCsc* parts, int sr, const int64_t* c_colptr, int32_t* c_rowids,

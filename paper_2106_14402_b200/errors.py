@@ -56,6 +56,10 @@ class OutOfMemory(Error):
     kind = "OutOfMemory"
 
 
+class StochasticityError(Error):
+    kind = "StochasticityError"
+
+
 BY_STATUS = {
     1: DimError,
     2: ShapeError,
@@ -67,4 +71,5 @@ BY_STATUS = {
     8: CudaError,
     9: OutOfMemory,
     10: DeadlockError,
+    11: StochasticityError,
 }

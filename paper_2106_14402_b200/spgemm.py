@@ -543,6 +543,20 @@ def slice_cols(m: DeviceCsc, c0: int, c1: int, sr: Semiring | None = None, ctx: 
     return _from_out(ctx, o, sr)
 
 
+def mcl_step(a, inflation: float = 2.0, prune_threshold: float = 1e-4, sr: Semiring | None = None,
+             ctx: Context | None = None) -> DeviceCsc:
+    """algorithms.cpp:267-293 mcl_step on one device: expansion A*A (direct
+    single pass), inflation, pruning, column renormalisation.  Raises
+    errors.StochasticityError if an input column does not sum to 1."""
+    ctx = _ctx(ctx)
+    A = _dev(a)
+    sr = _sr(sr) if sr is not None else (PlusTimesF32 if A.vals.dtype == torch.float32 else PlusTimesF64)
+    o = L.CscOut()
+    ctx.check(ctx.lib.slapcu_mcl_step(ctx.h, C.byref(A.view()), sr.id, float(inflation), float(prune_threshold),
+                                      C.byref(o)), "mcl_step")
+    return _from_out(ctx, o, sr)
+
+
 def column_checksums(m: DeviceCsc, sr: Semiring | None = None, with_values=True, ctx: Context | None = None):
     ctx = _ctx(ctx)
     sums = torch.empty(max(m.ncols, 1), dtype=torch.int64, device=m.colptr.device)
