@@ -39,6 +39,21 @@ def workload(name, ctx):
     raise ValueError(name)
 
 
+def stochastic_with_loops(A, sr):
+    """A's pattern plus the diagonal (isolated vertices would leave empty,
+    zero-sum columns, which mcl_step rejects), values 1/deg(col)."""
+    h = A.to_host()
+    n = h.ncols
+    cols = np.repeat(np.arange(n, dtype=np.int64), np.diff(h.colptr))
+    key = np.unique(np.concatenate([cols * n + h.rowids.astype(np.int64), np.arange(n, dtype=np.int64) * (n + 1)]))
+    c, r = key // n, (key % n).astype(np.int32)
+    cp = np.zeros(n + 1, np.int64)
+    np.cumsum(np.bincount(c, minlength=n), out=cp[1:])
+    deg = np.diff(cp)
+    vals = np.repeat(1.0 / deg, deg).astype(sr.np_dtype)
+    return P.CscMatrix(n, n, cp, r, vals).to_device()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="C1,C2,C4,C5")
@@ -81,6 +96,19 @@ def main():
         tol = 1e-12 if sr.dtype == "f64" else 1e-5
         gv, wv = gpu_slice.vals.astype(np.float64), want.vals.astype(np.float64)
         close = bool(np.all(np.abs(gv - wv) <= tol * np.maximum(1.0, np.maximum(np.abs(gv), np.abs(wv)))))
+        extra = {}
+        if name == "C4":  # the whole Markov-clustering step around the expansion (algorithms.cpp:267-293)
+            A = stochastic_with_loops(A, sr)  # mcl_step needs every column to sum to 1
+            P.mcl_step(A, 2.0, 1e-4, sr=sr, ctx=ctx)
+            torch.cuda.synchronize()
+            m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            m0.record(stream)
+            for _ in range(args.steps):
+                P.mcl_step(A, 2.0, 1e-4, sr=sr, ctx=ctx)
+            m1.record(stream)
+            torch.cuda.synchronize()
+            extra["mcl_step_ms"] = round(m0.elapsed_time(m1) / args.steps, 3)
+            extra["mcl_step_input"] = "A + I (no empty column), values 1/deg(col), inflation 2, prune 1e-4"
         peak = 6481.1
         vs = np.dtype(sr.np_dtype).itemsize
         step_bytes = sum(nz * (4 + vs) + (nc + 1) * 8 for nz, nc in ((A.nnz, A.ncols), (B.nnz, B.ncols), (nnz, B.ncols)))
@@ -91,6 +119,7 @@ def main():
             "cpu_reference": {"gflops": round(2 * ref_fl / secs / 1e9, 4), "threads": threads,
                               "sample": f"columns [{c0},{c0 + w}) of B, {ref_fl} multiplies in {secs:.3f} s"},
             "parity_slice": {"pattern_exact": same_pattern, f"values_rel_{tol}": close},
+            **extra,
         }), flush=True)
         del A, B
         torch.cuda.empty_cache()
