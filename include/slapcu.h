@@ -344,6 +344,47 @@ slapcu_status slapcu_summa2d(slapcu_comm comm, const slapcu_csc* A_local, const 
 slapcu_status slapcu_ca3d(slapcu_comm comm, int layers, const slapcu_csc* A_local, const slapcu_csc* B_local,
                           slapcu_semiring sr, slapcu_alg alg, slapcu_csc_out* C_local, slapcu_dist_stats* stats);
 
+
+/* ------------------------------------------------- redistribution (8f rank 2)
+ *
+ * A target layout is a tiling of the global nrows x ncols matrix: nr+1 row
+ * cuts, nc+1 column cuts (non-decreasing, from 0 to nrows / ncols) and the
+ * owning rank of tile (i, j) at owner[i*nc + j]; nr*nc == nranks and every
+ * rank owns exactly one tile.  All pointers are HOST pointers and every rank
+ * passes the same tiling (checked: SLAPCU_ERR_SHAPE otherwise).  The 2D
+ * (grid.hpp:15-24, block_offsets) and regular 3D (dist_matrix3d.hpp:54-80)
+ * layouts are built by paper_2106_14402_b200/grid.py tiling_2d / tiling_3d. */
+typedef struct {
+    int nr, nc;
+    const int64_t* row_cuts;
+    const int64_t* col_cuts;
+    const int32_t* owner;
+} slapcu_tiling;
+
+/* redistribute_3d (dist_matrix3d.hpp:117-170, regular variant) /
+ * redistribute_2d (dist_matrix3d.hpp:250-261), generalised: this rank's block
+ * `local` (block-local indices, global offsets row_start / col_start) is
+ * routed entry by entry to the owners of the target tiles (grouped
+ * ncclSend/ncclRecv after one count all-gather) and the received entries are
+ * assembled into this rank's tile as canonical CSC (allocated; free with
+ * slapcu_csc_free); out_row_start / out_col_start receive the tile's global
+ * offsets.  combine: 0 keeps the first of duplicate coordinates in arrival
+ * order (source rank, then source order), 1 folds them with the semiring add
+ * (local_matrix.hpp:167-188).  An entry outside nrows x ncols fails on every
+ * rank with SLAPCU_ERR_INDEX.  Collective over all ranks of `comm`. */
+slapcu_status slapcu_redistribute(slapcu_comm comm, const slapcu_csc* local, int64_t row_start, int64_t col_start,
+                                  int64_t nrows, int64_t ncols, slapcu_semiring sr, const slapcu_tiling* target,
+                                  int combine, slapcu_csc_out* out, int64_t* out_row_start, int64_t* out_col_start);
+
+/* distribute_triples (dist_matrix.hpp:89-119): `count` global (row, col, val)
+ * triples in DEVICE arrays (int64 rows / cols) from this rank, routed to the
+ * target tiles and assembled as above (duplicates: combine 0 keep-first,
+ * 1 semiring add, like the reference's `add` argument). */
+slapcu_status slapcu_distribute_triples(slapcu_comm comm, int64_t count, const int64_t* rows, const int64_t* cols,
+                                        const void* vals, int64_t nrows, int64_t ncols, slapcu_semiring sr,
+                                        const slapcu_tiling* target, int combine, slapcu_csc_out* out,
+                                        int64_t* out_row_start, int64_t* out_col_start);
+
 #ifdef __cplusplus
 }
 #endif

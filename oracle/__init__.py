@@ -196,6 +196,8 @@ class _Ref:
         L.ref_plan_batches.argtypes = [C.c_int, C.c_int, P, P, C.c_int64, C.c_void_p, C.c_void_p, C.c_int]
         L.ref_merge.argtypes = [C.c_int, C.c_int, P, P]
         L.ref_mcl_step.argtypes = [C.c_int, C.c_int, P, C.c_double, C.c_double, P]
+        L.ref_redistribute.argtypes = [C.c_int] * 8 + [C.c_int64] * 3 + [C.c_void_p] * 4 + [P, C.c_void_p,
+                                                                                            C.c_void_p]
         L.ref_free.argtypes = [C.c_void_p]
         L.ref_time_local_spgemm.argtypes = [C.c_int, C.c_int, C.c_int, P, P, C.c_int64, C.c_int64,
                                             C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
@@ -282,6 +284,26 @@ class _Ref:
             raise RuntimeError(f"ref_plan_batches failed: {nr}")
         return [(int(ranges[2 * i]), int(ranges[2 * i + 1])) for i in range(nr)], est[:nr].copy()
 
+    def redistribute(self, sr, p, pr, pc, nrows, ncols, src, rows, cols, vals, mode=0, layers=1, split="cols",
+                     combine="first"):
+        """ref_redistribute: distribute_triples (dist_matrix.hpp:89-119) of the
+        triples held by ranks src[k] onto pr x pc; mode 1 then redistribute_3d
+        (dist_matrix3d.hpp:117-170), mode 2 then redistribute_2d (:250-261).
+        Returns [(row_start, col_start, block Csc)] per rank."""
+        src = np.ascontiguousarray(src, np.int32)
+        rows = np.ascontiguousarray(rows, np.int64)
+        cols = np.ascontiguousarray(cols, np.int64)
+        vals = np.ascontiguousarray(vals, DTYPES[sr])
+        blocks = (_CCsc * p)()
+        rs = np.zeros(p, np.int64)
+        cs = np.zeros(p, np.int64)
+        rc = self.lib.ref_redistribute(sr, p, pr, pc, mode, layers, int(split == "rows"), int(combine == "add"),
+                                       nrows, ncols, len(rows), src.ctypes.data, rows.ctypes.data, cols.ctypes.data,
+                                       vals.ctypes.data, blocks, rs.ctypes.data, cs.ctypes.data)
+        if rc != 0:
+            raise RuntimeError(f"ref_redistribute failed: {rc}")
+        return [(int(rs[r]), int(cs[r]), _from_c(blocks[r], DTYPES[sr], self.lib.ref_free)) for r in range(p)]
+
     def merge(self, sr, parts) -> Csc:
         keep = []
         arr = (_CCsc * len(parts))(*[_as_c(p, keep) for p in parts])
@@ -330,6 +352,61 @@ def from_triples(nrows, ncols, rows, cols, vals, combine="first") -> Csc:
     np.add.at(colptr, c + 1, 1)
     colptr = np.cumsum(colptr).astype(np.int64)
     return Csc(nrows, ncols, colptr, r.astype(np.int32), v)
+
+
+def _sr_add(sr, x, y):
+    """semiring.hpp:36-93 add on the element type."""
+    if sr in (PLUS_TIMES_F64, PLUS_TIMES_F32, PLUS_TIMES_I64):
+        return (x + y).astype(x.dtype) if hasattr(x, "astype") else x + y
+    if sr in (MIN_PLUS_I32, MIN_PLUS_F64):
+        return x if x < y else y
+    return np.uint8(1 if (x or y) else 0)
+
+
+def redistribute(sr, tiling_rows, tiling_cols, owner, nrows, ncols, parts, combine="first"):
+    """Restatement of one routed redistribution (dist_matrix.hpp:89-119,
+    dist_matrix3d.hpp:117-174, local_matrix.hpp:167-188): `parts[r]` are the
+    global (rows, cols, vals) triples of source rank r in its push order; every
+    entry goes to the owner of the tile (block_of on the cuts) holding it; a
+    target assembles its arrivals (source-rank order) with a stable
+    (col, row) sort, keeping the first duplicate or folding the semiring add
+    left.  Returns {rank: (row_start, col_start, Csc)}."""
+    import bisect
+
+    nr, nc = len(tiling_rows) - 1, len(tiling_cols) - 1
+    inbox = {o: ([], [], []) for o in owner}
+    for rows, cols, vals in parts:
+        for r, c, v in zip(np.asarray(rows).tolist(), np.asarray(cols).tolist(), np.asarray(vals)):
+            if not (0 <= r < nrows and 0 <= c < ncols):
+                raise IndexError(f"triple ({r},{c}) outside {nrows}x{ncols}")
+            ti = bisect.bisect_right(tiling_rows, r) - 1
+            tj = bisect.bisect_right(tiling_cols, c) - 1
+            ti, tj = min(ti, nr - 1), min(tj, nc - 1)
+            box = inbox[owner[ti * nc + tj]]
+            box[0].append(r - tiling_rows[ti])
+            box[1].append(c - tiling_cols[tj])
+            box[2].append(v)
+    out = {}
+    for k, o in enumerate(owner):
+        ti, tj = divmod(k, nc)
+        tr, tc = tiling_rows[ti + 1] - tiling_rows[ti], tiling_cols[tj + 1] - tiling_cols[tj]
+        lr, lc, lv = inbox[o]
+        dtype = DTYPES[sr]
+        order = sorted(range(len(lr)), key=lambda e: (lc[e], lr[e]))  # stable
+        rr, cc, vv = [], [], []
+        for e in order:
+            if rr and rr[-1] == lr[e] and cc[-1] == lc[e]:
+                if combine == "add":
+                    vv[-1] = dtype(_sr_add(sr, dtype(vv[-1]), dtype(lv[e])))
+                continue
+            rr.append(lr[e])
+            cc.append(lc[e])
+            vv.append(dtype(lv[e]))
+        colptr = np.zeros(tc + 1, np.int64)
+        np.add.at(colptr, np.asarray(cc, np.int64) + 1, 1)
+        out[o] = (tiling_rows[ti], tiling_cols[tj],
+                  Csc(tr, tc, np.cumsum(colptr).astype(np.int64), np.asarray(rr, np.int32), np.asarray(vv, dtype)))
+    return out
 
 
 def random_triples(rng_seed, m, n, density, val_kind, dtype):

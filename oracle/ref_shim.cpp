@@ -17,6 +17,7 @@
 #include <cstring>
 #include <exception>
 #include <limits>
+#include <type_traits>
 #include <vector>
 
 #include "slap/algorithms.hpp"
@@ -135,6 +136,29 @@ int error_code(const std::exception& e) {
         if (err->kind() == "StochasticityError") return -8;
     }
     return -1;
+}
+
+
+// Block-local CSC of a DCSC / CSC local block (for_each_col order).
+template <class M>
+void from_local(const M& m, int64_t nrows, int64_t ncols, ref_csc* out) {
+    using VT = std::remove_cv_t<std::remove_reference_t<decltype(m.vals()[0])>>;
+    out->nrows = nrows;
+    out->ncols = ncols;
+    out->nnz = static_cast<int64_t>(m.nnz());
+    out->colptr = static_cast<int64_t*>(std::calloc(static_cast<std::size_t>(ncols) + 1, sizeof(int64_t)));
+    out->rowids = static_cast<int32_t*>(std::malloc(sizeof(int32_t) * (m.nnz() ? m.nnz() : 1)));
+    out->vals = std::malloc(sizeof(VT) * (m.nnz() ? m.nnz() : 1));
+    VT* ov = static_cast<VT*>(out->vals);
+    int64_t e = 0;
+    m.for_each_col([&](auto cv) {
+        out->colptr[cv.col + 1] = static_cast<int64_t>(cv.nnz());
+        for (std::size_t k = 0; k < cv.nnz(); ++k, ++e) {
+            out->rowids[e] = cv.rows[k];
+            ov[e] = cv.vals[k];
+        }
+    });
+    for (int64_t j = 0; j < ncols; ++j) out->colptr[j + 1] += out->colptr[j];
 }
 
 }  // namespace
@@ -413,6 +437,58 @@ int ref_merge(int sr, int nparts, const ref_csc* parts, ref_csc* out) {
             }
             auto csc = build_csc(t, [&](const VT& x, const VT& y) { return s.add(x, y); });
             from_csc(csc, out);
+            return 0;
+        });
+    } catch (const std::exception& e) {
+        return error_code(e);
+    }
+}
+
+/// distribute_triples (dist_matrix.hpp:89-119) of triples held by source
+/// ranks src[k] onto a pr x pc grid, duplicates combined keep-first
+/// (combine 0) or with the semiring add (1); mode 1 continues with
+/// redistribute_3d(layers, split) (dist_matrix3d.hpp:117-170, regular), mode
+/// 2 with redistribute_2d back to the pr x pc grid (:250-261).  Rank r's
+/// resulting local block goes to blocks[r] (block-local CSC) with its global
+/// offsets.
+int ref_redistribute(int sr, int p, int pr, int pc, int mode, int layers, int split_rows, int combine,
+                     int64_t nrows, int64_t ncols, int64_t n, const int32_t* src, const int64_t* rows,
+                     const int64_t* cols, const void* vals, ref_csc* blocks, int64_t* row_start, int64_t* col_start) {
+    try {
+        return with_semiring(sr, [&](auto s) -> int {
+            using VT = typename decltype(s)::left_type;
+            const VT* v = static_cast<const VT*>(vals);
+            run_world(p, [&](Comm& w) {
+                Triples<GlobalIdx, VT> mine;
+                mine.nrows = nrows;
+                mine.ncols = ncols;
+                for (int64_t k = 0; k < n; ++k)
+                    if (src[k] == w.rank()) mine.push_back(rows[k], cols[k], v[k]);
+                auto g = make_grid2d(w, pr, pc);
+                auto first = [](const VT& x, const VT&) { return x; };
+                auto add = [&](const VT& x, const VT& y) { return static_cast<VT>(s.add(x, y)); };
+                auto d2 = combine ? distribute_triples(mine, g, nrows, ncols, add)
+                                  : distribute_triples(mine, g, nrows, ncols, first);
+                const int r = w.rank();
+                if (mode == 0) {
+                    from_local(d2.local, d2.row_end() - d2.row_start(), d2.col_end() - d2.col_start(), &blocks[r]);
+                    row_start[r] = d2.row_start();
+                    col_start[r] = d2.col_start();
+                    return;
+                }
+                auto g3 = make_grid3d(w, layers);
+                auto d3 = redistribute_3d(d2, g3, split_rows ? SplitDim::rows : SplitDim::cols);
+                if (mode == 1) {
+                    from_local(d3.local, d3.row_len, d3.col_len, &blocks[r]);
+                    row_start[r] = d3.row_start;
+                    col_start[r] = d3.col_start;
+                    return;
+                }
+                auto b2 = redistribute_2d(d3, g);
+                from_local(b2.local, b2.row_end() - b2.row_start(), b2.col_end() - b2.col_start(), &blocks[r]);
+                row_start[r] = b2.row_start();
+                col_start[r] = b2.col_start();
+            });
             return 0;
         });
     } catch (const std::exception& e) {

@@ -82,6 +82,18 @@ class DistStats(C.Structure):
     ]
 
 
+class Tiling(C.Structure):
+    """slapcu_tiling (host pointers; see grid.tiling_2d / tiling_3d)."""
+
+    _fields_ = [
+        ("nr", C.c_int),
+        ("nc", C.c_int),
+        ("row_cuts", C.c_void_p),
+        ("col_cuts", C.c_void_p),
+        ("owner", C.c_void_p),
+    ]
+
+
 # (name, restype, argtypes) for every entry point of include/slapcu.h
 _P = C.c_void_p
 _I = C.c_int
@@ -132,6 +144,10 @@ SIGNATURES = [
     ("slapcu_comm_counters", _I, [_P, _I, C.POINTER(_L), C.POINTER(_L)]),
     ("slapcu_summa2d", _I, [_P, _PV, _PV, _I, _I, _PO, C.POINTER(DistStats)]),
     ("slapcu_ca3d", _I, [_P, _I, _PV, _PV, _I, _I, _PO, C.POINTER(DistStats)]),
+    ("slapcu_redistribute", _I, [_P, _PV, _L, _L, _L, _L, _I, C.POINTER(Tiling), _I, _PO, C.POINTER(_L),
+                                 C.POINTER(_L)]),
+    ("slapcu_distribute_triples", _I, [_P, _L, _P, _P, _P, _L, _L, _I, C.POINTER(Tiling), _I, _PO, C.POINTER(_L),
+                                       C.POINTER(_L)]),
 ]
 
 _lib = None

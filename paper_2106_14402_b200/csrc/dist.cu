@@ -32,27 +32,10 @@
 
 #include "kern.cuh"
 
-#define SLAPCU_NCCL(call)                                                                               \
-    do {                                                                                                \
-        ncclResult_t r_ = (call);                                                                       \
-        if (r_ != ncclSuccess)                                                                          \
-            throw ::slapcu::Fail{SLAPCU_ERR_COMM, std::string(#call) + ": " + ncclGetErrorString(r_)};  \
-    } while (0)
-
-struct slapcu_comm_s {
-    slapcu_ctx ctx = nullptr;
-    int rank = 0, nranks = 1;
-    ncclComm_t world = nullptr;
-    std::map<std::string, ncclComm_t> splits;
-    cudaStream_t comm_stream = nullptr;
-    int64_t calls[4] = {0, 0, 0, 0};
-    int64_t bytes[4] = {0, 0, 0, 0};
-};
+#include "comm.hpp"
 
 namespace slapcu {
 namespace {
-
-enum { kBcast = 0, kAlltoallv = 1, kReduce = 2, kAllgatherv = 3 };
 
 bool is_square(int64_t v, int64_t* root) {
     if (v < 0) return false;

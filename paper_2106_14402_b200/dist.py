@@ -174,3 +174,100 @@ def gather_to_host(local: DeviceCsc, row_start: int, col_start: int, nrows: int,
         return None
     cp, rw, vv = G.assemble(nrows, ncols, parts)
     return CscMatrix(nrows, ncols, cp, rw, vv.astype(h.vals.dtype) if h.vals is not None else vv)
+
+
+# ------------------------------------------------------------ redistribution
+
+
+def _tiling_struct(t: G.Tiling):
+    rc = np.ascontiguousarray(t.row_cuts, np.int64)
+    cc = np.ascontiguousarray(t.col_cuts, np.int64)
+    ow = np.ascontiguousarray(t.owner, np.int32)
+    st = L.Tiling(t.nr, t.nc, rc.ctypes.data, cc.ctypes.data, ow.ctypes.data)
+    return st, (rc, cc, ow)
+
+
+_COMBINE = {"first": 0, "add": 1}
+
+
+def redistribute(local: DeviceCsc, row_start: int, col_start: int, nrows: int, ncols: int, sr: Semiring,
+                 comm: NcclComm, target: G.Tiling, combine: str = "first"):
+    """Collective: re-route this rank's block (global offsets row_start /
+    col_start) to the target tiling; returns (tile as DeviceCsc, row_start,
+    col_start) of this rank's target tile.  slapcu_redistribute."""
+    sr = _sr(sr)
+    ctx = comm.ctx
+    ctx.sync_stream()
+    tl, keep = _tiling_struct(target)
+    out = L.CscOut()
+    rs, cs = C.c_int64(), C.c_int64()
+    ctx.check(comm.lib.slapcu_redistribute(comm.h, C.byref(local.view()), row_start, col_start, nrows, ncols, sr.id,
+                                           C.byref(tl), _COMBINE[combine], C.byref(out), C.byref(rs), C.byref(cs)),
+              "redistribute")
+    del keep
+    return _from_out(ctx, out, sr), int(rs.value), int(cs.value)
+
+
+def distribute_triples(rows: torch.Tensor, cols: torch.Tensor, vals: torch.Tensor, nrows: int, ncols: int,
+                       sr: Semiring, comm: NcclComm, pr: int | None = None, pc: int | None = None,
+                       combine: str = "first", target: G.Tiling | None = None):
+    """dist_matrix.hpp:89-119 distribute_triples: this rank's global COO
+    triples (device int64 rows / cols, values of the semiring type) routed to
+    the pr x pc block layout (default sqrt(p) x sqrt(p)); duplicates keep the
+    first (combine="first") or fold with the semiring add ("add").  Returns
+    (block, row_start, col_start)."""
+    sr = _sr(sr)
+    if target is None:
+        if pr is None or pc is None:
+            q = G.isqrt_exact(comm.size)
+            pr, pc = q, q
+        if pr * pc != comm.size:
+            raise E.ShapeError(f"{pr}x{pc} grid on {comm.size} ranks")
+        target = G.tiling_2d(nrows, ncols, pr, pc)
+    ctx = comm.ctx
+    rows = rows.to(torch.int64).contiguous()
+    cols = cols.to(torch.int64).contiguous()
+    vals = vals.contiguous()
+    if vals.dtype != sr.torch_dtype:
+        raise E.ShapeError(f"values must be {sr.torch_dtype} for {sr.name}")
+    ctx.sync_stream()
+    tl, keep = _tiling_struct(target)
+    out = L.CscOut()
+    rs, cs = C.c_int64(), C.c_int64()
+    ctx.check(comm.lib.slapcu_distribute_triples(comm.h, rows.numel(), rows.data_ptr(), cols.data_ptr(),
+                                                 vals.data_ptr(), nrows, ncols, sr.id, C.byref(tl),
+                                                 _COMBINE[combine], C.byref(out), C.byref(rs), C.byref(cs)),
+              "distribute_triples")
+    del keep
+    return _from_out(ctx, out, sr), int(rs.value), int(cs.value)
+
+
+def redistribute_3d(a2: DeviceCsc, nrows: int, ncols: int, sr: Semiring, comm: NcclComm, layers: int,
+                    split: str, pr: int | None = None, pc: int | None = None):
+    """dist_matrix3d.hpp:117-170 redistribute_3d (regular variant): this
+    rank's block of the pr x pc 2D layout (default sqrt(p) x sqrt(p)) to its
+    block of the c x q x q layout split by `split` ("cols" for A, "rows" for
+    B).  Returns (block, row_start, col_start)."""
+    p = comm.size
+    if pr is None or pc is None:
+        q2 = G.isqrt_exact(p)
+        pr, pc = q2, q2
+    if pr * pc != p:
+        raise E.ShapeError(f"3D grid has {p} ranks, matrix lives on {pr * pc}")
+    g = G.Grid3D.make(p, layers, comm.rank)
+    r0, _, c0, _ = G.block2d_range(nrows, ncols, pr, pc, comm.rank // pc, comm.rank % pc)
+    return redistribute(a2, r0, c0, nrows, ncols, sr, comm, G.tiling_3d(nrows, ncols, layers, g.q, split))
+
+
+def redistribute_2d(a3: DeviceCsc, row_start: int, col_start: int, nrows: int, ncols: int, sr: Semiring,
+                    comm: NcclComm, pr: int | None = None, pc: int | None = None):
+    """dist_matrix3d.hpp:250-261 redistribute_2d: any block with known global
+    offsets (a 3D operand, or a ca3d_spgemm output at ca3d_output_range) back
+    to the pr x pc 2D layout.  Returns (block, row_start, col_start)."""
+    p = comm.size
+    if pr is None or pc is None:
+        q2 = G.isqrt_exact(p)
+        pr, pc = q2, q2
+    if pr * pc != p:
+        raise E.ShapeError(f"{pr}x{pc} grid on {p} ranks")
+    return redistribute(a3, row_start, col_start, nrows, ncols, sr, comm, G.tiling_2d(nrows, ncols, pr, pc))

@@ -146,6 +146,69 @@ def ca3d_output_range(m: int, n_b: int, c: int, q: int, l: int, i: int, j: int):
     return ro[i], ro[i + 1] - ro[i], co[j] + piece[l], piece[l + 1] - piece[l]
 
 
+# ------------------------------------------------- redistribution tilings
+#
+# A target layout for slapcu_redistribute / slapcu_distribute_triples: row
+# cuts, column cuts and owner[i][j] = the rank holding tile (i, j).
+
+
+@dataclass(frozen=True)
+class Tiling:
+    row_cuts: tuple
+    col_cuts: tuple
+    owner: tuple  # row-major nr x nc ranks
+
+    @property
+    def nr(self) -> int:
+        return len(self.row_cuts) - 1
+
+    @property
+    def nc(self) -> int:
+        return len(self.col_cuts) - 1
+
+    def tile_of(self, rank: int):
+        """(row_start, row_len, col_start, col_len) of `rank`'s tile."""
+        k = self.owner.index(rank)
+        i, j = divmod(k, self.nc)
+        return (self.row_cuts[i], self.row_cuts[i + 1] - self.row_cuts[i], self.col_cuts[j],
+                self.col_cuts[j + 1] - self.col_cuts[j])
+
+
+def tiling_2d(m: int, n: int, pr: int, pc: int) -> Tiling:
+    """distribute_triples / redistribute_2d target (dist_matrix.hpp:95-97
+    block_offsets rows/cols, grid.hpp:15-24 rank = i*pc + j)."""
+    return Tiling(tuple(block_offsets(m, pr)), tuple(block_offsets(n, pc)),
+                  tuple(i * pc + j for i in range(pr) for j in range(pc)))
+
+
+def tiling_3d(m: int, n: int, c: int, q: int, split: str) -> Tiling:
+    """redistribute_3d regular target (dist_matrix3d.hpp:54-80 and :144-166):
+    the split dimension cut into c slabs, each slab into q sub-blocks; the
+    other dimension into q blocks; tile (l, i, j) on rank l*q*q + i*q + j."""
+    if split not in ("cols", "rows"):
+        raise E.ShapeError(f"split must be 'cols' or 'rows', got {split!r}")
+    ext = n if split == "cols" else m
+    slabs = block_offsets(ext, c)
+    cuts = []
+    for l in range(c):
+        sub = block_offsets(slabs[l + 1] - slabs[l], q)
+        cuts += [slabs[l] + x for x in sub[:-1]]
+    cuts.append(ext)
+    other = block_offsets(m if split == "cols" else n, q)
+    owner = []
+    if split == "cols":  # rows: q blocks (i); cols: c*q pieces (l, j)
+        for i in range(q):
+            for lj in range(c * q):
+                l, j = divmod(lj, q)
+                owner.append(l * q * q + i * q + j)
+        return Tiling(tuple(other), tuple(cuts), tuple(owner))
+    for li in range(c * q):  # rows: c*q pieces (l, i); cols: q blocks (j)
+        l, i = divmod(li, q)
+        for j in range(q):
+            owner.append(l * q * q + i * q + j)
+    return Tiling(tuple(cuts), tuple(other), tuple(owner))
+
+
 # ----------------------------------------------------- host block utilities
 
 
