@@ -44,7 +44,9 @@ typedef enum {
     SLAPCU_ERR_CUDA = 8,     /* CUDA runtime failure                               */
     SLAPCU_ERR_NOMEM = 9,    /* device allocation failure                          */
     SLAPCU_ERR_COMM = 10,    /* NCCL failure / collective mismatch (DeadlockError) */
-    SLAPCU_ERR_STOCHASTIC = 11 /* StochasticityError (algorithms.cpp:271-275, mcl_step input) */
+    SLAPCU_ERR_STOCHASTIC = 11, /* StochasticityError (algorithms.cpp:271-275, mcl_step input) */
+    SLAPCU_ERR_IO = 12,         /* IoError     (binary_io.cpp, mm_io.cpp:15-20)             */
+    SLAPCU_ERR_FORMAT = 13      /* FormatError (binary_io.cpp: magic / version / truncation) */
 } slapcu_status;
 
 /* semiring.hpp:36-93.  Ids are stable (shared with oracle/oracle.h). */
@@ -384,6 +386,31 @@ slapcu_status slapcu_distribute_triples(slapcu_comm comm, int64_t count, const i
                                         const void* vals, int64_t nrows, int64_t ncols, slapcu_semiring sr,
                                         const slapcu_tiling* target, int combine, slapcu_csc_out* out,
                                         int64_t* out_row_start, int64_t* out_col_start);
+
+
+/* ------------------------------------------------ CB2B binary I/O (8f rank 4)
+ *
+ * binary_io.hpp:10-28 format: "CB2B", uint32 version 1, int64 nrows / ncols /
+ * nnz, then nnz records (int64 row, int64 col, f64 value), little-endian.
+ * Values are f64 (semiring PLUS_TIMES_F64 or MIN_PLUS_F64 blocks). */
+
+/* Header only (no communicator): SLAPCU_ERR_IO if unreadable,
+ * SLAPCU_ERR_FORMAT on bad magic / version / size mismatch. */
+slapcu_status slapcu_cb2b_header(const char* path, int64_t* nrows, int64_t* ncols, int64_t* nnz);
+
+/* write_binary (binary_io.cpp): rank 0 writes the header, every rank writes
+ * its block's records (column-major block order, global indices) at its
+ * exclusive-scan offset -- records are built on the device and streamed
+ * through pinned buffers.  Collective; the file is complete on return. */
+slapcu_status slapcu_write_cb2b(slapcu_comm comm, const char* path, const slapcu_csc* local, int64_t row_start,
+                                int64_t col_start, int64_t nrows, int64_t ncols);
+
+/* read_binary (binary_io.cpp): rank r reads records [nnz*r/p, nnz*(r+1)/p),
+ * streams them to the device, and the entries are routed to the pr x pc 2D
+ * layout (rank = i*pc + j) by the redistribution above (keep-first).  Returns
+ * this rank's block (allocated), its global offsets and the global dims. */
+slapcu_status slapcu_read_cb2b(slapcu_comm comm, const char* path, int pr, int pc, slapcu_csc_out* out,
+                               int64_t* out_row_start, int64_t* out_col_start, int64_t* nrows, int64_t* ncols);
 
 #ifdef __cplusplus
 }

@@ -165,6 +165,26 @@ class _Port:
             raise RuntimeError(f"orc_spgemm failed: {rc}")
         return _from_c(out, DTYPES[sr], self.lib.orc_free)
 
+    def write_binary(self, a: Csc, path: str, p=1, pr=1, pc=1):
+        """binary_io.cpp write_binary of f64 `a` distributed on pr x pc ranks."""
+        keep = []
+        rc = self.lib.ref_write_binary(p, pr, pc, C.byref(_as_c(a, keep)), path.encode())
+        if rc != 0:
+            raise RuntimeError(f"ref_write_binary failed: {rc}")
+
+    def read_binary(self, path: str, p=1, pr=1, pc=1):
+        """binary_io.cpp read_binary -> [(row_start, col_start, block)] per rank;
+        raises ValueError("IoError" / "FormatError")."""
+        blocks = (_CCsc * p)()
+        rs = np.zeros(p, np.int64)
+        cs = np.zeros(p, np.int64)
+        rc = self.lib.ref_read_binary(path.encode(), p, pr, pc, blocks, rs.ctypes.data, cs.ctypes.data)
+        if rc in (-9, -10):
+            raise ValueError("IoError" if rc == -9 else "FormatError")
+        if rc != 0:
+            raise RuntimeError(f"ref_read_binary failed: {rc}")
+        return [(int(rs[r]), int(cs[r]), _from_c(blocks[r], np.float64, self.lib.ref_free)) for r in range(p)]
+
     def merge(self, sr, parts) -> Csc:
         keep = []
         arr = (_CCsc * len(parts))(*[_as_c(p, keep) for p in parts])
@@ -198,6 +218,8 @@ class _Ref:
         L.ref_mcl_step.argtypes = [C.c_int, C.c_int, P, C.c_double, C.c_double, P]
         L.ref_redistribute.argtypes = [C.c_int] * 8 + [C.c_int64] * 3 + [C.c_void_p] * 4 + [P, C.c_void_p,
                                                                                             C.c_void_p]
+        L.ref_write_binary.argtypes = [C.c_int, C.c_int, C.c_int, P, C.c_char_p]
+        L.ref_read_binary.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, P, C.c_void_p, C.c_void_p]
         L.ref_free.argtypes = [C.c_void_p]
         L.ref_time_local_spgemm.argtypes = [C.c_int, C.c_int, C.c_int, P, P, C.c_int64, C.c_int64,
                                             C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
@@ -304,6 +326,26 @@ class _Ref:
             raise RuntimeError(f"ref_redistribute failed: {rc}")
         return [(int(rs[r]), int(cs[r]), _from_c(blocks[r], DTYPES[sr], self.lib.ref_free)) for r in range(p)]
 
+    def write_binary(self, a: Csc, path: str, p=1, pr=1, pc=1):
+        """binary_io.cpp write_binary of f64 `a` distributed on pr x pc ranks."""
+        keep = []
+        rc = self.lib.ref_write_binary(p, pr, pc, C.byref(_as_c(a, keep)), path.encode())
+        if rc != 0:
+            raise RuntimeError(f"ref_write_binary failed: {rc}")
+
+    def read_binary(self, path: str, p=1, pr=1, pc=1):
+        """binary_io.cpp read_binary -> [(row_start, col_start, block)] per rank;
+        raises ValueError("IoError" / "FormatError")."""
+        blocks = (_CCsc * p)()
+        rs = np.zeros(p, np.int64)
+        cs = np.zeros(p, np.int64)
+        rc = self.lib.ref_read_binary(path.encode(), p, pr, pc, blocks, rs.ctypes.data, cs.ctypes.data)
+        if rc in (-9, -10):
+            raise ValueError("IoError" if rc == -9 else "FormatError")
+        if rc != 0:
+            raise RuntimeError(f"ref_read_binary failed: {rc}")
+        return [(int(rs[r]), int(cs[r]), _from_c(blocks[r], np.float64, self.lib.ref_free)) for r in range(p)]
+
     def merge(self, sr, parts) -> Csc:
         keep = []
         arr = (_CCsc * len(parts))(*[_as_c(p, keep) for p in parts])
@@ -407,6 +449,30 @@ def redistribute(sr, tiling_rows, tiling_cols, owner, nrows, ncols, parts, combi
         out[o] = (tiling_rows[ti], tiling_cols[tj],
                   Csc(tr, tc, np.cumsum(colptr).astype(np.int64), np.asarray(rr, np.int32), np.asarray(vv, dtype)))
     return out
+
+
+CB2B_RECORD = np.dtype([("row", "<i8"), ("col", "<i8"), ("val", "<f8")])
+
+
+def read_cb2b(path):
+    """binary_io.hpp:10-28 restated: (nrows, ncols, records) of a CB2B v1
+    file; ValueError("FormatError") on bad magic / version / size."""
+    raw = open(path, "rb").read()
+    if len(raw) < 32 or raw[:4] != b"CB2B" or np.frombuffer(raw[4:8], "<u4")[0] != 1:
+        raise ValueError("FormatError")
+    m, n, nnz = (int(x) for x in np.frombuffer(raw[8:32], "<i8"))
+    if m < 0 or n < 0 or nnz < 0 or len(raw) != 32 + 24 * nnz:
+        raise ValueError("FormatError")
+    return m, n, np.frombuffer(raw[32:], CB2B_RECORD)
+
+
+def write_cb2b(path, nrows, ncols, rows, cols, vals):
+    """binary_io.hpp:10-28 restated writer (records in the given order)."""
+    rec = np.empty(len(rows), CB2B_RECORD)
+    rec["row"], rec["col"], rec["val"] = rows, cols, vals
+    with open(path, "wb") as f:
+        f.write(b"CB2B" + np.uint32(1).tobytes() + np.asarray([nrows, ncols, len(rows)], "<i8").tobytes())
+        f.write(rec.tobytes())
 
 
 def random_triples(rng_seed, m, n, density, val_kind, dtype):

@@ -22,6 +22,7 @@
 
 #include "slap/algorithms.hpp"
 #include "slap/batched.hpp"
+#include "slap/binary_io.hpp"
 #include "slap/spgemm.hpp"
 #include "slap/spgemm3d.hpp"
 #include "slap/summa.hpp"
@@ -492,6 +493,52 @@ int ref_redistribute(int sr, int p, int pr, int pc, int mode, int layers, int sp
             return 0;
         });
     } catch (const std::exception& e) {
+        return error_code(e);
+    }
+}
+
+/// write_binary (binary_io.cpp) of the global f64 matrix `a` distributed by
+/// distribute_triples onto pr x pc rank threads.
+int ref_write_binary(int p, int pr, int pc, const ref_csc* a, const char* path) {
+    try {
+        auto t = to_triples64<double>(*a);
+        run_world(p, [&](Comm& w) {
+            auto g = make_grid2d(w, pr, pc);
+            Triples<GlobalIdx, double> mine;
+            mine.nrows = t.nrows;
+            mine.ncols = t.ncols;
+            if (w.rank() == 0) mine = t;
+            auto first = [](const double& x, const double&) { return x; };
+            write_binary(distribute_triples(mine, g, t.nrows, t.ncols, first), path);
+        });
+        return 0;
+    } catch (const std::exception& e) {
+        if (const auto* err = dynamic_cast<const Error*>(&e)) {
+            if (err->kind() == "IoError") return -9;
+            if (err->kind() == "FormatError") return -10;
+        }
+        return error_code(e);
+    }
+}
+
+/// read_binary (binary_io.cpp) onto pr x pc rank threads; rank r's block to
+/// blocks[r] with its global offsets.
+int ref_read_binary(const char* path, int p, int pr, int pc, ref_csc* blocks, int64_t* row_start, int64_t* col_start) {
+    try {
+        run_world(p, [&](Comm& w) {
+            auto g = make_grid2d(w, pr, pc);
+            auto d = read_binary(path, g);
+            const int r = w.rank();
+            from_local(d.local, d.row_end() - d.row_start(), d.col_end() - d.col_start(), &blocks[r]);
+            row_start[r] = d.row_start();
+            col_start[r] = d.col_start();
+        });
+        return 0;
+    } catch (const std::exception& e) {
+        if (const auto* err = dynamic_cast<const Error*>(&e)) {
+            if (err->kind() == "IoError") return -9;
+            if (err->kind() == "FormatError") return -10;
+        }
         return error_code(e);
     }
 }

@@ -146,6 +146,10 @@ SIGNATURES = [
     ("slapcu_ca3d", _I, [_P, _I, _PV, _PV, _I, _I, _PO, C.POINTER(DistStats)]),
     ("slapcu_redistribute", _I, [_P, _PV, _L, _L, _L, _L, _I, C.POINTER(Tiling), _I, _PO, C.POINTER(_L),
                                  C.POINTER(_L)]),
+    ("slapcu_cb2b_header", _I, [C.c_char_p, C.POINTER(_L), C.POINTER(_L), C.POINTER(_L)]),
+    ("slapcu_write_cb2b", _I, [_P, C.c_char_p, _PV, _L, _L, _L, _L]),
+    ("slapcu_read_cb2b", _I, [_P, C.c_char_p, _I, _I, _PO, C.POINTER(_L), C.POINTER(_L), C.POINTER(_L),
+                              C.POINTER(_L)]),
     ("slapcu_distribute_triples", _I, [_P, _L, _P, _P, _P, _L, _L, _I, C.POINTER(Tiling), _I, _PO, C.POINTER(_L),
                                        C.POINTER(_L)]),
 ]

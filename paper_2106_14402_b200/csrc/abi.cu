@@ -76,6 +76,8 @@ const char* slapcu_status_name(slapcu_status s) {
     case SLAPCU_ERR_CUDA: return "CudaError";
     case SLAPCU_ERR_NOMEM: return "OutOfMemory";
     case SLAPCU_ERR_COMM: return "DeadlockError";
+    case SLAPCU_ERR_IO: return "IoError";
+    case SLAPCU_ERR_FORMAT: return "FormatError";
     case SLAPCU_ERR_STOCHASTIC: return "StochasticityError";
     }
     return "Unknown";

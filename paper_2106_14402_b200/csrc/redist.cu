@@ -34,7 +34,13 @@
 // the same way before any data moves.
 #include <cub/cub.cuh>
 
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
 #include <algorithm>
+#include <cerrno>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -416,6 +422,128 @@ void redistribute(slapcu_comm_s* cm, Ctx& c, const Src& src, const void* vals, i
     SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
 }
 
+// ------------------------------------------------------------ CB2B binary I/O
+// binary_io.hpp:10-28 / binary_io.cpp.  Records are (int64 row, int64 col,
+// f64 value); they are built / taken apart on the device and streamed
+// through two pinned staging buffers so the file I/O of chunk k overlaps the
+// copy of chunk k-1.
+
+constexpr int64_t kHeaderBytes = 32;
+constexpr int64_t kRecBytes = 24;
+constexpr int64_t kChunkRecs = int64_t(1) << 21;  // 48 MB per staging buffer
+const char kMagic[4] = {'C', 'B', '2', 'B'};
+constexpr uint32_t kVersion = 1;
+
+struct Fd {
+    int fd = -1;
+    ~Fd() {
+        if (fd >= 0) ::close(fd);
+    }
+};
+
+struct Pinned {
+    void* p = nullptr;
+    explicit Pinned(size_t bytes) { SLAPCU_CUDA(cudaHostAlloc(&p, bytes, cudaHostAllocDefault)); }
+    ~Pinned() {
+        if (p) cudaFreeHost(p);
+    }
+};
+
+struct Header {
+    int64_t m = 0, n = 0, nnz = 0;
+};
+
+Header read_header(const char* path) {
+    if (!path) throw Fail{SLAPCU_ERR_INVALID, "null path"};
+    Fd f;
+    f.fd = ::open(path, O_RDONLY);
+    if (f.fd < 0) throw Fail{SLAPCU_ERR_IO, std::string("cannot open '") + path + "': " + std::strerror(errno)};
+    struct stat st {};
+    if (::fstat(f.fd, &st) != 0) throw Fail{SLAPCU_ERR_IO, std::string("cannot stat '") + path + "'"};
+    const int64_t size = st.st_size;
+    if (size < kHeaderBytes) throw Fail{SLAPCU_ERR_FORMAT, "file too short for a binary matrix header"};
+    unsigned char hb[kHeaderBytes];
+    if (::pread(f.fd, hb, kHeaderBytes, 0) != kHeaderBytes) throw Fail{SLAPCU_ERR_IO, "header read failed"};
+    if (std::memcmp(hb, kMagic, 4) != 0) throw Fail{SLAPCU_ERR_FORMAT, std::string("bad magic in '") + path + "'"};
+    uint32_t ver = 0;
+    std::memcpy(&ver, hb + 4, 4);
+    if (ver != kVersion) throw Fail{SLAPCU_ERR_FORMAT, "unsupported binary version " + std::to_string(ver)};
+    Header h;
+    std::memcpy(&h.m, hb + 8, 8);
+    std::memcpy(&h.n, hb + 16, 8);
+    std::memcpy(&h.nnz, hb + 24, 8);
+    if (h.m < 0 || h.n < 0 || h.nnz < 0) throw Fail{SLAPCU_ERR_FORMAT, "negative header field"};
+    if (h.nnz > (INT64_MAX - kHeaderBytes) / kRecBytes || size != kHeaderBytes + h.nnz * kRecBytes)
+        throw Fail{SLAPCU_ERR_FORMAT, "file size " + std::to_string(size) + " does not match " +
+                                          std::to_string(h.nnz) + " declared records"};
+    return h;
+}
+
+void pread_all(int fd, void* dst, int64_t bytes, int64_t off) {
+    char* d = static_cast<char*>(dst);
+    while (bytes > 0) {
+        const ssize_t r = ::pread(fd, d, size_t(std::min<int64_t>(bytes, int64_t(1) << 30)), off);
+        if (r <= 0) throw Fail{SLAPCU_ERR_FORMAT, "truncated record section"};
+        d += r;
+        off += r;
+        bytes -= r;
+    }
+}
+
+void pwrite_all(int fd, const void* src, int64_t bytes, int64_t off) {
+    const char* s_ = static_cast<const char*>(src);
+    while (bytes > 0) {
+        const ssize_t r = ::pwrite(fd, s_, size_t(std::min<int64_t>(bytes, int64_t(1) << 30)), off);
+        if (r <= 0) throw Fail{SLAPCU_ERR_IO, std::string("write failed: ") + std::strerror(errno)};
+        s_ += r;
+        off += r;
+        bytes -= r;
+    }
+}
+
+__global__ void k_split_records(int64_t n, const int64_t* __restrict__ rec, int64_t* __restrict__ rows,
+                                int64_t* __restrict__ cols, int64_t* __restrict__ vals) {
+    for (int64_t w = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; w < 3 * n; w += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t x = rec[w];
+        const int64_t e = w / 3;
+        switch (w - 3 * e) {
+        case 0: rows[e] = x; break;
+        case 1: cols[e] = x; break;
+        default: vals[e] = x; break;
+        }
+    }
+}
+
+__global__ void k_make_records(int64_t n, const int64_t* __restrict__ cp, const int32_t* __restrict__ rw,
+                               const int64_t* __restrict__ v, int64_t ncols, int64_t base, int64_t rs, int64_t cs,
+                               int64_t* __restrict__ rec) {
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t g = base + e;
+        int64_t lo = 0, hi = ncols;  // cp[lo] <= g < cp[hi]
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (cp[mid] <= g) lo = mid; else hi = mid;
+        }
+        rec[3 * e] = rs + rw[g];
+        rec[3 * e + 1] = cs + lo;
+        rec[3 * e + 2] = v[g];
+    }
+}
+
+// All-gather of a few int64 per rank over the world communicator (also the
+// collective's synchronisation point).
+std::vector<int64_t> allgather_small(slapcu_comm_s* cm, Ctx& c, const std::vector<int64_t>& mine) {
+    const int p = cm->nranks, w = int(mine.size());
+    DevBuf d(sizeof(int64_t) * w * (p + 1), c.stream);
+    SLAPCU_CUDA(cudaMemcpyAsync(d.as<int64_t>() + int64_t(w) * p, mine.data(), sizeof(int64_t) * w,
+                                cudaMemcpyHostToDevice, c.stream));
+    SLAPCU_NCCL(ncclAllGather(d.as<int64_t>() + int64_t(w) * p, d.get(), w, ncclInt64, cm->world, c.stream));
+    std::vector<int64_t> all(size_t(w) * p);
+    SLAPCU_CUDA(cudaMemcpyAsync(all.data(), d.get(), sizeof(int64_t) * w * p, cudaMemcpyDeviceToHost, c.stream));
+    SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+    return all;
+}
+
 struct OutGuard {  // frees a half-built output on failure
     Ctx& c;
     slapcu_csc_out* o;
@@ -480,6 +608,194 @@ slapcu_status slapcu_distribute_triples(slapcu_comm cm, int64_t count, const int
         s.grow = rows;
         s.gcol = cols;
         redistribute(cm, c, s, vals, 0, false, nrows, ncols, sr, target, combine, out, out_row_start, out_col_start);
+        guard.ok = true;
+        return SLAPCU_OK;
+    } catch (const Fail& e) {
+        c.last_error = e.msg;
+        return e.st;
+    }
+}
+
+}  // extern "C"
+
+extern "C" {
+
+slapcu_status slapcu_cb2b_header(const char* path, int64_t* nrows, int64_t* ncols, int64_t* nnz) {
+    try {
+        const Header h = read_header(path);
+        if (nrows) *nrows = h.m;
+        if (ncols) *ncols = h.n;
+        if (nnz) *nnz = h.nnz;
+        return SLAPCU_OK;
+    } catch (const Fail& e) {
+        return e.st;
+    }
+}
+
+slapcu_status slapcu_write_cb2b(slapcu_comm cm, const char* path, const slapcu_csc* local, int64_t row_start,
+                                int64_t col_start, int64_t nrows, int64_t ncols) {
+    if (!cm || !local || !path) return SLAPCU_ERR_INVALID;
+    Ctx& c = ctx_of(cm->ctx);
+    try {
+        SLAPCU_CUDA(cudaSetDevice(c.device));
+        DevCsc A = view(*local);
+        resolve(c, A);
+        const int p = cm->nranks, me = cm->rank;
+        const int64_t ne = A.span;
+        if (ne > 0 && !A.v) throw Fail{SLAPCU_ERR_INVALID, "null values"};
+        // records of my block on the device
+        DevBuf rec(size_t(kRecBytes) * std::max<int64_t>(ne, 1), c.stream);
+        if (ne > 0)
+            launch(c, k_make_records, dim3(grid_for(c, ne, 256)), dim3(256), 0, ne, A.cp, A.rw,
+                   static_cast<const int64_t*>(A.v), A.ncols, A.base, row_start, col_start, rec.as<int64_t>());
+        // counts (dist_nnz + exscan, binary_io.cpp) ...
+        auto cnt = allgather_small(cm, c, {ne});
+        int64_t total = 0, before = 0;
+        for (int r = 0; r < p; ++r) {
+            if (r < me) before += cnt[r];
+            total += cnt[r];
+        }
+        // ... rank 0 creates the file with the header; everyone learns whether it could
+        int64_t ok = 1;
+        std::string err;
+        if (me == 0) {
+            Fd f;
+            f.fd = ::open(path, O_WRONLY | O_CREAT | O_TRUNC, 0644);
+            if (f.fd < 0) {
+                ok = 0;
+                err = std::string("cannot create '") + path + "': " + std::strerror(errno);
+            } else {
+                unsigned char hb[kHeaderBytes];
+                std::memcpy(hb, kMagic, 4);
+                std::memcpy(hb + 4, &kVersion, 4);
+                const int64_t dims[3] = {nrows, ncols, total};
+                std::memcpy(hb + 8, dims, sizeof dims);
+                try {
+                    pwrite_all(f.fd, hb, kHeaderBytes, 0);
+                    if (::ftruncate(f.fd, kHeaderBytes + total * kRecBytes) != 0) throw Fail{SLAPCU_ERR_IO, "ftruncate"};
+                } catch (const Fail& e) {
+                    ok = 0;
+                    err = e.msg;
+                }
+            }
+        }
+        auto hdr = allgather_small(cm, c, {ok});
+        if (!hdr[0]) throw Fail{SLAPCU_ERR_IO, me == 0 ? err : "rank 0 could not create '" + std::string(path) + "'"};
+        // my records at 32 + before*24, streamed through two pinned buffers
+        ok = 1;
+        try {
+            Fd f;
+            f.fd = ::open(path, O_WRONLY);
+            if (f.fd < 0) throw Fail{SLAPCU_ERR_IO, std::string("cannot open '") + path + "' for writing"};
+            if (ne > 0) {
+                Pinned buf0(size_t(kChunkRecs) * kRecBytes), buf1(size_t(kChunkRecs) * kRecBytes);
+                void* bufs[2] = {buf0.p, buf1.p};
+                cudaEvent_t ev[2];
+                SLAPCU_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+                SLAPCU_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+                struct Ev {
+                    cudaEvent_t* e;
+                    ~Ev() {
+                        cudaEventDestroy(e[0]);
+                        cudaEventDestroy(e[1]);
+                    }
+                } evg{ev};
+                const int64_t nchunks = (ne + kChunkRecs - 1) / kChunkRecs;
+                auto issue = [&](int64_t k) {
+                    const int64_t o = k * kChunkRecs, m = std::min(kChunkRecs, ne - o);
+                    SLAPCU_CUDA(cudaMemcpyAsync(bufs[k & 1], rec.as<char>() + o * kRecBytes, size_t(m) * kRecBytes,
+                                                cudaMemcpyDeviceToHost, c.stream));
+                    SLAPCU_CUDA(cudaEventRecord(ev[k & 1], c.stream));
+                };
+                issue(0);
+                for (int64_t k = 0; k < nchunks; ++k) {
+                    SLAPCU_CUDA(cudaEventSynchronize(ev[k & 1]));
+                    if (k + 1 < nchunks) issue(k + 1);  // next copy overlaps this write
+                    const int64_t o = k * kChunkRecs, m = std::min(kChunkRecs, ne - o);
+                    pwrite_all(f.fd, bufs[k & 1], m * kRecBytes, kHeaderBytes + (before + o) * kRecBytes);
+                }
+            }
+        } catch (const Fail& e) {
+            ok = 0;
+            err = e.msg;
+        }
+        auto done = allgather_small(cm, c, {ok});
+        for (int r = 0; r < p; ++r)
+            if (!done[r]) throw Fail{SLAPCU_ERR_IO, ok ? "rank " + std::to_string(r) + " failed to write its records" : err};
+        cm->calls[kAllgatherv] += 3;
+        return SLAPCU_OK;
+    } catch (const Fail& e) {
+        c.last_error = e.msg;
+        return e.st;
+    }
+}
+
+slapcu_status slapcu_read_cb2b(slapcu_comm cm, const char* path, int pr, int pc, slapcu_csc_out* out,
+                               int64_t* out_row_start, int64_t* out_col_start, int64_t* nrows, int64_t* ncols) {
+    if (!cm || !path || !out || !out_row_start || !out_col_start) return SLAPCU_ERR_INVALID;
+    Ctx& c = ctx_of(cm->ctx);
+    *out = slapcu_csc_out{};
+    OutGuard guard{c, out};
+    try {
+        SLAPCU_CUDA(cudaSetDevice(c.device));
+        const int p = cm->nranks, me = cm->rank;
+        if (pr < 1 || pc < 1 || int64_t(pr) * pc != p)
+            throw Fail{SLAPCU_ERR_SHAPE, std::to_string(pr) + "x" + std::to_string(pc) + " grid on " +
+                                             std::to_string(p) + " ranks"};
+        const Header h = read_header(path);
+        const int64_t lo = h.nnz * me / p, hi = h.nnz * (me + 1) / p, ne = hi - lo;
+        DevBuf rec(size_t(kRecBytes) * std::max<int64_t>(ne, 1), c.stream);
+        if (ne > 0) {
+            Fd f;
+            f.fd = ::open(path, O_RDONLY);
+            if (f.fd < 0) throw Fail{SLAPCU_ERR_IO, std::string("cannot open '") + path + "'"};
+            Pinned buf0(size_t(kChunkRecs) * kRecBytes), buf1(size_t(kChunkRecs) * kRecBytes);
+            void* bufs[2] = {buf0.p, buf1.p};
+            cudaEvent_t ev[2];
+            SLAPCU_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+            SLAPCU_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+            struct Ev {
+                cudaEvent_t* e;
+                ~Ev() {
+                    cudaEventDestroy(e[0]);
+                    cudaEventDestroy(e[1]);
+                }
+            } evg{ev};
+            const int64_t nchunks = (ne + kChunkRecs - 1) / kChunkRecs;
+            for (int64_t k = 0; k < nchunks; ++k) {
+                if (k >= 2) SLAPCU_CUDA(cudaEventSynchronize(ev[k & 1]));  // buffer free again
+                const int64_t o = k * kChunkRecs, m = std::min(kChunkRecs, ne - o);
+                pread_all(f.fd, bufs[k & 1], m * kRecBytes, kHeaderBytes + (lo + o) * kRecBytes);
+                SLAPCU_CUDA(cudaMemcpyAsync(rec.as<char>() + o * kRecBytes, bufs[k & 1], size_t(m) * kRecBytes,
+                                            cudaMemcpyHostToDevice, c.stream));
+                SLAPCU_CUDA(cudaEventRecord(ev[k & 1], c.stream));
+            }
+            SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+        }
+        const int64_t ne1 = std::max<int64_t>(ne, 1);
+        DevBuf rows(sizeof(int64_t) * ne1, c.stream), cols(sizeof(int64_t) * ne1, c.stream),
+            vals(sizeof(int64_t) * ne1, c.stream);
+        if (ne > 0)
+            launch(c, k_split_records, dim3(grid_for(c, 3 * ne, 256)), dim3(256), 0, ne,
+                   (const int64_t*)rec.as<int64_t>(), rows.as<int64_t>(), cols.as<int64_t>(), vals.as<int64_t>());
+        rec.release();
+        // read_binary routes with distribute_triples onto block_offsets rows / cols
+        std::vector<int64_t> rc(pr + 1), cc(pc + 1);
+        for (int i = 0; i < pr; ++i) rc[i] = int64_t(i) * (h.m / pr);
+        rc[pr] = h.m;
+        for (int j = 0; j < pc; ++j) cc[j] = int64_t(j) * (h.n / pc);
+        cc[pc] = h.n;
+        std::vector<int32_t> owner(size_t(pr) * pc);
+        for (int k = 0; k < pr * pc; ++k) owner[k] = k;
+        slapcu_tiling t{pr, pc, rc.data(), cc.data(), owner.data()};
+        Src s;
+        s.n = ne;
+        s.grow = rows.as<int64_t>();
+        s.gcol = cols.as<int64_t>();
+        redistribute(cm, c, s, vals.get(), 0, false, h.m, h.n, SLAPCU_PLUS_TIMES_F64, &t, 0, out, out_row_start,
+                     out_col_start);
+        if (nrows) *nrows = h.m;
+        if (ncols) *ncols = h.n;
         guard.ok = true;
         return SLAPCU_OK;
     } catch (const Fail& e) {

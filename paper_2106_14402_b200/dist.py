@@ -271,3 +271,44 @@ def redistribute_2d(a3: DeviceCsc, row_start: int, col_start: int, nrows: int, n
     if pr * pc != p:
         raise E.ShapeError(f"{pr}x{pc} grid on {p} ranks")
     return redistribute(a3, row_start, col_start, nrows, ncols, sr, comm, G.tiling_2d(nrows, ncols, pr, pc))
+
+
+# ------------------------------------------------------- CB2B binary I/O
+
+
+def binary_header(path: str, ctx: Context | None = None):
+    """(nrows, ncols, nnz) of a CB2B file (binary_io.hpp:10-28)."""
+    ctx = ctx or default_context()
+    m, n, nnz = C.c_int64(), C.c_int64(), C.c_int64()
+    st = ctx.lib.slapcu_cb2b_header(path.encode(), C.byref(m), C.byref(n), C.byref(nnz))
+    if st != L.OK:
+        raise E.BY_STATUS.get(st, E.Error)(f"{path}")
+    return int(m.value), int(n.value), int(nnz.value)
+
+
+def write_binary(local: DeviceCsc, row_start: int, col_start: int, nrows: int, ncols: int, comm: NcclComm,
+                 path: str):
+    """binary_io.cpp write_binary: collective; f64 values."""
+    if local.vals is None or local.vals.dtype != torch.float64:
+        raise E.InvalidArgument("CB2B files hold f64 values")
+    ctx = comm.ctx
+    ctx.sync_stream()
+    ctx.check(comm.lib.slapcu_write_cb2b(comm.h, path.encode(), C.byref(local.view()), row_start, col_start, nrows,
+                                         ncols), "write_cb2b")
+
+
+def read_binary(path: str, comm: NcclComm, pr: int | None = None, pc: int | None = None):
+    """binary_io.cpp read_binary onto the pr x pc layout (default
+    sqrt(p) x sqrt(p)): returns (block f64, row_start, col_start, nrows, ncols)."""
+    if pr is None or pc is None:
+        q = G.isqrt_exact(comm.size)
+        pr, pc = q, q
+    ctx = comm.ctx
+    ctx.sync_stream()
+    out = L.CscOut()
+    rs, cs, m, n = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+    ctx.check(comm.lib.slapcu_read_cb2b(comm.h, path.encode(), pr, pc, C.byref(out), C.byref(rs), C.byref(cs),
+                                        C.byref(m), C.byref(n)), "read_cb2b")
+    from .spgemm import PlusTimesF64
+
+    return _from_out(ctx, out, PlusTimesF64), int(rs.value), int(cs.value), int(m.value), int(n.value)

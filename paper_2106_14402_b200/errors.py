@@ -60,6 +60,14 @@ class StochasticityError(Error):
     kind = "StochasticityError"
 
 
+class IoError(Error):
+    kind = "IoError"
+
+
+class FormatError(Error):
+    kind = "FormatError"
+
+
 BY_STATUS = {
     1: DimError,
     2: ShapeError,
@@ -72,4 +80,6 @@ BY_STATUS = {
     9: OutOfMemory,
     10: DeadlockError,
     11: StochasticityError,
+    12: IoError,
+    13: FormatError,
 }

@@ -12,6 +12,11 @@ Fixtures:
                              U[0,10)): stage-order fold differs bitwise from
                              the local product
   ca3d_p8_c2_rmat7_i64.npz   slap::ca3d_spgemm on a 2x2x2 grid (i64)
+  cb2b_rmat6_f64.npz         A = gen_rmat(6,16,1), values U[0,10) (f64)
+  cb2b_rmat6_p1.cb2b         slap::write_binary of A distributed on 1x1
+  cb2b_rmat6_p4.cb2b         ... on 2x2 (records rank by rank, each rank's
+                             column-major block order)
+(`python tests/golden/make_golden.py cb2b` regenerates only the CB2B files.)
 """
 import hashlib
 import os
@@ -57,8 +62,19 @@ def main():
     c3 = R.ca3d(oracle.PLUS_TIMES_I64, ai, ai, p=8, pr=2, pc=4, layers=2)
     save("ca3d_p8_c2_rmat7_i64.npz", n=a7.nrows, a_colptr=ai.colptr, a_rowids=ai.rowids, a_vals=ai.vals,
          c_colptr=c3.colptr, c_rowids=c3.rowids, c_vals=c3.vals)
+    cb2b()
     print("fixtures written to", HERE)
 
 
+def cb2b():
+    R = oracle.ref()
+    P = oracle.port()
+    a6 = R.gen_rmat(6, 16, 1)
+    av = a6.with_vals(P.fill_values(oracle.PLUS_TIMES_F64, 2, a6))
+    save("cb2b_rmat6_f64.npz", n=a6.nrows, a_colptr=av.colptr, a_rowids=av.rowids, a_vals=av.vals)
+    R.write_binary(av, os.path.join(HERE, "cb2b_rmat6_p1.cb2b"), p=1, pr=1, pc=1)
+    R.write_binary(av, os.path.join(HERE, "cb2b_rmat6_p4.cb2b"), p=4, pr=2, pc=2)
+
+
 if __name__ == "__main__":
-    main()
+    cb2b() if sys.argv[1:] == ["cb2b"] else main()

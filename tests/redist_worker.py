@@ -13,6 +13,9 @@ pinned to the compiled reference by tests/test_redistribute_host.py):
   * the reference's 3D pipeline end to end (acceptance.cpp:140-160):
     redistribute_3d(A, cols), redistribute_3d(B, rows), ca3d_spgemm,
     redistribute_2d(C3) against the oracle product's 2D block;
+  * CB2B read_binary / write_binary (binary_io.cpp): reading the reference-
+    written fixture gives the routed blocks, writing them back reproduces the
+    reference's bytes, an s+2 R-MAT round-trips, a bad magic is a FormatError;
   * an out-of-range triple on one rank fails with IndexError on EVERY rank,
     and ranks passing different layouts all fail with ShapeError.
 Prints "REDIST_OK p=<p>" on success."""
@@ -150,6 +153,67 @@ def main():
             assert (rs, cs) == (r0, c0)
             cp, rw, vv = G.extract_block(want_c.colptr, want_c.rowids, want_c.vals, r0, rl, c0, cl)
             assert_parity(c2, oracle.Csc(rl, cl, cp, rw, vv), sr.id, f"3D pipeline {sr.name} c={layers}")
+
+    # ---- CB2B binary I/O (binary_io.cpp) against the reference-written fixtures
+    gold = os.path.join(ROOT, "tests", "golden")
+    path4 = os.path.join(gold, "cb2b_rmat6_p4.cb2b")
+    m6, n6, rec = oracle.read_cb2b(path4)
+    nnz6 = len(rec)
+    parts = [(rec["row"][nnz6 * r // p:nnz6 * (r + 1) // p], rec["col"][nnz6 * r // p:nnz6 * (r + 1) // p],
+              rec["val"][nnz6 * r // p:nnz6 * (r + 1) // p]) for r in range(p)]
+    tl = G.tiling_2d(m6, n6, pr, pc)
+    want = oracle.redistribute(oracle.PLUS_TIMES_F64, tl.row_cuts, tl.col_cuts, tl.owner, m6, n6, parts)[rank]
+    blk, rs, cs, mm, nn = D.read_binary(path4, comm, pr, pc)
+    assert (mm, nn) == (m6, n6)
+    same_block((blk, rs, cs), want, "read_binary")
+    # write the blocks back: bytes identical to the reference's write_binary rule
+    obj = [f"/tmp/slapcu_cb2b_{os.getpid()}.cb2b" if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    out_path = obj[0]
+    D.write_binary(blk, rs, cs, m6, n6, comm, out_path)
+    dist.barrier()
+    if rank == 0:
+        z = np.load(os.path.join(gold, "cb2b_rmat6_f64.npz"))
+        a6 = oracle.Csc(int(z["n"]), int(z["n"]), z["a_colptr"], z["a_rowids"], z["a_vals"])
+        rows_w, cols_w, vals_w = [], [], []
+        for r in range(p):
+            r0, rl, c0, cl = G.block2d_range(m6, n6, pr, pc, r // pc, r % pc)
+            cp, rw, vv = G.extract_block(a6.colptr, a6.rowids, a6.vals, r0, rl, c0, cl)
+            cols_w.append(np.repeat(np.arange(cl, dtype=np.int64), np.diff(cp)) + c0)
+            rows_w.append(rw.astype(np.int64) + r0)
+            vals_w.append(vv)
+        want_path = out_path + ".want"
+        oracle.write_cb2b(want_path, m6, n6, np.concatenate(rows_w), np.concatenate(cols_w), np.concatenate(vals_w))
+        got_b = open(out_path, "rb").read()
+        assert got_b == open(want_path, "rb").read(), "write_binary bytes differ from the reference rule"
+        if (pr, pc) in ((1, 1), (2, 2)):
+            assert got_b == open(os.path.join(gold, f"cb2b_rmat6_p{p}.cb2b"), "rb").read()
+        os.remove(want_path)
+    dist.barrier()
+    # round trip at scale
+    A = P.fill_values(P.gen_rmat(a.scale + 2, 16, 7), P.PlusTimesF64, 2)
+    N = A.nrows
+    r0, rl, c0, cl = G.block2d_range(N, N, pr, pc, rank // pc, rank % pc)
+    a2 = D.device_block(A, r0, rl, c0, cl)
+    D.write_binary(a2, r0, c0, N, N, comm, out_path)
+    assert D.binary_header(out_path) == (N, N, A.nnz)
+    back, brs, bcs, _, _ = D.read_binary(out_path, comm, pr, pc)
+    assert (brs, bcs) == (r0, c0)
+    assert torch.equal(back.colptr, a2.colptr) and torch.equal(back.rowids, a2.rowids)
+    assert torch.equal(back.vals, a2.vals)
+    dist.barrier()
+    if rank == 0:
+        with open(out_path, "r+b") as f:
+            f.write(b"XXXX")
+    dist.barrier()
+    try:
+        D.read_binary(out_path, comm, pr, pc)
+        raise AssertionError("expected FormatError")
+    except P.errors.FormatError:
+        pass
+    dist.barrier()
+    if rank == 0:
+        os.remove(out_path)
 
     # ---- errors are raised on every rank
     bad_r = torch.tensor([0, 5 if rank != p - 1 else 10**6], dtype=torch.int64, device=dev)
