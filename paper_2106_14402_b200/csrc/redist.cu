@@ -40,6 +40,9 @@
 
 #include <algorithm>
 #include <cerrno>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -259,6 +262,18 @@ void redistribute(slapcu_comm_s* cm, Ctx& c, const Src& src, const void* vals, i
     const int64_t ne = src.n;
     if (ne > 0 && !vals) throw Fail{SLAPCU_ERR_INVALID, "null values"};
 
+    // phase trace (SLAPCU_REDIST_TRACE=1): host wall time per phase, stream-synchronised
+    static const bool trace = std::getenv("SLAPCU_REDIST_TRACE") != nullptr;
+    auto t_last = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+        if (!trace) return;
+        cudaStreamSynchronize(c.stream);
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[redist r%d] %-10s %8.3f ms\n", me, what,
+                     std::chrono::duration<double, std::milli>(now - t_last).count());
+        t_last = now;
+    };
+    mark("setup");
     // ---- route
     DevBuf cuts(sizeof(int64_t) * (g.nr + g.nc + 2), c.stream), own(sizeof(int32_t) * g.owner.size(), c.stream);
     std::vector<int64_t> hc(g.rc);
@@ -284,6 +299,7 @@ void redistribute(slapcu_comm_s* cm, Ctx& c, const Src& src, const void* vals, i
     }
     const uint64_t dg = digest(g, m, n, sr, combine);
     SLAPCU_CUDA(cudaMemcpyAsync(mine + p + 1, &dg, sizeof(uint64_t), cudaMemcpyHostToDevice, c.stream));
+    mark("route");
     // ---- partition by destination (stable)
     DevBuf order(sizeof(int64_t) * ne1, c.stream);
     const int dbits = std::max(1, bits_for(p));
@@ -308,6 +324,7 @@ void redistribute(slapcu_comm_s* cm, Ctx& c, const Src& src, const void* vals, i
                                 srow.as<int32_t>(), scol.as<int32_t>(), sval.get()); break;
         }
     }
+    mark("partition");
     // ---- exchange: counts / flags / digest, then the entries
     SLAPCU_NCCL(ncclAllGather(mine, meta.get(), W, ncclInt64, cm->world, c.stream));
     std::vector<int64_t> all(size_t(W) * p);
@@ -368,6 +385,7 @@ void redistribute(slapcu_comm_s* cm, Ctx& c, const Src& src, const void* vals, i
     lc.release();
     order.release();
 
+    mark("exchange");
     // ---- assemble the local tile
     out->nrows = tr;
     out->ncols = tc;
@@ -420,6 +438,7 @@ void redistribute(slapcu_comm_s* cm, Ctx& c, const Src& src, const void* vals, i
     launch(c, k_colptr_from_cols, dim3(grid_for(c, tc + 1, 256)), dim3(256), 0, tc, U,
            (const int32_t*)ucol.as<int32_t>(), out->colptr);
     SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+    mark("assemble");
 }
 
 // ------------------------------------------------------------ CB2B binary I/O

@@ -3,7 +3,8 @@ process per GPU: R-MAT s<scale> (ef 16, PlusTimes f64 values) on the
 sqrt(p) x sqrt(p) 2D layout (1 x p when p is not square) is redistributed to
 the c x q x q 3D layout split by columns (redistribute_3d,
 dist_matrix3d.hpp:117-170) and back (redistribute_2d, :250-261), timed with
-CUDA events as the max over ranks.  Also times distribute_triples of the
+CUDA events per step, max over ranks, median step reported (mean and max
+beside it).  Also times distribute_triples of the
 whole matrix held as COO on rank 0 (the reference's test pattern,
 dist_matrix.hpp:89-119).  Rank 0 prints one JSON line per operation:
 entries/s over all ranks and the bytes moved per entry.
@@ -26,6 +27,9 @@ from paper_2106_14402_b200 import dist as D  # noqa: E402
 from paper_2106_14402_b200 import grid as G  # noqa: E402
 
 
+STEPS = []
+
+
 def timed(fn, steps, warmup, comm):
     for _ in range(warmup):
         fn()
@@ -40,17 +44,21 @@ def timed(fn, steps, warmup, comm):
     per = [ev[k].elapsed_time(ev[k + 1]) for k in range(steps)]
     if os.environ.get("REDIST_VERBOSE"):
         print(f"rank {dist.get_rank()} per-step ms: {[round(x, 2) for x in per]}", file=sys.stderr, flush=True)
-    ms = torch.tensor([sum(per) / steps], dtype=torch.float64)
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    return float(ms.item())
+    # per-step max over ranks, then the median step (isolated slow steps --
+    # allocator / host hiccups -- are reported as ms_max, not averaged in)
+    t = torch.tensor(per, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    STEPS.append({"ms_mean": round(float(t.mean()), 3), "ms_max": round(float(t.max()), 3)})
+    return float(t.median())
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--scale", type=int, default=20)
     ap.add_argument("--layers", type=int, default=0, help="0: largest valid c")
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=9)
     ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--ref-scale", type=int, default=18, help="reference CB2B timing scale (p=1 only; 0 = off)")
     a = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     p = int(os.environ.get("WORLD_SIZE", 1))
@@ -99,13 +107,57 @@ def main():
     msd = timed(dtrip, a.steps, a.warmup, comm)
     d = holder["d"][0]
     assert torch.equal(d.colptr, a2.colptr) and torch.equal(d.rowids, a2.rowids) and torch.equal(d.vals, a2.vals)
+    # CB2B write_binary / read_binary through /tmp (binary_io.cpp)
+    obj = [f"/tmp/bench_redist_{os.getpid()}.cb2b" if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    path = obj[0]
+
+    def wr():
+        D.write_binary(a2, r0, c0, N, N, comm, path)
+
+    msw = timed(wr, a.steps, a.warmup, comm)
+
+    def rd():
+        holder["r"] = D.read_binary(path, comm, pr, pc)
+
+    msr = timed(rd, a.steps, a.warmup, comm)
+    rb = holder["r"][0]
+    assert torch.equal(rb.colptr, a2.colptr) and torch.equal(rb.rowids, a2.rowids) and torch.equal(rb.vals, a2.vals)
+    ref_line = None
+    if rank == 0 and p == 1 and a.ref_scale > 0:
+        import time
+
+        import oracle
+
+        if oracle.ref_available():
+            R = oracle.ref()
+            Ar = P.fill_values(P.gen_rmat(a.ref_scale, 16, 1), sr, 2).to_host()
+            ao = oracle.Csc(Ar.nrows, Ar.ncols, Ar.colptr, Ar.rowids, Ar.vals)
+            rp = path + ".ref"
+            t0 = time.perf_counter()
+            R.write_binary(ao, rp)
+            t1 = time.perf_counter()
+            R.read_binary(rp)
+            t2 = time.perf_counter()
+            os.remove(rp)
+            ref_line = {"scale": a.ref_scale, "nnz": ao.nnz, "write_s": round(t1 - t0, 3), "read_s": round(t2 - t1, 3),
+                        "write_entries_per_s": ao.nnz / (t1 - t0), "read_entries_per_s": ao.nnz / (t2 - t1),
+                        "kind": "reference", "cores": 1}
+    dist.barrier()
     if rank == 0:
+        os.remove(path)
         base = {"unit": "entries/s", "n_gpus": p, "scale": a.scale, "nnz": nnz, "pr": pr, "pc": pc,
                 "layers": layers, "steps": a.steps, "warmup": a.warmup, "semiring": "plus_times f64",
                 "wire_bytes_per_entry": 16, "parity": "round trip bit-exact"}
         for op, ms in (("redistribute_3d (2D -> 3D split cols)", ms3), ("redistribute_2d (3D -> 2D)", ms2),
-                       ("distribute_triples (COO on rank 0 -> 2D)", msd)):
-            print(json.dumps(dict(base, op=op, ms=round(ms, 3), value=nnz / (ms * 1e-3))), flush=True)
+                       ("distribute_triples (COO on rank 0 -> 2D)", msd),
+                       ("write_binary (CB2B, /tmp)", msw), ("read_binary (CB2B, /tmp -> 2D)", msr)):
+            line = dict(base, op=op, ms=round(ms, 3), value=nnz / (ms * 1e-3), **STEPS.pop(0))
+            if op.startswith(("write_binary", "read_binary")):
+                line["file_gb_per_s"] = round(nnz * 24 / (ms * 1e-3) / 1e9, 3)
+                if ref_line:
+                    line["cpu_baseline"] = ref_line
+            print(json.dumps(line), flush=True)
     comm.close()
     dist.barrier()
     dist.destroy_process_group()
