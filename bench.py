@@ -506,7 +506,8 @@ def run_ours(args):
 
 def run_e2e_single(args, A, sr, batches, counts, total_flops, ctx, stream):
     """Host-buffer end-to-end: H2D of A (pinned) + per-batch SpGEMM + D2H of
-    every batch's C (chunked into a pinned ring) inside the timed region."""
+    every batch's C (chunked into a pinned ring) inside the timed region; the
+    read-back of batch k overlaps the product of batch k+1."""
     import ctypes as C
 
     import torch
@@ -524,9 +525,14 @@ def run_e2e_single(args, A, sr, batches, counts, total_flops, ctx, stream):
     d_v = torch.empty_like(A.vals)
     max_nnz = max(int(counts[s:e].sum()) for s, e in batches)
     max_cols = max(e - s for s, e in batches)
-    o_cp = torch.empty(max_cols + 1, dtype=torch.int64, device=A.colptr.device)
-    o_rw = torch.empty(max(max_nnz, 1), dtype=torch.int32, device=A.colptr.device)
-    o_v = torch.empty(max(max_nnz, 1), dtype=sr.torch_dtype, device=A.colptr.device)
+    dev = A.colptr.device
+    # two output sets: batch k+1 is computed on the library's stream while
+    # batch k is read back on a copy stream (the D2H is the long pole)
+    outs2 = [(torch.empty(max_cols + 1, dtype=torch.int64, device=dev),
+              torch.empty(max(max_nnz, 1), dtype=torch.int32, device=dev),
+              torch.empty(max(max_nnz, 1), dtype=sr.torch_dtype, device=dev)) for _ in range(2)]
+    copy_stream = torch.cuda.Stream(device=dev)
+    freed = [torch.cuda.Event() for _ in range(2)]
     chunk = 1 << 28  # elements per D2H chunk
     h_out_rw = torch.empty(chunk, dtype=torch.int32).pin_memory()
     h_out_v = torch.empty(chunk, dtype=sr.torch_dtype).pin_memory()
@@ -542,7 +548,10 @@ def run_e2e_single(args, A, sr, batches, counts, total_flops, ctx, stream):
         d_rw.copy_(h_rw, non_blocking=True)
         d_v.copy_(h_v, non_blocking=True)
         av = L.CscView(A.nrows, A.ncols, A.nnz, d_cp.data_ptr(), d_rw.data_ptr(), d_v.data_ptr())
-        for s, e in batches:
+        for k, (s, e) in enumerate(batches):
+            o_cp, o_rw, o_v = outs2[k & 1]
+            if k >= 2:
+                stream.wait_event(freed[k & 1])  # batch k-2's read-back of this set is done
             w = L.CscView(A.nrows, e - s, A.nnz, d_cp.data_ptr() + 8 * s, d_rw.data_ptr(), d_v.data_ptr())
             nz = C.c_int64()
             if args.method == "direct":
@@ -555,14 +564,17 @@ def run_e2e_single(args, A, sr, batches, counts, total_flops, ctx, stream):
                 ctx.check(lib.slapcu_spgemm_finish(ctx.h, C.byref(av), C.byref(w), sr.id, o_rw.data_ptr(),
                                                    o_v.data_ptr()), "finish")
             nzv = int(nz.value)
-            h_out_cp[: e - s + 1].copy_(o_cp[: e - s + 1], non_blocking=True)
-            d2h += (e - s + 1) * 8
-            for o in range(0, nzv, chunk):
-                m = min(chunk, nzv - o)
-                h_out_rw[:m].copy_(o_rw[o:o + m], non_blocking=True)
-                h_out_v[:m].copy_(o_v[o:o + m], non_blocking=True)
-                d2h += m * (4 + vs)
-        torch.cuda.current_stream().synchronize()
+            copy_stream.wait_stream(stream)
+            with torch.cuda.stream(copy_stream):
+                h_out_cp[: e - s + 1].copy_(o_cp[: e - s + 1], non_blocking=True)
+                for o in range(0, nzv, chunk):
+                    m = min(chunk, nzv - o)
+                    h_out_rw[:m].copy_(o_rw[o:o + m], non_blocking=True)
+                    h_out_v[:m].copy_(o_v[o:o + m], non_blocking=True)
+                freed[k & 1].record(copy_stream)
+            d2h += (e - s + 1) * 8 + nzv * (4 + vs)
+        stream.wait_stream(copy_stream)  # the step ends when the last batch is on the host
+        stream.synchronize()
 
     one()  # warm-up
     t0 = time.perf_counter()

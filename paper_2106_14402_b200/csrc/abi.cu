@@ -410,8 +410,13 @@ slapcu_status slapcu_spgemm_host(slapcu_ctx ctx, const slapcu_host_csc* A, const
         try {
             const DevCsc av = view(a), bv = view(b);
             int64_t nnz = 0;
-            if (!direct_exact(c, av, bv, sr, alg, default_staging_budget(c), &dC.colptr, &dC.rowids, &dC.vals,
-                              &nnz)) {
+            // entries are read back straight out of the product scratch (no device copy)
+            int32_t* srw = nullptr;
+            void* sv = nullptr;
+            if (direct_exact(c, av, bv, sr, alg, default_staging_budget(c), &dC.colptr, &srw, &sv, &nnz, false)) {
+                dC.rowids = nullptr;
+                dC.vals = nullptr;
+            } else {
                 SLAPCU_CUDA(cudaMallocAsync((void**)&dC.colptr, sizeof(int64_t) * (bv.ncols + 1), c.stream));
                 nnz = spgemm_symbolic(c, av, bv, alg, dC.colptr);
                 SLAPCU_CUDA(cudaMallocAsync((void**)&dC.rowids, sizeof(int32_t) * std::max<int64_t>(nnz, 1), c.stream));
@@ -428,8 +433,10 @@ slapcu_status slapcu_spgemm_host(slapcu_ctx ctx, const slapcu_host_csc* A, const
             SLAPCU_CUDA(cudaMemcpyAsync(C->colptr, dC.colptr, sizeof(int64_t) * (bv.ncols + 1), cudaMemcpyDeviceToHost,
                                         c.stream));
             if (nnz) {
-                SLAPCU_CUDA(cudaMemcpyAsync(C->rowids, dC.rowids, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost, c.stream));
-                SLAPCU_CUDA(cudaMemcpyAsync(C->vals, dC.vals, size_t(vs) * nnz, cudaMemcpyDeviceToHost, c.stream));
+                SLAPCU_CUDA(cudaMemcpyAsync(C->rowids, srw ? srw : dC.rowids, sizeof(int32_t) * nnz,
+                                            cudaMemcpyDeviceToHost, c.stream));
+                SLAPCU_CUDA(cudaMemcpyAsync(C->vals, srw ? sv : dC.vals, size_t(vs) * nnz, cudaMemcpyDeviceToHost,
+                                            c.stream));
             }
             SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
         } catch (...) {

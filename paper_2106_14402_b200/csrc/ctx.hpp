@@ -235,7 +235,7 @@ void fused_copy_light(Ctx& c, int sr, bool ones, const int* list, int n, const F
 // direct.cu: single product pass straight into C; direct_exact returns exactly
 // sized library-owned buffers (false when the bound-sized scratch exceeds budget)
 bool direct_exact(Ctx& c, const DevCsc& A, const DevCsc& B, int sr, int alg, int64_t budget, int64_t** colptr,
-                  int32_t** rowids, void** vals, int64_t* nnz);
+                  int32_t** rowids, void** vals, int64_t* nnz, bool copy_out = true);
 int64_t direct_spgemm(Ctx& c, const DevCsc& A, const DevCsc& B, int sr, int alg, int64_t capacity, int64_t* c_colptr,
                       int32_t* c_rowids, void* c_vals);
 void any_zero_u8(Ctx& c, const uint8_t* v, int64_t n, int* flag);

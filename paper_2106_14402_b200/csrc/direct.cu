@@ -1831,7 +1831,7 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
 // nnz entries.  Returns false (nothing allocated) when the scratch would not
 // fit in `budget` bytes -- callers then take the staged or two-pass path.
 bool direct_exact(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int alg, int64_t budget, int64_t** cp,
-                  int32_t** rw, void** v, int64_t* nnz) {
+                  int32_t** rw, void** v, int64_t* nnz, bool copy_out) {
     check_operands(A_, B_);
     const int vs = value_size(sr);
     DevCsc A = A_, B = B_;
@@ -1857,6 +1857,11 @@ bool direct_exact(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int alg, i
         cudaFreeAsync(*cp, c.stream);
         *cp = nullptr;
         throw;
+    }
+    if (!copy_out) {  // entries stay in the context's scratch (valid until the next direct call)
+        *rw = d.dist_rw.as<int32_t>();
+        *v = d.dist_v.get();
+        return true;
     }
     SLAPCU_CUDA(cudaMallocAsync((void**)rw, sizeof(int32_t) * std::max<int64_t>(*nnz, 1), c.stream));
     SLAPCU_CUDA(cudaMallocAsync(v, size_t(vs) * std::max<int64_t>(*nnz, 1), c.stream));

@@ -30,25 +30,44 @@ __global__ void k_col_sum_check(int64_t ncols, const int64_t* __restrict__ cp, c
     }
 }
 
-template <class T>
+// v^e rounded to T.  MCL's usual inflation 2 is a double product (exact for
+// f32 inputs, correctly rounded for f64 like a correctly rounded pow); a
+// general double pow costs ~50x more and made the epilogue compute-bound.
+enum { kPow = 0, kSquare = 1, kIdentity = 2 };
+template <class T, int MODE>
 __device__ __forceinline__ T inflate(T v, double e) {
-    return (T)pow((double)v, e);
+    if constexpr (MODE == kSquare) return (T)((double)v * (double)v);
+    else if constexpr (MODE == kIdentity) return v;
+    else return (T)pow((double)v, e);
 }
 
-// kept entries per column and the column sum of the kept (inflated) values
-template <class T>
+// kept entries per column and the column sum of the kept (inflated) values.
+// Warp per column; each lane keeps kU independent loads in flight (the pass
+// is a 12 GB stream at C4 and one load per lane per trip left it latency-bound).
+constexpr int kU = 4;
+
+template <class T, int MODE>
 __global__ void k_mcl_count(int64_t ncols, const int64_t* __restrict__ cp, const T* __restrict__ v, double e,
                             double thr, int64_t* __restrict__ kept, double* __restrict__ sums) {
     const int lane = threadIdx.x & 31;
     for (int64_t j = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; j < ncols;
          j += (int64_t(gridDim.x) * blockDim.x) >> 5) {
+        const int64_t b1 = cp[j + 1];
         double s = 0;
         int k = 0;
-        for (int64_t q = cp[j] + lane; q < cp[j + 1]; q += 32) {
-            const T x = inflate(v[q], e);
-            if (!((double)x < thr)) {
-                s += (double)x;
-                ++k;
+        for (int64_t q = cp[j] + lane; q < b1; q += 32 * kU) {
+            T x[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) x[u] = q + 32 * u < b1 ? v[q + 32 * u] : T(0);
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                if (q + 32 * u < b1) {
+                    const T y = inflate<T, MODE>(x[u], e);
+                    if (!((double)y < thr)) {
+                        s += (double)y;
+                        ++k;
+                    }
+                }
             }
         }
 #pragma unroll
@@ -63,31 +82,43 @@ __global__ void k_mcl_count(int64_t ncols, const int64_t* __restrict__ cp, const
     }
 }
 
-// survivors in order (warp ballot compaction), divided by the column sum
-template <class T>
+// survivors in order (warp ballot compaction), divided by the column sum;
+// row ids are read only for survivors
+template <class T, int MODE>
 __global__ void k_mcl_write(int64_t ncols, const int64_t* __restrict__ cp, const int32_t* __restrict__ rw,
                             const T* __restrict__ v, double e, double thr, const double* __restrict__ sums,
                             const int64_t* __restrict__ ocp, int32_t* __restrict__ orw, T* __restrict__ ov) {
     const int lane = threadIdx.x & 31;
     for (int64_t j = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; j < ncols;
          j += (int64_t(gridDim.x) * blockDim.x) >> 5) {
+        const int64_t b1 = cp[j + 1];
+        if (ocp[j + 1] == ocp[j]) continue;  // nothing survives in this column
         const double s = sums[j];
         int64_t o = ocp[j];
-        for (int64_t b = cp[j]; b < cp[j + 1]; b += 32) {
-            const int64_t q = b + lane;
-            bool keep = false;
-            T x = T(0);
-            if (q < cp[j + 1]) {
-                x = inflate(v[q], e);
-                keep = !((double)x < thr);
+        for (int64_t b = cp[j]; b < b1; b += 32 * kU) {
+            T x[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int64_t q = b + 32 * u + lane;
+                x[u] = q < b1 ? v[q] : T(0);
             }
-            const unsigned m = __ballot_sync(0xffffffffu, keep);
-            if (keep) {
-                const int64_t at = o + __popc(m & ((1u << lane) - 1u));
-                orw[at] = rw[q];
-                ov[at] = s != 0.0 ? (T)((double)x / s) : x;
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int64_t q = b + 32 * u + lane;
+                bool keep = false;
+                T y = T(0);
+                if (q < b1) {
+                    y = inflate<T, MODE>(x[u], e);
+                    keep = !((double)y < thr);
+                }
+                const unsigned m = __ballot_sync(0xffffffffu, keep);
+                if (keep) {
+                    const int64_t at = o + __popc(m & ((1u << lane) - 1u));
+                    orw[at] = rw[q];
+                    ov[at] = s != 0.0 ? (T)((double)y / s) : y;
+                }
+                o += __popc(m);
             }
-            o += __popc(m);
         }
     }
 }
@@ -121,19 +152,25 @@ void mcl_step(Ctx& c, const DevCsc& A_, int sr, double inflation, double prune, 
             int32_t* erw = nullptr;
             void* ev = nullptr;
             int64_t enz = 0;
-            if (!direct_exact(c, A, A, sr, SLAPCU_ALG_HYBRID, 0, &ecp, &erw, &ev, &enz))
+            // the expansion stays in the context's product scratch; the
+            // epilogue reads it there (no exactly-sized copy of C)
+            if (!direct_exact(c, A, A, sr, SLAPCU_ALG_HYBRID, 0, &ecp, &erw, &ev, &enz, false))
                 throw Fail{SLAPCU_ERR_NOMEM, "mcl expansion does not fit"};
             struct Free {
                 Ctx& c;
-                void* p[3];
+                void* p;
                 ~Free() {
-                    for (void* q : p)
-                        if (q) cudaFreeAsync(q, c.stream);
+                    if (p) cudaFreeAsync(p, c.stream);
                 }
-            } fe{c, {ecp, erw, ev}};
+            } fe{c, ecp};
             DevBuf kept(sizeof(int64_t) * (n + 1), c.stream), sums(sizeof(double) * std::max<int64_t>(n, 1), c.stream);
             SLAPCU_CUDA(cudaMemsetAsync(kept.as<int64_t>() + n, 0, sizeof(int64_t), c.stream));
-            launch(c, k_mcl_count<T>, dim3(grid_for(c, n * 32, 256)), dim3(256), 0, n, (const int64_t*)ecp,
+            const int mode = inflation == 2.0 ? kSquare : inflation == 1.0 ? kIdentity : kPow;
+            auto kc = mode == kSquare ? k_mcl_count<T, kSquare> : mode == kIdentity ? k_mcl_count<T, kIdentity>
+                                                                                    : k_mcl_count<T, kPow>;
+            auto kw = mode == kSquare ? k_mcl_write<T, kSquare> : mode == kIdentity ? k_mcl_write<T, kIdentity>
+                                                                                    : k_mcl_write<T, kPow>;
+            launch(c, kc, dim3(grid_for(c, n * 32, 256)), dim3(256), 0, n, (const int64_t*)ecp,
                    (const T*)ev, inflation, prune, kept.as<int64_t>(), sums.as<double>());
             out->nrows = n;
             out->ncols = n;
@@ -143,7 +180,7 @@ void mcl_step(Ctx& c, const DevCsc& A_, int sr, double inflation, double prune, 
             SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
             SLAPCU_CUDA(cudaMallocAsync((void**)&out->rowids, sizeof(int32_t) * std::max<int64_t>(out->nnz, 1), c.stream));
             SLAPCU_CUDA(cudaMallocAsync(&out->vals, sizeof(T) * std::max<int64_t>(out->nnz, 1), c.stream));
-            launch(c, k_mcl_write<T>, dim3(grid_for(c, n * 32, 256)), dim3(256), 0, n, (const int64_t*)ecp,
+            launch(c, kw, dim3(grid_for(c, n * 32, 256)), dim3(256), 0, n, (const int64_t*)ecp,
                    (const int32_t*)erw, (const T*)ev, inflation, prune, (const double*)sums.as<double>(),
                    (const int64_t*)out->colptr, out->rowids, static_cast<T*>(out->vals));
         }

@@ -35,7 +35,7 @@ def stochastic_rmat(port, scale, seed=1):
 
 
 @pytest.mark.parametrize("scale", [8, 11])
-@pytest.mark.parametrize("inflation,prune", [(2.0, 1e-4), (1.5, 1e-3), (3.0, 0.0)])
+@pytest.mark.parametrize("inflation,prune", [(2.0, 1e-4), (1.5, 1e-3), (3.0, 0.0), (1.0, 1e-3)])
 def test_mcl_step_matches_reference(ref, port, scale, inflation, prune):
     a = stochastic_rmat(port, scale)
     want = ref.mcl_step(a, inflation, prune)
