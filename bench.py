@@ -449,7 +449,7 @@ def run_ours(args):
             dom_bytes += (int(colnnz_b[s:e][h].sum()) * (4 + vs) + int(counts[s:e][h].sum()) * (4 + vs) +
                           2 * (nh + 1) * 8 + A.nnz * (4 + vs) + (n + 1) * 8)
         achieved = dom_bytes / (dom_ms / 1e3) / 1e9
-        dom_launches = per_step["sym_heavy"][0]
+        dom_launches = sum(1 for s_, e_ in batches if heavy[s_:e_].any())  # one form+emit pair per batch
         tf, te = traffic.get("k_tile_form", {}), traffic.get("k_tile_emit", {})
         if tf.get("dram_bytes_per_launch") and te.get("dram_bytes_per_launch"):
             dom_traffic = tf["dram_bytes_per_launch"] + te["dram_bytes_per_launch"]
