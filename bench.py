@@ -510,7 +510,7 @@ def run_ours(args):
         "warmup": args.warmup,
         "ms_per_step": round(ms, 3),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": sr.dtype,
         "data": "synthetic",

@@ -519,10 +519,8 @@ struct EmitWarp {
 // (per odd, so the lanes' stage writes hit distinct banks) -- one search for
 // its first word and bit, then it walks bits serially -- into a stage
 // co-aligned with `out`, then the round is stored with 16-byte stores.
-__device__ __forceinline__ void emit_block(EmitWarp* ws, int pos, int cnt, int E, int32_t* __restrict__ out,
+__device__ __forceinline__ void emit_block(EmitWarp* ws, int pos, int ex, int E, int32_t* __restrict__ out,
                                            int lane) {
-    int all;
-    const int ex = warp_excl_scan(cnt, lane, &all);
     const int shift = (int)((reinterpret_cast<uintptr_t>(out) >> 2) & 3);
     for (int R0 = 0; R0 < E; R0 += kEmitStage) {
         const int RE = min(kEmitStage, E - R0);
@@ -551,16 +549,20 @@ __device__ __forceinline__ void emit_block(EmitWarp* ws, int pos, int cnt, int E
             unsigned w = cur.x;
             if (k) w &= ~((1u << nth_set_bit(w, k)) - 1u);  // drop the k lowest set bits
             int rb = (int)cur.y;
-            int* st = ws->stage + shift - R0;
-            for (int o = my0; o < my1; ++o) {
+            // pointer-stepped walk with a count-down (fewer address / compare
+            // instructions per output than indexing by o)
+            int* sp = ws->stage + shift - R0 + my0;
+            const uint2* wp = &ws->wr[wi];
+            int left = my1 - my0;
+            do {
                 if (w == 0u) {
-                    cur = ws->wr[++wi];
-                    w = cur.x;
-                    rb = (int)cur.y;
+                    const uint2 nw = *++wp;
+                    w = nw.x;
+                    rb = (int)nw.y;
                 }
-                st[o] = rb + (__ffs(w) - 1);
+                *sp++ = rb + (__ffs(w) - 1);
                 w &= w - 1u;
-            }
+            } while (--left);
         }
         __syncwarp();
         // stage[shift + i] -> out[R0 + i]; both 16-byte aligned where (shift + i) % 4 == 0
@@ -634,8 +636,10 @@ __global__ void __launch_bounds__(NT) k_tile_emit(EmitArgs g) {
                 cnt += __popc(xs[q]);
                 nz += xs[q] != 0u;
             }
-            int nzt;
-            const int pos = warp_excl_scan(nz, lane, &nzt);
+            // one scan for both: set bits (<= 128 per lane) high, non-zero words low
+            int tot;
+            const int packed = warp_excl_scan((cnt << 16) | nz, lane, &tot);
+            const int pos = packed & 0xffff, ex = packed >> 16;
             int p = pos;
 #pragma unroll
             for (int q = 0; q < kEmitWPL; ++q) {
@@ -645,7 +649,7 @@ __global__ void __launch_bounds__(NT) k_tile_emit(EmitArgs g) {
                 }
             }
             __syncwarp();
-            emit_block(ws, pos, cnt, E, g.crw + off + bbase, lane);
+            emit_block(ws, pos, ex, E, g.crw + off + bbase, lane);
         }
 #pragma unroll
         for (int q = 0; q < kEmitWPL; ++q) {
@@ -701,8 +705,9 @@ __global__ void __launch_bounds__(128) k_tile_emit_blocks(EmitArgs g, const int2
     if (!E) return;
     const int64_t off = g.lp[it.x] + g.hoff[item] + before;
     EmitWarp* ws = &wsm[warp];
-    int nzt;
-    const int pos = warp_excl_scan(nz, lane, &nzt);
+    int tot;
+    const int packed = warp_excl_scan((cnt << 16) | nz, lane, &tot);
+    const int pos = packed & 0xffff, ex = packed >> 16;
     int p = pos;
 #pragma unroll
     for (int q = 0; q < kEmitWPL; ++q) {
@@ -713,7 +718,7 @@ __global__ void __launch_bounds__(128) k_tile_emit_blocks(EmitArgs g, const int2
         }
     }
     __syncwarp();
-    emit_block(ws, pos, cnt, E, g.crw + off, lane);
+    emit_block(ws, pos, ex, E, g.crw + off, lane);
     if (g.cv) {  // values: E bytes of 1
         uint8_t* v = g.cv + off;
         const int head = (int)lmin(E, (16 - (reinterpret_cast<uintptr_t>(v) & 15)) & 15);
