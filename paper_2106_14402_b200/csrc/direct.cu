@@ -1251,6 +1251,69 @@ __global__ void k_item_flops(DevCsc B, const int32_t* __restrict__ Atp, int T, c
     }
 }
 
+// Chunked variant: heavy column h's B entries are cut into chunks of
+// kItemChunk; a warp per chunk adds its per-tile flops into iflops (zeroed)
+// with one atomic per non-zero tile, so hub columns (tens of thousands of
+// entries) are spread over many warps instead of serialising one.
+constexpr int kItemChunk = 1024;
+
+__global__ void k_item_chunks(DevCsc B, const int* __restrict__ hl, int nh, int64_t* __restrict__ nch) {
+    for (int64_t h = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; h < nh; h += int64_t(gridDim.x) * blockDim.x) {
+        const int j = hl[h];
+        nch[h] = (B.cp[j + 1] - B.cp[j] + kItemChunk - 1) / kItemChunk;
+    }
+}
+
+__global__ void k_item_chunk_fill(int nh, const int64_t* __restrict__ choff, int* __restrict__ chh) {
+    for (int64_t h = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; h < nh; h += int64_t(gridDim.x) * blockDim.x)
+        for (int64_t q = choff[h]; q < choff[h + 1]; ++q) chh[q] = (int)h;
+}
+
+__global__ void k_item_flops_chunked(DevCsc B, const int32_t* __restrict__ Atp, int T, const int* __restrict__ hl,
+                                     const int64_t* __restrict__ choff, const int* __restrict__ chh, int64_t nchunks,
+                                     unsigned long long* __restrict__ iflops) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t q = w0; q < nchunks; q += nw) {
+        const int h = chh[q];
+        const int j = hl[h];
+        const int64_t bs = B.cp[j] + (q - choff[h]) * kItemChunk;
+        const int64_t be = min(B.cp[j + 1], bs + kItemChunk);
+        for (int tb = 0; tb < T; tb += 8) {
+            unsigned long long g[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            const int nt = min(8, T - tb);
+            for (int64_t i = bs + lane; i < be; i += 32) {
+                const int32_t* tp = Atp + int64_t(B.rw[i]) * (T + 1) + tb;
+                int prev = tp[0];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    if (u < nt) {
+                        const int nx = tp[u + 1];
+                        g[u] += (unsigned long long)(nx - prev);
+                        prev = nx;
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (u < nt) {
+                    const unsigned long long sum = (unsigned long long)warp_reduce_sum64((long long)g[u]);
+                    if (lane == 0 && sum) atomicAdd(&iflops[int64_t(h) * T + tb + u], sum);
+                }
+            }
+        }
+    }
+}
+
+__global__ void k_item_count(int nh, int T, const int64_t* __restrict__ iflops, int64_t* __restrict__ nit) {
+    for (int64_t h = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; h < nh; h += int64_t(gridDim.x) * blockDim.x) {
+        int64_t k = 0;
+        for (int t = 0; t < T; ++t) k += iflops[h * T + t] > 0;
+        nit[h] = k;
+    }
+}
+
 // Items in C order; per item its work-unit count (split when above `split`
 // multiplies), stash reservation and partial-slot count.
 __global__ void k_item_fill(const int* __restrict__ hl, int nh, int T, int W, const int64_t* __restrict__ iflops,
@@ -1564,8 +1627,23 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
         DevBuf iflops(sizeof(int64_t) * int64_t(nh) * T, c.stream);
         DevBuf nit(sizeof(int64_t) * (nh + 1), c.stream), ioff(sizeof(int64_t) * (nh + 1), c.stream);
         SLAPCU_CUDA(cudaMemsetAsync(nit.as<int64_t>() + nh, 0, sizeof(int64_t), c.stream));
-        launch(c, k_item_flops, dim3(grid_for(c, int64_t(nh) * 32, 256)), dim3(256), 0, B, Atp, T,
-               (const int*)d.hl.as<int>(), nh, flops, iflops.as<int64_t>(), nit.as<int64_t>());
+        {
+            DevBuf nch(sizeof(int64_t) * (nh + 1), c.stream), choff(sizeof(int64_t) * (nh + 1), c.stream);
+            SLAPCU_CUDA(cudaMemsetAsync(nch.as<int64_t>() + nh, 0, sizeof(int64_t), c.stream));
+            launch(c, k_item_chunks, dim3(grid_for(c, nh, 256)), dim3(256), 0, B, (const int*)d.hl.as<int>(), nh,
+                   nch.as<int64_t>());
+            exclusive_scan_i64(c, nch.as<int64_t>(), choff.as<int64_t>(), nh + 1);
+            const int64_t nchunks = d2h(c, choff.as<int64_t>() + nh);
+            DevBuf chh(sizeof(int) * std::max<int64_t>(nchunks, 1), c.stream);
+            launch(c, k_item_chunk_fill, dim3(grid_for(c, nh, 256)), dim3(256), 0, nh,
+                   (const int64_t*)choff.as<int64_t>(), chh.as<int>());
+            SLAPCU_CUDA(cudaMemsetAsync(iflops.get(), 0, sizeof(int64_t) * int64_t(nh) * T, c.stream));
+            launch(c, k_item_flops_chunked, dim3(grid_for(c, nchunks * 32, 256)), dim3(256), 0, B, Atp, T,
+                   (const int*)d.hl.as<int>(), (const int64_t*)choff.as<int64_t>(), (const int*)chh.as<int>(),
+                   nchunks, reinterpret_cast<unsigned long long*>(iflops.as<int64_t>()));
+            launch(c, k_item_count, dim3(grid_for(c, nh, 256)), dim3(256), 0, nh, T,
+                   (const int64_t*)iflops.as<int64_t>(), nit.as<int64_t>());
+        }
         exclusive_scan_i64(c, nit.as<int64_t>(), ioff.as<int64_t>(), nh + 1);
         const int64_t nitems64 = d2h(c, ioff.as<int64_t>() + nh);
         if (nitems64 > INT32_MAX) throw Fail{SLAPCU_ERR_INVALID, "too many tile items"};

@@ -31,29 +31,55 @@ namespace slapcu {
 
 // ===================================================================== phase 1
 
-// One warp per output column; grid-stride.  Reads B's colptr/rowids once and
-// A's colptr at the gathered k (spgemm.hpp:68-88).
+// Entry-parallel over B's entries (spgemm.hpp:68-88): each thread takes a
+// contiguous run of kFlopsRun entries, finds the column of its first entry by
+// binary search on colptr and advances from there, adding nnz(A(:,k)) per
+// entry and flushing each column's partial sum with one 64-bit atomic into
+// flops[] (zeroed by the caller).  A warp per column left the R-MAT hub
+// columns (up to 64K entries) serialised on one warp: a 1.2 ms tail per batch.
+constexpr int kFlopsRun = 8;
 __global__ void __launch_bounds__(256) k_flops(const int64_t* __restrict__ Acp, const int64_t* __restrict__ Bcp,
                                                const int32_t* __restrict__ Brw, int64_t ncols,
-                                               int64_t* __restrict__ flops, unsigned long long* __restrict__ total) {
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-    long long acc = 0;
-    for (int64_t j = warp; j < ncols; j += nwarps) {
-        const int64_t bs = Bcp[j], be = Bcp[j + 1];
-        long long f = 0;
-        for (int64_t i = bs + lane; i < be; i += 32) {
-            const int k = Brw[i];
-            f += Acp[k + 1] - Acp[k];
+                                               unsigned long long* __restrict__ flops,
+                                               unsigned long long* __restrict__ total) {
+    const int64_t eb = Bcp[0], ee = Bcp[ncols];
+    const int64_t nthreads = int64_t(gridDim.x) * blockDim.x;
+    unsigned long long mine = 0;
+    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;; t += nthreads) {
+        const int64_t e0 = eb + t * kFlopsRun;
+        if (e0 >= ee) break;
+        const int64_t e1 = e0 + kFlopsRun < ee ? e0 + kFlopsRun : ee;
+        int64_t lo = 0, hi = ncols;  // Bcp[lo] <= e0 < Bcp[hi]
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (Bcp[mid] <= e0) lo = mid; else hi = mid;
         }
-        f = warp_reduce_sum64(f);
-        if (lane == 0) {
-            if (flops) flops[j] = f;
-            acc += f;
+        int64_t c = lo, cend = Bcp[c + 1];
+        unsigned long long f = 0;
+        int k[kFlopsRun];
+#pragma unroll
+        for (int q = 0; q < kFlopsRun; ++q) k[q] = e0 + q < e1 ? Brw[e0 + q] : 0;
+        unsigned long long d[kFlopsRun];
+#pragma unroll
+        for (int q = 0; q < kFlopsRun; ++q) d[q] = e0 + q < e1 ? (unsigned long long)(Acp[k[q] + 1] - Acp[k[q]]) : 0ull;
+#pragma unroll
+        for (int q = 0; q < kFlopsRun; ++q) {
+            const int64_t e = e0 + q;
+            if (e >= e1) break;
+            while (e >= cend) {  // next non-empty column
+                if (f && flops) atomicAdd(&flops[c], f);
+                mine += f;
+                f = 0;
+                ++c;
+                cend = Bcp[c + 1];
+            }
+            f += d[q];
         }
+        if (f && flops) atomicAdd(&flops[c], f);
+        mine += f;
     }
-    if (lane == 0 && total) atomicAdd(total, (unsigned long long)acc);
+    const unsigned long long w = (unsigned long long)warp_reduce_sum64((long long)mine);
+    if ((threadIdx.x & 31) == 0 && total && w) atomicAdd(total, w);
 }
 
 // ===================================================================== binning
@@ -518,8 +544,11 @@ void prepare_plan(Ctx& c, const DevCsc& A, const DevCsc& B) {
     p.counts.reset(sizeof(int64_t) * (B.ncols + 1), c.stream);
     p.cursor.reset(sizeof(int32_t) * 2 * std::max<int64_t>(B.span, 1), c.stream);
     KScope ks(c, KC_FLOPS);
-    launch(c, k_flops, dim3(grid_for(c, B.ncols * 32, 256, 16)), dim3(256), 0, A.cp, B.cp, B.rw, B.ncols,
-           p.flops.as<int64_t>(), (unsigned long long*)nullptr);
+    SLAPCU_CUDA(cudaMemsetAsync(p.flops.get(), 0, sizeof(int64_t) * std::max<int64_t>(B.ncols, 1), c.stream));
+    const int64_t runs = (std::max<int64_t>(B.span, B.nnz) + kFlopsRun - 1) / kFlopsRun;
+    if (B.ncols > 0)
+        launch(c, k_flops, dim3(grid_for(c, std::max<int64_t>(runs, 1), 256, 16)), dim3(256), 0, A.cp, B.cp, B.rw,
+               B.ncols, reinterpret_cast<unsigned long long*>(p.flops.as<int64_t>()), (unsigned long long*)nullptr);
     p.a_key = A.cp;
     p.b_key = B.cp;
     p.a_ncols = A.ncols;
@@ -612,8 +641,13 @@ void spgemm_flops(Ctx& c, const DevCsc& A, const DevCsc& B, int64_t* flops_dev, 
     DevBuf tot(sizeof(unsigned long long), c.stream);
     SLAPCU_CUDA(cudaMemsetAsync(tot.get(), 0, sizeof(unsigned long long), c.stream));
     KScope ks(c, KC_FLOPS);
-    launch(c, k_flops, dim3(grid_for(c, B.ncols * 32, 256, 16)), dim3(256), 0, A.cp, B.cp, B.rw, B.ncols, flops_dev,
-           tot.as<unsigned long long>());
+    if (flops_dev) SLAPCU_CUDA(cudaMemsetAsync(flops_dev, 0, sizeof(int64_t) * std::max<int64_t>(B.ncols, 1), c.stream));
+    // grid-stride over the entries: the grid is sized from an upper bound
+    // (a column window carries its parent's nnz)
+    const int64_t runs = (std::max<int64_t>(B.span, B.nnz) + kFlopsRun - 1) / kFlopsRun;
+    if (B.ncols > 0)
+        launch(c, k_flops, dim3(grid_for(c, std::max<int64_t>(runs, 1), 256, 16)), dim3(256), 0, A.cp, B.cp, B.rw,
+               B.ncols, reinterpret_cast<unsigned long long*>(flops_dev), tot.as<unsigned long long>());
     unsigned long long h = 0;
     SLAPCU_CUDA(cudaMemcpyAsync(&h, tot.get(), sizeof(h), cudaMemcpyDeviceToHost, c.stream));
     SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
