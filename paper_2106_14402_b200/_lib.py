@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libslapcu.so")
+LIB_PATH = os.environ.get("SLAPCU_LIB") or os.path.join(HERE, "libslapcu.so")  # SLAPCU_LIB: A/B builds
 
 # slapcu_status
 OK = 0

@@ -39,8 +39,14 @@ namespace slapcu {
 
 namespace {
 
-constexpr int kShortRun = 32;  // runs shorter than this are walked by one thread
-constexpr int kUnit = 256;     // products per warp work unit on long runs
+#ifndef SLAPCU_SHORT_RUN
+#define SLAPCU_SHORT_RUN 8  // measured best of 4..64 on C3 (form 103.6 -> 100.7 ms)
+#endif
+constexpr int kShortRun = SLAPCU_SHORT_RUN;  // runs shorter than this are walked by one thread
+#ifndef SLAPCU_UNIT
+#define SLAPCU_UNIT 256
+#endif
+constexpr int kUnit = SLAPCU_UNIT;  // products per warp work unit on long runs
 
 __host__ __device__ __forceinline__ int64_t lmin(int64_t a, int64_t b) { return a < b ? a : b; }
 
@@ -1384,9 +1390,12 @@ __global__ void __launch_bounds__(NT)
         const long long ex = (long long)block_excl_scan<NT>(len, wsum, &tot) + run_sh;
         const long long in = ex + len;
         if (len > 0) {
-            for (int64_t q = 1; q < p; ++q) {
+            // parts whose target ceil(q*f/p) lies in (ex, in]: start at the
+            // first q with target > ex instead of testing every part
+            for (int64_t q = (ex * p + f) / f > 1 ? (ex * p + f) / f : 1; q < p; ++q) {
                 const long long tg = (q * f + p - 1) / p;
-                if (tg > ex && tg <= in) bnd[q] = (int)(i - bs + 1);
+                if (tg > in) break;
+                if (tg > ex) bnd[q] = (int)(i - bs + 1);
             }
         }
         __syncthreads();
