@@ -441,6 +441,9 @@ def run_ours(args):
         # belong to the pair, so the pair is the roofline unit; the per-kernel
         # view is under "kernels".
         kernel_name = "k_tile_form+k_tile_emit (one product pass over the heavy columns)"
+        if sr is not P.OrAnd:  # the value pass shares the num_heavy class with emit
+            kernel_name = ("k_tile_form+k_tile_emit+value pass (k_item_values_hash / k_item_values_rank: "
+                           "pattern pass, then one value walk over the heavy columns)")
         dom_ms = per_step["sym_heavy"][1] + per_step["num_heavy"][1]
         dom_bytes = 0
         for s, e in batches:
