@@ -71,6 +71,8 @@ def parse():
     ap.add_argument("--value-threads", type=int, default=None, help="direct path value pass CTA size")
     ap.add_argument("--value-hash", type=int, default=None, help="direct path value pass hash table (0/13/14)")
     ap.add_argument("--value-rank", type=int, default=None, help="direct path value pass rank chunk (0 = sub-tiles)")
+    ap.add_argument("--value-interleave", type=int, default=None,
+                    help="direct path value pass: 4-byte values gathered with their rows (1) or not (0)")
     ap.add_argument("--quads", type=int, default=None, help="direct path: lane-contiguous quads (1) or strided (0)")
     ap.add_argument("--dist", default="1d", choices=["1d", "summa"],
                     help="N>1: 1d = flops-balanced column blocks with A replicated (no data-path collective); "
@@ -110,6 +112,8 @@ def apply_options(ctx, args):
         ctx.set_option(L.OPT_DIRECT_QUADS, args.quads)
     if args.value_rank is not None:
         ctx.set_option(L.OPT_DIRECT_VALUE_RANK, args.value_rank)
+    if args.value_interleave is not None:
+        ctx.set_option(L.OPT_DIRECT_VALUE_INTERLEAVE, args.value_interleave)
     if args.value_hash is not None:
         ctx.set_option(L.OPT_DIRECT_VALUE_HASH, args.value_hash)
     if args.value_threads is not None:

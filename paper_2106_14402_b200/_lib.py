@@ -36,7 +36,7 @@ ALG_HEAP, ALG_HASH, ALG_HYBRID = 0, 1, 2
  OPT_DIRECT_SPLIT_FLOPS, OPT_DIRECT_MARK_MODE, OPT_DIRECT_FORM_THREADS, OPT_DIRECT_EMIT_THREADS,
  OPT_DIRECT_DENSE_RUN_MIN, OPT_DIRECT_PERSISTENT, OPT_DIRECT_QUADS,
  OPT_DIRECT_VALUE_TILE_ROWS_LOG2, OPT_DIRECT_VALUE_THREADS, OPT_SUMMA_CONCAT,
- OPT_DIRECT_VALUE_HASH, OPT_DIRECT_VALUE_RANK) = range(22)
+ OPT_DIRECT_VALUE_HASH, OPT_DIRECT_VALUE_RANK, OPT_DIRECT_VALUE_INTERLEAVE) = range(23)
 NUM_KERNEL_CLASSES = 10
 KERNEL_CLASSES = ["other", "flops", "bin", "sym_light", "sym_heavy", "scan", "num_light", "num_heavy", "merge", "gen"]
 

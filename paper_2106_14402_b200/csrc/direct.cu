@@ -774,7 +774,31 @@ struct ValueArgs {
     const int* rbc;       // entries per 4096-row block of every item
     const int32_t* crw;
     void* cv;
+    const int2* arv;      // 4-byte values: A's (row, value bits) interleaved, or null
 };
+
+// One product's A row and value: from the interleaved copy when there is one
+// (one 8-byte gather, one sector), else from the two arrays.
+template <class T_>
+__device__ __forceinline__ void load_prod(const int32_t* __restrict__ Arw, const T_* Av, const int2* __restrict__ Arv,
+                                          int64_t p, int& r, T_& a) {
+    if constexpr (sizeof(T_) == 4) {
+        if (Arv) {
+            const int2 e = __ldg(Arv + p);
+            r = e.x;
+            memcpy(&a, &e.y, 4);
+            return;
+        }
+    }
+    r = __ldg(&Arw[p]);
+    a = Av[p];
+}
+
+__global__ void k_interleave_rv(int64_t n, const int32_t* __restrict__ rw, const int32_t* __restrict__ v,
+                                int2* __restrict__ out) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        out[i] = make_int2(__ldg(rw + i), __ldg(v + i));
+}
 
 template <int SRID, int NT>
 struct ValueWalkSm {
@@ -798,7 +822,8 @@ struct ValueWalkSm {
 // walks a run alone through a chain of dependent loads.
 template <int SRID, int NT, class Slot>
 __device__ __forceinline__ void value_walk(const DevCsc& A, const DevCsc& B, const int32_t* __restrict__ Atab, int T,
-                                           int t, int j, ValueWalkSm<SRID, NT>& sh, Slot slot, int t_hi = -1) {
+                                           int t, int j, ValueWalkSm<SRID, NT>& sh, Slot slot, int t_hi = -1,
+                                           const int2* __restrict__ Arv = nullptr) {
     using S_ = Sr<SRID>;
     using T_ = typename S_::T;
     constexpr int NW = NT / 32;
@@ -883,7 +908,10 @@ __device__ __forceinline__ void value_walk(const DevCsc& A, const DevCsc& B, con
                         b = mid - 1;
                 }
                 const int64_t p = sh.sst[a] + (o - sh.sp[a]);
-                S_::atomic_acc(slot(__ldg(&Arw[p])), S_::mul(Av[p], sh.sbv[a]));
+                int r;
+                T_ av;
+                load_prod(Arw, Av, Arv, p, r, av);
+                S_::atomic_acc(slot(r), S_::mul(av, sh.sbv[a]));
             }
         }
         const int u0 = (int)((int64_t(tot) * warp) / NW), u1 = (int)((int64_t(tot) * (warp + 1)) / NW);
@@ -906,11 +934,14 @@ __device__ __forceinline__ void value_walk(const DevCsc& A, const DevCsc& B, con
             const int m = min(256, sh.ulen[e] - c0);
             const T_ bv = sh.ubval[e];
             for (int x = lane; x < m; x += 64) {
-                const int r0 = __ldg(&Arw[p0 + x]);
-                const T_ a0 = Av[p0 + x];
+                int r0, r1 = 0;
+                T_ a0, a1;
+                load_prod(Arw, Av, Arv, p0 + x, r0, a0);
                 const bool two = x + 32 < m;
-                const int r1 = two ? __ldg(&Arw[p0 + x + 32]) : 0;
-                const T_ a1 = two ? Av[p0 + x + 32] : a0;
+                if (two)
+                    load_prod(Arw, Av, Arv, p0 + x + 32, r1, a1);
+                else
+                    a1 = a0;
                 S_::atomic_acc(slot(r0), S_::mul(a0, bv));
                 if (two) S_::atomic_acc(slot(r1), S_::mul(a1, bv));
             }
@@ -966,7 +997,7 @@ __global__ void __launch_bounds__(NT) k_tile_values(ValueArgs g) {
     if (lo == hi) return;
     for (int64_t q = lo + tid; q < hi; q += NT) val[g.crw[q] - s0] = S_::identity();
     __syncthreads();
-    value_walk<SRID, NT>(g.A, g.B, g.Atpv, g.Tv, ts, j, sh, [val, s0](int r) { return &val[r - s0]; });
+    value_walk<SRID, NT>(g.A, g.B, g.Atpv, g.Tv, ts, j, sh, [val, s0](int r) { return &val[r - s0]; }, -1, g.arv);
     T* Cv = static_cast<T*>(g.cv);
     for (int64_t q = lo + tid; q < hi; q += NT) Cv[q] = S_::out(val[g.crw[q] - s0]);
 }
@@ -1007,7 +1038,7 @@ __global__ void __launch_bounds__(NT) k_item_values_hash(ValueArgs g) {
         while (key[h] != r) h = (h + 1) & (HS - 1);
         return &val[h];
     };
-    value_walk<SRID, NT>(g.A, g.B, g.Atp, g.T, it.y, j, sh, slot);
+    value_walk<SRID, NT>(g.A, g.B, g.Atp, g.T, it.y, j, sh, slot, -1, g.arv);
     T* Cv = static_cast<T*>(g.cv);
     for (int64_t q = tid; q < c; q += NT) Cv[off + q] = S_::out(*slot(g.crw[off + q]));
 }
@@ -1100,7 +1131,7 @@ __global__ void __launch_bounds__(NT) k_item_values_rank(ValueArgs g, const Rank
         return &val[gbase[w >> 5] + pre16[w] + __popc(bm[w] & ((1u << (rr & 31)) - 1u))];
     };
     const int ts0 = (it.y << (g.TL - g.VTL)) + ch.b0, ts1 = (it.y << (g.TL - g.VTL)) + ch.b1;
-    value_walk<SRID, NT>(g.A, g.B, g.Atpv, g.Tv, ts0, j, sh, slot, ts1);
+    value_walk<SRID, NT>(g.A, g.B, g.Atpv, g.Tv, ts0, j, sh, slot, ts1, g.arv);
     T* Cv = static_cast<T*>(g.cv);
     for (int q = tid; q < n; q += NT) Cv[lo + q] = S_::out(val[q]);
 }
@@ -1841,7 +1872,16 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
         SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
         ValueArgs va{A, B, Atpv, Tv, VTL, TL, Atp, T, (const int2*)d.items.as<int2>(), nullptr,
                      (const int64_t*)d.cnt.as<int64_t>(), (const int64_t*)d.hoff.as<int64_t>(),
-                     (const int64_t*)d.lp.as<int64_t>(), (const int*)d.rbc.as<int>(), crw, cv};
+                     (const int64_t*)d.lp.as<int64_t>(), (const int*)d.rbc.as<int>(), crw, cv, nullptr};
+        // 4-byte values: A's rows and values interleaved, so a product's gather
+        // is one 8-byte load (one sector) instead of one from each array
+        DevBuf arv;
+        if (value_size(sr) == 4 && A.span > 0 && c.opt.direct_value_interleave) {
+            arv = DevBuf(sizeof(int2) * size_t(A.span), c.stream);
+            launch(c, k_interleave_rv, dim3(grid_for(c, A.span, 256)), dim3(256), 0, A.span, A.rw + A.base,
+                   static_cast<const int32_t*>(A.v) + A.base, arv.as<int2>());
+            va.arv = arv.as<int2>() - A.base;
+        }
         dispatch_sr(sr, [&](auto id) {
             constexpr int ID = decltype(id)::value;
             using Acc = typename Sr<ID>::Acc;

@@ -107,6 +107,20 @@ def test_direct_value_pass(port, sr, vtl, hash_, rank):
     assert_parity(got, want, sr.id, f"{sr.name} vtl={vtl}")
 
 
+@pytest.mark.parametrize("interleave", [0, 1])
+@pytest.mark.parametrize("sr", [P.PlusTimesF32, P.MinPlusI32], ids=lambda s: f"{s.name}_{s.dtype}")
+def test_direct_value_interleave(port, sr, interleave):
+    """4-byte value types: the value pass gathers A's (row, value) pairs from an
+    interleaved copy (default) or from the two arrays -- same output."""
+    a = with_values(port, port.gen_rmat(13), sr.id)
+    want = port.spgemm(sr.id, a, a)
+    ctx = P.Context()
+    ctx.set_option(L.OPT_DIRECT_TILE_ROWS_LOG2, 12)
+    ctx.set_option(L.OPT_DIRECT_VALUE_INTERLEAVE, interleave)
+    got = P.local_spgemm(to_device(a), to_device(a), sr, ctx=ctx, method="direct")
+    assert_parity(got, want, sr.id, f"{sr.name} interleave={interleave}")
+
+
 def test_direct_fallback_semirings(port):
     """Value semirings and OrAnd with stored zeros (structural pattern,
     values from the value pass): same contract, same output."""
