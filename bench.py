@@ -154,6 +154,14 @@ class ClockSampler:
             self.t.start()
         except Exception:
             self.proc = None
+            return
+        # nvidia-smi takes a while to produce its first line; a short timed
+        # region could otherwise end before any sample.  Wait until it is live
+        # (bounded) and keep only the samples taken after this point.
+        t0 = time.time()
+        while not self.lines and time.time() - t0 < 5.0 and self.proc.poll() is None:
+            time.sleep(0.02)
+        self.skip = len(self.lines)
 
     def _read(self):
         for line in self.proc.stdout:
@@ -169,7 +177,8 @@ class ClockSampler:
             self.proc.kill()
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = self.lines[getattr(self, "skip", 0):] or self.lines
+        for ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 6:
                 continue

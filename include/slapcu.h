@@ -145,8 +145,9 @@ typedef enum {
                                               table of 2^v slots keyed by their rows; 0 = every item
                                               takes the row sub-tile pass */
     SLAPCU_OPT_DIRECT_VALUE_RANK = 21,     /* direct path value pass: larger items are folded in rank
-                                              chunks of at most this many outputs (4096..16384, default
-                                              4096); 0 = row sub-tiles of 2^VTL rows */
+                                              chunks of at most this many outputs (4096..16384; default
+                                              8192 for 4-byte, 4096 for 8-byte accumulators);
+                                              0 = row sub-tiles of 2^VTL rows */
     SLAPCU_OPT_DIRECT_VALUE_INTERLEAVE = 22 /* direct path value pass, 4-byte value types: 1 (default) =
                                               A's rows and values gathered as one interleaved 8-byte
                                               pair per product; 0 = from the two arrays */

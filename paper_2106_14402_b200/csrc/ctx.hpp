@@ -133,7 +133,8 @@ struct Options {
     int direct_value_threads = 512;
     int direct_value_hash = 1;
     int direct_value_interleave = 1;       // value pass: 4-byte values gathered with their rows (0 = two arrays)
-    int direct_value_rank = 4096;           // value pass: large items by rank chunks of this many outputs (0 = sub-tiles)
+    int direct_value_rank = -1;  // value pass: large items by rank chunks of this many outputs (0 = sub-tiles,
+                                 // -1 = by accumulator width: 8192 for 4-byte, 4096 for 8-byte)
     int direct_emit_blocks = 0;             // emit: one warp per (item, block) (1) or one CTA per item (0)              // value pass: small items through the one-walk hash kernel         // CTA size of the value pass (256, 512)         // 1: value semirings use begin/finish instead                   // direct path: lane-contiguous quads merged per word
     int direct_persistent = 1;              // form kernel: persistent CTAs (1) or one CTA per unit (0)
     int direct_form_threads = 256;          // CTA size of the form kernel (128, 256, 512)

@@ -1854,7 +1854,7 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
         // sub-tiles are whole 4096-row blocks of the item (or the item itself)
         const int VTL = std::min(TL, std::max(12, c.opt.direct_value_tile_log2));
         const int Tv = (int)((A.nrows + (int64_t(1) << VTL) - 1) >> VTL);
-        const bool rank_path = c.opt.direct_value_rank > 0 && TL >= 12;
+        const bool rank_path = c.opt.direct_value_rank != 0 && TL >= 12;
         // (one cached table at a time: only the sub-tile path needs 2^VTL rows)
         const int32_t* Atpv = rank_path ? nullptr : value_tile_pointers(c, A, VTL, Tv);
         const int32_t* Atp = tile_pointers(c, A, TL, T);
@@ -1900,7 +1900,9 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
             }
             if (nsl[1] > 0 && rank_path) {
                 // large items by rank chunks over 4096-row blocks (tile pointers at 2^12 rows)
-                const int cap = c.opt.direct_value_rank;
+                // 8192 4-byte slots keep 3 CTAs of 512 threads per SM (C3 MinPlus: values
+                // 498 -> 441 ms vs 4096; 6144 467, 10240 508, 12288 492 ms)
+                const int cap = c.opt.direct_value_rank > 0 ? c.opt.direct_value_rank : (sizeof(Acc) <= 4 ? 8192 : 4096);
                 const int T12 = (int)((A.nrows + 4095) >> 12);
                 ValueArgs vr = va;
                 vr.Atpv = value_tile_pointers(c, A, 12, T12);

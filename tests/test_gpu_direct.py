@@ -87,7 +87,7 @@ def test_direct_window_and_rectangular(port):
 
 
 @pytest.mark.parametrize("vtl", [10, 12, 14])
-@pytest.mark.parametrize("rank", [0, 4096])
+@pytest.mark.parametrize("rank", [0, 4096, 8192])
 @pytest.mark.parametrize("hash_", [0, 1])
 @pytest.mark.parametrize("sr", [P.PlusTimesF64, P.PlusTimesF32, P.PlusTimesI64, P.MinPlusI32, P.MinPlusF64],
                          ids=lambda s: f"{s.name}_{s.dtype}")
