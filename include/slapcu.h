@@ -148,9 +148,10 @@ typedef enum {
                                               chunks of at most this many outputs (4096..16384; default
                                               8192 for 4-byte, 4096 for 8-byte accumulators);
                                               0 = row sub-tiles of 2^VTL rows */
-    SLAPCU_OPT_DIRECT_VALUE_INTERLEAVE = 22 /* direct path value pass, 4-byte value types: 1 (default) =
-                                              A's rows and values gathered as one interleaved 8-byte
-                                              pair per product; 0 = from the two arrays */
+    SLAPCU_OPT_DIRECT_VALUE_INTERLEAVE = 22 /* direct path value pass: A's rows and values gathered as
+                                              one interleaved pair per product -- 1 (default) for 4-byte
+                                              values (8-byte pairs), 2 also for 8-byte values (16-byte
+                                              pairs); 0 = from the two arrays */
 } slapcu_option;
 slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t value);
 

@@ -160,7 +160,10 @@ slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t v
             require(v == 0 || (v >= 4096 && v <= 16384), SLAPCU_ERR_INVALID, "value rank chunk: 0 or 4096..16384");
             c.opt.direct_value_rank = (int)v;
             break;
-        case SLAPCU_OPT_DIRECT_VALUE_INTERLEAVE: c.opt.direct_value_interleave = v != 0; break;
+        case SLAPCU_OPT_DIRECT_VALUE_INTERLEAVE:
+            require(v >= 0 && v <= 2, SLAPCU_ERR_INVALID, "value interleave: 0, 1 or 2");
+            c.opt.direct_value_interleave = (int)v;
+            break;
         case SLAPCU_OPT_DIRECT_VALUE_HASH:
             require(v == 0 || v == 1 || v == 13 || v == 14, SLAPCU_ERR_INVALID, "value hash: 0, 1, 13 or 14");
             c.opt.direct_value_hash = (int)v;

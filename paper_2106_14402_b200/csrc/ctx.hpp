@@ -132,7 +132,7 @@ struct Options {
     int summa_concat = 1;                   // SUMMA: one concatenated-k product per call (no stage merge)
     int direct_value_threads = 512;
     int direct_value_hash = 1;
-    int direct_value_interleave = 1;       // value pass: 4-byte values gathered with their rows (0 = two arrays)
+    int direct_value_interleave = 1;       // value pass: values gathered with their rows (0 off, 1 4-byte, 2 all)
     int direct_value_rank = -1;  // value pass: large items by rank chunks of this many outputs (0 = sub-tiles,
                                  // -1 = by accumulator width: 8192 for 4-byte, 4096 for 8-byte)
     int direct_emit_blocks = 0;             // emit: one warp per (item, block) (1) or one CTA per item (0)              // value pass: small items through the one-walk hash kernel         // CTA size of the value pass (256, 512)         // 1: value semirings use begin/finish instead                   // direct path: lane-contiguous quads merged per word

@@ -774,24 +774,40 @@ struct ValueArgs {
     const int* rbc;       // entries per 4096-row block of every item
     const int32_t* crw;
     void* cv;
-    const int2* arv;      // 4-byte values: A's (row, value bits) interleaved, or null
+    const void* arv;      // A's (row, value bits) interleaved (int2 for 4-byte, int4 for 8-byte values), or null
 };
 
 // One product's A row and value: from the interleaved copy when there is one
 // (one 8-byte gather, one sector), else from the two arrays.
 template <class T_>
-__device__ __forceinline__ void load_prod(const int32_t* __restrict__ Arw, const T_* Av, const int2* __restrict__ Arv,
+__device__ __forceinline__ void load_prod(const int32_t* __restrict__ Arw, const T_* Av, const void* __restrict__ Arv,
                                           int64_t p, int& r, T_& a) {
     if constexpr (sizeof(T_) == 4) {
         if (Arv) {
-            const int2 e = __ldg(Arv + p);
+            const int2 e = __ldg(static_cast<const int2*>(Arv) + p);
             r = e.x;
             memcpy(&a, &e.y, 4);
+            return;
+        }
+    } else if constexpr (sizeof(T_) == 8) {
+        if (Arv) {  // (row, pad, value): one 16-byte load
+            const int4 e = __ldg(static_cast<const int4*>(Arv) + p);
+            r = e.x;
+            const unsigned long long bits = (unsigned long long)(unsigned)e.z | ((unsigned long long)(unsigned)e.w << 32);
+            memcpy(&a, &bits, 8);
             return;
         }
     }
     r = __ldg(&Arw[p]);
     a = Av[p];
+}
+
+__global__ void k_interleave_rv8(int64_t n, const int32_t* __restrict__ rw, const long long* __restrict__ v,
+                                 int4* __restrict__ out) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const unsigned long long x = (unsigned long long)__ldg(v + i);
+        out[i] = make_int4(__ldg(rw + i), 0, (int)(unsigned)x, (int)(unsigned)(x >> 32));
+    }
 }
 
 __global__ void k_interleave_rv(int64_t n, const int32_t* __restrict__ rw, const int32_t* __restrict__ v,
@@ -823,7 +839,7 @@ struct ValueWalkSm {
 template <int SRID, int NT, class Slot>
 __device__ __forceinline__ void value_walk(const DevCsc& A, const DevCsc& B, const int32_t* __restrict__ Atab, int T,
                                            int t, int j, ValueWalkSm<SRID, NT>& sh, Slot slot, int t_hi = -1,
-                                           const int2* __restrict__ Arv = nullptr) {
+                                           const void* __restrict__ Arv = nullptr) {
     using S_ = Sr<SRID>;
     using T_ = typename S_::T;
     constexpr int NW = NT / 32;
@@ -1881,6 +1897,12 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
             launch(c, k_interleave_rv, dim3(grid_for(c, A.span, 256)), dim3(256), 0, A.span, A.rw + A.base,
                    static_cast<const int32_t*>(A.v) + A.base, arv.as<int2>());
             va.arv = arv.as<int2>() - A.base;
+        } else if (value_size(sr) == 8 && A.span > 0 && c.opt.direct_value_interleave == 2) {
+            // opt-in: at C2 / C5 (fp64, cf ~1-1.4) the 16-byte copy did not pay (C5 12.0 -> 12.2 ms)
+            arv = DevBuf(sizeof(int4) * size_t(A.span), c.stream);
+            launch(c, k_interleave_rv8, dim3(grid_for(c, A.span, 256)), dim3(256), 0, A.span, A.rw + A.base,
+                   static_cast<const long long*>(A.v) + A.base, arv.as<int4>());
+            va.arv = arv.as<int4>() - A.base;
         }
         dispatch_sr(sr, [&](auto id) {
             constexpr int ID = decltype(id)::value;

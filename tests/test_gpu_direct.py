@@ -107,11 +107,13 @@ def test_direct_value_pass(port, sr, vtl, hash_, rank):
     assert_parity(got, want, sr.id, f"{sr.name} vtl={vtl}")
 
 
-@pytest.mark.parametrize("interleave", [0, 1])
-@pytest.mark.parametrize("sr", [P.PlusTimesF32, P.MinPlusI32], ids=lambda s: f"{s.name}_{s.dtype}")
+@pytest.mark.parametrize("interleave", [0, 1, 2])
+@pytest.mark.parametrize("sr", [P.PlusTimesF32, P.MinPlusI32, P.PlusTimesF64, P.PlusTimesI64, P.MinPlusF64],
+                         ids=lambda s: f"{s.name}_{s.dtype}")
 def test_direct_value_interleave(port, sr, interleave):
-    """4-byte value types: the value pass gathers A's (row, value) pairs from an
-    interleaved copy (default) or from the two arrays -- same output."""
+    """The value pass gathers A's (row, value) pairs from an interleaved copy
+    (1, the default: 4-byte values; 2: also 8-byte values as 16-byte pairs) or
+    from the two arrays -- same output."""
     a = with_values(port, port.gen_rmat(13), sr.id)
     want = port.spgemm(sr.id, a, a)
     ctx = P.Context()
