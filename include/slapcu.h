@@ -140,7 +140,8 @@ typedef enum {
                                               broadcast, then ONE concatenated-k product forms C(i,j)
                                               (no stage partials, no merge); 0 = per-stage products
                                               double-buffered against the broadcasts + stage merge */
-    SLAPCU_OPT_DIRECT_VALUE_HASH = 20,     /* direct path value pass: 1 (default, = 13) / 13 / 14 = items
+    SLAPCU_OPT_DIRECT_VALUE_HASH = 20,     /* direct path value pass (default: 0 for 4-byte values, 13 for
+                                              8-byte): 1 (= 13) / 13 / 14 = items
                                               with <= 2^(v-1) outputs take one walk into a shared hash
                                               table of 2^v slots keyed by their rows; 0 = every item
                                               takes the row sub-tile pass */

@@ -131,7 +131,7 @@ struct Options {
     int direct_values_fallback = 0;
     int summa_concat = 1;                   // SUMMA: one concatenated-k product per call (no stage merge)
     int direct_value_threads = 512;
-    int direct_value_hash = 1;
+    int direct_value_hash = -1;  // -1 auto: off for 4-byte values (rank chunks take every item), 13 for 8-byte
     int direct_value_interleave = 1;       // value pass: values gathered with their rows (0 off, 1 4-byte, 2 all)
     int direct_value_rank = -1;  // value pass: large items by rank chunks of this many outputs (0 = sub-tiles,
                                  // -1 = by accumulator width: 8192 for 4-byte, 4096 for 8-byte)

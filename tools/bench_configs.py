@@ -61,11 +61,15 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--cpu-cols", type=int, default=256)
     ap.add_argument("--method", default="direct", choices=["direct", "fused", "two_pass"])
+    ap.add_argument("--value-hash", type=int, default=None, help="value pass hash kernel for small items (0 off)")
     ap.add_argument("--value-interleave", type=int, default=None, help="value pass gathers interleaved: 0 off, 1 4-byte values, 2 all")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     stream = torch.cuda.current_stream()
     ctx = P.Context(0, stream)
+    if args.value_hash is not None:
+        from paper_2106_14402_b200 import _lib as L
+        ctx.set_option(L.OPT_DIRECT_VALUE_HASH, args.value_hash)
     if args.value_interleave is not None:
         from paper_2106_14402_b200 import _lib as L
         ctx.set_option(L.OPT_DIRECT_VALUE_INTERLEAVE, args.value_interleave)
