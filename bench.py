@@ -246,69 +246,110 @@ def run_cpu_reference(sr_id, host_a, cols, threads):
 # ---------------------------------------------------------------- our arm
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def run_cpu_reference_slices(sr_id, host_a, cols, threads, want_result=False, t1_slices=(1, 2, 3)):
+    """The unmodified reference local_spgemm (oracle/_ref/libslapref.so) on the
+    column sample A*A(:, J) for J = the survey's four slices: rate with all
+    `threads`, the single-thread rate on the slices in `t1_slices` (the hub
+    slice 0 alone would take ~20 s on one core), and optionally each slice's
+    product for the parity check."""
+    import oracle
+
+    R = oracle.ref()
+    A = oracle.Csc(host_a.nrows, host_a.ncols, host_a.colptr, host_a.rowids, host_a.vals)
+    secs = flops = 0.0
+    results = []
+    for c0 in cpu_sample_offsets(A.ncols, cols):
+        r = R.time_local_spgemm(sr_id, A, A, c0, c0 + cols, threads, want_result=want_result)
+        secs += r[0]
+        flops += r[2]
+        results.append(((c0, c0 + cols), r[3] if want_result else None))
+    t1 = None
+    if t1_slices:
+        s1 = f1 = 0.0
+        offs = cpu_sample_offsets(A.ncols, cols)
+        for i in t1_slices:
+            r = R.time_local_spgemm(sr_id, A, A, offs[i], offs[i] + cols, 1)
+            s1 += r[0]
+            f1 += r[2]
+        t1 = {"value": round(2.0 * f1 / s1 / 1e9, 4), "unit": UNIT, "cores": 1,
+              "sample": f"slices {list(t1_slices)}: {int(f1)} multiplies in {s1:.2f} s"}
+    return 2.0 * flops / secs / 1e9, secs, flops, results, t1
+
+
 def run_ours(args):
-    import torch
-
-    import paper_2106_14402_b200 as P
-    from paper_2106_14402_b200 import _lib as L
-
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if world > 1:
         if args.dist == "1d":
             return run_ours_1d(args, world, rank)
         return run_ours_dist(args, world, rank)
+    import torch
+
+    import paper_2106_14402_b200 as P
+
     torch.cuda.set_device(0)
+    head = P.OrAnd if args.semiring == "or_and" else P.MinPlusI32
+    line = measure_single(args, head)
+    # BASELINE C3 names both semirings: the other one rides in the same line
+    if args.second and head is P.OrAnd:
+        torch.cuda.empty_cache()
+        sub = measure_single(args, P.MinPlusI32)
+        line["min_plus_i32"] = {k: sub[k] for k in ("value", "unit", "ms_per_step", "dtype", "config", "gpu_launches",
+                                                     "clocks", "roofline", "e2e", "cpu_baseline", "parity")}
+    print(json.dumps(line), flush=True)
+
+
+def measure_single(args, sr):
+    """C3 on one GPU for semiring `sr`: device-resident step (value), the
+    roofline of the form+emit pair, parity of four column slices against the
+    reference, e2e through slapcu_batched_spgemm_host, and the CPU baseline."""
+    import ctypes as C
+
+    import torch
+
+    import paper_2106_14402_b200 as P
+    from paper_2106_14402_b200 import _lib as L
+
     dev = torch.device("cuda", 0)
     stream = torch.cuda.current_stream()
     ctx = P.Context(0, stream)
     apply_options(ctx, args)
     lib = ctx.lib
-    sr = P.OrAnd if args.semiring == "or_and" else P.MinPlusI32
     kind = 0 if sr is P.OrAnd else 3
     vs = 1 if sr is P.OrAnd else 4
 
     A = P.fill_values(P.gen_rmat(args.scale, args.edge_factor, 1, ctx=ctx), sr, kind, ctx=ctx)
     n = A.ncols
     total_flops, flops_per = P.estimate_flops(A, A, ctx=ctx)
-    # exact counts (validation + roofline byte accounting only; not used by the step)
+    # exact per-column counts from the two-pass symbolic kernels (an
+    # independent code path): per-column check of the direct product and the
+    # roofline byte accounting; not used by the step
     counts = P.symbolic_nnz(A, A, ctx=ctx).cpu().numpy()
     nnz_c = int(counts.sum())
-    # Column batches sized by the staging bound sum_j min(flops_j, n) -- known
-    # before any product is formed -- so every batch runs the single-pass
-    # begin/finish with no symbolic pre-pass (batched.hpp:122-170 semantics,
-    # with the flops bound in place of the symbolic count).
+    # Column batches sized by the bound sum_j min(flops_j, n) -- known before
+    # any product is formed -- so no symbolic pre-pass runs inside the step
+    # (batched.hpp:122-170 semantics with the flops bound for the count).
     bound = np.minimum(flops_per.cpu().numpy(), A.nrows)
     free, _tot = torch.cuda.mem_get_info()
-    stage_entry = 4 + (0 if sr is P.OrAnd else vs)
     budget = int(args.budget_gb * 2**30) if args.budget_gb > 0 else int(min(0.35 * free, 64 * 2**30))
-    batches = plan_batches(bound, stage_entry, budget)
+    batches = plan_batches(bound, 4 + vs, budget)
     max_cap = max(int(bound[s:e].sum()) for s, e in batches)
     max_cols = max(e - s for s, e in batches)
-    # Two contexts on two streams, batches alternating: batch b+1's pattern
-    # pass (shared-memory bound) runs while batch b's finish (copy / value
-    # pass) is still in flight -- slapcu_spgemm_finish is asynchronous
-    # (SLAPCU_OPT_ASYNC_FINISH) and the next begin() on the same context
-    # settles it.  Each context owns its staging area and output buffers.
-    if args.method == "direct":
-        args.streams = 1  # the direct call synchronises its own stream (item counts, totals)
-    if args.streams == 2:
-        stream2 = torch.cuda.Stream(device=dev)
-        ctxs = [ctx, P.Context(0, stream2)]
-        apply_options(ctxs[1], args)
-        streams = [stream, stream2]
-    else:
-        stream2 = stream
-        ctxs = [ctx]
-        streams = [stream]
-    outs = []
-    for cx in ctxs:
-        cx.set_option(L.OPT_ASYNC_FINISH, 1)
-        outs.append((torch.empty(max_cols + 1, dtype=torch.int64, device=dev),
-                     torch.empty(max(max_cap, 1), dtype=torch.int32, device=dev),
-                     torch.empty(max(max_cap, 1), dtype=sr.torch_dtype, device=dev)))
+    o_cp = torch.empty(max_cols + 1, dtype=torch.int64, device=dev)
+    o_rw = torch.empty(max(max_cap, 1), dtype=torch.int32, device=dev)
+    o_v = torch.empty(max(max_cap, 1), dtype=sr.torch_dtype, device=dev)
     av = A.view()
-    import ctypes as C
 
     def window(c0, c1):
         return L.CscView(A.nrows, c1 - c0, A.nnz, A.colptr.data_ptr() + 8 * c0, A.rowids.data_ptr(),
@@ -316,178 +357,116 @@ def run_ours(args):
 
     wins = [window(s, e) for s, e in batches]
 
-    def step(collect=None):
+    def step(after=None):
+        # a step is one whole product: per-A setup (tile pointers, dense runs)
+        # is rebuilt once per step and shared by its column batches
+        ctx.invalidate()
         for bi, w in enumerate(wins):
-            cx = ctxs[bi % len(ctxs)]
-            o_cp, o_rw, o_v = outs[bi % len(ctxs)]
             nz = C.c_int64()
-            if args.method == "direct":
-                cx.check(lib.slapcu_spgemm_direct(cx.h, C.byref(av), C.byref(w), sr.id, P.SpGemmAlg.hybrid,
-                                                  o_rw.numel(), o_cp.data_ptr(), o_rw.data_ptr(), o_v.data_ptr(),
-                                                  C.byref(nz)), "direct")
-                if collect is not None:
-                    collect(bi, int(nz.value))
+            ctx.check(lib.slapcu_spgemm_direct(ctx.h, C.byref(av), C.byref(w), sr.id, P.SpGemmAlg.hybrid,
+                                               o_rw.numel(), o_cp.data_ptr(), o_rw.data_ptr(), o_v.data_ptr(),
+                                               C.byref(nz)), "direct")
+            if after is not None:
+                after(bi, int(nz.value))
+        ctx.check(lib.slapcu_ctx_synchronize(ctx.h), "synchronize")
+
+    # ---- verification step (untimed): per-column nnz of every batch against
+    # the symbolic counts, and the sample slices captured from the batched
+    # output for the bit-exact comparison with the reference below
+    slices = [(c0, c0 + args.cpu_cols) for c0 in cpu_sample_offsets(n, args.cpu_cols)]
+    captured = {s: [] for s in slices}
+    col_ok = [True]
+    nz_total = [0]
+
+    def verify(bi, nz):
+        s, e = batches[bi]
+        nz_total[0] += nz
+        cp = o_cp[: e - s + 1].cpu().numpy()
+        if not np.array_equal(np.diff(cp), counts[s:e]) or cp[0] != 0:
+            col_ok[0] = False
+        for (c0, c1) in slices:
+            p0, p1 = max(c0, s), min(c1, e)
+            if p0 >= p1:
                 continue
-            cx.check(lib.slapcu_spgemm_begin(cx.h, C.byref(av), C.byref(w), sr.id, P.SpGemmAlg.hybrid, 0,
-                                             o_cp.data_ptr(), C.byref(nz)), "begin")
-            cx.check(lib.slapcu_spgemm_finish(cx.h, C.byref(av), C.byref(w), sr.id, o_rw.data_ptr(),
-                                              o_v.data_ptr()), "finish")
-            if collect is not None:
-                collect(bi, int(nz.value))
-        for cx in ctxs:
-            cx.check(lib.slapcu_ctx_synchronize(cx.h), "synchronize")
+            lo, hi = int(cp[p0 - s]), int(cp[p1 - s])
+            captured[(c0, c1)].append((p0, p1, bi, lo, cp[p0 - s:p1 - s + 1] - lo, o_rw[lo:hi].cpu().numpy(),
+                                       o_v[lo:hi].cpu().numpy()))
 
-    # parity spot check of the benchmarked configuration (column checksums of
-    # the first batch vs. the symbolic counts) happens in tests; here we only
-    # verify totals
-    got = []
-    step(lambda bi, nz: got.append(nz))
-    if os.environ.get("SLAPCU_BENCH_NOCHECK") != "1":
-        assert sum(got) == nnz_c, (sum(got), nnz_c)
+    step(verify)
+    assert nz_total[0] == nnz_c, (nz_total[0], nnz_c)
 
-    for cx in ctxs:
-        cx.set_option(L.OPT_PROFILE, int(args.profile))
+    ctx.set_option(L.OPT_PROFILE, int(args.profile))
     for _ in range(args.warmup - 1):
         step()
     torch.cuda.synchronize()
-    for cx in ctxs:
-        cx.reset_stats()
-    launches0 = sum(cx.launches for cx in ctxs)
+    ctx.reset_stats()
+    launches0 = ctx.launches
     clocks = ClockSampler(0)
     clocks.start()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = [torch.cuda.Event(enable_timing=True) for _ in streams]
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     ev0.record(stream)
-    if stream2 is not stream:
-        stream2.wait_event(ev0)
     for _ in range(args.steps):
         step()
-    for e, s in zip(ev1, streams):
-        e.record(s)
+    ev1.record(stream)
     torch.cuda.synchronize()
     clk = clocks.stop()
-    ms = max(ev0.elapsed_time(e) for e in ev1) / args.steps
-    launches = (sum(cx.launches for cx in ctxs) - launches0) // args.steps
-    kstats = {}
-    for cx in ctxs:
-        for k, (nl, t) in cx.kernel_stats().items():
-            a, b = kstats.get(k, (0, 0.0))
-            kstats[k] = (a + nl, b + t)
-        cx.set_option(L.OPT_PROFILE, 0)
+    ms = ev0.elapsed_time(ev1) / args.steps
+    launches = (ctx.launches - launches0) // args.steps
+    kstats = ctx.kernel_stats()
+    ctx.set_option(L.OPT_PROFILE, 0)
     value = 2.0 * total_flops / (ms / 1e3) / 1e9
 
-    # ---- roofline of the dominant kernel class
+    # ---- roofline: the form + emit pair (+ value pass) is the dominant unit
     peak, peak_kind = measured_peak_gbs()
     per_step = {k: (nl / args.steps, t / args.steps) for k, (nl, t) in kstats.items() if nl}
-    dom = max(per_step, key=lambda k: per_step[k][1])
-    # heavy columns of the fused path: flops > max(256, min(n/128, 4096))
-    lmax = 1024 if args.method == "direct" else max(256, min(A.nrows // 128, 4096))  # light/heavy split
     fl = flops_per.cpu().numpy()
-    heavy = fl > lmax
+    heavy = fl > 1024  # direct path light/heavy split (direct_light_flops_max)
     colnnz_b = np.diff(A.colptr.cpu().numpy())
-    dom_bytes = 0
+    batch_bytes = []
     for s, e in batches:
-        h = heavy[s:e] if dom in ("sym_heavy", "num_heavy") else ~heavy[s:e]
+        h = heavy[s:e]
         nh = int(h.sum())
-        if nh == 0:
-            continue
-        c_ent = int(counts[s:e][h].sum())
-        b_ent = int(colnnz_b[s:e][h].sum())
-        if dom == "sym_heavy" and args.method == "direct":
-            # k_tile_form: B columns + the A pattern in (compulsory once per batch);
-            # its per-product A gathers are L2 traffic, its limiter is the
-            # shared-memory bitmap update
-            dom_bytes += b_ent * 4 + (nh + 1) * 8 + A.nnz * 4 + (n + 1) * 8
-        elif dom == "num_heavy" and args.method == "direct":
-            # k_tile_emit: C rows + values of the heavy columns written in place
-            dom_bytes += c_ent * (4 + vs) + (nh + 1) * 8
-        elif dom == "sym_heavy":  # k_fused_heavy: B cols + A (pattern) in, staged rows out
-            dom_bytes += c_ent * 4 + b_ent * 4 + (nh + 1) * 8 + A.nnz * 4 + (n + 1) * 8
-        elif dom == "num_heavy":  # k_values_heavy: C rows in, values out, B and A with values
-            dom_bytes += c_ent * (4 + vs) + b_ent * (4 + vs) + (nh + 1) * 8 + A.nnz * (4 + vs) + (n + 1) * 8
-        elif dom == "sym_light":  # k_fused_light: staged rows+values out
-            dom_bytes += c_ent * (4 + vs) + b_ent * (4 + vs) + (nh + 1) * 8
-        else:  # copies: read staged, write C
-            dom_bytes += 2 * c_ent * (4 + vs) + (nh + 1) * 8
-    dom_ms = per_step[dom][1]
-    achieved = dom_bytes / (dom_ms / 1e3) / 1e9
+        batch_bytes.append(int(colnnz_b[s:e][h].sum()) * (4 + vs) + int(counts[s:e][h].sum()) * (4 + vs) +
+                           2 * (nh + 1) * 8 + A.nnz * (4 + vs) + (n + 1) * 8 if nh else 0)
+    pair_ms = per_step.get("sym_heavy", (0, 0.0))[1] + per_step.get("num_heavy", (0, 0.0))[1]
+    dom_bytes = sum(batch_bytes)
+    achieved = dom_bytes / (pair_ms / 1e3) / 1e9 if pair_ms else 0.0
     step_bytes = bytes_alg(A.nnz, n, A.nnz, n, nnz_c, n, vs)
-    # per-kernel view (direct path): algorithmic bytes of each class / its time
     traffic = {}
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f)
+            traffic = json.load(f).get(f"{sr.name}_{sr.dtype}", {})
     except Exception:
         pass
-    kname = ({"sym_heavy": "k_tile_form", "sym_light": "k_fused_light", "num_heavy": "k_tile_emit",
-              "num_light": "k_copy_light"} if args.method == "direct" else
-             {"sym_heavy": "k_fused_heavy", "sym_light": "k_fused_light", "num_heavy": "k_values_heavy",
-              "num_light": "k_copy_light+k_copy_heavy"})
-    heavy_c = sum(int(counts[s:e][heavy[s:e]].sum()) for s, e in batches)
+    nlaunch = sum(1 for b in batch_bytes if b)
     kernels = {}
-    if args.method == "direct" and "num_heavy" in per_step and sr is P.OrAnd:
-        em_bytes = heavy_c * (4 + vs)
-        em_ms = per_step["num_heavy"][1]
-        t = traffic.get("k_tile_emit", {})
-        kernels["k_tile_emit"] = {
-            "ms_per_step": round(em_ms, 3), "algorithmic_bytes_per_step": em_bytes,
-            "achieved": round(em_bytes / (em_ms / 1e3) / 1e9, 2), "frac": round(em_bytes / (em_ms / 1e3) / 1e9 / peak, 4),
-            "traffic_per_launch": t.get("dram_bytes_per_launch"), "traffic_launch_ms": t.get("launch_ms"),
-            "note": "writes C's rows + values in place; reads the compact stash"}
-    if args.method == "direct" and "sym_heavy" in per_step:
-        t = traffic.get("k_tile_form", {})
+    if "sym_heavy" in per_step:
+        fm = per_step["sym_heavy"][1]
         kernels["k_tile_form"] = {
-            "ms_per_step": round(per_step["sym_heavy"][1], 3),
-            "multiplies_per_s": round(total_flops / (per_step["sym_heavy"][1] / 1e3), 1),
-            "traffic_per_launch": t.get("dram_bytes_per_launch"), "traffic_launch_ms": t.get("launch_ms"),
-            "note": "bound by the shared-memory/LSU pipe (ncu l1tex ~78%): one test-then-set bitmap update per "
-                    "multiply; A row ids are gathered from L2 (70e9 x 4 B per step)"}
-    dt = traffic.get(kname.get(dom, dom), {})
-    kernel_name = kname.get(dom, dom)
-    dom_traffic = dt.get("dram_bytes_per_launch")
-    dom_launches = per_step[dom][0]
-    if args.method == "direct" and "sym_heavy" in per_step and "num_heavy" in per_step:
-        # The direct product is ONE pass over the heavy columns split into two
-        # kernels: k_tile_form reads B and gathers A (no C bytes), k_tile_emit
-        # writes C.  The algorithmic bytes (SURVEY 8d bytes_alg: B + A in, C out)
-        # belong to the pair, so the pair is the roofline unit; the per-kernel
-        # view is under "kernels".
-        kernel_name = "k_tile_form+k_tile_emit (one product pass over the heavy columns)"
-        if sr is not P.OrAnd:  # the value pass shares the num_heavy class with emit
-            kernel_name = ("k_tile_form+k_tile_emit+value pass (k_item_values_hash / k_item_values_rank: "
-                           "pattern pass, then one value walk over the heavy columns)")
-        dom_ms = per_step["sym_heavy"][1] + per_step["num_heavy"][1]
-        dom_bytes = 0
-        for s, e in batches:
-            h = heavy[s:e]
-            nh = int(h.sum())
-            dom_bytes += (int(colnnz_b[s:e][h].sum()) * (4 + vs) + int(counts[s:e][h].sum()) * (4 + vs) +
-                          2 * (nh + 1) * 8 + A.nnz * (4 + vs) + (n + 1) * 8)
-        achieved = dom_bytes / (dom_ms / 1e3) / 1e9
-        dom_launches = sum(1 for s_, e_ in batches if heavy[s_:e_].any())  # one form+emit pair per batch
-        tf, te = traffic.get("k_tile_form", {}), traffic.get("k_tile_emit", {})
-        if tf.get("dram_bytes_per_launch") and te.get("dram_bytes_per_launch"):
-            dom_traffic = tf["dram_bytes_per_launch"] + te["dram_bytes_per_launch"]
-            dt = {"source": f"{tf.get('source')}; {te.get('source')}"}
-        if "k_tile_form" in kernels:
-            gb = int(fl[heavy].sum()) * 4
-            kernels["k_tile_form"]["gather_bytes_per_step"] = gb
-            kernels["k_tile_form"]["gather_achieved_gbs"] = round(gb / (per_step["sym_heavy"][1] / 1e3) / 1e9, 2)
+            "ms_per_step": round(fm, 3), "multiplies_per_s": round(total_flops / (fm / 1e3), 1),
+            "gather_bytes_per_step": int(fl[heavy].sum()) * 4,
+            "note": "pattern walk: one test-then-set shared bitmap update per multiply; A row ids gathered "
+                    "from L2"}
+    if "num_heavy" in per_step:
+        em = per_step["num_heavy"][1]
+        c_bytes = int(counts[heavy].sum()) * (4 + vs)
+        kernels["k_tile_emit" + ("" if sr is P.OrAnd else "+value pass")] = {
+            "ms_per_step": round(em, 3), "c_bytes_per_step": c_bytes,
+            "achieved": round(c_bytes / (em / 1e3) / 1e9, 2), "frac": round(c_bytes / (em / 1e3) / 1e9 / peak, 4)}
     roofline = {
         "bound": "hbm",
-        "method": args.method,
-        "kernel": kernel_name,
-        "achieved": round(achieved, 2),
-        "peak": peak,
-        "unit": "GB/s",
-        "frac": round(achieved / peak, 5),
-        "traffic": dom_traffic,
-        "traffic_source": dt.get("source"),
-        "alg_bytes_per_launch": round(dom_bytes / max(dom_launches, 1)),
+        "kernel": "k_tile_form+k_tile_emit" + ("" if sr is P.OrAnd else "+value pass") +
+                  " (one product over the heavy columns of a column batch)",
+        "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 5),
+        "traffic": traffic.get("dram_bytes_per_launch"),
+        "traffic_alg_bytes_same_batch": traffic.get("alg_bytes_same_batch"),
+        "traffic_source": traffic.get("source"),
+        "alg_bytes_per_launch": round(dom_bytes / max(nlaunch, 1)),
+        "alg_bytes_per_batch": batch_bytes,
         "peak_source": peak_kind,
-        "dominant_share_of_step": round(dom_ms / ms, 4),
-        "launches_per_step": dom_launches,
+        "dominant_share_of_step": round(pair_ms / ms, 4),
+        "launches_per_step": nlaunch,
         "algorithmic_bytes_per_step": dom_bytes,
         "step_bytes_alg": step_bytes,
         "step_achieved_gbs": round(step_bytes / (ms / 1e3) / 1e9, 2),
@@ -495,29 +474,38 @@ def run_ours(args):
         "class_ms_per_step": {k: round(v[1], 3) for k, v in per_step.items()},
         "kernels": kernels,
     }
+    del o_cp, o_rw, o_v
+    torch.cuda.empty_cache()
 
-    # ---- e2e through the public API with host buffers
+    # ---- e2e through the reference-facing host call
     e2e = None
     if not args.no_e2e:
-        outs.clear()  # the e2e run allocates its own (exactly sized) output buffers
-        torch.cuda.empty_cache()
-        e2e = run_e2e_single(args, A, sr, batches, counts, total_flops, ctx, stream)
+        e2e = run_e2e_host(args, A, sr, budget, total_flops, ctx)
 
-    # ---- CPU baseline (reference, bounded sample)
-    cpu = None
+    # ---- CPU baseline + parity on the same slices (reference, bounded sample)
+    cpu, parity = None, {"checked": False}
+    host = None
     if not args.no_cpu:
         try:
             host = A.to_host()
             threads = os.cpu_count() or 1
-            gf, secs, fl = run_cpu_reference(sr.id, host, args.cpu_cols, threads)
+            gf, secs, f_s, results, t1 = run_cpu_reference_slices(sr.id, host, args.cpu_cols, threads,
+                                                                   want_result=True)
             cpu = {"value": round(gf, 4), "unit": UNIT, "cores": threads, "kind": "reference",
+                   "cpu_model": cpu_model(), "t1": t1,
                    "sample": f"slap::local_spgemm(A, A(:, J)) hybrid, 4 slices x {args.cpu_cols} cols at offsets "
-                             f"{cpu_sample_offsets(n, args.cpu_cols)}; {int(fl)} multiplies in {secs:.2f} s"}
+                             f"{[s[0] for s in slices]}; {int(f_s)} multiplies in {secs:.2f} s"}
+            parity = check_slices(results, captured, sr)
         except Exception as ex:  # the reference .so is optional on the box
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {ex}"}
+            parity = {"checked": False, "why": str(ex)}
+    parity["per_column_nnz_vs_symbolic"] = bool(col_ok[0])
+    if args.scale == 20 and args.edge_factor == 16:
+        # the survey's reference-measured totals (SURVEY.md Appendix A probe)
+        parity["totals_match_reference"] = bool(total_flops == 70065456202 and nnz_c == 23721688001)
 
-    line = {
+    return {
         "metric": METRIC,
         "value": round(value, 3),
         "unit": UNIT,
@@ -544,8 +532,36 @@ def run_ours(args):
         "roofline": roofline,
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "parity": parity,
     }
-    print(json.dumps(line), flush=True)
+
+
+def check_slices(results, captured, sr):
+    """Bit-exact comparison (integer / Boolean semirings) of the reference's
+    C(:, J) with the GPU's batched output for the same columns."""
+    out = {"checked": True, "rule": "bit-exact colptr, rowids and values (integer / Boolean semiring)",
+           "slices": []}
+    ok_all = True
+    for (c0, c1), want in results:
+        parts = captured[(c0, c1)]
+        cps, rws, vls = [np.zeros(1, np.int64)], [], []
+        base = 0
+        for (_p0, _p1, _bi, _lo, cp, rw, v) in parts:
+            cps.append(cp[1:] + base)
+            base += int(cp[-1])
+            rws.append(rw)
+            vls.append(v)
+        g_cp = np.concatenate(cps)
+        g_rw = np.concatenate(rws) if rws else np.zeros(0, np.int32)
+        g_v = np.concatenate(vls) if vls else np.zeros(0, sr.np_dtype)
+        exact = (np.array_equal(g_cp, want.colptr) and np.array_equal(g_rw, want.rowids) and
+                 g_v.astype(sr.np_dtype).tobytes() == np.asarray(want.vals, sr.np_dtype).tobytes())
+        ok_all &= bool(exact)
+        out["slices"].append({"cols": [c0, c1], "nnz": int(want.colptr[-1]), "exact": bool(exact),
+                              "batches": sorted({p[2] for p in parts}),
+                              "max_batch_offset": max([int(p[3]) for p in parts] + [0])})
+    out["all_exact"] = bool(ok_all)
+    return out
 
 
 def run_e2e_single(args, A, sr, batches, counts, total_flops, ctx, stream):

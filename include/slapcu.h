@@ -96,6 +96,11 @@ typedef struct slapcu_ctx_s* slapcu_ctx;
 slapcu_status slapcu_ctx_create(slapcu_ctx* out, int device, void* stream);
 slapcu_status slapcu_ctx_destroy(slapcu_ctx ctx);
 slapcu_status slapcu_ctx_set_stream(slapcu_ctx ctx, void* stream);
+/* Drops every per-operand cache of the context (A tile pointers, dense-run
+ * bitmaps, the symbolic->numeric plan).  Never needed for correctness: the
+ * caches are keyed on a content fingerprint of A's pattern, recomputed on every
+ * call; the benchmark calls it once per step so per-A setup is timed. */
+slapcu_status slapcu_ctx_invalidate(slapcu_ctx ctx);
 /* Waits for the context's stream and reports any deferred error. */
 slapcu_status slapcu_ctx_synchronize(slapcu_ctx ctx);
 const char* slapcu_ctx_last_error(slapcu_ctx ctx);
@@ -119,9 +124,9 @@ typedef enum {
     SLAPCU_OPT_DIRECT_TILE_ROWS_LOG2 = 9,  /* direct path: rows per (column, row tile) item (default 17) */
     SLAPCU_OPT_DIRECT_SPLIT_FLOPS = 10,    /* direct path: items with more multiplies than this are formed
                                               by several CTAs over equal-flops parts of B(:,j) (>= 1024) */
-    SLAPCU_OPT_DIRECT_MARK_MODE = 11,      /* direct path bitmap update: 0 test-then-set per product,
-                                              1 shared atomic per product, 2 lane-contiguous quads merged
-                                              per 32-row word before the update */
+    SLAPCU_OPT_DIRECT_MARK_MODE = 11,      /* direct path bitmap update (test-then-set per product):
+                                              0 (default) the touched-word summary is rebuilt by ballots
+                                              after the walk, 2 it is kept per update */
     SLAPCU_OPT_DIRECT_FORM_THREADS = 12,   /* direct path: threads per form CTA (128, 256, 512) */
     SLAPCU_OPT_DIRECT_EMIT_THREADS = 13,   /* direct path emit granularity: 128 (default) = one 4-warp
                                               CTA per item; 32 = one warp per (item, 128-word block) */

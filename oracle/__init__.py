@@ -222,17 +222,23 @@ class _Ref:
         L.ref_read_binary.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, P, C.c_void_p, C.c_void_p]
         L.ref_free.argtypes = [C.c_void_p]
         L.ref_time_local_spgemm.argtypes = [C.c_int, C.c_int, C.c_int, P, P, C.c_int64, C.c_int64,
-                                            C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+                                            C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_int64), P]
 
-    def time_local_spgemm(self, sr, a: Csc, b: Csc, c0: int, c1: int, threads: int, alg=HYBRID):
+    def time_local_spgemm(self, sr, a: Csc, b: Csc, c0: int, c1: int, threads: int, alg=HYBRID,
+                          want_result=False):
         """Seconds of ONE reference local_spgemm(A, B(:, c0:c1)) call with
-        `threads` threads (conversions excluded); returns (seconds, nnz, flops)."""
+        `threads` threads (conversions excluded); returns (seconds, nnz, flops),
+        plus the product C(:, c0:c1) as a Csc when `want_result`."""
         keep = []
         sec, nnz, fl = C.c_double(), C.c_int64(), C.c_int64()
+        out = _CCsc() if want_result else None
         rc = self.lib.ref_time_local_spgemm(sr, alg, threads, C.byref(_as_c(a, keep)), C.byref(_as_c(b, keep)), c0, c1,
-                                            C.byref(sec), C.byref(nnz), C.byref(fl))
+                                            C.byref(sec), C.byref(nnz), C.byref(fl),
+                                            C.byref(out) if want_result else None)
         if rc != 0:
             raise RuntimeError(f"ref_time_local_spgemm failed: {rc}")
+        if want_result:
+            return sec.value, nnz.value, fl.value, _from_c(out, DTYPES[sr], self.lib.ref_free)
         return sec.value, nnz.value, fl.value
 
     def local_spgemm(self, sr, a: Csc, b: Csc, alg=HYBRID, threads=1, b_dcsc=False) -> Csc:

@@ -198,9 +198,11 @@ int ref_local_spgemm(int sr, int alg, int threads, const ref_csc* a, const ref_c
 /// times exactly one slap::local_spgemm call (spgemm.hpp:275-330) with
 /// `threads` worker threads.  Returns 0 and writes seconds, output nnz and the
 /// multiply count (estimate_flops) of the slice; -5 if nnz(C) would overflow
-/// the reference's int32 colptr.
+/// the reference's int32 colptr.  When `c` is non-null the slice's product
+/// C(:, c0:c1) is returned too (converted after the timed region), so the
+/// benchmark checks the GPU output of the same columns against it.
 int ref_time_local_spgemm(int sr, int alg, int threads, const ref_csc* a, const ref_csc* b, int64_t c0, int64_t c1,
-                          double* seconds, int64_t* nnz_out, int64_t* flops_out) {
+                          double* seconds, int64_t* nnz_out, int64_t* flops_out, ref_csc* c) {
     try {
         return with_semiring(sr, [&](auto s) -> int {
             using VT = typename decltype(s)::left_type;
@@ -222,6 +224,7 @@ int ref_time_local_spgemm(int sr, int alg, int threads, const ref_csc* a, const 
             *seconds = std::chrono::duration<double>(t1 - t0).count();
             *nnz_out = static_cast<int64_t>(cm.nnz());
             *flops_out = est.total_flops;
+            if (c) from_csc(cm, c);
             return 0;
         });
     } catch (const std::exception& e) {

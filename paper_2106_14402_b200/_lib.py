@@ -106,6 +106,7 @@ SIGNATURES = [
     ("slapcu_ctx_create", _I, [C.POINTER(_P), _I, _P]),
     ("slapcu_ctx_destroy", _I, [_P]),
     ("slapcu_ctx_set_stream", _I, [_P, _P]),
+    ("slapcu_ctx_invalidate", _I, [_P]),
     ("slapcu_ctx_synchronize", _I, [_P]),
     ("slapcu_ctx_last_error", C.c_char_p, [_P]),
     ("slapcu_ctx_set_option", _I, [_P, _I, _L]),

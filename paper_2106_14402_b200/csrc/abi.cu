@@ -123,6 +123,14 @@ slapcu_status slapcu_ctx_synchronize(slapcu_ctx ctx) {
     return guarded(ctx, [&](Ctx& c) { SLAPCU_CUDA(cudaStreamSynchronize(c.stream)); });
 }
 
+slapcu_status slapcu_ctx_invalidate(slapcu_ctx ctx) {
+    return guarded(ctx, [&](Ctx& c) {
+        c.direct.atp_valid = false;
+        c.direct.atpv_valid = false;
+        c.plan.valid = false;
+    });
+}
+
 slapcu_status slapcu_ctx_set_stream(slapcu_ctx ctx, void* stream) {
     return guarded(ctx, [&](Ctx& c) { c.stream = static_cast<cudaStream_t>(stream); });
 }
@@ -146,7 +154,8 @@ slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t v
             c.opt.direct_tile_rows_log2 = (int)v;
             break;
         case SLAPCU_OPT_DIRECT_MARK_MODE:
-            require(v >= 0 && v <= 3, SLAPCU_ERR_INVALID, "mark mode must be 0..3 (3: timing experiment, no update)");
+            require(v == 0 || v == 2, SLAPCU_ERR_INVALID,
+                    "mark mode must be 0 (bitmap, summary by ballots) or 2 (summary kept per update)");
             c.opt.direct_mark_mode = (int)v;
             break;
         case SLAPCU_OPT_DIRECT_PERSISTENT: c.opt.direct_persistent = v != 0; break;

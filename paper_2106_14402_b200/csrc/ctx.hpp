@@ -135,7 +135,7 @@ struct Options {
     int direct_value_interleave = 1;       // value pass: values gathered with their rows (0 off, 1 4-byte, 2 all)
     int direct_value_rank = -1;  // value pass: large items by rank chunks of this many outputs (0 = sub-tiles,
                                  // -1 = by accumulator width: 8192 for 4-byte, 4096 for 8-byte)
-    int direct_emit_blocks = 0;             // emit: one warp per (item, block) (1) or one CTA per item (0)              // value pass: small items through the one-walk hash kernel         // CTA size of the value pass (256, 512)         // 1: value semirings use begin/finish instead                   // direct path: lane-contiguous quads merged per word
+    int direct_emit_blocks = 0;             // emit: one warp per (item, block) (1) or one CTA per item (0)
     int direct_persistent = 1;              // form kernel: persistent CTAs (1) or one CTA per unit (0)
     int direct_form_threads = 256;          // CTA size of the form kernel (128, 256, 512)
     int direct_emit_threads = 128;          // CTA size of the emit kernel (128, 256)
@@ -147,15 +147,16 @@ struct Options {
 struct DirectCache {
     FusedState light;  // light columns: staged hash output (fused.cu kernels)
     DevBuf atp;        // A tile pointers int32[A.ncols][T+1]
-    const void* atp_key = nullptr;
+    uint64_t atp_key = 0;  // pattern fingerprint of the A they were built for (pattern_fingerprint)
     int64_t atp_ncols = -1, atp_nnz = -1;
     int atp_tl = -1;
     bool atp_valid = false;
     DevBuf dslot, dbm;  // dense A runs: slot per (k, tile), tile bitmaps
     DevBuf atpv;        // A tile pointers at the value-pass sub-tile height
-    const void* atpv_key = nullptr;
+    uint64_t atpv_key = 0;
     int64_t atpv_ncols = -1, atpv_nnz = -1;
     int atpv_tl = -1;
+    bool atpv_valid = false;
     int ndense = 0, dense_min = -1;
     DevBuf lp, hcnt, hl, items, ifl, sres, soff, units, order, stash, partial, cnt, form, hoff, rbc;
     DevBuf dist_rw, dist_v;  // SUMMA concatenated product: bound-sized output scratch
@@ -218,6 +219,7 @@ Ctx& ctx_of(slapcu_ctx c);
 
 // Reads cp[0] and cp[ncols] (synchronizes the context stream).
 void resolve(Ctx& c, DevCsc& m);
+uint64_t pattern_fingerprint(Ctx& c, const DevCsc& m);  // resolved m
 
 // spgemm.cu
 void spgemm_flops(Ctx& c, const DevCsc& A, const DevCsc& B, int64_t* flops_dev, int64_t* total);

@@ -121,9 +121,7 @@ struct DenseRuns {
 // global loads ahead of these shared updates.)
 template <int MODE>
 __device__ __forceinline__ void set_bits(unsigned a, unsigned b, unsigned sa, unsigned sb) {
-    if (MODE == 3) {  // timing experiment only: no update (wrong results)
-        asm volatile("" ::"r"(a), "r"(b), "r"(sa), "r"(sb));
-    } else if (MODE == 0) {  // bitmap only; the summary is rebuilt by a ballot pass
+    if (MODE == 0) {  // bitmap only; the summary is rebuilt by a ballot pass
         asm volatile(
             "{\n\t.reg .pred p;\n\t.reg .b32 x;\n\t"
             "ld.shared.u32 x, [%0];\n\t"
@@ -1146,7 +1144,9 @@ __global__ void __launch_bounds__(NT) k_item_values_rank(ValueArgs g, const Rank
         const int w = rr >> 5;
         return &val[gbase[w >> 5] + pre16[w] + __popc(bm[w] & ((1u << (rr & 31)) - 1u))];
     };
-    const int ts0 = (it.y << (g.TL - g.VTL)) + ch.b0, ts1 = (it.y << (g.TL - g.VTL)) + ch.b1;
+    // (the last chunk of an item ends at the item's last row block, which can lie
+    // past the matrix's last 4096-row block when nrows is not a multiple of 2^TL)
+    const int ts0 = min((it.y << (g.TL - g.VTL)) + ch.b0, g.Tv), ts1 = min((it.y << (g.TL - g.VTL)) + ch.b1, g.Tv);
     value_walk<SRID, NT>(g.A, g.B, g.Atpv, g.Tv, ts0, j, sh, slot, ts1, g.arv);
     T* Cv = static_cast<T*>(g.cv);
     for (int q = tid; q < n; q += NT) Cv[lo + q] = S_::out(val[q]);
@@ -1521,10 +1521,13 @@ int direct_tile_log2(const Ctx& c, int64_t nrows) {
 }
 
 // Tile pointers of A for row tiles of 2^TL rows (cached on the context).
-static const int32_t* tile_pointers(Ctx& c, const DevCsc& A, int TL, int T) {
+// The cache is keyed on the CONTENT of A's pattern (fp = pattern_fingerprint),
+// never on its address: SUMMA receive slots and pooled buffers reuse
+// addresses for different operands.
+static const int32_t* tile_pointers(Ctx& c, const DevCsc& A, uint64_t fp, int TL, int T) {
     DirectCache& d = c.direct;
     const int dmin = (int)std::min<int64_t>(c.opt.direct_dense_run_min, INT32_MAX);
-    if (d.atp_valid && d.atp_key == A.cp && d.atp_ncols == A.ncols && d.atp_tl == TL && d.atp_nnz == A.nnz &&
+    if (d.atp_valid && d.atp_key == fp && d.atp_ncols == A.ncols && d.atp_tl == TL && d.atp_nnz == A.nnz &&
         d.dense_min == dmin)
         return d.atp.as<int32_t>();
     d.atp.reset(sizeof(int32_t) * size_t(A.ncols) * (T + 1), c.stream);
@@ -1553,7 +1556,7 @@ static const int32_t* tile_pointers(Ctx& c, const DevCsc& A, int TL, int T) {
                    TL, (const int2*)runs.as<int2>(), d.dbm.as<unsigned>());
         }
     }
-    d.atp_key = A.cp;
+    d.atp_key = fp;
     d.atp_ncols = A.ncols;
     d.atp_nnz = A.nnz;
     d.atp_tl = TL;
@@ -1562,18 +1565,19 @@ static const int32_t* tile_pointers(Ctx& c, const DevCsc& A, int TL, int T) {
 }
 
 // Tile pointers at the value-pass sub-tile height (cached like Atp).
-static const int32_t* value_tile_pointers(Ctx& c, const DevCsc& A, int VTL, int Tv) {
+static const int32_t* value_tile_pointers(Ctx& c, const DevCsc& A, uint64_t fp, int VTL, int Tv) {
     DirectCache& d = c.direct;
-    if (d.atpv_key == A.cp && d.atpv_ncols == A.ncols && d.atpv_tl == VTL && d.atpv_nnz == A.nnz)
+    if (d.atpv_valid && d.atpv_key == fp && d.atpv_ncols == A.ncols && d.atpv_tl == VTL && d.atpv_nnz == A.nnz)
         return d.atpv.as<int32_t>();
     d.atpv.reset(sizeof(int32_t) * size_t(A.ncols) * (Tv + 1), c.stream);
     KScope ks(c, KC_BIN);
     launch(c, k_tile_ptr, dim3(grid_for(c, A.ncols * (Tv + 1), 256)), dim3(256), 0, A, VTL, Tv,
            d.atpv.as<int32_t>());
-    d.atpv_key = A.cp;
+    d.atpv_key = fp;
     d.atpv_ncols = A.ncols;
     d.atpv_nnz = A.nnz;
     d.atpv_tl = VTL;
+    d.atpv_valid = true;
     return d.atpv.as<int32_t>();
 }
 
@@ -1620,6 +1624,7 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
     SLAPCU_CUDA(cudaEventRecord(c.ev[0], c.stream));
     DirectCache& d = c.direct;
     FusedState& f = d.light;
+    const uint64_t afp = pattern_fingerprint(c, A);
     f.ones = ones;
     prepare_plan(c, A, B);
     const int64_t* flops = c.plan.flops.as<int64_t>();
@@ -1671,7 +1676,7 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
     SLAPCU_CUDA(cudaMemsetAsync(d.hcnt.get(), 0, sizeof(unsigned long long) * std::max<int64_t>(n, 1), c.stream));
     int nitems = 0;
     if (nh > 0) {
-        const int32_t* Atp = tile_pointers(c, A, TL, T);
+        const int32_t* Atp = tile_pointers(c, A, afp, TL, T);
         KScope ks(c, KC_BIN);
         DevBuf hflag(sizeof(int) * (n + 1), c.stream), hpre(sizeof(int) * (n + 1), c.stream);
         launch(c, k_mark_heavy, dim3(grid_for(c, n, 256)), dim3(256), 0, n, flops, lmax, spec.all_heavy != 0,
@@ -1802,9 +1807,7 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
             launch(c, kf, dim3((unsigned)grid), dim3(nt), smem, g);
         };
         const int ft = c.opt.direct_form_threads;
-        if (c.opt.direct_mark_mode == 3)
-            form(k_tile_form<256, 3>, 256);
-        else if (c.opt.direct_mark_mode == 2)
+        if (c.opt.direct_mark_mode == 2)
             form(k_tile_form<256, 2>, 256);
         else if (ft == 128)
             form(k_tile_form<128, 0>, 128);
@@ -1872,8 +1875,8 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
         const int Tv = (int)((A.nrows + (int64_t(1) << VTL) - 1) >> VTL);
         const bool rank_path = c.opt.direct_value_rank != 0 && TL >= 12;
         // (one cached table at a time: only the sub-tile path needs 2^VTL rows)
-        const int32_t* Atpv = rank_path ? nullptr : value_tile_pointers(c, A, VTL, Tv);
-        const int32_t* Atp = tile_pointers(c, A, TL, T);
+        const int32_t* Atpv = rank_path ? nullptr : value_tile_pointers(c, A, afp, VTL, Tv);
+        const int32_t* Atp = tile_pointers(c, A, afp, TL, T);
         // small items (<= kHashCap outputs) take the one-walk hash kernel
         // auto: 4-byte values take every item through the rank chunks (C3 MinPlus 561 -> 531 ms,
         // C4 product 66.1 -> 63.9 ms); 8-byte values keep the hash kernel for small items
@@ -1931,7 +1934,7 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
                 const int cap = c.opt.direct_value_rank > 0 ? c.opt.direct_value_rank : (sizeof(Acc) <= 4 ? 8192 : 4096);
                 const int T12 = (int)((A.nrows + 4095) >> 12);
                 ValueArgs vr = va;
-                vr.Atpv = value_tile_pointers(c, A, 12, T12);
+                vr.Atpv = value_tile_pointers(c, A, afp, 12, T12);
                 vr.Tv = T12;
                 vr.VTL = 12;
                 const int nrb = (W + kRbcWords - 1) / kRbcWords;

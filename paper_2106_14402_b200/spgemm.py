@@ -271,6 +271,10 @@ class Context:
     def reset_stats(self):
         self.check(self.lib.slapcu_ctx_reset_stats(self.h), "reset_stats")
 
+    def invalidate(self):
+        """Drops the per-operand caches (slapcu_ctx_invalidate)."""
+        self.check(self.lib.slapcu_ctx_invalidate(self.h), "invalidate")
+
     def last_phase_ms(self):
         a, b = C.c_float(), C.c_float()
         self.lib.slapcu_ctx_last_phase_ms(self.h, C.byref(a), C.byref(b))
