@@ -58,8 +58,6 @@ def parse():
     ap.add_argument("--sym-tile-log2", type=int, default=0, help="row-tile height of the pattern bitmap (0 = default)")
     ap.add_argument("--tile-log2", type=int, default=0, help="row-tile height of the value pass (0 = default)")
     ap.add_argument("--dense-min", type=int, default=None, help="byte-flag pattern path for flops >= this (0 off)")
-    ap.add_argument("--method", default="direct", choices=["direct", "fused"],
-                    help="direct: slapcu_spgemm_direct writes C in place in one pass; fused: begin/finish")
     ap.add_argument("--direct-tile-log2", type=int, default=0, help="rows per direct-path item (0 = default)")
     ap.add_argument("--direct-split", type=int, default=None, help="direct path: split items above this many flops")
     ap.add_argument("--mark-mode", type=int, default=None, help="direct path bitmap update mode (0/1/2)")
@@ -74,14 +72,16 @@ def parse():
     ap.add_argument("--value-interleave", type=int, default=None,
                     help="direct path value pass: 4-byte values gathered with their rows (1) or not (0)")
     ap.add_argument("--quads", type=int, default=None, help="direct path: lane-contiguous quads (1) or strided (0)")
+    ap.add_argument("--tile-major", type=int, default=None, help="direct path form: units ordered by row tile (1)")
+    ap.add_argument("--form-walk", type=int, default=None, help="direct path form: 1 warp-independent walk")
     ap.add_argument("--dist", default="1d", choices=["1d", "summa"],
                     help="N>1: 1d = flops-balanced column blocks with A replicated (no data-path collective); "
                          "summa = the 2D SUMMA / 3D drivers (NCCL stage broadcasts, fiber exchange, merge)")
     ap.add_argument("--balance-out", type=float, default=3.0, help="1d split: weight of a column's output bound")
     ap.add_argument("--balance-col", type=float, default=2000.0, help="1d split: per-column weight")
     ap.add_argument("--calibrate", type=int, default=4, help="1d split: timed re-balancing rounds before warmup")
-    ap.add_argument("--streams", type=int, default=1, choices=[1, 2],
-                    help="2: alternate column batches over two contexts/streams (async finish)")
+    ap.add_argument("--second", type=int, default=1,
+                    help="1: also measure MinPlus int32 C3 (BASELINE's other C3 semiring) into the same line")
     return ap.parse_args()
 
 
@@ -110,6 +110,10 @@ def apply_options(ctx, args):
         ctx.set_option(L.OPT_DIRECT_PERSISTENT, args.persistent)
     if args.quads is not None:
         ctx.set_option(L.OPT_DIRECT_QUADS, args.quads)
+    if args.tile_major is not None:
+        ctx.set_option(L.OPT_DIRECT_TILE_MAJOR, args.tile_major)
+    if args.form_walk is not None:
+        ctx.set_option(L.OPT_DIRECT_FORM_WALK, args.form_walk)
     if args.value_rank is not None:
         ctx.set_option(L.OPT_DIRECT_VALUE_RANK, args.value_rank)
     if args.value_interleave is not None:
@@ -564,91 +568,51 @@ def check_slices(results, captured, sr):
     return out
 
 
-def run_e2e_single(args, A, sr, batches, counts, total_flops, ctx, stream):
-    """Host-buffer end-to-end: H2D of A (pinned) + per-batch SpGEMM + D2H of
-    every batch's C (chunked into a pinned ring) inside the timed region; the
-    read-back of batch k overlaps the product of batch k+1."""
-    import ctypes as C
-
+def run_e2e_host(args, A, sr, budget, total_flops, ctx):
+    """End to end through the reference-facing host call
+    (slapcu_batched_spgemm_host = batched.hpp:153-170 with host operands): A
+    in pinned host memory, H2D of A and B inside the call, every column batch
+    of C read back into pinned host memory and handed to a consumer.  Timed
+    with CUDA events around the (synchronous) call."""
     import torch
 
     import paper_2106_14402_b200 as P
-    from paper_2106_14402_b200 import _lib as L
+    from paper_2106_14402_b200 import batched as BT
 
-    vs = 1 if sr is P.OrAnd else 4
-    ctx.set_option(L.OPT_ASYNC_FINISH, 0)  # one stream here; errors reported per call
-    h_cp = A.colptr.cpu().pin_memory()
-    h_rw = A.rowids.cpu().pin_memory()
-    h_v = A.vals.cpu().pin_memory()
-    d_cp = torch.empty_like(A.colptr)
-    d_rw = torch.empty_like(A.rowids)
-    d_v = torch.empty_like(A.vals)
-    max_nnz = max(int(counts[s:e].sum()) for s, e in batches)
-    max_cols = max(e - s for s, e in batches)
-    dev = A.colptr.device
-    # two output sets: batch k+1 is computed on the library's stream while
-    # batch k is read back on a copy stream (the D2H is the long pole)
-    outs2 = [(torch.empty(max_cols + 1, dtype=torch.int64, device=dev),
-              torch.empty(max(max_nnz, 1), dtype=torch.int32, device=dev),
-              torch.empty(max(max_nnz, 1), dtype=sr.torch_dtype, device=dev)) for _ in range(2)]
-    copy_stream = torch.cuda.Stream(device=dev)
-    freed = [torch.cuda.Event() for _ in range(2)]
-    chunk = 1 << 28  # elements per D2H chunk
-    h_out_rw = torch.empty(chunk, dtype=torch.int32).pin_memory()
-    h_out_v = torch.empty(chunk, dtype=sr.torch_dtype).pin_memory()
-    h_out_cp = torch.empty(max_cols + 1, dtype=torch.int64).pin_memory()
-    lib = ctx.lib
-    h2d = A.colptr.numel() * 8 + A.nnz * (4 + vs)
-    d2h = 0
+    hcp = A.colptr.cpu().pin_memory()
+    hrw = A.rowids.cpu().pin_memory()
+    hv = A.vals.cpu().pin_memory()
+    ha = P.CscMatrix(A.nrows, A.ncols, hcp.numpy(), hrw.numpy(), hv.numpy())
+    free, _ = torch.cuda.mem_get_info()
+    e2e_budget = int(min(0.12 * free, 16 * 2**30))
+    moved = [0, 0]
 
-    def one():
-        nonlocal d2h
-        d2h = 0
-        d_cp.copy_(h_cp, non_blocking=True)
-        d_rw.copy_(h_rw, non_blocking=True)
-        d_v.copy_(h_v, non_blocking=True)
-        av = L.CscView(A.nrows, A.ncols, A.nnz, d_cp.data_ptr(), d_rw.data_ptr(), d_v.data_ptr())
-        for k, (s, e) in enumerate(batches):
-            o_cp, o_rw, o_v = outs2[k & 1]
-            if k >= 2:
-                stream.wait_event(freed[k & 1])  # batch k-2's read-back of this set is done
-            w = L.CscView(A.nrows, e - s, A.nnz, d_cp.data_ptr() + 8 * s, d_rw.data_ptr(), d_v.data_ptr())
-            nz = C.c_int64()
-            if args.method == "direct":
-                ctx.check(lib.slapcu_spgemm_direct(ctx.h, C.byref(av), C.byref(w), sr.id, P.SpGemmAlg.hybrid,
-                                                   o_rw.numel(), o_cp.data_ptr(), o_rw.data_ptr(), o_v.data_ptr(),
-                                                   C.byref(nz)), "direct")
-            else:
-                ctx.check(lib.slapcu_spgemm_begin(ctx.h, C.byref(av), C.byref(w), sr.id, P.SpGemmAlg.hybrid, 0,
-                                                  o_cp.data_ptr(), C.byref(nz)), "begin")
-                ctx.check(lib.slapcu_spgemm_finish(ctx.h, C.byref(av), C.byref(w), sr.id, o_rw.data_ptr(),
-                                                   o_v.data_ptr()), "finish")
-            nzv = int(nz.value)
-            copy_stream.wait_stream(stream)
-            with torch.cuda.stream(copy_stream):
-                h_out_cp[: e - s + 1].copy_(o_cp[: e - s + 1], non_blocking=True)
-                for o in range(0, nzv, chunk):
-                    m = min(chunk, nzv - o)
-                    h_out_rw[:m].copy_(o_rw[o:o + m], non_blocking=True)
-                    h_out_v[:m].copy_(o_v[o:o + m], non_blocking=True)
-                freed[k & 1].record(copy_stream)
-            d2h += (e - s + 1) * 8 + nzv * (4 + vs)
-        stream.wait_stream(copy_stream)  # the step ends when the last batch is on the host
-        stream.synchronize()
+    def consumer(r, s, e, c):
+        moved[0] += c.colptr.nbytes + c.rowids.nbytes + c.vals.nbytes
+        moved[1] += int(c.colptr[-1])
 
-    one()  # warm-up
-    t0 = time.perf_counter()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
+    BT.batched_spgemm_host(ha, ha, sr, budget_bytes=e2e_budget, consumer=consumer, ctx=ctx)  # warm-up (pins buffers)
+    stream = torch.cuda.current_stream()
+    ms_all = []
     for _ in range(max(args.e2e_steps, 1)):
-        one()
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1) / max(args.e2e_steps, 1)
-    wall = (time.perf_counter() - t0) / max(args.e2e_steps, 1)
+        moved[0] = moved[1] = 0
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e0.record(stream)
+        nnz = BT.batched_spgemm_host(ha, ha, sr, budget_bytes=e2e_budget, consumer=consumer, ctx=ctx)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        ms_all.append(e0.elapsed_time(e1))
+    ms = statistics.mean(ms_all)
+    assert moved[1] == nnz
+    h2d = 2 * (hcp.numel() * 8 + hrw.numel() * 4 + hv.numel() * hv.element_size())  # A and B (= A) operands
     return {"value": round(2.0 * total_flops / (ms / 1e3) / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ms, 3), "wall_ms_per_step": round(wall * 1e3, 3),
-            "steps": max(args.e2e_steps, 1)}
+            "d2h_bytes_per_step": int(moved[0]), "ms_per_step": round(ms, 3), "wall_ms_per_step": round(wall * 1e3, 3),
+            "steps": max(args.e2e_steps, 1),
+            "api": "slapcu_batched_spgemm_host (host A, B; per-batch host consumer)",
+            "batch_budget_bytes": e2e_budget}
 
 
 def dist_shape(world: int):

@@ -154,10 +154,16 @@ typedef enum {
                                               chunks of at most this many outputs (4096..16384; default
                                               8192 for 4-byte, 4096 for 8-byte accumulators);
                                               0 = row sub-tiles of 2^VTL rows */
-    SLAPCU_OPT_DIRECT_VALUE_INTERLEAVE = 22 /* direct path value pass: A's rows and values gathered as
+    SLAPCU_OPT_DIRECT_VALUE_INTERLEAVE = 22, /* direct path value pass: A's rows and values gathered as
                                               one interleaved pair per product -- 1 (default) for 4-byte
                                               values (8-byte pairs), 2 also for 8-byte values (16-byte
                                               pairs); 0 = from the two arrays */
+    SLAPCU_OPT_DIRECT_TILE_MAJOR = 23,     /* direct path form: 1 = work units ordered by row tile, heaviest
+                                              first inside a tile (the tile's A slice stays in L2);
+                                              0 = heaviest first over all tiles */
+    SLAPCU_OPT_DIRECT_FORM_WALK = 24       /* direct path form: 1 = warp-independent walk (warps take 32
+                                              B entries at a time, no block barriers inside the walk);
+                                              0 = block-synchronous batches of entries */
 } slapcu_option;
 slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t value);
 
@@ -246,6 +252,25 @@ slapcu_status slapcu_spgemm(slapcu_ctx ctx, const slapcu_csc* A, const slapcu_cs
  * call the reference-side C++ template shim binds. */
 slapcu_status slapcu_spgemm_host(slapcu_ctx ctx, const slapcu_host_csc* A, const slapcu_host_csc* B,
                                  slapcu_semiring sr, slapcu_alg alg, slapcu_host_csc* C);
+
+/* batched.hpp:153-170 batched_spgemm (with batched.hpp:122-148 planning) for
+ * HOST operands: A and B are copied to the device once, then for every column
+ * range r of B, in order, C_r = A * B(:, range_r) is formed on the device and
+ * read back into pinned host memory, and consumer(user, r, col_begin, col_end,
+ * C_r) is called on the calling thread (batch r+1's product overlaps batch r's
+ * read-back).  C_r is a host CSC with colptr rebased to 0; its buffers belong
+ * to the library and are valid only during the call.  `col_ranges` holds
+ * nranges [begin, end) pairs partitioning B's columns (ShapeError otherwise,
+ * batched.hpp:157-163), or NULL: the library plans the fewest ranges whose
+ * output bound sum_j min(flops_j, nrows) * (4 + value bytes) fits
+ * `budget_bytes` (BudgetError if one column alone exceeds it).  A non-zero
+ * consumer return aborts with SLAPCU_ERR_INVALID.  *total_nnz = nnz(C). */
+typedef int (*slapcu_batch_consumer)(void* user, int batch, int64_t col_begin, int64_t col_end,
+                                     const slapcu_host_csc* C_r);
+slapcu_status slapcu_batched_spgemm_host(slapcu_ctx ctx, const slapcu_host_csc* A, const slapcu_host_csc* B,
+                                         slapcu_semiring sr, slapcu_alg alg, int nranges, const int64_t* col_ranges,
+                                         int64_t budget_bytes, slapcu_batch_consumer consumer, void* user,
+                                         int64_t* total_nnz);
 
 slapcu_status slapcu_csc_free(slapcu_ctx ctx, slapcu_csc_out* C);
 void slapcu_host_free(slapcu_host_csc* C);

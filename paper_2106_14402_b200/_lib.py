@@ -36,7 +36,8 @@ ALG_HEAP, ALG_HASH, ALG_HYBRID = 0, 1, 2
  OPT_DIRECT_SPLIT_FLOPS, OPT_DIRECT_MARK_MODE, OPT_DIRECT_FORM_THREADS, OPT_DIRECT_EMIT_THREADS,
  OPT_DIRECT_DENSE_RUN_MIN, OPT_DIRECT_PERSISTENT, OPT_DIRECT_QUADS,
  OPT_DIRECT_VALUE_TILE_ROWS_LOG2, OPT_DIRECT_VALUE_THREADS, OPT_SUMMA_CONCAT,
- OPT_DIRECT_VALUE_HASH, OPT_DIRECT_VALUE_RANK, OPT_DIRECT_VALUE_INTERLEAVE) = range(23)
+ OPT_DIRECT_VALUE_HASH, OPT_DIRECT_VALUE_RANK, OPT_DIRECT_VALUE_INTERLEAVE, OPT_DIRECT_TILE_MAJOR,
+ OPT_DIRECT_FORM_WALK) = range(25)
 NUM_KERNEL_CLASSES = 10
 KERNEL_CLASSES = ["other", "flops", "bin", "sym_light", "sym_heavy", "scan", "num_light", "num_heavy", "merge", "gen"]
 
@@ -94,6 +95,9 @@ class Tiling(C.Structure):
     ]
 
 
+# typedef int (*slapcu_batch_consumer)(void*, int, int64_t, int64_t, const slapcu_host_csc*)
+BatchConsumer = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.POINTER(CscOut))
+
 # (name, restype, argtypes) for every entry point of include/slapcu.h
 _P = C.c_void_p
 _I = C.c_int
@@ -126,6 +130,7 @@ SIGNATURES = [
     ("slapcu_spgemm_direct", _I, [_P, _PV, _PV, _I, _I, _L, _P, _P, _P, C.POINTER(_L)]),
     ("slapcu_spgemm", _I, [_P, _PV, _PV, _I, _I, _PO]),
     ("slapcu_spgemm_host", _I, [_P, _PO, _PO, _I, _I, _PO]),
+    ("slapcu_batched_spgemm_host", _I, [_P, _PO, _PO, _I, _I, _I, _P, _L, BatchConsumer, _P, C.POINTER(_L)]),
     ("slapcu_csc_free", _I, [_P, _PO]),
     ("slapcu_mcl_step", _I, [_P, _PV, _I, C.c_double, C.c_double, _PO]),
     ("slapcu_host_free", None, [_PO]),

@@ -16,7 +16,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import errors as E
-from .spgemm import DeviceCsc, Semiring, SpGemmAlg, local_spgemm, symbolic_nnz
+from .spgemm import CscMatrix, DeviceCsc, Semiring, SpGemmAlg, _ctx, _host_view, _sr, local_spgemm, symbolic_nnz
 
 K_BATCH_ENTRY_BYTES = 16  # batched.hpp:23 kBatchEntryBytes (value + index)
 
@@ -104,3 +104,56 @@ def batched_spgemm(a: DeviceCsc, b: DeviceCsc, plan: BatchPlan, sr: Semiring, al
         else:
             out.append(cr)
     return None if consumer is not None else out
+
+
+def batched_spgemm_host(a: CscMatrix, b: CscMatrix, sr: Semiring, alg=SpGemmAlg.hybrid, plan: BatchPlan | None = None,
+                        budget_bytes: int = 0, consumer=None, ctx=None) -> int:
+    """batched.hpp:153-170 for HOST operands through one library call
+    (slapcu_batched_spgemm_host): A and B go to the device once, every batch
+    product is read back into pinned host memory (batch r+1's product overlaps
+    batch r's read-back) and consumer(r, s, e, C_r) runs with C_r a host
+    CscMatrix whose arrays are views of library-owned pinned buffers, valid
+    during the call only (copy what you keep).  Without a plan the library
+    plans by `budget_bytes` on the output bound.  Returns nnz(C)."""
+    import ctypes as C
+
+    from . import _lib as L
+
+    sr = _sr(sr)
+    ctx = _ctx(ctx)
+    keep = []
+    A = _host_view(a, sr.np_dtype, keep)
+    B = _host_view(b, sr.np_dtype, keep)
+    rng = None
+    nr = 0
+    if plan is not None:
+        rng = np.asarray(plan.col_ranges, dtype=np.int64).reshape(-1)
+        nr = plan.batches()
+    err = []
+    vs = np.dtype(sr.np_dtype).itemsize
+
+    def _cb(_user, r, s, e, cp):
+        try:
+            if consumer is not None:
+                m = cp.contents
+                n, nz = int(m.ncols), int(m.nnz)
+                colptr = np.ctypeslib.as_array(C.cast(m.colptr, C.POINTER(C.c_int64)), shape=(n + 1,))
+                rows = (np.ctypeslib.as_array(C.cast(m.rowids, C.POINTER(C.c_int32)), shape=(nz,)) if nz
+                        else np.zeros(0, np.int32))
+                vals = (np.frombuffer((C.c_char * (nz * vs)).from_address(m.vals), dtype=sr.np_dtype) if nz
+                        else np.zeros(0, sr.np_dtype))
+                consumer(int(r), int(s), int(e), CscMatrix(int(m.nrows), n, colptr, rows, vals))
+            return 0
+        except Exception as ex:  # surfaced after the call returns
+            err.append(ex)
+            return 1
+
+    cb = L.BatchConsumer(_cb)
+    tot = C.c_int64()
+    st = ctx.lib.slapcu_batched_spgemm_host(ctx.h, C.byref(A), C.byref(B), sr.id, int(SpGemmAlg(int(alg))), nr,
+                                            rng.ctypes.data if rng is not None else None, int(budget_bytes), cb, None,
+                                            C.byref(tot))
+    if err:
+        raise err[0]
+    ctx.check(st, "batched_spgemm_host")
+    return int(tot.value)

@@ -115,6 +115,7 @@ slapcu_status slapcu_ctx_destroy(slapcu_ctx ctx) {
     for (auto& e : ctx->c.ev)
         if (e) cudaEventDestroy(e);
     if (ctx->c.err_host) cudaFreeHost(ctx->c.err_host);
+    free_host_cache(ctx->c);
     delete ctx;
     return SLAPCU_OK;
 }
@@ -159,6 +160,11 @@ slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t v
             c.opt.direct_mark_mode = (int)v;
             break;
         case SLAPCU_OPT_DIRECT_PERSISTENT: c.opt.direct_persistent = v != 0; break;
+        case SLAPCU_OPT_DIRECT_TILE_MAJOR: c.opt.direct_tile_major = v != 0; break;
+        case SLAPCU_OPT_DIRECT_FORM_WALK:
+            require(v == 0 || v == 1, SLAPCU_ERR_INVALID, "form walk: 0 (block batches) or 1 (warp-independent)");
+            c.opt.direct_form_walk = (int)v;
+            break;
         case SLAPCU_OPT_DIRECT_QUADS: c.opt.direct_quads = v != 0; break;
         case SLAPCU_OPT_DIRECT_VALUE_TILE_ROWS_LOG2:
             require(v >= 10 && v <= 15, SLAPCU_ERR_INVALID, "value tile rows log2 must be in 10..15");
@@ -388,6 +394,19 @@ slapcu_status slapcu_spgemm(slapcu_ctx ctx, const slapcu_csc* A, const slapcu_cs
         else
             spgemm_numeric(c, a, b, sr, alg, cp, C->rowids, C->vals);
     });
+}
+
+slapcu_status slapcu_batched_spgemm_host(slapcu_ctx ctx, const slapcu_host_csc* A, const slapcu_host_csc* B,
+                                         slapcu_semiring sr, slapcu_alg alg, int nranges, const int64_t* col_ranges,
+                                         int64_t budget_bytes, slapcu_batch_consumer consumer, void* user,
+                                         int64_t* total_nnz) {
+    int64_t tot = -1;
+    const slapcu_status st = guarded(ctx, [&](Ctx& c) {
+        require(A && B, SLAPCU_ERR_INVALID, "null argument");
+        tot = batched_host(c, *A, *B, sr, alg, nranges, col_ranges, budget_bytes, consumer, user);
+    });
+    if (total_nnz) *total_nnz = tot;
+    return st;
 }
 
 slapcu_status slapcu_spgemm_host(slapcu_ctx ctx, const slapcu_host_csc* A, const slapcu_host_csc* B,

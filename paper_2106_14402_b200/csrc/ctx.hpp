@@ -136,6 +136,8 @@ struct Options {
     int direct_value_rank = -1;  // value pass: large items by rank chunks of this many outputs (0 = sub-tiles,
                                  // -1 = by accumulator width: 8192 for 4-byte, 4096 for 8-byte)
     int direct_emit_blocks = 0;             // emit: one warp per (item, block) (1) or one CTA per item (0)
+    int direct_tile_major = 0;              // form: work units ordered by row tile, then heaviest first
+    int direct_form_walk = 0;               // form: 0 block-synchronous batches, 1 warp-independent walk
     int direct_persistent = 1;              // form kernel: persistent CTAs (1) or one CTA per unit (0)
     int direct_form_threads = 256;          // CTA size of the form kernel (128, 256, 512)
     int direct_emit_threads = 128;          // CTA size of the emit kernel (128, 256)
@@ -206,6 +208,11 @@ struct Ctx {
     bool err_pending = false;
     DevBuf err_flag;      // int
     DevBuf scratch_small; // misc small counters
+    // host batched path: pinned read-back buffers, grown on demand and kept
+    struct {
+        void* pinned[2] = {nullptr, nullptr};
+        size_t bytes[2] = {0, 0};
+    } host;
     // merge state carried from merge_symbolic to merge_numeric
     struct {
         DevBuf ranks, tot, counts;
@@ -240,6 +247,10 @@ void fused_copy_light(Ctx& c, int sr, bool ones, const int* list, int n, const F
 // sized library-owned buffers (false when the bound-sized scratch exceeds budget)
 bool direct_exact(Ctx& c, const DevCsc& A, const DevCsc& B, int sr, int alg, int64_t budget, int64_t** colptr,
                   int32_t** rowids, void** vals, int64_t* nnz, bool copy_out = true);
+// host.cu: batched product of host operands, per-batch host consumer
+int64_t batched_host(Ctx& c, const slapcu_host_csc& A, const slapcu_host_csc& B, int sr, int alg, int nranges,
+                     const int64_t* ranges, int64_t budget, slapcu_batch_consumer consumer, void* user);
+void free_host_cache(Ctx& c);
 int64_t direct_spgemm(Ctx& c, const DevCsc& A, const DevCsc& B, int sr, int alg, int64_t capacity, int64_t* c_colptr,
                       int32_t* c_rowids, void* c_vals);
 void any_zero_u8(Ctx& c, const uint8_t* v, int64_t n, int* flag);

@@ -461,6 +461,139 @@ __global__ void __launch_bounds__(NT) k_tile_form(FormArgs g) {
     }
 }
 
+// Warp-independent walk of B entries [b0, b1) (column j) into the tile
+// bitmap: the warps of the CTA take 32 entries at a time from a shared
+// cursor, so no block barrier sits inside the walk (the batch-synchronous
+// tile_walk above pays ~7 barriers per 256 entries and waits on its longest
+// run).  Per chunk: every lane gathers its entry's tile run; short runs are
+// walked by their own lane (4 loads in flight); long runs are walked by the
+// whole warp lane-strided, one after the other (ballot order); dense runs
+// OR their cached tile bitmap with 16-byte loads.
+template <int U>
+__device__ __forceinline__ void warp_walk(const DevCsc& A, const DevCsc& B, const int32_t* __restrict__ Atp, int T,
+                                          int64_t b0, int64_t b1, int t, int t0, unsigned* bm, int* cursor,
+                                          const DenseRuns& dr, int W) {
+    const int lane = threadIdx.x & 31;
+    const int32_t* __restrict__ Arw = A.rw;
+    const unsigned bm0 = smem_addr(bm);
+    const unsigned bmA = bm0 - (unsigned(t0 >> 5) << 2);
+    for (;;) {
+        int c = 0;
+        if (lane == 0) c = atomicAdd(cursor, 32);
+        c = __shfl_sync(0xffffffffu, c, 0);
+        const int64_t i = b0 + c + lane;
+        if (b0 + c >= b1) break;
+        int len = 0;
+        int64_t st = 0;
+        int dslot = -1;
+        if (i < b1) {
+            const int k = B.rw[i];
+            const int32_t* tp = Atp + int64_t(k) * (T + 1) + t;
+            const int lo = tp[0], hi = tp[1];
+            st = A.cp[k] + lo;
+            len = hi - lo;
+            if (dr.dmin && len >= dr.dmin) {
+                dslot = dr.slot[int64_t(k) * T + t];
+                len = 0;
+            }
+        }
+        // short runs: each lane its own
+        if (len < kShortRun) {
+            const int32_t* q = Arw + st;
+            int x = 0;
+            for (; x + 4 <= len; x += 4) {
+                const int r0 = __ldg(q + x), r1 = __ldg(q + x + 1), r2 = __ldg(q + x + 2), r3 = __ldg(q + x + 3);
+                mark<0>(bmA, 0, r0);
+                mark<0>(bmA, 0, r1);
+                mark<0>(bmA, 0, r2);
+                mark<0>(bmA, 0, r3);
+            }
+            for (; x < len; ++x) mark<0>(bmA, 0, __ldg(q + x));
+        }
+        // long runs: the warp walks each, lane-strided, U loads in flight
+        unsigned lm = __ballot_sync(0xffffffffu, len >= kShortRun);
+        while (lm) {
+            const int src = __ffs(lm) - 1;
+            lm &= lm - 1u;
+            const int m = __shfl_sync(0xffffffffu, len, src);
+            const int32_t* run = Arw + __shfl_sync(0xffffffffu, st, src);
+            int x = lane;
+            for (; x + 32 * (U - 1) < m; x += 32 * U) {
+                int r[U];
+#pragma unroll
+                for (int v = 0; v < U; ++v) r[v] = __ldg(run + x + 32 * v);
+#pragma unroll
+                for (int v = 0; v < U; ++v) mark<0>(bmA, 0, r[v]);
+            }
+            for (; x < m; x += 32) mark<0>(bmA, 0, __ldg(run + x));
+        }
+        // dense runs: OR the cached tile bitmap, the warp together
+        unsigned dm = __ballot_sync(0xffffffffu, dslot >= 0);
+        while (dm) {
+            const int src = __ffs(dm) - 1;
+            dm &= dm - 1u;
+            const int ds = __shfl_sync(0xffffffffu, dslot, src);
+            const uint4* srcb = reinterpret_cast<const uint4*>(dr.bm + int64_t(ds) * W);
+            for (int q = lane; q < (W >> 2); q += 32) {
+                const uint4 v = __ldg(srcb + q);
+                const unsigned a = bm0 + (unsigned(q) << 4);
+                if (v.x) set_bits<0>(a, v.x, 0, 0);
+                if (v.y) set_bits<0>(a + 4, v.y, 0, 0);
+                if (v.z) set_bits<0>(a + 8, v.z, 0, 0);
+                if (v.w) set_bits<0>(a + 12, v.w, 0, 0);
+            }
+        }
+    }
+}
+
+// k_tile_form with the warp-independent walk (SLAPCU_OPT_DIRECT_FORM_WALK 1).
+template <int NT>
+__global__ void __launch_bounds__(NT) k_tile_form_w(FormArgs g) {
+    extern __shared__ __align__(16) unsigned char sm_raw[];
+    const int W = 1 << (g.TL - 5);
+    unsigned* bm = reinterpret_cast<unsigned*>(sm_raw);
+    unsigned* summ = bm + W;                                    // [W/32]
+    uint16_t* tl = reinterpret_cast<uint16_t*>(summ + W / 32);  // [W]
+    __shared__ int wsum[NT / 32 + 1];
+    __shared__ int red[NT / 32];
+    __shared__ int ticket_sh, cursor;
+    __shared__ int bcs[kMaxBlocks];
+    smem_zero(bm, W + W / 32);
+    for (int b = threadIdx.x; b < kMaxBlocks; b += NT) bcs[b] = 0;
+    for (;;) {
+        if (threadIdx.x == 0) {
+            ticket_sh = atomicAdd(g.ticket, 1);
+            cursor = 0;
+        }
+        __syncthreads();
+        const int ui = ticket_sh;
+        if (ui >= g.nunits) break;
+        const int4 u = g.units[g.order[ui]];
+        const int2 it = g.items[u.x];
+        const int64_t bs = g.B.cp[it.x];
+        warp_walk<4>(g.A, g.B, g.Atp, g.T, bs + u.y, bs + u.z, it.y, it.y << g.TL, bm, &cursor, g.dr, W);
+        __syncthreads();
+        if (u.w >= 0) {  // one part of a split item: partial bitmap out, then clear
+            uint4* d4 = reinterpret_cast<uint4*>(g.partial + int64_t(u.w) * W);
+            uint4* s4 = reinterpret_cast<uint4*>(bm);
+            for (int q = threadIdx.x; q < W / 4; q += NT) {
+                d4[q] = s4[q];
+                s4[q] = make_uint4(0u, 0u, 0u, 0u);
+            }
+        } else {
+            const int lane = threadIdx.x & 31;
+            for (int cc = threadIdx.x >> 5; cc < W / 32; cc += NT / 32) {
+                const unsigned nz = __ballot_sync(0xffffffffu, bm[cc * 32 + lane] != 0u);
+                if (lane == 0) summ[cc] = nz;
+            }
+            __syncthreads();
+            stash_bitmap<NT>(bm, summ, tl, W, wsum, red, bcs, u.x, it.x, g.stash + g.soff[u.x], g.sres[u.x], g.cnt,
+                             g.form, g.hcnt, g.rbc);
+        }
+        __syncthreads();
+    }
+}
+
 // OR of the partial bitmaps of each split item -> its stash (bitmap or list).
 template <int NT>
 __global__ void __launch_bounds__(NT)
@@ -1393,15 +1526,24 @@ __global__ void k_item_fill(const int* __restrict__ hl, int nh, int T, int W, co
 }
 
 // Work units of unsplit items: the whole column range, in item order.
+// Sort key of a work unit: its multiplies (heaviest first, LPT), and with
+// tile_major the row tile above them, so that the units of one row tile run
+// together and its A slice stays L2-resident (T - 1 - t: ascending tiles
+// under the descending sort).
+__device__ __forceinline__ int64_t unit_key(int64_t f, int t, int T, int tile_major) {
+    const int64_t ff = f < (int64_t(1) << 40) ? f : (int64_t(1) << 40) - 1;
+    return tile_major ? (int64_t(T - 1 - t) << 40) | ff : ff;
+}
+
 __global__ void k_unit_fill_whole(const DevCsc B, int nitems, const int2* __restrict__ items,
                                   const int64_t* __restrict__ ifl, const int64_t* __restrict__ np,
                                   const int64_t* __restrict__ uoff, int4* __restrict__ units,
-                                  int64_t* __restrict__ ukey) {
+                                  int64_t* __restrict__ ukey, int T, int tile_major) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nitems; i += gridDim.x * blockDim.x) {
         if (np[i] != 1) continue;
         const int j = items[i].x;
         units[uoff[i]] = make_int4(i, 0, (int)(B.cp[j + 1] - B.cp[j]), -1);
-        ukey[uoff[i]] = ifl[i];
+        ukey[uoff[i]] = unit_key(ifl[i], items[i].y, T, tile_major);
     }
 }
 
@@ -1412,7 +1554,7 @@ __global__ void __launch_bounds__(NT)
     k_unit_fill_split(DevCsc B, const int32_t* __restrict__ Atp, int T, const int* __restrict__ sitems,
                       const int2* __restrict__ items, const int64_t* __restrict__ ifl, const int64_t* __restrict__ np,
                       const int64_t* __restrict__ uoff, const int64_t* __restrict__ poff, int4* __restrict__ units,
-                      int64_t* __restrict__ ukey) {
+                      int64_t* __restrict__ ukey, int tile_major) {
     __shared__ int wsum[NT / 32 + 1];
     __shared__ long long run_sh;
     __shared__ int bnd[65];
@@ -1452,7 +1594,7 @@ __global__ void __launch_bounds__(NT)
     if (threadIdx.x < p) {
         const int lo = bnd[threadIdx.x], hi = max(lo, bnd[threadIdx.x + 1]);
         units[u0 + threadIdx.x] = make_int4(item, lo, hi, (int)(poff[item] + threadIdx.x));
-        ukey[u0 + threadIdx.x] = f / p;
+        ukey[u0 + threadIdx.x] = unit_key(f / p, it.y, T, tile_major);
     }
 }
 
@@ -1748,12 +1890,12 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
         }
         launch(c, k_unit_fill_whole, dim3(grid_for(c, nitems, 256)), dim3(256), 0, B, nitems,
                (const int2*)d.items.as<int2>(), (const int64_t*)d.ifl.as<int64_t>(), (const int64_t*)np.as<int64_t>(),
-               (const int64_t*)uoff.as<int64_t>(), d.units.as<int4>(), ukey.as<int64_t>());
+               (const int64_t*)uoff.as<int64_t>(), d.units.as<int4>(), ukey.as<int64_t>(), T, c.opt.direct_tile_major);
         if (nsplit > 0)
             launch(c, k_unit_fill_split<256>, dim3(nsplit), dim3(256), 0, B, Atp, T, (const int*)si,
                    (const int2*)d.items.as<int2>(), (const int64_t*)d.ifl.as<int64_t>(),
                    (const int64_t*)np.as<int64_t>(), (const int64_t*)uoff.as<int64_t>(),
-                   (const int64_t*)poff.as<int64_t>(), d.units.as<int4>(), ukey.as<int64_t>());
+                   (const int64_t*)poff.as<int64_t>(), d.units.as<int4>(), ukey.as<int64_t>(), c.opt.direct_tile_major);
         // heaviest units first (LPT)
         d.order.reset(sizeof(int) * std::max<int64_t>(nunits, 1), c.stream);
         {
@@ -1763,12 +1905,12 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
             size_t tb = 0;
             SLAPCU_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, ukey.as<int64_t>(), kout.as<int64_t>(),
                                                                   idx.as<int>(), d.order.as<int>(), (int)nunits, 0,
-                                                                  40, c.stream));
+                                                                  62, c.stream));
             DevBuf tmp(tb, c.stream);
             timed(c, KC_BIN, [&] {
                 SLAPCU_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp.get(), tb, ukey.as<int64_t>(),
                                                                       kout.as<int64_t>(), idx.as<int>(),
-                                                                      d.order.as<int>(), (int)nunits, 0, 40,
+                                                                      d.order.as<int>(), (int)nunits, 0, 62,
                                                                       c.stream));
             });
             ++c.launches;
@@ -1807,7 +1949,9 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
             launch(c, kf, dim3((unsigned)grid), dim3(nt), smem, g);
         };
         const int ft = c.opt.direct_form_threads;
-        if (c.opt.direct_mark_mode == 2)
+        if (c.opt.direct_form_walk == 1)
+            ft == 512 ? form(k_tile_form_w<512>, 512) : form(k_tile_form_w<256>, 256);
+        else if (c.opt.direct_mark_mode == 2)
             form(k_tile_form<256, 2>, 256);
         else if (ft == 128)
             form(k_tile_form<128, 0>, 128);
