@@ -73,7 +73,8 @@ def parse():
                     help="direct path value pass: 4-byte values gathered with their rows (1) or not (0)")
     ap.add_argument("--quads", type=int, default=None, help="direct path: lane-contiguous quads (1) or strided (0)")
     ap.add_argument("--tile-major", type=int, default=None, help="direct path form: units ordered by row tile (1)")
-    ap.add_argument("--form-walk", type=int, default=None, help="direct path form: 1 warp-independent walk")
+    ap.add_argument("--form-walk", type=int, default=None, help="direct path form: 1 packed long-run products")
+    ap.add_argument("--short-run", type=int, default=None, help="direct path form: per-thread run threshold")
     ap.add_argument("--dist", default="1d", choices=["1d", "summa"],
                     help="N>1: 1d = flops-balanced column blocks with A replicated (no data-path collective); "
                          "summa = the 2D SUMMA / 3D drivers (NCCL stage broadcasts, fiber exchange, merge)")
@@ -114,6 +115,8 @@ def apply_options(ctx, args):
         ctx.set_option(L.OPT_DIRECT_TILE_MAJOR, args.tile_major)
     if args.form_walk is not None:
         ctx.set_option(L.OPT_DIRECT_FORM_WALK, args.form_walk)
+    if args.short_run is not None:
+        ctx.set_option(L.OPT_DIRECT_SHORT_RUN, args.short_run)
     if args.value_rank is not None:
         ctx.set_option(L.OPT_DIRECT_VALUE_RANK, args.value_rank)
     if args.value_interleave is not None:

@@ -161,9 +161,12 @@ typedef enum {
     SLAPCU_OPT_DIRECT_TILE_MAJOR = 23,     /* direct path form: 1 = work units ordered by row tile, heaviest
                                               first inside a tile (the tile's A slice stays in L2);
                                               0 = heaviest first over all tiles */
-    SLAPCU_OPT_DIRECT_FORM_WALK = 24       /* direct path form: 1 = warp-independent walk (warps take 32
-                                              B entries at a time, no block barriers inside the walk);
-                                              0 = block-synchronous batches of entries */
+    SLAPCU_OPT_DIRECT_FORM_WALK = 24,      /* direct path form: long runs of a batch of B entries walked as
+                                              0 = 256-product units, one run per warp step; 1 = packed
+                                              products (the warps split the concatenated products evenly,
+                                              several short runs per warp step) */
+    SLAPCU_OPT_DIRECT_SHORT_RUN = 25       /* direct path form: runs (A column x row tile) shorter than this
+                                              are walked by their own thread (0 = default 8) */
 } slapcu_option;
 slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t value);
 
@@ -273,6 +276,30 @@ slapcu_status slapcu_batched_spgemm_host(slapcu_ctx ctx, const slapcu_host_csc* 
                                          int64_t* total_nnz);
 
 slapcu_status slapcu_csc_free(slapcu_ctx ctx, slapcu_csc_out* C);
+
+/* spgemm.hpp:68-88 estimate_flops and spgemm.hpp:118-138 symbolic_nnz for
+ * HOST operands (pattern only; values are not read): per-column results into
+ * host arrays of B.ncols.  DimError on an inner-dimension mismatch. */
+slapcu_status slapcu_estimate_flops_host(slapcu_ctx ctx, const slapcu_host_csc* A, const slapcu_host_csc* B,
+                                         int64_t* flops_per_col, int64_t* total);
+slapcu_status slapcu_symbolic_nnz_host(slapcu_ctx ctx, const slapcu_host_csc* A, const slapcu_host_csc* B,
+                                       slapcu_alg alg, int64_t* counts);
+
+/* Number of CUDA devices visible to this process (0 when none). */
+slapcu_status slapcu_device_count(int* n);
+/* Host CSC -> library-allocated device CSC (free with slapcu_csc_free). */
+slapcu_status slapcu_csc_upload(slapcu_ctx ctx, const slapcu_host_csc* h, slapcu_semiring sr, slapcu_csc_out* d);
+/* Host DCSC (local_matrix.hpp:88-150: jc[nzc] nonempty column ids, cp[nzc+1]
+ * offsets, int32 like the reference's LocalIdx) -> device CSC: the arrays are
+ * copied as they are and the dense int64 colptr is built on the device
+ * (slapcu_dcsc_colptr), so a SUMMA block goes to the GPU without a host
+ * conversion.  Free with slapcu_csc_free. */
+slapcu_status slapcu_dcsc_upload(slapcu_ctx ctx, int64_t nrows, int64_t ncols, int64_t nzc, const int32_t* jc,
+                                 const int32_t* cp, const int32_t* rowids, const void* vals, slapcu_semiring sr,
+                                 slapcu_csc_out* d);
+/* Device CSC (any colptr base) -> malloc'd host CSC with colptr rebased to 0
+ * (free with slapcu_host_free). */
+slapcu_status slapcu_csc_download(slapcu_ctx ctx, const slapcu_csc* d, slapcu_semiring sr, slapcu_host_csc* h);
 void slapcu_host_free(slapcu_host_csc* C);
 
 /* algorithms.cpp:267-293 mcl_step on one device: expansion
@@ -373,6 +400,13 @@ typedef struct {
 slapcu_status slapcu_summa2d(slapcu_comm comm, const slapcu_csc* A_local, const slapcu_csc* B_local,
                              slapcu_semiring sr, slapcu_alg alg, slapcu_csc_out* C_local,
                              slapcu_dist_stats* stats);
+
+/* batched.hpp:70-117 dist_symbolic_col_nnz on the q x q grid of `comm`:
+ * exact per-output-column counts of A*B (pattern SUMMA, column-communicator
+ * allreduce, row-communicator all-gather).  Every rank receives all `ncols`
+ * counts of B's columns in `counts` (HOST int64[ncols]).  Collective. */
+slapcu_status slapcu_dist_symbolic_col_nnz(slapcu_comm comm, const slapcu_csc* A_local, const slapcu_csc* B_local,
+                                           int64_t* counts, int64_t ncols);
 
 /* spgemm3d.hpp:21-106 ca3d_spgemm on a c x q x q grid (regular variant,
  * grid.cpp:57 rank = l*q*q + i*q + j): A split by columns, B by rows; per

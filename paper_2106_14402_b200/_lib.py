@@ -37,7 +37,7 @@ ALG_HEAP, ALG_HASH, ALG_HYBRID = 0, 1, 2
  OPT_DIRECT_DENSE_RUN_MIN, OPT_DIRECT_PERSISTENT, OPT_DIRECT_QUADS,
  OPT_DIRECT_VALUE_TILE_ROWS_LOG2, OPT_DIRECT_VALUE_THREADS, OPT_SUMMA_CONCAT,
  OPT_DIRECT_VALUE_HASH, OPT_DIRECT_VALUE_RANK, OPT_DIRECT_VALUE_INTERLEAVE, OPT_DIRECT_TILE_MAJOR,
- OPT_DIRECT_FORM_WALK) = range(25)
+ OPT_DIRECT_FORM_WALK, OPT_DIRECT_SHORT_RUN) = range(26)
 NUM_KERNEL_CLASSES = 10
 KERNEL_CLASSES = ["other", "flops", "bin", "sym_light", "sym_heavy", "scan", "num_light", "num_heavy", "merge", "gen"]
 
@@ -132,6 +132,12 @@ SIGNATURES = [
     ("slapcu_spgemm_host", _I, [_P, _PO, _PO, _I, _I, _PO]),
     ("slapcu_batched_spgemm_host", _I, [_P, _PO, _PO, _I, _I, _I, _P, _L, BatchConsumer, _P, C.POINTER(_L)]),
     ("slapcu_csc_free", _I, [_P, _PO]),
+    ("slapcu_device_count", _I, [C.POINTER(_I)]),
+    ("slapcu_estimate_flops_host", _I, [_P, _PO, _PO, _P, C.POINTER(_L)]),
+    ("slapcu_symbolic_nnz_host", _I, [_P, _PO, _PO, _I, _P]),
+    ("slapcu_csc_upload", _I, [_P, _PO, _I, _PO]),
+    ("slapcu_dcsc_upload", _I, [_P, _L, _L, _L, _P, _P, _P, _P, _I, _PO]),
+    ("slapcu_csc_download", _I, [_P, _PV, _I, _PO]),
     ("slapcu_mcl_step", _I, [_P, _PV, _I, C.c_double, C.c_double, _PO]),
     ("slapcu_host_free", None, [_PO]),
     ("slapcu_dcsc_colptr", _I, [_P, _L, _L, _P, _P, _P]),
@@ -150,6 +156,7 @@ SIGNATURES = [
     ("slapcu_comm_counters", _I, [_P, _I, C.POINTER(_L), C.POINTER(_L)]),
     ("slapcu_summa2d", _I, [_P, _PV, _PV, _I, _I, _PO, C.POINTER(DistStats)]),
     ("slapcu_ca3d", _I, [_P, _I, _PV, _PV, _I, _I, _PO, C.POINTER(DistStats)]),
+    ("slapcu_dist_symbolic_col_nnz", _I, [_P, _PV, _PV, _P, _L]),
     ("slapcu_redistribute", _I, [_P, _PV, _L, _L, _L, _L, _I, C.POINTER(Tiling), _I, _PO, C.POINTER(_L),
                                  C.POINTER(_L)]),
     ("slapcu_cb2b_header", _I, [C.c_char_p, C.POINTER(_L), C.POINTER(_L), C.POINTER(_L)]),

@@ -162,8 +162,12 @@ slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t v
         case SLAPCU_OPT_DIRECT_PERSISTENT: c.opt.direct_persistent = v != 0; break;
         case SLAPCU_OPT_DIRECT_TILE_MAJOR: c.opt.direct_tile_major = v != 0; break;
         case SLAPCU_OPT_DIRECT_FORM_WALK:
-            require(v == 0 || v == 1, SLAPCU_ERR_INVALID, "form walk: 0 (block batches) or 1 (warp-independent)");
+            require(v == 0 || v == 1, SLAPCU_ERR_INVALID, "form walk: 0 (256-product units) or 1 (packed products)");
             c.opt.direct_form_walk = (int)v;
+            break;
+        case SLAPCU_OPT_DIRECT_SHORT_RUN:
+            require(v >= 0 && v <= 256, SLAPCU_ERR_INVALID, "short run threshold: 0 (default) .. 256");
+            c.opt.direct_short_run = (int)v;
             break;
         case SLAPCU_OPT_DIRECT_QUADS: c.opt.direct_quads = v != 0; break;
         case SLAPCU_OPT_DIRECT_VALUE_TILE_ROWS_LOG2:
@@ -393,6 +397,142 @@ slapcu_status slapcu_spgemm(slapcu_ctx ctx, const slapcu_csc* A, const slapcu_cs
             fused_finish(c, a, b, sr, C->rowids, C->vals);
         else
             spgemm_numeric(c, a, b, sr, alg, cp, C->rowids, C->vals);
+    });
+}
+
+slapcu_status slapcu_device_count(int* n) {
+    if (!n) return SLAPCU_ERR_INVALID;
+    *n = 0;
+    if (cudaGetDeviceCount(n) != cudaSuccess) {
+        cudaGetLastError();
+        *n = 0;
+    }
+    return SLAPCU_OK;
+}
+
+slapcu_status slapcu_csc_upload(slapcu_ctx ctx, const slapcu_host_csc* h, slapcu_semiring sr, slapcu_csc_out* d) {
+    return guarded(ctx, [&](Ctx& c) {
+        require(h && d, SLAPCU_ERR_INVALID, "null argument");
+        const int vs = value_size(sr);
+        require(vs > 0, SLAPCU_ERR_INVALID, "unknown semiring");
+        alloc_csc_out(c, d, h->nrows, h->ncols, h->nnz, vs);
+        SLAPCU_CUDA(cudaMemcpyAsync(d->colptr, h->colptr, sizeof(int64_t) * (h->ncols + 1), cudaMemcpyHostToDevice,
+                                    c.stream));
+        if (h->nnz) {
+            SLAPCU_CUDA(cudaMemcpyAsync(d->rowids, h->rowids, sizeof(int32_t) * h->nnz, cudaMemcpyHostToDevice, c.stream));
+            if (h->vals)
+                SLAPCU_CUDA(cudaMemcpyAsync(d->vals, h->vals, size_t(vs) * h->nnz, cudaMemcpyHostToDevice, c.stream));
+        }
+        SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+    });
+}
+
+slapcu_status slapcu_dcsc_upload(slapcu_ctx ctx, int64_t nrows, int64_t ncols, int64_t nzc, const int32_t* jc,
+                                 const int32_t* cp, const int32_t* rowids, const void* vals, slapcu_semiring sr,
+                                 slapcu_csc_out* d) {
+    return guarded(ctx, [&](Ctx& c) {
+        require(d && (nzc == 0 || (jc && cp)), SLAPCU_ERR_INVALID, "null argument");
+        const int vs = value_size(sr);
+        require(vs > 0, SLAPCU_ERR_INVALID, "unknown semiring");
+        const int64_t nnz = nzc ? cp[nzc] : 0;
+        alloc_csc_out(c, d, nrows, ncols, nnz, vs);
+        DevBuf djc(sizeof(int32_t) * std::max<int64_t>(nzc, 1), c.stream),
+            dcp(sizeof(int32_t) * (nzc + 1), c.stream);
+        if (nzc) {
+            SLAPCU_CUDA(cudaMemcpyAsync(djc.get(), jc, sizeof(int32_t) * nzc, cudaMemcpyHostToDevice, c.stream));
+            SLAPCU_CUDA(cudaMemcpyAsync(dcp.get(), cp, sizeof(int32_t) * (nzc + 1), cudaMemcpyHostToDevice, c.stream));
+        } else {
+            SLAPCU_CUDA(cudaMemsetAsync(dcp.get(), 0, sizeof(int32_t), c.stream));
+        }
+        // local_matrix.hpp:88-150 (jc, cp) -> dense colptr on the device
+        dcsc_colptr(c, ncols, nzc, djc.as<int32_t>(), dcp.as<int32_t>(), d->colptr);
+        if (nnz) {
+            SLAPCU_CUDA(cudaMemcpyAsync(d->rowids, rowids, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, c.stream));
+            if (vals) SLAPCU_CUDA(cudaMemcpyAsync(d->vals, vals, size_t(vs) * nnz, cudaMemcpyHostToDevice, c.stream));
+        }
+        SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+    });
+}
+
+slapcu_status slapcu_csc_download(slapcu_ctx ctx, const slapcu_csc* d, slapcu_semiring sr, slapcu_host_csc* h) {
+    return guarded(ctx, [&](Ctx& c) {
+        require(h && d, SLAPCU_ERR_INVALID, "null argument");
+        const int vs = value_size(sr);
+        require(vs > 0, SLAPCU_ERR_INVALID, "unknown semiring");
+        DevCsc m = view(*d);
+        resolve(c, m);
+        *h = slapcu_host_csc{m.nrows, m.ncols, m.span, nullptr, nullptr, nullptr};
+        h->colptr = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * (m.ncols + 1)));
+        h->rowids = static_cast<int32_t*>(std::malloc(sizeof(int32_t) * std::max<int64_t>(m.span, 1)));
+        h->vals = std::malloc(size_t(vs) * std::max<int64_t>(m.span, 1));
+        if (!h->colptr || !h->rowids || !h->vals) {
+            slapcu_host_free(h);
+            throw Fail{SLAPCU_ERR_NOMEM, "host allocation failed"};
+        }
+        SLAPCU_CUDA(cudaMemcpyAsync(h->colptr, m.cp, sizeof(int64_t) * (m.ncols + 1), cudaMemcpyDeviceToHost, c.stream));
+        if (m.span) {
+            SLAPCU_CUDA(cudaMemcpyAsync(h->rowids, m.rw + m.base, sizeof(int32_t) * m.span, cudaMemcpyDeviceToHost,
+                                        c.stream));
+            if (m.v)
+                SLAPCU_CUDA(cudaMemcpyAsync(h->vals, static_cast<const char*>(m.v) + size_t(vs) * m.base,
+                                            size_t(vs) * m.span, cudaMemcpyDeviceToHost, c.stream));
+        }
+        SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+        for (int64_t j = 0; j <= m.ncols; ++j) h->colptr[j] -= m.base;
+    });
+}
+
+// Pattern of a host CSC on the device (colptr + rowids; values are not read
+// by estimate_flops / symbolic_nnz).
+struct PatternUpload {
+    DevBuf cp, rw;
+    DevCsc m;
+    PatternUpload(Ctx& c, const slapcu_host_csc& h)
+        : cp(sizeof(int64_t) * (h.ncols + 1), c.stream), rw(sizeof(int32_t) * std::max<int64_t>(h.nnz, 1), c.stream) {
+        SLAPCU_CUDA(cudaMemcpyAsync(cp.get(), h.colptr, sizeof(int64_t) * (h.ncols + 1), cudaMemcpyHostToDevice, c.stream));
+        if (h.nnz)
+            SLAPCU_CUDA(cudaMemcpyAsync(rw.get(), h.rowids, sizeof(int32_t) * h.nnz, cudaMemcpyHostToDevice, c.stream));
+        m = DevCsc{h.nrows, h.ncols, h.nnz, cp.as<int64_t>(), rw.as<int32_t>(), nullptr};
+    }
+};
+
+static void host_dims(const slapcu_host_csc* A, const slapcu_host_csc* B) {
+    require(A && B, SLAPCU_ERR_INVALID, "null operand");
+    if (A->ncols != B->nrows)
+        throw Fail{SLAPCU_ERR_DIM, "spgemm inner dims: A is " + std::to_string(A->nrows) + "x" +
+                                       std::to_string(A->ncols) + ", B is " + std::to_string(B->nrows) + "x" +
+                                       std::to_string(B->ncols)};
+}
+
+slapcu_status slapcu_estimate_flops_host(slapcu_ctx ctx, const slapcu_host_csc* A, const slapcu_host_csc* B,
+                                         int64_t* flops_per_col, int64_t* total) {
+    return guarded(ctx, [&](Ctx& c) {
+        host_dims(A, B);
+        PatternUpload a(c, *A), b(c, *B);
+        DevBuf fl(sizeof(int64_t) * std::max<int64_t>(B->ncols, 1), c.stream);
+        int64_t tot = 0;
+        spgemm_flops(c, a.m, b.m, fl.as<int64_t>(), &tot);
+        if (flops_per_col && B->ncols)
+            SLAPCU_CUDA(cudaMemcpyAsync(flops_per_col, fl.get(), sizeof(int64_t) * B->ncols, cudaMemcpyDeviceToHost,
+                                        c.stream));
+        SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+        if (total) *total = tot;
+    });
+}
+
+slapcu_status slapcu_symbolic_nnz_host(slapcu_ctx ctx, const slapcu_host_csc* A, const slapcu_host_csc* B,
+                                       slapcu_alg alg, int64_t* counts) {
+    return guarded(ctx, [&](Ctx& c) {
+        host_dims(A, B);
+        require(counts || B->ncols == 0, SLAPCU_ERR_INVALID, "null counts");
+        PatternUpload a(c, *A), b(c, *B);
+        DevBuf cp(sizeof(int64_t) * (B->ncols + 1), c.stream);
+        spgemm_symbolic(c, a.m, b.m, alg, cp.as<int64_t>());
+        std::vector<int64_t> h(size_t(B->ncols) + 1);
+        SLAPCU_CUDA(cudaMemcpyAsync(h.data(), cp.get(), sizeof(int64_t) * (B->ncols + 1), cudaMemcpyDeviceToHost,
+                                    c.stream));
+        SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+        for (int64_t j = 0; j < B->ncols; ++j) counts[j] = h[j + 1] - h[j];
     });
 }
 

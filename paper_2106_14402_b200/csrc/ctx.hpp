@@ -137,7 +137,8 @@ struct Options {
                                  // -1 = by accumulator width: 8192 for 4-byte, 4096 for 8-byte)
     int direct_emit_blocks = 0;             // emit: one warp per (item, block) (1) or one CTA per item (0)
     int direct_tile_major = 0;              // form: work units ordered by row tile, then heaviest first
-    int direct_form_walk = 0;               // form: 0 block-synchronous batches, 1 warp-independent walk
+    int direct_form_walk = 0;               // form: long runs as 256-product units (0) or packed products (1)
+    int direct_short_run = 0;               // form: runs shorter than this walked per thread (0 = default 8)
     int direct_persistent = 1;              // form kernel: persistent CTAs (1) or one CTA per unit (0)
     int direct_form_threads = 256;          // CTA size of the form kernel (128, 256, 512)
     int direct_emit_threads = 128;          // CTA size of the emit kernel (128, 256)

@@ -156,10 +156,10 @@ __device__ __forceinline__ void mark(unsigned bmA, unsigned sumA, int rr) {
 // that the warps walk lane-strided with U loads in flight (coalesced,
 // balanced across warps; a warp's units are increasing, so the entry owning
 // a unit is found by advancing, not searching).
-template <int NT, int U, int MODE>
+template <int NT, int U, int MODE, bool PACK>
 __device__ __forceinline__ void tile_walk(const DevCsc& A, const DevCsc& B, const int32_t* __restrict__ Atp, int T,
                                           int64_t b0, int64_t b1, int t, int t0, unsigned* bm, unsigned* summ,
-                                          WalkSm<NT>& sh, const DenseRuns& dr, int W, int quads) {
+                                          WalkSm<NT>& sh, const DenseRuns& dr, int W, int quads, int short_run) {
     constexpr int NW = NT / 32;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int32_t* __restrict__ Arw = A.rw;
@@ -180,7 +180,7 @@ __device__ __forceinline__ void tile_walk(const DevCsc& A, const DevCsc& B, cons
             if (dr.dmin && len >= dr.dmin) {
                 sh.dense[atomicAdd(&sh.ndense, 1)] = dr.slot[int64_t(k) * T + t];
                 len = 0;
-            } else if (len < kShortRun) {
+            } else if (len < short_run) {
                 // loads in groups of 4 so a short run is not a chain of L2 round trips
                 const int32_t* q = Arw + s;
                 int x = 0;
@@ -206,17 +206,51 @@ __device__ __forceinline__ void tile_walk(const DevCsc& A, const DevCsc& B, cons
         }
         __syncthreads();
         const int nl = sh.nlong;
-        const int units = tid < nl ? (sh.len[tid] + kUnit - 1) / kUnit : 0;
+        // PACK: prefix of the long runs' products (the warps split the
+        // concatenated products evenly, 32 * U per step, so runs of 8..100
+        // products fill whole warps); else prefix of 256-product units
+        const int units = tid < nl ? (PACK ? sh.len[tid] : (sh.len[tid] + kUnit - 1) / kUnit) : 0;
         int tot;
         const int ex = block_excl_scan<NT>(units, sh.wsum, &tot);
         sh.ustart[tid] = ex;
         if (tid == 0) sh.ustart[nl] = tot;
         __syncthreads();
+        if (PACK) {
+            const int p0 = (int)((int64_t(tot) * warp) / NW), p1 = (int)((int64_t(tot) * (warp + 1)) / NW);
+            int e = 0;
+            if (p0 < p1) {  // owner of this lane's first product: largest e with ustart[e] <= o
+                const int o = min(p0 + lane, p1 - 1);
+                int lo = 0, hi = nl - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (sh.ustart[mid] <= o)
+                        lo = mid;
+                    else
+                        hi = mid - 1;
+                }
+                e = lo;
+            }
+            for (int base = p0; base < p1; base += 32 * U) {
+                int r[U];
+#pragma unroll
+                for (int v = 0; v < U; ++v) {
+                    const int o = base + lane + 32 * v;
+                    r[v] = -1;
+                    if (o < p1) {
+                        while (sh.ustart[e + 1] <= o) ++e;
+                        r[v] = __ldg(Arw + sh.start[e] + (o - sh.ustart[e]));
+                    }
+                }
+#pragma unroll
+                for (int v = 0; v < U; ++v)
+                    if (r[v] >= 0) mark<MODE>(bmA, sumA, r[v]);
+            }
+        }
         // warp w takes the contiguous unit range [u0, u1): one search for the
         // owning long run, then it only advances (every long run has units)
         const int u0 = (int)((int64_t(tot) * warp) / NW), u1 = (int)((int64_t(tot) * (warp + 1)) / NW);
         int e = 0;
-        if (u0 < u1) {
+        if (!PACK && u0 < u1) {
             int lo = 0, hi = nl - 1;
             while (lo < hi) {
                 const int mid = (lo + hi + 1) >> 1;
@@ -227,7 +261,7 @@ __device__ __forceinline__ void tile_walk(const DevCsc& A, const DevCsc& B, cons
             }
             e = lo;
         }
-        for (int u = u0; u < u1; ++u) {
+        for (int u = u0; !PACK && u < u1; ++u) {
             if (sh.ustart[e + 1] <= u) ++e;
             const int c0 = (u - sh.ustart[e]) * kUnit;
             const int32_t* run = Arw + sh.start[e] + c0;
@@ -314,6 +348,7 @@ struct FormArgs {
     int nunits;
     int* rbc;  // per item entries per 4096-row block (value semirings), or null
     int quads;  // 1: lane-contiguous quads merged per word before the shared update
+    int short_run;  // runs shorter than this are walked by their own thread
 };
 
 // Count, choose the stash form and write it, then clear the bitmap (whole
@@ -411,7 +446,7 @@ __device__ __forceinline__ void stash_bitmap(unsigned* bm, unsigned* summ, uint1
 }
 
 // Persistent: each CTA takes work units (heaviest first) by ticket.
-template <int NT, int MODE>
+template <int NT, int MODE, bool PACK = false>
 __global__ void __launch_bounds__(NT) k_tile_form(FormArgs g) {
     extern __shared__ __align__(16) unsigned char sm_raw[];
     const int W = 1 << (g.TL - 5);
@@ -436,7 +471,8 @@ __global__ void __launch_bounds__(NT) k_tile_form(FormArgs g) {
         const int4 u = g.units[g.order[ui]];
         const int2 it = g.items[u.x];
         const int64_t bs = g.B.cp[it.x];
-        tile_walk<NT, 4, MODE>(g.A, g.B, g.Atp, g.T, bs + u.y, bs + u.z, it.y, it.y << g.TL, bm, summ, sh, g.dr, W, g.quads);
+        tile_walk<NT, 4, MODE, PACK>(g.A, g.B, g.Atp, g.T, bs + u.y, bs + u.z, it.y, it.y << g.TL, bm, summ, sh, g.dr, W, g.quads,
+                                     g.short_run);
         if (MODE != 2 && u.w < 0) {  // summary by ballots over the bitmap
             const int lane = threadIdx.x & 31;
             for (int cc = threadIdx.x >> 5; cc < W / 32; cc += NT / 32) {
@@ -455,139 +491,6 @@ __global__ void __launch_bounds__(NT) k_tile_form(FormArgs g) {
             for (int q = threadIdx.x; q < W / 32; q += NT) summ[q] = 0u;
         } else {
             stash_bitmap<NT>(bm, summ, tl, W, sh.wsum, red, bcs, u.x, it.x, g.stash + g.soff[u.x], g.sres[u.x], g.cnt,
-                             g.form, g.hcnt, g.rbc);
-        }
-        __syncthreads();
-    }
-}
-
-// Warp-independent walk of B entries [b0, b1) (column j) into the tile
-// bitmap: the warps of the CTA take 32 entries at a time from a shared
-// cursor, so no block barrier sits inside the walk (the batch-synchronous
-// tile_walk above pays ~7 barriers per 256 entries and waits on its longest
-// run).  Per chunk: every lane gathers its entry's tile run; short runs are
-// walked by their own lane (4 loads in flight); long runs are walked by the
-// whole warp lane-strided, one after the other (ballot order); dense runs
-// OR their cached tile bitmap with 16-byte loads.
-template <int U>
-__device__ __forceinline__ void warp_walk(const DevCsc& A, const DevCsc& B, const int32_t* __restrict__ Atp, int T,
-                                          int64_t b0, int64_t b1, int t, int t0, unsigned* bm, int* cursor,
-                                          const DenseRuns& dr, int W) {
-    const int lane = threadIdx.x & 31;
-    const int32_t* __restrict__ Arw = A.rw;
-    const unsigned bm0 = smem_addr(bm);
-    const unsigned bmA = bm0 - (unsigned(t0 >> 5) << 2);
-    for (;;) {
-        int c = 0;
-        if (lane == 0) c = atomicAdd(cursor, 32);
-        c = __shfl_sync(0xffffffffu, c, 0);
-        const int64_t i = b0 + c + lane;
-        if (b0 + c >= b1) break;
-        int len = 0;
-        int64_t st = 0;
-        int dslot = -1;
-        if (i < b1) {
-            const int k = B.rw[i];
-            const int32_t* tp = Atp + int64_t(k) * (T + 1) + t;
-            const int lo = tp[0], hi = tp[1];
-            st = A.cp[k] + lo;
-            len = hi - lo;
-            if (dr.dmin && len >= dr.dmin) {
-                dslot = dr.slot[int64_t(k) * T + t];
-                len = 0;
-            }
-        }
-        // short runs: each lane its own
-        if (len < kShortRun) {
-            const int32_t* q = Arw + st;
-            int x = 0;
-            for (; x + 4 <= len; x += 4) {
-                const int r0 = __ldg(q + x), r1 = __ldg(q + x + 1), r2 = __ldg(q + x + 2), r3 = __ldg(q + x + 3);
-                mark<0>(bmA, 0, r0);
-                mark<0>(bmA, 0, r1);
-                mark<0>(bmA, 0, r2);
-                mark<0>(bmA, 0, r3);
-            }
-            for (; x < len; ++x) mark<0>(bmA, 0, __ldg(q + x));
-        }
-        // long runs: the warp walks each, lane-strided, U loads in flight
-        unsigned lm = __ballot_sync(0xffffffffu, len >= kShortRun);
-        while (lm) {
-            const int src = __ffs(lm) - 1;
-            lm &= lm - 1u;
-            const int m = __shfl_sync(0xffffffffu, len, src);
-            const int32_t* run = Arw + __shfl_sync(0xffffffffu, st, src);
-            int x = lane;
-            for (; x + 32 * (U - 1) < m; x += 32 * U) {
-                int r[U];
-#pragma unroll
-                for (int v = 0; v < U; ++v) r[v] = __ldg(run + x + 32 * v);
-#pragma unroll
-                for (int v = 0; v < U; ++v) mark<0>(bmA, 0, r[v]);
-            }
-            for (; x < m; x += 32) mark<0>(bmA, 0, __ldg(run + x));
-        }
-        // dense runs: OR the cached tile bitmap, the warp together
-        unsigned dm = __ballot_sync(0xffffffffu, dslot >= 0);
-        while (dm) {
-            const int src = __ffs(dm) - 1;
-            dm &= dm - 1u;
-            const int ds = __shfl_sync(0xffffffffu, dslot, src);
-            const uint4* srcb = reinterpret_cast<const uint4*>(dr.bm + int64_t(ds) * W);
-            for (int q = lane; q < (W >> 2); q += 32) {
-                const uint4 v = __ldg(srcb + q);
-                const unsigned a = bm0 + (unsigned(q) << 4);
-                if (v.x) set_bits<0>(a, v.x, 0, 0);
-                if (v.y) set_bits<0>(a + 4, v.y, 0, 0);
-                if (v.z) set_bits<0>(a + 8, v.z, 0, 0);
-                if (v.w) set_bits<0>(a + 12, v.w, 0, 0);
-            }
-        }
-    }
-}
-
-// k_tile_form with the warp-independent walk (SLAPCU_OPT_DIRECT_FORM_WALK 1).
-template <int NT>
-__global__ void __launch_bounds__(NT) k_tile_form_w(FormArgs g) {
-    extern __shared__ __align__(16) unsigned char sm_raw[];
-    const int W = 1 << (g.TL - 5);
-    unsigned* bm = reinterpret_cast<unsigned*>(sm_raw);
-    unsigned* summ = bm + W;                                    // [W/32]
-    uint16_t* tl = reinterpret_cast<uint16_t*>(summ + W / 32);  // [W]
-    __shared__ int wsum[NT / 32 + 1];
-    __shared__ int red[NT / 32];
-    __shared__ int ticket_sh, cursor;
-    __shared__ int bcs[kMaxBlocks];
-    smem_zero(bm, W + W / 32);
-    for (int b = threadIdx.x; b < kMaxBlocks; b += NT) bcs[b] = 0;
-    for (;;) {
-        if (threadIdx.x == 0) {
-            ticket_sh = atomicAdd(g.ticket, 1);
-            cursor = 0;
-        }
-        __syncthreads();
-        const int ui = ticket_sh;
-        if (ui >= g.nunits) break;
-        const int4 u = g.units[g.order[ui]];
-        const int2 it = g.items[u.x];
-        const int64_t bs = g.B.cp[it.x];
-        warp_walk<4>(g.A, g.B, g.Atp, g.T, bs + u.y, bs + u.z, it.y, it.y << g.TL, bm, &cursor, g.dr, W);
-        __syncthreads();
-        if (u.w >= 0) {  // one part of a split item: partial bitmap out, then clear
-            uint4* d4 = reinterpret_cast<uint4*>(g.partial + int64_t(u.w) * W);
-            uint4* s4 = reinterpret_cast<uint4*>(bm);
-            for (int q = threadIdx.x; q < W / 4; q += NT) {
-                d4[q] = s4[q];
-                s4[q] = make_uint4(0u, 0u, 0u, 0u);
-            }
-        } else {
-            const int lane = threadIdx.x & 31;
-            for (int cc = threadIdx.x >> 5; cc < W / 32; cc += NT / 32) {
-                const unsigned nz = __ballot_sync(0xffffffffu, bm[cc * 32 + lane] != 0u);
-                if (lane == 0) summ[cc] = nz;
-            }
-            __syncthreads();
-            stash_bitmap<NT>(bm, summ, tl, W, wsum, red, bcs, u.x, it.x, g.stash + g.soff[u.x], g.sres[u.x], g.cnt,
                              g.form, g.hcnt, g.rbc);
         }
         __syncthreads();
@@ -1934,7 +1837,7 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
                    (const int*)d.order.as<int>(), d.stash.as<unsigned>(), (const int64_t*)d.soff.as<int64_t>(),
                    (const int64_t*)d.sres.as<int64_t>(), d.partial.as<unsigned>(), d.cnt.as<int64_t>(),
                    d.form.as<int>(), d.hcnt.as<unsigned long long>(), nullptr, 0, rbc,
-                   c.opt.direct_quads};
+                   c.opt.direct_quads, c.opt.direct_short_run > 0 ? c.opt.direct_short_run : kShortRun};
         const size_t smem = sizeof(unsigned) * (W + W / 32) + sizeof(uint16_t) * W;
         DevBuf tick(sizeof(int), c.stream);
         SLAPCU_CUDA(cudaMemsetAsync(tick.get(), 0, sizeof(int), c.stream));
@@ -1950,7 +1853,7 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
         };
         const int ft = c.opt.direct_form_threads;
         if (c.opt.direct_form_walk == 1)
-            ft == 512 ? form(k_tile_form_w<512>, 512) : form(k_tile_form_w<256>, 256);
+            form(k_tile_form<256, 0, true>, 256);
         else if (c.opt.direct_mark_mode == 2)
             form(k_tile_form<256, 2>, 256);
         else if (ft == 128)

@@ -241,6 +241,7 @@ void concat_multiply(Ctx& c, const std::vector<DevCsc>& As, const std::vector<De
                      Block& out, float* ms) {
     const int q = (int)As.size();
     const int vs = value_size(sr);
+    if (q > 8) throw Fail{SLAPCU_ERR_INTERNAL, "concat_multiply: at most 8 parts (VStack)"};
     int64_t K = 0, annz = 0, bnnz = 0;
     for (int s = 0; s < q; ++s) {
         K += As[s].ncols;
@@ -357,6 +358,10 @@ __global__ void k_identity(int64_t n, int64_t* __restrict__ cp, int32_t* __restr
 void fast_merge(Ctx& c, std::vector<DevCsc> parts, int sr, int alg, slapcu_csc_out* C, float* ms) {
     const int vs = value_size(sr);
     for (auto& p : parts) resolve(c, p);
+    if (parts.size() > 8) {  // the concatenated product stacks at most 8 parts: multiway merge instead
+        merge_blocks(c, parts, sr, C);
+        return;
+    }
     const int64_t N = parts[0].ncols;
     Block id;
     id.nrows = N;
@@ -617,6 +622,100 @@ slapcu_status slapcu_summa2d(slapcu_comm cm, const slapcu_csc* A_local, const sl
             stats->ms_total = total.ms();
             stats->nnz_out = C_local->nnz;
         }
+        return SLAPCU_OK;
+    } catch (const Fail& e) {
+        c.last_error = e.msg;
+        return e.st;
+    }
+}
+
+__global__ void k_col_counts(int64_t n, const int64_t* __restrict__ cp, int64_t* __restrict__ out) {
+    for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < n; j += int64_t(gridDim.x) * blockDim.x)
+        out[j] = cp[j + 1] - cp[j];
+}
+
+// batched.hpp:70-117 dist_symbolic_col_nnz: the pattern product over the
+// q x q grid (OrAnd SUMMA on all-one copies of the operands' patterns), its
+// per-column counts summed over the grid column (allreduce on the column
+// communicator) and concatenated over the grid row (all-gather on the row
+// communicator): every rank returns all of B's column counts.
+slapcu_status slapcu_dist_symbolic_col_nnz(slapcu_comm cm, const slapcu_csc* A_local, const slapcu_csc* B_local,
+                                           int64_t* counts, int64_t ncols) {
+    if (!cm || !A_local || !B_local || !counts) return SLAPCU_ERR_INVALID;
+    Ctx& c = ctx_of(cm->ctx);
+    try {
+        SLAPCU_CUDA(cudaSetDevice(c.device));
+        int64_t q = 0;
+        if (!is_square(cm->nranks, &q))
+            throw Fail{SLAPCU_ERR_SHAPE, "2D SUMMA needs a square process grid, got p=" + std::to_string(cm->nranks)};
+        DevCsc A = view(*A_local), B = view(*B_local);
+        resolve(c, A);
+        resolve(c, B);
+        // pattern operands: values all 1 (u8), addressed like the originals
+        const int64_t mx = std::max<int64_t>(std::max<int64_t>(A.span, B.span), 1);
+        DevBuf ones(size_t(mx), c.stream);
+        SLAPCU_CUDA(cudaMemsetAsync(ones.get(), 1, size_t(mx), c.stream));
+        slapcu_csc ap = *A_local, bp = *B_local;
+        ap.vals = static_cast<const char*>(ones.get()) - A.base;
+        bp.vals = static_cast<const char*>(ones.get()) - B.base;
+        slapcu_csc_out cpat{};
+        const slapcu_status st =
+            slapcu_summa2d(cm, &ap, &bp, SLAPCU_OR_AND_U8, SLAPCU_ALG_HASH, &cpat, nullptr);
+        if (st != SLAPCU_OK) return st;
+        struct FreeOut {
+            Ctx& c;
+            slapcu_csc_out& o;
+            ~FreeOut() {
+                if (o.colptr) cudaFreeAsync(o.colptr, c.stream);
+                if (o.rowids) cudaFreeAsync(o.rowids, c.stream);
+                if (o.vals) cudaFreeAsync(o.vals, c.stream);
+            }
+        } free_pat{c, cpat};
+        const int i = cm->rank / (int)q, j = cm->rank % (int)q;
+        const int64_t nl = B.ncols;
+        // every grid column's block width (row all-gather of the local widths)
+        std::vector<int64_t> widths(size_t(q), nl);
+        ncclComm_t row = nullptr, col = nullptr;
+        if (q > 1) {
+            row = split(cm, "row2d", i, j);
+            col = split(cm, "col2d", j, i);
+            DevBuf w(sizeof(int64_t) * (q + 1), c.stream);
+            SLAPCU_CUDA(cudaMemcpyAsync(w.as<int64_t>() + q, &nl, sizeof(int64_t), cudaMemcpyHostToDevice, c.stream));
+            SLAPCU_NCCL(ncclAllGather(w.as<int64_t>() + q, w.as<int64_t>(), 1, ncclInt64, row, c.stream));
+            SLAPCU_CUDA(cudaMemcpyAsync(widths.data(), w.get(), sizeof(int64_t) * q, cudaMemcpyDeviceToHost, c.stream));
+            SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+        }
+        int64_t total = 0, wmax = 1;
+        for (auto x : widths) {
+            total += x;
+            wmax = std::max(wmax, x);
+        }
+        if (total != ncols)
+            throw Fail{SLAPCU_ERR_DIM, "column blocks sum to " + std::to_string(total) + ", B has " +
+                                           std::to_string(ncols) + " columns"};
+        DevBuf loc(sizeof(int64_t) * wmax * (q + 1), c.stream);
+        int64_t* mine = loc.as<int64_t>() + wmax * q;
+        SLAPCU_CUDA(cudaMemsetAsync(mine, 0, sizeof(int64_t) * wmax, c.stream));
+        if (nl) launch(c, k_col_counts, dim3(grid_for(c, nl, 256)), dim3(256), 0, nl, (const int64_t*)cpat.colptr, mine);
+        if (q > 1) {
+            // batched.hpp:109-110 col_comm.allreduce_vec, :111-112 row_comm.allgatherv (padded to the widest block)
+            SLAPCU_NCCL(ncclAllReduce(mine, mine, size_t(wmax), ncclInt64, ncclSum, col, c.stream));
+            SLAPCU_NCCL(ncclAllGather(mine, loc.as<int64_t>(), size_t(wmax), ncclInt64, row, c.stream));
+            cm->calls[kReduce] += 1;
+            cm->bytes[kReduce] += sizeof(int64_t) * nl;
+            cm->calls[kAllgatherv] += 1;
+            cm->bytes[kAllgatherv] += sizeof(int64_t) * nl;
+        } else {
+            SLAPCU_CUDA(cudaMemcpyAsync(loc.get(), mine, sizeof(int64_t) * wmax, cudaMemcpyDeviceToDevice, c.stream));
+        }
+        int64_t o = 0;
+        for (int b = 0; b < (int)q; ++b) {
+            if (widths[b])
+                SLAPCU_CUDA(cudaMemcpyAsync(counts + o, loc.as<int64_t>() + int64_t(b) * wmax, sizeof(int64_t) * widths[b],
+                                            cudaMemcpyDeviceToHost, c.stream));
+            o += widths[b];
+        }
+        SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
         return SLAPCU_OK;
     } catch (const Fail& e) {
         c.last_error = e.msg;

@@ -19,3 +19,17 @@ BIN = os.path.join(ROOT, "build", "shim_test")
 def test_cpp_dropin_matches_reference():
     r = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "SHIM_OK" in r.stdout, r.stdout + r.stderr
+
+
+DIST_BIN = os.path.join(ROOT, "build", "shim_dist_test")
+
+
+@pytest.mark.skipif(not torch.cuda.is_available(), reason="no CUDA device")
+@pytest.mark.skipif(not os.path.exists(DIST_BIN), reason="build/shim_dist_test not built (needs the reference headers)")
+def test_cpp_dist_dropins_match_reference():
+    """estimate_flops / symbolic_nnz / summa2d_spgemm / ca3d_spgemm /
+    dist_symbolic_col_nnz / plan_batches_by_budget / batched_spgemm drop-ins
+    against the reference templates inside one slap::run_world (p up to the
+    visible GPU count: 1 on the driver box, 4 on a 4-GPU box)."""
+    r = subprocess.run([DIST_BIN], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "SHIM_DIST_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
