@@ -75,6 +75,8 @@ def parse():
     ap.add_argument("--tile-major", type=int, default=None, help="direct path form: units ordered by row tile (1)")
     ap.add_argument("--form-walk", type=int, default=None, help="direct path form: 1 packed long-run products")
     ap.add_argument("--short-run", type=int, default=None, help="direct path form: per-thread run threshold")
+    ap.add_argument("--value-tmajor", type=int, default=None, help="direct value pass: tile-major table + row-order chunks")
+    ap.add_argument("--words", type=int, default=None, help="direct form: walk A's (word, mask) pairs")
     ap.add_argument("--dist", default="1d", choices=["1d", "summa"],
                     help="N>1: 1d = flops-balanced column blocks with A replicated (no data-path collective); "
                          "summa = the 2D SUMMA / 3D drivers (NCCL stage broadcasts, fiber exchange, merge)")
@@ -117,6 +119,10 @@ def apply_options(ctx, args):
         ctx.set_option(L.OPT_DIRECT_FORM_WALK, args.form_walk)
     if args.short_run is not None:
         ctx.set_option(L.OPT_DIRECT_SHORT_RUN, args.short_run)
+    if args.value_tmajor is not None:
+        ctx.set_option(L.OPT_DIRECT_VALUE_TMAJOR, args.value_tmajor)
+    if args.words is not None:
+        ctx.set_option(L.OPT_DIRECT_WORDS, args.words)
     if args.value_rank is not None:
         ctx.set_option(L.OPT_DIRECT_VALUE_RANK, args.value_rank)
     if args.value_interleave is not None:

@@ -165,8 +165,12 @@ typedef enum {
                                               0 = 256-product units, one run per warp step; 1 = packed
                                               products (the warps split the concatenated products evenly,
                                               several short runs per warp step) */
-    SLAPCU_OPT_DIRECT_SHORT_RUN = 25       /* direct path form: runs (A column x row tile) shorter than this
+    SLAPCU_OPT_DIRECT_SHORT_RUN = 25,      /* direct path form: runs (A column x row tile) shorter than this
                                               are walked by their own thread (0 = default 8) */
+    SLAPCU_OPT_DIRECT_VALUE_TMAJOR = 26,   /* direct path value pass: 1 = 4096-row tile pointers stored
+                                              tile-major and rank chunks run in row-block order */
+    SLAPCU_OPT_DIRECT_WORDS = 27           /* direct path form: 1 = walk A as (32-row word, row mask) pairs
+                                              (built per A): one shared update per distinct word of a run */
 } slapcu_option;
 slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t value);
 

@@ -128,6 +128,7 @@ slapcu_status slapcu_ctx_invalidate(slapcu_ctx ctx) {
     return guarded(ctx, [&](Ctx& c) {
         c.direct.atp_valid = false;
         c.direct.atpv_valid = false;
+        c.direct.aw_valid = false;
         c.plan.valid = false;
     });
 }
@@ -165,6 +166,8 @@ slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t v
             require(v == 0 || v == 1, SLAPCU_ERR_INVALID, "form walk: 0 (256-product units) or 1 (packed products)");
             c.opt.direct_form_walk = (int)v;
             break;
+        case SLAPCU_OPT_DIRECT_WORDS: c.opt.direct_words = v != 0; break;
+        case SLAPCU_OPT_DIRECT_VALUE_TMAJOR: c.opt.direct_value_tmajor = v != 0; break;
         case SLAPCU_OPT_DIRECT_SHORT_RUN:
             require(v >= 0 && v <= 256, SLAPCU_ERR_INVALID, "short run threshold: 0 (default) .. 256");
             c.opt.direct_short_run = (int)v;

@@ -138,6 +138,8 @@ struct Options {
     int direct_emit_blocks = 0;             // emit: one warp per (item, block) (1) or one CTA per item (0)
     int direct_tile_major = 0;              // form: work units ordered by row tile, then heaviest first
     int direct_form_walk = 0;               // form: long runs as 256-product units (0) or packed products (1)
+    int direct_words = 0;                   // form: walk A's (32-row word, mask) pairs instead of its rows
+    int direct_value_tmajor = 0;            // value pass: tile-major 4096-row pointer table + chunks in row order
     int direct_short_run = 0;               // form: runs shorter than this walked per thread (0 = default 8)
     int direct_persistent = 1;              // form kernel: persistent CTAs (1) or one CTA per unit (0)
     int direct_form_threads = 256;          // CTA size of the form kernel (128, 256, 512)
@@ -155,11 +157,17 @@ struct DirectCache {
     int atp_tl = -1;
     bool atp_valid = false;
     DevBuf dslot, dbm;  // dense A runs: slot per (k, tile), tile bitmaps
+    DevBuf aw, awcp, watp;  // word form of A: (word, mask) pairs, their colptr, word tile pointers
+    uint64_t aw_key = 0;
+    int aw_tl = -1;
+    int64_t aw_ncols = -1;
+    bool aw_valid = false;
     DevBuf atpv;        // A tile pointers at the value-pass sub-tile height
     uint64_t atpv_key = 0;
     int64_t atpv_ncols = -1, atpv_nnz = -1;
     int atpv_tl = -1;
     bool atpv_valid = false;
+    bool atpv_tmajor = false;
     int ndense = 0, dense_min = -1;
     DevBuf lp, hcnt, hl, items, ifl, sres, soff, units, order, stash, partial, cnt, form, hoff, rbc;
     DevBuf dist_rw, dist_v;  // SUMMA concatenated product: bound-sized output scratch

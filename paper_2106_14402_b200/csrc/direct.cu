@@ -230,6 +230,11 @@ __device__ __forceinline__ void tile_walk(const DevCsc& A, const DevCsc& B, cons
                 }
                 e = lo;
             }
+            // the current run lives in registers (next boundary, rebased
+            // pointer): shared memory is read only when a lane crosses into
+            // the next run -- the walk is LSU-bound, so no per-product LDS
+            int nextp = p0 < p1 ? sh.ustart[e + 1] : 0;
+            const int32_t* bp = p0 < p1 ? Arw + (sh.start[e] - sh.ustart[e]) : Arw;
             for (int base = p0; base < p1; base += 32 * U) {
                 int r[U];
 #pragma unroll
@@ -237,8 +242,12 @@ __device__ __forceinline__ void tile_walk(const DevCsc& A, const DevCsc& B, cons
                     const int o = base + lane + 32 * v;
                     r[v] = -1;
                     if (o < p1) {
-                        while (sh.ustart[e + 1] <= o) ++e;
-                        r[v] = __ldg(Arw + sh.start[e] + (o - sh.ustart[e]));
+                        while (o >= nextp) {
+                            ++e;
+                            nextp = sh.ustart[e + 1];
+                            bp = Arw + (sh.start[e] - sh.ustart[e]);
+                        }
+                        r[v] = __ldg(bp + o);
                     }
                 }
 #pragma unroll
@@ -327,6 +336,119 @@ __device__ __forceinline__ void tile_walk(const DevCsc& A, const DevCsc& B, cons
     }
 }
 
+// Word form of the walk: A is given as (32-row word, row mask) pairs per
+// column (A's distinct words in row order, built per A), so a run of rows
+// that share words costs one shared update per WORD instead of one per
+// product -- at R-MAT s20 the 70.1e9 multiplies of A*A are 36.9e9 word
+// updates (runs of 512-4096 rows compress 1.9x).  Same batch structure as
+// tile_walk; "products" below are word entries.
+__device__ __forceinline__ void mark_word(unsigned bmA, int2 e) {
+    set_bits<0>(bmA + (unsigned(e.x) << 2), (unsigned)e.y, 0, 0);
+}
+
+template <int NT, int U, bool PACK>
+__device__ __forceinline__ void tile_walk_words(const int2* __restrict__ Aw, const int64_t* __restrict__ Awcp,
+                                                const DevCsc& B, const int32_t* __restrict__ Atp, int T, int64_t b0,
+                                                int64_t b1, int t, int t0, unsigned* bm, WalkSm<NT>& sh, int short_run) {
+    constexpr int NW = NT / 32;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned bmA = smem_addr(bm) - (unsigned(t0 >> 5) << 2);  // absolute word index -> tile bitmap
+    for (int64_t base = b0; base < b1; base += NT) {
+        const int64_t i = base + tid;
+        if (i < b1) {
+            const int k = B.rw[i];
+            const int32_t* tp = Atp + int64_t(k) * (T + 1) + t;
+            const int lo = tp[0], hi = tp[1];
+            const int64_t s = Awcp[k] + lo;
+            const int len = hi - lo;
+            if (len < short_run) {
+                const int2* q = Aw + s;
+                int x = 0;
+                for (; x + 4 <= len; x += 4) {
+                    const int2 e0 = __ldg(q + x), e1 = __ldg(q + x + 1), e2 = __ldg(q + x + 2), e3 = __ldg(q + x + 3);
+                    mark_word(bmA, e0);
+                    mark_word(bmA, e1);
+                    mark_word(bmA, e2);
+                    mark_word(bmA, e3);
+                }
+                for (; x < len; ++x) mark_word(bmA, __ldg(q + x));
+            } else {
+                const unsigned peers = __activemask();
+                const int leader = __ffs(peers) - 1;
+                int pos = 0;
+                if (lane == leader) pos = atomicAdd(&sh.nlong, __popc(peers));
+                pos = __shfl_sync(peers, pos, leader) + __popc(peers & ((1u << lane) - 1u));
+                sh.len[pos] = len;
+                sh.start[pos] = s;
+            }
+        }
+        __syncthreads();
+        const int nl = sh.nlong;
+        const int units = tid < nl ? (PACK ? sh.len[tid] : (sh.len[tid] + kUnit - 1) / kUnit) : 0;
+        int tot;
+        const int ex = block_excl_scan<NT>(units, sh.wsum, &tot);
+        sh.ustart[tid] = ex;
+        if (tid == 0) sh.ustart[nl] = tot;
+        __syncthreads();
+        const int p0 = (int)((int64_t(tot) * warp) / NW), p1 = (int)((int64_t(tot) * (warp + 1)) / NW);
+        int e = 0;
+        if (p0 < p1) {
+            const int o = PACK ? min(p0 + lane, p1 - 1) : p0;
+            int lo = 0, hi = nl - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (sh.ustart[mid] <= o)
+                    lo = mid;
+                else
+                    hi = mid - 1;
+            }
+            e = lo;
+        }
+        if (PACK) {
+            int nextp = p0 < p1 ? sh.ustart[e + 1] : 0;
+            const int2* bp = p0 < p1 ? Aw + (sh.start[e] - sh.ustart[e]) : Aw;
+            for (int pb = p0; pb < p1; pb += 32 * U) {
+                int2 r[U];
+#pragma unroll
+                for (int v = 0; v < U; ++v) {
+                    const int o = pb + lane + 32 * v;
+                    r[v] = make_int2(-1, 0);
+                    if (o < p1) {
+                        while (o >= nextp) {
+                            ++e;
+                            nextp = sh.ustart[e + 1];
+                            bp = Aw + (sh.start[e] - sh.ustart[e]);
+                        }
+                        r[v] = __ldg(bp + o);
+                    }
+                }
+#pragma unroll
+                for (int v = 0; v < U; ++v)
+                    if (r[v].x >= 0) mark_word(bmA, r[v]);
+            }
+        } else {
+            for (int u = p0; u < p1; ++u) {
+                if (sh.ustart[e + 1] <= u) ++e;
+                const int c0 = (u - sh.ustart[e]) * kUnit;
+                const int2* run = Aw + sh.start[e] + c0;
+                const int m = min(kUnit, sh.len[e] - c0);
+                int x = lane;
+                for (; x + 32 * (U - 1) < m; x += 32 * U) {
+                    int2 r[U];
+#pragma unroll
+                    for (int v = 0; v < U; ++v) r[v] = __ldg(run + x + 32 * v);
+#pragma unroll
+                    for (int v = 0; v < U; ++v) mark_word(bmA, r[v]);
+                }
+                for (; x < m; x += 32) mark_word(bmA, __ldg(run + x));
+            }
+        }
+        __syncthreads();
+        if (tid == 0) sh.nlong = 0;
+        __syncthreads();
+    }
+}
+
 // ------------------------------------------------------------------- form
 
 struct FormArgs {
@@ -349,6 +471,8 @@ struct FormArgs {
     int* rbc;  // per item entries per 4096-row block (value semirings), or null
     int quads;  // 1: lane-contiguous quads merged per word before the shared update
     int short_run;  // runs shorter than this are walked by their own thread
+    const int2* Aw;        // word form of A (words mode), or null
+    const int64_t* Awcp;   // its column pointers
 };
 
 // Count, choose the stash form and write it, then clear the bitmap (whole
@@ -446,7 +570,7 @@ __device__ __forceinline__ void stash_bitmap(unsigned* bm, unsigned* summ, uint1
 }
 
 // Persistent: each CTA takes work units (heaviest first) by ticket.
-template <int NT, int MODE, bool PACK = false>
+template <int NT, int MODE, bool PACK = false, bool WORDS = false>
 __global__ void __launch_bounds__(NT) k_tile_form(FormArgs g) {
     extern __shared__ __align__(16) unsigned char sm_raw[];
     const int W = 1 << (g.TL - 5);
@@ -471,8 +595,12 @@ __global__ void __launch_bounds__(NT) k_tile_form(FormArgs g) {
         const int4 u = g.units[g.order[ui]];
         const int2 it = g.items[u.x];
         const int64_t bs = g.B.cp[it.x];
-        tile_walk<NT, 4, MODE, PACK>(g.A, g.B, g.Atp, g.T, bs + u.y, bs + u.z, it.y, it.y << g.TL, bm, summ, sh, g.dr, W, g.quads,
-                                     g.short_run);
+        if constexpr (WORDS)
+            tile_walk_words<NT, 4, PACK>(g.Aw, g.Awcp, g.B, g.Atp, g.T, bs + u.y, bs + u.z, it.y, it.y << g.TL, bm, sh,
+                                         g.short_run);
+        else
+            tile_walk<NT, 4, MODE, PACK>(g.A, g.B, g.Atp, g.T, bs + u.y, bs + u.z, it.y, it.y << g.TL, bm, summ, sh, g.dr,
+                                         W, g.quads, g.short_run);
         if (MODE != 2 && u.w < 0) {  // summary by ballots over the bitmap
             const int lane = threadIdx.x & 31;
             for (int cc = threadIdx.x >> 5; cc < W / 32; cc += NT / 32) {
@@ -809,6 +937,7 @@ struct ValueArgs {
     const int32_t* crw;
     void* cv;
     const void* arv;      // A's (row, value bits) interleaved (int2 for 4-byte, int4 for 8-byte values), or null
+    int64_t tv_stride;    // > 0: Atpv is tile-major (entry (k, t) at t * tv_stride + k), else column-major
 };
 
 // One product's A row and value: from the interleaved copy when there is one
@@ -873,7 +1002,7 @@ struct ValueWalkSm {
 template <int SRID, int NT, class Slot>
 __device__ __forceinline__ void value_walk(const DevCsc& A, const DevCsc& B, const int32_t* __restrict__ Atab, int T,
                                            int t, int j, ValueWalkSm<SRID, NT>& sh, Slot slot, int t_hi = -1,
-                                           const void* __restrict__ Arv = nullptr) {
+                                           const void* __restrict__ Arv = nullptr, int64_t tstride = 0) {
     using S_ = Sr<SRID>;
     using T_ = typename S_::T;
     constexpr int NW = NT / 32;
@@ -887,8 +1016,16 @@ __device__ __forceinline__ void value_walk(const DevCsc& A, const DevCsc& B, con
         int slen = 0;
         if (i < be) {
             const int k = B.rw[i];
-            const int32_t* tp = Atab + int64_t(k) * (T + 1);
-            const int rlo = tp[t], rhi = tp[t_hi < 0 ? t + 1 : t_hi];  // tiles [t, t_hi) of the table
+            const int th = t_hi < 0 ? t + 1 : t_hi;  // tiles [t, th) of the table
+            int rlo, rhi;
+            if (tstride > 0) {  // tile-major table: a chunk's two rows are small and stay in L2
+                rlo = __ldg(Atab + int64_t(t) * tstride + k);
+                rhi = __ldg(Atab + int64_t(th) * tstride + k);
+            } else {
+                const int32_t* tp = Atab + int64_t(k) * (T + 1);
+                rlo = tp[t];
+                rhi = tp[th];
+            }
             const int len = rhi - rlo;
             if (len > 0) {
                 const int64_t st = A.cp[k] + rlo;
@@ -1183,7 +1320,7 @@ __global__ void __launch_bounds__(NT) k_item_values_rank(ValueArgs g, const Rank
     // (the last chunk of an item ends at the item's last row block, which can lie
     // past the matrix's last 4096-row block when nrows is not a multiple of 2^TL)
     const int ts0 = min((it.y << (g.TL - g.VTL)) + ch.b0, g.Tv), ts1 = min((it.y << (g.TL - g.VTL)) + ch.b1, g.Tv);
-    value_walk<SRID, NT>(g.A, g.B, g.Atpv, g.Tv, ts0, j, sh, slot, ts1, g.arv);
+    value_walk<SRID, NT>(g.A, g.B, g.Atpv, g.Tv, ts0, j, sh, slot, ts1, g.arv, g.tv_stride);
     T* Cv = static_cast<T*>(g.cv);
     for (int q = tid; q < n; q += NT) Cv[lo + q] = S_::out(val[q]);
 }
@@ -1252,6 +1389,105 @@ __global__ void k_tile_ptr(DevCsc A, int TL, int T, int32_t* __restrict__ Atp) {
         }
         Atp[x] = (int32_t)(lo - as);
     }
+}
+
+// Word form of A: entry p starts a new (column, 32-row word) pair.
+__global__ void k_word_flag(DevCsc A, int* __restrict__ flag) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t k = w0; k < A.ncols; k += nw) {
+        const int64_t s = A.cp[k], e = A.cp[k + 1];
+        for (int64_t p = s + lane; p < e; p += 32)
+            flag[p - A.base] = (p == s) || ((A.rw[p] >> 5) != (A.rw[p - 1] >> 5));
+    }
+}
+
+// ex = exclusive scan of flag (span + 1 entries): word entry of p is
+// ex[p] + flag[p] - 1; its mask is the OR of its rows' bits.
+__global__ void k_word_fill(DevCsc A, const int* __restrict__ ex, const int* __restrict__ flag, int2* __restrict__ Aw) {
+    for (int64_t x = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < A.span; x += int64_t(gridDim.x) * blockDim.x) {
+        const int r = A.rw[A.base + x];
+        const int idx = ex[x] + flag[x] - 1;
+        if (flag[x]) Aw[idx].x = r >> 5;
+        atomicOr(reinterpret_cast<unsigned*>(&Aw[idx].y), 1u << (r & 31));
+    }
+}
+
+__global__ void k_word_cp(int64_t ncols, const int64_t* __restrict__ cp, int64_t base, const int* __restrict__ ex,
+                          int64_t* __restrict__ Awcp) {
+    for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k <= ncols; k += int64_t(gridDim.x) * blockDim.x)
+        Awcp[k] = ex[cp[k] - base];
+}
+
+// Word tile pointers: first word entry of column k with word >= t << (TL-5).
+__global__ void k_word_tile_ptr(int64_t ncols, const int64_t* __restrict__ Awcp, const int2* __restrict__ Aw, int TL,
+                                int T, int32_t* __restrict__ Atp) {
+    const int64_t n = ncols * int64_t(T + 1);
+    for (int64_t x = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < n; x += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t k = x / (T + 1);
+        const int t = (int)(x - k * (T + 1));
+        const int64_t as = Awcp[k], ae = Awcp[k + 1];
+        int64_t lo = as, hi = ae;
+        if (t == 0) {
+            hi = as;
+        } else if (t == T) {
+            lo = ae;
+        } else {
+            const int bound = t << (TL - 5);
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (Aw[mid].x < bound)
+                    lo = mid + 1;
+                else
+                    hi = mid;
+            }
+        }
+        Atp[x] = (int32_t)(lo - as);
+    }
+}
+
+// Tile-major layout of the same table: AtpT[t][k], t = 0..T (one row of
+// A.ncols entries per tile boundary).
+__global__ void k_tile_ptr_t(DevCsc A, int TL, int T, int32_t* __restrict__ AtpT) {
+    const int64_t n = A.ncols * int64_t(T + 1);
+    for (int64_t x = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < n; x += int64_t(gridDim.x) * blockDim.x) {
+        const int t = (int)(x / A.ncols);
+        const int64_t k = x - int64_t(t) * A.ncols;
+        const int64_t as = A.cp[k], ae = A.cp[k + 1];
+        int64_t lo = as, hi = ae;
+        if (t == 0) {
+            hi = as;
+        } else if (t == T) {
+            lo = ae;
+        } else {
+            const int64_t bound = int64_t(t) << TL;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (A.rw[mid] < bound)
+                    lo = mid + 1;
+                else
+                    hi = mid;
+            }
+        }
+        AtpT[x] = (int32_t)(lo - as);
+    }
+}
+
+// Rank chunks in row-block order (key = absolute first 4096-row block), so
+// the CTAs running together share A's rows and the table's rows in L2.
+__global__ void k_chunk_keys(int64_t n, const RankChunk* __restrict__ ch, const int2* __restrict__ items, int TL,
+                             int* __restrict__ key, int* __restrict__ idx) {
+    for (int64_t x = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < n; x += int64_t(gridDim.x) * blockDim.x) {
+        key[x] = (items[ch[x].item].y << (TL - 12)) + ch[x].b0;
+        idx[x] = (int)x;
+    }
+}
+
+__global__ void k_chunk_gather(int64_t n, const RankChunk* __restrict__ in, const int* __restrict__ order,
+                               RankChunk* __restrict__ out) {
+    for (int64_t x = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < n; x += int64_t(gridDim.x) * blockDim.x)
+        out[x] = in[order[x]];
 }
 
 __global__ void k_dense_flag(int64_t nkt, int T, const int32_t* __restrict__ Atp, int dmin, int* __restrict__ flag) {
@@ -1609,15 +1845,51 @@ static const int32_t* tile_pointers(Ctx& c, const DevCsc& A, uint64_t fp, int TL
     return d.atp.as<int32_t>();
 }
 
-// Tile pointers at the value-pass sub-tile height (cached like Atp).
-static const int32_t* value_tile_pointers(Ctx& c, const DevCsc& A, uint64_t fp, int VTL, int Tv) {
+// Word form of A and its tile pointers (cached like Atp, same fingerprint key).
+static const int32_t* word_pointers(Ctx& c, const DevCsc& A, uint64_t fp, int TL, int T) {
     DirectCache& d = c.direct;
-    if (d.atpv_valid && d.atpv_key == fp && d.atpv_ncols == A.ncols && d.atpv_tl == VTL && d.atpv_nnz == A.nnz)
+    if (d.aw_valid && d.aw_key == fp && d.aw_tl == TL && d.aw_ncols == A.ncols) return d.watp.as<int32_t>();
+    KScope ks(c, KC_BIN);
+    const int64_t span = A.span;
+    DevBuf flag(sizeof(int) * (span + 1), c.stream), ex(sizeof(int) * (span + 1), c.stream);
+    SLAPCU_CUDA(cudaMemsetAsync(flag.as<int>() + span, 0, sizeof(int), c.stream));
+    if (A.ncols)
+        launch(c, k_word_flag, dim3(grid_for(c, A.ncols * 32, 256)), dim3(256), 0, A, flag.as<int>());
+    excl_scan_i32(c, flag.as<int>(), ex.as<int>(), span + 1);
+    const int nw = d2h(c, ex.as<int>() + span);
+    d.aw.reset(sizeof(int2) * std::max(nw, 1), c.stream);
+    SLAPCU_CUDA(cudaMemsetAsync(d.aw.get(), 0, sizeof(int2) * std::max(nw, 1), c.stream));
+    if (span)
+        launch(c, k_word_fill, dim3(grid_for(c, span, 256)), dim3(256), 0, A, (const int*)ex.as<int>(),
+               (const int*)flag.as<int>(), d.aw.as<int2>());
+    d.awcp.reset(sizeof(int64_t) * (A.ncols + 1), c.stream);
+    launch(c, k_word_cp, dim3(grid_for(c, A.ncols + 1, 256)), dim3(256), 0, A.ncols, A.cp, A.base,
+           (const int*)ex.as<int>(), d.awcp.as<int64_t>());
+    d.watp.reset(sizeof(int32_t) * size_t(A.ncols) * (T + 1), c.stream);
+    launch(c, k_word_tile_ptr, dim3(grid_for(c, A.ncols * (T + 1), 256)), dim3(256), 0, A.ncols,
+           (const int64_t*)d.awcp.as<int64_t>(), (const int2*)d.aw.as<int2>(), TL, T, d.watp.as<int32_t>());
+    d.aw_key = fp;
+    d.aw_tl = TL;
+    d.aw_ncols = A.ncols;
+    d.aw_valid = true;
+    return d.watp.as<int32_t>();
+}
+
+// Tile pointers at the value-pass sub-tile height (cached like Atp).
+static const int32_t* value_tile_pointers(Ctx& c, const DevCsc& A, uint64_t fp, int VTL, int Tv, bool tmajor = false) {
+    DirectCache& d = c.direct;
+    if (d.atpv_valid && d.atpv_key == fp && d.atpv_ncols == A.ncols && d.atpv_tl == VTL && d.atpv_nnz == A.nnz &&
+        d.atpv_tmajor == tmajor)
         return d.atpv.as<int32_t>();
     d.atpv.reset(sizeof(int32_t) * size_t(A.ncols) * (Tv + 1), c.stream);
     KScope ks(c, KC_BIN);
-    launch(c, k_tile_ptr, dim3(grid_for(c, A.ncols * (Tv + 1), 256)), dim3(256), 0, A, VTL, Tv,
-           d.atpv.as<int32_t>());
+    if (tmajor)
+        launch(c, k_tile_ptr_t, dim3(grid_for(c, A.ncols * (Tv + 1), 256)), dim3(256), 0, A, VTL, Tv,
+               d.atpv.as<int32_t>());
+    else
+        launch(c, k_tile_ptr, dim3(grid_for(c, A.ncols * (Tv + 1), 256)), dim3(256), 0, A, VTL, Tv,
+               d.atpv.as<int32_t>());
+    d.atpv_tmajor = tmajor;
     d.atpv_key = fp;
     d.atpv_ncols = A.ncols;
     d.atpv_nnz = A.nnz;
@@ -1720,8 +1992,11 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
     d.hcnt.reset(sizeof(unsigned long long) * std::max<int64_t>(n, 1), c.stream);
     SLAPCU_CUDA(cudaMemsetAsync(d.hcnt.get(), 0, sizeof(unsigned long long) * std::max<int64_t>(n, 1), c.stream));
     int nitems = 0;
+    // words mode: the form walks A's (word, mask) pairs (one shared update
+    // per distinct word of a run) instead of its rows
+    const bool words = c.opt.direct_words != 0 && A.span < INT32_MAX;
     if (nh > 0) {
-        const int32_t* Atp = tile_pointers(c, A, afp, TL, T);
+        const int32_t* Atp = words ? word_pointers(c, A, afp, TL, T) : tile_pointers(c, A, afp, TL, T);
         KScope ks(c, KC_BIN);
         DevBuf hflag(sizeof(int) * (n + 1), c.stream), hpre(sizeof(int) * (n + 1), c.stream);
         launch(c, k_mark_heavy, dim3(grid_for(c, n, 256)), dim3(256), 0, n, flops, lmax, spec.all_heavy != 0,
@@ -1831,13 +2106,14 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
             d.rbc.reset(sizeof(int) * size_t(nitems) * nrb, c.stream);
             rbc = d.rbc.as<int>();
         }
-        const DenseRuns dr{d.ndense > 0 ? (const int*)d.dslot.as<int>() : nullptr,
-                           (const unsigned*)d.dbm.as<unsigned>(), d.ndense > 0 ? d.dense_min : 0};
+        const DenseRuns dr{(!words && d.ndense > 0) ? (const int*)d.dslot.as<int>() : nullptr,
+                           (const unsigned*)d.dbm.as<unsigned>(), (!words && d.ndense > 0) ? d.dense_min : 0};
         FormArgs g{A, B, Atp, dr, T, TL, (const int2*)d.items.as<int2>(), (const int4*)d.units.as<int4>(),
                    (const int*)d.order.as<int>(), d.stash.as<unsigned>(), (const int64_t*)d.soff.as<int64_t>(),
                    (const int64_t*)d.sres.as<int64_t>(), d.partial.as<unsigned>(), d.cnt.as<int64_t>(),
                    d.form.as<int>(), d.hcnt.as<unsigned long long>(), nullptr, 0, rbc,
-                   c.opt.direct_quads, c.opt.direct_short_run > 0 ? c.opt.direct_short_run : kShortRun};
+                   c.opt.direct_quads, c.opt.direct_short_run > 0 ? c.opt.direct_short_run : kShortRun,
+                   words ? (const int2*)d.aw.as<int2>() : nullptr, words ? (const int64_t*)d.awcp.as<int64_t>() : nullptr};
         const size_t smem = sizeof(unsigned) * (W + W / 32) + sizeof(uint16_t) * W;
         DevBuf tick(sizeof(int), c.stream);
         SLAPCU_CUDA(cudaMemsetAsync(tick.get(), 0, sizeof(int), c.stream));
@@ -1852,7 +2128,10 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
             launch(c, kf, dim3((unsigned)grid), dim3(nt), smem, g);
         };
         const int ft = c.opt.direct_form_threads;
-        if (c.opt.direct_form_walk == 1)
+        if (words)
+            c.opt.direct_form_walk == 1 ? form(k_tile_form<256, 0, true, true>, 256)
+                                        : form(k_tile_form<256, 0, false, true>, 256);
+        else if (c.opt.direct_form_walk == 1)
             form(k_tile_form<256, 0, true>, 256);
         else if (c.opt.direct_mark_mode == 2)
             form(k_tile_form<256, 2>, 256);
@@ -1942,7 +2221,7 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
         SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
         ValueArgs va{A, B, Atpv, Tv, VTL, TL, Atp, T, (const int2*)d.items.as<int2>(), nullptr,
                      (const int64_t*)d.cnt.as<int64_t>(), (const int64_t*)d.hoff.as<int64_t>(),
-                     (const int64_t*)d.lp.as<int64_t>(), (const int*)d.rbc.as<int>(), crw, cv, nullptr};
+                     (const int64_t*)d.lp.as<int64_t>(), (const int*)d.rbc.as<int>(), crw, cv, nullptr, 0};
         // 4-byte values: A's rows and values interleaved, so a product's gather
         // is one 8-byte load (one sector) instead of one from each array
         DevBuf arv;
@@ -1981,9 +2260,11 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
                 const int cap = c.opt.direct_value_rank > 0 ? c.opt.direct_value_rank : (sizeof(Acc) <= 4 ? 8192 : 4096);
                 const int T12 = (int)((A.nrows + 4095) >> 12);
                 ValueArgs vr = va;
-                vr.Atpv = value_tile_pointers(c, A, afp, 12, T12);
+                const bool tmajor = c.opt.direct_value_tmajor != 0;
+                vr.Atpv = value_tile_pointers(c, A, afp, 12, T12, tmajor);
                 vr.Tv = T12;
                 vr.VTL = 12;
+                vr.tv_stride = tmajor ? A.ncols : 0;
                 const int nrb = (W + kRbcWords - 1) / kRbcWords;
                 DevBuf ccount(sizeof(int64_t) * (size_t(nsl[1]) + 1), c.stream),
                     coff(sizeof(int64_t) * (size_t(nsl[1]) + 1), c.stream);
@@ -1997,6 +2278,27 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
                 launch(c, k_rank_chunks, dim3(grid_for(c, nsl[1], 256)), dim3(256), 0, nsl[1], (const int*)large,
                        (const int*)d.rbc.as<int>(), nrb, cap, (const int64_t*)coff.as<int64_t>(), ccount.as<int64_t>(),
                        chunks.as<RankChunk>());
+                if (c.opt.direct_value_tmajor && nch > 1) {  // row-block order (L2 locality of A and the table)
+                    DevBuf key(sizeof(int) * nch, c.stream), kout(sizeof(int) * nch, c.stream),
+                        idx(sizeof(int) * nch, c.stream), ord(sizeof(int) * nch, c.stream),
+                        sorted(sizeof(RankChunk) * nch, c.stream);
+                    launch(c, k_chunk_keys, dim3(grid_for(c, nch, 256)), dim3(256), 0, nch,
+                           (const RankChunk*)chunks.as<RankChunk>(), (const int2*)d.items.as<int2>(), TL, key.as<int>(),
+                           idx.as<int>());
+                    size_t tb = 0;
+                    SLAPCU_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, key.as<int>(), kout.as<int>(), idx.as<int>(),
+                                                                ord.as<int>(), (int)nch, 0, 31, c.stream));
+                    DevBuf tmp(tb, c.stream);
+                    timed(c, KC_BIN, [&] {
+                        SLAPCU_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, key.as<int>(), kout.as<int>(),
+                                                                    idx.as<int>(), ord.as<int>(), (int)nch, 0, 31,
+                                                                    c.stream));
+                    });
+                    ++c.launches;
+                    launch(c, k_chunk_gather, dim3(grid_for(c, nch, 256)), dim3(256), 0, nch,
+                           (const RankChunk*)chunks.as<RankChunk>(), (const int*)ord.as<int>(), sorted.as<RankChunk>());
+                    chunks = std::move(sorted);
+                }
                 const size_t smem = ((sizeof(Acc) * size_t(cap) + 15) & ~size_t(15)) + sizeof(unsigned) * W +
                                     sizeof(uint16_t) * W + sizeof(int) * (W / 32) + 16;
                 auto gor = [&](auto k, int nt) {

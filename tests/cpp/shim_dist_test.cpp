@@ -86,7 +86,9 @@ void check_2d(int p, const SR& sr, Val val, bool exact, std::uint64_t seed) {
         auto cw = slap::dist_symbolic_col_nnz(a, b);
         auto cg = slapcu_slap::dist_symbolic_col_nnz(a, b);
         if (cw != cg) fail("dist_symbolic_col_nnz", p);
-        const std::int64_t budget = 16 * 40;
+        std::int64_t cmax = 1;
+        for (auto x : cw) cmax = std::max(cmax, x);
+        const std::int64_t budget = 16 * 3 * cmax;  // a few batches
         auto pw = slap::plan_batches_by_budget(a, b, budget);
         auto pg = slapcu_slap::plan_batches_by_budget(a, b, budget);
         if (pw.col_ranges != pg.col_ranges || pw.est_entries != pg.est_entries) fail("plan_batches_by_budget", p);

@@ -61,19 +61,22 @@ def test_direct_bool_rmat(port, scale, mode, quads, emit):
     assert_parity(got, want, oracle.OR_AND_U8, f"s{scale} mode {mode} quads {quads} emit {emit}")
 
 
+@pytest.mark.parametrize("words", [0, 1])
 @pytest.mark.parametrize("walk", [0, 1])
 @pytest.mark.parametrize("tile_major", [0, 1])
 @pytest.mark.parametrize("dense_run", [0, 64])
 @pytest.mark.parametrize("scale", [11, 14])
-def test_direct_form_variants(port, scale, walk, tile_major, dense_run):
-    """Form kernel variants: warp-independent walk and tile-major unit order
-    (with split items: split threshold 4096), Boolean and MinPlus."""
+def test_direct_form_variants(port, scale, walk, tile_major, dense_run, words):
+    """Form kernel variants: packed long runs, tile-major unit order, the
+    word form of A (with split items: split threshold 4096), Boolean and
+    MinPlus."""
     for sr, kind in ((P.OrAnd, 0), (P.MinPlusI32, 3)):
         a = port.gen_rmat(scale)
         a = a.with_vals(port.fill_values(sr.id, kind, a))
         want = port.spgemm(sr.id, a, a)
         ctx = P.Context()
         ctx.set_option(L.OPT_DIRECT_FORM_WALK, walk)
+        ctx.set_option(L.OPT_DIRECT_WORDS, words)
         ctx.set_option(L.OPT_DIRECT_TILE_MAJOR, tile_major)
         ctx.set_option(L.OPT_DIRECT_DENSE_RUN_MIN, dense_run)
         ctx.set_option(L.OPT_DIRECT_TILE_ROWS_LOG2, 11)
@@ -126,6 +129,22 @@ def test_direct_value_pass(port, sr, vtl, hash_, rank):
     ctx.set_option(L.OPT_DIRECT_SPLIT_FLOPS, 4096)
     got = P.local_spgemm(to_device(a), to_device(a), sr, ctx=ctx, method="direct")
     assert_parity(got, want, sr.id, f"{sr.name} vtl={vtl}")
+
+
+@pytest.mark.parametrize("tmajor", [0, 1])
+@pytest.mark.parametrize("sr", [P.PlusTimesF64, P.PlusTimesF32, P.MinPlusI32, P.PlusTimesI64],
+                         ids=lambda s: f"{s.name}_{s.dtype}")
+def test_direct_value_tmajor(port, sr, tmajor):
+    """Value pass with the tile-major 4096-row pointer table and rank chunks
+    in row-block order (and without): same output."""
+    a = with_values(port, port.gen_rmat(14), sr.id)
+    want = port.spgemm(sr.id, a, a)
+    ctx = P.Context()
+    ctx.set_option(L.OPT_DIRECT_VALUE_TMAJOR, tmajor)
+    ctx.set_option(L.OPT_DIRECT_VALUE_HASH, 0)
+    ctx.set_option(L.OPT_DIRECT_TILE_ROWS_LOG2, 13)
+    got = P.local_spgemm(to_device(a), to_device(a), sr, ctx=ctx, method="direct")
+    assert_parity(got, want, sr.id, f"{sr.name} tmajor={tmajor}")
 
 
 @pytest.mark.parametrize("interleave", [0, 1, 2])

@@ -45,10 +45,11 @@ def test_value_pass_ragged_row_count(port, nrows, sr):
     b = random_csc(rng, 1500, 300, 5, 80)
     b = b.with_vals(port.fill_values(sr.id, kind, b))
     want = port.spgemm(sr.id, a, b)
-    for rank in (-1, 4096):  # default chunk (8192 for 4-byte, 4096 for 8-byte accumulators) and 4096
+    for rank, tmajor in ((-1, 0), (4096, 0), (-1, 1)):  # default chunk (8192 / 4096 by width), 4096; tile-major
         ctx = P.Context()
         if rank > 0:
             ctx.set_option(L.OPT_DIRECT_VALUE_RANK, rank)
+        ctx.set_option(L.OPT_DIRECT_VALUE_TMAJOR, tmajor)
         got = P.local_spgemm(to_device(a), to_device(b), sr, ctx=ctx, method="direct")
         assert_parity(got, want, sr.id, f"nrows={nrows} rank={rank}")
 
