@@ -113,7 +113,10 @@ typedef enum {
     SLAPCU_OPT_SYM_TILE_ROWS_LOG2 = 1,/* row-tile height of the symbolic bitmap    (default 19) */
     SLAPCU_OPT_LIGHT_NNZ_MAX = 2,     /* numeric: columns above this use the dense tile path */
     SLAPCU_OPT_LIGHT_FLOPS_MAX = 3,   /* symbolic: columns above this use the bitmap path   */
-    SLAPCU_OPT_DETERMINISTIC = 4,     /* reserved */
+    SLAPCU_OPT_DETERMINISTIC = 4,     /* 1: floating-point semirings fold every output entry in the
+                                         reference's order (ascending k, spgemm.hpp:156-159, :251-255) on
+                                         the ESC path -- bit-identical to slap::local_spgemm and run-to-run
+                                         reproducible; 0 (default): semiring atomics, within tolerance */
     SLAPCU_OPT_PROFILE = 5,           /* 1: CUDA events around every launch, per-class device time */
     SLAPCU_OPT_DENSE_FLOPS_MIN = 6,   /* fused path: byte-flag tiles for columns with flops >= v
                                          (-1 auto = nrows/4, 0 = off) */
@@ -169,8 +172,10 @@ typedef enum {
                                               are walked by their own thread (0 = default 8) */
     SLAPCU_OPT_DIRECT_VALUE_TMAJOR = 26,   /* direct path value pass: 1 = 4096-row tile pointers stored
                                               tile-major and rank chunks run in row-block order */
-    SLAPCU_OPT_DIRECT_WORDS = 27           /* direct path form: 1 = walk A as (32-row word, row mask) pairs
+    SLAPCU_OPT_DIRECT_WORDS = 27,          /* direct path form: 1 = walk A as (32-row word, row mask) pairs
                                               (built per A): one shared update per distinct word of a run */
+    SLAPCU_OPT_DIRECT_ESC = 28             /* direct path: 1 = every semiring on the ESC (expand, stable
+                                              segmented sort, left fold) path; 0 = bitmap / hash paths */
 } slapcu_option;
 slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t value);
 

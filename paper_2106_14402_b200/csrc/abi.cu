@@ -215,7 +215,8 @@ slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t v
             c.opt.light_flops_max = v;
             c.opt.direct_light_flops_max = v;
             break;
-        case SLAPCU_OPT_DETERMINISTIC: break;
+        case SLAPCU_OPT_DETERMINISTIC: c.opt.deterministic = v != 0; break;
+        case SLAPCU_OPT_DIRECT_ESC: c.opt.direct_esc = (int)v; break;
         case SLAPCU_OPT_DENSE_FLOPS_MIN: c.opt.dense_flops_min = v; break;
         case SLAPCU_OPT_ASYNC_FINISH: c.opt.async_finish = v != 0; break;
         case SLAPCU_OPT_DENSE_TILE_ROWS_LOG2:

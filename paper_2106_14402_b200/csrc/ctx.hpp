@@ -136,10 +136,12 @@ struct Options {
     int direct_value_rank = -1;  // value pass: large items by rank chunks of this many outputs (0 = sub-tiles,
                                  // -1 = by accumulator width: 8192 for 4-byte, 4096 for 8-byte)
     int direct_emit_blocks = 0;             // emit: one warp per (item, block) (1) or one CTA per item (0)
-    int direct_tile_major = 0;              // form: work units ordered by row tile, then heaviest first
+    int direct_tile_major = 1;              // form: work units ordered by row tile, then heaviest first
     int direct_form_walk = 0;               // form: long runs as 256-product units (0) or packed products (1)
-    int direct_words = 0;                   // form: walk A's (32-row word, mask) pairs instead of its rows
-    int direct_value_tmajor = 0;            // value pass: tile-major 4096-row pointer table + chunks in row order
+    int deterministic = 0;                  // 1: every product by ESC (the reference's fold order, bit-exact fp)
+    int direct_esc = 0;                     // 1: ESC for every semiring (sort-merge path), 0: bitmap / hash paths
+    int direct_words = 1;                   // form: walk A's (32-row word, mask) pairs instead of its rows
+    int direct_value_tmajor = 1;            // value pass: tile-major 4096-row pointer table + chunks in row order
     int direct_short_run = 0;               // form: runs shorter than this walked per thread (0 = default 8)
     int direct_persistent = 1;              // form kernel: persistent CTAs (1) or one CTA per unit (0)
     int direct_form_threads = 256;          // CTA size of the form kernel (128, 256, 512)
@@ -260,6 +262,9 @@ bool direct_exact(Ctx& c, const DevCsc& A, const DevCsc& B, int sr, int alg, int
 int64_t batched_host(Ctx& c, const slapcu_host_csc& A, const slapcu_host_csc& B, int sr, int alg, int nranges,
                      const int64_t* ranges, int64_t budget, slapcu_batch_consumer consumer, void* user);
 void free_host_cache(Ctx& c);
+// esc.cu: expand / stable segmented sort / left fold (reference fold order)
+int64_t esc_spgemm(Ctx& c, const DevCsc& A, const DevCsc& B, int sr, int64_t capacity, int64_t* c_colptr, int32_t* crw,
+                   void* cv);
 int64_t direct_spgemm(Ctx& c, const DevCsc& A, const DevCsc& B, int sr, int alg, int64_t capacity, int64_t* c_colptr,
                       int32_t* c_rowids, void* c_vals);
 void any_zero_u8(Ctx& c, const uint8_t* v, int64_t n, int* flag);

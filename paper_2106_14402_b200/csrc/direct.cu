@@ -1279,10 +1279,26 @@ __global__ void __launch_bounds__(NT) k_item_values_rank(ValueArgs g, const Rank
             sh.nlong = 0;
         }
     }
-    for (int q = tid; q < nwords; q += NT) bm[q] = 0u;
+    // dense chunks (their rows fit the value array): values indexed by row
+    // offset -- no bitmap, no ranks, one shared atomic per product
+    const bool dense = nwords * 32 <= cap;
+    if (!dense)
+        for (int q = tid; q < nwords; q += NT) bm[q] = 0u;
+    else
+        for (int q = tid; q < nwords * 32; q += NT) val[q] = S_::identity();
     __syncthreads();
     const int64_t lo = range_sh[0], hi = range_sh[1];
     const int n = (int)(hi - lo);
+    // (the last chunk of an item ends at the item's last row block, which can lie
+    // past the matrix's last 4096-row block when nrows is not a multiple of 2^TL)
+    const int ts0 = min((it.y << (g.TL - g.VTL)) + ch.b0, g.Tv), ts1 = min((it.y << (g.TL - g.VTL)) + ch.b1, g.Tv);
+    T* Cv = static_cast<T*>(g.cv);
+    if (dense) {
+        value_walk<SRID, NT>(g.A, g.B, g.Atpv, g.Tv, ts0, j, sh, [val, r0](int r) { return &val[r - r0]; }, ts1, g.arv,
+                             g.tv_stride);
+        for (int q = tid; q < n; q += NT) Cv[lo + q] = S_::out(val[g.crw[lo + q] - r0]);
+        return;
+    }
     for (int q = tid; q < n; q += NT) {
         const int rr = g.crw[lo + q] - r0;
         atomicOr(&bm[rr >> 5], 1u << (rr & 31));
@@ -1317,11 +1333,7 @@ __global__ void __launch_bounds__(NT) k_item_values_rank(ValueArgs g, const Rank
         const int w = rr >> 5;
         return &val[gbase[w >> 5] + pre16[w] + __popc(bm[w] & ((1u << (rr & 31)) - 1u))];
     };
-    // (the last chunk of an item ends at the item's last row block, which can lie
-    // past the matrix's last 4096-row block when nrows is not a multiple of 2^TL)
-    const int ts0 = min((it.y << (g.TL - g.VTL)) + ch.b0, g.Tv), ts1 = min((it.y << (g.TL - g.VTL)) + ch.b1, g.Tv);
     value_walk<SRID, NT>(g.A, g.B, g.Atpv, g.Tv, ts0, j, sh, slot, ts1, g.arv, g.tv_stride);
-    T* Cv = static_cast<T*>(g.cv);
     for (int q = tid; q < n; q += NT) Cv[lo + q] = S_::out(val[q]);
 }
 
@@ -1924,6 +1936,18 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
     resolve(c, B);
     if ((A.span && !A.v) || (B.span && !B.v)) throw Fail{SLAPCU_ERR_INVALID, "operand values are null"};
     ctx_settle(c);
+    // sort-merge (ESC) path: the reference's fold order for every output entry
+    // (bit-exact floating point), or forced for any semiring
+    const bool fp = sr == SLAPCU_PLUS_TIMES_F64 || sr == SLAPCU_PLUS_TIMES_F32 || sr == SLAPCU_MIN_PLUS_F64;
+    if ((c.opt.deterministic && fp) || c.opt.direct_esc == 1) {
+        SLAPCU_CUDA(cudaEventRecord(c.ev[0], c.stream));
+        const int64_t nz = esc_spgemm(c, A_, B_, sr, capacity, c_colptr, crw, cv);
+        SLAPCU_CUDA(cudaEventRecord(c.ev[1], c.stream));
+        SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+        cudaEventElapsedTime(&c.sym_ms, c.ev[0], c.ev[1]);
+        prof_flush(c);
+        return nz;
+    }
     if (c.opt.direct_values_fallback && sr != SLAPCU_OR_AND_U8)
         return direct_fallback(c, A_, B_, sr, alg, capacity, c_colptr, crw, cv);
     // OrAnd: if no stored value is 0 every product is 1 (pattern only, values

@@ -1,0 +1,225 @@
+// esc.cu -- expand / sort / compress (ESC) product: the sort-merge path for
+// low-compression columns and the deterministic (reference-order) fold.
+//
+// Per output column j every product A(i,k) * B(k,j) is written out in the
+// reference's enumeration order (B(:,j) entries ascending in k, then A(:,k)
+// ascending in i), the column's products are sorted by row with a STABLE
+// segmented radix sort, and each run of equal rows is folded left to right
+// with the semiring add.  That is exactly the reference's per-entry fold
+// order (heap: ties by stream = ascending k, spgemm.hpp:156-159; hash:
+// upserts in B-column order, spgemm.hpp:251-255), so floating-point
+// PlusTimes comes out BIT-identical to slap::local_spgemm, not just within
+// tolerance -- the atomics of the bitmap / hash paths fold in arrival order.
+// The cost is ~(8 + 2 sizeof(value)) bytes per product moved a few times
+// (expand, 3 radix passes over 20-22-bit row keys, fold), which is the cheaper
+// side when the compression factor flops / nnz(C) is near 1 (configs C2, C5)
+// and the price of determinism elsewhere.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "kern.cuh"
+
+namespace slapcu {
+
+namespace {
+
+// Products of each B entry of columns [j0, j1): nnz(A(:,k)).
+__global__ void k_entry_len(DevCsc A, DevCsc B, int64_t e0, int64_t ne, int64_t* __restrict__ len) {
+    for (int64_t x = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < ne; x += int64_t(gridDim.x) * blockDim.x) {
+        const int k = B.rw[e0 + x];
+        len[x] = A.cp[k + 1] - A.cp[k];
+    }
+}
+
+// Expand: one warp per B entry (grid-stride), lane-strided over A(:,k).
+template <int SRID>
+__global__ void k_expand(DevCsc A, DevCsc B, int64_t e0, int64_t ne, const int64_t* __restrict__ eoff,
+                         int* __restrict__ keys, typename Sr<SRID>::Acc* __restrict__ vals) {
+    using S_ = Sr<SRID>;
+    using T = typename S_::T;
+    const T* Av = static_cast<const T*>(A.v);
+    const T* Bv = static_cast<const T*>(B.v);
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t x = w0; x < ne; x += nw) {
+        const int k = B.rw[e0 + x];
+        const T b = Bv[e0 + x];
+        const int64_t s = A.cp[k], e = A.cp[k + 1];
+        const int64_t o = eoff[x];
+        for (int64_t p = s + lane; p < e; p += 32) {
+            keys[o + (p - s)] = A.rw[p];
+            vals[o + (p - s)] = S_::mul(Av[p], b);
+        }
+    }
+}
+
+// Segment (column) begin/end offsets of the group's products.
+__global__ void k_seg_bounds(int64_t ncols, const int64_t* __restrict__ Bcp, int64_t e0, const int64_t* __restrict__ eoff,
+                             int* __restrict__ beg, int* __restrict__ end) {
+    for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < ncols; j += int64_t(gridDim.x) * blockDim.x) {
+        beg[j] = (int)eoff[Bcp[j] - e0];
+        end[j] = (int)eoff[Bcp[j + 1] - e0];
+    }
+}
+
+// Run heads: first product of a column segment, or a row differing from its predecessor.
+__global__ void k_seg_mark(int64_t ncols, const int* __restrict__ beg, const int* __restrict__ end,
+                           int* __restrict__ head) {
+    for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < ncols; j += int64_t(gridDim.x) * blockDim.x)
+        if (end[j] > beg[j]) head[beg[j]] = 1;
+}
+
+__global__ void k_run_heads(int64_t P, const int* __restrict__ keys, int* __restrict__ head) {
+    for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < P; p += int64_t(gridDim.x) * blockDim.x)
+        if (p > 0 && keys[p] != keys[p - 1]) head[p] = 1;
+}
+
+// Fold each run left to right (the reference's order) and write (row, value).
+template <int SRID>
+__global__ void k_fold(int64_t P, const int* __restrict__ keys, const typename Sr<SRID>::Acc* __restrict__ vals,
+                       const int* __restrict__ head, const int* __restrict__ ex, int64_t obase, int32_t* __restrict__ crw,
+                       typename Sr<SRID>::T* __restrict__ cv) {
+    using S_ = Sr<SRID>;
+    for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < P; p += int64_t(gridDim.x) * blockDim.x) {
+        if (!head[p]) continue;
+        typename S_::Acc acc = vals[p];
+        for (int64_t q = p + 1; q < P && !head[q]; ++q) acc = S_::add(acc, vals[q]);
+        const int64_t o = obase + ex[p];
+        crw[o] = keys[p];
+        cv[o] = S_::out(acc);
+    }
+}
+
+__global__ void k_esc_colptr(int64_t ncols, const int* __restrict__ beg, const int* __restrict__ ex, int64_t obase,
+                             int64_t* __restrict__ cp) {
+    for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < ncols; j += int64_t(gridDim.x) * blockDim.x)
+        cp[j] = obase + ex[beg[j]];
+}
+
+template <class T>
+T d2h1(Ctx& c, const T* p) {
+    T v{};
+    SLAPCU_CUDA(cudaMemcpyAsync(&v, p, sizeof(T), cudaMemcpyDeviceToHost, c.stream));
+    SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+    return v;
+}
+
+}  // namespace
+
+// C = A * B by ESC into caller buffers (capacity entries); returns nnz(C).
+// Columns are processed in groups of at most `group_max` products (int32
+// sort offsets; bounded scratch).  BudgetError (exact nnz in c.direct.last_nnz)
+// when C needs more than `capacity` entries -- nothing past capacity is written.
+int64_t esc_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int64_t capacity, int64_t* c_colptr,
+                   int32_t* crw, void* cv) {
+    check_operands(A_, B_);
+    DevCsc A = A_, B = B_;
+    resolve(c, A);
+    resolve(c, B);
+    const int64_t n = B.ncols;
+    // per-column products, on the host for grouping
+    DevBuf fl(sizeof(int64_t) * std::max<int64_t>(n, 1), c.stream);
+    int64_t total = 0;
+    spgemm_flops(c, A, B, fl.as<int64_t>(), &total);
+    std::vector<int64_t> hf(size_t(std::max<int64_t>(n, 1)));
+    if (n) SLAPCU_CUDA(cudaMemcpyAsync(hf.data(), fl.get(), sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c.stream));
+    std::vector<int64_t> hbcp(size_t(n) + 1);
+    SLAPCU_CUDA(cudaMemcpyAsync(hbcp.data(), B.cp, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, c.stream));
+    SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+    size_t fr = 0, tot = 0;
+    SLAPCU_CUDA(cudaMemGetInfo(&fr, &tot));
+    const int vs = value_size(sr);
+    const int64_t per_prod = 4 * 4 + 2 * 8;  // keys x2, head, ex, values x2 (<= 8 bytes each)
+    const int64_t group_max = std::max<int64_t>(1, std::min<int64_t>(int64_t(1) << 30, int64_t(fr / 3) / per_prod));
+    int64_t obase = 0;
+    int64_t j0 = 0;
+    bool over = false;  // past capacity: keep counting for the exact requirement, write nothing
+    dispatch_sr(sr, [&](auto idc) {
+        constexpr int ID = decltype(idc)::value;
+        using Acc = typename Sr<ID>::Acc;
+        using T = typename Sr<ID>::T;
+        while (j0 < n) {
+            // the group: columns [j0, j1) with at most group_max products (a single larger column is an error)
+            int64_t j1 = j0, P = 0;
+            while (j1 < n && (j1 == j0 || P + hf[j1] <= group_max)) P += hf[j1++];
+            if (P > INT32_MAX)
+                throw Fail{SLAPCU_ERR_BUDGET, "ESC: column " + std::to_string(j0) + " has " + std::to_string(P) +
+                                                  " products (int32 sort offsets)"};
+            const int64_t ng = j1 - j0;
+            const int64_t e0 = hbcp[j0], ne = hbcp[j1] - e0;
+            DevBuf len(sizeof(int64_t) * (ne + 1), c.stream), eoff(sizeof(int64_t) * (ne + 1), c.stream);
+            SLAPCU_CUDA(cudaMemsetAsync(len.as<int64_t>() + ne, 0, sizeof(int64_t), c.stream));
+            DevBuf k0(sizeof(int) * std::max<int64_t>(P, 1), c.stream), k1(sizeof(int) * std::max<int64_t>(P, 1), c.stream);
+            DevBuf v0(sizeof(Acc) * std::max<int64_t>(P, 1), c.stream), v1(sizeof(Acc) * std::max<int64_t>(P, 1), c.stream);
+            DevBuf beg(sizeof(int) * std::max<int64_t>(ng, 1), c.stream), end(sizeof(int) * std::max<int64_t>(ng, 1), c.stream);
+            DevBuf head(sizeof(int) * (P + 1), c.stream), ex(sizeof(int) * (P + 1), c.stream);
+            {
+                KScope ks(c, KC_SYM_HEAVY);
+                if (ne) {
+                    launch(c, k_entry_len, dim3(grid_for(c, ne, 256)), dim3(256), 0, A, B, e0, ne, len.as<int64_t>());
+                }
+                exclusive_scan_i64(c, len.as<int64_t>(), eoff.as<int64_t>(), ne + 1);
+                if (ne)
+                    launch(c, k_expand<ID>, dim3(grid_for(c, ne * 32, 256)), dim3(256), 0, A, B, e0, ne,
+                           (const int64_t*)eoff.as<int64_t>(), k0.as<int>(), v0.as<Acc>());
+                launch(c, k_seg_bounds, dim3(grid_for(c, ng, 256)), dim3(256), 0, ng, (const int64_t*)(B.cp + j0), e0,
+                       (const int64_t*)eoff.as<int64_t>(), beg.as<int>(), end.as<int>());
+                if (P) {
+                    size_t tb = 0;
+                    SLAPCU_CUDA(cub::DeviceSegmentedSort::StableSortPairs(
+                        nullptr, tb, k0.as<int>(), k1.as<int>(), v0.as<Acc>(), v1.as<Acc>(), (int)P, (int)ng,
+                        beg.as<int>(), end.as<int>(), c.stream));
+                    DevBuf tmp(tb, c.stream);
+                    timed(c, KC_SYM_HEAVY, [&] {
+                        SLAPCU_CUDA(cub::DeviceSegmentedSort::StableSortPairs(
+                            tmp.get(), tb, k0.as<int>(), k1.as<int>(), v0.as<Acc>(), v1.as<Acc>(), (int)P, (int)ng,
+                            beg.as<int>(), end.as<int>(), c.stream));
+                    });
+                    ++c.launches;
+                }
+                SLAPCU_CUDA(cudaMemsetAsync(head.get(), 0, sizeof(int) * (P + 1), c.stream));
+                launch(c, k_seg_mark, dim3(grid_for(c, ng, 256)), dim3(256), 0, ng, (const int*)beg.as<int>(),
+                       (const int*)end.as<int>(), head.as<int>());
+                if (P)
+                    launch(c, k_run_heads, dim3(grid_for(c, P, 256)), dim3(256), 0, P, (const int*)k1.as<int>(),
+                           head.as<int>());
+            }
+            {
+                KScope ks(c, KC_SCAN);
+                size_t tb = 0;
+                SLAPCU_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, head.as<int>(), ex.as<int>(), P + 1, c.stream));
+                DevBuf tmp(tb, c.stream);
+                timed(c, KC_SCAN, [&] {
+                    SLAPCU_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tb, head.as<int>(), ex.as<int>(), P + 1,
+                                                              c.stream));
+                });
+                ++c.launches;
+            }
+            const int64_t gnnz = d2h1(c, ex.as<int>() + P);
+            launch(c, k_esc_colptr, dim3(grid_for(c, ng, 256)), dim3(256), 0, ng, (const int*)beg.as<int>(),
+                   (const int*)ex.as<int>(), obase, c_colptr + j0);
+            if (obase + gnnz > capacity) over = true;
+            if (P && !over) {
+                KScope ks(c, KC_NUM_HEAVY);
+                launch(c, k_fold<ID>, dim3(grid_for(c, P, 256)), dim3(256), 0, P, (const int*)k1.as<int>(),
+                       (const Acc*)v1.as<Acc>(), (const int*)head.as<int>(), (const int*)ex.as<int>(), obase, crw,
+                       static_cast<T*>(cv));
+            }
+            obase += gnnz;
+            j0 = j1;
+        }
+    });
+    SLAPCU_CUDA(cudaMemcpyAsync(c_colptr + n, &obase, sizeof(int64_t), cudaMemcpyHostToDevice, c.stream));
+    SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+    c.direct.last_nnz = obase;
+    if (over)
+        throw Fail{SLAPCU_ERR_BUDGET, "output needs " + std::to_string(obase) + " entries, capacity " +
+                                          std::to_string(capacity)};
+    return obase;
+}
+
+}  // namespace slapcu

@@ -63,6 +63,8 @@ def main():
     ap.add_argument("--method", default="direct", choices=["direct", "fused", "two_pass"])
     ap.add_argument("--value-hash", type=int, default=None, help="value pass hash kernel for small items (0 off)")
     ap.add_argument("--value-interleave", type=int, default=None, help="value pass gathers interleaved: 0 off, 1 4-byte values, 2 all")
+    ap.add_argument("--opt", action="append", default=[],
+                    help="NAME=VALUE library option (e.g. DETERMINISTIC=1, DIRECT_ESC=1, DIRECT_WORDS=1)")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     stream = torch.cuda.current_stream()
@@ -73,6 +75,12 @@ def main():
     if args.value_interleave is not None:
         from paper_2106_14402_b200 import _lib as L
         ctx.set_option(L.OPT_DIRECT_VALUE_INTERLEAVE, args.value_interleave)
+    from paper_2106_14402_b200 import _lib as L
+    for kv in args.opt:
+        k, v = kv.split("=")
+        ctx.set_option(getattr(L, "OPT_" + k), int(v))
+    from bench import measured_peak_gbs
+    peak, peak_kind = measured_peak_gbs()
     threads = os.cpu_count() or 1
     for name in args.configs.split(","):
         desc, A, B, sr = workload(name, ctx)
@@ -104,6 +112,7 @@ def main():
         tol = 1e-12 if sr.dtype == "f64" else 1e-5
         gv, wv = gpu_slice.vals.astype(np.float64), want.vals.astype(np.float64)
         close = bool(np.all(np.abs(gv - wv) <= tol * np.maximum(1.0, np.maximum(np.abs(gv), np.abs(wv)))))
+        bitwise = bool(same_pattern and gpu_slice.vals.tobytes() == np.asarray(want.vals).tobytes())
         extra = {}
         if name == "C4":  # the whole Markov-clustering step around the expansion (algorithms.cpp:267-293)
             A = stochastic_with_loops(A, sr)  # mcl_step needs every column to sum to 1
@@ -117,16 +126,16 @@ def main():
             torch.cuda.synchronize()
             extra["mcl_step_ms"] = round(m0.elapsed_time(m1) / args.steps, 3)
             extra["mcl_step_input"] = "A + I (no empty column), values 1/deg(col), inflation 2, prune 1e-4"
-        peak = 6481.1
         vs = np.dtype(sr.np_dtype).itemsize
         step_bytes = sum(nz * (4 + vs) + (nc + 1) * 8 for nz, nc in ((A.nnz, A.ncols), (B.nnz, B.ncols), (nnz, B.ncols)))
         print(json.dumps({
             "config": name, "workload": desc, "gflops": round(2 * flops / (ms / 1e3) / 1e9, 3),
             "ms_per_product": round(ms, 3), "multiplies": int(flops), "nnz_C": int(nnz),
             "step_bytes_alg": int(step_bytes), "step_frac_hbm": round(step_bytes / (ms / 1e3) / 1e9 / peak, 5),
+            "peak_gbs": peak, "peak_source": peak_kind, "options": args.opt,
             "cpu_reference": {"gflops": round(2 * ref_fl / secs / 1e9, 4), "threads": threads,
                               "sample": f"columns [{c0},{c0 + w}) of B, {ref_fl} multiplies in {secs:.3f} s"},
-            "parity_slice": {"pattern_exact": same_pattern, f"values_rel_{tol}": close},
+            "parity_slice": {"pattern_exact": same_pattern, f"values_rel_{tol}": close, "values_bitwise": bitwise},
             **extra,
         }), flush=True)
         del A, B
