@@ -77,6 +77,8 @@ def parse():
     ap.add_argument("--short-run", type=int, default=None, help="direct path form: per-thread run threshold")
     ap.add_argument("--value-tmajor", type=int, default=None, help="direct value pass: tile-major table + row-order chunks")
     ap.add_argument("--words", type=int, default=None, help="direct form: walk A's (word, mask) pairs")
+    ap.add_argument("--value-dense-rows", type=int, default=None, help="direct value pass: dense-chunk row span")
+    ap.add_argument("--opt", action="append", default=[], help="NAME=VALUE library option (OPT_NAME)")
     ap.add_argument("--dist", default="1d", choices=["1d", "summa"],
                     help="N>1: 1d = flops-balanced column blocks with A replicated (no data-path collective); "
                          "summa = the 2D SUMMA / 3D drivers (NCCL stage broadcasts, fiber exchange, merge)")
@@ -123,6 +125,11 @@ def apply_options(ctx, args):
         ctx.set_option(L.OPT_DIRECT_VALUE_TMAJOR, args.value_tmajor)
     if args.words is not None:
         ctx.set_option(L.OPT_DIRECT_WORDS, args.words)
+    if args.value_dense_rows is not None:
+        ctx.set_option(L.OPT_DIRECT_VALUE_DENSE_ROWS, args.value_dense_rows)
+    for kv in args.opt:
+        k, v = kv.split("=")
+        ctx.set_option(getattr(L, "OPT_" + k), int(v))
     if args.value_rank is not None:
         ctx.set_option(L.OPT_DIRECT_VALUE_RANK, args.value_rank)
     if args.value_interleave is not None:

@@ -141,6 +141,7 @@ struct Options {
     int deterministic = 0;                  // 1: every product by ESC (the reference's fold order, bit-exact fp)
     int direct_esc = 0;                     // 1: ESC for every semiring (sort-merge path), 0: bitmap / hash paths
     int direct_words = 1;                   // form: walk A's (32-row word, mask) pairs instead of its rows
+    int direct_value_dense_rows = 0;        // value pass: chunks spanning <= this many rows fold by row offset (0 = cap)
     int direct_value_tmajor = 1;            // value pass: tile-major 4096-row pointer table + chunks in row order
     int direct_short_run = 0;               // form: runs shorter than this walked per thread (0 = default 8)
     int direct_persistent = 1;              // form kernel: persistent CTAs (1) or one CTA per unit (0)

@@ -747,8 +747,11 @@ __device__ __forceinline__ void emit_block(EmitWarp* ws, int pos, int ex, int E,
     }
 }
 
+#ifndef SLAPCU_EMIT_MINB
+#define SLAPCU_EMIT_MINB 1
+#endif
 template <int NT>
-__global__ void __launch_bounds__(NT) k_tile_emit(EmitArgs g) {
+__global__ void __launch_bounds__(NT, SLAPCU_EMIT_MINB) k_tile_emit(EmitArgs g) {
     constexpr int NW = NT / 32;
     __shared__ EmitWarp wsm[NW];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1241,7 +1244,8 @@ struct RankChunk {
 };
 
 template <int SRID, int NT>
-__global__ void __launch_bounds__(NT) k_item_values_rank(ValueArgs g, const RankChunk* __restrict__ chunks, int cap) {
+__global__ void __launch_bounds__(NT) k_item_values_rank(ValueArgs g, const RankChunk* __restrict__ chunks, int cap,
+                                                         int dense_rows) {
     using S_ = Sr<SRID>;
     using T = typename S_::T;
     using Acc = typename S_::Acc;
@@ -1250,7 +1254,7 @@ __global__ void __launch_bounds__(NT) k_item_values_rank(ValueArgs g, const Rank
     extern __shared__ __align__(16) unsigned char sm_raw[];
     const int W = 1 << (g.TL - 5);
     Acc* val = reinterpret_cast<Acc*>(sm_raw);
-    unsigned* bm = reinterpret_cast<unsigned*>(sm_raw + ((sizeof(Acc) * size_t(cap) + 15) & ~size_t(15)));
+    unsigned* bm = reinterpret_cast<unsigned*>(sm_raw + ((sizeof(Acc) * size_t(max(cap, dense_rows)) + 15) & ~size_t(15)));
     uint16_t* pre16 = reinterpret_cast<uint16_t*>(bm + W);  // [W]
     int* gbase = reinterpret_cast<int*>(pre16 + W);         // [W / 32]
     __shared__ ValueWalkSm<SRID, NT> sh;
@@ -1281,7 +1285,7 @@ __global__ void __launch_bounds__(NT) k_item_values_rank(ValueArgs g, const Rank
     }
     // dense chunks (their rows fit the value array): values indexed by row
     // offset -- no bitmap, no ranks, one shared atomic per product
-    const bool dense = nwords * 32 <= cap;
+    const bool dense = nwords * 32 <= dense_rows;
     if (!dense)
         for (int q = tid; q < nwords; q += NT) bm[q] = 0u;
     else
@@ -1305,7 +1309,10 @@ __global__ void __launch_bounds__(NT) k_item_values_rank(ValueArgs g, const Rank
         val[q] = S_::identity();
     }
     __syncthreads();
-    // ranks: per 32-word group a warp scan (16-bit prefixes), then group bases
+    // ranks: per 32-word group a warp scan, group totals scanned, then the
+    // chunk-wide prefix of every word stored in 16 bits (a chunk holds at most
+    // cap <= 65535 outputs): a product's slot is pre[w] + popc(bits below it)
+    // -- two shared loads
     const int ng = (nwords + 31) >> 5;
     for (int gi = warp; gi < ng; gi += NW) {
         const int w = gi * 32 + lane;
@@ -1328,36 +1335,47 @@ __global__ void __launch_bounds__(NT) k_item_values_rank(ValueArgs g, const Rank
         }
     }
     __syncthreads();
-    auto slot = [bm, pre16, gbase, val, r0](int r) {
+    for (int w = tid; w < nwords; w += NT) pre16[w] = (uint16_t)(pre16[w] + gbase[w >> 5]);
+    __syncthreads();
+    auto slot = [bm, pre16, val, r0](int r) {
         const int rr = r - r0;
         const int w = rr >> 5;
-        return &val[gbase[w >> 5] + pre16[w] + __popc(bm[w] & ((1u << (rr & 31)) - 1u))];
+        return &val[pre16[w] + __popc(bm[w] & ((1u << (rr & 31)) - 1u))];
     };
     value_walk<SRID, NT>(g.A, g.B, g.Atpv, g.Tv, ts0, j, sh, slot, ts1, g.arv, g.tv_stride);
     for (int q = tid; q < n; q += NT) Cv[lo + q] = S_::out(val[q]);
 }
 
 // Rank chunks of the large items (thread per item, greedy over row blocks).
+// Chunks never start or end on an empty 4096-row block.  A chunk may grow
+// past `cap` outputs while its span stays within `dense_blocks` blocks (it is
+// then folded by row offset, no ranks); beyond that span it holds at most
+// `cap` outputs (rank slots).
 __global__ void k_rank_chunks(int n, const int* __restrict__ list, const int* __restrict__ rbc, int nrb, int cap,
-                              const int64_t* __restrict__ coff, int64_t* __restrict__ ccount,
+                              int dense_blocks, const int64_t* __restrict__ coff, int64_t* __restrict__ ccount,
                               RankChunk* __restrict__ out) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const int item = list[i];
         const int* rb = rbc + int64_t(item) * nrb;
         int64_t k = 0, acc = 0;
-        int b0 = 0;
+        int b0 = -1, blast = -1;
         for (int b = 0; b < nrb; ++b) {
             const int x = rb[b];
-            if (acc > 0 && acc + x > cap) {
-                if (out) out[coff[i] + k] = RankChunk{item, b0, b, 0};
+            if (x == 0) continue;
+            if (b0 >= 0 && b + 1 - b0 > dense_blocks && acc + x > cap) {
+                if (out) out[coff[i] + k] = RankChunk{item, b0, blast + 1, 0};
                 ++k;
+                b0 = -1;
+            }
+            if (b0 < 0) {
                 b0 = b;
                 acc = 0;
             }
             acc += x;
+            blast = b;
         }
-        if (acc > 0) {
-            if (out) out[coff[i] + k] = RankChunk{item, b0, nrb, 0};
+        if (b0 >= 0) {
+            if (out) out[coff[i] + k] = RankChunk{item, b0, blast + 1, 0};
             ++k;
         }
         if (!out) ccount[i] = k;
@@ -2282,6 +2300,13 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
                 // 8192 4-byte slots keep 3 CTAs of 512 threads per SM (C3 MinPlus: values
                 // 498 -> 441 ms vs 4096; 6144 467, 10240 508, 12288 492 ms)
                 const int cap = c.opt.direct_value_rank > 0 ? c.opt.direct_value_rank : (sizeof(Acc) <= 4 ? 8192 : 4096);
+                // chunks spanning at most dense_rows rows fold by row offset (no ranks)
+                constexpr int kBlkRows4096 = 4096;
+                int dense_rows = std::max(
+                    cap, (c.opt.direct_value_dense_rows > 0 ? c.opt.direct_value_dense_rows : cap) / kBlkRows4096 * kBlkRows4096);
+                while (dense_rows > cap && sizeof(Acc) * size_t(dense_rows) + sizeof(unsigned) * W + sizeof(uint16_t) * W +
+                                                   sizeof(int) * (W / 32) + 16 > size_t(c.smem_optin) - 8192)
+                    dense_rows -= kBlkRows4096;  // (a larger dense span than shared memory holds)
                 const int T12 = (int)((A.nrows + 4095) >> 12);
                 ValueArgs vr = va;
                 const bool tmajor = c.opt.direct_value_tmajor != 0;
@@ -2294,14 +2319,14 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
                     coff(sizeof(int64_t) * (size_t(nsl[1]) + 1), c.stream);
                 SLAPCU_CUDA(cudaMemsetAsync(ccount.as<int64_t>() + nsl[1], 0, sizeof(int64_t), c.stream));
                 launch(c, k_rank_chunks, dim3(grid_for(c, nsl[1], 256)), dim3(256), 0, nsl[1], (const int*)large,
-                       (const int*)d.rbc.as<int>(), nrb, cap, (const int64_t*)nullptr, ccount.as<int64_t>(),
-                       (RankChunk*)nullptr);
+                       (const int*)d.rbc.as<int>(), nrb, cap, dense_rows / kBlkRows4096, (const int64_t*)nullptr,
+                       ccount.as<int64_t>(), (RankChunk*)nullptr);
                 exclusive_scan_i64(c, ccount.as<int64_t>(), coff.as<int64_t>(), nsl[1] + 1);
                 const int64_t nch = d2h(c, coff.as<int64_t>() + nsl[1]);
                 DevBuf chunks(sizeof(RankChunk) * std::max<int64_t>(nch, 1), c.stream);
                 launch(c, k_rank_chunks, dim3(grid_for(c, nsl[1], 256)), dim3(256), 0, nsl[1], (const int*)large,
-                       (const int*)d.rbc.as<int>(), nrb, cap, (const int64_t*)coff.as<int64_t>(), ccount.as<int64_t>(),
-                       chunks.as<RankChunk>());
+                       (const int*)d.rbc.as<int>(), nrb, cap, dense_rows / kBlkRows4096,
+                       (const int64_t*)coff.as<int64_t>(), ccount.as<int64_t>(), chunks.as<RankChunk>());
                 if (c.opt.direct_value_tmajor && nch > 1) {  // row-block order (L2 locality of A and the table)
                     DevBuf key(sizeof(int) * nch, c.stream), kout(sizeof(int) * nch, c.stream),
                         idx(sizeof(int) * nch, c.stream), ord(sizeof(int) * nch, c.stream),
@@ -2323,12 +2348,12 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
                            (const RankChunk*)chunks.as<RankChunk>(), (const int*)ord.as<int>(), sorted.as<RankChunk>());
                     chunks = std::move(sorted);
                 }
-                const size_t smem = ((sizeof(Acc) * size_t(cap) + 15) & ~size_t(15)) + sizeof(unsigned) * W +
-                                    sizeof(uint16_t) * W + sizeof(int) * (W / 32) + 16;
+                const size_t smem = ((sizeof(Acc) * size_t(std::max(cap, dense_rows)) + 15) & ~size_t(15)) +
+                                    sizeof(unsigned) * W + sizeof(uint16_t) * W + sizeof(int) * (W / 32) + 16;
                 auto gor = [&](auto k, int nt) {
                     ensure_smem(k, smem);
                     launch(c, k, dim3((unsigned)nch), dim3(nt), smem, vr, (const RankChunk*)chunks.as<RankChunk>(),
-                           cap);
+                           cap, dense_rows);
                 };
                 if (c.opt.direct_value_threads == 512)
                     gor(k_item_values_rank<ID, 512>, 512);

@@ -34,25 +34,61 @@ __global__ void k_entry_len(DevCsc A, DevCsc B, int64_t e0, int64_t ne, int64_t*
     }
 }
 
-// Expand: one warp per B entry (grid-stride), lane-strided over A(:,k).
-template <int SRID>
+// Column (relative to the group) of each B entry of the group.
+__global__ void k_entry_col(int64_t ncols, const int64_t* __restrict__ Bcp, int64_t e0, int* __restrict__ col) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t j = w0; j < ncols; j += nw)
+        for (int64_t x = Bcp[j] + lane; x < Bcp[j + 1]; x += 32) col[x - e0] = (int)j;
+}
+
+// Expand: each lane takes one B entry; A columns shorter than 32 entries are
+// written by their lane, longer ones by the whole warp (ballot order,
+// lane-strided, coalesced).  The key is (column << row_bits) | row, so ONE
+// stable radix sort over the group orders products by (column, row) and keeps
+// the enumeration order (ascending k) inside every run.
+template <int SRID, class K>
 __global__ void k_expand(DevCsc A, DevCsc B, int64_t e0, int64_t ne, const int64_t* __restrict__ eoff,
-                         int* __restrict__ keys, typename Sr<SRID>::Acc* __restrict__ vals) {
+                         const int* __restrict__ ecol, int row_bits, K* __restrict__ keys,
+                         typename Sr<SRID>::Acc* __restrict__ vals) {
     using S_ = Sr<SRID>;
     using T = typename S_::T;
     const T* Av = static_cast<const T*>(A.v);
     const T* Bv = static_cast<const T*>(B.v);
     const int lane = threadIdx.x & 31;
-    const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
-    for (int64_t x = w0; x < ne; x += nw) {
-        const int k = B.rw[e0 + x];
-        const T b = Bv[e0 + x];
-        const int64_t s = A.cp[k], e = A.cp[k + 1];
-        const int64_t o = eoff[x];
-        for (int64_t p = s + lane; p < e; p += 32) {
-            keys[o + (p - s)] = A.rw[p];
-            vals[o + (p - s)] = S_::mul(Av[p], b);
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t base = int64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31); base < ne; base += stride) {
+        const int64_t x = base + lane;
+        int64_t s = 0, len = 0, o = 0;
+        T b{};
+        K hi = 0;
+        if (x < ne) {
+            const int k = B.rw[e0 + x];
+            b = Bv[e0 + x];
+            hi = K(ecol[x]) << row_bits;
+            s = A.cp[k];
+            len = A.cp[k + 1] - s;
+            o = eoff[x];
+            if (len < 32) {
+                for (int64_t q = 0; q < len; ++q) {
+                    keys[o + q] = hi | K(A.rw[s + q]);
+                    vals[o + q] = S_::mul(Av[s + q], b);
+                }
+            }
+        }
+        unsigned lm = __ballot_sync(0xffffffffu, len >= 32);
+        while (lm) {
+            const int src = __ffs(lm) - 1;
+            lm &= lm - 1u;
+            const int64_t ss = __shfl_sync(0xffffffffu, s, src), ll = __shfl_sync(0xffffffffu, len, src);
+            const int64_t oo = __shfl_sync(0xffffffffu, o, src);
+            const K hh = __shfl_sync(0xffffffffu, hi, src);
+            const T bb = __shfl_sync(0xffffffffu, b, src);
+            for (int64_t q = lane; q < ll; q += 32) {
+                keys[oo + q] = hh | K(A.rw[ss + q]);
+                vals[oo + q] = S_::mul(Av[ss + q], bb);
+            }
         }
     }
 }
@@ -66,30 +102,25 @@ __global__ void k_seg_bounds(int64_t ncols, const int64_t* __restrict__ Bcp, int
     }
 }
 
-// Run heads: first product of a column segment, or a row differing from its predecessor.
-__global__ void k_seg_mark(int64_t ncols, const int* __restrict__ beg, const int* __restrict__ end,
-                           int* __restrict__ head) {
-    for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < ncols; j += int64_t(gridDim.x) * blockDim.x)
-        if (end[j] > beg[j]) head[beg[j]] = 1;
-}
-
-__global__ void k_run_heads(int64_t P, const int* __restrict__ keys, int* __restrict__ head) {
-    for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < P; p += int64_t(gridDim.x) * blockDim.x)
-        if (p > 0 && keys[p] != keys[p - 1]) head[p] = 1;
+// Run heads: a (column, row) key differing from its predecessor.
+template <class K>
+__global__ void k_run_heads(int64_t P, const K* __restrict__ keys, int* __restrict__ head) {
+    for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p <= P; p += int64_t(gridDim.x) * blockDim.x)
+        head[p] = p < P && (p == 0 || keys[p] != keys[p - 1]);
 }
 
 // Fold each run left to right (the reference's order) and write (row, value).
-template <int SRID>
-__global__ void k_fold(int64_t P, const int* __restrict__ keys, const typename Sr<SRID>::Acc* __restrict__ vals,
-                       const int* __restrict__ head, const int* __restrict__ ex, int64_t obase, int32_t* __restrict__ crw,
-                       typename Sr<SRID>::T* __restrict__ cv) {
+template <int SRID, class K>
+__global__ void k_fold(int64_t P, const K* __restrict__ keys, const typename Sr<SRID>::Acc* __restrict__ vals,
+                       const int* __restrict__ head, const int* __restrict__ ex, int64_t obase, K row_mask,
+                       int32_t* __restrict__ crw, typename Sr<SRID>::T* __restrict__ cv) {
     using S_ = Sr<SRID>;
     for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < P; p += int64_t(gridDim.x) * blockDim.x) {
         if (!head[p]) continue;
         typename S_::Acc acc = vals[p];
         for (int64_t q = p + 1; q < P && !head[q]; ++q) acc = S_::add(acc, vals[q]);
         const int64_t o = obase + ex[p];
-        crw[o] = keys[p];
+        crw[o] = (int32_t)(keys[p] & row_mask);
         cv[o] = S_::out(acc);
     }
 }
@@ -132,8 +163,7 @@ int64_t esc_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int64_t c
     SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
     size_t fr = 0, tot = 0;
     SLAPCU_CUDA(cudaMemGetInfo(&fr, &tot));
-    const int vs = value_size(sr);
-    const int64_t per_prod = 4 * 4 + 2 * 8;  // keys x2, head, ex, values x2 (<= 8 bytes each)
+    const int64_t per_prod = 2 * 8 + 2 * 4 + 2 * 8;  // keys x2 (<= 8 bytes), head, ex, values x2 (<= 8 bytes)
     const int64_t group_max = std::max<int64_t>(1, std::min<int64_t>(int64_t(1) << 30, int64_t(fr / 3) / per_prod));
     int64_t obase = 0;
     int64_t j0 = 0;
@@ -151,64 +181,78 @@ int64_t esc_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int64_t c
                                                   " products (int32 sort offsets)"};
             const int64_t ng = j1 - j0;
             const int64_t e0 = hbcp[j0], ne = hbcp[j1] - e0;
-            DevBuf len(sizeof(int64_t) * (ne + 1), c.stream), eoff(sizeof(int64_t) * (ne + 1), c.stream);
-            SLAPCU_CUDA(cudaMemsetAsync(len.as<int64_t>() + ne, 0, sizeof(int64_t), c.stream));
-            DevBuf k0(sizeof(int) * std::max<int64_t>(P, 1), c.stream), k1(sizeof(int) * std::max<int64_t>(P, 1), c.stream);
-            DevBuf v0(sizeof(Acc) * std::max<int64_t>(P, 1), c.stream), v1(sizeof(Acc) * std::max<int64_t>(P, 1), c.stream);
-            DevBuf beg(sizeof(int) * std::max<int64_t>(ng, 1), c.stream), end(sizeof(int) * std::max<int64_t>(ng, 1), c.stream);
-            DevBuf head(sizeof(int) * (P + 1), c.stream), ex(sizeof(int) * (P + 1), c.stream);
-            {
-                KScope ks(c, KC_SYM_HEAVY);
-                if (ne) {
-                    launch(c, k_entry_len, dim3(grid_for(c, ne, 256)), dim3(256), 0, A, B, e0, ne, len.as<int64_t>());
+            int row_bits = 1, col_bits = 1;
+            while ((int64_t(1) << row_bits) < A.nrows) ++row_bits;
+            while ((int64_t(1) << col_bits) < ng) ++col_bits;
+            const bool narrow = row_bits + col_bits <= 32;
+            int64_t gnnz = 0;
+            auto run = [&](auto kz) {
+                using K = decltype(kz);
+                DevBuf len(sizeof(int64_t) * (ne + 1), c.stream), eoff(sizeof(int64_t) * (ne + 1), c.stream),
+                    ecol(sizeof(int) * std::max<int64_t>(ne, 1), c.stream);
+                SLAPCU_CUDA(cudaMemsetAsync(len.as<int64_t>() + ne, 0, sizeof(int64_t), c.stream));
+                DevBuf k0(sizeof(K) * std::max<int64_t>(P, 1), c.stream), k1(sizeof(K) * std::max<int64_t>(P, 1), c.stream);
+                DevBuf v0(sizeof(Acc) * std::max<int64_t>(P, 1), c.stream),
+                    v1(sizeof(Acc) * std::max<int64_t>(P, 1), c.stream);
+                DevBuf beg(sizeof(int) * std::max<int64_t>(ng, 1), c.stream), end(sizeof(int) * std::max<int64_t>(ng, 1), c.stream);
+                DevBuf head(sizeof(int) * (P + 1), c.stream), ex(sizeof(int) * (P + 1), c.stream);
+                {
+                    KScope ks(c, KC_SYM_HEAVY);
+                    if (ne) {
+                        launch(c, k_entry_len, dim3(grid_for(c, ne, 256)), dim3(256), 0, A, B, e0, ne, len.as<int64_t>());
+                        launch(c, k_entry_col, dim3(grid_for(c, ng * 32, 256)), dim3(256), 0, ng, (const int64_t*)(B.cp + j0),
+                               e0, ecol.as<int>());
+                    }
+                    exclusive_scan_i64(c, len.as<int64_t>(), eoff.as<int64_t>(), ne + 1);
+                    if (ne)
+                        launch(c, k_expand<ID, K>, dim3(grid_for(c, ne, 256)), dim3(256), 0, A, B, e0, ne,
+                               (const int64_t*)eoff.as<int64_t>(), (const int*)ecol.as<int>(), row_bits, k0.as<K>(),
+                               v0.as<Acc>());
+                    launch(c, k_seg_bounds, dim3(grid_for(c, ng, 256)), dim3(256), 0, ng, (const int64_t*)(B.cp + j0), e0,
+                           (const int64_t*)eoff.as<int64_t>(), beg.as<int>(), end.as<int>());
+                    if (P) {
+                        // one stable LSD radix sort by (column, row) over the group
+                        size_t tb = 0;
+                        const int bits = row_bits + col_bits;
+                        SLAPCU_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k0.as<K>(), k1.as<K>(), v0.as<Acc>(),
+                                                                    v1.as<Acc>(), (int)P, 0, bits, c.stream));
+                        DevBuf tmp(tb, c.stream);
+                        timed(c, KC_SYM_HEAVY, [&] {
+                            SLAPCU_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, k0.as<K>(), k1.as<K>(),
+                                                                        v0.as<Acc>(), v1.as<Acc>(), (int)P, 0, bits,
+                                                                        c.stream));
+                        });
+                        ++c.launches;
+                    }
+                    launch(c, k_run_heads<K>, dim3(grid_for(c, P + 1, 256)), dim3(256), 0, P, (const K*)k1.as<K>(),
+                           head.as<int>());
                 }
-                exclusive_scan_i64(c, len.as<int64_t>(), eoff.as<int64_t>(), ne + 1);
-                if (ne)
-                    launch(c, k_expand<ID>, dim3(grid_for(c, ne * 32, 256)), dim3(256), 0, A, B, e0, ne,
-                           (const int64_t*)eoff.as<int64_t>(), k0.as<int>(), v0.as<Acc>());
-                launch(c, k_seg_bounds, dim3(grid_for(c, ng, 256)), dim3(256), 0, ng, (const int64_t*)(B.cp + j0), e0,
-                       (const int64_t*)eoff.as<int64_t>(), beg.as<int>(), end.as<int>());
-                if (P) {
+                {
+                    KScope ks(c, KC_SCAN);
                     size_t tb = 0;
-                    SLAPCU_CUDA(cub::DeviceSegmentedSort::StableSortPairs(
-                        nullptr, tb, k0.as<int>(), k1.as<int>(), v0.as<Acc>(), v1.as<Acc>(), (int)P, (int)ng,
-                        beg.as<int>(), end.as<int>(), c.stream));
+                    SLAPCU_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, head.as<int>(), ex.as<int>(), P + 1, c.stream));
                     DevBuf tmp(tb, c.stream);
-                    timed(c, KC_SYM_HEAVY, [&] {
-                        SLAPCU_CUDA(cub::DeviceSegmentedSort::StableSortPairs(
-                            tmp.get(), tb, k0.as<int>(), k1.as<int>(), v0.as<Acc>(), v1.as<Acc>(), (int)P, (int)ng,
-                            beg.as<int>(), end.as<int>(), c.stream));
+                    timed(c, KC_SCAN, [&] {
+                        SLAPCU_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tb, head.as<int>(), ex.as<int>(), P + 1,
+                                                                  c.stream));
                     });
                     ++c.launches;
                 }
-                SLAPCU_CUDA(cudaMemsetAsync(head.get(), 0, sizeof(int) * (P + 1), c.stream));
-                launch(c, k_seg_mark, dim3(grid_for(c, ng, 256)), dim3(256), 0, ng, (const int*)beg.as<int>(),
-                       (const int*)end.as<int>(), head.as<int>());
-                if (P)
-                    launch(c, k_run_heads, dim3(grid_for(c, P, 256)), dim3(256), 0, P, (const int*)k1.as<int>(),
-                           head.as<int>());
-            }
-            {
-                KScope ks(c, KC_SCAN);
-                size_t tb = 0;
-                SLAPCU_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, head.as<int>(), ex.as<int>(), P + 1, c.stream));
-                DevBuf tmp(tb, c.stream);
-                timed(c, KC_SCAN, [&] {
-                    SLAPCU_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tb, head.as<int>(), ex.as<int>(), P + 1,
-                                                              c.stream));
-                });
-                ++c.launches;
-            }
-            const int64_t gnnz = d2h1(c, ex.as<int>() + P);
-            launch(c, k_esc_colptr, dim3(grid_for(c, ng, 256)), dim3(256), 0, ng, (const int*)beg.as<int>(),
-                   (const int*)ex.as<int>(), obase, c_colptr + j0);
-            if (obase + gnnz > capacity) over = true;
-            if (P && !over) {
-                KScope ks(c, KC_NUM_HEAVY);
-                launch(c, k_fold<ID>, dim3(grid_for(c, P, 256)), dim3(256), 0, P, (const int*)k1.as<int>(),
-                       (const Acc*)v1.as<Acc>(), (const int*)head.as<int>(), (const int*)ex.as<int>(), obase, crw,
-                       static_cast<T*>(cv));
-            }
+                gnnz = d2h1(c, ex.as<int>() + P);
+                launch(c, k_esc_colptr, dim3(grid_for(c, ng, 256)), dim3(256), 0, ng, (const int*)beg.as<int>(),
+                       (const int*)ex.as<int>(), obase, c_colptr + j0);
+                if (obase + gnnz > capacity) over = true;
+                if (P && !over) {
+                    KScope ks(c, KC_NUM_HEAVY);
+                    launch(c, k_fold<ID, K>, dim3(grid_for(c, P, 256)), dim3(256), 0, P, (const K*)k1.as<K>(),
+                           (const Acc*)v1.as<Acc>(), (const int*)head.as<int>(), (const int*)ex.as<int>(), obase,
+                           K((int64_t(1) << row_bits) - 1), crw, static_cast<T*>(cv));
+                }
+            };
+            if (narrow)
+                run(uint32_t(0));
+            else
+                run(uint64_t(0));
             obase += gnnz;
             j0 = j1;
         }
