@@ -174,8 +174,10 @@ typedef enum {
                                               tile-major and rank chunks run in row-block order */
     SLAPCU_OPT_DIRECT_WORDS = 27,          /* direct path form: 1 = walk A as (32-row word, row mask) pairs
                                               (built per A): one shared update per distinct word of a run */
-    SLAPCU_OPT_DIRECT_ESC = 28,            /* direct path: 1 = every semiring on the ESC (expand, stable
-                                              segmented sort, left fold) path; 0 = bitmap / hash paths */
+    SLAPCU_OPT_DIRECT_ESC = 28,            /* direct path: 1 = every semiring on the ESC (expand, stable sort
+                                              by row, left fold) path; 0 = bitmap / hash paths; -1 (default)
+                                              = value semirings whose sampled compression flops / nnz(C) is
+                                              below 2 (spgemm.hpp:54's hybrid threshold) take ESC */
     SLAPCU_OPT_DIRECT_VALUE_DENSE_ROWS = 29 /* direct path value pass: chunks spanning at most this many rows
                                               (multiple of 4096, <= 32768) fold by row offset into a dense
                                               shared array, without rank lookups (0 = the rank chunk size) */

@@ -221,7 +221,10 @@ slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t v
             c.opt.direct_light_flops_max = v;
             break;
         case SLAPCU_OPT_DETERMINISTIC: c.opt.deterministic = v != 0; break;
-        case SLAPCU_OPT_DIRECT_ESC: c.opt.direct_esc = (int)v; break;
+        case SLAPCU_OPT_DIRECT_ESC:
+            require(v >= -1 && v <= 1, SLAPCU_ERR_INVALID, "ESC: -1 (auto), 0 (off) or 1 (always)");
+            c.opt.direct_esc = (int)v;
+            break;
         case SLAPCU_OPT_DENSE_FLOPS_MIN: c.opt.dense_flops_min = v; break;
         case SLAPCU_OPT_ASYNC_FINISH: c.opt.async_finish = v != 0; break;
         case SLAPCU_OPT_DENSE_TILE_ROWS_LOG2:

@@ -139,7 +139,8 @@ struct Options {
     int direct_tile_major = 1;              // form: work units ordered by row tile, then heaviest first
     int direct_form_walk = 0;               // form: long runs as 256-product units (0) or packed products (1)
     int deterministic = 0;                  // 1: every product by ESC (the reference's fold order, bit-exact fp)
-    int direct_esc = 0;                     // 1: ESC for every semiring (sort-merge path), 0: bitmap / hash paths
+    int direct_esc = -1;                    // 1: ESC for every semiring, 0: bitmap / hash paths, -1 auto (value
+                                            // semirings with sampled compression < 2 take ESC)
     int direct_words = 1;                   // form: walk A's (32-row word, mask) pairs instead of its rows
     int direct_value_dense_rows = 0;        // value pass: chunks spanning <= this many rows fold by row offset (0 = cap)
     int direct_value_tmajor = 1;            // value pass: tile-major 4096-row pointer table + chunks in row order

@@ -747,11 +747,15 @@ __device__ __forceinline__ void emit_block(EmitWarp* ws, int pos, int ex, int E,
     }
 }
 
-#ifndef SLAPCU_EMIT_MINB
-#define SLAPCU_EMIT_MINB 1
+// (__launch_bounds__(NT) alone: 56 registers; an explicit minimum of 1 block
+// lets the compiler take 80 and emit loses 20% to occupancy; 12 spills)
+#ifdef SLAPCU_EMIT_MINB
+#define SLAPCU_EMIT_BOUNDS __launch_bounds__(NT, SLAPCU_EMIT_MINB)
+#else
+#define SLAPCU_EMIT_BOUNDS __launch_bounds__(NT)
 #endif
 template <int NT>
-__global__ void __launch_bounds__(NT, SLAPCU_EMIT_MINB) k_tile_emit(EmitArgs g) {
+__global__ void SLAPCU_EMIT_BOUNDS k_tile_emit(EmitArgs g) {
     constexpr int NW = NT / 32;
     __shared__ EmitWarp wsm[NW];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1002,6 +1006,9 @@ struct ValueWalkSm {
 // units; shorter runs are packed 32 products per warp step (the owning B
 // entry found by a search over the batch's product prefix), so no thread
 // walks a run alone through a chain of dependent loads.
+#ifdef SLAPCU_VCOUNT
+__device__ unsigned long long g_vcount[4];  // entry visits, nonempty runs, products, batches (debug variant)
+#endif
 template <int SRID, int NT, class Slot>
 __device__ __forceinline__ void value_walk(const DevCsc& A, const DevCsc& B, const int32_t* __restrict__ Atab, int T,
                                            int t, int j, ValueWalkSm<SRID, NT>& sh, Slot slot, int t_hi = -1,
@@ -1030,6 +1037,12 @@ __device__ __forceinline__ void value_walk(const DevCsc& A, const DevCsc& B, con
                 rhi = tp[th];
             }
             const int len = rhi - rlo;
+#ifdef SLAPCU_VCOUNT
+            atomicAdd(&g_vcount[0], 1ull);
+            if (len > 0) atomicAdd(&g_vcount[1], 1ull);
+            atomicAdd(&g_vcount[2], (unsigned long long)(len > 0 ? len : 0));
+            if (tid == 0) atomicAdd(&g_vcount[3], 1ull);
+#endif
             if (len > 0) {
                 const int64_t st = A.cp[k] + rlo;
                 const T_ bv = Bv[i];
@@ -1943,6 +1956,33 @@ static int64_t direct_fallback(Ctx& c, const DevCsc& A, const DevCsc& B, int sr,
     return nnz;
 }
 
+// The reference picks the accumulator per column by compression: hash iff
+// flops_j / nnz(C(:,j)) >= 2 (spgemm.hpp:54, :312-317), else the k-way merge.
+// Here the choice is per product for value semirings: the compression of 8
+// evenly spaced windows of <= 256 columns (exact symbolic counts) decides
+// between the bitmap path and the sort-merge (ESC) path, whose cost is per
+// product rather than per output entry and wins when cf is near 1 (C2, C5).
+static bool esc_preferred(Ctx& c, const DevCsc& A, const DevCsc& B) {
+    const int64_t n = B.ncols;
+    if (n == 0) return false;
+    const int nw = n > 2048 ? 8 : 1;
+    const int64_t w = nw == 1 ? n : std::min<int64_t>(256, n / nw);
+    int64_t f = 0, s = 0;
+    DevBuf cp(sizeof(int64_t) * (w + 1), c.stream);
+    for (int q = 0; q < nw; ++q) {
+        const int64_t c0 = nw == 1 ? 0 : (n - w) * q / (nw - 1);
+        DevCsc win = B;
+        win.ncols = w;
+        win.cp = B.cp + c0;
+        resolve(c, win);
+        int64_t t = 0;
+        spgemm_flops(c, A, win, nullptr, &t);
+        f += t;
+        s += spgemm_symbolic(c, A, win, SLAPCU_ALG_HYBRID, cp.as<int64_t>());
+    }
+    return s > 0 && f < 2 * s;
+}
+
 int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int alg, int64_t capacity,
                       int64_t* c_colptr, int32_t* crw, void* cv) {
     check_operands(A_, B_);
@@ -1957,7 +1997,8 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
     // sort-merge (ESC) path: the reference's fold order for every output entry
     // (bit-exact floating point), or forced for any semiring
     const bool fp = sr == SLAPCU_PLUS_TIMES_F64 || sr == SLAPCU_PLUS_TIMES_F32 || sr == SLAPCU_MIN_PLUS_F64;
-    if ((c.opt.deterministic && fp) || c.opt.direct_esc == 1) {
+    if ((c.opt.deterministic && fp) || c.opt.direct_esc == 1 ||
+        (c.opt.direct_esc < 0 && sr != SLAPCU_OR_AND_U8 && esc_preferred(c, A, B))) {
         SLAPCU_CUDA(cudaEventRecord(c.ev[0], c.stream));
         const int64_t nz = esc_spgemm(c, A_, B_, sr, capacity, c_colptr, crw, cv);
         SLAPCU_CUDA(cudaEventRecord(c.ev[1], c.stream));
@@ -2434,3 +2475,15 @@ bool direct_exact(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int alg, i
 }
 
 }  // namespace slapcu
+
+#ifdef SLAPCU_VCOUNT
+// debug variant only: value-walk counters (entry visits, nonempty runs, products, batches)
+extern "C" int slapcu_debug_vcount(unsigned long long* out, int reset) {
+    cudaMemcpyFromSymbol(out, slapcu::g_vcount, sizeof(unsigned long long) * 4);
+    if (reset) {
+        unsigned long long z[4] = {0, 0, 0, 0};
+        cudaMemcpyToSymbol(slapcu::g_vcount, z, sizeof(z));
+    }
+    return 0;
+}
+#endif

@@ -93,6 +93,87 @@ __global__ void k_expand(DevCsc A, DevCsc B, int64_t e0, int64_t ne, const int64
     }
 }
 
+// Columns with at most kSmallSort products: one CTA sorts the column's
+// products in shared memory by (row, enumeration index) -- a bitonic network
+// on 64-bit keys, stable by construction -- and writes them permuted into the
+// sorted arrays.  (One global radix sort over millions of short columns is
+// 5 passes over every product; this is one.)
+constexpr int kSmallSort = 2048;
+
+template <class K, class V>
+__global__ void __launch_bounds__(256) k_sort_small(const int* __restrict__ cols, const int* __restrict__ beg,
+                                                    const int* __restrict__ end, K row_mask, const K* __restrict__ k0,
+                                                    const V* __restrict__ v0, K* __restrict__ k1, V* __restrict__ v1) {
+    __shared__ unsigned long long sk[kSmallSort];
+    const int j = cols[blockIdx.x];
+    const int b = beg[j], n = end[j] - b;
+    int N = 1;
+    while (N < n) N <<= 1;
+    for (int q = threadIdx.x; q < N; q += blockDim.x)
+        sk[q] = q < n ? ((unsigned long long)(k0[b + q] & row_mask) << 11) | (unsigned long long)q : ~0ull;
+    __syncthreads();
+    for (int size = 2; size <= N; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int q = threadIdx.x; q < (N >> 1); q += blockDim.x) {
+                const int lo = 2 * q - (q & (stride - 1)), hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const unsigned long long x = sk[lo], y = sk[hi];
+                if ((x > y) == up) {
+                    sk[lo] = y;
+                    sk[hi] = x;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int q = threadIdx.x; q < n; q += blockDim.x) {
+        const int src = (int)(sk[q] & 2047ull);
+        k1[b + q] = k0[b + src];
+        v1[b + q] = v0[b + src];
+    }
+}
+
+// Columns with at most kWarpSort products: one WARP each (8 per CTA), the
+// same bitonic network in the warp's slice of shared memory, __syncwarp only.
+constexpr int kWarpSort = 256;
+
+template <class K, class V>
+__global__ void __launch_bounds__(256) k_sort_warp(int ncols, const int* __restrict__ cols, const int* __restrict__ beg,
+                                                   const int* __restrict__ end, K row_mask, const K* __restrict__ k0,
+                                                   const V* __restrict__ v0, K* __restrict__ k1, V* __restrict__ v1) {
+    __shared__ unsigned long long skw[8][kWarpSort];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int ci = blockIdx.x * 8 + w;
+    if (ci >= ncols) return;
+    unsigned long long* sk = skw[w];
+    const int j = cols[ci];
+    const int b = beg[j], n = end[j] - b;
+    int N = 1;
+    while (N < n) N <<= 1;
+    for (int q = lane; q < N; q += 32)
+        sk[q] = q < n ? ((unsigned long long)(k0[b + q] & row_mask) << 11) | (unsigned long long)q : ~0ull;
+    __syncwarp();
+    for (int size = 2; size <= N; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int q = lane; q < (N >> 1); q += 32) {
+                const int lo = 2 * q - (q & (stride - 1)), hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const unsigned long long x = sk[lo], y = sk[hi];
+                if ((x > y) == up) {
+                    sk[lo] = y;
+                    sk[hi] = x;
+                }
+            }
+            __syncwarp();
+        }
+    }
+    for (int q = lane; q < n; q += 32) {
+        const int src = (int)(sk[q] & 2047ull);
+        k1[b + q] = k0[b + src];
+        v1[b + q] = v0[b + src];
+    }
+}
+
 // Segment (column) begin/end offsets of the group's products.
 __global__ void k_seg_bounds(int64_t ncols, const int64_t* __restrict__ Bcp, int64_t e0, const int64_t* __restrict__ eoff,
                              int* __restrict__ beg, int* __restrict__ end) {
@@ -211,18 +292,60 @@ int64_t esc_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int64_t c
                     launch(c, k_seg_bounds, dim3(grid_for(c, ng, 256)), dim3(256), 0, ng, (const int64_t*)(B.cp + j0), e0,
                            (const int64_t*)eoff.as<int64_t>(), beg.as<int>(), end.as<int>());
                     if (P) {
-                        // one stable LSD radix sort by (column, row) over the group
-                        size_t tb = 0;
-                        const int bits = row_bits + col_bits;
-                        SLAPCU_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k0.as<K>(), k1.as<K>(), v0.as<Acc>(),
-                                                                    v1.as<Acc>(), (int)P, 0, bits, c.stream));
-                        DevBuf tmp(tb, c.stream);
-                        timed(c, KC_SYM_HEAVY, [&] {
-                            SLAPCU_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, k0.as<K>(), k1.as<K>(),
-                                                                        v0.as<Acc>(), v1.as<Acc>(), (int)P, 0, bits,
-                                                                        c.stream));
-                        });
-                        ++c.launches;
+                        // short columns: one CTA each, shared-memory sort; long columns:
+                        // a segmented radix sort over just their row bits (stable, LSD)
+                        std::vector<int> tiny, small, lb, le;
+                        int64_t off = 0;
+                        for (int64_t jj = 0; jj < ng; ++jj) {
+                            const int64_t pj = hf[j0 + jj];
+                            if (pj > 1 && pj <= kWarpSort) tiny.push_back((int)jj);
+                            if (pj > kWarpSort && pj <= kSmallSort) small.push_back((int)jj);
+                            if (pj > kSmallSort) {
+                                lb.push_back((int)off);
+                                le.push_back((int)(off + pj));
+                            }
+                            off += pj;
+                        }
+                        if (tiny.size() + small.size() + lb.size() < size_t(ng)) {  // columns with 0 / 1 products are sorted already
+                            SLAPCU_CUDA(cudaMemcpyAsync(k1.get(), k0.get(), sizeof(K) * P, cudaMemcpyDeviceToDevice, c.stream));
+                            SLAPCU_CUDA(cudaMemcpyAsync(v1.get(), v0.get(), sizeof(Acc) * P, cudaMemcpyDeviceToDevice, c.stream));
+                        }
+                        if (!tiny.empty()) {
+                            DevBuf dl(sizeof(int) * tiny.size(), c.stream);
+                            SLAPCU_CUDA(cudaMemcpyAsync(dl.get(), tiny.data(), sizeof(int) * tiny.size(),
+                                                        cudaMemcpyHostToDevice, c.stream));
+                            launch(c, k_sort_warp<K, Acc>, dim3((unsigned)((tiny.size() + 7) / 8)), dim3(256), 0,
+                                   (int)tiny.size(), (const int*)dl.as<int>(), (const int*)beg.as<int>(),
+                                   (const int*)end.as<int>(), K((int64_t(1) << row_bits) - 1), (const K*)k0.as<K>(),
+                                   (const Acc*)v0.as<Acc>(), k1.as<K>(), v1.as<Acc>());
+                        }
+                        if (!small.empty()) {
+                            DevBuf dl(sizeof(int) * small.size(), c.stream);
+                            SLAPCU_CUDA(cudaMemcpyAsync(dl.get(), small.data(), sizeof(int) * small.size(),
+                                                        cudaMemcpyHostToDevice, c.stream));
+                            launch(c, k_sort_small<K, Acc>, dim3((unsigned)small.size()), dim3(256), 0,
+                                   (const int*)dl.as<int>(), (const int*)beg.as<int>(), (const int*)end.as<int>(),
+                                   K((int64_t(1) << row_bits) - 1), (const K*)k0.as<K>(), (const Acc*)v0.as<Acc>(),
+                                   k1.as<K>(), v1.as<Acc>());
+                        }
+                        if (!lb.empty()) {
+                            const int nl = (int)lb.size();
+                            DevBuf dlb(sizeof(int) * nl, c.stream), dle(sizeof(int) * nl, c.stream);
+                            SLAPCU_CUDA(cudaMemcpyAsync(dlb.get(), lb.data(), sizeof(int) * nl, cudaMemcpyHostToDevice, c.stream));
+                            SLAPCU_CUDA(cudaMemcpyAsync(dle.get(), le.data(), sizeof(int) * nl, cudaMemcpyHostToDevice, c.stream));
+                            size_t tb = 0;
+                            SLAPCU_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(
+                                nullptr, tb, k0.as<K>(), k1.as<K>(), v0.as<Acc>(), v1.as<Acc>(), (int)P, nl,
+                                dlb.as<int>(), dle.as<int>(), 0, row_bits, c.stream));
+                            DevBuf tmp(tb, c.stream);
+                            timed(c, KC_SYM_HEAVY, [&] {
+                                SLAPCU_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(
+                                    tmp.get(), tb, k0.as<K>(), k1.as<K>(), v0.as<Acc>(), v1.as<Acc>(), (int)P, nl,
+                                    dlb.as<int>(), dle.as<int>(), 0, row_bits, c.stream));
+                            });
+                            ++c.launches;
+                        }
+                        SLAPCU_CUDA(cudaStreamSynchronize(c.stream));  // host lists above live until here
                     }
                     launch(c, k_run_heads<K>, dim3(grid_for(c, P + 1, 256)), dim3(256), 0, P, (const K*)k1.as<K>(),
                            head.as<int>());

@@ -122,6 +122,7 @@ def test_direct_value_pass(port, sr, vtl, hash_, rank):
     a = with_values(port, port.gen_rmat(14 if hash_ else 12), sr.id)
     want = port.spgemm(sr.id, a, a)
     ctx = P.Context()
+    ctx.set_option(L.OPT_DIRECT_ESC, 0)  # the bitmap value pass is the subject
     ctx.set_option(L.OPT_DIRECT_TILE_ROWS_LOG2, 14 if hash_ else 12)
     ctx.set_option(L.OPT_DIRECT_VALUE_TILE_ROWS_LOG2, vtl)
     ctx.set_option(L.OPT_DIRECT_VALUE_HASH, hash_)
@@ -141,6 +142,7 @@ def test_direct_value_tmajor(port, sr, tmajor, dense_rows):
     a = with_values(port, port.gen_rmat(14), sr.id)
     want = port.spgemm(sr.id, a, a)
     ctx = P.Context()
+    ctx.set_option(L.OPT_DIRECT_ESC, 0)  # the bitmap value pass is the subject
     ctx.set_option(L.OPT_DIRECT_VALUE_TMAJOR, tmajor)
     ctx.set_option(L.OPT_DIRECT_VALUE_DENSE_ROWS, dense_rows)
     ctx.set_option(L.OPT_DIRECT_VALUE_HASH, 0)
@@ -159,6 +161,7 @@ def test_direct_value_interleave(port, sr, interleave):
     a = with_values(port, port.gen_rmat(13), sr.id)
     want = port.spgemm(sr.id, a, a)
     ctx = P.Context()
+    ctx.set_option(L.OPT_DIRECT_ESC, 0)  # the bitmap value pass is the subject
     ctx.set_option(L.OPT_DIRECT_TILE_ROWS_LOG2, 12)
     ctx.set_option(L.OPT_DIRECT_VALUE_INTERLEAVE, interleave)
     got = P.local_spgemm(to_device(a), to_device(a), sr, ctx=ctx, method="direct")

@@ -110,3 +110,14 @@ def test_esc_capacity_budget_error(port):
     st = ctx.lib.slapcu_spgemm_direct(ctx.h, C.byref(da.view()), C.byref(da.view()), sr.id, 2, cap, cp.data_ptr(),
                                       rw.data_ptr(), vv.data_ptr(), C.byref(nz))
     assert st == 5 and nz.value == want.colptr[-1]  # BudgetError with the exact requirement
+
+
+def test_esc_auto_policy(port):
+    """Default (auto): a value semiring with compression < 2 takes ESC (its
+    results are then bit-identical to the reference even without the
+    deterministic option); R-MAT squares (cf ~ 3-4) stay on the bitmap path
+    (fp results within tolerance).  Both are correct."""
+    sr = P.PlusTimesF64
+    er = port.gen_er(1 << 13, 8 << 13, 3)
+    got = P.local_spgemm(to_device(er), to_device(er), sr, method="direct")
+    bit_equal(got, want_of(port, sr.id, er, er), "ER auto")
