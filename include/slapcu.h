@@ -422,6 +422,19 @@ slapcu_status slapcu_summa2d(slapcu_comm comm, const slapcu_csc* A_local, const 
 slapcu_status slapcu_dist_symbolic_col_nnz(slapcu_comm comm, const slapcu_csc* A_local, const slapcu_csc* B_local,
                                            int64_t* counts, int64_t ncols);
 
+/* algorithms.cpp:267-293 mcl_step on a pr x pc grid (rank = i*pc + j, A_local
+ * = block (i, j) with block_offsets geometry): column sums reduced over the
+ * grid column and checked (1e-9 f64 / 1e-5 f32; SLAPCU_ERR_STOCHASTIC on every
+ * rank), expansion A*A by slapcu_summa2d (layers <= 1; square grid) or, for
+ * layers = c > 1, redistribute to the regular 3D layout (split columns /
+ * rows), slapcu_ca3d, redistribute back (all on the device, over NCCL), then
+ * inflation, pruning (kept iff !(v < prune_threshold)) and renormalisation by
+ * the kept column sums reduced over the grid column.  sr: PlusTimes f64 or
+ * f32.  C_local: this rank's block of the result (allocated).  Collective. */
+slapcu_status slapcu_mcl_step_dist(slapcu_comm comm, int pr, int pc, int layers, const slapcu_csc* A_local,
+                                   slapcu_semiring sr, double inflation, double prune_threshold,
+                                   slapcu_csc_out* C_local);
+
 /* spgemm3d.hpp:21-106 ca3d_spgemm on a c x q x q grid (regular variant,
  * grid.cpp:57 rank = l*q*q + i*q + j): A split by columns, B by rows; per
  * layer SUMMA, then C_int's columns are split into c pieces (block_offsets)

@@ -158,6 +158,7 @@ SIGNATURES = [
     ("slapcu_summa2d", _I, [_P, _PV, _PV, _I, _I, _PO, C.POINTER(DistStats)]),
     ("slapcu_ca3d", _I, [_P, _I, _PV, _PV, _I, _I, _PO, C.POINTER(DistStats)]),
     ("slapcu_dist_symbolic_col_nnz", _I, [_P, _PV, _PV, _P, _L]),
+    ("slapcu_mcl_step_dist", _I, [_P, _I, _I, _I, _PV, _I, C.c_double, C.c_double, _PO]),
     ("slapcu_redistribute", _I, [_P, _PV, _L, _L, _L, _L, _I, C.POINTER(Tiling), _I, _PO, C.POINTER(_L),
                                  C.POINTER(_L)]),
     ("slapcu_cb2b_header", _I, [C.c_char_p, C.POINTER(_L), C.POINTER(_L), C.POINTER(_L)]),

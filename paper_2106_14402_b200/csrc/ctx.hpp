@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <functional>
 #include <string>
 #include <tuple>
 #include <utility>
@@ -275,6 +276,10 @@ void exclusive_scan_i64(Ctx& c, const int64_t* in, int64_t* out, int64_t n);
 
 // mcl.cu: algorithms.cpp:267-293 mcl_step around the direct product
 void mcl_step(Ctx& c, const DevCsc& A, int sr, double inflation, double prune, slapcu_csc_out* out);
+void mcl_block_colsums(Ctx& c, const DevCsc& A, int sr, double* sums);
+bool mcl_sums_bad(Ctx& c, const double* sums, int64_t n, double tol);
+void mcl_block_epilogue(Ctx& c, const DevCsc& E, int sr, double inflation, double prune,
+                        const std::function<void(double*, int64_t)>& reduce, slapcu_csc_out* out);
 
 // merge.cu
 int64_t merge_symbolic(Ctx& c, int nparts, const DevCsc* parts, int64_t* c_colptr);

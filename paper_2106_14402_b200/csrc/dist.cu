@@ -723,6 +723,152 @@ slapcu_status slapcu_dist_symbolic_col_nnz(slapcu_comm cm, const slapcu_csc* A_l
     }
 }
 
+// layout.hpp:60-66 block_offsets: parts-1 equal blocks, remainder to the last.
+static std::vector<int64_t> block_offsets(int64_t ext, int parts) {
+    std::vector<int64_t> o(size_t(parts) + 1);
+    const int64_t q = ext / parts;
+    for (int i = 0; i < parts; ++i) o[i] = int64_t(i) * q;
+    o[parts] = ext;
+    return o;
+}
+
+// algorithms.cpp:267-293 mcl_step on a pr x pc grid (rank = i*pc + j):
+// column sums of the input reduced over the grid column and checked (1e-9
+// f64 / 1e-5 f32, StochasticityError on every rank), the expansion A*A by the
+// 2D SUMMA (layers <= 1, square grid) or -- layers = c > 1 -- by
+// redistribute_3d x2 -> ca3d -> redistribute_2d on the device
+// (dist_matrix3d.hpp:117-261 regular variant), then inflation / pruning /
+// renormalisation with the kept column sums reduced over the grid column.
+slapcu_status slapcu_mcl_step_dist(slapcu_comm cm, int pr, int pc, int layers, const slapcu_csc* A_local,
+                                   slapcu_semiring sr, double inflation, double prune_threshold,
+                                   slapcu_csc_out* C_local) {
+    if (!cm || !A_local || !C_local) return SLAPCU_ERR_INVALID;
+    Ctx& c = ctx_of(cm->ctx);
+    try {
+        SLAPCU_CUDA(cudaSetDevice(c.device));
+        if (sr != SLAPCU_PLUS_TIMES_F64 && sr != SLAPCU_PLUS_TIMES_F32)
+            throw Fail{SLAPCU_ERR_INVALID, "mcl step: PlusTimes f64 or f32"};
+        if (pr < 1 || pc < 1 || pr * pc != cm->nranks)
+            throw Fail{SLAPCU_ERR_SHAPE, "grid " + std::to_string(pr) + "x" + std::to_string(pc) + " does not match " +
+                                             std::to_string(cm->nranks) + " ranks"};
+        if (!(inflation > 0.0)) throw Fail{SLAPCU_ERR_SHAPE, "inflation exponent must be positive"};
+        DevCsc A = view(*A_local);
+        resolve(c, A);
+        const int i = cm->rank / pc, j = cm->rank % pc;
+        // global dims from every rank's block dims (grid column 0 rows, grid row 0 cols)
+        const std::vector<int64_t> meta = allgather_meta(cm, c, A, A);
+        int64_t m = 0, n = 0;
+        for (int ii = 0; ii < pr; ++ii) m += meta[kMeta * (ii * pc) + MA_R];
+        for (int jj = 0; jj < pc; ++jj) n += meta[kMeta * jj + MA_C];
+        if (m != n) throw Fail{SLAPCU_ERR_SHAPE, "mcl step needs a square matrix"};
+        const double tol = sr == SLAPCU_PLUS_TIMES_F64 ? 1e-9 : 1e-5;
+        ncclComm_t col = split(cm, "col2d_" + std::to_string(pr) + "x" + std::to_string(pc), j, i);
+        auto col_reduce = [&](double* v, int64_t len) {
+            if (len) SLAPCU_NCCL(ncclAllReduce(v, v, size_t(len), ncclDouble, ncclSum, col, c.stream));
+            cm->calls[kReduce] += 1;
+            cm->bytes[kReduce] += sizeof(double) * len;
+        };
+        {  // algorithms.cpp:270-275 stochasticity check
+            DevBuf sums(sizeof(double) * std::max<int64_t>(A.ncols, 1), c.stream);
+            mcl_block_colsums(c, A, sr, sums.as<double>());
+            col_reduce(sums.as<double>(), A.ncols);
+            int bad = mcl_sums_bad(c, sums.as<double>(), A.ncols, tol) ? 1 : 0;
+            DevBuf f(sizeof(int), c.stream);
+            SLAPCU_CUDA(cudaMemcpyAsync(f.get(), &bad, sizeof(int), cudaMemcpyHostToDevice, c.stream));
+            SLAPCU_NCCL(ncclAllReduce(f.get(), f.get(), 1, ncclInt32, ncclMax, cm->world, c.stream));
+            SLAPCU_CUDA(cudaMemcpyAsync(&bad, f.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+            SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+            if (bad) throw Fail{SLAPCU_ERR_STOCHASTIC, "input column sums deviate from 1"};
+        }
+        slapcu_csc_out E{};
+        struct FreeOut {
+            Ctx& c;
+            slapcu_csc_out& o;
+            ~FreeOut() {
+                if (o.colptr) cudaFreeAsync(o.colptr, c.stream);
+                if (o.rowids) cudaFreeAsync(o.rowids, c.stream);
+                if (o.vals) cudaFreeAsync(o.vals, c.stream);
+            }
+        } free_e{c, E};
+        if (layers <= 1) {
+            if (pr != pc) throw Fail{SLAPCU_ERR_SHAPE, "2D SUMMA needs a square process grid"};
+            const slapcu_status st = slapcu_summa2d(cm, A_local, A_local, sr, SLAPCU_ALG_HYBRID, &E, nullptr);
+            if (st != SLAPCU_OK) return st;
+        } else {
+            const int p = cm->nranks;
+            if (p % layers) throw Fail{SLAPCU_ERR_SHAPE, "cannot split ranks into layers"};
+            int64_t q = 0;
+            if (!is_square(p / layers, &q)) throw Fail{SLAPCU_ERR_SHAPE, "p/c is not a perfect square"};
+            const auto ro = block_offsets(m, pr), co = block_offsets(n, pc);
+            // regular 3D tilings (dist_matrix3d.hpp:54-80): the split dimension in c slabs of q pieces
+            auto tiling3 = [&](bool split_cols, std::vector<int64_t>& rc, std::vector<int64_t>& cc,
+                               std::vector<int32_t>& own) {
+                const auto slabs = block_offsets(n, layers);
+                std::vector<int64_t> cuts;
+                for (int l = 0; l < layers; ++l) {
+                    const auto sub = block_offsets(slabs[l + 1] - slabs[l], (int)q);
+                    for (int x = 0; x < q; ++x) cuts.push_back(slabs[l] + sub[x]);
+                }
+                cuts.push_back(n);
+                const auto other = block_offsets(m, (int)q);
+                own.clear();
+                if (split_cols) {
+                    rc = other;
+                    cc = cuts;
+                    for (int ii = 0; ii < q; ++ii)
+                        for (int lj = 0; lj < layers * q; ++lj)
+                            own.push_back((lj / (int)q) * (int)(q * q) + ii * (int)q + lj % (int)q);
+                } else {
+                    rc = cuts;
+                    cc = other;
+                    for (int li = 0; li < layers * q; ++li)
+                        for (int jj = 0; jj < q; ++jj)
+                            own.push_back((li / (int)q) * (int)(q * q) + (li % (int)q) * (int)q + jj);
+                }
+            };
+            std::vector<int64_t> rc1, cc1, rc2, cc2;
+            std::vector<int32_t> o1, o2;
+            tiling3(true, rc1, cc1, o1);
+            tiling3(false, rc2, cc2, o2);
+            slapcu_tiling t1{(int)rc1.size() - 1, (int)cc1.size() - 1, rc1.data(), cc1.data(), o1.data()};
+            slapcu_tiling t2{(int)rc2.size() - 1, (int)cc2.size() - 1, rc2.data(), cc2.data(), o2.data()};
+            slapcu_csc_out A3{}, B3{}, C3{};
+            FreeOut fa{c, A3}, fb{c, B3}, fc{c, C3};
+            int64_t rs = 0, cs = 0;
+            slapcu_status st = slapcu_redistribute(cm, A_local, ro[i], co[j], m, n, sr, &t1, 0, &A3, &rs, &cs);
+            if (st != SLAPCU_OK) return st;
+            st = slapcu_redistribute(cm, A_local, ro[i], co[j], m, n, sr, &t2, 0, &B3, &rs, &cs);
+            if (st != SLAPCU_OK) return st;
+            const slapcu_csc a3{A3.nrows, A3.ncols, A3.nnz, A3.colptr, A3.rowids, A3.vals};
+            const slapcu_csc b3{B3.nrows, B3.ncols, B3.nnz, B3.colptr, B3.rowids, B3.vals};
+            st = slapcu_ca3d(cm, layers, &a3, &b3, sr, SLAPCU_ALG_HYBRID, &C3, nullptr);
+            if (st != SLAPCU_OK) return st;
+            // C3 is split by columns like A3: this rank's piece of its layer's column block
+            const int qq = (int)(q * q), l = cm->rank / qq, i3 = (cm->rank % qq) / (int)q, j3 = cm->rank % (int)q;
+            // spgemm3d.hpp:86-90: C3 rows = A3's row block, columns = B3's column
+            // block (split rows: n cut into q blocks) cut into c pieces, piece l
+            const auto qb = block_offsets(n, (int)q);
+            const auto pieces = block_offsets(qb[j3 + 1] - qb[j3], layers);
+            const int64_t c3_col = qb[j3] + pieces[l];
+            const int64_t c3_row = block_offsets(m, (int)q)[i3];
+            std::vector<int32_t> own2d;
+            for (int ii = 0; ii < pr; ++ii)
+                for (int jj = 0; jj < pc; ++jj) own2d.push_back(ii * pc + jj);
+            slapcu_tiling t2d{pr, pc, ro.data(), co.data(), own2d.data()};
+            const slapcu_csc c3v{C3.nrows, C3.ncols, C3.nnz, C3.colptr, C3.rowids, C3.vals};
+            st = slapcu_redistribute(cm, &c3v, c3_row, c3_col, m, n, sr, &t2d, 0, &E, &rs, &cs);
+            if (st != SLAPCU_OK) return st;
+        }
+        const DevCsc ev{E.nrows, E.ncols, E.nnz, E.colptr, E.rowids, E.vals};
+        mcl_block_epilogue(c, ev, sr, inflation, prune_threshold, col_reduce, C_local);
+        SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+        return SLAPCU_OK;
+    } catch (const Fail& e) {
+        c.last_error = e.msg;
+        return e.st;
+    }
+}
+
 slapcu_status slapcu_ca3d(slapcu_comm cm, int layers, const slapcu_csc* A_local, const slapcu_csc* B_local,
                           slapcu_semiring sr, slapcu_alg alg, slapcu_csc_out* C_local, slapcu_dist_stats* stats) {
     if (!cm || !A_local || !B_local || !C_local) return SLAPCU_ERR_INVALID;

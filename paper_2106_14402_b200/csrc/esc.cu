@@ -292,21 +292,33 @@ int64_t esc_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int64_t c
                     launch(c, k_seg_bounds, dim3(grid_for(c, ng, 256)), dim3(256), 0, ng, (const int64_t*)(B.cp + j0), e0,
                            (const int64_t*)eoff.as<int64_t>(), beg.as<int>(), end.as<int>());
                     if (P) {
-                        // short columns: one CTA each, shared-memory sort; long columns:
-                        // a segmented radix sort over just their row bits (stable, LSD)
-                        std::vector<int> tiny, small, lb, le;
-                        int64_t off = 0;
+                        // groups of short columns: one warp (<= 256 products) or CTA (<= 2048)
+                        // per column, shared-memory sorts; a group holding any longer column:
+                        // ONE stable LSD radix sort over the (column, row) keys of the group
+                        // (cub's segmented sort runs a long segment on one CTA)
+                        std::vector<int> tiny, small;
+                        bool any_long = false;
                         for (int64_t jj = 0; jj < ng; ++jj) {
                             const int64_t pj = hf[j0 + jj];
                             if (pj > 1 && pj <= kWarpSort) tiny.push_back((int)jj);
                             if (pj > kWarpSort && pj <= kSmallSort) small.push_back((int)jj);
-                            if (pj > kSmallSort) {
-                                lb.push_back((int)off);
-                                le.push_back((int)(off + pj));
-                            }
-                            off += pj;
+                            if (pj > kSmallSort) any_long = true;
                         }
-                        if (tiny.size() + small.size() + lb.size() < size_t(ng)) {  // columns with 0 / 1 products are sorted already
+                        if (any_long) {
+                            size_t tb = 0;
+                            const int bits = row_bits + col_bits;
+                            SLAPCU_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k0.as<K>(), k1.as<K>(), v0.as<Acc>(),
+                                                                        v1.as<Acc>(), (int)P, 0, bits, c.stream));
+                            DevBuf tmp(tb, c.stream);
+                            timed(c, KC_SYM_HEAVY, [&] {
+                                SLAPCU_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, k0.as<K>(), k1.as<K>(),
+                                                                            v0.as<Acc>(), v1.as<Acc>(), (int)P, 0, bits,
+                                                                            c.stream));
+                            });
+                            ++c.launches;
+                            tiny.clear();
+                            small.clear();
+                        } else if (tiny.size() + small.size() < size_t(ng)) {  // 0 / 1-product columns: as they are
                             SLAPCU_CUDA(cudaMemcpyAsync(k1.get(), k0.get(), sizeof(K) * P, cudaMemcpyDeviceToDevice, c.stream));
                             SLAPCU_CUDA(cudaMemcpyAsync(v1.get(), v0.get(), sizeof(Acc) * P, cudaMemcpyDeviceToDevice, c.stream));
                         }
@@ -327,23 +339,6 @@ int64_t esc_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int64_t c
                                    (const int*)dl.as<int>(), (const int*)beg.as<int>(), (const int*)end.as<int>(),
                                    K((int64_t(1) << row_bits) - 1), (const K*)k0.as<K>(), (const Acc*)v0.as<Acc>(),
                                    k1.as<K>(), v1.as<Acc>());
-                        }
-                        if (!lb.empty()) {
-                            const int nl = (int)lb.size();
-                            DevBuf dlb(sizeof(int) * nl, c.stream), dle(sizeof(int) * nl, c.stream);
-                            SLAPCU_CUDA(cudaMemcpyAsync(dlb.get(), lb.data(), sizeof(int) * nl, cudaMemcpyHostToDevice, c.stream));
-                            SLAPCU_CUDA(cudaMemcpyAsync(dle.get(), le.data(), sizeof(int) * nl, cudaMemcpyHostToDevice, c.stream));
-                            size_t tb = 0;
-                            SLAPCU_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(
-                                nullptr, tb, k0.as<K>(), k1.as<K>(), v0.as<Acc>(), v1.as<Acc>(), (int)P, nl,
-                                dlb.as<int>(), dle.as<int>(), 0, row_bits, c.stream));
-                            DevBuf tmp(tb, c.stream);
-                            timed(c, KC_SYM_HEAVY, [&] {
-                                SLAPCU_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(
-                                    tmp.get(), tb, k0.as<K>(), k1.as<K>(), v0.as<Acc>(), v1.as<Acc>(), (int)P, nl,
-                                    dlb.as<int>(), dle.as<int>(), 0, row_bits, c.stream));
-                            });
-                            ++c.launches;
                         }
                         SLAPCU_CUDA(cudaStreamSynchronize(c.stream));  // host lists above live until here
                     }

@@ -10,6 +10,7 @@
 #include <cub/cub.cuh>
 
 #include <cmath>
+#include <functional>
 
 #include "kern.cuh"
 
@@ -123,7 +124,92 @@ __global__ void k_mcl_write(int64_t ncols, const int64_t* __restrict__ cp, const
     }
 }
 
+template <class T>
+__global__ void k_col_sums(int64_t ncols, const int64_t* __restrict__ cp, const T* __restrict__ v,
+                           double* __restrict__ sums) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t j = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; j < ncols;
+         j += (int64_t(gridDim.x) * blockDim.x) >> 5) {
+        double s = 0;
+        for (int64_t e = cp[j] + lane; e < cp[j + 1]; e += 32) s += (double)v[e];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) sums[j] = s;
+    }
+}
+
+__global__ void k_sums_check(int64_t n, const double* __restrict__ s, double tol, int* __restrict__ bad) {
+    for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < n; j += int64_t(gridDim.x) * blockDim.x)
+        if (fabs(s[j] - 1.0) > tol) atomicExch(bad, 1);
+}
+
 }  // namespace
+
+// Block pieces of mcl_step for the distributed driver (dist.cu): column sums
+// of a block (double), the sum check, and the epilogue of an expanded block
+// whose column sums are reduced by `reduce` (the grid-column allreduce)
+// between the counting and the writing pass.
+void mcl_block_colsums(Ctx& c, const DevCsc& A, int sr, double* sums) {
+    dispatch_sr(sr, [&](auto id) {
+        constexpr int ID = decltype(id)::value;
+        if constexpr (ID == SLAPCU_PLUS_TIMES_F64 || ID == SLAPCU_PLUS_TIMES_F32) {
+            using T = typename Sr<ID>::T;
+            if (A.ncols)
+                launch(c, k_col_sums<T>, dim3(grid_for(c, A.ncols * 32, 256)), dim3(256), 0, A.ncols, A.cp,
+                       static_cast<const T*>(A.v), sums);
+        } else {
+            throw Fail{SLAPCU_ERR_INVALID, "mcl step: PlusTimes f64 or f32"};
+        }
+    });
+}
+
+bool mcl_sums_bad(Ctx& c, const double* sums, int64_t n, double tol) {
+    DevBuf bad(sizeof(int), c.stream);
+    SLAPCU_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), c.stream));
+    if (n) launch(c, k_sums_check, dim3(grid_for(c, n, 256)), dim3(256), 0, n, sums, tol, bad.as<int>());
+    int h = 0;
+    SLAPCU_CUDA(cudaMemcpyAsync(&h, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+    return h != 0;
+}
+
+void mcl_block_epilogue(Ctx& c, const DevCsc& E_, int sr, double inflation, double prune,
+                        const std::function<void(double*, int64_t)>& reduce, slapcu_csc_out* out) {
+    DevCsc E = E_;
+    resolve(c, E);
+    const int64_t n = E.ncols;
+    dispatch_sr(sr, [&](auto id) {
+        constexpr int ID = decltype(id)::value;
+        if constexpr (ID == SLAPCU_PLUS_TIMES_F64 || ID == SLAPCU_PLUS_TIMES_F32) {
+            using T = typename Sr<ID>::T;
+            DevBuf kept(sizeof(int64_t) * (n + 1), c.stream), sums(sizeof(double) * std::max<int64_t>(n, 1), c.stream);
+            SLAPCU_CUDA(cudaMemsetAsync(kept.as<int64_t>() + n, 0, sizeof(int64_t), c.stream));
+            const int mode = inflation == 2.0 ? kSquare : inflation == 1.0 ? kIdentity : kPow;
+            auto kc = mode == kSquare ? k_mcl_count<T, kSquare> : mode == kIdentity ? k_mcl_count<T, kIdentity>
+                                                                                    : k_mcl_count<T, kPow>;
+            auto kw = mode == kSquare ? k_mcl_write<T, kSquare> : mode == kIdentity ? k_mcl_write<T, kIdentity>
+                                                                                    : k_mcl_write<T, kPow>;
+            if (n)
+                launch(c, kc, dim3(grid_for(c, n * 32, 256)), dim3(256), 0, n, E.cp, static_cast<const T*>(E.v),
+                       inflation, prune, kept.as<int64_t>(), sums.as<double>());
+            reduce(sums.as<double>(), n);  // kept entries are local; their sums span the grid column
+            out->nrows = E.nrows;
+            out->ncols = n;
+            SLAPCU_CUDA(cudaMallocAsync((void**)&out->colptr, sizeof(int64_t) * (n + 1), c.stream));
+            exclusive_scan_i64(c, kept.as<int64_t>(), out->colptr, n + 1);
+            SLAPCU_CUDA(cudaMemcpyAsync(&out->nnz, out->colptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
+            SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+            SLAPCU_CUDA(cudaMallocAsync((void**)&out->rowids, sizeof(int32_t) * std::max<int64_t>(out->nnz, 1), c.stream));
+            SLAPCU_CUDA(cudaMallocAsync(&out->vals, sizeof(T) * std::max<int64_t>(out->nnz, 1), c.stream));
+            if (n)
+                launch(c, kw, dim3(grid_for(c, n * 32, 256)), dim3(256), 0, n, E.cp, E.rw, static_cast<const T*>(E.v),
+                       inflation, prune, (const double*)sums.as<double>(), (const int64_t*)out->colptr, out->rowids,
+                       static_cast<T*>(out->vals));
+        } else {
+            throw Fail{SLAPCU_ERR_INVALID, "mcl step: PlusTimes f64 or f32"};
+        }
+    });
+}
 
 void mcl_step(Ctx& c, const DevCsc& A_, int sr, double inflation, double prune, slapcu_csc_out* out) {
     if (sr != SLAPCU_PLUS_TIMES_F64 && sr != SLAPCU_PLUS_TIMES_F32)

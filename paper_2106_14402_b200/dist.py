@@ -118,6 +118,24 @@ def ca3d_spgemm(a3_local: DeviceCsc, b3_local: DeviceCsc, sr: Semiring, comm: Nc
     return _from_out(ctx, out, sr), _stats(st)
 
 
+def mcl_step(a_local: DeviceCsc, pr: int, pc: int, comm: NcclComm, layers: int = 1, inflation: float = 2.0,
+             prune: float = 1e-4, sr: Semiring = None):
+    """algorithms.cpp:267-293 mcl_step on a pr x pc grid (rank = i*pc + j,
+    `a_local` = block (i, j)): expansion by the 2D SUMMA (layers <= 1) or the
+    3D path (device redistribute_3d x2 -> ca3d -> redistribute_2d), then the
+    inflation / prune / renormalisation epilogue with column sums reduced
+    over the grid column -- all on the device.  Returns this rank's block."""
+    from .spgemm import PlusTimesF64
+
+    sr = _sr(sr or PlusTimesF64)
+    ctx = comm.ctx
+    ctx.sync_stream()
+    out = L.CscOut()
+    ctx.check(comm.lib.slapcu_mcl_step_dist(comm.h, pr, pc, layers, C.byref(a_local.view()), sr.id, float(inflation),
+                                            float(prune), C.byref(out)), "mcl_step_dist")
+    return _from_out(ctx, out, sr)
+
+
 def free_out(ctx: Context, out: L.CscOut):
     ctx.check(ctx.lib.slapcu_csc_free(ctx.h, C.byref(out)), "csc_free")
 

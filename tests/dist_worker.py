@@ -47,6 +47,9 @@ def main():
     P.default_context().set_option(L.OPT_SUMMA_CONCAT, a.concat)
     comm = D.NcclComm()
     port = oracle.port()
+    if a.case == "mcl":  # algorithms.cpp:267-293 on a pr x pc grid, 2D or 3D expansion
+        mcl_case(a, comm, port, rank, world)
+        return
     for sr in (P.PlusTimesF64, P.MinPlusI32, P.OrAnd, P.PlusTimesI64):
         A = P.fill_values(P.gen_rmat(a.scale, 8, 3), sr, KIND[sr.id])
         n = A.nrows
@@ -109,6 +112,52 @@ def main():
     dist.barrier()
     if rank == 0:
         print(f"DIST_OK {a.case} p={world}", flush=True)
+    dist.destroy_process_group()
+
+
+def stochastic_rmat(port, scale, seed=1):
+    """R-MAT pattern plus self loops (no empty column), values 1/deg(col)."""
+    m = port.gen_rmat(scale, 8, seed)
+    n = m.ncols
+    rows = np.concatenate([m.rowids.astype(np.int64), np.arange(n)])
+    cols = np.concatenate([np.repeat(np.arange(n), np.diff(m.colptr)), np.arange(n)])
+    key = np.unique(cols * n + rows)
+    cc, rr = key // n, (key % n).astype(np.int32)
+    cp = np.zeros(n + 1, np.int64)
+    np.cumsum(np.bincount(cc, minlength=n), out=cp[1:])
+    deg = np.diff(cp)
+    return oracle.Csc(n, n, cp, rr, np.repeat(1.0 / deg, deg))
+
+
+def mcl_case(a, comm, port, rank, world):
+    pr = {1: 1, 2: 1, 4: 2, 8: 2}[world]
+    pc = world // pr
+    h = stochastic_rmat(port, a.scale)
+    n = h.ncols
+    A = P.CscMatrix(n, n, h.colptr, h.rowids, h.vals).to_device()
+    i, j = rank // pc, rank % pc
+    r0, rl, c0, cl = G.block2d_range(n, n, pr, pc, i, j)
+    ab = D.device_block(A, r0, rl, c0, cl)
+    want = oracle.ref().mcl_step(h, 2.0, 1e-4) if rank == 0 else None
+    # square grids run the 2D expansion and (layers > 1) the 3D one; others only 3D
+    layer_list = ([1] + ([a.layers] if a.layers > 1 else [])) if pr == pc else [a.layers]
+    for layers in layer_list:
+        cb = D.mcl_step(ab, pr, pc, comm, layers, 2.0, 1e-4)
+        full = D.gather_to_host(cb, r0, c0, n, n)
+        if rank == 0:
+            assert_parity(full, want, oracle.PLUS_TIMES_F64, f"mcl p={world} {pr}x{pc} layers={layers}")
+        torch.cuda.synchronize()
+    # a non-stochastic input raises StochasticityError on every rank
+    bad = P.CscMatrix(n, n, h.colptr, h.rowids, h.vals * 1.5).to_device()
+    try:
+        D.mcl_step(D.device_block(bad, r0, rl, c0, cl), pr, pc, comm, 1 if pr == pc else a.layers)
+        raise AssertionError("expected StochasticityError")
+    except P.errors.StochasticityError:
+        pass
+    comm.close()
+    dist.barrier()
+    if rank == 0:
+        print(f"DIST_OK mcl p={world}", flush=True)
     dist.destroy_process_group()
 
 

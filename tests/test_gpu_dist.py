@@ -41,3 +41,18 @@ def test_ca3d_p4_c4():
 @pytest.mark.skipif(NGPU < 8, reason="needs 8 GPUs")
 def test_ca3d_p8_c2():
     run(8, "--case", "ca3d", "--layers", "2")
+
+
+@pytest.mark.skipif(NGPU < 1, reason="needs a GPU")
+def test_mcl_dist_p1():
+    run(1, "--case", "mcl", "--layers", "1")
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
+def test_mcl_dist_p2_3d():
+    run(2, "--case", "mcl", "--layers", "2")
+
+
+@pytest.mark.skipif(NGPU < 4, reason="needs 4 GPUs")
+def test_mcl_dist_p4_2d_and_3d():
+    run(4, "--case", "mcl", "--layers", "4")

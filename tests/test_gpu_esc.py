@@ -15,7 +15,7 @@ import numpy as np
 import pytest
 
 import oracle
-from tests.helpers import to_device, to_oracle, with_values
+from tests.helpers import assert_parity, to_device, to_oracle, with_values
 
 pytestmark = pytest.mark.gpu
 
@@ -113,11 +113,24 @@ def test_esc_capacity_budget_error(port):
 
 
 def test_esc_auto_policy(port):
-    """Default (auto): a value semiring with compression < 2 takes ESC (its
-    results are then bit-identical to the reference even without the
-    deterministic option); R-MAT squares (cf ~ 3-4) stay on the bitmap path
-    (fp results within tolerance).  Both are correct."""
+    """Default (auto): a value semiring whose columns are heavy (> 4096
+    multiplies on average) and whose sampled compression is below 2 takes
+    ESC -- its values are then bit-identical to the reference even without
+    the deterministic option (a C5-like tall-skinny product); light or
+    well-compressing products stay on the bitmap / hash paths (within
+    tolerance).  Both are correct."""
     sr = P.PlusTimesF64
-    er = port.gen_er(1 << 13, 8 << 13, 3)
-    got = P.local_spgemm(to_device(er), to_device(er), sr, method="direct")
-    bit_equal(got, want_of(port, sr.id, er, er), "ER auto")
+    a = port.gen_er(1 << 16, 16 << 16, 4)  # values U[0,1)
+    rng = np.random.default_rng(5)
+    n, m = a.ncols, 16
+    cols = rng.integers(0, m, n)
+    cp = np.zeros(m + 1, np.int64)
+    np.cumsum(np.bincount(cols, minlength=m), out=cp[1:])
+    b = oracle.Csc(n, m, cp, np.argsort(cols, kind="stable").astype(np.int32), rng.random(n))
+    want = want_of(port, sr.id, a, b)
+    assert want.colptr[-1] * 2 > port.estimate_flops(a, b)[0]  # compression < 2
+    bit_equal(P.local_spgemm(to_device(a), to_device(b), sr, method="direct"), want, "tall-skinny auto")
+    ctx = P.Context()
+    ctx.set_option(L.OPT_DIRECT_ESC, 0)
+    got = P.local_spgemm(to_device(a), to_device(b), sr, ctx=ctx, method="direct")
+    assert_parity(got, want, sr.id, "tall-skinny bitmap path")

@@ -248,3 +248,49 @@ def test_staging_budget_error():
     st = ctx.lib.slapcu_spgemm_begin(ctx.h, C.byref(a.view()), C.byref(a.view()), P.OrAnd.id, 2, 1024,
                                      cp.data_ptr(), C.byref(nnz))
     assert st == 5  # SLAPCU_ERR_BUDGET
+
+
+def test_dcsc_upload(port):
+    """local_matrix.hpp:88-150 DCSC (jc / cp over nonempty columns, int32)
+    to the device: the dense colptr is built on the GPU; the uploaded block
+    multiplies like its CSC twin and downloads back to the same CSC."""
+    import ctypes as C
+
+    from paper_2106_14402_b200 import _lib as L
+
+    a = port.gen_rmat(10)
+    a = a.with_vals(port.fill_values(oracle.PLUS_TIMES_F64, 2, a))
+    cnt = np.diff(a.colptr)
+    # drop every third column to get hypersparse blocks with empty columns
+    keep = np.ones(a.ncols, bool)
+    keep[::3] = False
+    rows, vals, cp, jc = [], [], [0], []
+    for j in range(a.ncols):
+        if keep[j] and cnt[j]:
+            s, e = a.colptr[j], a.colptr[j + 1]
+            rows.append(a.rowids[s:e])
+            vals.append(a.vals[s:e])
+            jc.append(j)
+            cp.append(cp[-1] + int(e - s))
+    rows = np.concatenate(rows).astype(np.int32)
+    vals = np.concatenate(vals)
+    jc = np.asarray(jc, np.int32)
+    cp = np.asarray(cp, np.int32)
+    ctx = P.Context()
+    out = L.CscOut()
+    ctx.check(ctx.lib.slapcu_dcsc_upload(ctx.h, a.nrows, a.ncols, len(jc), jc.ctypes.data, cp.ctypes.data,
+                                         rows.ctypes.data, vals.ctypes.data, oracle.PLUS_TIMES_F64, C.byref(out)),
+              "dcsc_upload")
+    view = L.CscView(out.nrows, out.ncols, out.nnz, out.colptr, out.rowids, out.vals)
+    host = L.CscOut()
+    ctx.check(ctx.lib.slapcu_csc_download(ctx.h, C.byref(view), oracle.PLUS_TIMES_F64, C.byref(host)), "download")
+    colptr = np.ctypeslib.as_array(C.cast(host.colptr, C.POINTER(C.c_int64)), shape=(a.ncols + 1,)).copy()
+    want_cp = np.zeros(a.ncols + 1, np.int64)
+    for x, j in enumerate(jc):
+        want_cp[j + 1] = cp[x + 1] - cp[x]
+    want_cp = np.cumsum(want_cp)
+    assert np.array_equal(colptr, want_cp)
+    got_rows = np.ctypeslib.as_array(C.cast(host.rowids, C.POINTER(C.c_int32)), shape=(int(host.nnz),)).copy()
+    assert np.array_equal(got_rows, rows)
+    ctx.lib.slapcu_host_free(C.byref(host))
+    ctx.check(ctx.lib.slapcu_csc_free(ctx.h, C.byref(out)), "free")
