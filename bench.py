@@ -60,9 +60,7 @@ def parse():
     ap.add_argument("--dense-min", type=int, default=None, help="byte-flag pattern path for flops >= this (0 off)")
     ap.add_argument("--direct-tile-log2", type=int, default=0, help="rows per direct-path item (0 = default)")
     ap.add_argument("--direct-split", type=int, default=None, help="direct path: split items above this many flops")
-    ap.add_argument("--mark-mode", type=int, default=None, help="direct path bitmap update mode (0/1/2)")
     ap.add_argument("--form-threads", type=int, default=None, help="direct path form CTA size")
-    ap.add_argument("--emit-threads", type=int, default=None, help="direct path emit CTA size")
     ap.add_argument("--dense-run", type=int, default=None, help="direct path dense A-run threshold (0 off)")
     ap.add_argument("--persistent", type=int, default=None, help="direct path form kernel persistent (1) or not (0)")
     ap.add_argument("--value-tile-log2", type=int, default=None, help="direct path value pass sub-tile rows")
@@ -71,9 +69,7 @@ def parse():
     ap.add_argument("--value-rank", type=int, default=None, help="direct path value pass rank chunk (0 = sub-tiles)")
     ap.add_argument("--value-interleave", type=int, default=None,
                     help="direct path value pass: 4-byte values gathered with their rows (1) or not (0)")
-    ap.add_argument("--quads", type=int, default=None, help="direct path: lane-contiguous quads (1) or strided (0)")
     ap.add_argument("--tile-major", type=int, default=None, help="direct path form: units ordered by row tile (1)")
-    ap.add_argument("--form-walk", type=int, default=None, help="direct path form: 1 packed long-run products")
     ap.add_argument("--short-run", type=int, default=None, help="direct path form: per-thread run threshold")
     ap.add_argument("--value-tmajor", type=int, default=None, help="direct value pass: tile-major table + row-order chunks")
     ap.add_argument("--words", type=int, default=None, help="direct form: walk A's (word, mask) pairs")
@@ -103,22 +99,14 @@ def apply_options(ctx, args):
         ctx.set_option(L.OPT_DIRECT_TILE_ROWS_LOG2, args.direct_tile_log2)
     if args.direct_split is not None:
         ctx.set_option(L.OPT_DIRECT_SPLIT_FLOPS, args.direct_split)
-    if args.mark_mode is not None:
-        ctx.set_option(L.OPT_DIRECT_MARK_MODE, args.mark_mode)
     if args.form_threads is not None:
         ctx.set_option(L.OPT_DIRECT_FORM_THREADS, args.form_threads)
-    if args.emit_threads is not None:
-        ctx.set_option(L.OPT_DIRECT_EMIT_THREADS, args.emit_threads)
     if args.dense_run is not None:
         ctx.set_option(L.OPT_DIRECT_DENSE_RUN_MIN, args.dense_run)
     if args.persistent is not None:
         ctx.set_option(L.OPT_DIRECT_PERSISTENT, args.persistent)
-    if args.quads is not None:
-        ctx.set_option(L.OPT_DIRECT_QUADS, args.quads)
     if args.tile_major is not None:
         ctx.set_option(L.OPT_DIRECT_TILE_MAJOR, args.tile_major)
-    if args.form_walk is not None:
-        ctx.set_option(L.OPT_DIRECT_FORM_WALK, args.form_walk)
     if args.short_run is not None:
         ctx.set_option(L.OPT_DIRECT_SHORT_RUN, args.short_run)
     if args.value_tmajor is not None:

@@ -127,32 +127,27 @@ typedef enum {
     SLAPCU_OPT_DIRECT_TILE_ROWS_LOG2 = 9,  /* direct path: rows per (column, row tile) item (default 17) */
     SLAPCU_OPT_DIRECT_SPLIT_FLOPS = 10,    /* direct path: items with more multiplies than this are formed
                                               by several CTAs over equal-flops parts of B(:,j) (>= 1024) */
-    SLAPCU_OPT_DIRECT_MARK_MODE = 11,      /* direct path bitmap update (test-then-set per product):
-                                              0 (default) the touched-word summary is rebuilt by ballots
-                                              after the walk, 2 it is kept per update */
+    SLAPCU_OPT_DIRECT_MARK_MODE = 11,      /* retired (round 2): only 0 (test-then-set, summary by ballots) */
     SLAPCU_OPT_DIRECT_FORM_THREADS = 12,   /* direct path: threads per form CTA (128, 256, 512) */
-    SLAPCU_OPT_DIRECT_EMIT_THREADS = 13,   /* direct path emit granularity: 128 (default) = one 4-warp
-                                              CTA per item; 32 = one warp per (item, 128-word block) */
+    SLAPCU_OPT_DIRECT_EMIT_THREADS = 13,   /* retired (round 2): only 128 (one 4-warp CTA per item) */
     SLAPCU_OPT_DIRECT_DENSE_RUN_MIN = 14,  /* direct path: A(:,k) runs inside one row tile with at least
                                               this many entries are OR-ed as cached tile bitmaps
-                                              (default 2048, 0 = never) */
+                                              (row form only; default 4096, 0 = never) */
     SLAPCU_OPT_DIRECT_PERSISTENT = 15,     /* direct path form kernel: 1 persistent CTAs taking units by
                                               ticket, 0 one CTA per unit */
-    SLAPCU_OPT_DIRECT_QUADS = 16,          /* direct path: 1 = each lane takes 4 consecutive entries of a
-                                              run (16-byte loads) and merges rows sharing a word before
-                                              the shared-memory update */
-    SLAPCU_OPT_DIRECT_VALUE_TILE_ROWS_LOG2 = 17, /* direct path value pass: rows per shared value array
-                                                    (12..15, default 14) */
+    SLAPCU_OPT_DIRECT_QUADS = 16,          /* retired (round 2): only 0 */
+    SLAPCU_OPT_DIRECT_VALUE_TILE_ROWS_LOG2 = 17, /* direct path value pass, sub-tile mode (VALUE_RANK = 0):
+                                                    rows per shared value array (10..15, default 13) */
     SLAPCU_OPT_DIRECT_VALUE_THREADS = 18,  /* direct path value pass: threads per CTA (256, 512) */
     SLAPCU_OPT_SUMMA_CONCAT = 19,          /* SUMMA / 3D layers: 1 (default) = all stage blocks are
                                               broadcast, then ONE concatenated-k product forms C(i,j)
                                               (no stage partials, no merge); 0 = per-stage products
                                               double-buffered against the broadcasts + stage merge */
-    SLAPCU_OPT_DIRECT_VALUE_HASH = 20,     /* direct path value pass (default: 0 for 4-byte values, 13 for
-                                              8-byte): 1 (= 13) / 13 / 14 = items
-                                              with <= 2^(v-1) outputs take one walk into a shared hash
-                                              table of 2^v slots keyed by their rows; 0 = every item
-                                              takes the row sub-tile pass */
+    SLAPCU_OPT_DIRECT_VALUE_HASH = 20,     /* direct path value pass: 1 (= 13) / 13 / 14 = items with
+                                              <= 2^(v-1) outputs take one walk into a shared hash table of
+                                              2^v slots keyed by their rows; 0 = every item takes the rank
+                                              chunks (or the row sub-tiles when VALUE_RANK = 0).  Default
+                                              (auto): 0 for 4-byte values with rank chunks, else 13 */
     SLAPCU_OPT_DIRECT_VALUE_RANK = 21,     /* direct path value pass: larger items are folded in rank
                                               chunks of at most this many outputs (4096..16384; default
                                               8192 for 4-byte, 4096 for 8-byte accumulators);
@@ -164,10 +159,7 @@ typedef enum {
     SLAPCU_OPT_DIRECT_TILE_MAJOR = 23,     /* direct path form: 1 = work units ordered by row tile, heaviest
                                               first inside a tile (the tile's A slice stays in L2);
                                               0 = heaviest first over all tiles */
-    SLAPCU_OPT_DIRECT_FORM_WALK = 24,      /* direct path form: long runs of a batch of B entries walked as
-                                              0 = 256-product units, one run per warp step; 1 = packed
-                                              products (the warps split the concatenated products evenly,
-                                              several short runs per warp step) */
+    SLAPCU_OPT_DIRECT_FORM_WALK = 24,      /* retired (round 2): only 0 (256-element units) */
     SLAPCU_OPT_DIRECT_SHORT_RUN = 25,      /* direct path form: runs (A column x row tile) shorter than this
                                               are walked by their own thread (0 = default 8) */
     SLAPCU_OPT_DIRECT_VALUE_TMAJOR = 26,   /* direct path value pass: 1 = 4096-row tile pointers stored

@@ -155,16 +155,14 @@ slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t v
             require(v == 0 || (v >= 10 && v <= 18), SLAPCU_ERR_INVALID, "direct tile rows log2: 0 (auto) or 10..18");
             c.opt.direct_tile_rows_log2 = (int)v;
             break;
+        // retired experiments (measured slower, removed in round 2): only the default is accepted
         case SLAPCU_OPT_DIRECT_MARK_MODE:
-            require(v == 0 || v == 2, SLAPCU_ERR_INVALID,
-                    "mark mode must be 0 (bitmap, summary by ballots) or 2 (summary kept per update)");
-            c.opt.direct_mark_mode = (int)v;
+            require(v == 0, SLAPCU_ERR_INVALID, "mark mode: removed (0 = test-then-set, summary by ballots)");
             break;
         case SLAPCU_OPT_DIRECT_PERSISTENT: c.opt.direct_persistent = v != 0; break;
         case SLAPCU_OPT_DIRECT_TILE_MAJOR: c.opt.direct_tile_major = v != 0; break;
         case SLAPCU_OPT_DIRECT_FORM_WALK:
-            require(v == 0 || v == 1, SLAPCU_ERR_INVALID, "form walk: 0 (256-product units) or 1 (packed products)");
-            c.opt.direct_form_walk = (int)v;
+            require(v == 0, SLAPCU_ERR_INVALID, "form walk: removed (0 = 256-element units)");
             break;
         case SLAPCU_OPT_DIRECT_WORDS: c.opt.direct_words = v != 0; break;
         case SLAPCU_OPT_DIRECT_VALUE_DENSE_ROWS:
@@ -177,7 +175,7 @@ slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t v
             require(v >= 0 && v <= 256, SLAPCU_ERR_INVALID, "short run threshold: 0 (default) .. 256");
             c.opt.direct_short_run = (int)v;
             break;
-        case SLAPCU_OPT_DIRECT_QUADS: c.opt.direct_quads = v != 0; break;
+        case SLAPCU_OPT_DIRECT_QUADS: require(v == 0, SLAPCU_ERR_INVALID, "quads: removed"); break;
         case SLAPCU_OPT_DIRECT_VALUE_TILE_ROWS_LOG2:
             require(v >= 10 && v <= 15, SLAPCU_ERR_INVALID, "value tile rows log2 must be in 10..15");
             c.opt.direct_value_tile_log2 = (int)v;
@@ -204,9 +202,7 @@ slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t v
             c.opt.direct_form_threads = (int)v;
             break;
         case SLAPCU_OPT_DIRECT_EMIT_THREADS:
-            // 0: one CTA per item; 32: one warp per (item, 128-word block) (default)
-            require(v == 0 || v == 32 || v == 128, SLAPCU_ERR_INVALID, "emit mode: 0/128 (CTA per item) or 32 (warp per block)");
-            c.opt.direct_emit_blocks = v == 32;
+            require(v == 0 || v == 128, SLAPCU_ERR_INVALID, "emit: one 128-thread CTA per item (warp-per-block removed)");
             break;
         case SLAPCU_OPT_DIRECT_DENSE_RUN_MIN:
             require(v >= 0, SLAPCU_ERR_INVALID, "dense run threshold must be >= 0");

@@ -126,8 +126,6 @@ struct Options {
     int64_t direct_light_flops_max = 1024;  // direct path: hash path for columns up to this many flops
     int64_t direct_dense_run_min = 4096;    // direct path: A runs (column x tile) this long are OR-ed
                                             // as precomputed tile bitmaps (0 = never)
-    int direct_mark_mode = 0;               // product update: 0 test+set, 1 atomic only, 2 quad-merged
-    int direct_quads = 0;
     int direct_value_tile_log2 = 13;        // direct path value pass: rows per shared value array
     int direct_values_fallback = 0;
     int summa_concat = 1;                   // SUMMA: one concatenated-k product per call (no stage merge)
@@ -136,9 +134,7 @@ struct Options {
     int direct_value_interleave = 1;       // value pass: values gathered with their rows (0 off, 1 4-byte, 2 all)
     int direct_value_rank = -1;  // value pass: large items by rank chunks of this many outputs (0 = sub-tiles,
                                  // -1 = by accumulator width: 8192 for 4-byte, 4096 for 8-byte)
-    int direct_emit_blocks = 0;             // emit: one warp per (item, block) (1) or one CTA per item (0)
     int direct_tile_major = 1;              // form: work units ordered by row tile, then heaviest first
-    int direct_form_walk = 0;               // form: long runs as 256-product units (0) or packed products (1)
     int deterministic = 0;                  // 1: every product by ESC (the reference's fold order, bit-exact fp)
     int direct_esc = -1;                    // 1: ESC for every semiring, 0: bitmap / hash paths, -1 auto (value
                                             // semirings with sampled compression < 2 take ESC)

@@ -107,92 +107,81 @@ struct DenseRuns {
     int dmin;  // 0: none
 };
 
-// Sets bits `b` of word address `a` (shared window): test before set -- a
+// Sets bits `b` of the bitmap word at shared address `a`, test before set: a
 // plain shared load is a broadcast for lanes hitting one word, and most
-// products of a dense column find their bits already set.  MODE 1 skips the
-// test (one shared atomic per product).
-// Sets bits `b` of the bitmap word at shared address `a`; the first setter of
-// a word (it read the word as 0) also sets the word's bit `sb` in the
-// summary word at `sa`, so the passes after the walk visit touched words only.
-// Test before set: a plain shared load is a broadcast for lanes hitting one
-// word, and most products of a dense column find their bits already set.
-// (No "memory" clobber: the bitmap is only read back after a __syncthreads,
-// and a clobber would stop the compiler from issuing the next products'
-// global loads ahead of these shared updates.)
-template <int MODE>
-__device__ __forceinline__ void set_bits(unsigned a, unsigned b, unsigned sa, unsigned sb) {
-    if (MODE == 0) {  // bitmap only; the summary is rebuilt by a ballot pass
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t.reg .b32 x;\n\t"
-            "ld.shared.u32 x, [%0];\n\t"
-            "and.b32 x, x, %1;\n\t"
-            "setp.ne.u32 p, x, %1;\n\t"
-            "@p red.shared.or.b32 [%0], %1;\n\t}" ::"r"(a),
-            "r"(b));
-    } else {
-        asm volatile(
-            "{\n\t.reg .pred p, q;\n\t.reg .b32 x, y;\n\t"
-            "ld.shared.u32 x, [%0];\n\t"
-            "and.b32 y, x, %1;\n\t"
-            "setp.ne.u32 p, y, %1;\n\t"
-            "setp.eq.and.u32 q, x, 0, p;\n\t"
-            "@p red.shared.or.b32 [%0], %1;\n\t"
-            "@q red.shared.or.b32 [%2], %3;\n\t}" ::"r"(a),
-            "r"(b), "r"(sa), "r"(sb));
-    }
+// updates of a dense column find their bits already set (without the test:
+// +20%, round 1).  The touched-word summary is rebuilt by ballots after the
+// walk.  (No "memory" clobber: the bitmap is only read back after a
+// __syncthreads, and a clobber would stop the compiler from issuing the next
+// updates' global loads ahead of these shared updates.)
+__device__ __forceinline__ void set_bits(unsigned a, unsigned b) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b32 x;\n\t"
+        "ld.shared.u32 x, [%0];\n\t"
+        "and.b32 x, x, %1;\n\t"
+        "setp.ne.u32 p, x, %1;\n\t"
+        "@p red.shared.or.b32 [%0], %1;\n\t}" ::"r"(a),
+        "r"(b));
 }
 
-// Marks absolute row rr: bmA / sumA are the bitmap / summary base addresses
-// shifted by the tile origin so that rows index them directly.
-template <int MODE>
-__device__ __forceinline__ void mark(unsigned bmA, unsigned sumA, int rr) {
-    set_bits<MODE>(bmA + (unsigned(rr >> 5) << 2), 1u << (rr & 31), sumA + (unsigned(rr >> 10) << 2),
-                   1u << ((rr >> 5) & 31));
+// Marks absolute row rr (bmA: the bitmap base shifted by the tile origin).
+__device__ __forceinline__ void mark(unsigned bmA, int rr) { set_bits(bmA + (unsigned(rr >> 5) << 2), 1u << (rr & 31)); }
+
+// Marks a (32-row word, row mask) pair of the word form of A.
+__device__ __forceinline__ void mark_word(unsigned bmA, int2 e) {
+    set_bits(bmA + (unsigned(e.x) << 2), (unsigned)e.y);
 }
 
-// All products of B entries [b0, b1) (column j) whose rows lie in tile t,
-// into the tile bitmap.  Entries are taken NT at a time; a thread walks its
-// own run when it is short, long runs are cut into units of kUnit products
-// that the warps walk lane-strided with U loads in flight (coalesced,
-// balanced across warps; a warp's units are increasing, so the entry owning
-// a unit is found by advancing, not searching).
-template <int NT, int U, int MODE, bool PACK>
-__device__ __forceinline__ void tile_walk(const DevCsc& A, const DevCsc& B, const int32_t* __restrict__ Atp, int T,
-                                          int64_t b0, int64_t b1, int t, int t0, unsigned* bm, unsigned* summ,
-                                          WalkSm<NT>& sh, const DenseRuns& dr, int W, int quads, int short_run) {
+// One element of a run: a row id (row form of A) or a (word, mask) pair
+// (word form).
+__device__ __forceinline__ void mark_el(unsigned bmA, int32_t r) { mark(bmA, r); }
+__device__ __forceinline__ void mark_el(unsigned bmA, int2 e) { mark_word(bmA, e); }
+
+// All updates of B entries [b0, b1) (column j) whose rows lie in tile t, into
+// the tile bitmap.  A's elements are rows (ET = int32_t) or, in the word form
+// (ET = int2), (32-row word, row mask) pairs: rows sharing a word cost one
+// update -- at R-MAT s20 A*A the 70.1e9 multiplies are 36.9e9 word updates
+// (runs of 512-4096 rows compress 1.9x).  Entries are taken NT at a time; a
+// thread walks its own run when it is short, long runs are cut into units of
+// kUnit elements that the warps walk lane-strided with U loads in flight
+// (coalesced, balanced across warps; a warp's units are increasing, so the
+// entry owning a unit is found by advancing, not searching).  Row-form runs of
+// at least dr.dmin rows OR a cached tile bitmap instead.
+// Tried and slower (same box): packing the long runs' elements evenly over the
+// warps (101 -> 107 ms), a warp-independent walk without block barriers (101 ->
+// 155 ms), lane-contiguous quads merged per word (+22%, round 1).
+template <int NT, int U, class ET>
+__device__ __forceinline__ void tile_walk(const ET* __restrict__ Ael, const int64_t* __restrict__ Acp, const DevCsc& B,
+                                          const int32_t* __restrict__ Atp, int T, int64_t b0, int64_t b1, int t,
+                                          int t0, unsigned* bm, WalkSm<NT>& sh, const DenseRuns& dr, int W,
+                                          int short_run) {
     constexpr int NW = NT / 32;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int32_t* __restrict__ Arw = A.rw;
-    const unsigned bm0 = smem_addr(bm), sum0 = smem_addr(summ);
-    const unsigned bmA = bm0 - (unsigned(t0 >> 5) << 2);  // rows index the tile directly
-    const unsigned sumA = sum0 - (unsigned(t0 >> 10) << 2);
+    const unsigned bm0 = smem_addr(bm);
+    const unsigned bmA = bm0 - (unsigned(t0 >> 5) << 2);  // absolute rows / words index the tile directly
     // (sh.ndense and sh.nlong are zeroed by the caller before a barrier)
     for (int64_t base = b0; base < b1; base += NT) {
         const int64_t i = base + tid;
-        int len = 0;
-        int64_t s = 0;
         if (i < b1) {
             const int k = B.rw[i];
             const int32_t* tp = Atp + int64_t(k) * (T + 1) + t;
             const int lo = tp[0], hi = tp[1];
-            s = A.cp[k] + lo;
-            len = hi - lo;
+            const int64_t s = Acp[k] + lo;
+            const int len = hi - lo;
             if (dr.dmin && len >= dr.dmin) {
                 sh.dense[atomicAdd(&sh.ndense, 1)] = dr.slot[int64_t(k) * T + t];
-                len = 0;
             } else if (len < short_run) {
                 // loads in groups of 4 so a short run is not a chain of L2 round trips
-                const int32_t* q = Arw + s;
+                const ET* q = Ael + s;
                 int x = 0;
                 for (; x + 4 <= len; x += 4) {
-                    const int r0 = __ldg(q + x), r1 = __ldg(q + x + 1), r2 = __ldg(q + x + 2), r3 = __ldg(q + x + 3);
-                    mark<MODE>(bmA, sumA, r0);
-                    mark<MODE>(bmA, sumA, r1);
-                    mark<MODE>(bmA, sumA, r2);
-                    mark<MODE>(bmA, sumA, r3);
+                    const ET e0 = __ldg(q + x), e1 = __ldg(q + x + 1), e2 = __ldg(q + x + 2), e3 = __ldg(q + x + 3);
+                    mark_el(bmA, e0);
+                    mark_el(bmA, e1);
+                    mark_el(bmA, e2);
+                    mark_el(bmA, e3);
                 }
-                for (; x < len; ++x) mark<MODE>(bmA, sumA, __ldg(q + x));
-                len = 0;
+                for (; x < len; ++x) mark_el(bmA, __ldg(q + x));
             } else {
                 // long run: into the compact list (order is irrelevant)
                 const unsigned peers = __activemask();
@@ -206,60 +195,17 @@ __device__ __forceinline__ void tile_walk(const DevCsc& A, const DevCsc& B, cons
         }
         __syncthreads();
         const int nl = sh.nlong;
-        // PACK: prefix of the long runs' products (the warps split the
-        // concatenated products evenly, 32 * U per step, so runs of 8..100
-        // products fill whole warps); else prefix of 256-product units
-        const int units = tid < nl ? (PACK ? sh.len[tid] : (sh.len[tid] + kUnit - 1) / kUnit) : 0;
+        const int units = tid < nl ? (sh.len[tid] + kUnit - 1) / kUnit : 0;
         int tot;
         const int ex = block_excl_scan<NT>(units, sh.wsum, &tot);
         sh.ustart[tid] = ex;
         if (tid == 0) sh.ustart[nl] = tot;
         __syncthreads();
-        if (PACK) {
-            const int p0 = (int)((int64_t(tot) * warp) / NW), p1 = (int)((int64_t(tot) * (warp + 1)) / NW);
-            int e = 0;
-            if (p0 < p1) {  // owner of this lane's first product: largest e with ustart[e] <= o
-                const int o = min(p0 + lane, p1 - 1);
-                int lo = 0, hi = nl - 1;
-                while (lo < hi) {
-                    const int mid = (lo + hi + 1) >> 1;
-                    if (sh.ustart[mid] <= o)
-                        lo = mid;
-                    else
-                        hi = mid - 1;
-                }
-                e = lo;
-            }
-            // the current run lives in registers (next boundary, rebased
-            // pointer): shared memory is read only when a lane crosses into
-            // the next run -- the walk is LSU-bound, so no per-product LDS
-            int nextp = p0 < p1 ? sh.ustart[e + 1] : 0;
-            const int32_t* bp = p0 < p1 ? Arw + (sh.start[e] - sh.ustart[e]) : Arw;
-            for (int base = p0; base < p1; base += 32 * U) {
-                int r[U];
-#pragma unroll
-                for (int v = 0; v < U; ++v) {
-                    const int o = base + lane + 32 * v;
-                    r[v] = -1;
-                    if (o < p1) {
-                        while (o >= nextp) {
-                            ++e;
-                            nextp = sh.ustart[e + 1];
-                            bp = Arw + (sh.start[e] - sh.ustart[e]);
-                        }
-                        r[v] = __ldg(bp + o);
-                    }
-                }
-#pragma unroll
-                for (int v = 0; v < U; ++v)
-                    if (r[v] >= 0) mark<MODE>(bmA, sumA, r[v]);
-            }
-        }
         // warp w takes the contiguous unit range [u0, u1): one search for the
         // owning long run, then it only advances (every long run has units)
         const int u0 = (int)((int64_t(tot) * warp) / NW), u1 = (int)((int64_t(tot) * (warp + 1)) / NW);
         int e = 0;
-        if (!PACK && u0 < u1) {
+        if (u0 < u1) {
             int lo = 0, hi = nl - 1;
             while (lo < hi) {
                 const int mid = (lo + hi + 1) >> 1;
@@ -270,47 +216,20 @@ __device__ __forceinline__ void tile_walk(const DevCsc& A, const DevCsc& B, cons
             }
             e = lo;
         }
-        for (int u = u0; !PACK && u < u1; ++u) {
+        for (int u = u0; u < u1; ++u) {
             if (sh.ustart[e + 1] <= u) ++e;
             const int c0 = (u - sh.ustart[e]) * kUnit;
-            const int32_t* run = Arw + sh.start[e] + c0;
+            const ET* run = Ael + sh.start[e] + c0;
             const int m = min(kUnit, sh.len[e] - c0);
             int x = lane;
-            if (quads) {
-                // lane-contiguous quads (16-byte loads from the aligned-down
-                // unit start): rows of a quad that share a word are OR-ed in
-                // registers, so a dense run touches shared memory once per
-                // word run instead of once per product (branch-free heads)
-                const int mis = (int)((reinterpret_cast<uintptr_t>(run) >> 2) & 3);
-                const int4* q4 = reinterpret_cast<const int4*>(run - mis);
-                const int total = m + mis;
-                for (int y = 4 * lane; y < total; y += 128) {
-                    const int4 q = __ldg(q4 + (y >> 2));
-                    const int p0 = y - mis;
-                    const bool v0 = p0 >= 0 && p0 < m, v1 = p0 + 1 >= 0 && p0 + 1 < m;
-                    const bool v2 = p0 + 2 >= 0 && p0 + 2 < m, v3 = p0 + 3 < m;
-                    const int w0 = q.x >> 5, w1 = q.y >> 5, w2 = q.z >> 5, w3 = q.w >> 5;
-                    const bool m1 = v0 && v1 && w1 == w0, m2 = v1 && v2 && w2 == w1, m3 = v2 && v3 && w3 == w2;
-                    const unsigned b3 = 1u << (q.w & 31);
-                    const unsigned a3 = b3;
-                    const unsigned a2 = (1u << (q.z & 31)) | (m3 ? a3 : 0u);
-                    const unsigned a1 = (1u << (q.y & 31)) | (m2 ? a2 : 0u);
-                    const unsigned a0 = (1u << (q.x & 31)) | (m1 ? a1 : 0u);
-                    if (v0) set_bits<MODE>(bmA + (unsigned(w0) << 2), a0, sumA + (unsigned(q.x >> 10) << 2), 1u << (w0 & 31));
-                    if (v1 && !m1) set_bits<MODE>(bmA + (unsigned(w1) << 2), a1, sumA + (unsigned(q.y >> 10) << 2), 1u << (w1 & 31));
-                    if (v2 && !m2) set_bits<MODE>(bmA + (unsigned(w2) << 2), a2, sumA + (unsigned(q.z >> 10) << 2), 1u << (w2 & 31));
-                    if (v3 && !m3) set_bits<MODE>(bmA + (unsigned(w3) << 2), a3, sumA + (unsigned(q.w >> 10) << 2), 1u << (w3 & 31));
-                }
-                continue;
-            }
             for (; x + 32 * (U - 1) < m; x += 32 * U) {
-                int r[U];
+                ET r[U];
 #pragma unroll
                 for (int v = 0; v < U; ++v) r[v] = __ldg(run + x + 32 * v);
 #pragma unroll
-                for (int v = 0; v < U; ++v) mark<MODE>(bmA, sumA, r[v]);
+                for (int v = 0; v < U; ++v) mark_el(bmA, r[v]);
             }
-            for (; x < m; x += 32) mark<MODE>(bmA, sumA, __ldg(run + x));
+            for (; x < m; x += 32) mark_el(bmA, __ldg(run + x));
         }
         // dense runs of this batch: OR whole words of their tile bitmaps
         const int nd = sh.ndense;
@@ -319,12 +238,10 @@ __device__ __forceinline__ void tile_walk(const DevCsc& A, const DevCsc& B, cons
             for (int q = tid; q < (W >> 2); q += NT) {
                 const uint4 v = __ldg(src + q);
                 const unsigned a = bm0 + (unsigned(q) << 4);
-                const unsigned sa = sum0 + (unsigned(q >> 3) << 2);
-                const unsigned sb = 1u << ((q << 2) & 31);
-                if (v.x) set_bits<MODE>(a, v.x, sa, sb);
-                if (v.y) set_bits<MODE>(a + 4, v.y, sa, sb << 1);
-                if (v.z) set_bits<MODE>(a + 8, v.z, sa, sb << 2);
-                if (v.w) set_bits<MODE>(a + 12, v.w, sa, sb << 3);
+                if (v.x) set_bits(a, v.x);
+                if (v.y) set_bits(a + 4, v.y);
+                if (v.z) set_bits(a + 8, v.z);
+                if (v.w) set_bits(a + 12, v.w);
             }
         }
         __syncthreads();
@@ -332,119 +249,6 @@ __device__ __forceinline__ void tile_walk(const DevCsc& A, const DevCsc& B, cons
             sh.ndense = 0;
             sh.nlong = 0;
         }
-        __syncthreads();
-    }
-}
-
-// Word form of the walk: A is given as (32-row word, row mask) pairs per
-// column (A's distinct words in row order, built per A), so a run of rows
-// that share words costs one shared update per WORD instead of one per
-// product -- at R-MAT s20 the 70.1e9 multiplies of A*A are 36.9e9 word
-// updates (runs of 512-4096 rows compress 1.9x).  Same batch structure as
-// tile_walk; "products" below are word entries.
-__device__ __forceinline__ void mark_word(unsigned bmA, int2 e) {
-    set_bits<0>(bmA + (unsigned(e.x) << 2), (unsigned)e.y, 0, 0);
-}
-
-template <int NT, int U, bool PACK>
-__device__ __forceinline__ void tile_walk_words(const int2* __restrict__ Aw, const int64_t* __restrict__ Awcp,
-                                                const DevCsc& B, const int32_t* __restrict__ Atp, int T, int64_t b0,
-                                                int64_t b1, int t, int t0, unsigned* bm, WalkSm<NT>& sh, int short_run) {
-    constexpr int NW = NT / 32;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const unsigned bmA = smem_addr(bm) - (unsigned(t0 >> 5) << 2);  // absolute word index -> tile bitmap
-    for (int64_t base = b0; base < b1; base += NT) {
-        const int64_t i = base + tid;
-        if (i < b1) {
-            const int k = B.rw[i];
-            const int32_t* tp = Atp + int64_t(k) * (T + 1) + t;
-            const int lo = tp[0], hi = tp[1];
-            const int64_t s = Awcp[k] + lo;
-            const int len = hi - lo;
-            if (len < short_run) {
-                const int2* q = Aw + s;
-                int x = 0;
-                for (; x + 4 <= len; x += 4) {
-                    const int2 e0 = __ldg(q + x), e1 = __ldg(q + x + 1), e2 = __ldg(q + x + 2), e3 = __ldg(q + x + 3);
-                    mark_word(bmA, e0);
-                    mark_word(bmA, e1);
-                    mark_word(bmA, e2);
-                    mark_word(bmA, e3);
-                }
-                for (; x < len; ++x) mark_word(bmA, __ldg(q + x));
-            } else {
-                const unsigned peers = __activemask();
-                const int leader = __ffs(peers) - 1;
-                int pos = 0;
-                if (lane == leader) pos = atomicAdd(&sh.nlong, __popc(peers));
-                pos = __shfl_sync(peers, pos, leader) + __popc(peers & ((1u << lane) - 1u));
-                sh.len[pos] = len;
-                sh.start[pos] = s;
-            }
-        }
-        __syncthreads();
-        const int nl = sh.nlong;
-        const int units = tid < nl ? (PACK ? sh.len[tid] : (sh.len[tid] + kUnit - 1) / kUnit) : 0;
-        int tot;
-        const int ex = block_excl_scan<NT>(units, sh.wsum, &tot);
-        sh.ustart[tid] = ex;
-        if (tid == 0) sh.ustart[nl] = tot;
-        __syncthreads();
-        const int p0 = (int)((int64_t(tot) * warp) / NW), p1 = (int)((int64_t(tot) * (warp + 1)) / NW);
-        int e = 0;
-        if (p0 < p1) {
-            const int o = PACK ? min(p0 + lane, p1 - 1) : p0;
-            int lo = 0, hi = nl - 1;
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (sh.ustart[mid] <= o)
-                    lo = mid;
-                else
-                    hi = mid - 1;
-            }
-            e = lo;
-        }
-        if (PACK) {
-            int nextp = p0 < p1 ? sh.ustart[e + 1] : 0;
-            const int2* bp = p0 < p1 ? Aw + (sh.start[e] - sh.ustart[e]) : Aw;
-            for (int pb = p0; pb < p1; pb += 32 * U) {
-                int2 r[U];
-#pragma unroll
-                for (int v = 0; v < U; ++v) {
-                    const int o = pb + lane + 32 * v;
-                    r[v] = make_int2(-1, 0);
-                    if (o < p1) {
-                        while (o >= nextp) {
-                            ++e;
-                            nextp = sh.ustart[e + 1];
-                            bp = Aw + (sh.start[e] - sh.ustart[e]);
-                        }
-                        r[v] = __ldg(bp + o);
-                    }
-                }
-#pragma unroll
-                for (int v = 0; v < U; ++v)
-                    if (r[v].x >= 0) mark_word(bmA, r[v]);
-            }
-        } else {
-            for (int u = p0; u < p1; ++u) {
-                if (sh.ustart[e + 1] <= u) ++e;
-                const int c0 = (u - sh.ustart[e]) * kUnit;
-                const int2* run = Aw + sh.start[e] + c0;
-                const int m = min(kUnit, sh.len[e] - c0);
-                int x = lane;
-                for (; x + 32 * (U - 1) < m; x += 32 * U) {
-                    int2 r[U];
-#pragma unroll
-                    for (int v = 0; v < U; ++v) r[v] = __ldg(run + x + 32 * v);
-#pragma unroll
-                    for (int v = 0; v < U; ++v) mark_word(bmA, r[v]);
-                }
-                for (; x < m; x += 32) mark_word(bmA, __ldg(run + x));
-            }
-        }
-        __syncthreads();
-        if (tid == 0) sh.nlong = 0;
         __syncthreads();
     }
 }
@@ -469,7 +273,6 @@ struct FormArgs {
     int* ticket;
     int nunits;
     int* rbc;  // per item entries per 4096-row block (value semirings), or null
-    int quads;  // 1: lane-contiguous quads merged per word before the shared update
     int short_run;  // runs shorter than this are walked by their own thread
     const int2* Aw;        // word form of A (words mode), or null
     const int64_t* Awcp;   // its column pointers
@@ -570,14 +373,27 @@ __device__ __forceinline__ void stash_bitmap(unsigned* bm, unsigned* summ, uint1
 }
 
 // Persistent: each CTA takes work units (heaviest first) by ticket.
-template <int NT, int MODE, bool PACK = false, bool WORDS = false>
-__global__ void __launch_bounds__(NT) k_tile_form(FormArgs g) {
+#ifdef SLAPCU_FORM_MINB
+#define SLAPCU_FORM_BOUNDS __launch_bounds__(NT, SLAPCU_FORM_MINB)
+#else
+#define SLAPCU_FORM_BOUNDS __launch_bounds__(NT)
+#endif
+__host__ __device__ __forceinline__ size_t form_tail_offset(int W) {
+    return (sizeof(unsigned) * size_t(W + W / 32) + 15) & ~size_t(15);
+}
+
+template <int NT, bool WORDS>
+__global__ void SLAPCU_FORM_BOUNDS k_tile_form(FormArgs g) {
     extern __shared__ __align__(16) unsigned char sm_raw[];
     const int W = 1 << (g.TL - 5);
     unsigned* bm = reinterpret_cast<unsigned*>(sm_raw);
-    unsigned* summ = bm + W;                                // [W/32]
-    uint16_t* tl = reinterpret_cast<uint16_t*>(summ + W / 32);  // [W]
-    __shared__ WalkSm<NT> sh;
+    unsigned* summ = bm + W;  // [W/32]
+    // the stash's word list (after the walk) and the walk's batch state share
+    // one region: 4 KB less shared memory per CTA, one more CTA per SM
+    unsigned char* shared_tail = sm_raw + form_tail_offset(W);
+    uint16_t* tl = reinterpret_cast<uint16_t*>(shared_tail);  // [W]
+    WalkSm<NT>& sh = *reinterpret_cast<WalkSm<NT>*>(shared_tail);
+    __shared__ int wsum2[NT / 32 + 1];
     __shared__ int red[NT / 32];
     __shared__ int ticket_sh;
     __shared__ int bcs[kMaxBlocks];
@@ -596,12 +412,12 @@ __global__ void __launch_bounds__(NT) k_tile_form(FormArgs g) {
         const int2 it = g.items[u.x];
         const int64_t bs = g.B.cp[it.x];
         if constexpr (WORDS)
-            tile_walk_words<NT, 4, PACK>(g.Aw, g.Awcp, g.B, g.Atp, g.T, bs + u.y, bs + u.z, it.y, it.y << g.TL, bm, sh,
-                                         g.short_run);
+            tile_walk<NT, 4, int2>(g.Aw, g.Awcp, g.B, g.Atp, g.T, bs + u.y, bs + u.z, it.y, it.y << g.TL, bm, sh,
+                                   DenseRuns{nullptr, nullptr, 0}, W, g.short_run);
         else
-            tile_walk<NT, 4, MODE, PACK>(g.A, g.B, g.Atp, g.T, bs + u.y, bs + u.z, it.y, it.y << g.TL, bm, summ, sh, g.dr,
-                                         W, g.quads, g.short_run);
-        if (MODE != 2 && u.w < 0) {  // summary by ballots over the bitmap
+            tile_walk<NT, 4, int32_t>(g.A.rw, g.A.cp, g.B, g.Atp, g.T, bs + u.y, bs + u.z, it.y, it.y << g.TL, bm, sh,
+                                      g.dr, W, g.short_run);
+        if (u.w < 0) {  // summary by ballots over the bitmap
             const int lane = threadIdx.x & 31;
             for (int cc = threadIdx.x >> 5; cc < W / 32; cc += NT / 32) {
                 const unsigned nz = __ballot_sync(0xffffffffu, bm[cc * 32 + lane] != 0u);
@@ -618,7 +434,7 @@ __global__ void __launch_bounds__(NT) k_tile_form(FormArgs g) {
             }
             for (int q = threadIdx.x; q < W / 32; q += NT) summ[q] = 0u;
         } else {
-            stash_bitmap<NT>(bm, summ, tl, W, sh.wsum, red, bcs, u.x, it.x, g.stash + g.soff[u.x], g.sres[u.x], g.cnt,
+            stash_bitmap<NT>(bm, summ, tl, W, wsum2, red, bcs, u.x, it.x, g.stash + g.soff[u.x], g.sres[u.x], g.cnt,
                              g.form, g.hcnt, g.rbc);
         }
         __syncthreads();
@@ -842,80 +658,6 @@ __global__ void SLAPCU_EMIT_BOUNDS k_tile_emit(EmitArgs g) {
         for (int64_t q = tid; q < body; q += NT) v4[q] = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
         for (int64_t q = head + (body << 4) + tid; q < c; q += NT) v[q] = 1;
     }
-}
-
-// Block-granular emission: one warp per (item, 128-word block) pair from a
-// flat list, so small items (one block) do not leave a CTA's other warps
-// idle.  The block's output base is the item's offset plus the header
-// counts of the blocks before it.
-__global__ void __launch_bounds__(128) k_tile_emit_blocks(EmitArgs g, const int2* __restrict__ blocks, int64_t nblocks) {
-    __shared__ EmitWarp wsm[4];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t bi = int64_t(blockIdx.x) * 4 + warp;
-    if (bi >= nblocks) return;
-    const int2 ib = blocks[bi];
-    const int item = ib.x, b = ib.y;
-    const int2 it = g.items[item];
-    const int U = g.form[item];
-    const int W = 1 << (g.TL - 5);
-    const int nwords = U >= 0 ? U : W;
-    const unsigned* hdr = g.stash + g.soff[item];
-    const unsigned* words = hdr + stash_header_words(W);
-    const uint16_t* idx = U >= 0 ? reinterpret_cast<const uint16_t*>(words + U) : nullptr;
-    const int t0 = it.y << g.TL;
-    // this block's words (4 per lane) and the item's header prefix up to b
-    unsigned xs[kEmitWPL];
-    int cnt = 0, nz = 0;
-#pragma unroll
-    for (int q = 0; q < kEmitWPL; ++q) {
-        const int w = b * kEmitBlock + lane * kEmitWPL + q;
-        xs[q] = w < nwords ? words[w] : 0u;
-        cnt += __popc(xs[q]);
-        nz += xs[q] != 0u;
-    }
-    int before = 0;
-    for (int k = lane; k < b; k += 32) before += (int)hdr[k];
-    before = warp_reduce_sum(before);
-    const int E = __reduce_add_sync(0xffffffffu, (unsigned)cnt);
-    if (!E) return;
-    const int64_t off = g.lp[it.x] + g.hoff[item] + before;
-    EmitWarp* ws = &wsm[warp];
-    int tot;
-    const int packed = warp_excl_scan((cnt << 16) | nz, lane, &tot);
-    const int pos = packed & 0xffff, ex = packed >> 16;
-    int p = pos;
-#pragma unroll
-    for (int q = 0; q < kEmitWPL; ++q) {
-        if (xs[q]) {
-            const int w = b * kEmitBlock + lane * kEmitWPL + q;
-            ws->wr[p] = make_uint2(xs[q], (unsigned)(t0 + ((idx ? (int)idx[w] : w) << 5)));
-            ++p;
-        }
-    }
-    __syncwarp();
-    emit_block(ws, pos, ex, E, g.crw + off, lane);
-    if (g.cv) {  // values: E bytes of 1
-        uint8_t* v = g.cv + off;
-        const int head = (int)lmin(E, (16 - (reinterpret_cast<uintptr_t>(v) & 15)) & 15);
-        if (lane < head) v[lane] = 1;
-        const int body = (E - head) >> 4;
-        uint4* v4 = reinterpret_cast<uint4*>(v + head);
-        for (int q = lane; q < body; q += 32) v4[q] = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
-        for (int q = head + (body << 4) + lane; q < E; q += 32) v[q] = 1;
-    }
-}
-
-__global__ void k_emit_nblk(int nitems, const int* __restrict__ form, int W, int64_t* __restrict__ nb) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nitems; i += gridDim.x * blockDim.x) {
-        const int nw = form[i] >= 0 ? form[i] : W;
-        nb[i] = (nw + kEmitBlock - 1) / kEmitBlock;
-    }
-}
-
-__global__ void k_emit_fill(int nitems, const int64_t* __restrict__ nb, const int64_t* __restrict__ boff,
-                            int2* __restrict__ blocks) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nitems; i += gridDim.x * blockDim.x)
-        for (int64_t b = 0; b < nb[i]; ++b) blocks[boff[i] + b] = make_int2(i, (int)b);
 }
 
 // ------------------------------------------------------------ value pass
@@ -2235,14 +1977,15 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
                    (const int*)d.order.as<int>(), d.stash.as<unsigned>(), (const int64_t*)d.soff.as<int64_t>(),
                    (const int64_t*)d.sres.as<int64_t>(), d.partial.as<unsigned>(), d.cnt.as<int64_t>(),
                    d.form.as<int>(), d.hcnt.as<unsigned long long>(), nullptr, 0, rbc,
-                   c.opt.direct_quads, c.opt.direct_short_run > 0 ? c.opt.direct_short_run : kShortRun,
+                   c.opt.direct_short_run > 0 ? c.opt.direct_short_run : kShortRun,
                    words ? (const int2*)d.aw.as<int2>() : nullptr, words ? (const int64_t*)d.awcp.as<int64_t>() : nullptr};
-        const size_t smem = sizeof(unsigned) * (W + W / 32) + sizeof(uint16_t) * W;
         DevBuf tick(sizeof(int), c.stream);
         SLAPCU_CUDA(cudaMemsetAsync(tick.get(), 0, sizeof(int), c.stream));
         g.ticket = tick.as<int>();
         g.nunits = (int)nunits;
         auto form = [&](auto kf, int nt) {
+            const size_t walk = nt == 512 ? sizeof(WalkSm<512>) : nt == 128 ? sizeof(WalkSm<128>) : sizeof(WalkSm<256>);
+            const size_t smem = form_tail_offset(W) + std::max(sizeof(uint16_t) * W, walk);
             ensure_smem(kf, smem);
             int per_sm = 0;
             SLAPCU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kf, nt, smem));
@@ -2252,20 +1995,14 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
         };
         const int ft = c.opt.direct_form_threads;
         if (words)
-            c.opt.direct_form_walk == 1 ? form(k_tile_form<256, 0, true, true>, 256)
-                                        : form(k_tile_form<256, 0, false, true>, 256);
-        else if (c.opt.direct_form_walk == 1)
-            form(k_tile_form<256, 0, true>, 256);
-        else if (c.opt.direct_mark_mode == 2)
-            form(k_tile_form<256, 2>, 256);
-        else if (ft == 128)
-            form(k_tile_form<128, 0>, 128);
-        else if (ft == 512)
-            form(k_tile_form<512, 0>, 512);
+            ft == 512 ? form(k_tile_form<512, true>, 512) : ft == 128 ? form(k_tile_form<128, true>, 128)
+                                                          : form(k_tile_form<256, true>, 256);
         else
-            form(k_tile_form<256, 0>, 256);
+            ft == 512 ? form(k_tile_form<512, false>, 512) : ft == 128 ? form(k_tile_form<128, false>, 128)
+                                                           : form(k_tile_form<256, false>, 256);
         if (nsplit > 0) {
             auto kc = k_tile_combine<kFormThreads>;
+            const size_t smem = sizeof(unsigned) * (W + W / 32) + sizeof(uint16_t) * W;
             ensure_smem(kc, smem);
             launch(c, kc, dim3(nsplit), dim3(kFormThreads), smem, TL, (const int2*)d.items.as<int2>(),
                    (const int*)si, (const int*)(si + nitems), (const int*)(si + 2 * nitems),
@@ -2296,26 +2033,12 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
                    (const int64_t*)d.hoff.as<int64_t>(), (const int64_t*)d.lp.as<int64_t>(), TL, crw,
                    ones ? static_cast<uint8_t*>(cv) : nullptr};  // values: 1s here, else the value pass
         const size_t smem = 0;
-        if (c.opt.direct_emit_blocks) {
-            DevBuf nb(sizeof(int64_t) * (size_t(nitems) + 1), c.stream), boff(sizeof(int64_t) * (size_t(nitems) + 1),
-                                                                                c.stream);
-            SLAPCU_CUDA(cudaMemsetAsync(nb.as<int64_t>() + nitems, 0, sizeof(int64_t), c.stream));
-            launch(c, k_emit_nblk, dim3(grid_for(c, nitems, 256)), dim3(256), 0, nitems, (const int*)d.form.as<int>(),
-                   W, nb.as<int64_t>());
-            exclusive_scan_i64(c, nb.as<int64_t>(), boff.as<int64_t>(), nitems + 1);
-            const int64_t nblocks = d2h(c, boff.as<int64_t>() + nitems);
-            d.eblocks.reset(sizeof(int2) * std::max<int64_t>(nblocks, 1), c.stream);
-            launch(c, k_emit_fill, dim3(grid_for(c, nitems, 256)), dim3(256), 0, nitems,
-                   (const int64_t*)nb.as<int64_t>(), (const int64_t*)boff.as<int64_t>(), d.eblocks.as<int2>());
-            launch(c, k_tile_emit_blocks, dim3((unsigned)((nblocks + 3) / 4)), dim3(128), 0, e,
-                   (const int2*)d.eblocks.as<int2>(), nblocks);
-        } else {
-            auto emit = [&](auto ke, int nt) {
-                ensure_smem(ke, smem);
-                launch(c, ke, dim3(nitems), dim3(nt), smem, e);
-            };
-            emit(k_tile_emit<128>, 128);  // (per-warp state is static shared memory: 4 warps)
-        }
+        auto emit = [&](auto ke, int nt) {
+            ensure_smem(ke, smem);
+            launch(c, ke, dim3(nitems), dim3(nt), smem, e);
+        };
+        emit(k_tile_emit<128>, 128);  // (per-warp state is static shared memory: 4 warps)
+
     }
     if (nitems > 0 && !ones) {
         KScope ks(c, KC_NUM_HEAVY);

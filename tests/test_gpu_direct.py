@@ -46,43 +46,48 @@ def test_direct_bool_tiles_and_splits(port, tile_log2, split, dense_run):
         assert_parity(got, want, oracle.OR_AND_U8, f"TL={tile_log2} split={split} {alg.name}")
 
 
-@pytest.mark.parametrize("mode", [0, 2])
-@pytest.mark.parametrize("quads", [0, 1])
-@pytest.mark.parametrize("emit", [32, 128])
+@pytest.mark.parametrize("form_threads", [128, 256, 512])
+@pytest.mark.parametrize("words", [0, 1])
 @pytest.mark.parametrize("scale", [8, 11, 14])
-def test_direct_bool_rmat(port, scale, mode, quads, emit):
+def test_direct_bool_rmat(port, scale, words, form_threads):
     a = _ones(port.gen_rmat(scale))
     want = port.spgemm(oracle.OR_AND_U8, a, a)
     ctx = P.Context()
-    ctx.set_option(L.OPT_DIRECT_MARK_MODE, mode)
-    ctx.set_option(L.OPT_DIRECT_QUADS, quads)
-    ctx.set_option(L.OPT_DIRECT_EMIT_THREADS, emit)
+    ctx.set_option(L.OPT_DIRECT_WORDS, words)
+    ctx.set_option(L.OPT_DIRECT_FORM_THREADS, form_threads)
     got = P.local_spgemm(to_device(a), to_device(a), P.OrAnd, ctx=ctx, method="direct")
-    assert_parity(got, want, oracle.OR_AND_U8, f"s{scale} mode {mode} quads {quads} emit {emit}")
+    assert_parity(got, want, oracle.OR_AND_U8, f"s{scale} words {words} threads {form_threads}")
+
+
+def test_retired_options_rejected():
+    """Experiments measured slower and removed: only their defaults remain."""
+    ctx = P.Context()
+    for opt, bad in ((L.OPT_DIRECT_MARK_MODE, 2), (L.OPT_DIRECT_QUADS, 1), (L.OPT_DIRECT_FORM_WALK, 1),
+                     (L.OPT_DIRECT_EMIT_THREADS, 32)):
+        with pytest.raises(P.errors.Error):
+            ctx.set_option(opt, bad)
 
 
 @pytest.mark.parametrize("words", [0, 1])
-@pytest.mark.parametrize("walk", [0, 1])
 @pytest.mark.parametrize("tile_major", [0, 1])
 @pytest.mark.parametrize("dense_run", [0, 64])
 @pytest.mark.parametrize("scale", [11, 14])
-def test_direct_form_variants(port, scale, walk, tile_major, dense_run, words):
-    """Form kernel variants: packed long runs, tile-major unit order, the
-    word form of A (with split items: split threshold 4096), Boolean and
+def test_direct_form_variants(port, scale, tile_major, dense_run, words):
+    """Form kernel variants: tile-major unit order, the row / word form of A,
+    dense runs (with split items: split threshold 4096), Boolean and
     MinPlus."""
     for sr, kind in ((P.OrAnd, 0), (P.MinPlusI32, 3)):
         a = port.gen_rmat(scale)
         a = a.with_vals(port.fill_values(sr.id, kind, a))
         want = port.spgemm(sr.id, a, a)
         ctx = P.Context()
-        ctx.set_option(L.OPT_DIRECT_FORM_WALK, walk)
         ctx.set_option(L.OPT_DIRECT_WORDS, words)
         ctx.set_option(L.OPT_DIRECT_TILE_MAJOR, tile_major)
         ctx.set_option(L.OPT_DIRECT_DENSE_RUN_MIN, dense_run)
         ctx.set_option(L.OPT_DIRECT_TILE_ROWS_LOG2, 11)
         ctx.set_option(L.OPT_DIRECT_SPLIT_FLOPS, 4096)
         got = P.local_spgemm(to_device(a), to_device(a), sr, ctx=ctx, method="direct")
-        assert_parity(got, want, sr.id, f"s{scale} walk {walk} tile_major {tile_major} {sr.name}")
+        assert_parity(got, want, sr.id, f"s{scale} words {words} tile_major {tile_major} {sr.name}")
 
 
 def test_direct_window_and_rectangular(port):
