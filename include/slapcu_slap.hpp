@@ -39,6 +39,7 @@
 #include <string>
 #include <vector>
 
+#include <algorithm>
 #include <array>
 #include <cmath>
 #include <iostream>
@@ -483,9 +484,11 @@ void batched_spgemm(const slap::DistSparseMat2D<VT1>& a, const slap::DistSparseM
     const slap::GlobalIdx cs = b.col_start(), ce = b.col_end();
     for (int r = 0; r < plan.batches(); ++r) {
         const auto [s, e] = plan.col_ranges[static_cast<std::size_t>(r)];
-        // this rank's block of the slice: global columns [max(cs, s), min(ce, e))
-        const slap::GlobalIdx g0 = std::min(std::max(cs, s), e), g1 = std::max(std::min(ce, e), g0);
-        const slapcu_csc bv = db.window(std::min(g0 - cs, ce - cs), std::min(g1 - cs, ce - cs));
+        // this rank's block of the slice: global columns [max(cs, s), min(ce, e)),
+        // empty (a zero-width window at the block's edge) when the range misses it
+        const slap::GlobalIdx w0 = std::clamp<slap::GlobalIdx>(s - cs, 0, ce - cs);
+        const slap::GlobalIdx w1 = std::clamp<slap::GlobalIdx>(e - cs, w0, ce - cs);
+        const slapcu_csc bv = db.window(w0, w1);
         slapcu_csc_out cd{};
         slapcu_dist_stats st{};
         raise(slapcu_summa2d(comm, &av, &bv, sr, alg_of(alg), &cd, &st), ctx);

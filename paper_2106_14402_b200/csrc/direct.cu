@@ -748,6 +748,10 @@ struct ValueWalkSm {
 // units; shorter runs are packed 32 products per warp step (the owning B
 // entry found by a search over the batch's product prefix), so no thread
 // walks a run alone through a chain of dependent loads.
+#ifndef SLAPCU_VTINY
+#define SLAPCU_VTINY 2
+#endif
+constexpr int kValueTinyRun = SLAPCU_VTINY;  // value walk: runs this short are folded by their own thread
 #ifdef SLAPCU_VCOUNT
 __device__ unsigned long long g_vcount[4];  // entry visits, nonempty runs, products, batches (debug variant)
 #endif
@@ -788,7 +792,16 @@ __device__ __forceinline__ void value_walk(const DevCsc& A, const DevCsc& B, con
             if (len > 0) {
                 const int64_t st = A.cp[k] + rlo;
                 const T_ bv = Bv[i];
-                if (len < 32) {
+                if (len <= kValueTinyRun) {
+                    // one or two products: folded by this thread right away (no
+                    // packing search -- 9 shared loads per product for runs of 1)
+                    int r0, r1 = 0;
+                    T_ a0, a1;
+                    load_prod(Arw, Av, Arv, st, r0, a0);
+                    if (len > 1) load_prod(Arw, Av, Arv, st + 1, r1, a1);
+                    S_::atomic_acc(slot(r0), S_::mul(a0, bv));
+                    if (len > 1) S_::atomic_acc(slot(r1), S_::mul(a1, bv));
+                } else if (len < 32) {
                     slen = len;
                     sh.sst[tid] = st;
                     sh.sbv[tid] = bv;

@@ -56,6 +56,14 @@ bool same(const Triples<GlobalIdx, VT>& a, const Triples<GlobalIdx, VT>& b, bool
 
 std::mutex g_mu;
 std::atomic<int> g_fail{0};
+const bool g_trace = std::getenv("SLAPCU_SHIM_TRACE") != nullptr;
+#define TRACE(what)                                                                 \
+    do {                                                                            \
+        if (g_trace) {                                                              \
+            std::lock_guard<std::mutex> lk_(g_mu);                                  \
+            std::fprintf(stderr, "[rank %d] %s\n", w.rank(), what);                  \
+        }                                                                           \
+    } while (0)
 void fail(const char* what, int p) {
     std::lock_guard<std::mutex> lk(g_mu);
     std::printf("SHIM_DIST_FAIL %s p=%d\n", what, p);
@@ -77,14 +85,19 @@ void check_2d(int p, const SR& sr, Val val, bool exact, std::uint64_t seed) {
         auto a = dist_from(ga, grid);
         auto b = dist_from(gb, grid);
         DistKernelStats s1, s2;
+        TRACE("2d: reference summa");
         auto want = slap::summa2d_spgemm(a, b, sr, SpGemmAlg::hybrid, 1, &s1);
+        TRACE("2d: gpu summa");
         auto got = slapcu_slap::summa2d_spgemm(a, b, sr, SpGemmAlg::hybrid, 1, &s2);
+        TRACE("2d: gather");
         auto tw = gather_matrix(want), tg = gather_matrix(got);
         if (w.rank() == 0 && !same(tw, tg, exact)) fail("summa2d", p);
         if (s1.stages != s2.stages || s1.nnz_out != s2.nnz_out) fail("summa2d stats", p);
         // batched.hpp: counts, plan, batches
+        TRACE("2d: counts");
         auto cw = slap::dist_symbolic_col_nnz(a, b);
         auto cg = slapcu_slap::dist_symbolic_col_nnz(a, b);
+        TRACE("2d: plans");
         if (cw != cg) fail("dist_symbolic_col_nnz", p);
         std::int64_t cmax = 1;
         for (auto x : cw) cmax = std::max(cmax, x);
@@ -93,6 +106,7 @@ void check_2d(int p, const SR& sr, Val val, bool exact, std::uint64_t seed) {
         auto pg = slapcu_slap::plan_batches_by_budget(a, b, budget);
         if (pw.col_ranges != pg.col_ranges || pw.est_entries != pg.est_entries) fail("plan_batches_by_budget", p);
         std::vector<Triples<GlobalIdx, typename SR::result_type>> bw, bg;
+        TRACE("2d: batched");
         slap::batched_spgemm(a, b, pw, sr, SpGemmAlg::hash, 1,
                              [&](int, GlobalIdx, GlobalIdx, const auto& cr) { bw.push_back(gather_matrix(cr)); });
         slapcu_slap::batched_spgemm(a, b, pw, sr, SpGemmAlg::hash, 1,
@@ -100,6 +114,7 @@ void check_2d(int p, const SR& sr, Val val, bool exact, std::uint64_t seed) {
         if (bw.size() != bg.size()) fail("batched_spgemm count", p);
         for (std::size_t r = 0; r < std::min(bw.size(), bg.size()); ++r)
             if (w.rank() == 0 && !same(bw[r], bg[r], exact)) fail("batched_spgemm batch", p);
+        TRACE("2d: errors");
         // error contract: inner-dimension mismatch -> DimError on every rank before any collective
         auto bad = dist_from(random_global<VT>(rng, k + 1, n, 0.05, val), grid);
         try {
@@ -127,8 +142,11 @@ void check_3d(int p, int feeder_pr, int feeder_pc, const SR& sr, Val val, bool e
         auto a3 = redistribute_3d(a2, g3, SplitDim::cols);
         auto b3 = redistribute_3d(b2, g3, SplitDim::rows);
         DistKernelStats s1, s2;
+        TRACE("3d: reference");
         auto want = slap::ca3d_spgemm(a3, b3, sr, SpGemmAlg::hybrid, 1, &s1);
+        TRACE("3d: gpu");
         auto got = slapcu_slap::ca3d_spgemm(a3, b3, sr, SpGemmAlg::hybrid, 1, &s2);
+        TRACE("3d: done");
         if (want.col_start != got.col_start || want.col_len != got.col_len) fail("ca3d piece", p);
         auto tw = gather_matrix(want), tg = gather_matrix(got);
         if (w.rank() == 0 && !same(tw, tg, exact)) fail("ca3d", p);
