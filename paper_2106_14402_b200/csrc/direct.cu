@@ -1717,15 +1717,16 @@ static int64_t direct_fallback(Ctx& c, const DevCsc& A, const DevCsc& B, int sr,
 // evenly spaced windows of <= 256 columns (exact symbolic counts) decides
 // between the bitmap path and the sort-merge (ESC) path, whose cost is per
 // product rather than per output entry and wins when cf is near 1 (C2, C5).
-// Compression of up to 16 evenly spaced columns, exactly: one CTA per
-// sampled column marks its rows in a global bitmap (atomicOr; a newly set
-// bit is a new output entry), at most kSampleProducts products per column.
+// Compression of up to 16 sampled columns, exactly: one CTA per sampled
+// column marks its rows in a global bitmap (atomicOr; a newly set bit is a
+// new output entry), at most kSampleProducts products per column.
 constexpr int kSampleCols = 16;
-constexpr int64_t kSampleProducts = 1 << 16;
+constexpr int64_t kSampleProducts = 1 << 20;
+constexpr int64_t kEscAutoMaxProducts = int64_t(1) << 28;
 
-__global__ void __launch_bounds__(256) k_sample_cf(DevCsc A, DevCsc B, int64_t stride, int words,
+__global__ void __launch_bounds__(256) k_sample_cf(DevCsc A, DevCsc B, const int* __restrict__ cols, int words,
                                                    unsigned* __restrict__ bm, unsigned long long* __restrict__ out) {
-    const int64_t j = int64_t(blockIdx.x) * stride;
+    const int64_t j = cols[blockIdx.x];
     unsigned* m = bm + int64_t(blockIdx.x) * words;
     unsigned long long f = 0, s = 0;
     int64_t done = 0;
@@ -1752,25 +1753,45 @@ __global__ void __launch_bounds__(256) k_sample_cf(DevCsc A, DevCsc B, int64_t s
 
 // The reference picks the accumulator per column by compression: hash iff
 // flops_j / nnz(C(:,j)) >= 2 (spgemm.hpp:54, :312-317), else the k-way merge.
-// Here, for value semirings, per product: heavy columns on average (> 4096
-// multiplies per column, so the light hash kernels do not take them) whose
-// sampled compression is below 2 go to the sort-merge (ESC) path, which costs
-// per product rather than per output entry (C5: 12.8 -> ~5 ms).
+// Here, for value semirings, per product: products of at most 2^28
+// multiplies with heavy columns on average (> 4096 multiplies per column, so
+// the light hash kernels do not take them) whose flops-weighted sampled
+// compression is below 2 go to the sort-merge (ESC) path, which costs per
+// product rather than per output entry (C5: 12.8 -> ~5 ms).
 static bool esc_preferred(Ctx& c, const DevCsc& A, const DevCsc& B) {
     const int64_t n = B.ncols;
     if (n == 0) return false;
+    DevBuf fl(sizeof(int64_t) * n, c.stream);
     int64_t total = 0;
-    spgemm_flops(c, A, B, nullptr, &total);
-    if (total <= 4096 * n) return false;
-    const int ns = (int)std::min<int64_t>(kSampleCols, n);
-    const int64_t stride = std::max<int64_t>(1, n / ns);
+    spgemm_flops(c, A, B, fl.as<int64_t>(), &total);
+    // ESC moves ~40 bytes per product: only products it finishes in a few
+    // milliseconds are candidates (a misjudged large product would cost seconds)
+    if (total <= 4096 * n || total > kEscAutoMaxProducts) return false;
     const int64_t words64 = (A.nrows + 31) / 32;
     if (words64 > (int64_t(1) << 22)) return false;  // (sample bitmaps of > 16 MB each: not worth it)
+    // sampled columns at evenly spaced quantiles of the cumulative flops, so
+    // the columns holding most of the work are the ones measured
+    std::vector<int64_t> hf(static_cast<size_t>(n));
+    SLAPCU_CUDA(cudaMemcpyAsync(hf.data(), fl.get(), sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c.stream));
+    SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+    std::vector<int> cols;
+    int64_t acc = 0;
+    int next = 0;
+    for (int64_t j = 0; j < n && next < kSampleCols; ++j) {
+        acc += hf[size_t(j)];
+        while (next < kSampleCols && acc * kSampleCols > total * next) {
+            if (cols.empty() || cols.back() != (int)j) cols.push_back((int)j);
+            ++next;
+        }
+    }
+    const int ns = (int)cols.size();
     const int words = (int)words64;
+    DevBuf dcols(sizeof(int) * std::max(ns, 1), c.stream);
+    SLAPCU_CUDA(cudaMemcpyAsync(dcols.get(), cols.data(), sizeof(int) * ns, cudaMemcpyHostToDevice, c.stream));
     DevBuf bm(sizeof(unsigned) * size_t(words) * ns, c.stream), cnt(sizeof(unsigned long long) * 2, c.stream);
     SLAPCU_CUDA(cudaMemsetAsync(bm.get(), 0, sizeof(unsigned) * size_t(words) * ns, c.stream));
     SLAPCU_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(unsigned long long) * 2, c.stream));
-    launch(c, k_sample_cf, dim3(ns), dim3(256), 0, A, B, stride, words, bm.as<unsigned>(),
+    launch(c, k_sample_cf, dim3(ns), dim3(256), 0, A, B, (const int*)dcols.as<int>(), words, bm.as<unsigned>(),
            cnt.as<unsigned long long>());
     unsigned long long h[2] = {0, 0};
     SLAPCU_CUDA(cudaMemcpyAsync(h, cnt.get(), sizeof(h), cudaMemcpyDeviceToHost, c.stream));
