@@ -170,9 +170,11 @@ typedef enum {
                                               by row, left fold) path; 0 = bitmap / hash paths; -1 (default)
                                               = value semirings whose sampled compression flops / nnz(C) is
                                               below 2 (spgemm.hpp:54's hybrid threshold) take ESC */
-    SLAPCU_OPT_DIRECT_VALUE_DENSE_ROWS = 29 /* direct path value pass: chunks spanning at most this many rows
+    SLAPCU_OPT_DIRECT_VALUE_DENSE_ROWS = 29, /* direct path value pass: chunks spanning at most this many rows
                                               (multiple of 4096, <= 32768) fold by row offset into a dense
                                               shared array, without rank lookups (0 = the rank chunk size) */
+    SLAPCU_OPT_DIRECT_VALUE_DENSE_ONLY = 30 /* direct path value pass: 1 = every chunk is of the dense kind
+                                              (cut at the dense span), 0 = rank chunks beyond it */
 } slapcu_option;
 slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t value);
 

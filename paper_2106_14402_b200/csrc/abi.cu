@@ -170,6 +170,7 @@ slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t v
                     "value dense rows: 0 (= rank chunk) or a multiple of 4096 up to 32768");
             c.opt.direct_value_dense_rows = (int)v;
             break;
+        case SLAPCU_OPT_DIRECT_VALUE_DENSE_ONLY: c.opt.direct_value_dense_only = v != 0; break;
         case SLAPCU_OPT_DIRECT_VALUE_TMAJOR: c.opt.direct_value_tmajor = v != 0; break;
         case SLAPCU_OPT_DIRECT_SHORT_RUN:
             require(v >= 0 && v <= 256, SLAPCU_ERR_INVALID, "short run threshold: 0 (default) .. 256");

@@ -139,6 +139,7 @@ struct Options {
     int direct_esc = -1;                    // 1: ESC for every semiring, 0: bitmap / hash paths, -1 auto (value
                                             // semirings with sampled compression < 2 take ESC)
     int direct_words = 1;                   // form: walk A's (32-row word, mask) pairs instead of its rows
+    int direct_value_dense_only = 0;        // value pass: chunks only of the dense kind (<= dense rows span)
     int direct_value_dense_rows = 0;        // value pass: chunks spanning <= this many rows fold by row offset (0 = cap)
     int direct_value_tmajor = 1;            // value pass: tile-major 4096-row pointer table + chunks in row order
     int direct_short_run = 0;               // form: runs shorter than this walked per thread (0 = default 8)

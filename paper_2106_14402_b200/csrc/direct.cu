@@ -753,12 +753,15 @@ struct ValueWalkSm {
 #endif
 constexpr int kValueTinyRun = SLAPCU_VTINY;  // value walk: runs this short are folded by their own thread
 #ifdef SLAPCU_VCOUNT
-__device__ unsigned long long g_vcount[4];  // entry visits, nonempty runs, products, batches (debug variant)
+// entry visits, nonempty runs, products, batches, products in rank / dense chunks,
+// products in runs of <= 2 / 3..31 / >= 32 (debug variant)
+__device__ unsigned long long g_vcount[12];
 #endif
 template <int SRID, int NT, class Slot>
 __device__ __forceinline__ void value_walk(const DevCsc& A, const DevCsc& B, const int32_t* __restrict__ Atab, int T,
                                            int t, int j, ValueWalkSm<SRID, NT>& sh, Slot slot, int t_hi = -1,
-                                           const void* __restrict__ Arv = nullptr, int64_t tstride = 0) {
+                                           const void* __restrict__ Arv = nullptr, int64_t tstride = 0,
+                                           int vtag = 0) {
     using S_ = Sr<SRID>;
     using T_ = typename S_::T;
     constexpr int NW = NT / 32;
@@ -788,6 +791,10 @@ __device__ __forceinline__ void value_walk(const DevCsc& A, const DevCsc& B, con
             if (len > 0) atomicAdd(&g_vcount[1], 1ull);
             atomicAdd(&g_vcount[2], (unsigned long long)(len > 0 ? len : 0));
             if (tid == 0) atomicAdd(&g_vcount[3], 1ull);
+            if (len > 0) {
+                atomicAdd(&g_vcount[4 + vtag], (unsigned long long)len);
+                atomicAdd(&g_vcount[len <= 2 ? 8 : len < 32 ? 9 : 10], (unsigned long long)len);
+            }
 #endif
             if (len > 0) {
                 const int64_t st = A.cp[k] + rlo;
@@ -1067,7 +1074,7 @@ __global__ void __launch_bounds__(NT) k_item_values_rank(ValueArgs g, const Rank
     T* Cv = static_cast<T*>(g.cv);
     if (dense) {
         value_walk<SRID, NT>(g.A, g.B, g.Atpv, g.Tv, ts0, j, sh, [val, r0](int r) { return &val[r - r0]; }, ts1, g.arv,
-                             g.tv_stride);
+                             g.tv_stride, 1);
         for (int q = tid; q < n; q += NT) Cv[lo + q] = S_::out(val[g.crw[lo + q] - r0]);
         return;
     }
@@ -1724,13 +1731,16 @@ constexpr int kSampleCols = 16;
 constexpr int64_t kSampleProducts = 1 << 20;
 constexpr int64_t kEscAutoMaxProducts = int64_t(1) << 28;
 
+constexpr int kSampleParts = 16;  // CTAs per sampled column (its B entries interleaved)
+
 __global__ void __launch_bounds__(256) k_sample_cf(DevCsc A, DevCsc B, const int* __restrict__ cols, int words,
                                                    unsigned* __restrict__ bm, unsigned long long* __restrict__ out) {
-    const int64_t j = cols[blockIdx.x];
-    unsigned* m = bm + int64_t(blockIdx.x) * words;
+    const int sc = blockIdx.x / kSampleParts, part = blockIdx.x % kSampleParts;
+    const int64_t j = cols[sc];
+    unsigned* m = bm + int64_t(sc) * words;
     unsigned long long f = 0, s = 0;
     int64_t done = 0;
-    for (int64_t i = B.cp[j]; i < B.cp[j + 1] && done < kSampleProducts; ++i) {
+    for (int64_t i = B.cp[j] + part; i < B.cp[j + 1] && done < kSampleProducts / kSampleParts; i += kSampleParts) {
         const int k = B.rw[i];
         const int64_t a0 = A.cp[k], a1 = A.cp[k + 1];
         for (int64_t p = a0 + threadIdx.x; p < a1; p += blockDim.x) {
@@ -1791,8 +1801,8 @@ static bool esc_preferred(Ctx& c, const DevCsc& A, const DevCsc& B) {
     DevBuf bm(sizeof(unsigned) * size_t(words) * ns, c.stream), cnt(sizeof(unsigned long long) * 2, c.stream);
     SLAPCU_CUDA(cudaMemsetAsync(bm.get(), 0, sizeof(unsigned) * size_t(words) * ns, c.stream));
     SLAPCU_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(unsigned long long) * 2, c.stream));
-    launch(c, k_sample_cf, dim3(ns), dim3(256), 0, A, B, (const int*)dcols.as<int>(), words, bm.as<unsigned>(),
-           cnt.as<unsigned long long>());
+    launch(c, k_sample_cf, dim3(ns * kSampleParts), dim3(256), 0, A, B, (const int*)dcols.as<int>(), words,
+           bm.as<unsigned>(), cnt.as<unsigned long long>());
     unsigned long long h[2] = {0, 0};
     SLAPCU_CUDA(cudaMemcpyAsync(h, cnt.get(), sizeof(h), cudaMemcpyDeviceToHost, c.stream));
     SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
@@ -2145,6 +2155,9 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
                 while (dense_rows > cap && sizeof(Acc) * size_t(dense_rows) + sizeof(unsigned) * W + sizeof(uint16_t) * W +
                                                    sizeof(int) * (W / 32) + 16 > size_t(c.smem_optin) - 8192)
                     dense_rows -= kBlkRows4096;  // (a larger dense span than shared memory holds)
+                // dense-only: every chunk spans at most dense_rows rows (more chunks, each
+                // walking B(:,j) once, but one shared atomic per product and no ranks)
+                const int chunk_cap = c.opt.direct_value_dense_only ? 0 : cap;
                 const int T12 = (int)((A.nrows + 4095) >> 12);
                 ValueArgs vr = va;
                 const bool tmajor = c.opt.direct_value_tmajor != 0;
@@ -2157,13 +2170,13 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
                     coff(sizeof(int64_t) * (size_t(nsl[1]) + 1), c.stream);
                 SLAPCU_CUDA(cudaMemsetAsync(ccount.as<int64_t>() + nsl[1], 0, sizeof(int64_t), c.stream));
                 launch(c, k_rank_chunks, dim3(grid_for(c, nsl[1], 256)), dim3(256), 0, nsl[1], (const int*)large,
-                       (const int*)d.rbc.as<int>(), nrb, cap, dense_rows / kBlkRows4096, (const int64_t*)nullptr,
+                       (const int*)d.rbc.as<int>(), nrb, chunk_cap, dense_rows / kBlkRows4096, (const int64_t*)nullptr,
                        ccount.as<int64_t>(), (RankChunk*)nullptr);
                 exclusive_scan_i64(c, ccount.as<int64_t>(), coff.as<int64_t>(), nsl[1] + 1);
                 const int64_t nch = d2h(c, coff.as<int64_t>() + nsl[1]);
                 DevBuf chunks(sizeof(RankChunk) * std::max<int64_t>(nch, 1), c.stream);
                 launch(c, k_rank_chunks, dim3(grid_for(c, nsl[1], 256)), dim3(256), 0, nsl[1], (const int*)large,
-                       (const int*)d.rbc.as<int>(), nrb, cap, dense_rows / kBlkRows4096,
+                       (const int*)d.rbc.as<int>(), nrb, chunk_cap, dense_rows / kBlkRows4096,
                        (const int64_t*)coff.as<int64_t>(), ccount.as<int64_t>(), chunks.as<RankChunk>());
                 if (c.opt.direct_value_tmajor && nch > 1) {  // row-block order (L2 locality of A and the table)
                     DevBuf key(sizeof(int) * nch, c.stream), kout(sizeof(int) * nch, c.stream),
@@ -2276,9 +2289,9 @@ bool direct_exact(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int alg, i
 #ifdef SLAPCU_VCOUNT
 // debug variant only: value-walk counters (entry visits, nonempty runs, products, batches)
 extern "C" int slapcu_debug_vcount(unsigned long long* out, int reset) {
-    cudaMemcpyFromSymbol(out, slapcu::g_vcount, sizeof(unsigned long long) * 4);
+    cudaMemcpyFromSymbol(out, slapcu::g_vcount, sizeof(unsigned long long) * 12);
     if (reset) {
-        unsigned long long z[4] = {0, 0, 0, 0};
+        unsigned long long z[12] = {};
         cudaMemcpyToSymbol(slapcu::g_vcount, z, sizeof(z));
     }
     return 0;

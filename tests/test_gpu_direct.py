@@ -137,11 +137,12 @@ def test_direct_value_pass(port, sr, vtl, hash_, rank):
     assert_parity(got, want, sr.id, f"{sr.name} vtl={vtl}")
 
 
+@pytest.mark.parametrize("dense_only", [0, 1])
 @pytest.mark.parametrize("dense_rows", [0, 16384, 32768])
 @pytest.mark.parametrize("tmajor", [0, 1])
 @pytest.mark.parametrize("sr", [P.PlusTimesF64, P.PlusTimesF32, P.MinPlusI32, P.PlusTimesI64],
                          ids=lambda s: f"{s.name}_{s.dtype}")
-def test_direct_value_tmajor(port, sr, tmajor, dense_rows):
+def test_direct_value_tmajor(port, sr, tmajor, dense_rows, dense_only):
     """Value pass with the tile-major 4096-row pointer table and rank chunks
     in row-block order (and without): same output."""
     a = with_values(port, port.gen_rmat(14), sr.id)
@@ -150,6 +151,7 @@ def test_direct_value_tmajor(port, sr, tmajor, dense_rows):
     ctx.set_option(L.OPT_DIRECT_ESC, 0)  # the bitmap value pass is the subject
     ctx.set_option(L.OPT_DIRECT_VALUE_TMAJOR, tmajor)
     ctx.set_option(L.OPT_DIRECT_VALUE_DENSE_ROWS, dense_rows)
+    ctx.set_option(L.OPT_DIRECT_VALUE_DENSE_ONLY, dense_only)
     ctx.set_option(L.OPT_DIRECT_VALUE_HASH, 0)
     ctx.set_option(L.OPT_DIRECT_TILE_ROWS_LOG2, 16)
     got = P.local_spgemm(to_device(a), to_device(a), sr, ctx=ctx, method="direct")

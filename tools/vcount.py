@@ -25,11 +25,12 @@ w = L.CscView(A.nrows, c1, A.nnz, A.colptr.data_ptr(), A.rowids.data_ptr(), A.va
 av = A.view()
 lib = ctx.lib
 dbg = lib.slapcu_debug_vcount
-out = (C.c_ulonglong * 4)()
+out = (C.c_ulonglong * 12)()
 dbg(out, 1)
 nz = C.c_int64()
 ctx.check(lib.slapcu_spgemm_direct(ctx.h, C.byref(av), C.byref(w), P.MinPlusI32.id, 2, cap, cp.data_ptr(),
                                    rw.data_ptr(), vv.data_ptr(), C.byref(nz)), "direct")
 dbg(out, 0)
 print(f"columns [0,{c1}) nnz {nz.value} flops {int(fl[:c1].sum())}: entry visits {out[0]:.3e} nonempty runs {out[1]:.3e} "
-      f"products {out[2]:.3e} batches(512) {out[3]:.3e}")
+      f"products {out[2]:.3e} batches(512) {out[3]:.3e}; rank-chunk products {out[4]:.3e} dense-chunk {out[5]:.3e}; "
+      f"runs <=2 {out[8]:.3e} 3..31 {out[9]:.3e} >=32 {out[10]:.3e}")
