@@ -467,6 +467,7 @@ def measure_single(args, sr):
         "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 5),
         "traffic": traffic.get("dram_bytes_per_launch"),
         "traffic_alg_bytes_same_batch": traffic.get("alg_bytes_same_batch"),
+        "traffic_over_alg_same_batch": traffic.get("traffic_over_alg"),
         "traffic_source": traffic.get("source"),
         "alg_bytes_per_launch": round(dom_bytes / max(nlaunch, 1)),
         "alg_bytes_per_batch": batch_bytes,

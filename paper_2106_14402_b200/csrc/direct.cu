@@ -1196,16 +1196,17 @@ __global__ void k_tile_ptr(DevCsc A, int TL, int T, int32_t* __restrict__ Atp) {
     }
 }
 
-// Word form of A: entry p starts a new (column, 32-row word) pair.
+// Word form of A: entry p starts a new (column, 32-row word) pair -- its word
+// differs from its predecessor's (thread per entry, coalesced), or it starts
+// a column (k_word_colstart, after).
 __global__ void k_word_flag(DevCsc A, int* __restrict__ flag) {
-    const int lane = threadIdx.x & 31;
-    const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
-    for (int64_t k = w0; k < A.ncols; k += nw) {
-        const int64_t s = A.cp[k], e = A.cp[k + 1];
-        for (int64_t p = s + lane; p < e; p += 32)
-            flag[p - A.base] = (p == s) || ((A.rw[p] >> 5) != (A.rw[p - 1] >> 5));
-    }
+    for (int64_t x = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < A.span; x += int64_t(gridDim.x) * blockDim.x)
+        flag[x] = x == 0 || (A.rw[A.base + x] >> 5) != (A.rw[A.base + x - 1] >> 5);
+}
+
+__global__ void k_word_colstart(DevCsc A, int* __restrict__ flag) {
+    for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < A.ncols; k += int64_t(gridDim.x) * blockDim.x)
+        if (A.cp[k + 1] > A.cp[k]) flag[A.cp[k] - A.base] = 1;
 }
 
 // ex = exclusive scan of flag (span + 1 entries): word entry of p is
@@ -1658,8 +1659,8 @@ static const int32_t* word_pointers(Ctx& c, const DevCsc& A, uint64_t fp, int TL
     const int64_t span = A.span;
     DevBuf flag(sizeof(int) * (span + 1), c.stream), ex(sizeof(int) * (span + 1), c.stream);
     SLAPCU_CUDA(cudaMemsetAsync(flag.as<int>() + span, 0, sizeof(int), c.stream));
-    if (A.ncols)
-        launch(c, k_word_flag, dim3(grid_for(c, A.ncols * 32, 256)), dim3(256), 0, A, flag.as<int>());
+    if (span) launch(c, k_word_flag, dim3(grid_for(c, span, 256)), dim3(256), 0, A, flag.as<int>());
+    if (A.ncols) launch(c, k_word_colstart, dim3(grid_for(c, A.ncols, 256)), dim3(256), 0, A, flag.as<int>());
     excl_scan_i32(c, flag.as<int>(), ex.as<int>(), span + 1);
     const int nw = d2h(c, ex.as<int>() + span);
     d.aw.reset(sizeof(int2) * std::max(nw, 1), c.stream);
