@@ -173,8 +173,9 @@ typedef enum {
     SLAPCU_OPT_DIRECT_VALUE_DENSE_ROWS = 29, /* direct path value pass: chunks spanning at most this many rows
                                               (multiple of 4096, <= 32768) fold by row offset into a dense
                                               shared array, without rank lookups (0 = the rank chunk size) */
-    SLAPCU_OPT_DIRECT_VALUE_DENSE_ONLY = 30 /* direct path value pass: 1 = every chunk is of the dense kind
-                                              (cut at the dense span), 0 = rank chunks beyond it */
+    SLAPCU_OPT_DIRECT_VALUE_DENSE_ONLY = 30, /* retired (round 2, measured 2.6x slower on MinPlus C3): only 0 */
+    SLAPCU_OPT_DIRECT_VALUE_L2 = 31        /* retired (round 2: global-atomic folds, one walk per form unit,
+                                              measured 501 -> 609 ms on MinPlus C3): only 0 */
 } slapcu_option;
 slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t value);
 

@@ -170,7 +170,11 @@ slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t v
                     "value dense rows: 0 (= rank chunk) or a multiple of 4096 up to 32768");
             c.opt.direct_value_dense_rows = (int)v;
             break;
-        case SLAPCU_OPT_DIRECT_VALUE_DENSE_ONLY: c.opt.direct_value_dense_only = v != 0; break;
+        // retired (measured slower, round 2): only the default is accepted
+        case SLAPCU_OPT_DIRECT_VALUE_L2: require(v == 0, SLAPCU_ERR_INVALID, "value L2 folds: removed"); break;
+        case SLAPCU_OPT_DIRECT_VALUE_DENSE_ONLY:
+            require(v == 0, SLAPCU_ERR_INVALID, "dense-only value chunks: removed");
+            break;
         case SLAPCU_OPT_DIRECT_VALUE_TMAJOR: c.opt.direct_value_tmajor = v != 0; break;
         case SLAPCU_OPT_DIRECT_SHORT_RUN:
             require(v >= 0 && v <= 256, SLAPCU_ERR_INVALID, "short run threshold: 0 (default) .. 256");

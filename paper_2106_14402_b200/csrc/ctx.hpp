@@ -139,7 +139,6 @@ struct Options {
     int direct_esc = -1;                    // 1: ESC for every semiring, 0: bitmap / hash paths, -1 auto (value
                                             // semirings with sampled compression < 2 take ESC)
     int direct_words = 1;                   // form: walk A's (32-row word, mask) pairs instead of its rows
-    int direct_value_dense_only = 0;        // value pass: chunks only of the dense kind (<= dense rows span)
     int direct_value_dense_rows = 0;        // value pass: chunks spanning <= this many rows fold by row offset (0 = cap)
     int direct_value_tmajor = 1;            // value pass: tile-major 4096-row pointer table + chunks in row order
     int direct_short_run = 0;               // form: runs shorter than this walked per thread (0 = default 8)
@@ -175,6 +174,7 @@ struct DirectCache {
     DevBuf dist_rw, dist_v;  // SUMMA concatenated product: bound-sized output scratch
     DevBuf eblocks;          // emit work list: (item, block) pairs
     int64_t last_nnz = -1;  // exact nnz(C) of the last call (also on BudgetError)
+    int64_t nunits = 0;     // form work units of the last call (the L2 value pass reuses them)
 };
 
 // Kernel classes for the per-class device-time breakdown (profiling mode).

@@ -31,6 +31,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cmath>
+#include <cstring>
 #include <vector>
 
 #include "kern.cuh"
@@ -488,7 +490,9 @@ struct EmitArgs {
     const int64_t* lp;    // light prefix per column
     int TL;
     int32_t* crw;
-    uint8_t* cv;
+    uint8_t* cv;      // values written by emit (null: the value pass writes them)
+    int vsize;        // bytes per value
+    uint4 vpattern;   // 16 bytes of the value to write (1s for OrAnd, the identity for the L2 value pass)
 };
 
 // Per-warp shared state of the emission.
@@ -649,14 +653,20 @@ __global__ void SLAPCU_EMIT_BOUNDS k_tile_emit(EmitArgs g) {
         }
     }
     if (g.cv) {
-        // values: c bytes of 1 (head bytes, 16-byte body, tail bytes)
-        uint8_t* v = g.cv + off;
-        const int64_t head = lmin(c, (16 - (reinterpret_cast<uintptr_t>(v) & 15)) & 15);
-        for (int64_t q = tid; q < head; q += NT) v[q] = 1;
-        const int64_t body = (c - head) >> 4;
+        // values: c copies of the pattern value (head elements, 16-byte body, tail elements)
+        uint8_t* v = g.cv + off * g.vsize;
+        const int64_t bytes = c * g.vsize;
+        const int64_t head = lmin(bytes, (16 - (reinterpret_cast<uintptr_t>(v) & 15)) & 15);
+        const uint4 pat = g.vpattern;
+        auto pbyte = [pat](int b) {  // byte b of the 16-byte pattern (no address taken: no stack copy)
+            const unsigned wd = b < 8 ? (b < 4 ? pat.x : pat.y) : (b < 12 ? pat.z : pat.w);
+            return (uint8_t)(wd >> ((b & 3) * 8));
+        };
+        for (int64_t q = tid; q < head; q += NT) v[q] = pbyte((int)(q % g.vsize));
+        const int64_t body = (bytes - head) >> 4;
         uint4* v4 = reinterpret_cast<uint4*>(v + head);
-        for (int64_t q = tid; q < body; q += NT) v4[q] = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
-        for (int64_t q = head + (body << 4) + tid; q < c; q += NT) v[q] = 1;
+        for (int64_t q = tid; q < body; q += NT) v4[q] = pat;  // (head is a multiple of vsize)
+        for (int64_t q = head + (body << 4) + tid; q < bytes; q += NT) v[q] = pbyte((int)(q % g.vsize));
     }
 }
 
@@ -761,7 +771,7 @@ template <int SRID, int NT, class Slot>
 __device__ __forceinline__ void value_walk(const DevCsc& A, const DevCsc& B, const int32_t* __restrict__ Atab, int T,
                                            int t, int j, ValueWalkSm<SRID, NT>& sh, Slot slot, int t_hi = -1,
                                            const void* __restrict__ Arv = nullptr, int64_t tstride = 0,
-                                           int vtag = 0) {
+                                           int vtag = 0, int64_t eb0 = -1, int64_t eb1 = -1) {
     using S_ = Sr<SRID>;
     using T_ = typename S_::T;
     constexpr int NW = NT / 32;
@@ -769,7 +779,7 @@ __device__ __forceinline__ void value_walk(const DevCsc& A, const DevCsc& B, con
     const T_* Av = static_cast<const T_*>(A.v);
     const T_* Bv = static_cast<const T_*>(B.v);
     const int32_t* __restrict__ Arw = A.rw;
-    const int64_t bs = B.cp[j], be = B.cp[j + 1];
+    const int64_t bs = eb0 >= 0 ? eb0 : B.cp[j], be = eb0 >= 0 ? eb1 : B.cp[j + 1];
     for (int64_t base = bs; base < be; base += NT) {
         const int64_t i = base + tid;
         int slen = 0;
@@ -1599,6 +1609,24 @@ constexpr int kMaxParts = 64;
 
 }  // namespace
 
+// 16 bytes of the value emit writes: 1s for the OrAnd pattern path, the
+// semiring's identity (semiring.hpp zero()) for the global-atomic value pass.
+static uint4 value_pattern(int sr, bool ones) {
+    unsigned char b[16] = {};
+    if (ones) {
+        for (auto& x : b) x = 1;
+    } else if (sr == SLAPCU_MIN_PLUS_I32) {
+        const int32_t v = INT32_MAX;
+        for (int q = 0; q < 4; ++q) std::memcpy(b + 4 * q, &v, 4);
+    } else if (sr == SLAPCU_MIN_PLUS_F64) {
+        const double v = INFINITY;
+        for (int q = 0; q < 2; ++q) std::memcpy(b + 8 * q, &v, 8);
+    }  // PlusTimes: +0
+    uint4 r;
+    std::memcpy(&r, b, 16);
+    return r;
+}
+
 int direct_tile_log2(const Ctx& c, int64_t nrows) {
     // auto: 2^17-row tiles up to 2^20 rows, 2^18 above (fewer items walking
     // the same B columns when rows are many and columns sparse)
@@ -1962,6 +1990,7 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
         SLAPCU_CUDA(cudaMemcpyAsync(&tail[2], d.soff.as<int64_t>() + nitems, 8, cudaMemcpyDeviceToHost, c.stream));
         SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
         const int64_t nunits = tail[0], nslots = tail[1], swords = tail[2];
+        d.nunits = nunits;
         if (nunits > INT32_MAX || nslots > INT32_MAX) throw Fail{SLAPCU_ERR_INVALID, "too many work units"};
         d.units.reset(sizeof(int4) * std::max<int64_t>(nunits, 1), c.stream);
         DevBuf ukey(sizeof(int64_t) * std::max<int64_t>(nunits, 1), c.stream);
@@ -2076,7 +2105,8 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
         EmitArgs e{(const int2*)d.items.as<int2>(), (const int64_t*)d.cnt.as<int64_t>(), (const int*)d.form.as<int>(),
                    (const unsigned*)d.stash.as<unsigned>(), (const int64_t*)d.soff.as<int64_t>(),
                    (const int64_t*)d.hoff.as<int64_t>(), (const int64_t*)d.lp.as<int64_t>(), TL, crw,
-                   ones ? static_cast<uint8_t*>(cv) : nullptr};  // values: 1s here, else the value pass
+                   ones ? static_cast<uint8_t*>(cv) : nullptr,  // 1s here, else the value pass
+                   value_size(sr), value_pattern(sr, ones)};
         const size_t smem = 0;
         auto emit = [&](auto ke, int nt) {
             ensure_smem(ke, smem);
@@ -2156,9 +2186,7 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
                 while (dense_rows > cap && sizeof(Acc) * size_t(dense_rows) + sizeof(unsigned) * W + sizeof(uint16_t) * W +
                                                    sizeof(int) * (W / 32) + 16 > size_t(c.smem_optin) - 8192)
                     dense_rows -= kBlkRows4096;  // (a larger dense span than shared memory holds)
-                // dense-only: every chunk spans at most dense_rows rows (more chunks, each
-                // walking B(:,j) once, but one shared atomic per product and no ranks)
-                const int chunk_cap = c.opt.direct_value_dense_only ? 0 : cap;
+                const int chunk_cap = cap;
                 const int T12 = (int)((A.nrows + 4095) >> 12);
                 ValueArgs vr = va;
                 const bool tmajor = c.opt.direct_value_tmajor != 0;

@@ -63,7 +63,7 @@ def test_retired_options_rejected():
     """Experiments measured slower and removed: only their defaults remain."""
     ctx = P.Context()
     for opt, bad in ((L.OPT_DIRECT_MARK_MODE, 2), (L.OPT_DIRECT_QUADS, 1), (L.OPT_DIRECT_FORM_WALK, 1),
-                     (L.OPT_DIRECT_EMIT_THREADS, 32)):
+                     (L.OPT_DIRECT_EMIT_THREADS, 32), (L.OPT_DIRECT_VALUE_L2, 1), (L.OPT_DIRECT_VALUE_DENSE_ONLY, 1)):
         with pytest.raises(P.errors.Error):
             ctx.set_option(opt, bad)
 
@@ -137,12 +137,11 @@ def test_direct_value_pass(port, sr, vtl, hash_, rank):
     assert_parity(got, want, sr.id, f"{sr.name} vtl={vtl}")
 
 
-@pytest.mark.parametrize("dense_only", [0, 1])
 @pytest.mark.parametrize("dense_rows", [0, 16384, 32768])
 @pytest.mark.parametrize("tmajor", [0, 1])
 @pytest.mark.parametrize("sr", [P.PlusTimesF64, P.PlusTimesF32, P.MinPlusI32, P.PlusTimesI64],
                          ids=lambda s: f"{s.name}_{s.dtype}")
-def test_direct_value_tmajor(port, sr, tmajor, dense_rows, dense_only):
+def test_direct_value_tmajor(port, sr, tmajor, dense_rows):
     """Value pass with the tile-major 4096-row pointer table and rank chunks
     in row-block order (and without): same output."""
     a = with_values(port, port.gen_rmat(14), sr.id)
@@ -151,7 +150,6 @@ def test_direct_value_tmajor(port, sr, tmajor, dense_rows, dense_only):
     ctx.set_option(L.OPT_DIRECT_ESC, 0)  # the bitmap value pass is the subject
     ctx.set_option(L.OPT_DIRECT_VALUE_TMAJOR, tmajor)
     ctx.set_option(L.OPT_DIRECT_VALUE_DENSE_ROWS, dense_rows)
-    ctx.set_option(L.OPT_DIRECT_VALUE_DENSE_ONLY, dense_only)
     ctx.set_option(L.OPT_DIRECT_VALUE_HASH, 0)
     ctx.set_option(L.OPT_DIRECT_TILE_ROWS_LOG2, 16)
     got = P.local_spgemm(to_device(a), to_device(a), sr, ctx=ctx, method="direct")
