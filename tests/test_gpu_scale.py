@@ -35,11 +35,14 @@ def offsets(n, w):
     return [0, min(n // 4 + 12345, n - w), min(n // 2 + 777, n - w), n - w]
 
 
-def batched_slices(A, B, sr, slices, budget=24 << 30):
+def batched_slices(A, B, sr, slices, budget=None):
     """The bench's step: column batches by the flops bound, one direct call
     each; returns per-slice (colptr, rows, vals, max output offset) and the
     per-column nnz of every column."""
     ctx = P.Context()
+    if budget is None:  # one batch where it fits, so late columns sit at output offsets > 2^31
+        free, _ = torch.cuda.mem_get_info()
+        budget = int(0.6 * free)
     _, fl = P.estimate_flops(A, B, ctx=ctx)
     bound = torch.clamp(fl, max=A.nrows).cpu().numpy()
     vs = np.dtype(sr.np_dtype).itemsize
