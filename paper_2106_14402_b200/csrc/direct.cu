@@ -49,6 +49,9 @@ constexpr int kShortRun = SLAPCU_SHORT_RUN;  // runs shorter than this are walke
 #define SLAPCU_UNIT 256
 #endif
 constexpr int kUnit = SLAPCU_UNIT;  // products per warp work unit on long runs
+#ifndef SLAPCU_FORM_U
+#define SLAPCU_FORM_U 4  // loads in flight per lane on long runs
+#endif
 
 __host__ __device__ __forceinline__ int64_t lmin(int64_t a, int64_t b) { return a < b ? a : b; }
 
@@ -414,10 +417,10 @@ __global__ void SLAPCU_FORM_BOUNDS k_tile_form(FormArgs g) {
         const int2 it = g.items[u.x];
         const int64_t bs = g.B.cp[it.x];
         if constexpr (WORDS)
-            tile_walk<NT, 4, int2>(g.Aw, g.Awcp, g.B, g.Atp, g.T, bs + u.y, bs + u.z, it.y, it.y << g.TL, bm, sh,
+            tile_walk<NT, SLAPCU_FORM_U, int2>(g.Aw, g.Awcp, g.B, g.Atp, g.T, bs + u.y, bs + u.z, it.y, it.y << g.TL, bm, sh,
                                    DenseRuns{nullptr, nullptr, 0}, W, g.short_run);
         else
-            tile_walk<NT, 4, int32_t>(g.A.rw, g.A.cp, g.B, g.Atp, g.T, bs + u.y, bs + u.z, it.y, it.y << g.TL, bm, sh,
+            tile_walk<NT, SLAPCU_FORM_U, int32_t>(g.A.rw, g.A.cp, g.B, g.Atp, g.T, bs + u.y, bs + u.z, it.y, it.y << g.TL, bm, sh,
                                       g.dr, W, g.short_run);
         if (u.w < 0) {  // summary by ballots over the bitmap
             const int lane = threadIdx.x & 31;
@@ -492,7 +495,8 @@ struct EmitArgs {
     int32_t* crw;
     uint8_t* cv;      // values written by emit (null: the value pass writes them)
     int vsize;        // bytes per value
-    uint4 vpattern;   // 16 bytes of the value to write (1s for OrAnd, the identity for the L2 value pass)
+    uint4 vpattern;   // 16 bytes of the value to write (1s for OrAnd)
+    int nitems;
 };
 
 // Per-warp shared state of the emission.
@@ -576,10 +580,14 @@ __device__ __forceinline__ void emit_block(EmitWarp* ws, int pos, int ex, int E,
 #endif
 template <int NT>
 __global__ void SLAPCU_EMIT_BOUNDS k_tile_emit(EmitArgs g) {
+    // one warp per item (NW items per CTA; default 1): most items stash 1-4
+    // blocks of 128 words, so the warps of a multi-warp item CTA idled (4
+    // warps per item 42.7 ms, 2: 40.9, 1: 39.1 at C3)
     constexpr int NW = NT / 32;
     __shared__ EmitWarp wsm[NW];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int item = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int item = blockIdx.x * NW + warp;
+    if (item >= g.nitems) return;
     const int2 it = g.items[item];
     const int64_t c = g.cnt[item];
     const int64_t off = g.lp[it.x] + g.hoff[item];
@@ -617,11 +625,11 @@ __global__ void SLAPCU_EMIT_BOUNDS k_tile_emit(EmitArgs g) {
     };
     unsigned xs[kEmitWPL];
     int wi[kEmitWPL];
-    load(warp, xs, wi);
-    for (int b = warp; b < nblk; b += NW) {
+    load(0, xs, wi);
+    for (int b = 0; b < nblk; ++b) {
         unsigned xn[kEmitWPL];
         int wn[kEmitWPL];
-        load(b + NW, xn, wn);
+        load(b + 1, xn, wn);
         const int E = __shfl_sync(0xffffffffu, sel(hv, b >> 5), b & 31);
         const int bbase = __shfl_sync(0xffffffffu, sel(hb, b >> 5), b & 31);
         if (E) {
@@ -662,11 +670,11 @@ __global__ void SLAPCU_EMIT_BOUNDS k_tile_emit(EmitArgs g) {
             const unsigned wd = b < 8 ? (b < 4 ? pat.x : pat.y) : (b < 12 ? pat.z : pat.w);
             return (uint8_t)(wd >> ((b & 3) * 8));
         };
-        for (int64_t q = tid; q < head; q += NT) v[q] = pbyte((int)(q % g.vsize));
+        for (int64_t q = lane; q < head; q += 32) v[q] = pbyte((int)(q % g.vsize));
         const int64_t body = (bytes - head) >> 4;
         uint4* v4 = reinterpret_cast<uint4*>(v + head);
-        for (int64_t q = tid; q < body; q += NT) v4[q] = pat;  // (head is a multiple of vsize)
-        for (int64_t q = head + (body << 4) + tid; q < bytes; q += NT) v[q] = pbyte((int)(q % g.vsize));
+        for (int64_t q = lane; q < body; q += 32) v4[q] = pat;  // (head is a multiple of vsize)
+        for (int64_t q = head + (body << 4) + lane; q < bytes; q += 32) v[q] = pbyte((int)(q % g.vsize));
     }
 }
 
@@ -2106,13 +2114,17 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
                    (const unsigned*)d.stash.as<unsigned>(), (const int64_t*)d.soff.as<int64_t>(),
                    (const int64_t*)d.hoff.as<int64_t>(), (const int64_t*)d.lp.as<int64_t>(), TL, crw,
                    ones ? static_cast<uint8_t*>(cv) : nullptr,  // 1s here, else the value pass
-                   value_size(sr), value_pattern(sr, ones)};
+                   value_size(sr), value_pattern(sr, ones), nitems};
         const size_t smem = 0;
         auto emit = [&](auto ke, int nt) {
             ensure_smem(ke, smem);
-            launch(c, ke, dim3(nitems), dim3(nt), smem, e);
+            launch(c, ke, dim3((unsigned)((nitems + nt / 32 - 1) / (nt / 32))), dim3(nt), smem, e);
         };
-        emit(k_tile_emit<128>, 128);  // (per-warp state is static shared memory: 4 warps)
+#ifndef SLAPCU_EMIT_NT
+#define SLAPCU_EMIT_NT 32  // one warp, one item per CTA (C3: 39.1 ms; 2 / 4 / 8 items per CTA 44.4 / 41.2 / 50.7:
+                            // a CTA lives as long as its largest item)
+#endif
+        emit(k_tile_emit<SLAPCU_EMIT_NT>, SLAPCU_EMIT_NT);  // (per-warp state is static shared memory)
 
     }
     if (nitems > 0 && !ones) {
