@@ -43,11 +43,14 @@ __global__ void k_entry_col(int64_t ncols, const int64_t* __restrict__ Bcp, int6
         for (int64_t x = Bcp[j] + lane; x < Bcp[j + 1]; x += 32) col[x - e0] = (int)j;
 }
 
-// Expand: each lane takes one B entry; A columns shorter than 32 entries are
-// written by their lane, longer ones by the whole warp (ballot order,
-// lane-strided, coalesced).  The key is (column << row_bits) | row, so ONE
-// stable radix sort over the group orders products by (column, row) and keeps
-// the enumeration order (ascending k) inside every run.
+// Expand: a warp takes 32 B entries; their products are contiguous in the
+// output (eoff is the prefix of the entries' A column lengths), so the warp
+// walks that range with consecutive lanes on consecutive products -- reads of
+// A and writes of keys / values coalesced -- finding each product's entry by a
+// 5-step search over the lanes' prefix (shuffles).  The key is
+// (column << row_bits) | row, so ONE stable radix sort over the group orders
+// products by (column, row) and keeps the enumeration order (ascending k)
+// inside every run.
 template <int SRID, class K>
 __global__ void k_expand(DevCsc A, DevCsc B, int64_t e0, int64_t ne, const int64_t* __restrict__ eoff,
                          const int* __restrict__ ecol, int row_bits, K* __restrict__ keys,
@@ -60,7 +63,8 @@ __global__ void k_expand(DevCsc A, DevCsc B, int64_t e0, int64_t ne, const int64
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     for (int64_t base = int64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31); base < ne; base += stride) {
         const int64_t x = base + lane;
-        int64_t s = 0, len = 0, o = 0;
+        int64_t s = 0;
+        int len = 0;
         T b{};
         K hi = 0;
         if (x < ne) {
@@ -68,26 +72,29 @@ __global__ void k_expand(DevCsc A, DevCsc B, int64_t e0, int64_t ne, const int64
             b = Bv[e0 + x];
             hi = K(ecol[x]) << row_bits;
             s = A.cp[k];
-            len = A.cp[k + 1] - s;
-            o = eoff[x];
-            if (len < 32) {
-                for (int64_t q = 0; q < len; ++q) {
-                    keys[o + q] = hi | K(A.rw[s + q]);
-                    vals[o + q] = S_::mul(Av[s + q], b);
-                }
-            }
+            len = (int)(A.cp[k + 1] - s);
         }
-        unsigned lm = __ballot_sync(0xffffffffu, len >= 32);
-        while (lm) {
-            const int src = __ffs(lm) - 1;
-            lm &= lm - 1u;
-            const int64_t ss = __shfl_sync(0xffffffffu, s, src), ll = __shfl_sync(0xffffffffu, len, src);
-            const int64_t oo = __shfl_sync(0xffffffffu, o, src);
+        const int64_t o0 = __shfl_sync(0xffffffffu, x < ne ? eoff[x] : 0, 0);  // the warp's first product
+        int tot;
+        const int ex = warp_excl_scan(len, lane, &tot);
+        for (int q0 = 0; q0 < tot; q0 += 32) {
+            const int q = q0 + lane;
+            // owner: the last lane whose prefix is <= q (lanes with len 0 are skipped by <=)
+            int src = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const int cand = src + step;
+                const int exc = __shfl_sync(0xffffffffu, ex, cand & 31);
+                if (cand < 32 && exc <= q) src = cand;
+            }
+            const int exs = __shfl_sync(0xffffffffu, ex, src);
+            const int64_t ss = __shfl_sync(0xffffffffu, s, src);
             const K hh = __shfl_sync(0xffffffffu, hi, src);
             const T bb = __shfl_sync(0xffffffffu, b, src);
-            for (int64_t q = lane; q < ll; q += 32) {
-                keys[oo + q] = hh | K(A.rw[ss + q]);
-                vals[oo + q] = S_::mul(Av[ss + q], bb);
+            if (q < tot) {
+                const int64_t p = ss + (q - exs);
+                keys[o0 + q] = hh | K(A.rw[p]);
+                vals[o0 + q] = S_::mul(Av[p], bb);
             }
         }
     }
