@@ -1079,8 +1079,8 @@ __global__ void __launch_bounds__(NT) k_item_values_rank(ValueArgs g, const Rank
     // dense chunks (their rows fit the value array): values indexed by row
     // offset -- no bitmap, no ranks, one shared atomic per product
     const bool dense = nwords * 32 <= dense_rows;
-    if (!dense)
-        for (int q = tid; q < nwords; q += NT) bm[q] = 0u;
+    if (!dense)  // (nwords is a multiple of 128 and bm 16-byte aligned)
+        for (int q = tid; q < (nwords >> 2); q += NT) reinterpret_cast<uint4*>(bm)[q] = make_uint4(0u, 0u, 0u, 0u);
     else
         for (int q = tid; q < nwords * 32; q += NT) val[q] = S_::identity();
     __syncthreads();
@@ -1096,39 +1096,17 @@ __global__ void __launch_bounds__(NT) k_item_values_rank(ValueArgs g, const Rank
         for (int q = tid; q < n; q += NT) Cv[lo + q] = S_::out(val[g.crw[lo + q] - r0]);
         return;
     }
+    // C's rows of the chunk are sorted, so output q IS the q-th rank: a word's
+    // prefix is the index of its first output (set where the word changes) --
+    // no scans over the chunk's span.  A product's slot is pre[w] + popc(bits
+    // below it in the word): two shared loads.  (Words without outputs keep a
+    // stale prefix; no product lands in them.)
     for (int q = tid; q < n; q += NT) {
         const int rr = g.crw[lo + q] - r0;
         atomicOr(&bm[rr >> 5], 1u << (rr & 31));
+        if (q == 0 || ((g.crw[lo + q - 1] - r0) >> 5) != (rr >> 5)) pre16[rr >> 5] = (uint16_t)q;
         val[q] = S_::identity();
     }
-    __syncthreads();
-    // ranks: per 32-word group a warp scan, group totals scanned, then the
-    // chunk-wide prefix of every word stored in 16 bits (a chunk holds at most
-    // cap <= 65535 outputs): a product's slot is pre[w] + popc(bits below it)
-    // -- two shared loads
-    const int ng = (nwords + 31) >> 5;
-    for (int gi = warp; gi < ng; gi += NW) {
-        const int w = gi * 32 + lane;
-        const int x = w < nwords ? __popc(bm[w]) : 0;
-        int tot;
-        const int ex = warp_excl_scan(x, lane, &tot);
-        if (w < nwords) pre16[w] = (uint16_t)ex;
-        if (lane == 0) gbase[gi] = tot;
-    }
-    __syncthreads();
-    if (warp == 0) {
-        int run = 0;
-        for (int b0 = 0; b0 < ng; b0 += 32) {
-            const int gi = b0 + lane;
-            const int x = gi < ng ? gbase[gi] : 0;
-            int tt;
-            const int e = warp_excl_scan(x, lane, &tt);
-            if (gi < ng) gbase[gi] = run + e;
-            run += tt;
-        }
-    }
-    __syncthreads();
-    for (int w = tid; w < nwords; w += NT) pre16[w] = (uint16_t)(pre16[w] + gbase[w >> 5]);
     __syncthreads();
     auto slot = [bm, pre16, val, r0](int r) {
         const int rr = r - r0;
