@@ -770,6 +770,14 @@ struct ValueWalkSm {
 #define SLAPCU_VTINY 2
 #endif
 constexpr int kValueTinyRun = SLAPCU_VTINY;  // value walk: runs this short are folded by their own thread
+#ifndef SLAPCU_VALUE_U
+#define SLAPCU_VALUE_U 8  // MinPlus C3: 2 / 4 / 8 -> 469 / 454 / 443 ms (latency-bound gathers)
+#endif
+#ifndef SLAPCU_VALUE_UNIT
+#define SLAPCU_VALUE_UNIT 256
+#endif
+constexpr int kValueU = SLAPCU_VALUE_U;        // value walk: products per lane per trip on long runs
+constexpr int kValueUnit = SLAPCU_VALUE_UNIT;  // value walk: products per warp work unit on long runs
 #ifdef SLAPCU_VCOUNT
 // entry visits, nonempty runs, products, batches, products in rank / dense chunks,
 // products in runs of <= 2 / 3..31 / >= 32 (debug variant)
@@ -844,7 +852,7 @@ __device__ __forceinline__ void value_walk(const DevCsc& A, const DevCsc& B, con
         }
         __syncthreads();
         const int nl = sh.nlong;
-        const int units = tid < nl ? (sh.ulen[tid] + 255) / 256 : 0;
+        const int units = tid < nl ? (sh.ulen[tid] + kValueUnit - 1) / kValueUnit : 0;
         int tot, stot;
         {
             int wt, wt2;
@@ -912,21 +920,22 @@ __device__ __forceinline__ void value_walk(const DevCsc& A, const DevCsc& B, con
         }
         for (int u = u0; u < u1; ++u) {
             if (sh.ustart[e + 1] <= u) ++e;
-            const int c0 = (u - sh.ustart[e]) * 256;
+            const int c0 = (u - sh.ustart[e]) * kValueUnit;
             const int64_t p0 = sh.ustartp[e] + c0;
-            const int m = min(256, sh.ulen[e] - c0);
+            const int m = min(kValueUnit, sh.ulen[e] - c0);
             const T_ bv = sh.ubval[e];
-            for (int x = lane; x < m; x += 64) {
-                int r0, r1 = 0;
-                T_ a0, a1;
-                load_prod(Arw, Av, Arv, p0 + x, r0, a0);
-                const bool two = x + 32 < m;
-                if (two)
-                    load_prod(Arw, Av, Arv, p0 + x + 32, r1, a1);
-                else
-                    a1 = a0;
-                S_::atomic_acc(slot(r0), S_::mul(a0, bv));
-                if (two) S_::atomic_acc(slot(r1), S_::mul(a1, bv));
+            // kValueU products per lane per trip: independent gathers in flight
+            for (int x = lane; x < m; x += 32 * kValueU) {
+                int r[kValueU];
+                T_ a[kValueU];
+#pragma unroll
+                for (int v = 0; v < kValueU; ++v) {
+                    r[v] = -1;
+                    if (x + 32 * v < m) load_prod(Arw, Av, Arv, p0 + x + 32 * v, r[v], a[v]);
+                }
+#pragma unroll
+                for (int v = 0; v < kValueU; ++v)
+                    if (r[v] >= 0) S_::atomic_acc(slot(r[v]), S_::mul(a[v], bv));
             }
         }
         __syncthreads();
