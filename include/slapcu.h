@@ -174,8 +174,19 @@ typedef enum {
                                               (multiple of 4096, <= 32768) fold by row offset into a dense
                                               shared array, without rank lookups (0 = the rank chunk size) */
     SLAPCU_OPT_DIRECT_VALUE_DENSE_ONLY = 30, /* retired (round 2, measured 2.6x slower on MinPlus C3): only 0 */
-    SLAPCU_OPT_DIRECT_VALUE_L2 = 31        /* retired (round 2: global-atomic folds, one walk per form unit,
+    SLAPCU_OPT_DIRECT_VALUE_L2 = 31,       /* retired (round 2: global-atomic folds, one walk per form unit,
                                               measured 501 -> 609 ms on MinPlus C3): only 0 */
+    SLAPCU_OPT_DIRECT_VALUE_FORM = 32,     /* direct path, semirings with values: log2 rows of the value
+                                              form's item tile (one product walk folds values into a dense
+                                              shared array of the tile and stashes them in row order; emit
+                                              copies them into C).  0 (default) = off (pattern form + the
+                                              value pass: measured faster at C3, whose 2^14-row items are
+                                              too many and too small), -1 = auto (2^14 rows for accumulators
+                                              of <= 4 bytes, 2^13 for 8 bytes), 12..15 = that height */
+    SLAPCU_OPT_DIRECT_VALUE_TINY_RUN = 33  /* direct path value walks: runs (A column x tile) of at most this
+                                              many products are folded by their own thread with 4 loads in
+                                              flight; longer runs below 32 are packed 32 products per warp
+                                              step, 32 and up cut into warp units.  -1 = default */
 } slapcu_option;
 slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t value);
 

@@ -176,6 +176,15 @@ slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t v
             require(v == 0, SLAPCU_ERR_INVALID, "dense-only value chunks: removed");
             break;
         case SLAPCU_OPT_DIRECT_VALUE_TMAJOR: c.opt.direct_value_tmajor = v != 0; break;
+        case SLAPCU_OPT_DIRECT_VALUE_TINY_RUN:
+            require(v >= -1 && v <= 64, SLAPCU_ERR_INVALID, "value tiny run: -1 (default) or 0..64");
+            c.opt.direct_value_tiny_run = (int)v;
+            break;
+        case SLAPCU_OPT_DIRECT_VALUE_FORM:
+            require(v == -1 || v == 0 || (v >= 12 && v <= 15), SLAPCU_ERR_INVALID,
+                    "value form tile rows log2: -1 (auto), 0 (off) or 12..15");
+            c.opt.direct_value_form = (int)v;
+            break;
         case SLAPCU_OPT_DIRECT_SHORT_RUN:
             require(v >= 0 && v <= 256, SLAPCU_ERR_INVALID, "short run threshold: 0 (default) .. 256");
             c.opt.direct_short_run = (int)v;

@@ -497,6 +497,8 @@ struct EmitArgs {
     int vsize;        // bytes per value
     uint4 vpattern;   // 16 bytes of the value to write (1s for OrAnd)
     int nitems;
+    const uint8_t* vst;    // value form: every item's values in row order (else null: vpattern)
+    const int64_t* voff;   // their first entry per item
 };
 
 // Per-warp shared state of the emission.
@@ -660,7 +662,23 @@ __global__ void SLAPCU_EMIT_BOUNDS k_tile_emit(EmitArgs g) {
             wi[q] = wn[q];
         }
     }
-    if (g.cv) {
+    if (g.cv && g.vst) {
+        // values from the value form's stash (same order as the rows)
+        if (c > 0) {
+            const int64_t vo = g.voff[item];
+            if (g.vsize == 4) {
+                const unsigned* s = reinterpret_cast<const unsigned*>(g.vst) + vo;
+                unsigned* d = reinterpret_cast<unsigned*>(g.cv) + off;
+                for (int64_t q = lane; q < c; q += 32) d[q] = __ldg(s + q);
+            } else if (g.vsize == 8) {
+                const unsigned long long* s = reinterpret_cast<const unsigned long long*>(g.vst) + vo;
+                unsigned long long* d = reinterpret_cast<unsigned long long*>(g.cv) + off;
+                for (int64_t q = lane; q < c; q += 32) d[q] = __ldg(s + q);
+            } else {
+                for (int64_t q = lane; q < c * g.vsize; q += 32) g.cv[off * g.vsize + q] = g.vst[vo * g.vsize + q];
+            }
+        }
+    } else if (g.cv) {
         // values: c copies of the pattern value (head elements, 16-byte body, tail elements)
         uint8_t* v = g.cv + off * g.vsize;
         const int64_t bytes = c * g.vsize;
@@ -705,6 +723,7 @@ struct ValueArgs {
     void* cv;
     const void* arv;      // A's (row, value bits) interleaved (int2 for 4-byte, int4 for 8-byte values), or null
     int64_t tv_stride;    // > 0: Atpv is tile-major (entry (k, t) at t * tv_stride + k), else column-major
+    int tiny;             // runs of at most this many products are folded by their own thread
 };
 
 // One product's A row and value: from the interleaved copy when there is one
@@ -761,11 +780,12 @@ struct ValueWalkSm {
 };
 
 // Every product of B(:,j) whose A row lies in tile `t` of the pointer table
-// `tp0` (T+1 entries per A column) is folded into *slot(row) with the
-// semiring's atomic.  Runs of >= 32 products are cut into 256-product warp
-// units; shorter runs are packed 32 products per warp step (the owning B
-// entry found by a search over the batch's product prefix), so no thread
-// walks a run alone through a chain of dependent loads.
+// `tp0` (T+1 entries per A column) is handed to fold(row, product) -- for the
+// value passes the semiring's atomic into *slot(row) (into<S_>(slot)).  Runs
+// of >= 32 products are cut into 256-product warp units; shorter runs are
+// packed 32 products per warp step (the owning B entry found by a search over
+// the batch's product prefix), so no thread walks a run alone through a chain
+// of dependent loads.
 #ifndef SLAPCU_VTINY
 #define SLAPCU_VTINY 2
 #endif
@@ -783,11 +803,35 @@ constexpr int kValueUnit = SLAPCU_VALUE_UNIT;  // value walk: products per warp 
 // products in runs of <= 2 / 3..31 / >= 32 (debug variant)
 __device__ unsigned long long g_vcount[12];
 #endif
-template <int SRID, int NT, class Slot>
+// MinPlus folds test first: a product only takes the shared atomic when it
+// lowers the slot (slots only decrease), like the pattern walk's test-then-set.
+template <class S_>
+constexpr bool kMinFold = std::is_same<S_, Sr<SLAPCU_MIN_PLUS_I32>>::value || std::is_same<S_, Sr<SLAPCU_MIN_PLUS_F64>>::value;
+
+template <class S_, class Slot>
+struct AtomicInto {
+    Slot slot;
+    __device__ __forceinline__ void operator()(int r, typename S_::Acc v) const {
+        typename S_::Acc* p = slot(r);
+        if constexpr (kMinFold<S_>) {
+            // (!(cur <= v) rather than v < cur: a NaN product still reaches the atomic, as without the test)
+            if (!(*reinterpret_cast<volatile typename S_::Acc*>(p) <= v)) S_::atomic_acc(p, v);
+        } else {
+            S_::atomic_acc(p, v);
+        }
+    }
+};
+template <class S_, class Slot>
+__device__ __forceinline__ AtomicInto<S_, Slot> into(Slot s) {
+    return AtomicInto<S_, Slot>{s};
+}
+
+template <int SRID, int NT, class Fold>
 __device__ __forceinline__ void value_walk(const DevCsc& A, const DevCsc& B, const int32_t* __restrict__ Atab, int T,
-                                           int t, int j, ValueWalkSm<SRID, NT>& sh, Slot slot, int t_hi = -1,
+                                           int t, int j, ValueWalkSm<SRID, NT>& sh, Fold fold, int t_hi = -1,
                                            const void* __restrict__ Arv = nullptr, int64_t tstride = 0,
-                                           int vtag = 0, int64_t eb0 = -1, int64_t eb1 = -1) {
+                                           int vtag = 0, int64_t eb0 = -1, int64_t eb1 = -1,
+                                           int tiny = kValueTinyRun) {
     using S_ = Sr<SRID>;
     using T_ = typename S_::T;
     constexpr int NW = NT / 32;
@@ -825,15 +869,24 @@ __device__ __forceinline__ void value_walk(const DevCsc& A, const DevCsc& B, con
             if (len > 0) {
                 const int64_t st = A.cp[k] + rlo;
                 const T_ bv = Bv[i];
-                if (len <= kValueTinyRun) {
-                    // one or two products: folded by this thread right away (no
-                    // packing search -- 9 shared loads per product for runs of 1)
-                    int r0, r1 = 0;
-                    T_ a0, a1;
-                    load_prod(Arw, Av, Arv, st, r0, a0);
-                    if (len > 1) load_prod(Arw, Av, Arv, st + 1, r1, a1);
-                    S_::atomic_acc(slot(r0), S_::mul(a0, bv));
-                    if (len > 1) S_::atomic_acc(slot(r1), S_::mul(a1, bv));
+                if (len <= tiny) {
+                    // short run: folded by this thread, loads in groups of 4 in
+                    // flight (no packing search -- 9 shared loads per product)
+                    int x = 0;
+                    for (; x + 4 <= len; x += 4) {
+                        int r[4];
+                        T_ a[4];
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) load_prod(Arw, Av, Arv, st + x + v, r[v], a[v]);
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) fold(r[v], S_::mul(a[v], bv));
+                    }
+                    for (; x < len; ++x) {
+                        int r0;
+                        T_ a0;
+                        load_prod(Arw, Av, Arv, st + x, r0, a0);
+                        fold(r0, S_::mul(a0, bv));
+                    }
                 } else if (len < 32) {
                     slen = len;
                     sh.sst[tid] = st;
@@ -902,7 +955,7 @@ __device__ __forceinline__ void value_walk(const DevCsc& A, const DevCsc& B, con
                 int r;
                 T_ av;
                 load_prod(Arw, Av, Arv, p, r, av);
-                S_::atomic_acc(slot(r), S_::mul(av, sh.sbv[a]));
+                fold(r, S_::mul(av, sh.sbv[a]));
             }
         }
         const int u0 = (int)((int64_t(tot) * warp) / NW), u1 = (int)((int64_t(tot) * (warp + 1)) / NW);
@@ -935,7 +988,7 @@ __device__ __forceinline__ void value_walk(const DevCsc& A, const DevCsc& B, con
                 }
 #pragma unroll
                 for (int v = 0; v < kValueU; ++v)
-                    if (r[v] >= 0) S_::atomic_acc(slot(r[v]), S_::mul(a[v], bv));
+                    if (r[v] >= 0) fold(r[v], S_::mul(a[v], bv));
             }
         }
         __syncthreads();
@@ -989,7 +1042,8 @@ __global__ void __launch_bounds__(NT) k_tile_values(ValueArgs g) {
     if (lo == hi) return;
     for (int64_t q = lo + tid; q < hi; q += NT) val[g.crw[q] - s0] = S_::identity();
     __syncthreads();
-    value_walk<SRID, NT>(g.A, g.B, g.Atpv, g.Tv, ts, j, sh, [val, s0](int r) { return &val[r - s0]; }, -1, g.arv);
+    value_walk<SRID, NT>(g.A, g.B, g.Atpv, g.Tv, ts, j, sh, into<S_>([val, s0](int r) { return &val[r - s0]; }), -1,
+                         g.arv, 0, 0, -1, -1, g.tiny);
     T* Cv = static_cast<T*>(g.cv);
     for (int64_t q = lo + tid; q < hi; q += NT) Cv[q] = S_::out(val[g.crw[q] - s0]);
 }
@@ -1030,7 +1084,7 @@ __global__ void __launch_bounds__(NT) k_item_values_hash(ValueArgs g) {
         while (key[h] != r) h = (h + 1) & (HS - 1);
         return &val[h];
     };
-    value_walk<SRID, NT>(g.A, g.B, g.Atp, g.T, it.y, j, sh, slot, -1, g.arv);
+    value_walk<SRID, NT>(g.A, g.B, g.Atp, g.T, it.y, j, sh, into<S_>(slot), -1, g.arv, 0, 0, -1, -1, g.tiny);
     T* Cv = static_cast<T*>(g.cv);
     for (int64_t q = tid; q < c; q += NT) Cv[off + q] = S_::out(*slot(g.crw[off + q]));
 }
@@ -1100,8 +1154,8 @@ __global__ void __launch_bounds__(NT) k_item_values_rank(ValueArgs g, const Rank
     const int ts0 = min((it.y << (g.TL - g.VTL)) + ch.b0, g.Tv), ts1 = min((it.y << (g.TL - g.VTL)) + ch.b1, g.Tv);
     T* Cv = static_cast<T*>(g.cv);
     if (dense) {
-        value_walk<SRID, NT>(g.A, g.B, g.Atpv, g.Tv, ts0, j, sh, [val, r0](int r) { return &val[r - r0]; }, ts1, g.arv,
-                             g.tv_stride, 1);
+        value_walk<SRID, NT>(g.A, g.B, g.Atpv, g.Tv, ts0, j, sh, into<S_>([val, r0](int r) { return &val[r - r0]; }), ts1,
+                             g.arv, g.tv_stride, 1, -1, -1, g.tiny);
         for (int q = tid; q < n; q += NT) Cv[lo + q] = S_::out(val[g.crw[lo + q] - r0]);
         return;
     }
@@ -1122,7 +1176,8 @@ __global__ void __launch_bounds__(NT) k_item_values_rank(ValueArgs g, const Rank
         const int w = rr >> 5;
         return &val[pre16[w] + __popc(bm[w] & ((1u << (rr & 31)) - 1u))];
     };
-    value_walk<SRID, NT>(g.A, g.B, g.Atpv, g.Tv, ts0, j, sh, slot, ts1, g.arv, g.tv_stride);
+    value_walk<SRID, NT>(g.A, g.B, g.Atpv, g.Tv, ts0, j, sh, into<S_>(slot), ts1, g.arv, g.tv_stride, 0, -1, -1,
+                         g.tiny);
     for (int q = tid; q < n; q += NT) Cv[lo + q] = S_::out(val[q]);
 }
 
@@ -1170,6 +1225,233 @@ __global__ void k_value_split(int nitems, const int64_t* __restrict__ cnt, int64
         else
             large[atomicAdd(&counts[1], 1)] = i;
     }
+}
+
+// ------------------------------------------------------------ value form
+//
+// Semirings with values in ONE product walk: items are (column j, tile of 2^TL
+// rows) with TL small enough that the tile's accumulators fit in shared
+// memory (2^14 x 4 bytes, 2^13 x 8 bytes).  Every product of the item is
+// folded into val[row - t0] with the semiring's atomic and marks the row in a
+// bitmap; the item then writes its values in row order to a value stash (a
+// bump cursor hands out the space) and its pattern stash exactly like
+// k_tile_form, and emit copies the values beside the rows.  This replaces the
+// pattern walk + value re-walk pair (k_tile_form + k_item_values_rank), whose
+// rank chunks re-walked B(:,j) once per chunk.  The reference folds a column's
+// products into one accumulator the same way (spgemm.hpp:251-255).
+//
+// For MinPlus (add = min, zero = +inf, semiring.hpp:58-69) the fold tests
+// first: a product only takes the atomic when it lowers the slot, and only the
+// product meeting an untouched slot (still the identity) marks its row --
+// slots only decrease, so the thread that moves a slot off the identity is one
+// that saw it there.  Other semirings mark every product (test-then-set).
+template <int SRID>
+struct MinSentinel : std::false_type {};
+template <>
+struct MinSentinel<SLAPCU_MIN_PLUS_I32> : std::true_type {};
+template <>
+struct MinSentinel<SLAPCU_MIN_PLUS_F64> : std::true_type {};
+
+struct VFormArgs {
+    DevCsc A, B;
+    const int32_t* tab;  // A tile pointers at 2^TL rows: tile-major (tstride = A.ncols) or per column (tstride 0)
+    int64_t tstride;
+    int T, TL;
+    const int2* items;
+    const int4* units;
+    const int* order;
+    unsigned* stash;
+    const int64_t* soff;
+    const int64_t* sres;
+    unsigned char* partial;  // split items: per part slot W bitmap words, then 2^TL accumulators
+    int64_t pslot_bytes;
+    int64_t* cnt;
+    int* form;
+    unsigned long long* hcnt;
+    int* ticket;
+    int nunits;
+    const void* arv;           // A's (row, value) interleaved (4-byte values) or null
+    void* vst;                 // value stash: each item's values in row order
+    int64_t* voff;             // per item: its first entry in vst
+    unsigned long long* vcur;  // bump cursor into vst
+    int64_t vcap;              // entries of vst
+    int* overflow;
+    int tiny;                  // runs of at most this many products are folded by their own thread
+};
+
+template <int SRID>
+__device__ __forceinline__ void vfold(typename Sr<SRID>::Acc* val, unsigned bm0, int rr, typename Sr<SRID>::Acc v) {
+    using S_ = Sr<SRID>;
+    using Acc = typename S_::Acc;
+    if constexpr (MinSentinel<SRID>::value) {
+        const Acc cur = *reinterpret_cast<volatile Acc*>(&val[rr]);
+        if (cur == S_::identity()) mark(bm0, rr);
+        if (v < cur) S_::atomic_acc(&val[rr], v);
+    } else {
+        mark(bm0, rr);
+        S_::atomic_acc(&val[rr], v);
+    }
+}
+
+// The item's values in row order -> the value stash (and val back to the
+// identity), then its pattern stash (stash_bitmap: count, bitmap or word
+// list, clears bm).  Thread tid owns a contiguous range of bitmap words, so
+// one block scan of its output count places its values.
+template <int SRID, int NT>
+__device__ __forceinline__ void vform_finish(typename Sr<SRID>::Acc* val, unsigned* bm, unsigned* summ, uint16_t* tl,
+                                             int* wsum, int* red, int* bcs, int item, int j, const VFormArgs& g) {
+    using S_ = Sr<SRID>;
+    using T = typename S_::T;
+    constexpr int NW = NT / 32;
+    __shared__ long long vbase_sh;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int W = 1 << (g.TL - 5);
+    const int P = (W + NT - 1) / NT;
+    const int w0 = min(W, tid * P), w1 = min(W, w0 + P);
+    int c = 0;
+    for (int w = w0; w < w1; ++w) c += __popc(bm[w]);
+    int tot;
+    int o = block_excl_scan<NT>(c, wsum, &tot);
+    if (tid == 0) {
+        long long b = -1;
+        if (tot > 0) {
+            b = (long long)atomicAdd(g.vcur, (unsigned long long)tot);
+            if (b + tot > g.vcap) {
+                atomicExch(g.overflow, 1);
+                b = -1;
+            }
+        }
+        vbase_sh = b;
+        g.voff[item] = b;
+    }
+    __syncthreads();
+    const long long vb = vbase_sh;
+    T* vst = static_cast<T*>(g.vst) + (vb >= 0 ? vb : 0);
+    for (int w = w0; w < w1; ++w) {
+        unsigned x = bm[w];
+        while (x) {
+            const int r = (w << 5) + __ffs(x) - 1;
+            x &= x - 1u;
+            if (vb >= 0) vst[o] = S_::out(val[r]);
+            ++o;
+            val[r] = S_::identity();
+        }
+    }
+    for (int cc = warp; cc < W / 32; cc += NW) {
+        const unsigned nz = __ballot_sync(0xffffffffu, bm[cc * 32 + lane] != 0u);
+        if (lane == 0) summ[cc] = nz;
+    }
+    __syncthreads();
+    stash_bitmap<NT>(bm, summ, tl, W, wsum, red, bcs, item, j, g.stash + g.soff[item], g.sres[item], g.cnt, g.form,
+                     g.hcnt, nullptr);
+}
+
+__host__ __device__ __forceinline__ size_t vform_smem(int TL, size_t acc) {
+    const size_t R = size_t(1) << TL, W = R >> 5;
+    return ((acc * R + sizeof(unsigned) * (W + W / 32) + sizeof(uint16_t) * W) + 15) & ~size_t(15);
+}
+
+// Persistent like k_tile_form: CTAs take work units (row tile, then heaviest
+// first) by ticket; a unit walks its B-entry range of the item's column.
+template <int SRID, int NT>
+__global__ void __launch_bounds__(NT) k_value_form(VFormArgs g) {
+    using S_ = Sr<SRID>;
+    using Acc = typename S_::Acc;
+    extern __shared__ __align__(16) unsigned char sm_raw[];
+    const int R = 1 << g.TL, W = R >> 5;
+    Acc* val = reinterpret_cast<Acc*>(sm_raw);
+    unsigned* bm = reinterpret_cast<unsigned*>(sm_raw + sizeof(Acc) * size_t(R));
+    unsigned* summ = bm + W;
+    uint16_t* tl = reinterpret_cast<uint16_t*>(summ + W / 32);
+    __shared__ ValueWalkSm<SRID, NT> sh;
+    __shared__ int wsum2[NT / 32 + 1];
+    __shared__ int red[NT / 32];
+    __shared__ int bcs[kMaxBlocks];
+    __shared__ int ticket_sh;
+    for (int q = threadIdx.x; q < R; q += NT) val[q] = S_::identity();
+    smem_zero(bm, W + W / 32);
+    for (int b = threadIdx.x; b < kMaxBlocks; b += NT) bcs[b] = 0;
+    const unsigned bm0 = smem_addr(bm);
+    for (;;) {
+        if (threadIdx.x == 0) {
+            ticket_sh = atomicAdd(g.ticket, 1);
+            sh.nlong = 0;
+        }
+        __syncthreads();
+        const int ui = ticket_sh;
+        if (ui >= g.nunits) break;
+        const int4 u = g.units[g.order[ui]];
+        const int2 it = g.items[u.x];
+        const int64_t bs = g.B.cp[it.x];
+        const int t0 = it.y << g.TL;
+        value_walk<SRID, NT>(
+            g.A, g.B, g.tab, g.T, it.y, it.x, sh, [val, bm0, t0](int r, Acc v) { vfold<SRID>(val, bm0, r - t0, v); },
+            -1, g.arv, g.tstride, 0, bs + u.y, bs + u.z, g.tiny);
+        if (u.w >= 0) {  // one part of a split item: partial bitmap and accumulators out, then reset
+            unsigned char* slot = g.partial + int64_t(u.w) * g.pslot_bytes;
+            unsigned* pb = reinterpret_cast<unsigned*>(slot);
+            Acc* pv = reinterpret_cast<Acc*>(slot + sizeof(unsigned) * W);
+            for (int q = threadIdx.x; q < W; q += NT) {
+                pb[q] = bm[q];
+                bm[q] = 0u;
+            }
+            for (int q = threadIdx.x; q < R; q += NT) {
+                pv[q] = val[q];
+                val[q] = S_::identity();
+            }
+        } else {
+            vform_finish<SRID, NT>(val, bm, summ, tl, wsum2, red, bcs, u.x, it.x, g);
+        }
+        __syncthreads();
+    }
+}
+
+// Split items: the parts' partial bitmaps OR-ed and accumulators folded (part
+// order), then the same finish.  One CTA per split item.
+template <int SRID, int NT>
+__global__ void __launch_bounds__(NT)
+    k_value_combine(VFormArgs g, const int* __restrict__ sitems, const int* __restrict__ spart,
+                    const int* __restrict__ snp) {
+    using S_ = Sr<SRID>;
+    using Acc = typename S_::Acc;
+    extern __shared__ __align__(16) unsigned char sm_raw[];
+    const int R = 1 << g.TL, W = R >> 5;
+    Acc* val = reinterpret_cast<Acc*>(sm_raw);
+    unsigned* bm = reinterpret_cast<unsigned*>(sm_raw + sizeof(Acc) * size_t(R));
+    unsigned* summ = bm + W;
+    uint16_t* tl = reinterpret_cast<uint16_t*>(summ + W / 32);
+    __shared__ int wsum[NT / 32 + 1];
+    __shared__ int red[NT / 32];
+    __shared__ int bcs[kMaxBlocks];
+    for (int b = threadIdx.x; b < kMaxBlocks; b += NT) bcs[b] = 0;
+    const int item = sitems[blockIdx.x];
+    const int np = snp[blockIdx.x];
+    const unsigned char* p0 = g.partial + int64_t(spart[blockIdx.x]) * g.pslot_bytes;
+    for (int w = threadIdx.x; w < W; w += NT) {
+        unsigned x = 0;
+        for (int p = 0; p < np; ++p) {
+            const unsigned char* sl = p0 + int64_t(p) * g.pslot_bytes;
+            const unsigned xp = reinterpret_cast<const unsigned*>(sl)[w];
+            const Acc* pv = reinterpret_cast<const Acc*>(sl + sizeof(unsigned) * W);
+            for (unsigned y = xp; y; y &= y - 1u) {
+                const int b = __ffs(y) - 1, r = (w << 5) + b;
+                val[r] = ((x >> b) & 1u) ? S_::add(val[r], pv[r]) : pv[r];
+            }
+            x |= xp;
+        }
+        bm[w] = x;
+    }
+    __syncthreads();
+    vform_finish<SRID, NT>(val, bm, summ, tl, wsum, red, bcs, item, g.items[item].x, g);
+}
+
+// Upper bound of the heavy output entries: sum over items of min(multiplies, 2^TL).
+__global__ void k_sum_min(int64_t n, const int64_t* __restrict__ f, int64_t cap, unsigned long long* __restrict__ out) {
+    long long s = 0;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        s += lmin(f[i], cap);
+    s = warp_reduce_sum64(s);
+    if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, (unsigned long long)s);
 }
 
 // ------------------------------------------------------------ item setup
@@ -1622,6 +1904,21 @@ static uint4 value_pattern(int sr, bool ones) {
     return r;
 }
 
+// Value walks: runs of at most this many products are folded by their own thread.
+static int value_tiny_run(const Ctx& c) { return c.opt.direct_value_tiny_run >= 0 ? c.opt.direct_value_tiny_run : kValueTinyRun; }
+
+// Value form (semirings with values): log2 rows of an item tile whose
+// accumulators fit in shared memory, or 0 when the pattern form + value pass
+// run instead (option 0, or OrAnd operands without stored zeros).
+static int value_form_log2(const Ctx& c, int sr, bool ones, int64_t nrows) {
+    if (ones || c.opt.direct_value_form == 0) return 0;
+    const size_t acc = sr == SLAPCU_OR_AND_U8 ? 4 : size_t(value_size(sr));
+    int tl = c.opt.direct_value_form > 0 ? c.opt.direct_value_form : (acc <= 4 ? 14 : 13);
+    while (tl > 10 && vform_smem(tl, acc) + 24 * 1024 > size_t(c.smem_optin)) --tl;
+    while (tl > 10 && (int64_t(1) << (tl - 1)) >= nrows) --tl;
+    return tl;
+}
+
 int direct_tile_log2(const Ctx& c, int64_t nrows) {
     // auto: 2^17-row tiles up to 2^20 rows, 2^18 above (fewer items walking
     // the same B columns when rows are many and columns sparse)
@@ -1634,9 +1931,9 @@ int direct_tile_log2(const Ctx& c, int64_t nrows) {
 // The cache is keyed on the CONTENT of A's pattern (fp = pattern_fingerprint),
 // never on its address: SUMMA receive slots and pooled buffers reuse
 // addresses for different operands.
-static const int32_t* tile_pointers(Ctx& c, const DevCsc& A, uint64_t fp, int TL, int T) {
+static const int32_t* tile_pointers(Ctx& c, const DevCsc& A, uint64_t fp, int TL, int T, bool dense = true) {
     DirectCache& d = c.direct;
-    const int dmin = (int)std::min<int64_t>(c.opt.direct_dense_run_min, INT32_MAX);
+    const int dmin = dense ? (int)std::min<int64_t>(c.opt.direct_dense_run_min, INT32_MAX) : 0;
     if (d.atp_valid && d.atp_key == fp && d.atp_ncols == A.ncols && d.atp_tl == TL && d.atp_nnz == A.nnz &&
         d.dense_min == dmin)
         return d.atp.as<int32_t>();
@@ -1919,7 +2216,10 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
 
     // ---- heavy columns in column order, cut into row-tile items
     const int nh = f.bins.count[spec.nlight];
-    const int TL = direct_tile_log2(c, A.nrows);
+    // value form: one walk folds the values in small shared tiles (no value pass)
+    const int vtl = value_form_log2(c, sr, ones, A.nrows);
+    const bool vform = vtl > 0;
+    const int TL = vform ? vtl : direct_tile_log2(c, A.nrows);
     const int T = (int)((A.nrows + (int64_t(1) << TL) - 1) >> TL);
     const int W = 1 << (TL - 5);
     d.hcnt.reset(sizeof(unsigned long long) * std::max<int64_t>(n, 1), c.stream);
@@ -1927,9 +2227,10 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
     int nitems = 0;
     // words mode: the form walks A's (word, mask) pairs (one shared update
     // per distinct word of a run) instead of its rows
-    const bool words = c.opt.direct_words != 0 && A.span < INT32_MAX;
+    const bool words = !vform && c.opt.direct_words != 0 && A.span < INT32_MAX;
+    DevBuf vst, voff, vcur, arv_form;  // value form: value stash, per-item offsets, bump cursor + overflow flag
     if (nh > 0) {
-        const int32_t* Atp = words ? word_pointers(c, A, afp, TL, T) : tile_pointers(c, A, afp, TL, T);
+        const int32_t* Atp = words ? word_pointers(c, A, afp, TL, T) : tile_pointers(c, A, afp, TL, T, !vform);
         KScope ks(c, KC_BIN);
         DevBuf hflag(sizeof(int) * (n + 1), c.stream), hpre(sizeof(int) * (n + 1), c.stream);
         launch(c, k_mark_heavy, dim3(grid_for(c, n, 256)), dim3(256), 0, n, flops, lmax, spec.all_heavy != 0,
@@ -2028,7 +2329,11 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
             ++c.launches;
         }
         d.stash.reset(sizeof(unsigned) * std::max<int64_t>(swords, 4), c.stream);
-        d.partial.reset(sizeof(unsigned) * size_t(W) * std::max<int64_t>(nslots, 1), c.stream);
+        const size_t vacc = sr == SLAPCU_OR_AND_U8 ? 4 : size_t(value_size(sr));
+        const int64_t pslot_bytes =
+            vform ? int64_t((sizeof(unsigned) * size_t(W) + vacc * (size_t(1) << TL) + 15) & ~size_t(15))
+                  : int64_t(sizeof(unsigned) * size_t(W));
+        d.partial.reset(size_t(pslot_bytes) * std::max<int64_t>(nslots, 1), c.stream);
         d.cnt.reset(sizeof(int64_t) * ni1, c.stream);
         d.form.reset(sizeof(int) * ni1, c.stream);
         d.hoff.reset(sizeof(int64_t) * ni1, c.stream);
@@ -2036,7 +2341,7 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
         KScope ks2(c, KC_SYM_HEAVY);
         const int nrb = (W + kRbcWords - 1) / kRbcWords;
         int* rbc = nullptr;
-        if (!ones) {
+        if (!ones && !vform) {
             d.rbc.reset(sizeof(int) * size_t(nitems) * nrb, c.stream);
             rbc = d.rbc.as<int>();
         }
@@ -2063,13 +2368,68 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
             launch(c, kf, dim3((unsigned)grid), dim3(nt), smem, g);
         };
         const int ft = c.opt.direct_form_threads;
-        if (words)
+        if (vform) {
+            // value stash: at most min(multiplies, 2^TL) entries per item, and no more than C holds
+            DevBuf smin(sizeof(unsigned long long), c.stream);
+            SLAPCU_CUDA(cudaMemsetAsync(smin.get(), 0, sizeof(unsigned long long), c.stream));
+            if (nitems > 0)
+                launch(c, k_sum_min, dim3(grid_for(c, nitems, 256)), dim3(256), 0, int64_t(nitems),
+                       (const int64_t*)d.ifl.as<int64_t>(), int64_t(1) << TL, smin.as<unsigned long long>());
+            const int64_t vcap = std::min<int64_t>(std::max<int64_t>(capacity, 0),
+                                                   (int64_t)d2h(c, smin.as<unsigned long long>()));
+            vst = DevBuf(size_t(value_size(sr)) * std::max<int64_t>(vcap, 1), c.stream);
+            voff = DevBuf(sizeof(int64_t) * ni1, c.stream);
+            vcur = DevBuf(sizeof(unsigned long long) * 2, c.stream);
+            SLAPCU_CUDA(cudaMemsetAsync(vcur.get(), 0, sizeof(unsigned long long) * 2, c.stream));
+            const void* arvp = nullptr;
+            if (value_size(sr) == 4 && A.span > 0 && c.opt.direct_value_interleave) {
+                arv_form = DevBuf(sizeof(int2) * size_t(A.span), c.stream);
+                launch(c, k_interleave_rv, dim3(grid_for(c, A.span, 256)), dim3(256), 0, A.span, A.rw + A.base,
+                       static_cast<const int32_t*>(A.v) + A.base, arv_form.as<int2>());
+                arvp = arv_form.as<int2>() - A.base;
+            } else if (value_size(sr) == 8 && A.span > 0 && c.opt.direct_value_interleave == 2) {
+                arv_form = DevBuf(sizeof(int4) * size_t(A.span), c.stream);
+                launch(c, k_interleave_rv8, dim3(grid_for(c, A.span, 256)), dim3(256), 0, A.span, A.rw + A.base,
+                       static_cast<const long long*>(A.v) + A.base, arv_form.as<int4>());
+                arvp = arv_form.as<int4>() - A.base;
+            }
+            // the walk reads the tile-major table (a row tile's two rows stay in L2 while its units run)
+            const bool tmaj = c.opt.direct_value_tmajor != 0;
+            VFormArgs vg{A, B, tmaj ? value_tile_pointers(c, A, afp, TL, T, true) : Atp, tmaj ? A.ncols : 0, T, TL,
+                         (const int2*)d.items.as<int2>(), (const int4*)d.units.as<int4>(), (const int*)d.order.as<int>(),
+                         d.stash.as<unsigned>(), (const int64_t*)d.soff.as<int64_t>(),
+                         (const int64_t*)d.sres.as<int64_t>(), d.partial.as<unsigned char>(), pslot_bytes,
+                         d.cnt.as<int64_t>(), d.form.as<int>(), d.hcnt.as<unsigned long long>(), tick.as<int>(),
+                         (int)nunits, arvp, vst.get(), voff.as<int64_t>(), vcur.as<unsigned long long>(), vcap,
+                         reinterpret_cast<int*>(vcur.as<unsigned long long>() + 1), value_tiny_run(c)};
+            const size_t smem = vform_smem(TL, vacc);
+            dispatch_sr(sr, [&](auto id) {
+                constexpr int ID = decltype(id)::value;
+                auto go = [&](auto kf, int nt) {
+                    ensure_smem(kf, smem);
+                    int per_sm = 0;
+                    SLAPCU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kf, nt, smem));
+                    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(nunits, int64_t(std::max(per_sm, 1)) * c.num_sms));
+                    launch(c, kf, dim3((unsigned)grid), dim3(nt), smem, vg);
+                };
+                if (c.opt.direct_value_threads == 512)
+                    go(k_value_form<ID, 512>, 512);
+                else
+                    go(k_value_form<ID, 256>, 256);
+                if (nsplit > 0) {
+                    auto kc = k_value_combine<ID, 256>;
+                    ensure_smem(kc, smem);
+                    launch(c, kc, dim3(nsplit), dim3(256), smem, vg, (const int*)si, (const int*)(si + nitems),
+                           (const int*)(si + 2 * nitems));
+                }
+            });
+        } else if (words)
             ft == 512 ? form(k_tile_form<512, true>, 512) : ft == 128 ? form(k_tile_form<128, true>, 128)
                                                           : form(k_tile_form<256, true>, 256);
         else
             ft == 512 ? form(k_tile_form<512, false>, 512) : ft == 128 ? form(k_tile_form<128, false>, 128)
                                                            : form(k_tile_form<256, false>, 256);
-        if (nsplit > 0) {
+        if (nsplit > 0 && !vform) {
             auto kc = k_tile_combine<kFormThreads>;
             const size_t smem = sizeof(unsigned) * (W + W / 32) + sizeof(uint16_t) * W;
             ensure_smem(kc, smem);
@@ -2092,6 +2452,9 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
     }
     const int64_t total = d2h(c, c_colptr + n);
     d.last_nnz = total;
+    if (vform && nitems > 0 && total <= capacity &&
+        d2h(c, reinterpret_cast<const int*>(vcur.as<unsigned long long>() + 1)) != 0)
+        throw Fail{SLAPCU_ERR_CUDA, "value form: value stash overflow"};
     if (total > capacity)
         throw Fail{SLAPCU_ERR_BUDGET, "output needs " + std::to_string(total) + " entries, capacity " +
                                           std::to_string(capacity)};
@@ -2100,8 +2463,9 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
         EmitArgs e{(const int2*)d.items.as<int2>(), (const int64_t*)d.cnt.as<int64_t>(), (const int*)d.form.as<int>(),
                    (const unsigned*)d.stash.as<unsigned>(), (const int64_t*)d.soff.as<int64_t>(),
                    (const int64_t*)d.hoff.as<int64_t>(), (const int64_t*)d.lp.as<int64_t>(), TL, crw,
-                   ones ? static_cast<uint8_t*>(cv) : nullptr,  // 1s here, else the value pass
-                   value_size(sr), value_pattern(sr, ones), nitems};
+                   (ones || vform) ? static_cast<uint8_t*>(cv) : nullptr,  // 1s / the value form's values, else the value pass
+                   value_size(sr), value_pattern(sr, ones), nitems,
+                   vform ? (const uint8_t*)vst.get() : nullptr, vform ? (const int64_t*)voff.as<int64_t>() : nullptr};
         const size_t smem = 0;
         auto emit = [&](auto ke, int nt) {
             ensure_smem(ke, smem);
@@ -2114,7 +2478,7 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
         emit(k_tile_emit<SLAPCU_EMIT_NT>, SLAPCU_EMIT_NT);  // (per-warp state is static shared memory)
 
     }
-    if (nitems > 0 && !ones) {
+    if (nitems > 0 && !ones && !vform) {
         KScope ks(c, KC_NUM_HEAVY);
         // sub-tiles are whole 4096-row blocks of the item (or the item itself)
         const int VTL = std::min(TL, std::max(12, c.opt.direct_value_tile_log2));
@@ -2141,7 +2505,8 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
         SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
         ValueArgs va{A, B, Atpv, Tv, VTL, TL, Atp, T, (const int2*)d.items.as<int2>(), nullptr,
                      (const int64_t*)d.cnt.as<int64_t>(), (const int64_t*)d.hoff.as<int64_t>(),
-                     (const int64_t*)d.lp.as<int64_t>(), (const int*)d.rbc.as<int>(), crw, cv, nullptr, 0};
+                     (const int64_t*)d.lp.as<int64_t>(), (const int*)d.rbc.as<int>(), crw, cv, nullptr, 0,
+                     value_tiny_run(c)};
         // 4-byte values: A's rows and values interleaved, so a product's gather
         // is one 8-byte load (one sector) instead of one from each array
         DevBuf arv;
@@ -2281,11 +2646,13 @@ bool direct_exact(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int alg, i
     DevBuf fl(sizeof(int64_t) * std::max<int64_t>(N, 1), c.stream);
     int64_t tot = 0;
     spgemm_flops(c, A, B, fl.as<int64_t>(), &tot);
-    std::vector<int64_t> hf(N);
-    if (N) SLAPCU_CUDA(cudaMemcpyAsync(hf.data(), fl.get(), sizeof(int64_t) * N, cudaMemcpyDeviceToHost, c.stream));
-    SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
-    int64_t cap = 0;
-    for (int64_t x = 0; x < N; ++x) cap += std::min(hf[x], A.nrows);
+    // the output bound sum_j min(flops_j, nrows), reduced on the device (one 8-byte read back)
+    DevBuf bsum(sizeof(unsigned long long), c.stream);
+    SLAPCU_CUDA(cudaMemsetAsync(bsum.get(), 0, sizeof(unsigned long long), c.stream));
+    if (N)
+        launch(c, k_sum_min, dim3(grid_for(c, N, 256)), dim3(256), 0, N, (const int64_t*)fl.as<int64_t>(), A.nrows,
+               bsum.as<unsigned long long>());
+    const int64_t cap = (int64_t)d2h(c, bsum.as<unsigned long long>());
     if (budget > 0 && cap * (4 + vs) > budget) return false;
     DirectCache& d = c.direct;
     d.dist_rw.reset(sizeof(int32_t) * std::max<int64_t>(cap, 1), c.stream);

@@ -128,6 +128,7 @@ def test_direct_value_pass(port, sr, vtl, hash_, rank):
     want = port.spgemm(sr.id, a, a)
     ctx = P.Context()
     ctx.set_option(L.OPT_DIRECT_ESC, 0)  # the bitmap value pass is the subject
+    ctx.set_option(L.OPT_DIRECT_VALUE_FORM, 0)  # (not the one-walk value form)
     ctx.set_option(L.OPT_DIRECT_TILE_ROWS_LOG2, 14 if hash_ else 12)
     ctx.set_option(L.OPT_DIRECT_VALUE_TILE_ROWS_LOG2, vtl)
     ctx.set_option(L.OPT_DIRECT_VALUE_HASH, hash_)
@@ -148,6 +149,7 @@ def test_direct_value_tmajor(port, sr, tmajor, dense_rows):
     want = port.spgemm(sr.id, a, a)
     ctx = P.Context()
     ctx.set_option(L.OPT_DIRECT_ESC, 0)  # the bitmap value pass is the subject
+    ctx.set_option(L.OPT_DIRECT_VALUE_FORM, 0)  # (not the one-walk value form)
     ctx.set_option(L.OPT_DIRECT_VALUE_TMAJOR, tmajor)
     ctx.set_option(L.OPT_DIRECT_VALUE_DENSE_ROWS, dense_rows)
     ctx.set_option(L.OPT_DIRECT_VALUE_HASH, 0)
@@ -167,6 +169,7 @@ def test_direct_value_interleave(port, sr, interleave):
     want = port.spgemm(sr.id, a, a)
     ctx = P.Context()
     ctx.set_option(L.OPT_DIRECT_ESC, 0)  # the bitmap value pass is the subject
+    ctx.set_option(L.OPT_DIRECT_VALUE_FORM, 0)  # (not the one-walk value form)
     ctx.set_option(L.OPT_DIRECT_TILE_ROWS_LOG2, 12)
     ctx.set_option(L.OPT_DIRECT_VALUE_INTERLEAVE, interleave)
     got = P.local_spgemm(to_device(a), to_device(a), sr, ctx=ctx, method="direct")

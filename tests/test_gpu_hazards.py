@@ -48,6 +48,7 @@ def test_value_pass_ragged_row_count(port, nrows, sr):
     for rank, tmajor in ((-1, 0), (4096, 0), (-1, 1)):  # default chunk (8192 / 4096 by width), 4096; tile-major
         ctx = P.Context()
         ctx.set_option(L.OPT_DIRECT_ESC, 0)  # the bitmap value pass is the subject (low cf would pick ESC)
+        ctx.set_option(L.OPT_DIRECT_VALUE_FORM, 0)
         if rank > 0:
             ctx.set_option(L.OPT_DIRECT_VALUE_RANK, rank)
         ctx.set_option(L.OPT_DIRECT_VALUE_TMAJOR, tmajor)
