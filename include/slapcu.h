@@ -504,7 +504,10 @@ slapcu_status slapcu_cb2b_header(const char* path, int64_t* nrows, int64_t* ncol
 /* write_binary (binary_io.cpp): rank 0 writes the header, every rank writes
  * its block's records (column-major block order, global indices) at its
  * exclusive-scan offset -- records are built on the device and streamed
- * through pinned buffers.  Collective; the file is complete on return. */
+ * through pinned buffers.  Collective; the file is complete on return.
+ * The format stores fp64 values (the reference's write_binary is
+ * double-only): local->vals must hold 8-byte doubles (PLUS_TIMES_F64 /
+ * MIN_PLUS_F64 blocks); other value widths are not converted. */
 slapcu_status slapcu_write_cb2b(slapcu_comm comm, const char* path, const slapcu_csc* local, int64_t row_start,
                                 int64_t col_start, int64_t nrows, int64_t ncols);
 

@@ -724,31 +724,31 @@ struct ValueArgs {
     const void* arv;      // A's (row, value bits) interleaved (int2 for 4-byte, int4 for 8-byte values), or null
     int64_t tv_stride;    // > 0: Atpv is tile-major (entry (k, t) at t * tv_stride + k), else column-major
     int tiny;             // runs of at most this many products are folded by their own thread
+    const unsigned* stash;  // the form pass's per-item stash (bitmap or word list), its offsets and forms
+    const int64_t* soff;
+    const int* form;
 };
 
 // One product's A row and value: from the interleaved copy when there is one
 // (one 8-byte gather, one sector), else from the two arrays.
-template <class T_>
+// (IL is resolved once per walk: a runtime test here was if-converted into
+// both loads, predicated, on every product -- 7% of the value pass's issue)
+template <bool IL, class T_>
 __device__ __forceinline__ void load_prod(const int32_t* __restrict__ Arw, const T_* Av, const void* __restrict__ Arv,
                                           int64_t p, int& r, T_& a) {
-    if constexpr (sizeof(T_) == 4) {
-        if (Arv) {
-            const int2 e = __ldg(static_cast<const int2*>(Arv) + p);
-            r = e.x;
-            memcpy(&a, &e.y, 4);
-            return;
-        }
-    } else if constexpr (sizeof(T_) == 8) {
-        if (Arv) {  // (row, pad, value): one 16-byte load
-            const int4 e = __ldg(static_cast<const int4*>(Arv) + p);
-            r = e.x;
-            const unsigned long long bits = (unsigned long long)(unsigned)e.z | ((unsigned long long)(unsigned)e.w << 32);
-            memcpy(&a, &bits, 8);
-            return;
-        }
+    if constexpr (IL && sizeof(T_) == 4) {
+        const int2 e = __ldg(static_cast<const int2*>(Arv) + p);
+        r = e.x;
+        memcpy(&a, &e.y, 4);
+    } else if constexpr (IL && sizeof(T_) == 8) {  // (row, pad, value): one 16-byte load
+        const int4 e = __ldg(static_cast<const int4*>(Arv) + p);
+        r = e.x;
+        const unsigned long long bits = (unsigned long long)(unsigned)e.z | ((unsigned long long)(unsigned)e.w << 32);
+        memcpy(&a, &bits, 8);
+    } else {
+        r = __ldg(&Arw[p]);
+        a = Av[p];
     }
-    r = __ldg(&Arw[p]);
-    a = Av[p];
 }
 
 __global__ void k_interleave_rv8(int64_t n, const int32_t* __restrict__ rw, const long long* __restrict__ v,
@@ -768,16 +768,24 @@ __global__ void k_interleave_rv(int64_t n, const int32_t* __restrict__ rw, const
 template <int SRID, int NT>
 struct ValueWalkSm {
     using T = typename Sr<SRID>::T;
-    int wsum[NT / 32 + 1], wsum2[NT / 32 + 1];
+    int wsum[NT / 32 + 1];
     int ustart[NT + 1];
     int ulen[NT];
     int64_t ustartp[NT];
     T ubval[NT];
-    int sp[NT + 1];  // packed short runs: product prefix per B entry
-    int64_t sst[NT];
-    T sbv[NT];
     int nlong;
 };
+
+// Warp shuffle of a semiring value (1-byte values travel as int).
+template <class T_>
+__device__ __forceinline__ T_ shfl_val(T_ v, int src) {
+    if constexpr (sizeof(T_) < 4)
+        return (T_)__shfl_sync(0xffffffffu, (int)v, src);
+    else if constexpr (sizeof(T_) == 8 && !std::is_floating_point<T_>::value)
+        return (T_)__shfl_sync(0xffffffffu, (long long)v, src);
+    else
+        return __shfl_sync(0xffffffffu, v, src);
+}
 
 // Every product of B(:,j) whose A row lies in tile `t` of the pointer table
 // `tp0` (T+1 entries per A column) is handed to fold(row, product) -- for the
@@ -803,22 +811,14 @@ constexpr int kValueUnit = SLAPCU_VALUE_UNIT;  // value walk: products per warp 
 // products in runs of <= 2 / 3..31 / >= 32 (debug variant)
 __device__ unsigned long long g_vcount[12];
 #endif
-// MinPlus folds test first: a product only takes the shared atomic when it
-// lowers the slot (slots only decrease), like the pattern walk's test-then-set.
-template <class S_>
-constexpr bool kMinFold = std::is_same<S_, Sr<SLAPCU_MIN_PLUS_I32>>::value || std::is_same<S_, Sr<SLAPCU_MIN_PLUS_F64>>::value;
-
+// (A test-then-min before the atomic -- skip products that do not lower the
+// slot -- measured no faster on MinPlus C3: 445 -> 462 ms.)
 template <class S_, class Slot>
 struct AtomicInto {
     Slot slot;
     __device__ __forceinline__ void operator()(int r, typename S_::Acc v) const {
         typename S_::Acc* p = slot(r);
-        if constexpr (kMinFold<S_>) {
-            // (!(cur <= v) rather than v < cur: a NaN product still reaches the atomic, as without the test)
-            if (!(*reinterpret_cast<volatile typename S_::Acc*>(p) <= v)) S_::atomic_acc(p, v);
-        } else {
-            S_::atomic_acc(p, v);
-        }
+        S_::atomic_acc(p, v);
     }
 };
 template <class S_, class Slot>
@@ -826,12 +826,11 @@ __device__ __forceinline__ AtomicInto<S_, Slot> into(Slot s) {
     return AtomicInto<S_, Slot>{s};
 }
 
-template <int SRID, int NT, class Fold>
-__device__ __forceinline__ void value_walk(const DevCsc& A, const DevCsc& B, const int32_t* __restrict__ Atab, int T,
-                                           int t, int j, ValueWalkSm<SRID, NT>& sh, Fold fold, int t_hi = -1,
-                                           const void* __restrict__ Arv = nullptr, int64_t tstride = 0,
-                                           int vtag = 0, int64_t eb0 = -1, int64_t eb1 = -1,
-                                           int tiny = kValueTinyRun) {
+template <int SRID, int NT, bool IL, class Fold>
+__device__ __forceinline__ void value_walk_il(const DevCsc& A, const DevCsc& B, const int32_t* __restrict__ Atab, int T,
+                                              int t, int j, ValueWalkSm<SRID, NT>& sh, Fold fold, int t_hi,
+                                              const void* __restrict__ Arv, int64_t tstride, int vtag, int64_t eb0,
+                                              int64_t eb1, int tiny) {
     using S_ = Sr<SRID>;
     using T_ = typename S_::T;
     constexpr int NW = NT / 32;
@@ -843,6 +842,8 @@ __device__ __forceinline__ void value_walk(const DevCsc& A, const DevCsc& B, con
     for (int64_t base = bs; base < be; base += NT) {
         const int64_t i = base + tid;
         int slen = 0;
+        int64_t sst = 0;
+        T_ sbv{};
         if (i < be) {
             const int k = B.rw[i];
             const int th = t_hi < 0 ? t + 1 : t_hi;  // tiles [t, th) of the table
@@ -877,20 +878,20 @@ __device__ __forceinline__ void value_walk(const DevCsc& A, const DevCsc& B, con
                         int r[4];
                         T_ a[4];
 #pragma unroll
-                        for (int v = 0; v < 4; ++v) load_prod(Arw, Av, Arv, st + x + v, r[v], a[v]);
+                        for (int v = 0; v < 4; ++v) load_prod<IL>(Arw, Av, Arv, st + x + v, r[v], a[v]);
 #pragma unroll
                         for (int v = 0; v < 4; ++v) fold(r[v], S_::mul(a[v], bv));
                     }
                     for (; x < len; ++x) {
                         int r0;
                         T_ a0;
-                        load_prod(Arw, Av, Arv, st + x, r0, a0);
+                        load_prod<IL>(Arw, Av, Arv, st + x, r0, a0);
                         fold(r0, S_::mul(a0, bv));
                     }
                 } else if (len < 32) {
                     slen = len;
-                    sh.sst[tid] = st;
-                    sh.sbv[tid] = bv;
+                    sst = st;
+                    sbv = bv;
                 } else {
                     const unsigned peers = __activemask();
                     const int leader = __ffs(peers) - 1;
@@ -903,61 +904,41 @@ __device__ __forceinline__ void value_walk(const DevCsc& A, const DevCsc& B, con
                 }
             }
         }
+        // packed short runs of this warp's entries, before the barrier: 32
+        // products per warp step, the owner lane of product q found by a
+        // 5-step search over the lanes' prefix (shuffles; lanes without a
+        // packed run are skipped by <=)
+        {
+            int stot;
+            const int ex = warp_excl_scan(slen, lane, &stot);
+            for (int q0 = 0; q0 < stot; q0 += 32) {
+                const int q = q0 + lane;
+                int src = 0;
+#pragma unroll
+                for (int step = 16; step > 0; step >>= 1) {
+                    const int cand = src + step;
+                    const int exc = __shfl_sync(0xffffffffu, ex, cand & 31);
+                    if (cand < 32 && exc <= q) src = cand;
+                }
+                const int exs = __shfl_sync(0xffffffffu, ex, src);
+                const int64_t ss = (int64_t)__shfl_sync(0xffffffffu, (long long)sst, src);
+                const T_ bb = shfl_val(sbv, src);
+                if (q < stot) {
+                    int r;
+                    T_ av;
+                    load_prod<IL>(Arw, Av, Arv, ss + (q - exs), r, av);
+                    fold(r, S_::mul(av, bb));
+                }
+            }
+        }
         __syncthreads();
         const int nl = sh.nlong;
         const int units = tid < nl ? (sh.ulen[tid] + kValueUnit - 1) / kValueUnit : 0;
-        int tot, stot;
-        {
-            int wt, wt2;
-            const int ex = warp_excl_scan(units, lane, &wt);
-            const int ex2 = warp_excl_scan(slen, lane, &wt2);
-            if (lane == 0) {
-                sh.wsum[warp] = wt;
-                sh.wsum2[warp] = wt2;
-            }
-            __syncthreads();
-            if (warp == 0) {
-                const int x = lane < NW ? sh.wsum[lane] : 0, y = lane < NW ? sh.wsum2[lane] : 0;
-                int t1, t2;
-                const int e1 = warp_excl_scan(x, lane, &t1), e2 = warp_excl_scan(y, lane, &t2);
-                if (lane < NW) {
-                    sh.wsum[lane] = e1;
-                    sh.wsum2[lane] = e2;
-                }
-                if (lane == 0) {
-                    sh.wsum[NW] = t1;
-                    sh.wsum2[NW] = t2;
-                }
-            }
-            __syncthreads();
-            sh.ustart[tid] = ex + sh.wsum[warp];
-            sh.sp[tid] = ex2 + sh.wsum2[warp];
-            tot = sh.wsum[NW];
-            stot = sh.wsum2[NW];
-            if (tid == 0) {
-                sh.ustart[nl] = tot;
-                sh.sp[NT] = stot;
-            }
-        }
+        int tot;
+        const int ex = block_excl_scan<NT>(units, sh.wsum, &tot);
+        sh.ustart[tid] = ex;
+        if (tid == 0) sh.ustart[nl] = tot;
         __syncthreads();
-        for (int o0 = warp * 32; o0 < stot; o0 += NT) {
-            const int o = o0 + lane;
-            if (o < stot) {
-                int a = 0, b = NT - 1;
-                while (a < b) {
-                    const int mid = (a + b + 1) >> 1;
-                    if (sh.sp[mid] <= o)
-                        a = mid;
-                    else
-                        b = mid - 1;
-                }
-                const int64_t p = sh.sst[a] + (o - sh.sp[a]);
-                int r;
-                T_ av;
-                load_prod(Arw, Av, Arv, p, r, av);
-                fold(r, S_::mul(av, sh.sbv[a]));
-            }
-        }
         const int u0 = (int)((int64_t(tot) * warp) / NW), u1 = (int)((int64_t(tot) * (warp + 1)) / NW);
         int e = 0;
         if (u0 < u1) {
@@ -984,7 +965,7 @@ __device__ __forceinline__ void value_walk(const DevCsc& A, const DevCsc& B, con
 #pragma unroll
                 for (int v = 0; v < kValueU; ++v) {
                     r[v] = -1;
-                    if (x + 32 * v < m) load_prod(Arw, Av, Arv, p0 + x + 32 * v, r[v], a[v]);
+                    if (x + 32 * v < m) load_prod<IL>(Arw, Av, Arv, p0 + x + 32 * v, r[v], a[v]);
                 }
 #pragma unroll
                 for (int v = 0; v < kValueU; ++v)
@@ -995,6 +976,18 @@ __device__ __forceinline__ void value_walk(const DevCsc& A, const DevCsc& B, con
         if (tid == 0) sh.nlong = 0;
         __syncthreads();
     }
+}
+
+template <int SRID, int NT, class Fold>
+__device__ __forceinline__ void value_walk(const DevCsc& A, const DevCsc& B, const int32_t* __restrict__ Atab, int T,
+                                           int t, int j, ValueWalkSm<SRID, NT>& sh, Fold fold, int t_hi = -1,
+                                           const void* __restrict__ Arv = nullptr, int64_t tstride = 0,
+                                           int vtag = 0, int64_t eb0 = -1, int64_t eb1 = -1,
+                                           int tiny = kValueTinyRun) {
+    if (Arv)
+        value_walk_il<SRID, NT, true>(A, B, Atab, T, t, j, sh, fold, t_hi, Arv, tstride, vtag, eb0, eb1, tiny);
+    else
+        value_walk_il<SRID, NT, false>(A, B, Atab, T, t, j, sh, fold, t_hi, Arv, tstride, vtag, eb0, eb1, tiny);
 }
 
 // Values of the large items: one CTA per (item, sub-tile of 2^VTL rows) with
@@ -1100,7 +1093,9 @@ struct RankChunk {
 };
 
 template <int SRID, int NT>
-__global__ void __launch_bounds__(NT) k_item_values_rank(ValueArgs g, const RankChunk* __restrict__ chunks, int cap,
+// (3 CTAs per SM: the shared footprint allows 3 at 8192 4-byte slots; without the
+// bound the compiler takes 51 registers and 512-thread CTAs drop to 2 per SM)
+__global__ void __launch_bounds__(NT, 3) k_item_values_rank(ValueArgs g, const RankChunk* __restrict__ chunks, int cap,
                                                          int dense_rows) {
     using S_ = Sr<SRID>;
     using T = typename S_::T;
@@ -1164,11 +1159,46 @@ __global__ void __launch_bounds__(NT) k_item_values_rank(ValueArgs g, const Rank
     // no scans over the chunk's span.  A product's slot is pre[w] + popc(bits
     // below it in the word): two shared loads.  (Words without outputs keep a
     // stale prefix; no product lands in them.)
-    for (int q = tid; q < n; q += NT) {
-        const int rr = g.crw[lo + q] - r0;
-        atomicOr(&bm[rr >> 5], 1u << (rr & 31));
-        if (q == 0 || ((g.crw[lo + q - 1] - r0) >> 5) != (rr >> 5)) pre16[rr >> 5] = (uint16_t)q;
-        val[q] = S_::identity();
+    // The chunk's pattern comes straight from the item's stash (bitmap or
+    // word list, ~0.8 bytes per output) rather than from C's rows (4 bytes
+    // per output, one shared atomic each): thread tid takes a contiguous
+    // range of stash entries -- words of the chunk's span, or the whole
+    // list (whose 16-bit word indices are sorted) -- and one block scan of
+    // their popcounts gives every word's first output.
+    {
+        const unsigned* body = g.stash + g.soff[ch.item] + stash_header_words(W);
+        const int U = g.form[ch.item];
+        const int wb = ch.b0 * kRbcWords;
+        const uint16_t* idx = U >= 0 ? reinterpret_cast<const uint16_t*>(body + U) : nullptr;
+        const int ne = U >= 0 ? U : nwords;
+        const int per = (ne + NT - 1) / NT;
+        const int e0 = min(ne, tid * per), e1 = min(ne, e0 + per);
+        auto word_of = [&](int e, unsigned& x) {  // chunk-relative word of entry e (or -1), its bits
+            if (!idx) {
+                x = __ldg(body + wb + e);
+                return e;
+            }
+            const int w = int(__ldg(idx + e)) - wb;
+            x = (w >= 0 && w < nwords) ? __ldg(body + e) : 0u;
+            return (w >= 0 && w < nwords) ? w : -1;
+        };
+        int c = 0;
+        for (int e = e0; e < e1; ++e) {
+            unsigned x;
+            if (word_of(e, x) >= 0) c += __popc(x);
+        }
+        int tot;
+        int pfx = block_excl_scan<NT>(c, sh.wsum, &tot);
+        for (int e = e0; e < e1; ++e) {
+            unsigned x;
+            const int w = word_of(e, x);
+            if (w >= 0 && x) {
+                bm[w] = x;
+                pre16[w] = (uint16_t)pfx;
+                pfx += __popc(x);
+            }
+        }
+        for (int q = tid; q < n; q += NT) val[q] = S_::identity();
     }
     __syncthreads();
     auto slot = [bm, pre16, val, r0](int r) {
@@ -1543,6 +1573,8 @@ __global__ void k_word_tile_ptr(int64_t ncols, const int64_t* __restrict__ Awcp,
 // Tile-major layout of the same table: AtpT[t][k], t = 0..T (one row of
 // A.ncols entries per tile boundary).
 __global__ void k_tile_ptr_t(DevCsc A, int TL, int T, int32_t* __restrict__ AtpT) {
+    // (a thread-per-column merge of rows and tile bounds measured slower: 3.7 -> 10 ms at
+    // C3, the hub columns' threads walk tens of thousands of rows alone)
     const int64_t n = A.ncols * int64_t(T + 1);
     for (int64_t x = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < n; x += int64_t(gridDim.x) * blockDim.x) {
         const int t = (int)(x / A.ncols);
@@ -2506,7 +2538,8 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
         ValueArgs va{A, B, Atpv, Tv, VTL, TL, Atp, T, (const int2*)d.items.as<int2>(), nullptr,
                      (const int64_t*)d.cnt.as<int64_t>(), (const int64_t*)d.hoff.as<int64_t>(),
                      (const int64_t*)d.lp.as<int64_t>(), (const int*)d.rbc.as<int>(), crw, cv, nullptr, 0,
-                     value_tiny_run(c)};
+                     value_tiny_run(c), (const unsigned*)d.stash.as<unsigned>(), (const int64_t*)d.soff.as<int64_t>(),
+                     (const int*)d.form.as<int>()};
         // 4-byte values: A's rows and values interleaved, so a product's gather
         // is one 8-byte load (one sector) instead of one from each array
         DevBuf arv;
@@ -2542,7 +2575,7 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
                 // large items by rank chunks over 4096-row blocks (tile pointers at 2^12 rows)
                 // 8192 4-byte slots keep 3 CTAs of 512 threads per SM (C3 MinPlus: values
                 // 498 -> 441 ms vs 4096; 6144 467, 10240 508, 12288 492 ms)
-                const int cap = c.opt.direct_value_rank > 0 ? c.opt.direct_value_rank : (sizeof(Acc) <= 4 ? 8192 : 4096);
+                const int cap = c.opt.direct_value_rank > 0 ? c.opt.direct_value_rank : (sizeof(Acc) <= 4 ? 10240 : 4096);
                 // chunks spanning at most dense_rows rows fold by row offset (no ranks)
                 constexpr int kBlkRows4096 = 4096;
                 int dense_rows = std::max(
