@@ -234,6 +234,8 @@ __device__ __forceinline__ void tile_walk(const ET* __restrict__ Ael, const int6
 #pragma unroll
                 for (int v = 0; v < U; ++v) mark_el(bmA, r[v]);
             }
+            // (tail one load per trip: issuing the tail's loads together, predicated,
+            // measured slower on the same box, form 83.3 -> 86.2 ms)
             for (; x < m; x += 32) mark_el(bmA, __ldg(run + x));
         }
         // dense runs of this batch: OR whole words of their tile bitmaps
@@ -841,7 +843,7 @@ __device__ __forceinline__ void value_walk_il(const DevCsc& A, const DevCsc& B, 
     const int64_t bs = eb0 >= 0 ? eb0 : B.cp[j], be = eb0 >= 0 ? eb1 : B.cp[j + 1];
     for (int64_t base = bs; base < be; base += NT) {
         const int64_t i = base + tid;
-        int slen = 0;
+        int slen = 0, units = 0;
         int64_t sst = 0;
         T_ sbv{};
         if (i < be) {
@@ -892,15 +894,11 @@ __device__ __forceinline__ void value_walk_il(const DevCsc& A, const DevCsc& B, 
                     slen = len;
                     sst = st;
                     sbv = bv;
-                } else {
-                    const unsigned peers = __activemask();
-                    const int leader = __ffs(peers) - 1;
-                    int pos = 0;
-                    if (lane == leader) pos = atomicAdd(&sh.nlong, __popc(peers));
-                    pos = __shfl_sync(peers, pos, leader) + __popc(peers & ((1u << lane) - 1u));
-                    sh.ulen[pos] = len;
-                    sh.ustartp[pos] = st;
-                    sh.ubval[pos] = bv;
+                } else {  // long run: this thread's slot of the batch
+                    units = (len + kValueUnit - 1) / kValueUnit;
+                    sh.ulen[tid] = len;
+                    sh.ustartp[tid] = st;
+                    sh.ubval[tid] = bv;
                 }
             }
         }
@@ -931,18 +929,26 @@ __device__ __forceinline__ void value_walk_il(const DevCsc& A, const DevCsc& B, 
                 }
             }
         }
+        // long runs: thread slots, unit prefix = warp scan + warp bases (two
+        // barriers per batch of entries; the slot list needs no atomics or resets)
+        int wtot;
+        const int uex = warp_excl_scan(units, lane, &wtot);
+        if (lane == 31) sh.wsum[warp] = wtot;
         __syncthreads();
-        const int nl = sh.nlong;
-        const int units = tid < nl ? (sh.ulen[tid] + kValueUnit - 1) / kValueUnit : 0;
-        int tot;
-        const int ex = block_excl_scan<NT>(units, sh.wsum, &tot);
-        sh.ustart[tid] = ex;
-        if (tid == 0) sh.ustart[nl] = tot;
+        int wb = 0, tot = 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            const int x = sh.wsum[w];
+            wb += w < warp ? x : 0;
+            tot += x;
+        }
+        sh.ustart[tid] = wb + uex;
+        if (tid == 0) sh.ustart[NT] = tot;
         __syncthreads();
         const int u0 = (int)((int64_t(tot) * warp) / NW), u1 = (int)((int64_t(tot) * (warp + 1)) / NW);
         int e = 0;
-        if (u0 < u1) {
-            int a = 0, b = nl - 1;
+        if (u0 < u1) {  // the slot owning unit u0: the last slot whose prefix is <= u0
+            int a = 0, b = NT - 1;
             while (a < b) {
                 const int mid = (a + b + 1) >> 1;
                 if (sh.ustart[mid] <= u0)
@@ -953,7 +959,7 @@ __device__ __forceinline__ void value_walk_il(const DevCsc& A, const DevCsc& B, 
             e = a;
         }
         for (int u = u0; u < u1; ++u) {
-            if (sh.ustart[e + 1] <= u) ++e;
+            while (sh.ustart[e + 1] <= u) ++e;  // (slots without a long run hold no units)
             const int c0 = (u - sh.ustart[e]) * kValueUnit;
             const int64_t p0 = sh.ustartp[e] + c0;
             const int m = min(kValueUnit, sh.ulen[e] - c0);
@@ -972,9 +978,7 @@ __device__ __forceinline__ void value_walk_il(const DevCsc& A, const DevCsc& B, 
                     if (r[v] >= 0) fold(r[v], S_::mul(a[v], bv));
             }
         }
-        __syncthreads();
-        if (tid == 0) sh.nlong = 0;
-        __syncthreads();
+        __syncthreads();  // (the next batch rewrites the slots)
     }
 }
 
@@ -1137,9 +1141,9 @@ __global__ void __launch_bounds__(NT, 3) k_item_values_rank(ValueArgs g, const R
     // dense chunks (their rows fit the value array): values indexed by row
     // offset -- no bitmap, no ranks, one shared atomic per product
     const bool dense = nwords * 32 <= dense_rows;
-    if (!dense)  // (nwords is a multiple of 128 and bm 16-byte aligned)
-        for (int q = tid; q < (nwords >> 2); q += NT) reinterpret_cast<uint4*>(bm)[q] = make_uint4(0u, 0u, 0u, 0u);
-    else
+    // (nwords is a multiple of 128 and bm 16-byte aligned)
+    for (int q = tid; q < (nwords >> 2); q += NT) reinterpret_cast<uint4*>(bm)[q] = make_uint4(0u, 0u, 0u, 0u);
+    if (dense)
         for (int q = tid; q < nwords * 32; q += NT) val[q] = S_::identity();
     __syncthreads();
     const int64_t lo = range_sh[0], hi = range_sh[1];
@@ -1148,23 +1152,17 @@ __global__ void __launch_bounds__(NT, 3) k_item_values_rank(ValueArgs g, const R
     // past the matrix's last 4096-row block when nrows is not a multiple of 2^TL)
     const int ts0 = min((it.y << (g.TL - g.VTL)) + ch.b0, g.Tv), ts1 = min((it.y << (g.TL - g.VTL)) + ch.b1, g.Tv);
     T* Cv = static_cast<T*>(g.cv);
-    if (dense) {
-        value_walk<SRID, NT>(g.A, g.B, g.Atpv, g.Tv, ts0, j, sh, into<S_>([val, r0](int r) { return &val[r - r0]; }), ts1,
-                             g.arv, g.tv_stride, 1, -1, -1, g.tiny);
-        for (int q = tid; q < n; q += NT) Cv[lo + q] = S_::out(val[g.crw[lo + q] - r0]);
-        return;
-    }
-    // C's rows of the chunk are sorted, so output q IS the q-th rank: a word's
-    // prefix is the index of its first output (set where the word changes) --
-    // no scans over the chunk's span.  A product's slot is pre[w] + popc(bits
-    // below it in the word): two shared loads.  (Words without outputs keep a
-    // stale prefix; no product lands in them.)
     // The chunk's pattern comes straight from the item's stash (bitmap or
-    // word list, ~0.8 bytes per output) rather than from C's rows (4 bytes
-    // per output, one shared atomic each): thread tid takes a contiguous
-    // range of stash entries -- words of the chunk's span, or the whole
-    // list (whose 16-bit word indices are sorted) -- and one block scan of
-    // their popcounts gives every word's first output.
+    // word list, ~0.8 bytes per output), not from C's rows (4 bytes per
+    // output and a shared atomic each; this pass no longer depends on the
+    // emit pass -- run beside it on a second stream it measured no faster,
+    // the value pass fills the SMs alone): thread tid takes a
+    // contiguous range of stash entries (words of the chunk's span, or the
+    // whole list, whose 16-bit word indices are sorted) and one block scan of
+    // their popcounts gives every word's first output pre16[w].  A product's
+    // rank slot is pre16[w] + popc(bits below it in the word): two shared
+    // loads.  (Words without outputs keep a stale prefix; no product lands in
+    // them.)
     {
         const unsigned* body = g.stash + g.soff[ch.item] + stash_header_words(W);
         const int U = g.form[ch.item];
@@ -1198,9 +1196,25 @@ __global__ void __launch_bounds__(NT, 3) k_item_values_rank(ValueArgs g, const R
                 pfx += __popc(x);
             }
         }
-        for (int q = tid; q < n; q += NT) val[q] = S_::identity();
+        if (!dense)
+            for (int q = tid; q < n; q += NT) val[q] = S_::identity();
     }
     __syncthreads();
+    if (dense) {  // values indexed by row offset; outputs in row order from the chunk's bitmap
+        value_walk<SRID, NT>(g.A, g.B, g.Atpv, g.Tv, ts0, j, sh, into<S_>([val, r0](int r) { return &val[r - r0]; }), ts1,
+                             g.arv, g.tv_stride, 1, -1, -1, g.tiny);
+        const int per = (nwords + NT - 1) / NT;
+        const int w0 = min(nwords, tid * per), w1 = min(nwords, w0 + per);
+        for (int w = w0; w < w1; ++w) {
+            unsigned x = bm[w];
+            int o = pre16[w];
+            while (x) {
+                Cv[lo + o++] = S_::out(val[(w << 5) + __ffs(x) - 1]);
+                x &= x - 1u;
+            }
+        }
+        return;
+    }
     auto slot = [bm, pre16, val, r0](int r) {
         const int rr = r - r0;
         const int w = rr >> 5;
@@ -2490,6 +2504,11 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
     if (total > capacity)
         throw Fail{SLAPCU_ERR_BUDGET, "output needs " + std::to_string(total) + " entries, capacity " +
                                           std::to_string(capacity)};
+    // value pass parameters: rank chunks (every item, 4-byte values) or the
+    // small-item hash table + rank chunks (8-byte values)
+    const bool rank_path = c.opt.direct_value_rank != 0 && TL >= 12;
+    const int hopt = c.opt.direct_value_hash >= 0 ? c.opt.direct_value_hash
+                                                  : ((value_size(sr) == 4 && rank_path) ? 0 : 1);
     if (nitems > 0) {
         KScope ks(c, KC_NUM_HEAVY);
         EmitArgs e{(const int2*)d.items.as<int2>(), (const int64_t*)d.cnt.as<int64_t>(), (const int*)d.form.as<int>(),
@@ -2508,22 +2527,18 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
                             // a CTA lives as long as its largest item)
 #endif
         emit(k_tile_emit<SLAPCU_EMIT_NT>, SLAPCU_EMIT_NT);  // (per-warp state is static shared memory)
-
     }
     if (nitems > 0 && !ones && !vform) {
         KScope ks(c, KC_NUM_HEAVY);
         // sub-tiles are whole 4096-row blocks of the item (or the item itself)
         const int VTL = std::min(TL, std::max(12, c.opt.direct_value_tile_log2));
         const int Tv = (int)((A.nrows + (int64_t(1) << VTL) - 1) >> VTL);
-        const bool rank_path = c.opt.direct_value_rank != 0 && TL >= 12;
         // (one cached table at a time: only the sub-tile path needs 2^VTL rows)
         const int32_t* Atpv = rank_path ? nullptr : value_tile_pointers(c, A, afp, VTL, Tv);
         const int32_t* Atp = tile_pointers(c, A, afp, TL, T);
         // small items (<= kHashCap outputs) take the one-walk hash kernel
-        // auto: 4-byte values take every item through the rank chunks (C3 MinPlus 561 -> 531 ms,
-        // C4 product 66.1 -> 63.9 ms); 8-byte values keep the hash kernel for small items
-        const int hopt = c.opt.direct_value_hash >= 0 ? c.opt.direct_value_hash
-                                                      : ((value_size(sr) == 4 && rank_path) ? 0 : 1);
+        // auto (hopt above): 4-byte values take every item through the rank chunks (C3 MinPlus
+        // 561 -> 531 ms, C4 product 66.1 -> 63.9 ms); 8-byte values keep the hash kernel for small items
         const int hlog2 = hopt >= 14 ? 14 : 13;  // table slots (load <= 1/2)
         const int64_t hcap = hopt ? (int64_t(1) << hlog2) / 2 : -1;
         DevBuf lists(sizeof(int) * (2 * size_t(nitems) + 2), c.stream), lc(sizeof(int) * 2, c.stream);

@@ -77,24 +77,46 @@ __global__ void k_expand(DevCsc A, DevCsc B, int64_t e0, int64_t ne, const int64
         const int64_t o0 = __shfl_sync(0xffffffffu, x < ne ? eoff[x] : 0, 0);  // the warp's first product
         int tot;
         const int ex = warp_excl_scan(len, lane, &tot);
-        for (int q0 = 0; q0 < tot; q0 += 32) {
-            const int q = q0 + lane;
-            // owner: the last lane whose prefix is <= q (lanes with len 0 are skipped by <=)
-            int src = 0;
+        // kExpandU warp steps at a time: every lane has kExpandU independent
+        // (row, value) gathers in flight (one step at a time left the kernel
+        // latency-bound: long_scoreboard 86%, C5 expand 3.5 ms)
+        constexpr int kExpandU = 4;
+        for (int q0 = 0; q0 < tot; q0 += 32 * kExpandU) {
+            int64_t pp[kExpandU];
+            T bv[kExpandU];
+            K hv[kExpandU];
 #pragma unroll
-            for (int step = 16; step > 0; step >>= 1) {
-                const int cand = src + step;
-                const int exc = __shfl_sync(0xffffffffu, ex, cand & 31);
-                if (cand < 32 && exc <= q) src = cand;
+            for (int u = 0; u < kExpandU; ++u) {
+                const int q = q0 + 32 * u + lane;
+                // owner: the last lane whose prefix is <= q (lanes with len 0 are skipped by <=)
+                int src = 0;
+#pragma unroll
+                for (int step = 16; step > 0; step >>= 1) {
+                    const int cand = src + step;
+                    const int exc = __shfl_sync(0xffffffffu, ex, cand & 31);
+                    if (cand < 32 && exc <= q) src = cand;
+                }
+                const int exs = __shfl_sync(0xffffffffu, ex, src);
+                pp[u] = (int64_t)__shfl_sync(0xffffffffu, (long long)s, src) + (q - exs);
+                hv[u] = __shfl_sync(0xffffffffu, hi, src);
+                bv[u] = __shfl_sync(0xffffffffu, b, src);
             }
-            const int exs = __shfl_sync(0xffffffffu, ex, src);
-            const int64_t ss = __shfl_sync(0xffffffffu, s, src);
-            const K hh = __shfl_sync(0xffffffffu, hi, src);
-            const T bb = __shfl_sync(0xffffffffu, b, src);
-            if (q < tot) {
-                const int64_t p = ss + (q - exs);
-                keys[o0 + q] = hh | K(A.rw[p]);
-                vals[o0 + q] = S_::mul(Av[p], bb);
+            int r[kExpandU];
+            T a[kExpandU];
+#pragma unroll
+            for (int u = 0; u < kExpandU; ++u) {
+                if (q0 + 32 * u + lane < tot) {
+                    r[u] = __ldg(&A.rw[pp[u]]);
+                    a[u] = Av[pp[u]];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kExpandU; ++u) {
+                const int q = q0 + 32 * u + lane;
+                if (q < tot) {
+                    keys[o0 + q] = hv[u] | K(r[u]);
+                    vals[o0 + q] = S_::mul(a[u], bv[u]);
+                }
             }
         }
     }

@@ -99,6 +99,46 @@ __global__ void __launch_bounds__(G* CPB)
     }
     group_sync<G, CPB>(g);
     const int m = ctr[g];
+    if constexpr (G == 32 && PER <= 4) {
+        // one warp per column (<= 128 entries): rank by counting -- every key
+        // is compared with the column's keys read as shared-memory broadcasts,
+        // and goes straight to its sorted place in the staging area (C2, ER
+        // d = 8, bin of <= 64 products: 0.94 -> 0.82 ms; at <= 256 entries the
+        // bitonic network is cheaper: 2.1 -> 2.5 ms)
+        if (active && lane == 0) {
+            const unsigned long long off = atomicAdd(scur, (unsigned long long)m);
+            off_sh[g] = off;
+            cnt[j] = m;
+            soff[j] = (int64_t)off;
+        }
+        __syncwarp();
+        if (active) {
+            const int64_t off = (int64_t)off_sh[g];
+            const int nq = (m + 31) >> 5;
+            int mk[PER], rk[PER];
+#pragma unroll
+            for (int q = 0; q < PER; ++q) {
+                const int i = lane + q * 32;
+                mk[q] = i < m ? keys[i] : INT_MAX;
+                rk[q] = 0;
+            }
+            for (int x = 0; x < m; ++x) {
+                const int kx = keys[x];
+#pragma unroll
+                for (int q = 0; q < PER; ++q)
+                    if (q < nq) rk[q] += kx < mk[q];
+            }
+#pragma unroll
+            for (int q = 0; q < PER; ++q) {
+                const int i = lane + q * 32;
+                if (i < m) {
+                    srows[off + rk[q]] = mk[q];
+                    if constexpr (!ONES) svals[off + rk[q]] = S_::out(vals[i]);
+                }
+            }
+        }
+        return;
+    }
     int P = 1;
     while (P < m) P <<= 1;
     for (int s = m + lane; s < P; s += G) keys[s] = INT_MAX;
