@@ -167,8 +167,6 @@ __device__ __forceinline__ void tile_walk(const ET* __restrict__ Ael, const int6
     // (sh.ndense and sh.nlong are zeroed by the caller before a barrier)
     for (int64_t base = b0; base < b1; base += NT) {
         const int64_t i = base + tid;
-        int slen = 0;
-        int64_t sst = 0;
         if (i < b1) {
             const int k = B.rw[i];
             const int32_t* tp = Atp + int64_t(k) * (T + 1) + t;
@@ -178,10 +176,8 @@ __device__ __forceinline__ void tile_walk(const ET* __restrict__ Ael, const int6
             if (dr.dmin && len >= dr.dmin) {
                 sh.dense[atomicAdd(&sh.ndense, 1)] = dr.slot[int64_t(k) * T + t];
             } else if (len < short_run) {
-#ifdef SLAPCU_FORM_PACK
-                slen = len;
-                sst = s;
-#else
+                // (packing the short runs per warp, 32 elements per step with a shuffle
+                // owner search, measured slower on the same box: form 83.8 -> 88.7 ms)
                 // loads in groups of 4 so a short run is not a chain of L2 round trips
                 const ET* q = Ael + s;
                 int x = 0;
@@ -193,7 +189,6 @@ __device__ __forceinline__ void tile_walk(const ET* __restrict__ Ael, const int6
                     mark_el(bmA, e3);
                 }
                 for (; x < len; ++x) mark_el(bmA, __ldg(q + x));
-#endif
             } else {
                 // long run: into the compact list (order is irrelevant)
                 const unsigned peers = __activemask();
@@ -205,36 +200,6 @@ __device__ __forceinline__ void tile_walk(const ET* __restrict__ Ael, const int6
                 sh.start[pos] = s;
             }
         }
-#ifdef SLAPCU_FORM_PACK
-        // short runs packed per warp: 32 consecutive elements per step, the
-        // owner lane found by a 5-step shuffle search -- a run's elements sit
-        // in neighbouring lanes, so a step's loads touch a few lines instead
-        // of one line per lane
-        {
-            int stot;
-            const int ex = warp_excl_scan(slen, lane, &stot);
-            for (int q0 = 0; q0 < stot; q0 += 64) {
-                ET e[2];
-#pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    const int q = q0 + 32 * u + lane;
-                    int src = 0;
-#pragma unroll
-                    for (int step = 16; step > 0; step >>= 1) {
-                        const int cand = src + step;
-                        const int exc = __shfl_sync(0xffffffffu, ex, cand & 31);
-                        if (cand < 32 && exc <= q) src = cand;
-                    }
-                    const int exs = __shfl_sync(0xffffffffu, ex, src);
-                    const int64_t ss = (int64_t)__shfl_sync(0xffffffffu, (long long)sst, src);
-                    if (q < stot) e[u] = __ldg(Ael + ss + (q - exs));
-                }
-#pragma unroll
-                for (int u = 0; u < 2; ++u)
-                    if (q0 + 32 * u + lane < stot) mark_el(bmA, e[u]);
-            }
-        }
-#endif
         __syncthreads();
         const int nl = sh.nlong;
         const int units = tid < nl ? (sh.len[tid] + kUnit - 1) / kUnit : 0;
