@@ -203,6 +203,23 @@ __global__ void __launch_bounds__(256) k_sort_warp(int ncols, const int* __restr
     }
 }
 
+// Columns of a group by product count: 2..kWarpSort -> tiny (one warp each),
+// ..kSmallSort -> small (one CTA each), more -> a long column (flag[0]).
+// (On the device: a host pass over millions of light columns cost more than
+// the sorts, C2 ESC 9.8 ms.)
+__global__ void k_esc_classify(int64_t ng, const int64_t* __restrict__ flops, int* __restrict__ tiny,
+                               int* __restrict__ small, int* __restrict__ counts) {
+    for (int64_t jj = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; jj < ng; jj += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t pj = flops[jj];
+        if (pj > 1 && pj <= kWarpSort)
+            tiny[atomicAdd(&counts[0], 1)] = (int)jj;
+        else if (pj > kWarpSort && pj <= kSmallSort)
+            small[atomicAdd(&counts[1], 1)] = (int)jj;
+        else if (pj > kSmallSort)
+            counts[2] = 1;
+    }
+}
+
 // Segment (column) begin/end offsets of the group's products.
 __global__ void k_seg_bounds(int64_t ncols, const int64_t* __restrict__ Bcp, int64_t e0, const int64_t* __restrict__ eoff,
                              int* __restrict__ beg, int* __restrict__ end) {
@@ -266,15 +283,21 @@ int64_t esc_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int64_t c
     DevBuf fl(sizeof(int64_t) * std::max<int64_t>(n, 1), c.stream);
     int64_t total = 0;
     spgemm_flops(c, A, B, fl.as<int64_t>(), &total);
-    std::vector<int64_t> hf(size_t(std::max<int64_t>(n, 1)));
-    if (n) SLAPCU_CUDA(cudaMemcpyAsync(hf.data(), fl.get(), sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c.stream));
-    std::vector<int64_t> hbcp(size_t(n) + 1);
-    SLAPCU_CUDA(cudaMemcpyAsync(hbcp.data(), B.cp, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, c.stream));
-    SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
     size_t fr = 0, tot = 0;
     SLAPCU_CUDA(cudaMemGetInfo(&fr, &tot));
     const int64_t per_prod = 2 * 8 + 2 * 4 + 2 * 8;  // keys x2 (<= 8 bytes), head, ex, values x2 (<= 8 bytes)
     const int64_t group_max = std::max<int64_t>(1, std::min<int64_t>(int64_t(1) << 30, int64_t(fr / 3) / per_prod));
+    // per-column counts and B's column pointers on the host only when the
+    // product needs several groups (one group: the bounds are B's span)
+    const bool one_group = total <= group_max;
+    std::vector<int64_t> hf, hbcp;
+    if (!one_group) {
+        hf.resize(size_t(std::max<int64_t>(n, 1)));
+        hbcp.resize(size_t(n) + 1);
+        if (n) SLAPCU_CUDA(cudaMemcpyAsync(hf.data(), fl.get(), sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c.stream));
+        SLAPCU_CUDA(cudaMemcpyAsync(hbcp.data(), B.cp, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, c.stream));
+        SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+    }
     int64_t obase = 0;
     int64_t j0 = 0;
     bool over = false;  // past capacity: keep counting for the exact requirement, write nothing
@@ -285,12 +308,17 @@ int64_t esc_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int64_t c
         while (j0 < n) {
             // the group: columns [j0, j1) with at most group_max products (a single larger column is an error)
             int64_t j1 = j0, P = 0;
-            while (j1 < n && (j1 == j0 || P + hf[j1] <= group_max)) P += hf[j1++];
+            if (one_group) {
+                j1 = n;
+                P = total;
+            } else {
+                while (j1 < n && (j1 == j0 || P + hf[j1] <= group_max)) P += hf[j1++];
+            }
             if (P > INT32_MAX)
                 throw Fail{SLAPCU_ERR_BUDGET, "ESC: column " + std::to_string(j0) + " has " + std::to_string(P) +
                                                   " products (int32 sort offsets)"};
             const int64_t ng = j1 - j0;
-            const int64_t e0 = hbcp[j0], ne = hbcp[j1] - e0;
+            const int64_t e0 = one_group ? B.base : hbcp[j0], ne = one_group ? B.span : hbcp[j1] - e0;
             int row_bits = 1, col_bits = 1;
             while ((int64_t(1) << row_bits) < A.nrows) ++row_bits;
             while ((int64_t(1) << col_bits) < ng) ++col_bits;
@@ -325,14 +353,18 @@ int64_t esc_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int64_t c
                         // per column, shared-memory sorts; a group holding any longer column:
                         // ONE stable LSD radix sort over the (column, row) keys of the group
                         // (cub's segmented sort runs a long segment on one CTA)
-                        std::vector<int> tiny, small;
-                        bool any_long = false;
-                        for (int64_t jj = 0; jj < ng; ++jj) {
-                            const int64_t pj = hf[j0 + jj];
-                            if (pj > 1 && pj <= kWarpSort) tiny.push_back((int)jj);
-                            if (pj > kWarpSort && pj <= kSmallSort) small.push_back((int)jj);
-                            if (pj > kSmallSort) any_long = true;
-                        }
+                        DevBuf lists(sizeof(int) * 2 * size_t(std::max<int64_t>(ng, 1)), c.stream),
+                            lcnt(sizeof(int) * 3, c.stream);
+                        SLAPCU_CUDA(cudaMemsetAsync(lcnt.get(), 0, sizeof(int) * 3, c.stream));
+                        int* dtiny = lists.as<int>();
+                        int* dsmall = dtiny + ng;
+                        launch(c, k_esc_classify, dim3(grid_for(c, ng, 256)), dim3(256), 0, ng,
+                               (const int64_t*)(fl.as<int64_t>() + j0), dtiny, dsmall, lcnt.as<int>());
+                        int hc[3];
+                        SLAPCU_CUDA(cudaMemcpyAsync(hc, lcnt.get(), sizeof(hc), cudaMemcpyDeviceToHost, c.stream));
+                        SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+                        int ntiny = hc[0], nsmall = hc[1];
+                        const bool any_long = hc[2] != 0;
                         if (any_long) {
                             size_t tb = 0;
                             const int bits = row_bits + col_bits;
@@ -345,31 +377,23 @@ int64_t esc_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int64_t c
                                                                             c.stream));
                             });
                             ++c.launches;
-                            tiny.clear();
-                            small.clear();
-                        } else if (tiny.size() + small.size() < size_t(ng)) {  // 0 / 1-product columns: as they are
+                            ntiny = nsmall = 0;
+                        } else if (int64_t(ntiny) + nsmall < ng) {  // 0 / 1-product columns: as they are
                             SLAPCU_CUDA(cudaMemcpyAsync(k1.get(), k0.get(), sizeof(K) * P, cudaMemcpyDeviceToDevice, c.stream));
                             SLAPCU_CUDA(cudaMemcpyAsync(v1.get(), v0.get(), sizeof(Acc) * P, cudaMemcpyDeviceToDevice, c.stream));
                         }
-                        if (!tiny.empty()) {
-                            DevBuf dl(sizeof(int) * tiny.size(), c.stream);
-                            SLAPCU_CUDA(cudaMemcpyAsync(dl.get(), tiny.data(), sizeof(int) * tiny.size(),
-                                                        cudaMemcpyHostToDevice, c.stream));
-                            launch(c, k_sort_warp<K, Acc>, dim3((unsigned)((tiny.size() + 7) / 8)), dim3(256), 0,
-                                   (int)tiny.size(), (const int*)dl.as<int>(), (const int*)beg.as<int>(),
+                        if (ntiny) {
+                            launch(c, k_sort_warp<K, Acc>, dim3((unsigned)((ntiny + 7) / 8)), dim3(256), 0,
+                                   ntiny, (const int*)dtiny, (const int*)beg.as<int>(),
                                    (const int*)end.as<int>(), K((int64_t(1) << row_bits) - 1), (const K*)k0.as<K>(),
                                    (const Acc*)v0.as<Acc>(), k1.as<K>(), v1.as<Acc>());
                         }
-                        if (!small.empty()) {
-                            DevBuf dl(sizeof(int) * small.size(), c.stream);
-                            SLAPCU_CUDA(cudaMemcpyAsync(dl.get(), small.data(), sizeof(int) * small.size(),
-                                                        cudaMemcpyHostToDevice, c.stream));
-                            launch(c, k_sort_small<K, Acc>, dim3((unsigned)small.size()), dim3(256), 0,
-                                   (const int*)dl.as<int>(), (const int*)beg.as<int>(), (const int*)end.as<int>(),
+                        if (nsmall) {
+                            launch(c, k_sort_small<K, Acc>, dim3((unsigned)nsmall), dim3(256), 0, (const int*)dsmall,
+                                   (const int*)beg.as<int>(), (const int*)end.as<int>(),
                                    K((int64_t(1) << row_bits) - 1), (const K*)k0.as<K>(), (const Acc*)v0.as<Acc>(),
                                    k1.as<K>(), v1.as<Acc>());
                         }
-                        SLAPCU_CUDA(cudaStreamSynchronize(c.stream));  // host lists above live until here
                     }
                     launch(c, k_run_heads<K>, dim3(grid_for(c, P + 1, 256)), dim3(256), 0, P, (const K*)k1.as<K>(),
                            head.as<int>());
