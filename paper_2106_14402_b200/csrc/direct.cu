@@ -2134,10 +2134,11 @@ __global__ void __launch_bounds__(256) k_sample_cf(DevCsc A, DevCsc B, const int
 // The reference picks the accumulator per column by compression: hash iff
 // flops_j / nnz(C(:,j)) >= 2 (spgemm.hpp:54, :312-317), else the k-way merge.
 // Here, for value semirings, per product: products of at most 2^28
-// multiplies with heavy columns on average (> 4096 multiplies per column, so
-// the light hash kernels do not take them) whose flops-weighted sampled
-// compression is below 2 go to the sort-merge (ESC) path, which costs per
-// product rather than per output entry (C5: 12.8 -> ~5 ms).
+// multiplies whose sampled compression is below 2 go to the sort-merge (ESC)
+// path, which costs per product rather than per output entry (C5: 12.8 ->
+// ~5 ms; C2, light columns of ~64 products at compression 1.0: 5.4 -> 4.7 ms
+// once ESC kept its per-column work on the device).  Heavy products sample
+// columns at flops quantiles, light ones evenly spaced columns.
 static bool esc_preferred(Ctx& c, const DevCsc& A, const DevCsc& B) {
     const int64_t n = B.ncols;
     if (n == 0) return false;
@@ -2146,22 +2147,31 @@ static bool esc_preferred(Ctx& c, const DevCsc& A, const DevCsc& B) {
     spgemm_flops(c, A, B, fl.as<int64_t>(), &total);
     // ESC moves ~40 bytes per product: only products it finishes in a few
     // milliseconds are candidates (a misjudged large product would cost seconds)
-    if (total <= 4096 * n || total > kEscAutoMaxProducts) return false;
+    if (total > kEscAutoMaxProducts) return false;
     const int64_t words64 = (A.nrows + 31) / 32;
     if (words64 > (int64_t(1) << 22)) return false;  // (sample bitmaps of > 16 MB each: not worth it)
-    // sampled columns at evenly spaced quantiles of the cumulative flops, so
-    // the columns holding most of the work are the ones measured
-    std::vector<int64_t> hf(static_cast<size_t>(n));
-    SLAPCU_CUDA(cudaMemcpyAsync(hf.data(), fl.get(), sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c.stream));
-    SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
     std::vector<int> cols;
-    int64_t acc = 0;
-    int next = 0;
-    for (int64_t j = 0; j < n && next < kSampleCols; ++j) {
-        acc += hf[size_t(j)];
-        while (next < kSampleCols && acc * kSampleCols > total * next) {
-            if (cols.empty() || cols.back() != (int)j) cols.push_back((int)j);
-            ++next;
+    if (total <= 4096 * n) {
+        // light columns on average (C2: 64 products each): evenly spaced sample
+        // columns -- no per-column counts on the host (1M columns: a ms of copy)
+        for (int q = 0; q < kSampleCols; ++q) {
+            const int j = (int)((n * (2 * q + 1)) / (2 * kSampleCols));
+            if (cols.empty() || cols.back() != j) cols.push_back(j);
+        }
+    } else {
+        // sampled columns at evenly spaced quantiles of the cumulative flops, so
+        // the columns holding most of the work are the ones measured
+        std::vector<int64_t> hf(static_cast<size_t>(n));
+        SLAPCU_CUDA(cudaMemcpyAsync(hf.data(), fl.get(), sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c.stream));
+        SLAPCU_CUDA(cudaStreamSynchronize(c.stream));
+        int64_t acc = 0;
+        int next = 0;
+        for (int64_t j = 0; j < n && next < kSampleCols; ++j) {
+            acc += hf[size_t(j)];
+            while (next < kSampleCols && acc * kSampleCols > total * next) {
+                if (cols.empty() || cols.back() != (int)j) cols.push_back((int)j);
+                ++next;
+            }
         }
     }
     const int ns = (int)cols.size();

@@ -179,6 +179,44 @@ __global__ void __launch_bounds__(256) k_sort_warp(int ncols, const int* __restr
     const int b = beg[j], n = end[j] - b;
     int N = 1;
     while (N < n) N <<= 1;
+    if (N <= 64) {
+        // <= 64 products: the same network in registers, element e = r * 32 + lane,
+        // partners across lanes by shuffles, across the two registers in-thread
+        // (no shared-memory round trip per stage)
+        unsigned long long x[2];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int e = r * 32 + lane;
+            x[r] = e < n ? ((unsigned long long)(k0[b + e] & row_mask) << 11) | (unsigned long long)e : ~0ull;
+        }
+        for (int size = 2; size <= N; size <<= 1) {
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                if (stride == 32) {  // (size == 64: ascending)
+                    const unsigned long long lo = x[0] < x[1] ? x[0] : x[1], hi = x[0] < x[1] ? x[1] : x[0];
+                    x[0] = lo;
+                    x[1] = hi;
+                    continue;
+                }
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    const int e = r * 32 + lane;
+                    const unsigned long long y = __shfl_xor_sync(0xffffffffu, x[r], stride);
+                    const bool keep_min = ((e & stride) == 0) == ((e & size) == 0);
+                    x[r] = keep_min ? (x[r] < y ? x[r] : y) : (x[r] < y ? y : x[r]);
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int q = r * 32 + lane;
+            if (q < n) {
+                const int src = (int)(x[r] & 2047ull);
+                k1[b + q] = k0[b + src];
+                v1[b + q] = v0[b + src];
+            }
+        }
+        return;
+    }
     for (int q = lane; q < N; q += 32)
         sk[q] = q < n ? ((unsigned long long)(k0[b + q] & row_mask) << 11) | (unsigned long long)q : ~0ull;
     __syncwarp();

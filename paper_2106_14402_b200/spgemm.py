@@ -405,6 +405,8 @@ def local_spgemm(a, b, sr: Semiring, alg=SpGemmAlg.hybrid, threads: int = 1, ctx
         ctx.check(ctx.lib.slapcu_spgemm_direct(ctx.h, C.byref(av), C.byref(bv), sr.id, int(alg), cap, cp.data_ptr(),
                                                rw.data_ptr(), vals.data_ptr(), C.byref(nnz)), "direct")
         n = int(nnz.value)
+        if n * 10 >= cap * 9:  # the bound was (nearly) tight (compression ~1, e.g. C2): keep the buffers
+            return DeviceCsc(A.nrows, B.ncols, cp, rw[:n], vals[:n])
         return DeviceCsc(A.nrows, B.ncols, cp, rw[:n].clone(), vals[:n].clone())
     if method == "fused":
         free, _ = torch.cuda.mem_get_info(dev)

@@ -1,0 +1,17 @@
+#!/bin/bash
+TAG=${1:-esc2}
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_esc.py tests/test_gpu_local.py -x -q > gpurun_out/${TAG}_pytest.log 2>&1
+echo "pytest rc=$?"; tail -1 gpurun_out/${TAG}_pytest.log
+for o in "DIRECT_ESC=-1" "DIRECT_ESC=1"; do
+timeout 900 python tools/bench_configs.py --configs C1,C2,C5 --steps 5 --warmup 3 --opt $o > gpurun_out/${TAG}_$o.jsonl 2>&1
+python - gpurun_out/${TAG}_$o.jsonl "$o" <<'PY'
+import json,sys
+for l in open(sys.argv[1]):
+    if l.startswith('{'):
+        d=json.loads(l); print(sys.argv[2], d['config'], d['ms_per_product'], 'ms', 'frac', d['step_frac_hbm'], d['parity_slice'])
+PY
+done
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_c2esc_launches.csv \
+  python tools/bench_configs.py --configs C2 --steps 1 --warmup 1 --opt DIRECT_ESC=1 > gpurun_out/${TAG}_c2l.log 2>&1
+echo "launches rc=$?"
