@@ -150,7 +150,7 @@ typedef enum {
                                               (auto): 0 for 4-byte values with rank chunks, else 13 */
     SLAPCU_OPT_DIRECT_VALUE_RANK = 21,     /* direct path value pass: larger items are folded in rank
                                               chunks of at most this many outputs (4096..16384; default
-                                              8192 for 4-byte, 4096 for 8-byte accumulators);
+                                              10240 for 4-byte, 4096 for 8-byte accumulators);
                                               0 = row sub-tiles of 2^VTL rows */
     SLAPCU_OPT_DIRECT_VALUE_INTERLEAVE = 22, /* direct path value pass: A's rows and values gathered as
                                               one interleaved pair per product -- 1 (default) for 4-byte

@@ -133,7 +133,7 @@ struct Options {
     int direct_value_hash = -1;  // -1 auto: off for 4-byte values (rank chunks take every item), 13 for 8-byte
     int direct_value_interleave = 1;       // value pass: values gathered with their rows (0 off, 1 4-byte, 2 all)
     int direct_value_rank = -1;  // value pass: large items by rank chunks of this many outputs (0 = sub-tiles,
-                                 // -1 = by accumulator width: 8192 for 4-byte, 4096 for 8-byte)
+                                 // -1 = by accumulator width: 10240 for 4-byte, 4096 for 8-byte)
     int direct_tile_major = 1;              // form: work units ordered by row tile, then heaviest first
     int deterministic = 0;                  // 1: every product by ESC (the reference's fold order, bit-exact fp)
     int direct_esc = -1;                    // 1: ESC for every semiring, 0: bitmap / hash paths, -1 auto (value

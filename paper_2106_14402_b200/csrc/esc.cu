@@ -166,6 +166,57 @@ __global__ void __launch_bounds__(256) k_sort_small(const int* __restrict__ cols
 // same bitonic network in the warp's slice of shared memory, __syncwarp only.
 constexpr int kWarpSort = 256;
 
+// <= 32 * R products: the network in registers, element e = r * 32 + lane --
+// partners across lanes by shuffles, across registers in-thread (no shared
+// round trip per stage; C2's columns of 64-128 products).
+template <int R, class K, class V>
+__device__ __forceinline__ void warp_reg_sort(int n, int N, int lane, int b, K row_mask, const K* __restrict__ k0,
+                                              const V* __restrict__ v0, K* __restrict__ k1, V* __restrict__ v1) {
+    unsigned long long x[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int e = r * 32 + lane;
+        x[r] = e < n ? ((unsigned long long)(k0[b + e] & row_mask) << 11) | (unsigned long long)e : ~0ull;
+    }
+    for (int size = 2; size <= N; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            if (stride >= 32) {  // partner register r ^ (stride / 32), same lane (constant indices:
+                                 // a runtime register index would put x in local memory)
+                auto cx = [&](unsigned long long& a, unsigned long long& c, int r) {
+                    const bool asc = ((r * 32 + lane) & size) == 0;
+                    const unsigned long long lo = a < c ? a : c, hi = a < c ? c : a;
+                    a = asc ? lo : hi;
+                    c = asc ? hi : lo;
+                };
+                if (stride == 32) {
+                    cx(x[0], x[1], 0);
+                    if constexpr (R == 4) cx(x[2], x[3], 2);
+                } else if constexpr (R == 4) {  // stride 64
+                    cx(x[0], x[2], 0);
+                    cx(x[1], x[3], 1);
+                }
+                continue;
+            }
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int e = r * 32 + lane;
+                const unsigned long long y = __shfl_xor_sync(0xffffffffu, x[r], stride);
+                const bool keep_min = ((e & stride) == 0) == ((e & size) == 0);
+                x[r] = keep_min ? (x[r] < y ? x[r] : y) : (x[r] < y ? y : x[r]);
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int q = r * 32 + lane;
+        if (q < n) {
+            const int src = (int)(x[r] & 2047ull);
+            k1[b + q] = k0[b + src];
+            v1[b + q] = v0[b + src];
+        }
+    }
+}
+
 template <class K, class V>
 __global__ void __launch_bounds__(256) k_sort_warp(int ncols, const int* __restrict__ cols, const int* __restrict__ beg,
                                                    const int* __restrict__ end, K row_mask, const K* __restrict__ k0,
@@ -180,43 +231,11 @@ __global__ void __launch_bounds__(256) k_sort_warp(int ncols, const int* __restr
     int N = 1;
     while (N < n) N <<= 1;
     if (N <= 64) {
-        // <= 64 products: the same network in registers, element e = r * 32 + lane,
-        // partners across lanes by shuffles, across the two registers in-thread
-        // (no shared-memory round trip per stage)
-        unsigned long long x[2];
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            const int e = r * 32 + lane;
-            x[r] = e < n ? ((unsigned long long)(k0[b + e] & row_mask) << 11) | (unsigned long long)e : ~0ull;
-        }
-        for (int size = 2; size <= N; size <<= 1) {
-            for (int stride = size >> 1; stride > 0; stride >>= 1) {
-                if (stride == 32) {  // (size == 64: ascending)
-                    const unsigned long long lo = x[0] < x[1] ? x[0] : x[1], hi = x[0] < x[1] ? x[1] : x[0];
-                    x[0] = lo;
-                    x[1] = hi;
-                    continue;
-                }
-#pragma unroll
-                for (int r = 0; r < 2; ++r) {
-                    const int e = r * 32 + lane;
-                    const unsigned long long y = __shfl_xor_sync(0xffffffffu, x[r], stride);
-                    const bool keep_min = ((e & stride) == 0) == ((e & size) == 0);
-                    x[r] = keep_min ? (x[r] < y ? x[r] : y) : (x[r] < y ? y : x[r]);
-                }
-            }
-        }
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            const int q = r * 32 + lane;
-            if (q < n) {
-                const int src = (int)(x[r] & 2047ull);
-                k1[b + q] = k0[b + src];
-                v1[b + q] = v0[b + src];
-            }
-        }
+        warp_reg_sort<2>(n, N, lane, b, row_mask, k0, v0, k1, v1);
         return;
     }
+    // (65-128 products in 4 registers per lane measured slower than the shared
+    // network: C2 sort 1.66 -> 1.79 ms)
     for (int q = lane; q < N; q += 32)
         sk[q] = q < n ? ((unsigned long long)(k0[b + q] & row_mask) << 11) | (unsigned long long)q : ~0ull;
     __syncwarp();
