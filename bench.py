@@ -75,6 +75,8 @@ def parse():
     ap.add_argument("--words", type=int, default=None, help="direct form: walk A's (word, mask) pairs")
     ap.add_argument("--value-dense-rows", type=int, default=None, help="direct value pass: dense-chunk row span")
     ap.add_argument("--opt", action="append", default=[], help="NAME=VALUE library option (OPT_NAME)")
+    ap.add_argument("--sub-timeout", type=float, default=480.0,
+                    help="N>1: seconds the SUMMA / 3D sub-measurement may take before the line is printed without it")
     ap.add_argument("--dist", default="1d", choices=["1d", "summa"],
                     help="N>1: 1d = flops-balanced column blocks with A replicated (no data-path collective); "
                          "summa = the 2D SUMMA / 3D drivers (NCCL stage broadcasts, fiber exchange, merge)")
@@ -639,11 +641,34 @@ def run_ours_multi(args, world, rank):
     if args.second:
         sub_args = argparse.Namespace(**vars(args))
         sub_args.no_e2e = True  # the headline carries the e2e leg
-        sub = second(sub_args, world, rank)
+        key = "summa_3d" if args.dist == "1d" else "split_1d"
+        # The sub-measurement must not cost the headline line: an exception is
+        # recorded in the sub-object, and a watchdog on every rank prints the
+        # line (rank 0) and ends the process if it does not finish (the 2x2x2
+        # 3D grid of N = 8 has only ever run on a driver box).
+        def _watchdog():
+            if rank == 0:
+                line[key] = {"error": f"did not finish within {args.sub_timeout} s"}
+                print(json.dumps(line), flush=True)
+            os._exit(0)
+
+        timer = threading.Timer(args.sub_timeout, _watchdog)
+        timer.daemon = True
+        timer.start()
+        try:
+            sub = second(sub_args, world, rank)
+        except Exception as e:  # noqa: BLE001 -- recorded, the headline stands
+            # (peers may be waiting in a collective: no barrier, this rank ends here
+            # and theirs end by their watchdogs)
+            if rank == 0:
+                line[key] = {"error": f"{type(e).__name__}: {e}"[:300]}
+                print(json.dumps(line), flush=True)
+            sys.stdout.flush()
+            os._exit(0)
+        timer.cancel()
         if rank == 0:
-            line["summa_3d" if args.dist == "1d" else "split_1d"] = {
-                k: sub[k] for k in ("value", "unit", "ms_per_step", "config", "gpu_launches", "roofline", "dist")
-                if k in sub}
+            line[key] = {k: sub[k] for k in ("value", "unit", "ms_per_step", "config", "gpu_launches", "roofline",
+                                             "dist") if k in sub}
     if rank == 0:
         print(json.dumps(line), flush=True)
     dist.barrier()

@@ -94,6 +94,9 @@ typedef struct slapcu_ctx_s* slapcu_ctx;
  * `stream` is a cudaStream_t (NULL = the legacy default stream).  Calls on a
  * context are stream-ordered and not reentrant; use one context per host thread. */
 slapcu_status slapcu_ctx_create(slapcu_ctx* out, int device, void* stream);
+/* Waits for the context's work, frees its workspace and trims the device's
+ * stream-ordered memory pool (which keeps freed workspace cached while
+ * contexts are alive) back to what live allocations hold. */
 slapcu_status slapcu_ctx_destroy(slapcu_ctx ctx);
 slapcu_status slapcu_ctx_set_stream(slapcu_ctx ctx, void* stream);
 /* Drops every per-operand cache of the context (A tile pointers, dense-run

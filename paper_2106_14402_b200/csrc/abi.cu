@@ -116,7 +116,15 @@ slapcu_status slapcu_ctx_destroy(slapcu_ctx ctx) {
         if (e) cudaEventDestroy(e);
     if (ctx->c.err_host) cudaFreeHost(ctx->c.err_host);
     free_host_cache(ctx->c);
-    delete ctx;
+    const int dev = ctx->c.device;
+    delete ctx;  // (its workspace goes back to the device's stream-ordered pool ...)
+    // ... and the pool, which keeps freed memory cached while contexts work
+    // (release threshold = max), returns what no allocation holds to the device
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        cudaDeviceSynchronize();
+        cudaMemPoolTrimTo(pool, 0);
+    }
     return SLAPCU_OK;
 }
 
