@@ -800,14 +800,14 @@ __device__ __forceinline__ T_ shfl_val(T_ v, int src) {
 // the batch's product prefix), so no thread walks a run alone through a chain
 // of dependent loads.
 #ifndef SLAPCU_VTINY
-#define SLAPCU_VTINY 2
+#define SLAPCU_VTINY 0  // with the per-warp shuffle packing, runs of 1-2 pack too (MinPlus C3 413.8 -> 410.0 ms)
 #endif
 constexpr int kValueTinyRun = SLAPCU_VTINY;  // value walk: runs this short are folded by their own thread
 #ifndef SLAPCU_VALUE_U
 #define SLAPCU_VALUE_U 8  // MinPlus C3: 2 / 4 / 8 -> 469 / 454 / 443 ms (latency-bound gathers)
 #endif
 #ifndef SLAPCU_VALUE_UNIT
-#define SLAPCU_VALUE_UNIT 256
+#define SLAPCU_VALUE_UNIT 128  // MinPlus C3 (same box): 128 / 256 / 512 -> 407.6 / 409.6 / 428.3 ms
 #endif
 constexpr int kValueU = SLAPCU_VALUE_U;        // value walk: products per lane per trip on long runs
 constexpr int kValueUnit = SLAPCU_VALUE_UNIT;  // value walk: products per warp work unit on long runs
@@ -1954,7 +1954,9 @@ static uint4 value_pattern(int sr, bool ones) {
 }
 
 // Value walks: runs of at most this many products are folded by their own thread.
-static int value_tiny_run(const Ctx& c) { return c.opt.direct_value_tiny_run >= 0 ? c.opt.direct_value_tiny_run : kValueTinyRun; }
+static int value_tiny_run(const Ctx& c) {
+    return c.opt.direct_value_tiny_run >= 0 ? c.opt.direct_value_tiny_run : kValueTinyRun;
+}
 
 // Value form (semirings with values): log2 rows of an item tile whose
 // accumulators fit in shared memory, or 0 when the pattern form + value pass
