@@ -373,11 +373,7 @@ slapcu_status slapcu_spgemm_direct(slapcu_ctx ctx, const slapcu_csc* A, const sl
 }
 
 // Largest staging area the one-shot call will take: half the free device memory.
-static int64_t default_staging_budget(Ctx& c) {
-    size_t fr = 0, tot = 0;
-    SLAPCU_CUDA(cudaMemGetInfo(&fr, &tot));
-    return int64_t(fr / 2);
-}
+static int64_t default_staging_budget(Ctx& c) { return int64_t(device_available(c) / 2); }
 
 slapcu_status slapcu_spgemm(slapcu_ctx ctx, const slapcu_csc* A, const slapcu_csc* B, slapcu_semiring sr,
                             slapcu_alg alg, slapcu_csc_out* C) {

@@ -238,6 +238,23 @@ struct Ctx {
 
 Ctx& ctx_of(slapcu_ctx c);
 
+// Device memory a new workspace can take: what the driver reports free plus
+// what the stream-ordered pool holds cached but unused (the pool keeps freed
+// workspace, release threshold = max) -- sizing by the free memory alone made
+// the ESC group size depend on what earlier products left cached.
+inline size_t device_available(const Ctx& c) {
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return 0;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, c.device) == cudaSuccess) {
+        uint64_t reserved = 0, used = 0;
+        if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess &&
+            cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess && reserved > used)
+            fr += size_t(reserved - used);
+    }
+    return fr;
+}
+
 // Reads cp[0] and cp[ncols] (synchronizes the context stream).
 void resolve(Ctx& c, DevCsc& m);
 uint64_t pattern_fingerprint(Ctx& c, const DevCsc& m);  // resolved m

@@ -128,8 +128,7 @@ void local_multiply(Ctx& c, const DevCsc& A, const DevCsc& B, int sr, int alg, B
     out.cp.reset(sizeof(int64_t) * (B.ncols + 1), c.stream);
     // single product pass when its staging area fits in half the free memory,
     // else the two-pass symbolic -> numeric contract
-    size_t fr = 0, tot = 0;
-    SLAPCU_CUDA(cudaMemGetInfo(&fr, &tot));
+    const size_t fr = device_available(c);
     bool fused = true;
     try {
         out.nnz = fused_begin(c, A, B, sr, alg, out.cp.as<int64_t>(), int64_t(fr / 2));

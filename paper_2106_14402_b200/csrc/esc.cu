@@ -340,8 +340,7 @@ int64_t esc_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int64_t c
     DevBuf fl(sizeof(int64_t) * std::max<int64_t>(n, 1), c.stream);
     int64_t total = 0;
     spgemm_flops(c, A, B, fl.as<int64_t>(), &total);
-    size_t fr = 0, tot = 0;
-    SLAPCU_CUDA(cudaMemGetInfo(&fr, &tot));
+    const size_t fr = device_available(c);
     const int64_t per_prod = 2 * 8 + 2 * 4 + 2 * 8;  // keys x2 (<= 8 bytes), head, ex, values x2 (<= 8 bytes)
     const int64_t group_max = std::max<int64_t>(1, std::min<int64_t>(int64_t(1) << 30, int64_t(fr / 3) / per_prod));
     // per-column counts and B's column pointers on the host only when the
