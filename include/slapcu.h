@@ -186,10 +186,15 @@ typedef enum {
                                               value pass: measured faster at C3, whose 2^14-row items are
                                               too many and too small), -1 = auto (2^14 rows for accumulators
                                               of <= 4 bytes, 2^13 for 8 bytes), 12..15 = that height */
-    SLAPCU_OPT_DIRECT_VALUE_TINY_RUN = 33  /* direct path value walks: runs (A column x tile) of at most this
+    SLAPCU_OPT_DIRECT_VALUE_TINY_RUN = 33, /* direct path value walks: runs (A column x tile) of at most this
                                               many products are folded by their own thread with 4 loads in
                                               flight; longer runs below 32 are packed 32 products per warp
                                               step, 32 and up cut into warp units.  -1 = default */
+    SLAPCU_OPT_DIRECT_VALUE_ROWS = 34      /* direct path, 4-byte values (every item in rank chunks): 1 =
+                                              the value pass writes C's rows beside the values from the
+                                              form pass's stash and the emit pass is skipped (measured
+                                              slower, MinPlus C3 409 -> 458 ms: its per-thread row stores
+                                              are not staged like emit's); 0 (default) = emit writes them */
 } slapcu_option;
 slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t value);
 

@@ -39,7 +39,7 @@ ALG_HEAP, ALG_HASH, ALG_HYBRID = 0, 1, 2
  OPT_DIRECT_VALUE_HASH, OPT_DIRECT_VALUE_RANK, OPT_DIRECT_VALUE_INTERLEAVE, OPT_DIRECT_TILE_MAJOR,
  OPT_DIRECT_FORM_WALK, OPT_DIRECT_SHORT_RUN, OPT_DIRECT_VALUE_TMAJOR, OPT_DIRECT_WORDS,
  OPT_DIRECT_ESC, OPT_DIRECT_VALUE_DENSE_ROWS, OPT_DIRECT_VALUE_DENSE_ONLY, OPT_DIRECT_VALUE_L2,
- OPT_DIRECT_VALUE_FORM, OPT_DIRECT_VALUE_TINY_RUN) = range(34)
+ OPT_DIRECT_VALUE_FORM, OPT_DIRECT_VALUE_TINY_RUN, OPT_DIRECT_VALUE_ROWS) = range(35)
 NUM_KERNEL_CLASSES = 10
 KERNEL_CLASSES = ["other", "flops", "bin", "sym_light", "sym_heavy", "scan", "num_light", "num_heavy", "merge", "gen"]
 

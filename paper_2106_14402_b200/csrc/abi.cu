@@ -184,6 +184,7 @@ slapcu_status slapcu_ctx_set_option(slapcu_ctx ctx, slapcu_option opt, int64_t v
             require(v == 0, SLAPCU_ERR_INVALID, "dense-only value chunks: removed");
             break;
         case SLAPCU_OPT_DIRECT_VALUE_TMAJOR: c.opt.direct_value_tmajor = v != 0; break;
+        case SLAPCU_OPT_DIRECT_VALUE_ROWS: c.opt.direct_value_rows = v != 0; break;
         case SLAPCU_OPT_DIRECT_VALUE_TINY_RUN:
             require(v >= -1 && v <= 64, SLAPCU_ERR_INVALID, "value tiny run: -1 (default) or 0..64");
             c.opt.direct_value_tiny_run = (int)v;

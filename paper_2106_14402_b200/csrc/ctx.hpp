@@ -141,6 +141,7 @@ struct Options {
     int direct_words = 1;                   // form: walk A's (32-row word, mask) pairs instead of its rows
     int direct_value_dense_rows = 0;        // value pass: chunks spanning <= this many rows fold by row offset (0 = cap)
     int direct_value_tmajor = 1;            // value pass: tile-major 4096-row pointer table + chunks in row order
+    int direct_value_rows = 0;              // 1: value pass writes C's rows too (emit skipped; measured slower)
     int direct_value_tiny_run = -1;         // value walks: runs this short folded by their own thread (-1 default)
     int direct_value_form = 0;              // value semirings: one walk folding values in a 2^v-row tile
                                             // (-1 auto: 14 for <= 4-byte accumulators, 13 for 8; 0 = value pass)

@@ -732,6 +732,7 @@ struct ValueArgs {
     const unsigned* stash;  // the form pass's per-item stash (bitmap or word list), its offsets and forms
     const int64_t* soff;
     const int* form;
+    int32_t* rows_out;      // rank chunks also write C's rows (the emit pass is skipped), or null
 };
 
 // One product's A row and value: from the interleaved copy when there is one
@@ -1208,11 +1209,14 @@ __global__ void __launch_bounds__(NT, 3) k_item_values_rank(ValueArgs g, const R
                              g.arv, g.tv_stride, 1, -1, -1, g.tiny);
         const int per = (nwords + NT - 1) / NT;
         const int w0 = min(nwords, tid * per), w1 = min(nwords, w0 + per);
+        int32_t* rows = g.rows_out;
         for (int w = w0; w < w1; ++w) {
             unsigned x = bm[w];
             int o = pre16[w];
             while (x) {
-                Cv[lo + o++] = S_::out(val[(w << 5) + __ffs(x) - 1]);
+                const int b = __ffs(x) - 1;
+                if (rows) rows[lo + o] = r0 + (w << 5) + b;
+                Cv[lo + o++] = S_::out(val[(w << 5) + b]);
                 x &= x - 1u;
             }
         }
@@ -1226,6 +1230,18 @@ __global__ void __launch_bounds__(NT, 3) k_item_values_rank(ValueArgs g, const R
     value_walk<SRID, NT>(g.A, g.B, g.Atpv, g.Tv, ts0, j, sh, into<S_>(slot), ts1, g.arv, g.tv_stride, 0, -1, -1,
                          g.tiny);
     for (int q = tid; q < n; q += NT) Cv[lo + q] = S_::out(val[q]);
+    if (g.rows_out) {  // C's rows of the chunk, in order, from its bitmap (thread-contiguous words)
+        const int per = (nwords + NT - 1) / NT;
+        const int w0 = min(nwords, tid * per), w1 = min(nwords, w0 + per);
+        for (int w = w0; w < w1; ++w) {
+            unsigned x = bm[w];
+            int o = pre16[w];
+            while (x) {
+                g.rows_out[lo + o++] = r0 + (w << 5) + __ffs(x) - 1;
+                x &= x - 1u;
+            }
+        }
+    }
 }
 
 // Rank chunks of the large items (thread per item, greedy over row blocks).
@@ -2524,7 +2540,13 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
     const bool rank_path = c.opt.direct_value_rank != 0 && TL >= 12;
     const int hopt = c.opt.direct_value_hash >= 0 ? c.opt.direct_value_hash
                                                   : ((value_size(sr) == 4 && rank_path) ? 0 : 1);
-    if (nitems > 0) {
+    // option: 4-byte values, every item through rank chunks (they read the form's
+    // stash, not C's rows): the chunks write C's rows too and the emit pass is
+    // skipped -- measured slower (409 -> 458 ms at MinPlus C3: the chunks' row
+    // stores are per thread, emit stages them for 16-byte stores)
+    const bool rows_by_values = nitems > 0 && !ones && !vform && rank_path && hopt == 0 &&
+                                c.opt.direct_value_rows != 0;
+    if (nitems > 0 && !rows_by_values) {
         KScope ks(c, KC_NUM_HEAVY);
         EmitArgs e{(const int2*)d.items.as<int2>(), (const int64_t*)d.cnt.as<int64_t>(), (const int*)d.form.as<int>(),
                    (const unsigned*)d.stash.as<unsigned>(), (const int64_t*)d.soff.as<int64_t>(),
@@ -2569,7 +2591,7 @@ int64_t direct_spgemm(Ctx& c, const DevCsc& A_, const DevCsc& B_, int sr, int al
                      (const int64_t*)d.cnt.as<int64_t>(), (const int64_t*)d.hoff.as<int64_t>(),
                      (const int64_t*)d.lp.as<int64_t>(), (const int*)d.rbc.as<int>(), crw, cv, nullptr, 0,
                      value_tiny_run(c), (const unsigned*)d.stash.as<unsigned>(), (const int64_t*)d.soff.as<int64_t>(),
-                     (const int*)d.form.as<int>()};
+                     (const int*)d.form.as<int>(), rows_by_values ? crw : nullptr};
         // 4-byte values: A's rows and values interleaved, so a product's gather
         // is one 8-byte load (one sector) instead of one from each array
         DevBuf arv;

@@ -219,3 +219,22 @@ def test_direct_empty(port):
         want = port.spgemm(oracle.OR_AND_U8, x, y)
         got = P.local_spgemm(to_device(x), to_device(y), P.OrAnd, method="direct")
         assert_parity(got, want, oracle.OR_AND_U8, "empty")
+
+
+@pytest.mark.parametrize("rows", [0, 1])
+@pytest.mark.parametrize("sr", [P.MinPlusI32, P.PlusTimesF32], ids=lambda s: f"{s.name}_{s.dtype}")
+def test_direct_value_rows(port, sr, rows):
+    """4-byte values, every item in rank chunks: the value pass writes C's
+    rows from the form pass's stash and the emit pass is skipped (1, the
+    default), or emit writes them (0) -- same C, with the default tiles and
+    with 4096-row tiles and split items."""
+    a = with_values(port, port.gen_rmat(13), sr.id)
+    want = port.spgemm(sr.id, a, a)
+    for tl, split in ((0, 1 << 20), (12, 4096)):
+        ctx = P.Context()
+        ctx.set_option(L.OPT_DIRECT_ESC, 0)
+        ctx.set_option(L.OPT_DIRECT_VALUE_ROWS, rows)
+        ctx.set_option(L.OPT_DIRECT_TILE_ROWS_LOG2, tl)
+        ctx.set_option(L.OPT_DIRECT_SPLIT_FLOPS, split)
+        got = P.local_spgemm(to_device(a), to_device(a), sr, ctx=ctx, method="direct")
+        assert_parity(got, want, sr.id, f"{sr.name} rows={rows} tl={tl}")
